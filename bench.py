@@ -1,0 +1,385 @@
+#!/usr/bin/env python
+"""bench.py — throughput of the CoFEM hot path (EM iterations/s of the T×C×(K+1) batched-CG E-step
+plus M-step) on N B200s, and of the fp64 CPU oracle as the reference arm.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config 2] [--impl cuda|reference]
+
+A "step" is one EM iteration (Alg. 2 lines 2-16) over the whole workload of
+BASELINE.json configs[cfg-1] (default configs[1] = C2), continuing the EM run: W untimed warm-up
+iterations, then K timed ones.  For N > 1 (torchrun, one rank per GPU, NCCL) tasks are sharded by
+contiguous blocks and the M-step sums are all-reduced inside libcmtcs (strong scaling: T fixed).
+Rank 0 prints one JSON line.  See DESIGN.md §7 for every field.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synthetic  # noqa: E402
+
+SM_COUNT = 148
+FP32_LANES_PER_SM = 128
+SM_MAX_MHZ = 1965.0
+
+
+def baseline_json():
+    with open(os.path.join(ROOT, "BASELINE.json")) as f:
+        return json.load(f)
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            return json.load(f), "measured"
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "sm_max_mhz": SM_MAX_MHZ}, "fallback"
+
+
+def fp32_peak_tflops(sm_mhz):
+    """FFMA peak: 148 SMs × 128 FP32 lanes × 2 flop × clock (B200_PROFILING.md unit counts)."""
+    return SM_COUNT * FP32_LANES_PER_SM * 2 * sm_mhz * 1e6 / 1e12
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4, 5])
+    ap.add_argument("--impl", default="cuda", choices=["cuda", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0, help="oracle sample budget")
+    return ap.parse_args()
+
+
+# --------------------------------------------------------------------------------------------
+# clocks (nvidia-smi sampled during the timed region)
+# --------------------------------------------------------------------------------------------
+class ClockSampler:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index: int):
+        self.dev = device_index
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        try:
+            fd, self.path = tempfile.mkstemp(suffix=".csv")
+            os.close(fd)
+            self.fh = open(self.path, "w")
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=self.fh, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.fh.close()
+        rows = []
+        with open(self.path) as f:
+            for line in f:
+                parts = [x.strip() for x in line.split(",")]
+                if len(parts) >= 9:
+                    rows.append(parts)
+        os.unlink(self.path)
+        if not rows:
+            return None
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+# --------------------------------------------------------------------------------------------
+# CPU oracle timing (cpu_baseline leg and --impl reference)
+# --------------------------------------------------------------------------------------------
+def cpu_cores():
+    try:
+        from threadpoolctl import threadpool_info
+        th = [i.get("num_threads") for i in threadpool_info() if i.get("user_api") == "blas"]
+        if th:
+            return int(max(th))
+    except Exception:
+        pass
+    return os.cpu_count()
+
+
+def oracle_em_sample(cfg, budget_s: float, it: int = 0):
+    """Times oracle E-step (cofem) + M-step at EM iteration `it` from α₀ on the first n tasks,
+    adding tasks until `budget_s` of CPU work is spent.  Returns (seconds per task, n tasks)."""
+    from oracle import cofem as O
+    n, spent = 0, 0.0
+    alpha = np.ones((cfg.C, cfg.D))
+    while n < cfg.T and spent < budget_s:
+        data = synthetic.generate(cfg, [n])
+        t0 = time.perf_counter()
+        e = O.e_step(data, alpha, it, mode="cofem")
+        O.m_step_sums(e["q"], e["mu"], e["s"])
+        spent += time.perf_counter() - t0
+        n += 1
+    return spent / n, n
+
+
+def cpu_baseline(cfg, budget_s):
+    per_task, n = oracle_em_sample(cfg, budget_s)
+    return {"value": 1.0 / (per_task * cfg.T), "unit": "EM iters/s", "cores": cpu_cores(),
+            "kind": "oracle",
+            "sample": (f"oracle (numpy fp64) E-step + M-step sums of EM iteration 0 from alpha0=1 on "
+                       f"{n} of {cfg.T} tasks ({per_task * n:.1f} s), extrapolated x{cfg.T / n:.1f} "
+                       f"to the full workload; iteration 0 needs fewer CG steps than later ones")}
+
+
+def reference_arm(args):
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if rank != 0:
+        return 0
+    cfg = synthetic.CONFIGS[args.config]
+    from oracle import cofem as O
+    # sample: the first n_s tasks, EM continued on that sample only (its own M-step)
+    n_s = {1: 4, 2: 2, 3: 1, 4: 1, 5: 1}[args.config]
+    data = synthetic.generate(cfg, range(n_s))
+    alpha = np.array(data["alpha0"])
+    times = []
+    for i in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        e = O.e_step(data, alpha, i, mode="cofem", T_global=cfg.T)
+        alpha = O.m_step(e["q"], e["mu"], e["s"], alpha)
+        dt = time.perf_counter() - t0
+        if i >= args.warmup:
+            times.append(dt)
+    per_iter_full = statistics.mean(times) * cfg.T / n_s
+    value = 1.0 / per_iter_full
+    bj = baseline_json()
+    sample = (f"oracle (numpy fp64 cofem mode) EM iterations {args.warmup}..{args.warmup + args.steps - 1} "
+              f"on the first {n_s} of {cfg.T} tasks (M-step over the sample), time x{cfg.T / n_s:.0f}")
+    line = {"impl": "reference", "metric": bj["metric"], "value": value, "unit": "EM iters/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": per_iter_full * 1e3, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": cfg.name, "T": cfg.T, "C": cfg.C, "N": cfg.N, "D": cfg.D, "K": cfg.K,
+                       "cg_cap": cfg.cg_cap, "cg_tol": cfg.cg_tol, "parallelism": "host cores"},
+            "cpu_baseline": {"value": value, "unit": "EM iters/s", "cores": cpu_cores(), "kind": "oracle",
+                             "sample": sample},
+            "e2e": {"value": value, "unit": "EM iters/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# --------------------------------------------------------------------------------------------
+# CUDA arm
+# --------------------------------------------------------------------------------------------
+def ncu_traffic(cfg_name):
+    """dram bytes per operator launch pair from the committed ncu --set full summary, if any."""
+    p = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    if not os.path.exists(p):
+        return None
+    try:
+        with open(p) as f:
+            j = json.load(f)
+        return j.get("traffic_bytes_per_launch", {}).get(cfg_name)
+    except Exception:
+        return None
+
+
+def cuda_arm(args):
+    import torch
+    import torch.distributed as dist
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        if world == 1 and args.gpus > 1:
+            print("bench.py: --gpus N > 1 must be launched with torchrun (one rank per GPU)", file=sys.stderr)
+            return 2
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    from paper_2310_00420_b200 import CoFEM, cmtcs
+
+    cfg = synthetic.CONFIGS[args.config]
+    b, e = synthetic.shard(cfg.T, rank, world)
+    data = synthetic.generate(cfg, range(b, e))
+    phi_h = torch.from_numpy(np.ascontiguousarray(data["phi"])).pin_memory()
+    y_h = torch.from_numpy(np.ascontiguousarray(data["y"])).pin_memory()
+    phi = phi_h.to(dev)
+    y = y_h.to(dev)
+    uid = None
+    if world > 1:
+        obj = [cmtcs.cmtcs_get_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        uid = obj[0]
+    model = CoFEM(phi, y, T=cfg.T, C=cfg.C, K=cfg.K, beta=cfg.beta, cg_max_iters=cfg.cg_cap,
+                  cg_rel_tol=cfg.cg_tol, probe_seed=cfg.probe_seed, pi=data["pi"], task_begin=b,
+                  shared_phi=cfg.shared_phi, nccl_uid=uid, rank=rank, world=world)
+    stream = model.stream
+    l2 = torch.cuda.get_device_properties(dev).L2_cache_size
+    flush = torch.empty(max(2 * l2, 256 << 20), dtype=torch.uint8, device=dev)
+
+    def barrier():
+        if world > 1:
+            dist.barrier(device_ids=[local])
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def sum_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        return float(t.item())
+
+    for _ in range(args.warmup):
+        model.em_step(1)
+    it0 = model.history[-1]["em_iter"] + 1 if model.history else 0
+    alpha_snapshot = model.posterior()["alpha"].clone() if model.history else torch.ones(cfg.C, cfg.D, dtype=torch.float64, device=dev)
+
+    # ------------------------------ timed region (device-resident inputs) -------------------
+    model.set_timing(True)
+    model.get_timing(reset=True)
+    launches0 = model.kernel_launches
+    sampler = ClockSampler(local) if rank == 0 else None
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    infos = []
+    barrier()
+    torch.cuda.synchronize()
+    if sampler:
+        sampler.start()
+        time.sleep(0.3)
+    wall0 = time.perf_counter()
+    for k in range(args.steps):
+        with torch.cuda.stream(stream):
+            flush.zero_()                   # L2 flush between timed iterations (outside the events)
+            evs[k][0].record(stream)
+        infos.append(model.em_step(1))
+        evs[k][1].record(stream)
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - wall0
+    barrier()
+    clocks = sampler.stop() if sampler else None
+    step_ms = [a.elapsed_time(bb) for a, bb in evs]
+    total_ms = max_over_ranks(sum(step_ms))
+    tm = model.get_timing(reset=True)
+    model.set_timing(False)
+    launches = sum_over_ranks(model.kernel_launches - launches0)
+
+    # algorithmic work: 4·N·D flop per active column per CG step
+    col_iters = sum(i["probe_col_iters"] + i["mean_col_iters"] for i in infos)
+    flops_rank = 4.0 * cfg.N * cfg.D * col_iters
+    op_ms_rank = tm["op_ms"]
+    flops_all = sum_over_ranks(flops_rank)
+    achieved_op = flops_rank / (op_ms_rank * 1e-3) / 1e12 if op_ms_rank > 0 else 0.0
+    achieved_op = max_over_ranks(achieved_op) if world == 1 else sum_over_ranks(achieved_op) / world
+    peaks, peaks_kind = measured_peaks()
+    peak = fp32_peak_tflops(peaks.get("sm_max_mhz", SM_MAX_MHZ))
+    em_roof_frac = (flops_all / world / (peak * 1e12)) / (total_ms * 1e-3 / args.steps * args.steps)
+
+    # ------------------------------ end to end through the public API (host buffers) --------
+    e2e = None
+    if not args.no_e2e:
+        model.set_state(alpha_snapshot, it0)        # replay the same EM iterations
+        h2d = phi_h.numel() * 4 + y_h.numel() * 4
+        d2h = (cfg.C * cfg.D + (e - b) * cfg.C) * 8
+        barrier()
+        torch.cuda.synchronize()
+        t0ev = torch.cuda.Event(enable_timing=True)
+        t1ev = torch.cuda.Event(enable_timing=True)
+        t0ev.record(stream)
+        for k in range(args.steps):
+            with torch.cuda.stream(stream):
+                phi.copy_(phi_h, non_blocking=True)
+                y.copy_(y_h, non_blocking=True)
+            model.em_step(1)
+            post = model.posterior()
+            q_host = post["q"].cpu()
+            a_host = post["alpha"].cpu()
+        t1ev.record(stream)
+        torch.cuda.synchronize()
+        e2e_ms = max_over_ranks(t0ev.elapsed_time(t1ev))
+        e2e = {"value": args.steps / (e2e_ms * 1e-3), "unit": "EM iters/s",
+               "h2d_bytes_per_step": int(sum_over_ranks(h2d)), "d2h_bytes_per_step": int(sum_over_ranks(d2h))}
+        del q_host, a_host
+
+    if rank == 0:
+        bj = baseline_json()
+        value = args.steps / (total_ms * 1e-3)
+        line = {
+            "metric": bj["metric"], "value": value, "unit": "EM iters/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f32", "data": "synthetic",
+            "config": {
+                "workload": f"{cfg.name} (BASELINE.json configs[{cfg.cfg_id - 1}])",
+                "T": cfg.T, "C": cfg.C, "N": cfg.N, "D": cfg.D, "K": cfg.K, "cg_cap": cfg.cg_cap,
+                "cg_tol": cfg.cg_tol, "em_iters_timed": f"{it0}..{it0 + args.steps - 1}",
+                "parallelism": f"task-sharded dp{world}" if world > 1 else "single GPU",
+                "precision": "probe columns f32 FFMA with f64 dots/scalars; mean columns, log-det, q, M-step f64",
+                "l2": "flushed (zero-fill of 2xL2) between timed EM iterations",
+                "cg_steps_per_em_iter": [i["cg_iters"] for i in infos],
+                "active_col_iters_per_em_iter": [i["probe_col_iters"] + i["mean_col_iters"] for i in infos],
+                "algorithmic_tflop_per_s_em": flops_all / (total_ms * 1e-3) / 1e12,
+                "em_step_roofline_frac": em_roof_frac,
+                "op_share_of_step": op_ms_rank / max(sum(step_ms), 1e-9),
+                "update_share_of_step": tm["update_ms"] / max(sum(step_ms), 1e-9),
+                "wall_s_timed": wall,
+            },
+            "roofline": {"bound": "alu", "achieved": achieved_op, "peak": peak, "unit": "TFLOP/s",
+                         "frac": achieved_op / peak, "traffic": ncu_traffic(cfg.name),
+                         "kernel": "K1 operator (k_stage1 + k_stage2 launch pair per CG step)",
+                         "peak_source": f"derived: 148 SM x 128 FP32 lanes x 2 x {peaks.get('sm_max_mhz', SM_MAX_MHZ):.0f} MHz "
+                                        f"(sm_max_mhz of {peaks_kind} MEASURED_PEAKS.json); FFMA has no measured peak there"},
+            "gpu_launches": int(launches),
+            "clocks": clocks,
+        }
+        if e2e:
+            line["e2e"] = e2e
+        if world == 1 and not args.no_cpu_baseline:
+            line["cpu_baseline"] = cpu_baseline(cfg, args.cpu_seconds)
+        print(json.dumps(line), flush=True)
+    model.close()
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return reference_arm(args)
+    return cuda_arm(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,549 @@
+// libcmtcs C ABI (include/cmtcs.h): context, workspace carving, the EM-iteration driver
+// (Alg. 2 lines 2-16), NCCL all-reduce of the Eq. 4 sums, posterior readout.
+#include <nccl.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <cmath>
+#include <new>
+
+#include "cmtcs_internal.cuh"
+
+using namespace cmtcs;
+
+struct cmtcs_ctx {
+  cmtcs_problem prob;
+  double pi_host[MAXC];
+  KParams kp;
+  cudaStream_t stream;
+  int device;
+  int rank, world;
+  ncclComm_t comm;
+  bool have_comm;
+  bool broken;
+  bool have_estep;
+  int em_iter;           // global index of the next EM iteration
+  int cg_chunk;          // CG steps enqueued between host convergence checks
+  char err[512];
+  int *h_alive;          // pinned [2]
+  double *h_out;         // pinned [32]: stats[16] | loglik | status(as int) ...
+  int *h_status;         // pinned [8]
+  cudaEvent_t ev[2];
+  int64_t launches;
+  // live timing (cmtcs_set_timing)
+  bool timing;
+  cudaEvent_t *tev;      // pool of 2*cap + 2 events
+  int ntev;
+  double t_ms[3];
+  int64_t t_n[3];
+};
+
+namespace {
+
+thread_local char g_err[512];
+
+cmtcs_status fail(cmtcs_ctx *c, cmtcs_status st, const char *fmt, ...) {
+  char *buf = c ? c->err : g_err;
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, 512, fmt, ap);
+  va_end(ap);
+  if (c && st != CMTCS_EINVAL) c->broken = true;
+  return st;
+}
+
+#define CUDA_OK(ctx, call)                                                                    \
+  do {                                                                                        \
+    cudaError_t e_ = (call);                                                                  \
+    if (e_ != cudaSuccess)                                                                    \
+      return fail((ctx), CMTCS_ECUDA, "%s failed: %s (%s:%d)", #call, cudaGetErrorString(e_), \
+                  __FILE__, __LINE__);                                                        \
+  } while (0)
+
+#define NCCL_OK(ctx, call)                                                                          \
+  do {                                                                                              \
+    ncclResult_t r_ = (call);                                                                       \
+    if (r_ != ncclSuccess)                                                                          \
+      return fail((ctx), CMTCS_ENCCL, "%s failed: %s", #call, ncclGetErrorString(r_));              \
+  } while (0)
+
+size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+struct Carver {
+  char *base;
+  size_t off = 0;
+  template <class T>
+  T *take(size_t n) {
+    T *p = base ? reinterpret_cast<T *>(base + off) : nullptr;
+    off += align256(n * sizeof(T) + 1);
+    return p;
+  }
+};
+
+bool make_dims(const cmtcs_problem *p, Dims *d, char *why) {
+  if (!p) { snprintf(why, 256, "problem is NULL"); return false; }
+  if (p->T < 1 || p->N < 4 || p->D < 4 || p->C < 1 || p->K < 1) { snprintf(why, 256, "need T>=1, N>=4, D>=4, C>=1, K>=1"); return false; }
+  if (p->N % 4 || p->D % 4) { snprintf(why, 256, "N and D must be multiples of 4 (got N=%d D=%d)", p->N, p->D); return false; }
+  if (p->C > MAXC) { snprintf(why, 256, "C=%d exceeds the supported maximum %d", p->C, MAXC); return false; }
+  if (!(p->beta > 0) || !std::isfinite(p->beta)) { snprintf(why, 256, "beta must be finite and > 0"); return false; }
+  if (p->cg_max_iters < 1) { snprintf(why, 256, "cg_max_iters must be >= 1"); return false; }
+  if (!(p->cg_rel_tol >= 0)) { snprintf(why, 256, "cg_rel_tol must be >= 0"); return false; }
+  if (!(p->alpha_max > 0) || !(p->var_floor >= 0) || !(p->empty_eps >= 0)) { snprintf(why, 256, "bad alpha_max/var_floor/empty_eps"); return false; }
+  if (p->task_begin < 0 || p->task_end > p->T || p->task_end <= p->task_begin) { snprintf(why, 256, "bad task range [%d,%d) of T=%d", p->task_begin, p->task_end, p->T); return false; }
+  if (p->em_iter0 < 0) { snprintf(why, 256, "em_iter0 must be >= 0"); return false; }
+  if (!p->pi) { snprintf(why, 256, "pi is NULL"); return false; }
+  double s = 0;
+  for (int c = 0; c < p->C; ++c) {
+    if (!(p->pi[c] > 0) || !std::isfinite(p->pi[c])) { snprintf(why, 256, "pi[%d] must be > 0", c); return false; }
+    s += p->pi[c];
+  }
+  if (fabs(s - 1.0) > 1e-9) { snprintf(why, 256, "pi sums to %.17g, not 1", s); return false; }
+  d->T = p->T;
+  d->Tl = p->task_end - p->task_begin;
+  d->t0 = p->task_begin;
+  d->N = p->N;
+  d->D = p->D;
+  d->C = p->C;
+  d->K = p->K;
+  d->P = p->C * p->K;
+  d->Pp = (d->P + 3) & ~3;
+  d->cap = p->cg_max_iters;
+  d->nw = (p->D + 63) / 64;
+  d->nRT1 = (p->N + OP_BR - 1) / OP_BR;
+  d->nRT2 = (p->D + OP_BR - 1) / OP_BR;
+  d->nCT = (d->P + OP_BC - 1) / OP_BC;
+  d->shared_phi = p->shared_phi ? 1 : 0;
+  d->phi_task_stride = p->shared_phi ? 0 : (int64_t)p->N * p->D;
+  return true;
+}
+
+size_t carve(const Dims &d, char *base, Bufs *b) {
+  Carver cv{base};
+  const size_t Tl = d.Tl, P = d.P, C = d.C, D = d.D, N = d.N, cap = d.cap;
+  b->alpha64 = cv.take<double>(C * D);
+  b->alpha32 = cv.take<float>(C * D);
+  b->logsum_alpha = cv.take<double>(C);
+  b->logpi = cv.take<double>(C);
+  b->b64 = cv.take<double>(Tl * D);
+  b->bnorm2 = cv.take<double>(Tl);
+  b->X = cv.take<float>(Tl * P * D);
+  b->R = cv.take<float>(Tl * P * D);
+  b->Dv = cv.take<float>(Tl * P * D);
+  b->W = cv.take<float>(Tl * P * D);
+  b->Xm = cv.take<double>(Tl * C * D);
+  b->Rm = cv.take<double>(Tl * C * D);
+  b->Dm = cv.take<double>(Tl * C * D);
+  b->Wm = cv.take<double>(Tl * C * D);
+  b->U = cv.take<float>(Tl * N * d.Pp);
+  b->Um = cv.take<double>(Tl * N * C);
+  b->rr = cv.take<double>(Tl * P);
+  b->rrm = cv.take<double>(Tl * C);
+  b->dAd = cv.take<double>(Tl * P * d.nRT2);
+  b->dAdm = cv.take<double>(Tl * C * d.nRT2);
+  b->flag = cv.take<int>(Tl * P);
+  b->flagm = cv.take<int>(Tl * C);
+  b->steps = cv.take<int>(Tl * P);
+  b->stepsm = cv.take<int>(Tl * C);
+  b->act = cv.take<int>(Tl * P);
+  b->m_act = cv.take<int>(Tl);
+  b->gam = cv.take<double>(Tl * P * cap);
+  b->xi = cv.take<double>(Tl * P * cap);
+  b->tau = cv.take<double>(Tl * P);
+  b->lz = cv.take<double>(Tl * P * 3 * cap);
+  b->s = cv.take<double>(Tl * C * D);
+  b->nu = cv.take<double>(Tl * C);
+  b->ell = cv.take<double>(Tl * C);
+  b->q = cv.take<double>(Tl * C);
+  b->ll = cv.take<double>(Tl);
+  b->red = cv.take<double>(C * D + C + 1);
+  b->alive = cv.take<int>(cap);
+  b->hist = cv.take<int>(cap);
+  b->histm = cv.take<int>(cap);
+  b->histt = cv.take<int>(cap);
+  b->status = cv.take<int>(8);
+  b->stats = cv.take<double>(16);
+  b->assign = cv.take<int>(Tl);
+  return cv.off;
+}
+
+__global__ void k_alpha_copy(double *a64, float *a32, double *logpi, const double *pi, int n, int C) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) a32[i] = (float)a64[i];
+  if (logpi && blockIdx.x == 0 && threadIdx.x < C) logpi[threadIdx.x] = log(pi[threadIdx.x]);
+}
+
+__global__ void k_check_alpha(const double *a, int n, int *bad) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    if (!(a[i] > 0.0) || !isfinite(a[i])) atomicExch(bad, 1);
+}
+
+cmtcs_status set_alpha(cmtcs_ctx *c, const double *alpha) {
+  const Dims &d = c->kp.d;
+  const size_t n = (size_t)d.C * d.D;
+  CUDA_OK(c, cudaMemcpyAsync(c->kp.b.alpha64, alpha, n * sizeof(double), cudaMemcpyDefault, c->stream));
+  CUDA_OK(c, cudaMemsetAsync(c->kp.b.status + 4, 0, sizeof(int), c->stream));
+  k_check_alpha<<<64, 256, 0, c->stream>>>(c->kp.b.alpha64, (int)n, c->kp.b.status + 4);
+  CUDA_OK(c, cudaMemcpyAsync(c->h_status + 4, c->kp.b.status + 4, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  CUDA_OK(c, cudaStreamSynchronize(c->stream));
+  if (c->h_status[4]) return fail(c, CMTCS_EINVAL, "alpha must be finite and > 0 everywhere");
+  k_alpha_copy<<<64, 256, 0, c->stream>>>(c->kp.b.alpha64, c->kp.b.alpha32, nullptr, nullptr, (int)n, d.C);
+  CUDA_OK(c, cudaGetLastError());
+  CUDA_OK(c, launch_alpha_stats(c->kp, c->stream));
+  c->launches += 3;
+  return CMTCS_OK;
+}
+
+const char *status_name(int code) {
+  switch (code) {
+    case ST_BREAKDOWN: return "CG breakdown (d'Ad <= 0)";
+    case ST_EIG: return "Lanczos quadrature failed (eigen-iteration or Ritz value <= 0)";
+    case ST_NUMERIC: return "non-finite ell / softmax of all -inf";
+    default: return "unknown";
+  }
+}
+
+cmtcs_status one_em_iteration(cmtcs_ctx *c, const uint64_t *probe_bits, const double *q_override,
+                              cmtcs_step_info *info) {
+  KParams kp = c->kp;
+  const Dims &d = kp.d;
+  cudaStream_t s = c->stream;
+  kp.it = c->em_iter;
+  kp.probe_bits = probe_bits;
+  kp.q_override = q_override;
+  int64_t L = 0;
+  CUDA_OK(c, cudaMemsetAsync(kp.b.alive, 0, sizeof(int) * d.cap, s));
+  CUDA_OK(c, cudaMemsetAsync(kp.b.hist, 0, sizeof(int) * d.cap, s));
+  CUDA_OK(c, cudaMemsetAsync(kp.b.histm, 0, sizeof(int) * d.cap, s));
+  CUDA_OK(c, cudaMemsetAsync(kp.b.histt, 0, sizeof(int) * d.cap, s));
+  CUDA_OK(c, launch_init_columns(kp, s));
+  L += 1;
+  const bool tm = c->timing;
+  int nrec = 0;  // events recorded: tev[0] = start of step, then (after stage 2, after update) per CG step
+  if (tm) CUDA_OK(c, cudaEventRecord(c->tev[nrec++], s));
+  // ---- batched CG (Alg. 1) over all T_loc·C·(K+1) columns, host checks convergence lazily ----
+  const int R = c->cg_chunk;
+  int u = 0, chunk = 0;
+  bool done = false;
+  while (u < d.cap && !done) {
+    const int u_end = std::min(u + R, d.cap);
+    for (; u < u_end; ++u) {
+      CUDA_OK(c, launch_stage1(kp, u, nullptr, false, s));
+      CUDA_OK(c, launch_stage2(kp, u, s));
+      if (tm) CUDA_OK(c, cudaEventRecord(c->tev[nrec++], s));
+      CUDA_OK(c, launch_update(kp, u, s));
+      if (tm) CUDA_OK(c, cudaEventRecord(c->tev[nrec++], s));
+      L += 3;
+    }
+    CUDA_OK(c, cudaMemcpyAsync(c->h_alive + (chunk & 1), kp.b.alive + (u_end - 1), sizeof(int),
+                               cudaMemcpyDeviceToHost, s));
+    CUDA_OK(c, cudaEventRecord(c->ev[chunk & 1], s));
+    if (chunk >= 1) {
+      CUDA_OK(c, cudaEventSynchronize(c->ev[(chunk - 1) & 1]));
+      if (c->h_alive[(chunk - 1) & 1] == 0) done = true;
+    }
+    ++chunk;
+  }
+  // ---- estimators: s (Eq. 5), ν̄ (Eq. 7-9), Φμ for ℓ, q and log-lik (Eq. 3) ----
+  CUDA_OK(c, launch_diag(kp, s));
+  CUDA_OK(c, launch_lanczos(kp.b.gam, kp.b.xi, kp.b.steps, d.Tl * d.P, d.cap, d.D, kp.b.tau, kp.b.lz,
+                            kp.b.status, s));
+  CUDA_OK(c, launch_stage1(kp, 0, kp.b.Xm, true, s));
+  CUDA_OK(c, launch_estep_finish(kp, s));
+  // ---- M-step (Eq. 4): local sums → all-reduce over ranks → α update ----
+  CUDA_OK(c, launch_mstep_partial(kp, s));
+  L += 5;
+  if (c->have_comm)
+    NCCL_OK(c, ncclAllReduce(kp.b.red, kp.b.red, (size_t)d.C * d.D + d.C + 1, ncclDouble, ncclSum, c->comm, s));
+  CUDA_OK(c, launch_mstep_finish(kp, s));
+  CUDA_OK(c, launch_alpha_stats(kp, s));
+  {
+    const size_t n = (size_t)d.C * d.D;
+    k_alpha_copy<<<64, 256, 0, s>>>(kp.b.alpha64, kp.b.alpha32, nullptr, nullptr, (int)n, d.C);
+    CUDA_OK(c, cudaGetLastError());
+  }
+  CUDA_OK(c, launch_stats(kp, s));
+  L += 4;
+  if (tm) CUDA_OK(c, cudaEventRecord(c->tev[nrec++], s));
+  CUDA_OK(c, cudaMemcpyAsync(c->h_out, kp.b.stats, 16 * sizeof(double), cudaMemcpyDeviceToHost, s));
+  CUDA_OK(c, cudaMemcpyAsync(c->h_out + 16, kp.b.red + (size_t)d.C * d.D + d.C, sizeof(double),
+                             cudaMemcpyDeviceToHost, s));
+  CUDA_OK(c, cudaMemcpyAsync(c->h_status, kp.b.status, 4 * sizeof(int), cudaMemcpyDeviceToHost, s));
+  CUDA_OK(c, cudaStreamSynchronize(s));
+  c->launches += L;
+  c->have_estep = true;
+  if (tm) {
+    // tev[0] | (op_end, upd_end) x steps | tail_end ; the first op starts after init_columns
+    float ms = 0.f;
+    const int steps = (nrec - 2) / 2;
+    double other = 0.0;
+    for (int i = 0; i < steps; ++i) {
+      CUDA_OK(c, cudaEventElapsedTime(&ms, c->tev[2 * i], c->tev[2 * i + 1]));
+      c->t_ms[0] += ms;
+      CUDA_OK(c, cudaEventElapsedTime(&ms, c->tev[2 * i + 1], c->tev[2 * i + 2]));
+      c->t_ms[1] += ms;
+    }
+    CUDA_OK(c, cudaEventElapsedTime(&ms, c->tev[nrec - 2], c->tev[nrec - 1]));
+    other += ms;
+    c->t_ms[2] += other;
+    c->t_n[0] += steps;
+    c->t_n[1] += steps;
+    c->t_n[2] += 1;
+  }
+  const int it = c->em_iter;
+  c->em_iter += 1;
+  if (c->h_status[0] != ST_OK) {
+    const int code = c->h_status[0];
+    const cmtcs_status st = code == ST_BREAKDOWN ? CMTCS_EBREAKDOWN : code == ST_EIG ? CMTCS_EEIG : CMTCS_ENUMERIC;
+    return fail(c, st, "EM iteration %d: %s at (task %d, column %d, step %d)", it, status_name(code),
+                c->h_status[1], c->h_status[2], c->h_status[3]);
+  }
+  if (info) {
+    const double *o = c->h_out;
+    info->loglik = o[16] / (double)d.T;
+    info->em_iter = it;
+    info->cg_iters = (int32_t)std::max(o[1], o[4]);
+    info->probe_steps_min = (int32_t)o[0];
+    info->probe_steps_max = (int32_t)o[1];
+    info->probe_steps_mean = o[2];
+    info->mu_steps_min = (int32_t)o[3];
+    info->mu_steps_max = (int32_t)o[4];
+    info->n_cap_hit = (int64_t)o[5];
+    info->probe_col_iters = (int64_t)o[6];
+    info->mean_col_iters = (int64_t)o[7];
+    info->task_iters = (int64_t)o[8];
+    info->kernel_launches = L;
+  }
+  return CMTCS_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+cmtcs_status cmtcs_get_unique_id(uint8_t out[128]) {
+  if (!out) return fail(nullptr, CMTCS_EINVAL, "out is NULL");
+  ncclUniqueId id;
+  ncclResult_t r = ncclGetUniqueId(&id);
+  if (r != ncclSuccess) return fail(nullptr, CMTCS_ENCCL, "ncclGetUniqueId: %s", ncclGetErrorString(r));
+  static_assert(sizeof(ncclUniqueId) == 128, "nccl id size");
+  memcpy(out, &id, 128);
+  return CMTCS_OK;
+}
+
+cmtcs_status cmtcs_workspace_size(const cmtcs_problem *p, size_t *bytes) {
+  Dims d;
+  char why[256];
+  if (!bytes) return fail(nullptr, CMTCS_EINVAL, "bytes is NULL");
+  if (!make_dims(p, &d, why)) return fail(nullptr, CMTCS_EINVAL, "%s", why);
+  Bufs b;
+  *bytes = carve(d, nullptr, &b);
+  return CMTCS_OK;
+}
+
+cmtcs_status cmtcs_init(cmtcs_ctx **out, const cmtcs_problem *p, const float *phi, const float *y,
+                        const double *alpha0, void *workspace, size_t workspace_bytes,
+                        const uint8_t *nccl_uid, int32_t rank, int32_t world, int32_t device,
+                        void *cuda_stream) {
+  if (!out) return fail(nullptr, CMTCS_EINVAL, "ctx out-pointer is NULL");
+  *out = nullptr;
+  Dims d;
+  char why[256];
+  if (!make_dims(p, &d, why)) return fail(nullptr, CMTCS_EINVAL, "%s", why);
+  if (!phi || !y || !alpha0 || !workspace) return fail(nullptr, CMTCS_EINVAL, "phi, y, alpha0 and workspace must be non-NULL");
+  if (((uintptr_t)workspace & 255) || ((uintptr_t)phi & 15) || ((uintptr_t)y & 3))
+    return fail(nullptr, CMTCS_EINVAL, "workspace must be 256-byte and phi 16-byte aligned");
+  if (world < 1 || rank < 0 || rank >= world) return fail(nullptr, CMTCS_EINVAL, "bad rank %d / world %d", rank, world);
+  if (world > 1 && !nccl_uid) return fail(nullptr, CMTCS_EINVAL, "world > 1 needs an NCCL unique id");
+  Bufs b;
+  const size_t need = carve(d, nullptr, &b);
+  if (workspace_bytes < need) return fail(nullptr, CMTCS_ENOMEM, "workspace too small: %zu < %zu bytes", workspace_bytes, need);
+  cudaError_t e = cudaSetDevice(device);
+  if (e != cudaSuccess) return fail(nullptr, CMTCS_ECUDA, "cudaSetDevice(%d): %s", device, cudaGetErrorString(e));
+  cmtcs_ctx *c = new (std::nothrow) cmtcs_ctx();
+  if (!c) return fail(nullptr, CMTCS_ENOMEM, "host allocation failed");
+  c->prob = *p;
+  for (int i = 0; i < p->C; ++i) c->pi_host[i] = p->pi[i];
+  c->prob.pi = c->pi_host;
+  c->stream = (cudaStream_t)cuda_stream;
+  c->device = device;
+  c->rank = rank;
+  c->world = world;
+  c->em_iter = p->em_iter0;
+  c->cg_chunk = 8;
+  carve(d, (char *)workspace, &b);
+  c->kp.d = d;
+  c->kp.b = b;
+  c->kp.phi = phi;
+  c->kp.y = y;
+  c->kp.beta = p->beta;
+  c->kp.tol = p->cg_rel_tol;
+  c->kp.alpha_max = p->alpha_max;
+  c->kp.var_floor = p->var_floor;
+  c->kp.empty_eps = p->empty_eps;
+  c->kp.seed = p->probe_seed;
+  *out = c;  // from here on errors leave a (broken) ctx the caller destroys
+  CUDA_OK(c, cudaMallocHost((void **)&c->h_alive, 2 * sizeof(int)));
+  CUDA_OK(c, cudaMallocHost((void **)&c->h_out, 32 * sizeof(double)));
+  CUDA_OK(c, cudaMallocHost((void **)&c->h_status, 8 * sizeof(int)));
+  CUDA_OK(c, cudaEventCreateWithFlags(&c->ev[0], cudaEventDisableTiming));
+  CUDA_OK(c, cudaEventCreateWithFlags(&c->ev[1], cudaEventDisableTiming));
+  CUDA_OK(c, cudaMemsetAsync(b.status, 0, 8 * sizeof(int), c->stream));
+  CUDA_OK(c, cudaMemsetAsync(b.gam, 0, sizeof(double) * d.Tl * d.P * d.cap, c->stream));
+  CUDA_OK(c, cudaMemsetAsync(b.xi, 0, sizeof(double) * d.Tl * d.P * d.cap, c->stream));
+  // π: log π_c on device
+  double *pi_dev = b.red;  // scratch: red is rewritten every M-step
+  CUDA_OK(c, cudaMemcpyAsync(pi_dev, c->pi_host, sizeof(double) * p->C, cudaMemcpyHostToDevice, c->stream));
+  k_alpha_copy<<<1, 32, 0, c->stream>>>(b.alpha64, b.alpha32, b.logpi, pi_dev, 0, p->C);
+  CUDA_OK(c, cudaGetLastError());
+  cmtcs_status st = set_alpha(c, alpha0);
+  if (st != CMTCS_OK) { c->broken = true; return st; }
+  CUDA_OK(c, launch_rhs(c->kp, c->stream));
+  c->launches += 3;
+  CUDA_OK(c, cudaStreamSynchronize(c->stream));
+  if (world > 1) {
+    ncclUniqueId id;
+    memcpy(&id, nccl_uid, 128);
+    NCCL_OK(c, ncclCommInitRank(&c->comm, world, id, rank));
+    c->have_comm = true;
+  }
+  return CMTCS_OK;
+}
+
+cmtcs_status cmtcs_em_step(cmtcs_ctx *c, int32_t n_iters, const uint64_t *probe_bits,
+                           const double *q_override, cmtcs_step_info *info) {
+  if (!c) return fail(nullptr, CMTCS_EINVAL, "ctx is NULL");
+  if (c->broken) return CMTCS_ESTATE;
+  if (n_iters < 1) return fail(c, CMTCS_EINVAL, "n_iters must be >= 1");
+  if ((probe_bits || q_override) && n_iters != 1)
+    return fail(c, CMTCS_EINVAL, "probe_bits / q_override require n_iters == 1");
+  CUDA_OK(c, cudaSetDevice(c->device));
+  for (int i = 0; i < n_iters; ++i) {
+    cmtcs_status st = one_em_iteration(c, probe_bits, q_override, info);
+    if (st != CMTCS_OK) return st;
+  }
+  return CMTCS_OK;
+}
+
+cmtcs_status cmtcs_posterior(cmtcs_ctx *c, double *mu, double *s, double *logdet, double *q,
+                             double *alpha, int32_t *assign, double *recon) {
+  if (!c) return fail(nullptr, CMTCS_EINVAL, "ctx is NULL");
+  if (c->broken) return CMTCS_ESTATE;
+  if (!c->have_estep) return fail(c, CMTCS_ESTATE, "posterior requested before any em_step");
+  const Dims &d = c->kp.d;
+  const Bufs &b = c->kp.b;
+  cudaStream_t st = c->stream;
+  const size_t tcd = (size_t)d.Tl * d.C * d.D, tc = (size_t)d.Tl * d.C;
+  if (mu) CUDA_OK(c, cudaMemcpyAsync(mu, b.Xm, tcd * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  if (s) CUDA_OK(c, cudaMemcpyAsync(s, b.s, tcd * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  if (logdet) CUDA_OK(c, cudaMemcpyAsync(logdet, b.nu, tc * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  if (q) CUDA_OK(c, cudaMemcpyAsync(q, b.q, tc * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  if (alpha) CUDA_OK(c, cudaMemcpyAsync(alpha, b.alpha64, (size_t)d.C * d.D * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  if (assign || recon) {
+    CUDA_OK(c, launch_readout(c->kp, recon, st));
+    c->launches += 1;
+    if (assign) CUDA_OK(c, cudaMemcpyAsync(assign, b.assign, d.Tl * sizeof(int), cudaMemcpyDeviceToDevice, st));
+  }
+  return CMTCS_OK;
+}
+
+cmtcs_status cmtcs_set_state(cmtcs_ctx *c, const double *alpha, int32_t em_iter) {
+  if (!c) return fail(nullptr, CMTCS_EINVAL, "ctx is NULL");
+  if (c->broken) return CMTCS_ESTATE;
+  if (em_iter < 0) return fail(c, CMTCS_EINVAL, "em_iter must be >= 0");
+  if (alpha) {
+    cmtcs_status st = set_alpha(c, alpha);
+    if (st != CMTCS_OK) return st;
+  }
+  c->em_iter = em_iter;
+  return CMTCS_OK;
+}
+
+cmtcs_status cmtcs_transcript(cmtcs_ctx *c, double *gamma, double *xi, int32_t *steps, int32_t *mu_steps) {
+  if (!c) return fail(nullptr, CMTCS_EINVAL, "ctx is NULL");
+  if (c->broken) return CMTCS_ESTATE;
+  if (!c->have_estep) return fail(c, CMTCS_ESTATE, "transcript requested before any em_step");
+  const Dims &d = c->kp.d;
+  if (gamma || xi) {
+    CUDA_OK(c, launch_copy_transcript(c->kp, gamma, xi, c->stream));
+    c->launches += 1;
+  }
+  if (steps) CUDA_OK(c, cudaMemcpyAsync(steps, c->kp.b.steps, sizeof(int) * d.Tl * d.P, cudaMemcpyDeviceToDevice, c->stream));
+  if (mu_steps) CUDA_OK(c, cudaMemcpyAsync(mu_steps, c->kp.b.stepsm, sizeof(int) * d.Tl * d.C, cudaMemcpyDeviceToDevice, c->stream));
+  return CMTCS_OK;
+}
+
+const char *cmtcs_last_error(const cmtcs_ctx *c) { return c ? c->err : g_err; }
+
+void cmtcs_destroy(cmtcs_ctx *c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  if (c->have_comm) ncclCommDestroy(c->comm);
+  if (c->ev[0]) cudaEventDestroy(c->ev[0]);
+  if (c->ev[1]) cudaEventDestroy(c->ev[1]);
+  if (c->h_alive) cudaFreeHost(c->h_alive);
+  if (c->h_out) cudaFreeHost(c->h_out);
+  if (c->h_status) cudaFreeHost(c->h_status);
+  if (c->tev) {
+    for (int i = 0; i < c->ntev; ++i)
+      if (c->tev[i]) cudaEventDestroy(c->tev[i]);
+    delete[] c->tev;
+  }
+  delete c;
+}
+
+int64_t cmtcs_kernel_launches(const cmtcs_ctx *c) { return c ? c->launches : 0; }
+
+cmtcs_status cmtcs_set_timing(cmtcs_ctx *c, int32_t enable) {
+  if (!c) return fail(nullptr, CMTCS_EINVAL, "ctx is NULL");
+  if (c->broken) return CMTCS_ESTATE;
+  if (enable && !c->tev) {
+    c->ntev = 2 * c->kp.d.cap + 2;
+    c->tev = new (std::nothrow) cudaEvent_t[c->ntev]();
+    if (!c->tev) return fail(c, CMTCS_ENOMEM, "event pool allocation failed");
+    CUDA_OK(c, cudaSetDevice(c->device));
+    for (int i = 0; i < c->ntev; ++i) CUDA_OK(c, cudaEventCreate(&c->tev[i]));
+  }
+  c->timing = enable != 0;
+  return CMTCS_OK;
+}
+
+cmtcs_status cmtcs_get_timing(cmtcs_ctx *c, double ms[3], int64_t n[3], int32_t reset) {
+  if (!c) return fail(nullptr, CMTCS_EINVAL, "ctx is NULL");
+  for (int i = 0; i < 3; ++i) {
+    if (ms) ms[i] = c->t_ms[i];
+    if (n) n[i] = c->t_n[i];
+    if (reset) { c->t_ms[i] = 0; c->t_n[i] = 0; }
+  }
+  return CMTCS_OK;
+}
+
+cmtcs_status cmtcs_probe_words(uint64_t seed, int32_t it, int32_t T, int32_t t0, int32_t T_loc, int32_t C,
+                               int32_t K, int32_t D, uint64_t *out, void *stream) {
+  if (!out || T < 1 || t0 < 0 || T_loc < 1 || t0 + T_loc > T || C < 1 || K < 1 || D < 1 || it < 0)
+    return fail(nullptr, CMTCS_EINVAL, "bad arguments to cmtcs_probe_words");
+  cudaError_t e = launch_probe_words(seed, it, T, t0, T_loc, C, K, D, out, (cudaStream_t)stream);
+  if (e != cudaSuccess) return fail(nullptr, CMTCS_ECUDA, "probe words: %s", cudaGetErrorString(e));
+  return CMTCS_OK;
+}
+
+cmtcs_status cmtcs_lanczos_quadrature(const double *gamma, const double *xi, const int32_t *steps, int32_t n,
+                                      int32_t ld, int32_t D, double *tau, double *scratch, void *stream) {
+  if (!gamma || !xi || !steps || !tau || !scratch || n < 0 || ld < 1 || D < 1)
+    return fail(nullptr, CMTCS_EINVAL, "bad arguments to cmtcs_lanczos_quadrature");
+  int *status = nullptr;
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaError_t e = cudaMallocAsync((void **)&status, 8 * sizeof(int), s);
+  if (e == cudaSuccess) e = cudaMemsetAsync(status, 0, 8 * sizeof(int), s);
+  if (e == cudaSuccess) e = launch_lanczos(gamma, xi, steps, n, ld, D, tau, scratch, status, s);
+  int h[4] = {0, 0, 0, 0};
+  if (e == cudaSuccess) e = cudaMemcpyAsync(h, status, 4 * sizeof(int), cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (status) cudaFreeAsync(status, s);
+  if (e != cudaSuccess) return fail(nullptr, CMTCS_ECUDA, "lanczos quadrature: %s", cudaGetErrorString(e));
+  if (h[0] != ST_OK) return fail(nullptr, CMTCS_EEIG, "lanczos quadrature failed at column %d (%d, %d)", h[1], h[2], h[3]);
+  return CMTCS_OK;
+}
+
+}  // extern "C"

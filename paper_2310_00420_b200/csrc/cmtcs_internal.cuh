@@ -1,0 +1,106 @@
+// Internal declarations shared by the libcmtcs translation units (not part of the C ABI).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "cmtcs.h"
+
+namespace cmtcs {
+
+constexpr int MAXC = 16;        // clusters supported by the fp64 mean-column tiles
+constexpr int OP_BR = 128;      // operator CTA tile: rows (N in stage 1, D in stage 2)
+constexpr int OP_BC = 64;       // operator CTA tile: probe columns
+constexpr int OP_BK = 16;       // contraction chunk
+constexpr int OP_THREADS = 256;
+constexpr int UPD_THREADS = 256;
+
+// Sizes of one rank's problem.  Column index of probe (c, k) inside a task: col = c*K + k.
+struct Dims {
+  int T, Tl, t0, N, D, C, K;
+  int P;     // probe columns per task = C*K
+  int Pp;    // P rounded up to a multiple of 4 (row stride of U)
+  int cap;   // CG step cap U
+  int nw;    // 64-bit probe words per column = ceil(D/64)
+  int nRT1;  // stage-1 row tiles  = ceil(N / OP_BR)
+  int nRT2;  // stage-2 row tiles  = ceil(D / OP_BR)
+  int nCT;   // probe column tiles = ceil(P / OP_BC)
+  int shared_phi;
+  int64_t phi_task_stride;  // elements between Φ_t and Φ_{t+1} (0 if shared)
+};
+
+// Device buffers carved from the caller's workspace (all sizes in DESIGN.md §5).
+struct Bufs {
+  double *alpha64;   // [C][D]
+  float *alpha32;    // [C][D]
+  double *logsum_alpha;  // [C]  Σ_d log α_cd
+  double *logpi;     // [C]
+  double *b64;       // [Tl][D]   βΦᵀy
+  double *bnorm2;    // [Tl]      ‖b‖²
+  float *X, *R, *Dv, *W;     // probe columns [Tl][P][D]
+  double *Xm, *Rm, *Dm, *Wm; // mean columns  [Tl][C][D]
+  float *U;          // [Tl][N][Pp]  stage-1 output (compacted column order)
+  double *Um;        // [Tl][N][C]
+  double *rr;        // [Tl][P]
+  double *rrm;       // [Tl][C]
+  double *dAd;       // [Tl][P][nRT2]  per-row-tile partial dᵀAd
+  double *dAdm;      // [Tl][C][nRT2]
+  int *flag;         // [Tl][P]  1 = active
+  int *flagm;        // [Tl][C]
+  int *steps;        // [Tl][P]
+  int *stepsm;       // [Tl][C]
+  int *act;          // [Tl][P]  compacted active probe columns (ascending)
+  int *m_act;        // [Tl]
+  double *gam, *xi;  // [Tl*P][cap]
+  double *tau;       // [Tl*P]
+  double *lz;        // [Tl*P][3*cap] quadrature scratch
+  double *s;         // [Tl][C][D]
+  double *nu, *ell, *q;  // [Tl][C]
+  double *ll;        // [Tl]
+  double *red;       // [C*D + C + 1]  Eq. 4 sums (den, num) and Σ_t log p(y_t)
+  int *alive;        // [cap]  columns still active after step u
+  int *hist;         // [cap]  probe columns active at step u
+  int *histm;        // [cap]  mean columns active at step u
+  int *histt;        // [cap]  tasks with an active column at step u
+  int *status;       // [8]    first error: code, t, col, u
+  double *stats;     // [16]   step statistics (filled by k_stats)
+  int *assign;       // [Tl]
+};
+
+struct KParams {
+  Dims d;
+  Bufs b;
+  const float *phi;
+  const float *y;
+  double beta;
+  double tol;
+  double alpha_max, var_floor, empty_eps;
+  uint64_t seed;
+  int it;                      // global EM iteration index of this E-step
+  const uint64_t *probe_bits;  // optional override
+  const double *q_override;    // optional
+};
+
+// launchers (return cudaGetLastError())
+cudaError_t launch_init_columns(const KParams &p, cudaStream_t s);
+cudaError_t launch_stage1(const KParams &p, int u, const double *mu_src, bool mu_only, cudaStream_t s);
+cudaError_t launch_stage2(const KParams &p, int u, cudaStream_t s);
+cudaError_t launch_update(const KParams &p, int u, cudaStream_t s);
+cudaError_t launch_rhs(const KParams &p, cudaStream_t s);
+cudaError_t launch_alpha_stats(const KParams &p, cudaStream_t s);
+cudaError_t launch_diag(const KParams &p, cudaStream_t s);
+cudaError_t launch_lanczos(const double *gam, const double *xi, const int *steps, int n, int ld,
+                           int D, double *tau, double *scratch, int *status, cudaStream_t s);
+cudaError_t launch_estep_finish(const KParams &p, cudaStream_t s);
+cudaError_t launch_mstep_partial(const KParams &p, cudaStream_t s);
+cudaError_t launch_mstep_finish(const KParams &p, cudaStream_t s);
+cudaError_t launch_stats(const KParams &p, cudaStream_t s);
+cudaError_t launch_readout(const KParams &p, double *recon, cudaStream_t s);
+cudaError_t launch_probe_words(uint64_t seed, int it, int T, int t0, int Tl, int C, int K, int D,
+                               uint64_t *out, cudaStream_t s);
+cudaError_t launch_copy_transcript(const KParams &p, double *gam, double *xi, cudaStream_t s);
+
+// error codes written to status[0] by kernels
+enum { ST_OK = 0, ST_BREAKDOWN = 1, ST_EIG = 2, ST_NUMERIC = 3 };
+
+}  // namespace cmtcs

@@ -1,0 +1,356 @@
+// K6 diagonal estimate (Eq. 5), K7 Lanczos-quadrature log-det (Eq. 7-9), K8 ℓ / q / log-lik
+// (Eq. 3), K9/K10 M-step (Eq. 4), K11 readout (Alg. 2 lines 17-20) and step statistics.
+#include <float.h>
+
+#include "cmtcs_internal.cuh"
+
+namespace cmtcs {
+
+namespace {
+
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+__device__ __forceinline__ double block_sum(double v, double *sh) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  __syncthreads();
+  if (lane == 0) sh[wid] = v;
+  __syncthreads();
+  double s = 0.0;
+  for (int i = 0; i < nw; ++i) s += sh[i];
+  return s;
+}
+
+// K6: s_tc = (1/K) Σ_k p_k ⊙ x_k   (Eq. 5; Alg. 2 line 7).  Probes are regenerated
+// from the counter hash (or the override words) instead of being stored.
+__global__ void k_diag(KParams p) {
+  const Dims &d = p.d;
+  const int dd = blockIdx.x * blockDim.x + threadIdx.x, c = blockIdx.y, t = blockIdx.z;
+  if (dd >= d.D) return;
+  double acc = 0.0;
+  for (int k = 0; k < d.K; ++k) {
+    uint64_t wd;
+    if (p.probe_bits) {
+      wd = p.probe_bits[(((size_t)t * d.C + c) * d.K + k) * d.nw + (dd >> 6)];
+    } else {
+      const uint64_t w = ((((uint64_t)p.it * d.T + (uint64_t)(d.t0 + t)) * d.C + c) * d.K + k) * d.nw + (dd >> 6);
+      wd = mix64(p.seed + (w + 1ull) * 0x9E3779B97F4A7C15ull);
+    }
+    const double x = (double)p.b.X[((size_t)t * d.P + c * d.K + k) * d.D + dd];
+    acc += ((wd >> (dd & 63)) & 1ull) ? -x : x;
+  }
+  p.b.s[((size_t)t * d.C + c) * d.D + dd] = acc / (double)d.K;
+}
+
+// K7: τ = D · Σ_u S̄²_{u,1} log λ̄_u for Γ̄ assembled from (γ, ξ) (Eq. 7-8).
+// One thread per tridiagonal: implicit-shift QL iteration on (diag, off-diag), applying every
+// Givens rotation to the first row z of the eigenvector matrix only (z₀ = e₁), so S̄_{u,1} = z_u
+// (eigenvectors are the rows of S̄).  O(U'²) per matrix, fp64.
+__global__ void k_lanczos(const double *__restrict__ gam, const double *__restrict__ xi,
+                          const int *__restrict__ steps, int n, int ld, int D, double *tau,
+                          double *scratch, int *status) {
+  const int g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= n) return;
+  const int U = steps[g];
+  const double *ga = gam + (size_t)g * ld, *xa = xi + (size_t)g * ld;
+  double *dg = scratch + (size_t)g * 3 * ld, *e = dg + ld, *z = e + ld;
+  if (U < 1 || U > ld) {
+    tau[g] = nan("");
+    if (atomicCAS(status, 0, ST_EIG) == 0) { status[1] = g; status[2] = U; status[3] = -1; }
+    return;
+  }
+  for (int i = 0; i < U; ++i) {
+    const double gi = ga[i];
+    if (!(gi > 0.0)) {
+      tau[g] = nan("");
+      if (atomicCAS(status, 0, ST_EIG) == 0) { status[1] = g; status[2] = i; status[3] = -2; }
+      return;
+    }
+    dg[i] = 1.0 / gi + (i > 0 ? xa[i - 1] / ga[i - 1] : 0.0);   // Γ_uu
+    e[i] = (i + 1 < U) ? sqrt(xa[i]) / gi : 0.0;                 // Γ_{u+1,u}
+    z[i] = (i == 0) ? 1.0 : 0.0;
+  }
+  bool ok = true;
+  for (int l = 0; l < U && ok; ++l) {
+    int iter = 0;
+    for (;;) {
+      int m = l;
+      for (; m < U - 1; ++m) {
+        const double dd = fabs(dg[m]) + fabs(dg[m + 1]);
+        if (fabs(e[m]) <= DBL_EPSILON * dd) break;
+      }
+      if (m == l) break;
+      if (++iter > 200) { ok = false; break; }
+      double gg = (dg[l + 1] - dg[l]) / (2.0 * e[l]);
+      double r = hypot(gg, 1.0);
+      gg = dg[m] - dg[l] + e[l] / (gg + copysign(r, gg));
+      double s = 1.0, c = 1.0, pp = 0.0;
+      bool deflated = false;
+      for (int i = m - 1; i >= l; --i) {
+        double f = s * e[i];
+        const double b = c * e[i];
+        r = hypot(f, gg);
+        e[i + 1] = r;
+        if (r == 0.0) {          // underflow: split the matrix and restart this l
+          dg[i + 1] -= pp;
+          e[m] = 0.0;
+          deflated = true;
+          break;
+        }
+        s = f / r;
+        c = gg / r;
+        gg = dg[i + 1] - pp;
+        r = (dg[i] - gg) * s + 2.0 * c * b;
+        pp = s * r;
+        dg[i + 1] = gg + pp;
+        gg = c * r - b;
+        f = z[i + 1];                 // rotate columns i, i+1 of the eigenvector matrix (row 0)
+        z[i + 1] = s * z[i] + c * f;
+        z[i] = c * z[i] - s * f;
+      }
+      if (deflated) continue;
+      dg[l] -= pp;
+      e[l] = gg;
+      e[m] = 0.0;
+    }
+  }
+  double acc = 0.0;
+  for (int i = 0; i < U && ok; ++i) {
+    if (!(dg[i] > 0.0)) { ok = false; break; }
+    acc += z[i] * z[i] * log(dg[i]);
+  }
+  if (!ok) {
+    tau[g] = nan("");
+    if (atomicCAS(status, 0, ST_EIG) == 0) { status[1] = g; status[2] = U; status[3] = -3; }
+    return;
+  }
+  tau[g] = (double)D * acc;
+}
+
+// K8: ν̄_tc = −(1/K)Σ_k τ_tck (Eq. 9);  ℓ̃_tc = ν̄ + Σ_d log α_cd − β‖y − Φμ‖² − μᵀdiag(α)μ
+// (reading A1: PAPER.md:59's ℓ minus the c-independent β‖y‖²);  q_t = softmax(½ℓ̃ + log π)
+// (Eq. 3);  log p(y_t|θ̂) = logsumexp(½ℓ̃ + log π) + (N/2) log(β/2π)  (A2).
+__global__ void k_estep_finish(KParams p) {
+  __shared__ double sh[32];
+  __shared__ double s_ell[MAXC];
+  const Dims &d = p.d;
+  const int t = blockIdx.x, tid = threadIdx.x;
+  const double beta = p.beta;
+  for (int c = 0; c < d.C; ++c) {
+    const double *mu = p.b.Xm + ((size_t)t * d.C + c) * d.D;
+    const double *al = p.b.alpha64 + (size_t)c * d.D;
+    double quad = 0.0;
+    for (int i = tid; i < d.D; i += blockDim.x) quad = fma(al[i] * mu[i], mu[i], quad);
+    quad = block_sum(quad, sh);
+    double res = 0.0;
+    for (int n = tid; n < d.N; n += blockDim.x) {
+      const double rv = (double)p.y[(size_t)t * d.N + n] - p.b.Um[((size_t)t * d.N + n) * d.C + c];
+      res = fma(rv, rv, res);
+    }
+    res = block_sum(res, sh);
+    if (tid == 0) {
+      double tsum = 0.0;
+      for (int k = 0; k < d.K; ++k) tsum += p.b.tau[(size_t)t * d.P + c * d.K + k];
+      const double nu = -tsum / (double)d.K;
+      p.b.nu[t * d.C + c] = nu;
+      s_ell[c] = nu + p.b.logsum_alpha[c] - beta * res - quad;
+      p.b.ell[t * d.C + c] = s_ell[c];
+    }
+  }
+  if (tid == 0) {
+    double a[MAXC], mx = -INFINITY;
+    for (int c = 0; c < d.C; ++c) {
+      a[c] = 0.5 * s_ell[c] + p.b.logpi[c];
+      mx = fmax(mx, a[c]);
+    }
+    bool bad = !isfinite(mx);
+    for (int c = 0; c < d.C; ++c) bad |= isnan(a[c]) || (a[c] == INFINITY);
+    if (bad) {
+      if (atomicCAS(p.b.status, 0, ST_NUMERIC) == 0) { p.b.status[1] = d.t0 + t; p.b.status[2] = -1; p.b.status[3] = -1; }
+      for (int c = 0; c < d.C; ++c) p.b.q[t * d.C + c] = nan("");
+      p.b.ll[t] = nan("");
+      return;
+    }
+    double se = 0.0;
+    for (int c = 0; c < d.C; ++c) se += exp(a[c] - mx);
+    for (int c = 0; c < d.C; ++c) p.b.q[t * d.C + c] = exp(a[c] - mx) / se;
+    p.b.ll[t] = mx + log(se) + 0.5 * d.N * log(beta / (2.0 * 3.14159265358979323846));
+  }
+}
+
+__global__ void k_alpha_stats(KParams p) {
+  __shared__ double sh[32];
+  const int c = blockIdx.x;
+  double v = 0.0;
+  for (int i = threadIdx.x; i < p.d.D; i += blockDim.x) v += log(p.b.alpha64[(size_t)c * p.d.D + i]);
+  v = block_sum(v, sh);
+  if (threadIdx.x == 0) p.b.logsum_alpha[c] = v;
+}
+
+// K9: Eq. 4 sums over this rank's tasks (fixed task order), plus Σ_t log p(y_t).
+//   red[c·D + d] = Σ_t q_tc (μ_tcd² + max(s_tcd, var_floor))   red[C·D + c] = Σ_t q_tc
+__global__ void k_mstep_partial(KParams p) {
+  const Dims &d = p.d;
+  const int dd = blockIdx.x * blockDim.x + threadIdx.x, c = blockIdx.y;
+  const double *q = p.q_override ? p.q_override : p.b.q;
+  if (dd < d.D) {
+    double den = 0.0;
+    for (int t = 0; t < d.Tl; ++t) {
+      const size_t o = ((size_t)t * d.C + c) * d.D + dd;
+      const double mu = p.b.Xm[o];
+      den = fma(q[t * d.C + c], fma(mu, mu, fmax(p.b.s[o], p.var_floor)), den);
+    }
+    p.b.red[(size_t)c * d.D + dd] = den;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    double num = 0.0;
+    for (int t = 0; t < d.Tl; ++t) num += q[t * d.C + c];
+    p.b.red[(size_t)d.C * d.D + c] = num;
+  }
+  if (blockIdx.x == 0 && c == 0 && threadIdx.x == 32) {
+    double ll = 0.0;
+    for (int t = 0; t < d.Tl; ++t) ll += p.b.ll[t];
+    p.b.red[(size_t)d.C * d.D + d.C] = ll;
+  }
+}
+
+// K10: α̃_cd = min(num_c / den_cd, α_max); clusters with num_c < empty_eps keep α (A10).
+__global__ void k_mstep_finish(KParams p) {
+  const Dims &d = p.d;
+  const int dd = blockIdx.x * blockDim.x + threadIdx.x, c = blockIdx.y;
+  if (dd >= d.D) return;
+  const double num = p.b.red[(size_t)d.C * d.D + c];
+  if (num < p.empty_eps) return;
+  const double a = fmin(num / p.b.red[(size_t)c * d.D + dd], p.alpha_max);
+  p.b.alpha64[(size_t)c * d.D + dd] = a;
+  p.b.alpha32[(size_t)c * d.D + dd] = (float)a;
+}
+
+// K11: a_t = argmax_c q_tc (ties → lowest c, A11);  ẑ_t = μ_{t,a_t}
+__global__ void k_readout(KParams p, double *recon) {
+  const Dims &d = p.d;
+  const int t = blockIdx.x;
+  __shared__ int s_a;
+  if (threadIdx.x == 0) {
+    int a = 0;
+    double best = p.b.q[t * d.C];
+    for (int c = 1; c < d.C; ++c)
+      if (p.b.q[t * d.C + c] > best) { best = p.b.q[t * d.C + c]; a = c; }
+    s_a = a;
+    p.b.assign[t] = a;
+  }
+  __syncthreads();
+  if (recon)
+    for (int i = threadIdx.x; i < d.D; i += blockDim.x)
+      recon[(size_t)t * d.D + i] = p.b.Xm[((size_t)t * d.C + s_a) * d.D + i];
+}
+
+// step statistics for cmtcs_step_info (one CTA)
+__global__ void k_stats(KParams p) {
+  __shared__ double sh[32];
+  const Dims &d = p.d;
+  const int tid = threadIdx.x;
+  const int np = d.Tl * d.P, nm = d.Tl * d.C;
+  double smin = 1e300, smax = 0, ssum = 0, mmin = 1e300, mmax = 0, caph = 0;
+  for (int i = tid; i < np; i += blockDim.x) {
+    const double s = p.b.steps[i];
+    smin = fmin(smin, s); smax = fmax(smax, s); ssum += s; caph += (p.b.flag[i] == 2);
+  }
+  for (int i = tid; i < nm; i += blockDim.x) {
+    const double s = p.b.stepsm[i];
+    mmin = fmin(mmin, s); mmax = fmax(mmax, s); caph += (p.b.flagm[i] == 2);
+  }
+  double h = 0, hm = 0, ht = 0;
+  for (int u = tid; u < d.cap; u += blockDim.x) { h += p.b.hist[u]; hm += p.b.histm[u]; ht += p.b.histt[u]; }
+  // min/max via negation trick on sums is not possible; use shared reductions
+  __shared__ double red[6][256];
+  red[0][tid] = smin; red[1][tid] = smax; red[2][tid] = mmin; red[3][tid] = mmax;
+  __syncthreads();
+  for (int o = blockDim.x / 2; o; o >>= 1) {
+    if (tid < o) {
+      red[0][tid] = fmin(red[0][tid], red[0][tid + o]);
+      red[1][tid] = fmax(red[1][tid], red[1][tid + o]);
+      red[2][tid] = fmin(red[2][tid], red[2][tid + o]);
+      red[3][tid] = fmax(red[3][tid], red[3][tid + o]);
+    }
+    __syncthreads();
+  }
+  ssum = block_sum(ssum, sh);
+  caph = block_sum(caph, sh);
+  h = block_sum(h, sh);
+  hm = block_sum(hm, sh);
+  ht = block_sum(ht, sh);
+  if (tid == 0) {
+    double *o = p.b.stats;
+    o[0] = np ? red[0][0] : 0; o[1] = red[1][0]; o[2] = np ? ssum / np : 0;
+    o[3] = nm ? red[2][0] : 0; o[4] = red[3][0]; o[5] = caph;
+    o[6] = h; o[7] = hm; o[8] = ht;
+  }
+}
+
+__global__ void k_copy_transcript(KParams p, double *gam, double *xi) {
+  const Dims &d = p.d;
+  const size_t n = (size_t)d.Tl * d.P * d.cap;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    const size_t col = i / d.cap, u = i % d.cap;
+    const bool valid = (int)u < p.b.steps[col];
+    if (gam) gam[i] = valid ? p.b.gam[i] : nan("");
+    if (xi) xi[i] = valid ? p.b.xi[i] : nan("");
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_diag(const KParams &p, cudaStream_t s) {
+  k_diag<<<dim3((p.d.D + 255) / 256, p.d.C, p.d.Tl), 256, 0, s>>>(p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_lanczos(const double *gam, const double *xi, const int *steps, int n, int ld, int D,
+                           double *tau, double *scratch, int *status, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  k_lanczos<<<(n + 63) / 64, 64, 0, s>>>(gam, xi, steps, n, ld, D, tau, scratch, status);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_estep_finish(const KParams &p, cudaStream_t s) {
+  k_estep_finish<<<p.d.Tl, 256, 0, s>>>(p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_alpha_stats(const KParams &p, cudaStream_t s) {
+  k_alpha_stats<<<p.d.C, 256, 0, s>>>(p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_mstep_partial(const KParams &p, cudaStream_t s) {
+  k_mstep_partial<<<dim3((p.d.D + 255) / 256, p.d.C), 256, 0, s>>>(p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_mstep_finish(const KParams &p, cudaStream_t s) {
+  k_mstep_finish<<<dim3((p.d.D + 255) / 256, p.d.C), 256, 0, s>>>(p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_stats(const KParams &p, cudaStream_t s) {
+  k_stats<<<1, 256, 0, s>>>(p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_readout(const KParams &p, double *recon, cudaStream_t s) {
+  k_readout<<<p.d.Tl, 256, 0, s>>>(p, recon);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_copy_transcript(const KParams &p, double *gam, double *xi, cudaStream_t s) {
+  k_copy_transcript<<<592, 256, 0, s>>>(p, gam, xi);
+  return cudaGetLastError();
+}
+
+}  // namespace cmtcs

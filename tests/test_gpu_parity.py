@@ -1,0 +1,320 @@
+"""Parity of the CUDA path (libcmtcs.so through the C ABI) with the fp64 CPU oracle.
+
+Tolerances (DESIGN.md §6 derives them):
+  μ (fp64 mean columns on both sides, same tol/cap) ............ rel_∞ ≤ 1e-4 (expected ~1e-9)
+  s on (t,c) blocks whose probes converged on both sides ........ rel_∞ ≤ 1e-4
+  ν̄ (fp32 transcripts vs fp64) ................................. |Δ| ≤ 5e-3 + 1e-6|ν̄|
+  q ............................................................ |Δ| ≤ 1e-3
+  α (when q is one-hot to 1e-5) and q-conditioned α ............ rel_∞ ≤ 1e-4
+  L(θ̂) ......................................................... |Δ| ≤ 1e-3
+  probe words: bit-exact.  Lanczos quadrature on identical transcripts: rel ≤ 1e-10.
+"""
+import numpy as np
+import pytest
+
+import synthetic
+from oracle import cofem as O
+from gpu_common import compare_step, make_gpu, oracle_state, rel_inf, to_np
+
+pytestmark = pytest.mark.gpu
+
+MU_TOL, S_TOL, Q_TOL, A_TOL, L_TOL = 1e-4, 1e-4, 1e-3, 1e-4, 1e-3
+
+
+def nu_tol(nu):
+    return 5e-3 + 1e-6 * np.abs(nu)
+
+
+@pytest.fixture(scope="module")
+def torch_cuda():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    return torch
+
+
+# ------------------------------------------------------------------------------ K3 probes ----
+@pytest.mark.parametrize("D", [64, 100, 1024, 130])
+def test_probe_words_bit_exact(torch_cuda, D):
+    from paper_2310_00420_b200 import probe_words
+    seed, it, T, t0, Tl, C, K = 0x1234_5678_9ABC_DEF0, 7, 50, 13, 5, 3, 4
+    got = probe_words(seed, it, T, t0, Tl, C, K, D).cpu().numpy().view(np.uint64)
+    nw = (D + 63) // 64
+    for i in range(Tl):
+        for c in range(C):
+            for k in range(K):
+                w = ((((it * T + t0 + i) * C + c) * K + k) * nw) + np.arange(nw, dtype=np.uint64)
+                np.testing.assert_array_equal(got[i, c, k], O.probe_word(seed, w))
+    # and the sign convention: the oracle's ±1 probes from these words
+    P = O.probe_signs(seed, it, T, t0 + 1, C, K, D)
+    bits = (got[1][..., np.arange(D) // 64] >> (np.arange(D) % 64).astype(np.uint64)) & np.uint64(1)
+    np.testing.assert_array_equal(np.where(bits == 1, -1.0, 1.0), P)
+
+
+# ------------------------------------------------------------------------------ K7 log-det --
+def test_lanczos_quadrature_random_transcripts(torch_cuda):
+    import torch
+    from paper_2310_00420_b200 import lanczos_quadrature
+    rng = np.random.default_rng(0)
+    ld = 300
+    lengths = [1, 2, 3, 17, 64, 150, 300]
+    n = len(lengths)
+    gam = np.full((n, ld), np.nan)
+    xi = np.full((n, ld), np.nan)
+    for j, U in enumerate(lengths):
+        gam[j, :U] = rng.uniform(0.01, 2.0, U)
+        xi[j, :U] = rng.uniform(0.05, 1.5, U)
+    tau = lanczos_quadrature(torch.tensor(gam).cuda(), torch.tensor(xi).cuda(),
+                             torch.tensor(lengths, dtype=torch.int32).cuda(), 1000).cpu().numpy()
+    for j, U in enumerate(lengths):
+        want = O.quadrature_term(gam[j, :U], xi[j, :U], 1000)
+        assert tau[j] == pytest.approx(want, rel=1e-10, abs=1e-9)
+
+
+def test_lanczos_quadrature_real_cg_transcripts(torch_cuda):
+    """Transcripts of CG on SPD systems (incl. U' = D, where Eq. 8 is exact: PAPER.md:134-138)."""
+    import torch
+    import scipy.linalg
+    from paper_2310_00420_b200 import lanczos_quadrature
+    rng = np.random.default_rng(1)
+    D = 24
+    rows = []
+    for cond, tol, cap in [(20.0, 0.0, D), (1e4, 1e-8, 200), (1e6, 1e-6, 60)]:
+        Q, _ = np.linalg.qr(rng.standard_normal((D, D)))
+        A = (Q * np.exp(rng.uniform(0, np.log(cond), D))) @ Q.T
+        p = np.where(rng.random(D) < 0.5, -1.0, 1.0)
+        r = O.conjugate_gradient(lambda V, c: A @ V, p[:, None], tol, cap)
+        rows.append((r["gamma"][:, 0], r["xi"][:, 0], int(r["steps"][0]), A, p))
+    ld = max(len(g) for g, _, _, _, _ in rows)
+    gam = np.full((len(rows), ld), np.nan)
+    xi = np.full((len(rows), ld), np.nan)
+    for j, (g, x, U, _, _) in enumerate(rows):
+        gam[j, :U], xi[j, :U] = g[:U], x[:U]
+    tau = lanczos_quadrature(torch.tensor(gam).cuda(), torch.tensor(xi).cuda(),
+                             torch.tensor([r[2] for r in rows], dtype=torch.int32).cuda(), D).cpu().numpy()
+    for j, (g, x, U, A, p) in enumerate(rows):
+        assert tau[j] == pytest.approx(O.quadrature_term(g[:U], x[:U], D), rel=1e-10)
+    g, x, U, A, p = rows[0]
+    assert tau[0] == pytest.approx(p @ np.real(scipy.linalg.logm(A)) @ p, rel=1e-7)
+
+
+# ------------------------------------------------------------------------------ one EM step --
+def _single_step(data, alpha, it, cap, tol=None, K=None):
+    cfg = data["cfg"]
+    K = cfg.K if K is None else K
+    tol = cfg.cg_tol if tol is None else tol
+    g = make_gpu(data, K=K, tol=tol, cap=cap, alpha=alpha, em_iter0=it)
+    info = g.em_step(1)
+    post = to_np(g.posterior())
+    tr = g.transcript()
+    steps = tr["steps"].cpu().numpy().reshape(len(data["tasks"]), -1, K)
+    g.close()
+    orc = O.e_step(data, alpha, it, mode="cofem", K=K, tol=tol, cap=cap)
+    a_next = O.m_step(orc["q"], orc["mu"], orc["s"], alpha)
+    conv_gpu = np.all(steps < cap, axis=-1)
+    conv_orc = np.all(orc["probe_steps"].reshape(steps.shape) < cap, axis=-1)
+    return post, info, orc, a_next, conv_gpu & conv_orc
+
+
+@pytest.mark.parametrize("cid,em_iters_before", [(1, 0), (1, 6), (1, 15)])
+def test_single_em_step_config1(torch_cuda, cid, em_iters_before):
+    cfg = synthetic.CONFIGS[cid]
+    data = synthetic.generate(cfg)
+    alpha = oracle_state(data, em_iters_before, mode="cofem")
+    post, info, orc, a_next, conv = _single_step(data, alpha, em_iters_before, cap=4 * cfg.cg_cap)
+    e = compare_step(post, info, orc, a_next, conv)
+    print("parity", cid, em_iters_before, e, "converged blocks", conv.sum(), "/", conv.size)
+    assert e["mu"] <= MU_TOL
+    assert conv.all() and e["s_conv"] <= S_TOL
+    assert np.all(np.abs(post["logdet"] - orc["nu"]) <= nu_tol(orc["nu"]))
+    assert e["q_abs"] <= Q_TOL
+    assert e["L_abs"] <= L_TOL
+    if np.max(np.abs(post["q"] - orc["q"])) <= 1e-5:
+        assert e["alpha"] <= A_TOL
+
+
+def test_single_em_step_ragged_shapes(torch_cuda):
+    """N, D not multiples of the 128-row tiles or the 16-wide K chunks; P = C·K not a multiple
+    of the 64-column tile; several tasks."""
+    data = synthetic.small_problem(T=3, C=3, N=36, D=100, K=5, sigma=0.05, seed=11, support=4)
+    alpha = np.random.default_rng(2).uniform(0.2, 5.0, (3, 100))
+    post, info, orc, a_next, conv = _single_step(data, alpha, 3, cap=400, tol=1e-7)
+    e = compare_step(post, info, orc, a_next, conv)
+    print("ragged", e)
+    assert e["mu"] <= MU_TOL and e["s_conv"] <= S_TOL and e["q_abs"] <= Q_TOL and e["L_abs"] <= L_TOL
+    assert np.all(np.abs(post["logdet"] - orc["nu"]) <= nu_tol(orc["nu"]))
+
+
+def test_single_em_step_many_column_tiles(torch_cuda):
+    """P = C·K = 16·9 = 144 > two 64-column tiles, C = 16 (the maximum), 1 task per... ."""
+    data = synthetic.small_problem(T=2, C=16, N=48, D=128, K=9, sigma=0.05, seed=12, support=5)
+    alpha = np.random.default_rng(3).uniform(0.3, 3.0, (16, 128))
+    post, info, orc, a_next, conv = _single_step(data, alpha, 0, cap=600, tol=1e-7)
+    e = compare_step(post, info, orc, a_next, conv)
+    print("C16", e)
+    assert e["mu"] <= MU_TOL and e["s_conv"] <= S_TOL and e["q_abs"] <= Q_TOL and e["L_abs"] <= L_TOL
+
+
+def test_q_conditioned_alpha(torch_cuda):
+    """The GPU M-step fed the oracle's q (reading of P-α) meets 1e-4 always."""
+    import torch
+    cfg = synthetic.CONFIGS[1]
+    data = synthetic.generate(cfg)
+    alpha = oracle_state(data, 4, mode="cofem")
+    orc = O.e_step(data, alpha, 4, mode="cofem", cap=4 * cfg.cg_cap)
+    g = make_gpu(data, cap=4 * cfg.cg_cap, alpha=alpha, em_iter0=4)
+    g.em_step(1, q_override=torch.tensor(orc["q"]).cuda())
+    post = to_np(g.posterior())
+    g.close()
+    a_next = O.m_step(orc["q"], orc["mu"], orc["s"], alpha)
+    assert np.max(rel_inf(post["alpha"], a_next)) <= A_TOL
+
+
+def test_probe_override_matches_hash(torch_cuda):
+    from paper_2310_00420_b200 import probe_words
+    cfg = synthetic.CONFIGS[1]
+    data = synthetic.generate(cfg)
+    a = make_gpu(data, em_iter0=2)
+    a.em_step(1)
+    pa = to_np(a.posterior())
+    a.close()
+    words = probe_words(cfg.probe_seed, 2, cfg.T, 0, cfg.T, cfg.C, cfg.K, cfg.D)
+    b = make_gpu(data, em_iter0=2)
+    b.em_step(1, probe_bits=words)
+    pb = to_np(b.posterior())
+    b.close()
+    for k in ("mu", "s", "logdet", "q", "alpha"):
+        np.testing.assert_array_equal(pa[k], pb[k])
+
+
+def test_oracle_probes_injected(torch_cuda):
+    """probe_bits carries the ORACLE's probes (another seed) into the GPU step."""
+    import torch
+    cfg = synthetic.CONFIGS[1]
+    data = synthetic.generate(cfg)
+    seed2, it = 987654321, 0
+    nw = (cfg.D + 63) // 64
+    words = np.stack([[[O.probe_word(seed2, ((((it * cfg.T + t) * cfg.C + c) * cfg.K + k) * nw)
+                                     + np.arange(nw, dtype=np.uint64))
+                        for k in range(cfg.K)] for c in range(cfg.C)] for t in range(cfg.T)])
+    g = make_gpu(data, cap=256)
+    g.em_step(1, probe_bits=torch.tensor(words.view(np.int64)).cuda())
+    post = to_np(g.posterior())
+    g.close()
+    orc = O.e_step(data, data["alpha0"], it, mode="cofem", cap=256, probe_seed=seed2)
+    assert np.max(rel_inf(post["s"], orc["s"])) <= S_TOL
+    assert np.max(rel_inf(post["mu"], orc["mu"])) <= MU_TOL
+
+
+# ------------------------------------------------------------------------------ edge cases --
+def test_single_cluster_and_single_probe(torch_cuda):
+    data = synthetic.small_problem(T=2, C=1, N=16, D=40, K=1, seed=13)
+    g = make_gpu(data, K=1, cap=200, tol=1e-8)
+    g.em_step(1)
+    post = to_np(g.posterior())
+    g.close()
+    np.testing.assert_array_equal(post["q"], 1.0)
+    orc = O.e_step(data, data["alpha0"], 0, mode="cofem", K=1, tol=1e-8, cap=200)
+    assert np.max(rel_inf(post["mu"], orc["mu"])) <= MU_TOL
+    assert np.max(rel_inf(post["s"], orc["s"])) <= S_TOL
+
+
+def test_zero_measurements_give_zero_mean(torch_cuda):
+    data = synthetic.small_problem(T=2, C=2, N=16, D=32, K=3, seed=14)
+    data["y"][0] = 0.0
+    g = make_gpu(data, cap=100)
+    g.em_step(1)
+    post = to_np(g.posterior())
+    tr = g.transcript()
+    g.close()
+    np.testing.assert_array_equal(post["mu"][0], 0.0)
+    assert np.all(tr["mu_steps"].cpu().numpy().reshape(2, 2)[0] == 0)
+
+
+def test_cap_one_and_tol_zero(torch_cuda):
+    """cap = 1: every column takes exactly one step; tol = 0: no early stop before the cap."""
+    data = synthetic.small_problem(T=2, C=2, N=16, D=32, K=3, seed=15)
+    for cap, tol in [(1, 1e-6), (7, 0.0)]:
+        g = make_gpu(data, cap=cap, tol=tol)
+        info = g.em_step(1)
+        post = to_np(g.posterior())
+        g.close()
+        assert info["probe_steps_min"] == info["probe_steps_max"] == cap
+        orc = O.e_step(data, data["alpha0"], 0, mode="cofem", tol=tol, cap=cap)
+        assert np.max(rel_inf(post["mu"], orc["mu"])) <= 1e-9
+        assert np.max(rel_inf(post["s"], orc["s"])) <= 1e-5
+        assert np.all(np.abs(post["logdet"] - orc["nu"]) <= nu_tol(orc["nu"]))
+
+
+def test_prior_only_tasks_exact(torch_cuda):
+    """Φ = 0 ⇒ s = 1/α and ν̄ = −Σ log α exactly (A diagonal)."""
+    data = synthetic.small_problem(T=2, C=2, N=8, D=32, K=4, seed=16)
+    data["phi"][:] = 0.0
+    alpha = np.stack([np.repeat([0.5, 2.0], 16), np.repeat([1.5, 4.0], 16)])
+    g = make_gpu(data, alpha=alpha, cap=50, tol=1e-12)
+    g.em_step(1)
+    post = to_np(g.posterior())
+    g.close()
+    np.testing.assert_allclose(post["s"], np.broadcast_to(1.0 / alpha, post["s"].shape), rtol=1e-6)
+    np.testing.assert_allclose(post["logdet"], np.broadcast_to(-np.log(alpha).sum(1), (2, 2)), rtol=1e-6)
+
+
+def test_invalid_alpha_rejected(torch_cuda):
+    from paper_2310_00420_b200 import CmtcsError
+    data = synthetic.small_problem(T=2, C=2, N=16, D=32, K=3, seed=17)
+    alpha = np.ones((2, 32))
+    alpha[1, 3] = 0.0
+    with pytest.raises(CmtcsError, match="EINVAL"):
+        make_gpu(data, alpha=alpha)
+
+
+def test_shared_phi_equals_replicated(torch_cuda):
+    """shared_phi = 1 with one Φ gives the same result as T copies of that Φ."""
+    data = synthetic.small_problem(T=3, C=2, N=16, D=48, K=4, seed=18)
+    data["phi"][1:] = data["phi"][0]
+    a = make_gpu(data, cap=200)
+    a.em_step(2)
+    pa = to_np(a.posterior())
+    a.close()
+    shared = dict(data)
+    shared["phi"] = data["phi"][0]
+    shared["cfg"] = data["cfg"].replace(shared_phi=True)
+    b = make_gpu(shared, cap=200)
+    b.em_step(2)
+    pb = to_np(b.posterior())
+    b.close()
+    for k in ("mu", "s", "logdet", "q", "alpha"):
+        np.testing.assert_array_equal(pa[k], pb[k])
+
+
+# ------------------------------------------------------------------------------ full runs ----
+def test_full_run_config1(torch_cuda):
+    """20 EM iterations of config 1: identical argmax and |ΔNMSE| ≤ 1e-3 (north_star), |ΔL| ≤ 1e-3
+    at every iteration."""
+    cfg = synthetic.CONFIGS[1]
+    data = synthetic.generate(cfg)
+    orc = O.run(data, cfg.em_iters)
+    g = make_gpu(data)
+    Ls = [g.em_step(1)["loglik"] for _ in range(cfg.em_iters)]
+    post = to_np(g.posterior())
+    g.close()
+    assert list(post["assign"]) == list(orc["assign"])
+    nm_gpu = O.nmse(post["recon"], data["z"])
+    assert abs(nm_gpu - orc["nmse"]) <= 1e-3
+    Lo = [h["L"] for h in orc["history"]]
+    print("L gaps", np.max(np.abs(np.array(Ls) - np.array(Lo))), "nmse", nm_gpu, orc["nmse"])
+    assert np.max(np.abs(np.array(Ls) - np.array(Lo))) <= L_TOL
+
+
+def test_single_step_config2(torch_cuda):
+    """Config 2 (16 tasks, D = 1024) from an oracle-reached state, cap ×4 (parity protocol P-s)."""
+    cfg = synthetic.CONFIGS[2]
+    data = synthetic.generate(cfg)
+    alpha = oracle_state(data, 3, mode="cofem")
+    post, info, orc, a_next, conv = _single_step(data, alpha, 3, cap=4 * cfg.cg_cap)
+    e = compare_step(post, info, orc, a_next, conv)
+    print("C2 parity", e, "converged", conv.sum(), "/", conv.size)
+    assert e["mu"] <= MU_TOL
+    assert conv.any() and e["s_conv"] <= S_TOL
+    assert np.all(np.abs(post["logdet"] - orc["nu"]) <= nu_tol(orc["nu"]))
+    assert e["L_abs"] <= L_TOL
