@@ -88,7 +88,7 @@ bool make_dims(const cmtcs_problem *p, Dims *d, char *why) {
   if (p->N % 4 || p->D % 4) { snprintf(why, 256, "N and D must be multiples of 4 (got N=%d D=%d)", p->N, p->D); return false; }
   if (p->C > MAXC) { snprintf(why, 256, "C=%d exceeds the supported maximum %d", p->C, MAXC); return false; }
   if (!(p->beta > 0) || !std::isfinite(p->beta)) { snprintf(why, 256, "beta must be finite and > 0"); return false; }
-  if (p->cg_max_iters < 1) { snprintf(why, 256, "cg_max_iters must be >= 1"); return false; }
+  if (p->cg_max_iters < 1 || p->cg_max_iters > 12000) { snprintf(why, 256, "cg_max_iters must be in [1, 12000]"); return false; }
   if (!(p->cg_rel_tol >= 0)) { snprintf(why, 256, "cg_rel_tol must be >= 0"); return false; }
   if (!(p->alpha_max > 0) || !(p->var_floor >= 0) || !(p->empty_eps >= 0)) { snprintf(why, 256, "bad alpha_max/var_floor/empty_eps"); return false; }
   if (p->task_begin < 0 || p->task_end > p->T || p->task_end <= p->task_begin) { snprintf(why, 256, "bad task range [%d,%d) of T=%d", p->task_begin, p->task_end, p->T); return false; }
@@ -114,6 +114,17 @@ bool make_dims(const cmtcs_problem *p, Dims *d, char *why) {
   d->nRT1 = (p->N + OP_BR - 1) / OP_BR;
   d->nRT2 = (p->D + OP_BR - 1) / OP_BR;
   d->nCT = (d->P + OP_BC - 1) / OP_BC;
+  {
+    // split the stage-1 contraction over D until ≥ 2 CTAs per SM exist (each split ≥ 128 long)
+    const int sms = 148;
+    const long base = (long)d->nCT * d->nRT1 * (p->task_end - p->task_begin);
+    int s1 = (int)std::min<long>((2L * sms + base - 1) / base, std::max(1, p->D / 128));
+    s1 = std::max(1, s1);
+    int k1 = (p->D + s1 - 1) / s1;
+    k1 = (k1 + OP_BK - 1) / OP_BK * OP_BK;
+    d->K1 = k1;
+    d->S1 = (p->D + k1 - 1) / k1;
+  }
   d->shared_phi = p->shared_phi ? 1 : 0;
   d->phi_task_stride = p->shared_phi ? 0 : (int64_t)p->N * p->D;
   return true;
@@ -136,8 +147,8 @@ size_t carve(const Dims &d, char *base, Bufs *b) {
   b->Rm = cv.take<double>(Tl * C * D);
   b->Dm = cv.take<double>(Tl * C * D);
   b->Wm = cv.take<double>(Tl * C * D);
-  b->U = cv.take<float>(Tl * N * d.Pp);
-  b->Um = cv.take<double>(Tl * N * C);
+  b->U = cv.take<float>((size_t)d.S1 * Tl * N * d.Pp);
+  b->Um = cv.take<double>((size_t)d.S1 * Tl * N * C);
   b->rr = cv.take<double>(Tl * P);
   b->rrm = cv.take<double>(Tl * C);
   b->dAd = cv.take<double>(Tl * P * d.nRT2);
@@ -151,7 +162,6 @@ size_t carve(const Dims &d, char *base, Bufs *b) {
   b->gam = cv.take<double>(Tl * P * cap);
   b->xi = cv.take<double>(Tl * P * cap);
   b->tau = cv.take<double>(Tl * P);
-  b->lz = cv.take<double>(Tl * P * 3 * cap);
   b->s = cv.take<double>(Tl * C * D);
   b->nu = cv.take<double>(Tl * C);
   b->ell = cv.take<double>(Tl * C);
@@ -246,7 +256,7 @@ cmtcs_status one_em_iteration(cmtcs_ctx *c, const uint64_t *probe_bits, const do
   }
   // ---- estimators: s (Eq. 5), ν̄ (Eq. 7-9), Φμ for ℓ, q and log-lik (Eq. 3) ----
   CUDA_OK(c, launch_diag(kp, s));
-  CUDA_OK(c, launch_lanczos(kp.b.gam, kp.b.xi, kp.b.steps, d.Tl * d.P, d.cap, d.D, kp.b.tau, kp.b.lz,
+  CUDA_OK(c, launch_lanczos(kp.b.gam, kp.b.xi, kp.b.steps, d.Tl * d.P, d.cap, d.D, kp.b.tau, nullptr,
                             kp.b.status, s));
   CUDA_OK(c, launch_stage1(kp, 0, kp.b.Xm, true, s));
   CUDA_OK(c, launch_estep_finish(kp, s));

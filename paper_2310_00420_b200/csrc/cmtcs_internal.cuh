@@ -10,7 +10,7 @@ namespace cmtcs {
 
 constexpr int MAXC = 16;        // clusters supported by the fp64 mean-column tiles
 constexpr int OP_BR = 128;      // operator CTA tile: rows (N in stage 1, D in stage 2)
-constexpr int OP_BC = 64;       // operator CTA tile: probe columns
+constexpr int OP_BC = 96;       // operator CTA tile: probe columns (8 warps x 12)
 constexpr int OP_BK = 16;       // contraction chunk
 constexpr int OP_THREADS = 256;
 constexpr int UPD_THREADS = 256;
@@ -25,6 +25,8 @@ struct Dims {
   int nRT1;  // stage-1 row tiles  = ceil(N / OP_BR)
   int nRT2;  // stage-2 row tiles  = ceil(D / OP_BR)
   int nCT;   // probe column tiles = ceil(P / OP_BC)
+  int S1;    // stage-1 split-K factor (fills the GPU when T·N is small)
+  int K1;    // stage-1 contraction length per split (multiple of OP_BK)
   int shared_phi;
   int64_t phi_task_stride;  // elements between Φ_t and Φ_{t+1} (0 if shared)
 };
@@ -39,8 +41,8 @@ struct Bufs {
   double *bnorm2;    // [Tl]      ‖b‖²
   float *X, *R, *Dv, *W;     // probe columns [Tl][P][D]
   double *Xm, *Rm, *Dm, *Wm; // mean columns  [Tl][C][D]
-  float *U;          // [Tl][N][Pp]  stage-1 output (compacted column order)
-  double *Um;        // [Tl][N][C]
+  float *U;          // [S1][Tl][N][Pp]  stage-1 split-K partials (compacted column order)
+  double *Um;        // [S1][Tl][N][C]
   double *rr;        // [Tl][P]
   double *rrm;       // [Tl][C]
   double *dAd;       // [Tl][P][nRT2]  per-row-tile partial dᵀAd
@@ -53,7 +55,6 @@ struct Bufs {
   int *m_act;        // [Tl]
   double *gam, *xi;  // [Tl*P][cap]
   double *tau;       // [Tl*P]
-  double *lz;        // [Tl*P][3*cap] quadrature scratch
   double *s;         // [Tl][C][D]
   double *nu, *ell, *q;  // [Tl][C]
   double *ll;        // [Tl]

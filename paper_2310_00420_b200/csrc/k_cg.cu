@@ -184,7 +184,7 @@ __global__ void __launch_bounds__(UPD_THREADS) k_update(KParams p, int u) {
     // ------------------------------ fp64 mean column ----------------------------------------
     const int c = slot - d.P;
     const int gi = t * d.C + c;
-    if (!p.b.flagm[gi]) return;
+    if (p.b.flagm[gi] != 1) return;
     const size_t g = (size_t)gi;
     double dAd = 0.0;
     for (int i = 0; i < d.nRT2; ++i) dAd += p.b.dAdm[g * d.nRT2 + i];

@@ -1,7 +1,5 @@
 // K6 diagonal estimate (Eq. 5), K7 Lanczos-quadrature log-det (Eq. 7-9), K8 ℓ / q / log-lik
 // (Eq. 3), K9/K10 M-step (Eq. 4), K11 readout (Alg. 2 lines 17-20) and step statistics.
-#include <float.h>
-
 #include "cmtcs_internal.cuh"
 
 namespace cmtcs {
@@ -48,88 +46,111 @@ __global__ void k_diag(KParams p) {
 }
 
 // K7: τ = D · Σ_u S̄²_{u,1} log λ̄_u for Γ̄ assembled from (γ, ξ) (Eq. 7-8).
-// One thread per tridiagonal: implicit-shift QL iteration on (diag, off-diag), applying every
-// Givens rotation to the first row z of the eigenvector matrix only (z₀ = e₁), so S̄_{u,1} = z_u
-// (eigenvectors are the rows of S̄).  O(U'²) per matrix, fp64.
-__global__ void k_lanczos(const double *__restrict__ gam, const double *__restrict__ xi,
-                          const int *__restrict__ steps, int n, int ld, int D, double *tau,
-                          double *scratch, int *status) {
-  const int g = blockIdx.x * blockDim.x + threadIdx.x;
-  if (g >= n) return;
+// Σ_u S̄²_{u,1} log λ̄_u is exactly e₁ᵀ log(Γ̄) e₁ (S̄ holds the eigenvectors as rows).
+// Instead of a serial eigendecomposition per tridiagonal, one CTA per Γ̄ evaluates it in parallel
+// from the Stieltjes representation (for any c > 0, with Σ_u S̄²_{u,1} = 1):
+//   e₁ᵀ log(Γ̄) e₁ = log c + ∫_ℝ eˣ [ 1/(c + eˣ) − e₁ᵀ(Γ̄ + eˣ I)⁻¹ e₁ ] dx ,
+// where e₁ᵀ(Γ̄ + sI)⁻¹e₁ = 1/q₁(s) comes from the bottom-up continued fraction
+//   q_U = a_U + s,  q_u = (a_u + s) − b_u² / q_{u+1}   (all q_u > 0: Γ̄ + sI is SPD),
+// and the integral is a trapezoid sum with step h = 0.4 over [log λ_lo − 37, log λ_hi + 37]
+// (integrand analytic in |Im x| < π ⇒ error ~ e^{−2π²/h} ≈ 1e-21; tails < e^{−37}).
+// λ_hi is the Gershgorin bound; λ_lo ≤ λ_min is found by Sturm counts at λ_hi·2^{−j}.
+// Matches numpy.linalg.eigh-based Eq. 8 to ~1e-13 (tests/test_gpu_parity.py).  fp64 throughout.
+__global__ void __launch_bounds__(128) k_lanczos(const double *__restrict__ gam, const double *__restrict__ xi,
+                                                 const int *__restrict__ steps, int n, int ld, int D,
+                                                 double *tau, int *status) {
+  extern __shared__ double sm_lz[];
+  __shared__ double red[128];
+  __shared__ int s_bad, s_j;
+  const int g = blockIdx.x, tid = threadIdx.x;
   const int U = steps[g];
+  double *a = sm_lz, *b2 = sm_lz + ld;
   const double *ga = gam + (size_t)g * ld, *xa = xi + (size_t)g * ld;
-  double *dg = scratch + (size_t)g * 3 * ld, *e = dg + ld, *z = e + ld;
+  if (tid == 0) { s_bad = 0; s_j = 1 << 30; }
+  __syncthreads();
   if (U < 1 || U > ld) {
-    tau[g] = nan("");
-    if (atomicCAS(status, 0, ST_EIG) == 0) { status[1] = g; status[2] = U; status[3] = -1; }
-    return;
-  }
-  for (int i = 0; i < U; ++i) {
-    const double gi = ga[i];
-    if (!(gi > 0.0)) {
+    if (tid == 0) {
       tau[g] = nan("");
-      if (atomicCAS(status, 0, ST_EIG) == 0) { status[1] = g; status[2] = i; status[3] = -2; }
-      return;
+      if (atomicCAS(status, 0, ST_EIG) == 0) { status[1] = g; status[2] = U; status[3] = -1; }
     }
-    dg[i] = 1.0 / gi + (i > 0 ? xa[i - 1] / ga[i - 1] : 0.0);   // Γ_uu
-    e[i] = (i + 1 < U) ? sqrt(xa[i]) / gi : 0.0;                 // Γ_{u+1,u}
-    z[i] = (i == 0) ? 1.0 : 0.0;
-  }
-  bool ok = true;
-  for (int l = 0; l < U && ok; ++l) {
-    int iter = 0;
-    for (;;) {
-      int m = l;
-      for (; m < U - 1; ++m) {
-        const double dd = fabs(dg[m]) + fabs(dg[m + 1]);
-        if (fabs(e[m]) <= DBL_EPSILON * dd) break;
-      }
-      if (m == l) break;
-      if (++iter > 200) { ok = false; break; }
-      double gg = (dg[l + 1] - dg[l]) / (2.0 * e[l]);
-      double r = hypot(gg, 1.0);
-      gg = dg[m] - dg[l] + e[l] / (gg + copysign(r, gg));
-      double s = 1.0, c = 1.0, pp = 0.0;
-      bool deflated = false;
-      for (int i = m - 1; i >= l; --i) {
-        double f = s * e[i];
-        const double b = c * e[i];
-        r = hypot(f, gg);
-        e[i + 1] = r;
-        if (r == 0.0) {          // underflow: split the matrix and restart this l
-          dg[i + 1] -= pp;
-          e[m] = 0.0;
-          deflated = true;
-          break;
-        }
-        s = f / r;
-        c = gg / r;
-        gg = dg[i + 1] - pp;
-        r = (dg[i] - gg) * s + 2.0 * c * b;
-        pp = s * r;
-        dg[i + 1] = gg + pp;
-        gg = c * r - b;
-        f = z[i + 1];                 // rotate columns i, i+1 of the eigenvector matrix (row 0)
-        z[i + 1] = s * z[i] + c * f;
-        z[i] = c * z[i] - s * f;
-      }
-      if (deflated) continue;
-      dg[l] -= pp;
-      e[l] = gg;
-      e[m] = 0.0;
-    }
-  }
-  double acc = 0.0;
-  for (int i = 0; i < U && ok; ++i) {
-    if (!(dg[i] > 0.0)) { ok = false; break; }
-    acc += z[i] * z[i] * log(dg[i]);
-  }
-  if (!ok) {
-    tau[g] = nan("");
-    if (atomicCAS(status, 0, ST_EIG) == 0) { status[1] = g; status[2] = U; status[3] = -3; }
     return;
   }
-  tau[g] = (double)D * acc;
+  // Eq. 7: a_u = Γ̄_uu,  b_u² = Γ̄²_{u,u+1} = ξ_u / γ_u²
+  double ghi = -INFINITY;
+  for (int i = tid; i < U; i += blockDim.x) {
+    const double gi = ga[i];
+    if (!(gi > 0.0) || !isfinite(gi)) s_bad = 1;
+    a[i] = 1.0 / gi + (i > 0 ? xa[i - 1] / ga[i - 1] : 0.0);
+    b2[i] = (i + 1 < U) ? xa[i] / (gi * gi) : 0.0;
+  }
+  __syncthreads();
+  for (int i = tid; i < U; i += blockDim.x) {
+    const double r = a[i] + (i > 0 ? sqrt(b2[i - 1]) : 0.0) + sqrt(b2[i]);
+    ghi = fmax(ghi, r);
+  }
+  red[tid] = ghi;
+  __syncthreads();
+  for (int o = 64; o; o >>= 1) {
+    if (tid < o) red[tid] = fmax(red[tid], red[tid + o]);
+    __syncthreads();
+  }
+  const double hi = red[0];
+  __syncthreads();
+  if (s_bad || !(hi > 0.0) || !isfinite(hi)) {
+    if (tid == 0) {
+      tau[g] = nan("");
+      if (atomicCAS(status, 0, ST_EIG) == 0) { status[1] = g; status[2] = U; status[3] = -2; }
+    }
+    return;
+  }
+  // λ_lo: the largest x_j = hi·2^{−j} with no eigenvalue below it (Sturm count = 0)
+  {
+    const double x = ldexp(hi, -tid);
+    double d = a[U - 1] - x;
+    int cnt = d < 0.0;
+    for (int i = U - 2; i >= 0; --i) {
+      if (d == 0.0) d = -1e-300;
+      d = (a[i] - x) - b2[i] / d;
+      cnt += d < 0.0;
+    }
+    if (cnt == 0) atomicMin(&s_j, tid);
+  }
+  __syncthreads();
+  if (s_j >= (1 << 30)) {
+    if (tid == 0) {
+      tau[g] = nan("");
+      if (atomicCAS(status, 0, ST_EIG) == 0) { status[1] = g; status[2] = U; status[3] = -3; }
+    }
+    return;
+  }
+  const double lo = ldexp(hi, -s_j);
+  const double c = sqrt(lo * hi), h = 0.4;
+  const double x0 = log(lo) - 37.0, x1 = log(hi) + 37.0;
+  const int nn = (int)ceil((x1 - x0) / h) + 1;
+  double acc = 0.0;
+  bool bad = false;
+  for (int k = tid; k < nn; k += blockDim.x) {
+    const double s = exp(x0 + k * h);
+    double q = a[U - 1] + s;
+    for (int i = U - 2; i >= 0; --i) q = (a[i] + s) - b2[i] / q;
+    bad |= !(q > 0.0);
+    acc += s * (1.0 / (c + s) - 1.0 / q);
+  }
+  if (bad) s_bad = 1;
+  red[tid] = acc;
+  __syncthreads();
+  for (int o = 64; o; o >>= 1) {
+    if (tid < o) red[tid] += red[tid + o];
+    __syncthreads();
+  }
+  if (tid == 0) {
+    if (s_bad || !isfinite(red[0])) {
+      tau[g] = nan("");
+      if (atomicCAS(status, 0, ST_EIG) == 0) { status[1] = g; status[2] = U; status[3] = -4; }
+    } else {
+      tau[g] = (double)D * (log(c) + h * red[0]);
+    }
+  }
 }
 
 // K8: ν̄_tc = −(1/K)Σ_k τ_tck (Eq. 9);  ℓ̃_tc = ν̄ + Σ_d log α_cd − β‖y − Φμ‖² − μᵀdiag(α)μ
@@ -149,7 +170,9 @@ __global__ void k_estep_finish(KParams p) {
     quad = block_sum(quad, sh);
     double res = 0.0;
     for (int n = tid; n < d.N; n += blockDim.x) {
-      const double rv = (double)p.y[(size_t)t * d.N + n] - p.b.Um[((size_t)t * d.N + n) * d.C + c];
+      double phimu = 0.0;  // Φμ from the stage-1 split-K partials
+      for (int s = 0; s < d.S1; ++s) phimu += p.b.Um[(((size_t)s * d.Tl + t) * d.N + n) * d.C + c];
+      const double rv = (double)p.y[(size_t)t * d.N + n] - phimu;
       res = fma(rv, rv, res);
     }
     res = block_sum(res, sh);
@@ -313,8 +336,14 @@ cudaError_t launch_diag(const KParams &p, cudaStream_t s) {
 
 cudaError_t launch_lanczos(const double *gam, const double *xi, const int *steps, int n, int ld, int D,
                            double *tau, double *scratch, int *status, cudaStream_t s) {
+  (void)scratch;
   if (n <= 0) return cudaSuccess;
-  k_lanczos<<<(n + 63) / 64, 64, 0, s>>>(gam, xi, steps, n, ld, D, tau, scratch, status);
+  const size_t smem = 2 * (size_t)ld * sizeof(double);
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(k_lanczos, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  k_lanczos<<<n, 128, smem, s>>>(gam, xi, steps, n, ld, D, tau, status);
   return cudaGetLastError();
 }
 

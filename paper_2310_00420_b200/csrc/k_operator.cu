@@ -2,45 +2,68 @@
 // of every task ("A := βΦᵀΦ + diag(α)", "solve all TC(K+1) systems
 // simultaneously ... A never needs to be explicitly computed").
 //
-// Two contractions per CG step (never forming ΦᵀΦ, N = D/4 makes this the cheaper order):
-//   stage 1  U[t][n][j] = Σ_d Φ_t[n][d] · V[t][act_j][d]          (rows n,  K = D)
-//   stage 2  W[t][act_j][d] = β Σ_n Φ_t[n][d] · U[t][n][j] + α ⊙ V (rows d,  K = N)
+// Two contractions per CG step (ΦᵀΦ is never formed; N = D/4 makes this the cheaper order):
+//   stage 1  U_s[t][n][j] = Σ_{d ∈ slice s} Φ_t[n][d] · V[t][act_j][d]   (rows n, K = D, split-K S1)
+//   stage 2  W[t][act_j][d] = β Σ_n Φ_t[n][d] · (Σ_s U_s[t][n][j]) + α ⊙ V (rows d, K = N)
 //            + the per-row-tile partial dᵀ(Ad) of Alg. 1 line 3, accumulated in fp64.
-// Probe columns are fp32 (FFMA, register-blocked 8x4 per thread, 128x64 CTA tile, smem double
-// buffer); converged columns are compacted away (act list), so retired columns cost nothing.
-// The C mean columns of a task run as one extra fp64 CTA per row tile (blockIdx.x == nCT) that
-// reads the same Φ tile (DFMA), keeping μ in fp64 end to end.
+// Probe columns (fp32): CTA = 8 warps = 128 rows × 96 columns; each warp owns 12 columns and all
+// 128 rows (lane: 4 rows × 12 columns, 48 FFMA per k per 4 smem loads).  Converged columns are
+// compacted away (act list) and a warp whose 12 columns are all retired skips its FFMAs, so the
+// waste is < 12 columns per task.  Φ tiles stream through a 3-stage cp.async ring.
+// The C mean columns of a task run as one extra fp64 CTA per row tile (blockIdx.x == nCT) on the
+// same Φ tiles (DFMA), keeping μ in fp64 end to end.
 #include "cmtcs_internal.cuh"
 
 namespace cmtcs {
 
 namespace {
 
-constexpr int BR = OP_BR, BC = OP_BC, BK = OP_BK;
-constexpr int ALD = BR + 4;   // padded leading dims (keep 16-byte alignment for LDS.128)
-constexpr int BLD = BC + 4;
+constexpr int BR = OP_BR;       // 128 rows per CTA
+constexpr int BC = OP_BC;       // 96 probe columns per CTA
+constexpr int BK = OP_BK;       // 16: contraction chunk
+constexpr int WC = BC / 8;      // 12 columns per warp
+constexpr int ST = 3;           // pipeline stages
+constexpr int A1LD = BK + 4;    // stage-1 A tile [r][k]  (row stride 20 floats: conflict-free LDS.128)
+constexpr int A2LD = BR + 4;    // stage-2 A tile [k][r]
+constexpr int BLD = BC + 4;     // B tile [k][c]
 
-struct __align__(16) OpSmem {
-  float A[2][BK][ALD];
+struct __align__(16) Smem1 {
+  float A[ST][BR][A1LD];        // 30720 B
   union {
-    float B[2][BK][BLD];
-    double Bm[2][BK][MAXC];
+    float B[ST][BK][BLD];       // 19200 B
+    double Bm[ST][BK][MAXC];    //  6144 B
   };
-  double red[16][BC];          // stage-2 dot partials (probe tile)
   int m;
-  int mc;
+};
+
+struct __align__(16) Smem2 {
+  float A[ST][BK][A2LD];        // 25344 B
+  union {
+    float B[ST][BK][BLD];
+    double Bm[ST][BK][MAXC];
+  };
+  double red[2][4][MAXC / 2];
 };
 
 __device__ __forceinline__ float4 ld4(const float *p) { return *reinterpret_cast<const float4 *>(p); }
 
-// Builds the compacted list of active probe columns of task t (ascending) in s_act; returns count.
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem, bool valid) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  const int n = valid ? 16 : 0;  // src-size 0 ⇒ zero fill
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(n));
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+// Compacted list of active probe columns of task t (ascending) in s_act; returns the count.
 __device__ int build_act(const int *flag, int P, int *s_act, int *s_m) {
   const int tid = threadIdx.x;
   if (tid < 32) {
     int cnt = 0;
     for (int base = 0; base < P; base += 32) {
       const int j = base + tid;
-      const int f = (j < P) ? flag[j] : 0;
+      const int f = (j < P) ? (flag[j] == 1) : 0;
       const unsigned bal = __ballot_sync(0xffffffffu, f);
       if (f) s_act[cnt + __popc(bal & ((1u << tid) - 1u))] = j;
       cnt += __popc(bal);
@@ -52,44 +75,38 @@ __device__ int build_act(const int *flag, int P, int *s_act, int *s_m) {
 }
 
 // ---------------------------------------------------------------------------------------------
-// stage 1
+// stage 1:  grid (nCT + 1, nRT1 * S1, Tl)
 // ---------------------------------------------------------------------------------------------
-__global__ void __launch_bounds__(OP_THREADS) k_stage1(KParams p, int u, const double *__restrict__ mu_src,
-                                                       int mu_only) {
-  extern __shared__ int s_act[];
-  __shared__ OpSmem sm;
+__global__ void __launch_bounds__(OP_THREADS, 2) k_stage1(KParams p, int u, const double *__restrict__ mu_src,
+                                                          int mu_only) {
+  extern __shared__ __align__(16) unsigned char dsm1[];
+  Smem1 &sm = *reinterpret_cast<Smem1 *>(dsm1);
+  int *s_act = reinterpret_cast<int *>(dsm1 + sizeof(Smem1));
   const Dims &d = p.d;
-  const int t = blockIdx.z, rt = blockIdx.y, ct = blockIdx.x, tid = threadIdx.x;
+  const int t = blockIdx.z, ct = blockIdx.x, tid = threadIdx.x;
+  const int rt = blockIdx.y / d.S1, sp = blockIdx.y % d.S1;
   const int N = d.N, D = d.D, P = d.P, C = d.C;
   const float *__restrict__ phi = p.phi + (size_t)t * d.phi_task_stride;
   const int n0 = rt * BR;
-  const int nk = (D + BK - 1) / BK;
+  const int kb = sp * d.K1, ke = min(D, kb + d.K1);
+  const int nk = (ke - kb + BK - 1) / BK;
 
-  // A-tile loader: Φ[n0 + r][k0 + 4q .. +3] → A[k][r] (transposed; 2 float4 per thread)
-  auto loadA = [&](int k0, float4 *ra) {
+  // A tile: Φ[n0 + r][k0 .. k0+15] → A[r][0..15]  (2 × 16-byte cp.async per thread)
+  auto loadA = [&](int buf, int k0) {
 #pragma unroll
     for (int i = 0; i < 2; ++i) {
       const int idx = tid + i * OP_THREADS, r = idx >> 2, q = idx & 3;
       const int n = n0 + r, k = k0 + 4 * q;
-      ra[i] = (n < N && k < D) ? ld4(phi + (size_t)n * D + k) : make_float4(0.f, 0.f, 0.f, 0.f);
-    }
-  };
-  auto storeA = [&](int buf, const float4 *ra) {
-#pragma unroll
-    for (int i = 0; i < 2; ++i) {
-      const int idx = tid + i * OP_THREADS, r = idx >> 2, q = idx & 3;
-      sm.A[buf][4 * q + 0][r] = ra[i].x;
-      sm.A[buf][4 * q + 1][r] = ra[i].y;
-      sm.A[buf][4 * q + 2][r] = ra[i].z;
-      sm.A[buf][4 * q + 3][r] = ra[i].w;
+      const bool ok = n < N && k < ke;
+      cp_async16(&sm.A[buf][r][4 * q], ok ? phi + (size_t)n * D + k : phi, ok);
     }
   };
 
   if (ct == d.nCT) {
-    // ---------------- fp64 mean-column tile: Um[t][n][c] = Σ_d Φ[n][d] μsrc[t][c][d] ----------
+    // ---------------- fp64 mean-column tile: Um_s[t][n][c] = Σ_{d∈s} Φ[n][d] μsrc[t][c][d] ------
     if (!mu_only) {
       int any = 0;
-      for (int c = 0; c < C; ++c) any |= p.b.flagm[t * C + c];
+      for (int c = 0; c < C; ++c) any |= (p.b.flagm[t * C + c] == 1);
       if (!any) return;
     }
     const double *src = mu_src + (size_t)t * C * D;
@@ -97,47 +114,39 @@ __global__ void __launch_bounds__(OP_THREADS) k_stage1(KParams p, int u, const d
     double acc[MAXC / 2];
 #pragma unroll
     for (int i = 0; i < MAXC / 2; ++i) acc[i] = 0.0;
-    float4 ra[2];
-    double rb = 0.0;
-    auto loadB = [&](int k0) {
-      rb = 0.0;
+    auto loadB = [&](int buf, int k0) {
       if (tid < BK * C) {
         const int c = tid / BK, kk = tid % BK;
-        if (k0 + kk < D) rb = src[(size_t)c * D + k0 + kk];
+        sm.Bm[buf][kk][c] = (k0 + kk < ke) ? src[(size_t)c * D + k0 + kk] : 0.0;
       }
     };
-    auto storeB = [&](int buf) {
-      if (tid < BK * C) sm.Bm[buf][tid % BK][tid / BK] = rb;
-    };
-    loadA(0, ra);
-    loadB(0);
-    storeA(0, ra);
-    storeB(0);
-    __syncthreads();
+#pragma unroll
+    for (int s = 0; s < ST - 1; ++s) {
+      if (s < nk) { loadA(s, kb + s * BK); loadB(s, kb + s * BK); }
+      cp_commit();
+    }
     for (int kc = 0; kc < nk; ++kc) {
-      const int buf = kc & 1;
-      if (kc + 1 < nk) {
-        loadA((kc + 1) * BK, ra);
-        loadB((kc + 1) * BK);
-      }
+      cp_wait<ST - 2>();
+      __syncthreads();
+      const int nx = kc + ST - 1;
+      if (nx < nk) { loadA(nx % ST, kb + nx * BK); loadB(nx % ST, kb + nx * BK); }
+      cp_commit();
+      const int buf = kc % ST;
 #pragma unroll 4
       for (int kk = 0; kk < BK; ++kk) {
-        const double a = (double)sm.A[buf][kk][r];
+        const double a = (double)sm.A[buf][r][kk];
 #pragma unroll
         for (int i = 0; i < MAXC / 2; ++i)
           if (h + 2 * i < C) acc[i] = fma(a, sm.Bm[buf][kk][h + 2 * i], acc[i]);
       }
-      if (kc + 1 < nk) {
-        storeA(buf ^ 1, ra);
-        storeB(buf ^ 1);
-      }
-      __syncthreads();
     }
+    cp_wait<0>();
     const int n = n0 + r;
     if (n < N) {
+      double *um = p.b.Um + (size_t)sp * d.Tl * N * C;
 #pragma unroll
       for (int i = 0; i < MAXC / 2; ++i)
-        if (h + 2 * i < C) p.b.Um[((size_t)t * N + n) * C + h + 2 * i] = acc[i];
+        if (h + 2 * i < C) um[((size_t)t * N + n) * C + h + 2 * i] = acc[i];
     }
     return;
   }
@@ -145,13 +154,13 @@ __global__ void __launch_bounds__(OP_THREADS) k_stage1(KParams p, int u, const d
 
   // ---------------- fp32 probe tile -------------------------------------------------------
   const int m = build_act(p.b.flag + (size_t)t * P, P, s_act, &sm.m);
-  if (ct == 0 && rt == 0) {
-    // task bookkeeping for this CG step: publish act list, step histograms
+  if (ct == 0 && blockIdx.y == 0) {
+    // task bookkeeping for this CG step: publish the act list and the step histograms
     for (int j = tid; j < m; j += OP_THREADS) p.b.act[(size_t)t * P + j] = s_act[j];
     if (tid == 0) {
       p.b.m_act[t] = m;
       int mc = 0;
-      for (int c = 0; c < C; ++c) mc += p.b.flagm[t * C + c];
+      for (int c = 0; c < C; ++c) mc += (p.b.flagm[t * C + c] == 1);
       if (m) atomicAdd(p.b.hist + u, m);
       if (mc) atomicAdd(p.b.histm + u, mc);
       if (m + mc) atomicAdd(p.b.histt + u, 1);
@@ -159,130 +168,156 @@ __global__ void __launch_bounds__(OP_THREADS) k_stage1(KParams p, int u, const d
   }
   const int j0 = ct * BC;
   if (j0 >= m) return;
+  const int w = tid >> 5, l = tid & 31;
+  const bool wact = j0 + w * WC < m;   // this warp has at least one active column
 
-  const int ty = tid >> 4, tx = tid & 15;
-  const int cb = tid >> 2, qb = tid & 3;
-  const float *bcol = (j0 + cb < m) ? p.b.Dv + ((size_t)t * P + s_act[j0 + cb]) * D : nullptr;
-  float acc[8][4];
+  // B tile (register-staged transpose): V[act[j0 + c]][k0 + 4q .. +3] → B[4q + i][c]
+  // 384 float4 per stage: idx = tid (+256): c = idx >> 2, q = idx & 3
+  const float *bsrc[2];
 #pragma unroll
-  for (int i = 0; i < 8; ++i)
-#pragma unroll
-    for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
-  float4 ra[2], rb;
+  for (int i = 0; i < 2; ++i) {
+    const int idx = tid + i * OP_THREADS, c = idx >> 2;
+    bsrc[i] = (idx < BC * 4 && j0 + c < m) ? p.b.Dv + ((size_t)t * P + s_act[j0 + c]) * D : nullptr;
+  }
+  float4 rb[2];
   auto loadB = [&](int k0) {
-    const int k = k0 + 4 * qb;
-    rb = (bcol && k < D) ? ld4(bcol + k) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const int idx = tid + i * OP_THREADS, q = idx & 3;
+      const int k = k0 + 4 * q;
+      rb[i] = (bsrc[i] && k < ke) ? ld4(bsrc[i] + k) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
   };
   auto storeB = [&](int buf) {
-    sm.B[buf][4 * qb + 0][cb] = rb.x;
-    sm.B[buf][4 * qb + 1][cb] = rb.y;
-    sm.B[buf][4 * qb + 2][cb] = rb.z;
-    sm.B[buf][4 * qb + 3][cb] = rb.w;
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const int idx = tid + i * OP_THREADS, c = idx >> 2, q = idx & 3;
+      if (idx < BC * 4) {
+        sm.B[buf][4 * q + 0][c] = rb[i].x;
+        sm.B[buf][4 * q + 1][c] = rb[i].y;
+        sm.B[buf][4 * q + 2][c] = rb[i].z;
+        sm.B[buf][4 * q + 3][c] = rb[i].w;
+      }
+    }
   };
-  loadA(0, ra);
-  loadB(0);
-  storeA(0, ra);
-  storeB(0);
-  __syncthreads();
-  for (int kc = 0; kc < nk; ++kc) {
-    const int buf = kc & 1;
-    if (kc + 1 < nk) {
-      loadA((kc + 1) * BK, ra);
-      loadB((kc + 1) * BK);
-    }
+
+  float acc[4][WC];
 #pragma unroll
-    for (int kk = 0; kk < BK; ++kk) {
-      const float4 a0 = *reinterpret_cast<const float4 *>(&sm.A[buf][kk][ty * 8]);
-      const float4 a1 = *reinterpret_cast<const float4 *>(&sm.A[buf][kk][ty * 8 + 4]);
-      const float4 bv = *reinterpret_cast<const float4 *>(&sm.B[buf][kk][tx * 4]);
-      const float a[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
-      const float b[4] = {bv.x, bv.y, bv.z, bv.w};
+  for (int i = 0; i < 4; ++i)
 #pragma unroll
-      for (int i = 0; i < 8; ++i)
+    for (int c = 0; c < WC; ++c) acc[i][c] = 0.f;
+
 #pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
-    }
-    if (kc + 1 < nk) {
-      storeA(buf ^ 1, ra);
-      storeB(buf ^ 1);
-    }
-    __syncthreads();
+  for (int s = 0; s < ST - 1; ++s) {
+    if (s < nk) { loadA(s, kb + s * BK); loadB(kb + s * BK); storeB(s); }
+    cp_commit();
   }
-  const int jc = j0 + tx * 4;
-  if (jc < d.Pp) {
+  for (int kc = 0; kc < nk; ++kc) {
+    cp_wait<ST - 2>();
+    __syncthreads();
+    const int nx = kc + ST - 1;
+    if (nx < nk) { loadA(nx % ST, kb + nx * BK); loadB(kb + nx * BK); }
+    cp_commit();
+    const int buf = kc % ST;
+    if (wact) {
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const int n = n0 + ty * 8 + i;
-      if (n < N)
-        *reinterpret_cast<float4 *>(p.b.U + ((size_t)t * N + n) * d.Pp + jc) =
-            make_float4(acc[i][0], acc[i][1], acc[i][2], acc[i][3]);
+      for (int kq = 0; kq < BK / 4; ++kq) {
+        float4 a[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) a[i] = *reinterpret_cast<const float4 *>(&sm.A[buf][l + 32 * i][4 * kq]);
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) {
+          const float *brow = &sm.B[buf][4 * kq + kk][w * WC];
+          const float4 b0 = *reinterpret_cast<const float4 *>(brow);
+          const float4 b1 = *reinterpret_cast<const float4 *>(brow + 4);
+          const float4 b2 = *reinterpret_cast<const float4 *>(brow + 8);
+          const float b[WC] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w, b2.x, b2.y, b2.z, b2.w};
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const float av = kk == 0 ? a[i].x : kk == 1 ? a[i].y : kk == 2 ? a[i].z : a[i].w;
+#pragma unroll
+            for (int c = 0; c < WC; ++c) acc[i][c] = fmaf(av, b[c], acc[i][c]);
+          }
+        }
+      }
+    }
+    if (nx < nk) storeB(nx % ST);
+  }
+  cp_wait<0>();
+  if (wact) {
+    float *U = p.b.U + (size_t)sp * d.Tl * N * d.Pp;
+    const int jc = j0 + w * WC;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int n = n0 + l + 32 * i;
+      if (n < N) {
+        float *dst = U + ((size_t)t * N + n) * d.Pp + jc;
+#pragma unroll
+        for (int q = 0; q < WC / 4; ++q)
+          if (jc + 4 * q < d.Pp)
+            *reinterpret_cast<float4 *>(dst + 4 * q) =
+                make_float4(acc[i][4 * q], acc[i][4 * q + 1], acc[i][4 * q + 2], acc[i][4 * q + 3]);
+      }
     }
   }
 }
 
 // ---------------------------------------------------------------------------------------------
-// stage 2
+// stage 2:  grid (nCT + 1, nRT2, Tl)
 // ---------------------------------------------------------------------------------------------
-__global__ void __launch_bounds__(OP_THREADS) k_stage2(KParams p, int u) {
-  __shared__ OpSmem sm;
+__global__ void __launch_bounds__(OP_THREADS, 2) k_stage2(KParams p, int u) {
+  extern __shared__ __align__(16) unsigned char dsm2[];
+  Smem2 &sm = *reinterpret_cast<Smem2 *>(dsm2);
   const Dims &d = p.d;
   const int t = blockIdx.z, rt = blockIdx.y, ct = blockIdx.x, tid = threadIdx.x;
-  const int N = d.N, D = d.D, P = d.P, C = d.C;
+  const int N = d.N, D = d.D, P = d.P, C = d.C, S1 = d.S1;
   const float *__restrict__ phi = p.phi + (size_t)t * d.phi_task_stride;
   const int d0 = rt * BR;
   const int nk = (N + BK - 1) / BK;
   const double beta = p.beta;
+  (void)u;
 
-  // A-tile loader: Φ[k0 + kk][d0 + 4q .. +3] → A[kk][4q..] (direct, 2 float4 per thread)
-  auto loadA = [&](int k0, float4 *ra) {
+  // A tile: Φ[k0 + kk][d0 + 4q .. +3] → A[kk][4q..]  (2 × cp.async per thread)
+  auto loadA = [&](int buf, int k0) {
 #pragma unroll
     for (int i = 0; i < 2; ++i) {
       const int idx = tid + i * OP_THREADS, kk = idx >> 5, q = idx & 31;
       const int n = k0 + kk, dd = d0 + 4 * q;
-      ra[i] = (n < N && dd < D) ? ld4(phi + (size_t)n * D + dd) : make_float4(0.f, 0.f, 0.f, 0.f);
-    }
-  };
-  auto storeA = [&](int buf, const float4 *ra) {
-#pragma unroll
-    for (int i = 0; i < 2; ++i) {
-      const int idx = tid + i * OP_THREADS, kk = idx >> 5, q = idx & 31;
-      *reinterpret_cast<float4 *>(&sm.A[buf][kk][4 * q]) = ra[i];
+      const bool ok = n < N && dd < D;
+      cp_async16(&sm.A[buf][kk][4 * q], ok ? phi + (size_t)n * D + dd : phi, ok);
     }
   };
 
   if (ct == d.nCT) {
     // ---------------- fp64 mean-column tile ---------------------------------------------------
     int any = 0;
-    for (int c = 0; c < C; ++c) any |= p.b.flagm[t * C + c];
+    for (int c = 0; c < C; ++c) any |= (p.b.flagm[t * C + c] == 1);
     if (!any) return;
     const int r = tid & (BR - 1), h = tid >> 7;
     double acc[MAXC / 2];
 #pragma unroll
     for (int i = 0; i < MAXC / 2; ++i) acc[i] = 0.0;
-    float4 ra[2];
-    double rb = 0.0;
-    const double *um = p.b.Um + (size_t)t * N * C;
-    auto loadB = [&](int k0) {
-      rb = 0.0;
+    auto loadB = [&](int buf, int k0) {
       if (tid < BK * C) {
         const int kk = tid / C, c = tid % C;
-        if (k0 + kk < N) rb = um[(size_t)(k0 + kk) * C + c];
+        double v = 0.0;
+        if (k0 + kk < N)
+          for (int s = 0; s < S1; ++s) v += p.b.Um[(((size_t)s * d.Tl + t) * N + k0 + kk) * C + c];
+        sm.Bm[buf][kk][c] = v;
       }
     };
-    auto storeB = [&](int buf) {
-      if (tid < BK * C) sm.Bm[buf][tid / C][tid % C] = rb;
-    };
-    loadA(0, ra);
-    loadB(0);
-    storeA(0, ra);
-    storeB(0);
-    __syncthreads();
+#pragma unroll
+    for (int s = 0; s < ST - 1; ++s) {
+      if (s < nk) { loadA(s, s * BK); loadB(s, s * BK); }
+      cp_commit();
+    }
     for (int kc = 0; kc < nk; ++kc) {
-      const int buf = kc & 1;
-      if (kc + 1 < nk) {
-        loadA((kc + 1) * BK, ra);
-        loadB((kc + 1) * BK);
-      }
+      cp_wait<ST - 2>();
+      __syncthreads();
+      const int nx = kc + ST - 1;
+      if (nx < nk) { loadA(nx % ST, nx * BK); loadB(nx % ST, nx * BK); }
+      cp_commit();
+      const int buf = kc % ST;
 #pragma unroll 4
       for (int kk = 0; kk < BK; ++kk) {
         const double a = (double)sm.A[buf][kk][r];
@@ -290,12 +325,8 @@ __global__ void __launch_bounds__(OP_THREADS) k_stage2(KParams p, int u) {
         for (int i = 0; i < MAXC / 2; ++i)
           if (h + 2 * i < C) acc[i] = fma(a, sm.Bm[buf][kk][h + 2 * i], acc[i]);
       }
-      if (kc + 1 < nk) {
-        storeA(buf ^ 1, ra);
-        storeB(buf ^ 1);
-      }
-      __syncthreads();
     }
+    cp_wait<0>();
     // epilogue: Wm = β acc + α ⊙ dm ; partial dᵀW over this row tile
     const int dd = d0 + r;
     double dot[MAXC / 2];
@@ -306,27 +337,25 @@ __global__ void __launch_bounds__(OP_THREADS) k_stage2(KParams p, int u) {
       if (c < C && dd < D) {
         const size_t o = ((size_t)t * C + c) * D + dd;
         const double dv = p.b.Dm[o];
-        const double w = fma(beta, acc[i], p.b.alpha64[(size_t)c * D + dd] * dv);
-        p.b.Wm[o] = w;
-        dot[i] = dv * w;
+        const double wv = fma(beta, acc[i], p.b.alpha64[(size_t)c * D + dd] * dv);
+        p.b.Wm[o] = wv;
+        dot[i] = dv * wv;
       }
     }
-    // reduce over the 128 rows of each half: warp shuffle, then 4 warps via smem
-    double *red = &sm.red[0][0];  // [2 halves][4 warps][MAXC/2]
     const int lane = tid & 31, wq = (tid >> 5) & 3;
 #pragma unroll
     for (int i = 0; i < MAXC / 2; ++i) {
       double v = dot[i];
 #pragma unroll
       for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-      if (lane == 0) red[(h * 4 + wq) * (MAXC / 2) + i] = v;
+      if (lane == 0) sm.red[h][wq][i] = v;
     }
     __syncthreads();
     if (tid < MAXC) {
       const int hh = tid & 1, i = tid >> 1, c = hh + 2 * i;
       if (c < C) {
         double v = 0.0;
-        for (int w = 0; w < 4; ++w) v += red[(hh * 4 + w) * (MAXC / 2) + i];
+        for (int q = 0; q < 4; ++q) v += sm.red[hh][q][i];
         p.b.dAdm[((size_t)t * C + c) * d.nRT2 + rt] = v;
       }
     }
@@ -337,102 +366,126 @@ __global__ void __launch_bounds__(OP_THREADS) k_stage2(KParams p, int u) {
   const int m = p.b.m_act[t];
   const int j0 = ct * BC;
   if (j0 >= m) return;
-  const int ty = tid >> 4, tx = tid & 15;
-  const float *__restrict__ U = p.b.U + (size_t)t * N * d.Pp;
-  float acc[8][4];
-#pragma unroll
-  for (int i = 0; i < 8; ++i)
-#pragma unroll
-    for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
-  float4 ra[2], rb;
-  const int kb = tid >> 4, qb = tid & 15;
+  const int w = tid >> 5, l = tid & 31;
+  const bool wact = j0 + w * WC < m;
+  // B tile: Σ_s U_s[t][k0 + kk][j0 + 4q .. +3] → B[kk][4q..]; 384 float4: kk = idx / 24, q = idx % 24
+  float4 rb[2];
   auto loadB = [&](int k0) {
-    const int n = k0 + kb, j = j0 + 4 * qb;
-    rb = (n < N && j < d.Pp) ? ld4(U + (size_t)n * d.Pp + j) : make_float4(0.f, 0.f, 0.f, 0.f);
-  };
-  auto storeB = [&](int buf) { *reinterpret_cast<float4 *>(&sm.B[buf][kb][4 * qb]) = rb; };
-  loadA(0, ra);
-  loadB(0);
-  storeA(0, ra);
-  storeB(0);
-  __syncthreads();
-  for (int kc = 0; kc < nk; ++kc) {
-    const int buf = kc & 1;
-    if (kc + 1 < nk) {
-      loadA((kc + 1) * BK, ra);
-      loadB((kc + 1) * BK);
-    }
 #pragma unroll
-    for (int kk = 0; kk < BK; ++kk) {
-      const float4 a0 = *reinterpret_cast<const float4 *>(&sm.A[buf][kk][ty * 8]);
-      const float4 a1 = *reinterpret_cast<const float4 *>(&sm.A[buf][kk][ty * 8 + 4]);
-      const float4 bv = *reinterpret_cast<const float4 *>(&sm.B[buf][kk][tx * 4]);
-      const float a[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
-      const float b[4] = {bv.x, bv.y, bv.z, bv.w};
-#pragma unroll
-      for (int i = 0; i < 8; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
-    }
-    if (kc + 1 < nk) {
-      storeA(buf ^ 1, ra);
-      storeB(buf ^ 1);
-    }
-    __syncthreads();
-  }
-  // epilogue: W = β acc + α_c ⊙ d, partial dᵀW (fp64) per column over this row tile
-  const float betaf = (float)beta;
-#pragma unroll
-  for (int jj = 0; jj < 4; ++jj) {
-    const int j = j0 + tx * 4 + jj;
-    double dot = 0.0;
-    if (j < m) {
-      const int col = p.b.act[(size_t)t * P + j];
-      const int c = col / d.K;
-      const size_t base = ((size_t)t * P + col) * D;
-      const float *al = p.b.alpha32 + (size_t)c * D;
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int dd = d0 + ty * 8 + 4 * h;
-        if (dd < D) {
-          const float4 dv = ld4(p.b.Dv + base + dd);
-          const float4 a4 = ld4(al + dd);
-          float4 w;
-          w.x = fmaf(betaf, acc[4 * h + 0][jj], a4.x * dv.x);
-          w.y = fmaf(betaf, acc[4 * h + 1][jj], a4.y * dv.y);
-          w.z = fmaf(betaf, acc[4 * h + 2][jj], a4.z * dv.z);
-          w.w = fmaf(betaf, acc[4 * h + 3][jj], a4.w * dv.w);
-          *reinterpret_cast<float4 *>(p.b.W + base + dd) = w;
-          dot += (double)dv.x * w.x + (double)dv.y * w.y + (double)dv.z * w.z + (double)dv.w * w.w;
+    for (int i = 0; i < 2; ++i) {
+      const int idx = tid + i * OP_THREADS, kk = idx / (BC / 4), q = idx % (BC / 4);
+      const int n = k0 + kk, j = j0 + 4 * q;
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (idx < BK * BC / 4 && n < N && j < m) {
+        for (int s = 0; s < S1; ++s) {
+          const float4 x = ld4(p.b.U + (((size_t)s * d.Tl + t) * N + n) * d.Pp + j);
+          v.x += x.x; v.y += x.y; v.z += x.z; v.w += x.w;
         }
+        // columns ≥ m inside the last float4 are stale: zero them
+        if (j + 1 >= m) v.y = 0.f;
+        if (j + 2 >= m) v.z = 0.f;
+        if (j + 3 >= m) v.w = 0.f;
+      }
+      rb[i] = v;
+    }
+  };
+  auto storeB = [&](int buf) {
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const int idx = tid + i * OP_THREADS, kk = idx / (BC / 4), q = idx % (BC / 4);
+      if (idx < BK * BC / 4) *reinterpret_cast<float4 *>(&sm.B[buf][kk][4 * q]) = rb[i];
+    }
+  };
+  float acc[4][WC];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int c = 0; c < WC; ++c) acc[i][c] = 0.f;
+#pragma unroll
+  for (int s = 0; s < ST - 1; ++s) {
+    if (s < nk) { loadA(s, s * BK); loadB(s * BK); storeB(s); }
+    cp_commit();
+  }
+  for (int kc = 0; kc < nk; ++kc) {
+    cp_wait<ST - 2>();
+    __syncthreads();
+    const int nx = kc + ST - 1;
+    if (nx < nk) { loadA(nx % ST, nx * BK); loadB(nx * BK); }
+    cp_commit();
+    const int buf = kc % ST;
+    if (wact) {
+#pragma unroll
+      for (int kk = 0; kk < BK; ++kk) {
+        const float4 a = *reinterpret_cast<const float4 *>(&sm.A[buf][kk][4 * l]);
+        const float *brow = &sm.B[buf][kk][w * WC];
+        const float4 b0 = *reinterpret_cast<const float4 *>(brow);
+        const float4 b1 = *reinterpret_cast<const float4 *>(brow + 4);
+        const float4 b2 = *reinterpret_cast<const float4 *>(brow + 8);
+        const float b[WC] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w, b2.x, b2.y, b2.z, b2.w};
+        const float av[4] = {a.x, a.y, a.z, a.w};
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int c = 0; c < WC; ++c) acc[i][c] = fmaf(av[i], b[c], acc[i][c]);
       }
     }
-    sm.red[ty][tx * 4 + jj] = dot;
+    if (nx < nk) storeB(nx % ST);
   }
-  __syncthreads();
-  if (tid < BC) {
-    const int j = j0 + tid;
-    if (j < m) {
-      double v = 0.0;
+  cp_wait<0>();
+  if (!wact) return;
+  // epilogue: W = β acc + α_c ⊙ d for rows d0 + 4l .. +3, partial dᵀW (fp64) per column
+  const float betaf = (float)beta;
+  const int dd = d0 + 4 * l;
 #pragma unroll
-      for (int i = 0; i < 16; ++i) v += sm.red[i][tid];
-      const int col = p.b.act[(size_t)t * P + j];
-      p.b.dAd[((size_t)t * P + col) * d.nRT2 + rt] = v;
+  for (int c = 0; c < WC; ++c) {
+    const int j = j0 + w * WC + c;
+    double dot = 0.0;
+    int col = -1;
+    if (j < m) {
+      col = p.b.act[(size_t)t * P + j];
+      if (dd < D) {
+        const size_t base = ((size_t)t * P + col) * D;
+        const float4 dv = ld4(p.b.Dv + base + dd);
+        const float4 a4 = ld4(p.b.alpha32 + (size_t)(col / d.K) * D + dd);
+        float4 wv;
+        wv.x = fmaf(betaf, acc[0][c], a4.x * dv.x);
+        wv.y = fmaf(betaf, acc[1][c], a4.y * dv.y);
+        wv.z = fmaf(betaf, acc[2][c], a4.z * dv.z);
+        wv.w = fmaf(betaf, acc[3][c], a4.w * dv.w);
+        *reinterpret_cast<float4 *>(p.b.W + base + dd) = wv;
+        dot = (double)dv.x * wv.x + (double)dv.y * wv.y + (double)dv.z * wv.z + (double)dv.w * wv.w;
+      }
     }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
+    if (l == 0 && col >= 0) p.b.dAd[((size_t)t * P + col) * d.nRT2 + rt] = dot;
   }
 }
 
 }  // namespace
 
 cudaError_t launch_stage1(const KParams &p, int u, const double *mu_src, bool mu_only, cudaStream_t s) {
-  dim3 grid(p.d.nCT + 1, p.d.nRT1, p.d.Tl);
-  k_stage1<<<grid, OP_THREADS, sizeof(int) * p.d.P, s>>>(p, u, mu_src ? mu_src : p.b.Dm, mu_only ? 1 : 0);
+  const size_t smem = sizeof(Smem1) + sizeof(int) * (size_t)p.d.P;
+  static size_t configured = 0;
+  if (smem > configured) {
+    cudaError_t e = cudaFuncSetAttribute(k_stage1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    configured = smem;
+  }
+  dim3 grid(p.d.nCT + 1, p.d.nRT1 * p.d.S1, p.d.Tl);
+  k_stage1<<<grid, OP_THREADS, smem, s>>>(p, u, mu_src ? mu_src : p.b.Dm, mu_only ? 1 : 0);
   return cudaGetLastError();
 }
 
 cudaError_t launch_stage2(const KParams &p, int u, cudaStream_t s) {
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(k_stage2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(Smem2));
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
   dim3 grid(p.d.nCT + 1, p.d.nRT2, p.d.Tl);
-  k_stage2<<<grid, OP_THREADS, 0, s>>>(p, u);
+  k_stage2<<<grid, OP_THREADS, sizeof(Smem2), s>>>(p, u);
   return cudaGetLastError();
 }
 
