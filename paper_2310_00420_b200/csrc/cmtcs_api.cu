@@ -25,19 +25,21 @@ struct cmtcs_ctx {
   bool broken;
   bool have_estep;
   int em_iter;           // global index of the next EM iteration
-  int cg_chunk;          // CG steps enqueued between host convergence checks
   char err[512];
-  int *h_alive;          // pinned [2]
   double *h_out;         // pinned [32]: stats[16] | loglik | status(as int) ...
   int *h_status;         // pinned [8]
-  cudaEvent_t ev[2];
   int64_t launches;
   // live timing (cmtcs_set_timing)
   bool timing;
-  cudaEvent_t *tev;      // pool of 2*cap + 2 events
-  int ntev;
+  cudaEvent_t tev[3];
+  unsigned long long *h_ts;  // pinned [cap][4]
   double t_ms[3];
   int64_t t_n[3];
+  // the CG loop as one graph: WHILE(any column active) { stage1; stage2; update; advance }
+  cudaStream_t cap_stream;
+  cudaGraph_t cg_graph;
+  cudaGraphExec_t cg_exec;
+  int *h_u;                 // pinned: CG steps executed
 };
 
 namespace {
@@ -173,6 +175,8 @@ size_t carve(const Dims &d, char *base, Bufs *b) {
   b->histm = cv.take<int>(cap);
   b->histt = cv.take<int>(cap);
   b->status = cv.take<int>(8);
+  b->u = cv.take<int>(1);
+  b->ts = cv.take<unsigned long long>((size_t)cap * 4);
   b->stats = cv.take<double>(16);
   b->assign = cv.take<int>(Tl);
   return cv.off;
@@ -213,6 +217,33 @@ const char *status_name(int code) {
   }
 }
 
+cmtcs_status build_cg_graph(cmtcs_ctx *c) {
+  const KParams &kp = c->kp;
+  cudaGraph_t g = nullptr;
+  CUDA_OK(c, cudaGraphCreate(&g, 0));
+  c->cg_graph = g;
+  cudaGraphConditionalHandle h;
+  CUDA_OK(c, cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault));
+  cudaGraphNodeParams cp = {};
+  cp.type = cudaGraphNodeTypeConditional;
+  cp.conditional.handle = h;
+  cp.conditional.type = cudaGraphCondTypeWhile;
+  cp.conditional.size = 1;
+  cudaGraphNode_t node;
+  CUDA_OK(c, cudaGraphAddNode(&node, g, nullptr, 0, &cp));
+  cudaGraph_t body = cp.conditional.phGraph_out[0];
+  CUDA_OK(c, cudaStreamBeginCaptureToGraph(c->cap_stream, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+  cudaError_t e1 = launch_stage1(kp, nullptr, false, c->cap_stream);
+  cudaError_t e2 = e1 == cudaSuccess ? launch_stage2(kp, c->cap_stream) : e1;
+  cudaError_t e3 = e2 == cudaSuccess ? launch_update(kp, c->cap_stream) : e2;
+  cudaError_t e4 = e3 == cudaSuccess ? launch_advance(kp, (unsigned long long)h, c->cap_stream) : e3;
+  cudaGraph_t captured = body;
+  CUDA_OK(c, cudaStreamEndCapture(c->cap_stream, &captured));
+  CUDA_OK(c, e4);
+  CUDA_OK(c, cudaGraphInstantiate(&c->cg_exec, g, 0));
+  return CMTCS_OK;
+}
+
 cmtcs_status one_em_iteration(cmtcs_ctx *c, const uint64_t *probe_bits, const double *q_override,
                               cmtcs_step_info *info) {
   KParams kp = c->kp;
@@ -229,36 +260,22 @@ cmtcs_status one_em_iteration(cmtcs_ctx *c, const uint64_t *probe_bits, const do
   CUDA_OK(c, launch_init_columns(kp, s));
   L += 1;
   const bool tm = c->timing;
-  int nrec = 0;  // events recorded: tev[0] = start of step, then (after stage 2, after update) per CG step
-  if (tm) CUDA_OK(c, cudaEventRecord(c->tev[nrec++], s));
-  // ---- batched CG (Alg. 1) over all T_loc·C·(K+1) columns, host checks convergence lazily ----
-  const int R = c->cg_chunk;
-  int u = 0, chunk = 0;
-  bool done = false;
-  while (u < d.cap && !done) {
-    const int u_end = std::min(u + R, d.cap);
-    for (; u < u_end; ++u) {
-      CUDA_OK(c, launch_stage1(kp, u, nullptr, false, s));
-      CUDA_OK(c, launch_stage2(kp, u, s));
-      if (tm) CUDA_OK(c, cudaEventRecord(c->tev[nrec++], s));
-      CUDA_OK(c, launch_update(kp, u, s));
-      if (tm) CUDA_OK(c, cudaEventRecord(c->tev[nrec++], s));
-      L += 3;
-    }
-    CUDA_OK(c, cudaMemcpyAsync(c->h_alive + (chunk & 1), kp.b.alive + (u_end - 1), sizeof(int),
-                               cudaMemcpyDeviceToHost, s));
-    CUDA_OK(c, cudaEventRecord(c->ev[chunk & 1], s));
-    if (chunk >= 1) {
-      CUDA_OK(c, cudaEventSynchronize(c->ev[(chunk - 1) & 1]));
-      if (c->h_alive[(chunk - 1) & 1] == 0) done = true;
-    }
-    ++chunk;
+  if (tm) {
+    CUDA_OK(c, cudaMemsetAsync(kp.b.ts, 0, sizeof(unsigned long long) * 4 * d.cap, s));
+    CUDA_OK(c, cudaEventRecord(c->tev[0], s));
   }
+  // ---- batched CG (Alg. 1) over all T_loc·C·(K+1) columns: one graph launch, device-side loop ----
+  if (!c->cg_exec) {
+    cmtcs_status st = build_cg_graph(c);
+    if (st != CMTCS_OK) return st;
+  }
+  CUDA_OK(c, cudaGraphLaunch(c->cg_exec, s));
+  if (tm) CUDA_OK(c, cudaEventRecord(c->tev[1], s));
   // ---- estimators: s (Eq. 5), ν̄ (Eq. 7-9), Φμ for ℓ, q and log-lik (Eq. 3) ----
   CUDA_OK(c, launch_diag(kp, s));
   CUDA_OK(c, launch_lanczos(kp.b.gam, kp.b.xi, kp.b.steps, d.Tl * d.P, d.cap, d.D, kp.b.tau, nullptr,
                             kp.b.status, s));
-  CUDA_OK(c, launch_stage1(kp, 0, kp.b.Xm, true, s));
+  CUDA_OK(c, launch_stage1(kp, kp.b.Xm, true, s));
   CUDA_OK(c, launch_estep_finish(kp, s));
   // ---- M-step (Eq. 4): local sums → all-reduce over ranks → α update ----
   CUDA_OK(c, launch_mstep_partial(kp, s));
@@ -274,7 +291,11 @@ cmtcs_status one_em_iteration(cmtcs_ctx *c, const uint64_t *probe_bits, const do
   }
   CUDA_OK(c, launch_stats(kp, s));
   L += 4;
-  if (tm) CUDA_OK(c, cudaEventRecord(c->tev[nrec++], s));
+  if (tm) {
+    CUDA_OK(c, cudaEventRecord(c->tev[2], s));
+    CUDA_OK(c, cudaMemcpyAsync(c->h_ts, kp.b.ts, sizeof(unsigned long long) * 4 * d.cap, cudaMemcpyDeviceToHost, s));
+  }
+  CUDA_OK(c, cudaMemcpyAsync(c->h_u, kp.b.u, sizeof(int), cudaMemcpyDeviceToHost, s));
   CUDA_OK(c, cudaMemcpyAsync(c->h_out, kp.b.stats, 16 * sizeof(double), cudaMemcpyDeviceToHost, s));
   CUDA_OK(c, cudaMemcpyAsync(c->h_out + 16, kp.b.red + (size_t)d.C * d.D + d.C, sizeof(double),
                              cudaMemcpyDeviceToHost, s));
@@ -282,22 +303,23 @@ cmtcs_status one_em_iteration(cmtcs_ctx *c, const uint64_t *probe_bits, const do
   CUDA_OK(c, cudaStreamSynchronize(s));
   c->launches += L;
   c->have_estep = true;
+  const int steps_run = *c->h_u;
+  L += 4 * (int64_t)steps_run;  // stage1, stage2, update, advance per CG step inside the graph
+  c->launches += 4 * (int64_t)steps_run;
   if (tm) {
-    // tev[0] | (op_end, upd_end) x steps | tail_end ; the first op starts after init_columns
-    float ms = 0.f;
-    const int steps = (nrec - 2) / 2;
-    double other = 0.0;
-    for (int i = 0; i < steps; ++i) {
-      CUDA_OK(c, cudaEventElapsedTime(&ms, c->tev[2 * i], c->tev[2 * i + 1]));
-      c->t_ms[0] += ms;
-      CUDA_OK(c, cudaEventElapsedTime(&ms, c->tev[2 * i + 1], c->tev[2 * i + 2]));
-      c->t_ms[1] += ms;
+    // per CG step: %globaltimer stamps of the first stage-1 CTA entry, the last stage-2 CTA exit
+    // and the last update-warp exit (device clock, ns)
+    for (int u = 0; u < steps_run; ++u) {
+      const unsigned long long *q = c->h_ts + 4 * u;
+      const unsigned long long t0 = ~q[0], t1 = q[1], t2 = q[2];
+      if (q[0] && t1 >= t0) c->t_ms[0] += (t1 - t0) * 1e-6;
+      if (t1 && t2 >= t1) c->t_ms[1] += (t2 - t1) * 1e-6;
     }
-    CUDA_OK(c, cudaEventElapsedTime(&ms, c->tev[nrec - 2], c->tev[nrec - 1]));
-    other += ms;
-    c->t_ms[2] += other;
-    c->t_n[0] += steps;
-    c->t_n[1] += steps;
+    float ms = 0.f;
+    CUDA_OK(c, cudaEventElapsedTime(&ms, c->tev[1], c->tev[2]));
+    c->t_ms[2] += ms;
+    c->t_n[0] += steps_run;
+    c->t_n[1] += steps_run;
     c->t_n[2] += 1;
   }
   const int it = c->em_iter;
@@ -380,7 +402,6 @@ cmtcs_status cmtcs_init(cmtcs_ctx **out, const cmtcs_problem *p, const float *ph
   c->rank = rank;
   c->world = world;
   c->em_iter = p->em_iter0;
-  c->cg_chunk = 8;
   carve(d, (char *)workspace, &b);
   c->kp.d = d;
   c->kp.b = b;
@@ -393,11 +414,12 @@ cmtcs_status cmtcs_init(cmtcs_ctx **out, const cmtcs_problem *p, const float *ph
   c->kp.empty_eps = p->empty_eps;
   c->kp.seed = p->probe_seed;
   *out = c;  // from here on errors leave a (broken) ctx the caller destroys
-  CUDA_OK(c, cudaMallocHost((void **)&c->h_alive, 2 * sizeof(int)));
   CUDA_OK(c, cudaMallocHost((void **)&c->h_out, 32 * sizeof(double)));
   CUDA_OK(c, cudaMallocHost((void **)&c->h_status, 8 * sizeof(int)));
-  CUDA_OK(c, cudaEventCreateWithFlags(&c->ev[0], cudaEventDisableTiming));
-  CUDA_OK(c, cudaEventCreateWithFlags(&c->ev[1], cudaEventDisableTiming));
+  CUDA_OK(c, cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking));
+  CUDA_OK(c, cudaMallocHost((void **)&c->h_u, sizeof(int)));
+  CUDA_OK(c, cudaMallocHost((void **)&c->h_ts, sizeof(unsigned long long) * 4 * d.cap));
+  for (int i = 0; i < 3; ++i) CUDA_OK(c, cudaEventCreate(&c->tev[i]));
   CUDA_OK(c, cudaMemsetAsync(b.status, 0, 8 * sizeof(int), c->stream));
   CUDA_OK(c, cudaMemsetAsync(b.gam, 0, sizeof(double) * d.Tl * d.P * d.cap, c->stream));
   CUDA_OK(c, cudaMemsetAsync(b.xi, 0, sizeof(double) * d.Tl * d.P * d.cap, c->stream));
@@ -490,16 +512,15 @@ void cmtcs_destroy(cmtcs_ctx *c) {
   cudaSetDevice(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
   if (c->have_comm) ncclCommDestroy(c->comm);
-  if (c->ev[0]) cudaEventDestroy(c->ev[0]);
-  if (c->ev[1]) cudaEventDestroy(c->ev[1]);
-  if (c->h_alive) cudaFreeHost(c->h_alive);
+  if (c->cg_exec) cudaGraphExecDestroy(c->cg_exec);
+  if (c->cg_graph) cudaGraphDestroy(c->cg_graph);
+  if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
+  for (int i = 0; i < 3; ++i)
+    if (c->tev[i]) cudaEventDestroy(c->tev[i]);
+  if (c->h_u) cudaFreeHost(c->h_u);
+  if (c->h_ts) cudaFreeHost(c->h_ts);
   if (c->h_out) cudaFreeHost(c->h_out);
   if (c->h_status) cudaFreeHost(c->h_status);
-  if (c->tev) {
-    for (int i = 0; i < c->ntev; ++i)
-      if (c->tev[i]) cudaEventDestroy(c->tev[i]);
-    delete[] c->tev;
-  }
   delete c;
 }
 
@@ -508,13 +529,6 @@ int64_t cmtcs_kernel_launches(const cmtcs_ctx *c) { return c ? c->launches : 0; 
 cmtcs_status cmtcs_set_timing(cmtcs_ctx *c, int32_t enable) {
   if (!c) return fail(nullptr, CMTCS_EINVAL, "ctx is NULL");
   if (c->broken) return CMTCS_ESTATE;
-  if (enable && !c->tev) {
-    c->ntev = 2 * c->kp.d.cap + 2;
-    c->tev = new (std::nothrow) cudaEvent_t[c->ntev]();
-    if (!c->tev) return fail(c, CMTCS_ENOMEM, "event pool allocation failed");
-    CUDA_OK(c, cudaSetDevice(c->device));
-    for (int i = 0; i < c->ntev; ++i) CUDA_OK(c, cudaEventCreate(&c->tev[i]));
-  }
   c->timing = enable != 0;
   return CMTCS_OK;
 }

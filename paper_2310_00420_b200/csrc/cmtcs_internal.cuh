@@ -13,7 +13,7 @@ constexpr int OP_BR = 128;      // operator CTA tile: rows (N in stage 1, D in s
 constexpr int OP_BC = 96;       // operator CTA tile: probe columns (8 warps x 12)
 constexpr int OP_BK = 16;       // contraction chunk
 constexpr int OP_THREADS = 256;
-constexpr int UPD_THREADS = 256;
+constexpr int UPD_THREADS = 256;  // 8 warps = 8 columns per CTA
 
 // Sizes of one rank's problem.  Column index of probe (c, k) inside a task: col = c*K + k.
 struct Dims {
@@ -64,6 +64,9 @@ struct Bufs {
   int *histm;        // [cap]  mean columns active at step u
   int *histt;        // [cap]  tasks with an active column at step u
   int *status;       // [8]    first error: code, t, col, u
+  int *u;            // [1]    current CG step (device-side loop counter of the CG graph)
+  unsigned long long *ts;  // [cap][4] per-step %globaltimer stamps: stage-1 first entry (min),
+                           //          stage-2 last exit, update last exit (max), unused
   double *stats;     // [16]   step statistics (filled by k_stats)
   int *assign;       // [Tl]
 };
@@ -84,9 +87,10 @@ struct KParams {
 
 // launchers (return cudaGetLastError())
 cudaError_t launch_init_columns(const KParams &p, cudaStream_t s);
-cudaError_t launch_stage1(const KParams &p, int u, const double *mu_src, bool mu_only, cudaStream_t s);
-cudaError_t launch_stage2(const KParams &p, int u, cudaStream_t s);
-cudaError_t launch_update(const KParams &p, int u, cudaStream_t s);
+cudaError_t launch_stage1(const KParams &p, const double *mu_src, bool mu_only, cudaStream_t s);
+cudaError_t launch_stage2(const KParams &p, cudaStream_t s);
+cudaError_t launch_update(const KParams &p, cudaStream_t s);
+cudaError_t launch_advance(const KParams &p, unsigned long long cond_handle, cudaStream_t s);
 cudaError_t launch_rhs(const KParams &p, cudaStream_t s);
 cudaError_t launch_alpha_stats(const KParams &p, cudaStream_t s);
 cudaError_t launch_diag(const KParams &p, cudaStream_t s);
@@ -100,6 +104,12 @@ cudaError_t launch_readout(const KParams &p, double *recon, cudaStream_t s);
 cudaError_t launch_probe_words(uint64_t seed, int it, int T, int t0, int Tl, int C, int K, int D,
                                uint64_t *out, cudaStream_t s);
 cudaError_t launch_copy_transcript(const KParams &p, double *gam, double *xi, cudaStream_t s);
+
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
 
 // error codes written to status[0] by kernels
 enum { ST_OK = 0, ST_BREAKDOWN = 1, ST_EIG = 2, ST_NUMERIC = 3 };

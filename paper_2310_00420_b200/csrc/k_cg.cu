@@ -81,6 +81,7 @@ __global__ void k_init_columns(KParams p) {
     }
     if (threadIdx.x == 0) {
       const size_t g = (size_t)t * d.P + slot;
+      if (g == 0) *p.b.u = 0;
       p.b.rr[g] = (double)d.D;  // ‖p‖² = D exactly
       p.b.flag[g] = 1;
       p.b.steps[g] = 0;
@@ -112,11 +113,18 @@ __device__ void report(int *status, int code, int t, int col, int u) {
   }
 }
 
-__global__ void __launch_bounds__(UPD_THREADS) k_update(KParams p, int u) {
-  __shared__ double sh[32];
-  __shared__ double s_g;
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// One warp per column (8 columns per CTA): Alg. 1 lines 3-7 with warp-shuffle fp64 dot products.
+__global__ void __launch_bounds__(UPD_THREADS) k_update(KParams p) {
   const Dims &d = p.d;
-  const int slot = blockIdx.x, t = blockIdx.y, tid = threadIdx.x;
+  const int u = *p.b.u;
+  const int lane = threadIdx.x & 31;
+  const int slot = blockIdx.x * (UPD_THREADS / 32) + (threadIdx.x >> 5), t = blockIdx.y;
   const double tol = p.tol;
   if (slot < d.P) {
     // ------------------------------ fp32 probe column ---------------------------------------
@@ -127,7 +135,7 @@ __global__ void __launch_bounds__(UPD_THREADS) k_update(KParams p, int u) {
     for (int i = 0; i < d.nRT2; ++i) dAd += p.b.dAd[g * d.nRT2 + i];
     const double rr = p.b.rr[g];
     if (!(dAd > 0.0)) {  // Alg. 1 line 3 breakdown
-      if (tid == 0) {
+      if (lane == 0) {
         report(p.b.status, ST_BREAKDOWN, d.t0 + t, col, u + 1);
         p.b.flag[g] = 0;
       }
@@ -140,7 +148,7 @@ __global__ void __launch_bounds__(UPD_THREADS) k_update(KParams p, int u) {
     const float4 *w4 = reinterpret_cast<const float4 *>(p.b.W + g * d.D);
     const int n4 = d.D >> 2;
     double acc = 0.0;
-    for (int i = tid; i < n4; i += blockDim.x) {
+    for (int i = lane; i < n4; i += 32) {
       const float4 dv = d4[i], wv = w4[i];
       float4 xv = x4[i], rv = r4[i];
       xv.x = (float)fma(gam, (double)dv.x, (double)xv.x);
@@ -155,11 +163,11 @@ __global__ void __launch_bounds__(UPD_THREADS) k_update(KParams p, int u) {
       r4[i] = rv;
       acc += (double)rv.x * rv.x + (double)rv.y * rv.y + (double)rv.z * rv.z + (double)rv.w * rv.w;
     }
-    const double rrn = block_sum(acc, sh);
+    const double rrn = warp_sum(acc);
     const double xi = rrn / rr;
     const bool conv = sqrt(rrn) <= tol * sqrt((double)d.D);
     const bool stop = conv || (u + 1 >= d.cap);
-    if (tid == 0) {
+    if (lane == 0) {
       p.b.gam[g * d.cap + u] = gam;
       p.b.xi[g * d.cap + u] = xi;
       p.b.steps[g] = u + 1;
@@ -168,9 +176,7 @@ __global__ void __launch_bounds__(UPD_THREADS) k_update(KParams p, int u) {
       else atomicAdd(p.b.alive + u, 1);
     }
     if (!stop) {
-      const float xf = (float)xi;
-      (void)xf;
-      for (int i = tid; i < n4; i += blockDim.x) {
+      for (int i = lane; i < n4; i += 32) {
         const float4 rv = r4[i];
         float4 dv = d4[i];
         dv.x = (float)fma(xi, (double)dv.x, (double)rv.x);
@@ -180,7 +186,7 @@ __global__ void __launch_bounds__(UPD_THREADS) k_update(KParams p, int u) {
         d4[i] = dv;
       }
     }
-  } else {
+  } else if (slot < d.P + d.C) {
     // ------------------------------ fp64 mean column ----------------------------------------
     const int c = slot - d.P;
     const int gi = t * d.C + c;
@@ -190,36 +196,60 @@ __global__ void __launch_bounds__(UPD_THREADS) k_update(KParams p, int u) {
     for (int i = 0; i < d.nRT2; ++i) dAd += p.b.dAdm[g * d.nRT2 + i];
     const double rr = p.b.rrm[g];
     if (!(dAd > 0.0)) {
-      if (tid == 0) {
+      if (lane == 0) {
         report(p.b.status, ST_BREAKDOWN, d.t0 + t, -1 - c, u + 1);
         p.b.flagm[g] = 0;
       }
       return;
     }
     const double gam = rr / dAd;
-    double *x = p.b.Xm + g * d.D, *r = p.b.Rm + g * d.D, *dv = p.b.Dm + g * d.D;
-    const double *w = p.b.Wm + g * d.D;
+    double2 *x = reinterpret_cast<double2 *>(p.b.Xm + g * d.D);
+    double2 *r = reinterpret_cast<double2 *>(p.b.Rm + g * d.D);
+    double2 *dv = reinterpret_cast<double2 *>(p.b.Dm + g * d.D);
+    const double2 *w = reinterpret_cast<const double2 *>(p.b.Wm + g * d.D);
+    const int n2 = d.D >> 1;
     double acc = 0.0;
-    for (int i = tid; i < d.D; i += blockDim.x) {
-      x[i] = fma(gam, dv[i], x[i]);
-      const double rn = fma(-gam, w[i], r[i]);
+    for (int i = lane; i < n2; i += 32) {
+      const double2 dd = dv[i], ww = w[i];
+      double2 xx = x[i], rn = r[i];
+      xx.x = fma(gam, dd.x, xx.x);
+      xx.y = fma(gam, dd.y, xx.y);
+      rn.x = fma(-gam, ww.x, rn.x);
+      rn.y = fma(-gam, ww.y, rn.y);
+      x[i] = xx;
       r[i] = rn;
-      acc = fma(rn, rn, acc);
+      acc = fma(rn.x, rn.x, acc);
+      acc = fma(rn.y, rn.y, acc);
     }
-    const double rrn = block_sum(acc, sh);
+    const double rrn = warp_sum(acc);
     const double xi = rrn / rr;
     const bool conv = sqrt(rrn) <= tol * sqrt(p.b.bnorm2[t]);
     const bool stop = conv || (u + 1 >= d.cap);
-    if (tid == 0) {
+    if (lane == 0) {
       p.b.stepsm[g] = u + 1;
       p.b.rrm[g] = rrn;
       if (stop) p.b.flagm[g] = conv ? 0 : 2;
       else atomicAdd(p.b.alive + u, 1);
     }
     if (!stop)
-      for (int i = tid; i < d.D; i += blockDim.x) dv[i] = fma(xi, dv[i], r[i]);
+      for (int i = lane; i < n2; i += 32) {
+        const double2 rn = r[i];
+        double2 dd = dv[i];
+        dd.x = fma(xi, dd.x, rn.x);
+        dd.y = fma(xi, dd.y, rn.y);
+        dv[i] = dd;
+      }
   }
-  (void)s_g;
+  if (threadIdx.x == 0) atomicMax(p.b.ts + 4 * u + 2, globaltimer());
+}
+
+// End of one CG step inside the graph's WHILE body: advance the step counter and keep looping
+// while some column is still active and the cap is not reached.
+__global__ void k_advance(KParams p, cudaGraphConditionalHandle h) {
+  const int u = *p.b.u;
+  const int more = (p.b.alive[u] > 0) && (u + 1 < p.d.cap);
+  *p.b.u = u + 1;
+  cudaGraphSetConditional(h, more ? 1u : 0u);
 }
 
 __global__ void k_probe_words(uint64_t seed, int it, int T, int t0, int Tl, int C, int K, int D,
@@ -247,8 +277,14 @@ cudaError_t launch_init_columns(const KParams &p, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-cudaError_t launch_update(const KParams &p, int u, cudaStream_t s) {
-  k_update<<<dim3(p.d.P + p.d.C, p.d.Tl), UPD_THREADS, 0, s>>>(p, u);
+cudaError_t launch_update(const KParams &p, cudaStream_t s) {
+  const int per = UPD_THREADS / 32;
+  k_update<<<dim3((p.d.P + p.d.C + per - 1) / per, p.d.Tl), UPD_THREADS, 0, s>>>(p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_advance(const KParams &p, unsigned long long cond_handle, cudaStream_t s) {
+  k_advance<<<1, 1, 0, s>>>(p, (cudaGraphConditionalHandle)cond_handle);
   return cudaGetLastError();
 }
 

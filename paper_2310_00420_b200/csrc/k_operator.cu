@@ -77,7 +77,7 @@ __device__ int build_act(const int *flag, int P, int *s_act, int *s_m) {
 // ---------------------------------------------------------------------------------------------
 // stage 1:  grid (nCT + 1, nRT1 * S1, Tl)
 // ---------------------------------------------------------------------------------------------
-__global__ void __launch_bounds__(OP_THREADS, 2) k_stage1(KParams p, int u, const double *__restrict__ mu_src,
+__global__ void __launch_bounds__(OP_THREADS, 2) k_stage1(KParams p, const double *__restrict__ mu_src,
                                                           int mu_only) {
   extern __shared__ __align__(16) unsigned char dsm1[];
   Smem1 &sm = *reinterpret_cast<Smem1 *>(dsm1);
@@ -108,6 +108,7 @@ __global__ void __launch_bounds__(OP_THREADS, 2) k_stage1(KParams p, int u, cons
       int any = 0;
       for (int c = 0; c < C; ++c) any |= (p.b.flagm[t * C + c] == 1);
       if (!any) return;
+      if (tid == 0) atomicMax(p.b.ts + 4 * (*p.b.u), ~globaltimer());
     }
     const double *src = mu_src + (size_t)t * C * D;
     const int r = tid & (BR - 1), h = tid >> 7;
@@ -153,6 +154,8 @@ __global__ void __launch_bounds__(OP_THREADS, 2) k_stage1(KParams p, int u, cons
   if (mu_only) return;
 
   // ---------------- fp32 probe tile -------------------------------------------------------
+  const int u = *p.b.u;
+  if (tid == 0) atomicMax(p.b.ts + 4 * u, ~globaltimer());  // ~t: max ⇔ min
   const int m = build_act(p.b.flag + (size_t)t * P, P, s_act, &sm.m);
   if (ct == 0 && blockIdx.y == 0) {
     // task bookkeeping for this CG step: publish the act list and the step histograms
@@ -265,7 +268,7 @@ __global__ void __launch_bounds__(OP_THREADS, 2) k_stage1(KParams p, int u, cons
 // ---------------------------------------------------------------------------------------------
 // stage 2:  grid (nCT + 1, nRT2, Tl)
 // ---------------------------------------------------------------------------------------------
-__global__ void __launch_bounds__(OP_THREADS, 2) k_stage2(KParams p, int u) {
+__global__ void __launch_bounds__(OP_THREADS, 2) k_stage2(KParams p) {
   extern __shared__ __align__(16) unsigned char dsm2[];
   Smem2 &sm = *reinterpret_cast<Smem2 *>(dsm2);
   const Dims &d = p.d;
@@ -275,7 +278,6 @@ __global__ void __launch_bounds__(OP_THREADS, 2) k_stage2(KParams p, int u) {
   const int d0 = rt * BR;
   const int nk = (N + BK - 1) / BK;
   const double beta = p.beta;
-  (void)u;
 
   // A tile: Φ[k0 + kk][d0 + 4q .. +3] → A[kk][4q..]  (2 × cp.async per thread)
   auto loadA = [&](int buf, int k0) {
@@ -359,6 +361,7 @@ __global__ void __launch_bounds__(OP_THREADS, 2) k_stage2(KParams p, int u) {
         p.b.dAdm[((size_t)t * C + c) * d.nRT2 + rt] = v;
       }
     }
+    if (tid == 0) atomicMax(p.b.ts + 4 * (*p.b.u) + 1, globaltimer());
     return;
   }
 
@@ -460,11 +463,12 @@ __global__ void __launch_bounds__(OP_THREADS, 2) k_stage2(KParams p, int u) {
     for (int o = 16; o; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
     if (l == 0 && col >= 0) p.b.dAd[((size_t)t * P + col) * d.nRT2 + rt] = dot;
   }
+  if (tid == 0) atomicMax(p.b.ts + 4 * (*p.b.u) + 1, globaltimer());  // warp 0 is always active here
 }
 
 }  // namespace
 
-cudaError_t launch_stage1(const KParams &p, int u, const double *mu_src, bool mu_only, cudaStream_t s) {
+cudaError_t launch_stage1(const KParams &p, const double *mu_src, bool mu_only, cudaStream_t s) {
   const size_t smem = sizeof(Smem1) + sizeof(int) * (size_t)p.d.P;
   static size_t configured = 0;
   if (smem > configured) {
@@ -473,11 +477,11 @@ cudaError_t launch_stage1(const KParams &p, int u, const double *mu_src, bool mu
     configured = smem;
   }
   dim3 grid(p.d.nCT + 1, p.d.nRT1 * p.d.S1, p.d.Tl);
-  k_stage1<<<grid, OP_THREADS, smem, s>>>(p, u, mu_src ? mu_src : p.b.Dm, mu_only ? 1 : 0);
+  k_stage1<<<grid, OP_THREADS, smem, s>>>(p, mu_src ? mu_src : p.b.Dm, mu_only ? 1 : 0);
   return cudaGetLastError();
 }
 
-cudaError_t launch_stage2(const KParams &p, int u, cudaStream_t s) {
+cudaError_t launch_stage2(const KParams &p, cudaStream_t s) {
   static bool configured = false;
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(k_stage2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(Smem2));
@@ -485,7 +489,7 @@ cudaError_t launch_stage2(const KParams &p, int u, cudaStream_t s) {
     configured = true;
   }
   dim3 grid(p.d.nCT + 1, p.d.nRT2, p.d.Tl);
-  k_stage2<<<grid, OP_THREADS, sizeof(Smem2), s>>>(p, u);
+  k_stage2<<<grid, OP_THREADS, sizeof(Smem2), s>>>(p);
   return cudaGetLastError();
 }
 
