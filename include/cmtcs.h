@@ -65,6 +65,8 @@ typedef struct cmtcs_problem {
   int32_t task_begin;    /* this rank owns global tasks [task_begin, task_end)                  */
   int32_t task_end;
   int32_t em_iter0;      /* global EM-iteration index of the next em_step (probe counter `it`) */
+  double mean_rel_tol;   /* tolerance of the C mean systems A μ = βΦᵀy; < 0 ⇒ cg_rel_tol.  A tighter
+                            value (e.g. 1e-10) makes μ independent of where CG stops (DESIGN.md §3 A5) */
 } cmtcs_problem;
 
 /* Statistics of the last EM iteration run by cmtcs_em_step (host struct, filled on return). */

@@ -33,7 +33,8 @@ class cmtcs_problem(ctypes.Structure):
                 ("shared_phi", c_int32), ("beta", c_double), ("pi", POINTER(c_double)),
                 ("cg_max_iters", c_int32), ("cg_rel_tol", c_double), ("alpha_max", c_double),
                 ("var_floor", c_double), ("empty_eps", c_double), ("probe_seed", c_uint64),
-                ("task_begin", c_int32), ("task_end", c_int32), ("em_iter0", c_int32)]
+                ("task_begin", c_int32), ("task_end", c_int32), ("em_iter0", c_int32),
+                ("mean_rel_tol", c_double)]
 
 
 class cmtcs_step_info(ctypes.Structure):

@@ -77,7 +77,8 @@ struct KParams {
   const float *phi;
   const float *y;
   double beta;
-  double tol;
+  double tol;                  // probe columns: stop when ‖r‖ ≤ tol·‖p‖
+  double tol_mean;             // mean columns
   double alpha_max, var_floor, empty_eps;
   uint64_t seed;
   int it;                      // global EM iteration index of this E-step

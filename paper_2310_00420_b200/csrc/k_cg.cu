@@ -223,7 +223,7 @@ __global__ void __launch_bounds__(UPD_THREADS) k_update(KParams p) {
     }
     const double rrn = warp_sum(acc);
     const double xi = rrn / rr;
-    const bool conv = sqrt(rrn) <= tol * sqrt(p.b.bnorm2[t]);
+    const bool conv = sqrt(rrn) <= p.tol_mean * sqrt(p.b.bnorm2[t]);
     const bool stop = conv || (u + 1 >= d.cap);
     if (lane == 0) {
       p.b.stepsm[g] = u + 1;
@@ -283,8 +283,11 @@ cudaError_t launch_update(const KParams &p, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+__global__ void k_advance_plain(KParams p) { *p.b.u += 1; }
+
 cudaError_t launch_advance(const KParams &p, unsigned long long cond_handle, cudaStream_t s) {
-  k_advance<<<1, 1, 0, s>>>(p, (cudaGraphConditionalHandle)cond_handle);
+  if (cond_handle == 0ull) k_advance_plain<<<1, 1, 0, s>>>(p);
+  else k_advance<<<1, 1, 0, s>>>(p, (cudaGraphConditionalHandle)cond_handle);
   return cudaGetLastError();
 }
 

@@ -22,6 +22,7 @@ class CoFEM:
                  cg_max_iters: int, cg_rel_tol: float, probe_seed: int, pi=None, alpha0=None,
                  task_begin: int = 0, shared_phi: bool = False, em_iter0: int = 0,
                  alpha_max: float = 1e12, var_floor: float = 1e-12, empty_eps: float = 1e-10,
+                 mean_rel_tol: float = -1.0,
                  nccl_uid: bytes | None = None, rank: int = 0, world: int = 1, stream=None):
         if not (phi.is_cuda and y.is_cuda):
             raise ValueError("phi and y must be CUDA tensors (no CPU path exists)")
@@ -38,7 +39,8 @@ class CoFEM:
             pi=self._pi.ctypes.data_as(_c.POINTER(_c.c_double)), cg_max_iters=int(cg_max_iters),
             cg_rel_tol=float(cg_rel_tol), alpha_max=float(alpha_max), var_floor=float(var_floor),
             empty_eps=float(empty_eps), probe_seed=int(probe_seed) & ((1 << 64) - 1),
-            task_begin=int(task_begin), task_end=int(task_begin) + T_loc, em_iter0=int(em_iter0))
+            task_begin=int(task_begin), task_end=int(task_begin) + T_loc, em_iter0=int(em_iter0),
+            mean_rel_tol=float(mean_rel_tol))
         a0 = torch.ones(C, D, dtype=torch.float64, device=self.device) if alpha0 is None else \
             torch.as_tensor(np.asarray(alpha0, np.float64) if not torch.is_tensor(alpha0) else alpha0,
                             dtype=torch.float64).to(self.device).contiguous()

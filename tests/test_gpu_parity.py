@@ -99,17 +99,20 @@ def test_lanczos_quadrature_real_cg_transcripts(torch_cuda):
 
 
 # ------------------------------------------------------------------------------ one EM step --
+MEAN_TOL = 1e-10   # μ parity compares converged means (DESIGN.md §6 P-μ): both sides solve Aμ = b to 1e-10
+
+
 def _single_step(data, alpha, it, cap, tol=None, K=None):
     cfg = data["cfg"]
     K = cfg.K if K is None else K
     tol = cfg.cg_tol if tol is None else tol
-    g = make_gpu(data, K=K, tol=tol, cap=cap, alpha=alpha, em_iter0=it)
+    g = make_gpu(data, K=K, tol=tol, cap=cap, alpha=alpha, em_iter0=it, mean_tol=MEAN_TOL)
     info = g.em_step(1)
     post = to_np(g.posterior())
     tr = g.transcript()
     steps = tr["steps"].cpu().numpy().reshape(len(data["tasks"]), -1, K)
     g.close()
-    orc = O.e_step(data, alpha, it, mode="cofem", K=K, tol=tol, cap=cap)
+    orc = O.e_step(data, alpha, it, mode="cofem", K=K, tol=tol, cap=cap, mu_tol=MEAN_TOL, mu_cap=cap)
     a_next = O.m_step(orc["q"], orc["mu"], orc["s"], alpha)
     conv_gpu = np.all(steps < cap, axis=-1)
     conv_orc = np.all(orc["probe_steps"].reshape(steps.shape) < cap, axis=-1)
