@@ -119,15 +119,17 @@ bool make_dims(const cmtcs_problem *p, Dims *d, char *why) {
   d->nRT2 = (p->D + OP_BR - 1) / OP_BR;
   d->nCT = (d->P + OP_BC - 1) / OP_BC;
   {
-    // split the stage-1 contraction over D until ≥ 2 CTAs per SM exist (each split ≥ 128 long)
+    // split the stage-1 contraction over D until ≥ 2 CTAs per SM exist; S1 ∈ {1, 2, 4, 8} (the
+    // cluster of split CTAs reduces its 128-row tile by rows) and every split ≥ 128 long
     const int sms = 148;
     const long base = (long)d->nCT * d->nRT1 * (p->task_end - p->task_begin);
-    int s1 = (int)std::min<long>((2L * sms + base - 1) / base, std::max(1, p->D / 128));
-    s1 = std::max(1, s1);
+    int s1 = 1;
+    while (s1 < 8 && base * s1 < 2L * sms && p->D / (2 * s1) >= 128) s1 *= 2;
     int k1 = (p->D + s1 - 1) / s1;
     k1 = (k1 + OP_BK - 1) / OP_BK * OP_BK;
     d->K1 = k1;
-    d->S1 = (p->D + k1 - 1) / k1;
+    d->S1 = s1;
+    if ((p->D + k1 - 1) / k1 != s1) { snprintf(why, 256, "internal: bad split of D=%d", p->D); return false; }
   }
   d->shared_phi = p->shared_phi ? 1 : 0;
   d->phi_task_stride = p->shared_phi ? 0 : (int64_t)p->N * p->D;
@@ -151,8 +153,8 @@ size_t carve(const Dims &d, char *base, Bufs *b) {
   b->Rm = cv.take<double>(Tl * C * D);
   b->Dm = cv.take<double>(Tl * C * D);
   b->Wm = cv.take<double>(Tl * C * D);
-  b->U = cv.take<float>((size_t)d.S1 * Tl * N * d.Pp);
-  b->Um = cv.take<double>((size_t)d.S1 * Tl * N * C);
+  b->U = cv.take<float>(Tl * N * d.Pp);
+  b->Um = cv.take<double>(Tl * N * C);
   b->rr = cv.take<double>(Tl * P);
   b->rrm = cv.take<double>(Tl * C);
   b->dAd = cv.take<double>(Tl * P * d.nRT2);

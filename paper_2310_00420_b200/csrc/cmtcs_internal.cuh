@@ -41,8 +41,8 @@ struct Bufs {
   double *bnorm2;    // [Tl]      ‖b‖²
   float *X, *R, *Dv, *W;     // probe columns [Tl][P][D]
   double *Xm, *Rm, *Dm, *Wm; // mean columns  [Tl][C][D]
-  float *U;          // [S1][Tl][N][Pp]  stage-1 split-K partials (compacted column order)
-  double *Um;        // [S1][Tl][N][C]
+  float *U;          // [Tl][N][Pp]  stage-1 output (compacted column order)
+  double *Um;        // [Tl][N][C]
   double *rr;        // [Tl][P]
   double *rrm;       // [Tl][C]
   double *dAd;       // [Tl][P][nRT2]  per-row-tile partial dᵀAd

@@ -170,9 +170,7 @@ __global__ void k_estep_finish(KParams p) {
     quad = block_sum(quad, sh);
     double res = 0.0;
     for (int n = tid; n < d.N; n += blockDim.x) {
-      double phimu = 0.0;  // Φμ from the stage-1 split-K partials
-      for (int s = 0; s < d.S1; ++s) phimu += p.b.Um[(((size_t)s * d.Tl + t) * d.N + n) * d.C + c];
-      const double rv = (double)p.y[(size_t)t * d.N + n] - phimu;
+      const double rv = (double)p.y[(size_t)t * d.N + n] - p.b.Um[((size_t)t * d.N + n) * d.C + c];
       res = fma(rv, rv, res);
     }
     res = block_sum(res, sh);

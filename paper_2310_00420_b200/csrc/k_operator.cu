@@ -3,8 +3,10 @@
 // simultaneously ... A never needs to be explicitly computed").
 //
 // Two contractions per CG step (ΦᵀΦ is never formed; N = D/4 makes this the cheaper order):
-//   stage 1  U_s[t][n][j] = Σ_{d ∈ slice s} Φ_t[n][d] · V[t][act_j][d]   (rows n, K = D, split-K S1)
-//   stage 2  W[t][act_j][d] = β Σ_n Φ_t[n][d] · (Σ_s U_s[t][n][j]) + α ⊙ V (rows d, K = N)
+//   stage 1  U[t][n][j] = Σ_s Σ_{d ∈ slice s} Φ_t[n][d] · V[t][act_j][d]   (rows n, K = D)
+//            split-K over S1 slices when T·N is small; the S1 CTAs of a tile form a thread-block
+//            cluster and reduce their partial tiles over DSMEM in fixed order (deterministic)
+//   stage 2  W[t][act_j][d] = β Σ_n Φ_t[n][d] · U[t][n][j] + α ⊙ V          (rows d, K = N)
 //            + the per-row-tile partial dᵀ(Ad) of Alg. 1 line 3, accumulated in fp64.
 // Probe columns (fp32): CTA = 8 warps = 128 rows × 96 columns; each warp owns 12 columns and all
 // 128 rows (lane: 4 rows × 12 columns, 48 FFMA per k per 4 smem loads).  Converged columns are
@@ -12,7 +14,11 @@
 // waste is < 12 columns per task.  Φ tiles stream through a 3-stage cp.async ring.
 // The C mean columns of a task run as one extra fp64 CTA per row tile (blockIdx.x == nCT) on the
 // same Φ tiles (DFMA), keeping μ in fp64 end to end.
+#include <cooperative_groups.h>
+
 #include "cmtcs_internal.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace cmtcs {
 
@@ -142,13 +148,25 @@ __global__ void __launch_bounds__(OP_THREADS, 2) k_stage1(KParams p, const doubl
       }
     }
     cp_wait<0>();
-    const int n = n0 + r;
-    if (n < N) {
-      double *um = p.b.Um + (size_t)sp * d.Tl * N * C;
+    __syncthreads();
+    // split-K partial tile [BR][C] (fp64) in this CTA's smem, then a DSMEM reduction by rows
+    double *part = reinterpret_cast<double *>(dsm1);
 #pragma unroll
-      for (int i = 0; i < MAXC / 2; ++i)
-        if (h + 2 * i < C) um[((size_t)t * N + n) * C + h + 2 * i] = acc[i];
+    for (int i = 0; i < MAXC / 2; ++i)
+      if (h + 2 * i < C) part[r * MAXC + h + 2 * i] = acc[i];
+    cg::cluster_group cl = cg::this_cluster();
+    if (d.S1 > 1) cl.sync(); else __syncthreads();
+    const int rows = BR / d.S1, rb = sp * rows;
+    for (int e = tid; e < rows * C; e += OP_THREADS) {
+      const int rr = rb + e / C, c = e % C;
+      double v = 0.0;
+      for (int q = 0; q < d.S1; ++q) {
+        const double *pp = d.S1 > 1 ? cl.map_shared_rank(part, q) : part;
+        v += pp[rr * MAXC + c];
+      }
+      if (n0 + rr < N) p.b.Um[((size_t)t * N + n0 + rr) * C + c] = v;
     }
+    if (d.S1 > 1) cl.sync();
     return;
   }
   if (mu_only) return;
@@ -247,22 +265,52 @@ __global__ void __launch_bounds__(OP_THREADS, 2) k_stage1(KParams p, const doubl
     if (nx < nk) storeB(nx % ST);
   }
   cp_wait<0>();
-  if (wact) {
-    float *U = p.b.U + (size_t)sp * d.Tl * N * d.Pp;
-    const int jc = j0 + w * WC;
+  const int jc = j0 + w * WC;
+  if (d.S1 == 1) {
+    if (wact) {
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const int n = n0 + l + 32 * i;
-      if (n < N) {
-        float *dst = U + ((size_t)t * N + n) * d.Pp + jc;
+      for (int i = 0; i < 4; ++i) {
+        const int n = n0 + l + 32 * i;
+        if (n < N) {
+          float *dst = p.b.U + ((size_t)t * N + n) * d.Pp + jc;
 #pragma unroll
-        for (int q = 0; q < WC / 4; ++q)
-          if (jc + 4 * q < d.Pp)
-            *reinterpret_cast<float4 *>(dst + 4 * q) =
-                make_float4(acc[i][4 * q], acc[i][4 * q + 1], acc[i][4 * q + 2], acc[i][4 * q + 3]);
+          for (int q = 0; q < WC / 4; ++q)
+            if (jc + 4 * q < d.Pp)
+              *reinterpret_cast<float4 *>(dst + 4 * q) =
+                  make_float4(acc[i][4 * q], acc[i][4 * q + 1], acc[i][4 * q + 2], acc[i][4 * q + 3]);
+        }
       }
     }
+    return;
   }
+  // split-K: partial tile [BR][BC] in smem (aliases the pipeline buffers), cluster-wide reduction
+  __syncthreads();
+  float *part = reinterpret_cast<float *>(dsm1);
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int q = 0; q < WC / 4; ++q)
+      *reinterpret_cast<float4 *>(part + (l + 32 * i) * BC + w * WC + 4 * q) =
+          wact ? make_float4(acc[i][4 * q], acc[i][4 * q + 1], acc[i][4 * q + 2], acc[i][4 * q + 3])
+               : make_float4(0.f, 0.f, 0.f, 0.f);
+  cg::cluster_group cl = cg::this_cluster();
+  cl.sync();
+  {
+    // this CTA (cluster rank sp) owns rows [sp·BR/S1, (sp+1)·BR/S1) of the tile
+    const int rows = BR / d.S1, rb = sp * rows;
+    const int ncol4 = min(BC, ((m - j0) + 3) & ~3) / 4;   // float4 groups holding active columns
+    for (int e = tid; e < rows * ncol4; e += OP_THREADS) {
+      const int rr = rb + e / ncol4, q = e % ncol4;
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int src = 0; src < d.S1; ++src) {   // fixed order: deterministic sum
+        const float4 x = *reinterpret_cast<const float4 *>(cl.map_shared_rank(part, src) + rr * BC + 4 * q);
+        v.x += x.x; v.y += x.y; v.z += x.z; v.w += x.w;
+      }
+      const int n = n0 + rr;
+      if (n < N && j0 + 4 * q < d.Pp) *reinterpret_cast<float4 *>(p.b.U + ((size_t)t * N + n) * d.Pp + j0 + 4 * q) = v;
+    }
+  }
+  cl.sync();
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -273,7 +321,7 @@ __global__ void __launch_bounds__(OP_THREADS, 2) k_stage2(KParams p) {
   Smem2 &sm = *reinterpret_cast<Smem2 *>(dsm2);
   const Dims &d = p.d;
   const int t = blockIdx.z, rt = blockIdx.y, ct = blockIdx.x, tid = threadIdx.x;
-  const int N = d.N, D = d.D, P = d.P, C = d.C, S1 = d.S1;
+  const int N = d.N, D = d.D, P = d.P, C = d.C;
   const float *__restrict__ phi = p.phi + (size_t)t * d.phi_task_stride;
   const int d0 = rt * BR;
   const int nk = (N + BK - 1) / BK;
@@ -302,10 +350,7 @@ __global__ void __launch_bounds__(OP_THREADS, 2) k_stage2(KParams p) {
     auto loadB = [&](int buf, int k0) {
       if (tid < BK * C) {
         const int kk = tid / C, c = tid % C;
-        double v = 0.0;
-        if (k0 + kk < N)
-          for (int s = 0; s < S1; ++s) v += p.b.Um[(((size_t)s * d.Tl + t) * N + k0 + kk) * C + c];
-        sm.Bm[buf][kk][c] = v;
+        sm.Bm[buf][kk][c] = (k0 + kk < N) ? p.b.Um[((size_t)t * N + k0 + kk) * C + c] : 0.0;
       }
     };
 #pragma unroll
@@ -371,32 +416,17 @@ __global__ void __launch_bounds__(OP_THREADS, 2) k_stage2(KParams p) {
   if (j0 >= m) return;
   const int w = tid >> 5, l = tid & 31;
   const bool wact = j0 + w * WC < m;
-  // B tile: Σ_s U_s[t][k0 + kk][j0 + 4q .. +3] → B[kk][4q..]; 384 float4: kk = idx / 24, q = idx % 24
-  float4 rb[2];
-  auto loadB = [&](int k0) {
+  // B tile: U[t][k0 + kk][j0 + 4q .. +3] → B[kk][4q..]  (cp.async; 384 float4: kk = idx / 24, q = idx % 24)
+  // columns ≥ m hold stale values: they only feed accumulators that are never stored
+  auto loadB = [&](int buf, int k0) {
 #pragma unroll
     for (int i = 0; i < 2; ++i) {
       const int idx = tid + i * OP_THREADS, kk = idx / (BC / 4), q = idx % (BC / 4);
-      const int n = k0 + kk, j = j0 + 4 * q;
-      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (idx < BK * BC / 4 && n < N && j < m) {
-        for (int s = 0; s < S1; ++s) {
-          const float4 x = ld4(p.b.U + (((size_t)s * d.Tl + t) * N + n) * d.Pp + j);
-          v.x += x.x; v.y += x.y; v.z += x.z; v.w += x.w;
-        }
-        // columns ≥ m inside the last float4 are stale: zero them
-        if (j + 1 >= m) v.y = 0.f;
-        if (j + 2 >= m) v.z = 0.f;
-        if (j + 3 >= m) v.w = 0.f;
+      if (idx < BK * BC / 4) {
+        const int n = k0 + kk, j = j0 + 4 * q;
+        const bool ok = n < N && j < d.Pp;
+        cp_async16(&sm.B[buf][kk][4 * q], ok ? p.b.U + ((size_t)t * N + n) * d.Pp + j : p.b.U, ok);
       }
-      rb[i] = v;
-    }
-  };
-  auto storeB = [&](int buf) {
-#pragma unroll
-    for (int i = 0; i < 2; ++i) {
-      const int idx = tid + i * OP_THREADS, kk = idx / (BC / 4), q = idx % (BC / 4);
-      if (idx < BK * BC / 4) *reinterpret_cast<float4 *>(&sm.B[buf][kk][4 * q]) = rb[i];
     }
   };
   float acc[4][WC];
@@ -406,14 +436,14 @@ __global__ void __launch_bounds__(OP_THREADS, 2) k_stage2(KParams p) {
     for (int c = 0; c < WC; ++c) acc[i][c] = 0.f;
 #pragma unroll
   for (int s = 0; s < ST - 1; ++s) {
-    if (s < nk) { loadA(s, s * BK); loadB(s * BK); storeB(s); }
+    if (s < nk) { loadA(s, s * BK); loadB(s, s * BK); }
     cp_commit();
   }
   for (int kc = 0; kc < nk; ++kc) {
     cp_wait<ST - 2>();
     __syncthreads();
     const int nx = kc + ST - 1;
-    if (nx < nk) { loadA(nx % ST, nx * BK); loadB(nx * BK); }
+    if (nx < nk) { loadA(nx % ST, nx * BK); loadB(nx % ST, nx * BK); }
     cp_commit();
     const int buf = kc % ST;
     if (wact) {
@@ -432,7 +462,6 @@ __global__ void __launch_bounds__(OP_THREADS, 2) k_stage2(KParams p) {
           for (int c = 0; c < WC; ++c) acc[i][c] = fmaf(av[i], b[c], acc[i][c]);
       }
     }
-    if (nx < nk) storeB(nx % ST);
   }
   cp_wait<0>();
   if (!wact) return;
@@ -476,9 +505,19 @@ cudaError_t launch_stage1(const KParams &p, const double *mu_src, bool mu_only, 
     if (e != cudaSuccess) return e;
     configured = smem;
   }
-  dim3 grid(p.d.nCT + 1, p.d.nRT1 * p.d.S1, p.d.Tl);
-  k_stage1<<<grid, OP_THREADS, smem, s>>>(p, mu_src ? mu_src : p.b.Dm, mu_only ? 1 : 0);
-  return cudaGetLastError();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(p.d.nCT + 1, p.d.nRT1 * p.d.S1, p.d.Tl);
+  cfg.blockDim = dim3(OP_THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 1;
+  attr[0].val.clusterDim.y = p.d.S1;   // the split-K CTAs of one output tile form a cluster
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k_stage1, p, mu_src ? mu_src : p.b.Dm, (int)(mu_only ? 1 : 0));
 }
 
 cudaError_t launch_stage2(const KParams &p, cudaStream_t s) {
