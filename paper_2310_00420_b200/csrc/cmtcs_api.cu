@@ -38,6 +38,9 @@ struct cmtcs_ctx {
   int64_t t_n[3];
   // the CG loop as one graph: WHILE(any column active) { stage1; stage2; update; advance }
   cudaStream_t cap_stream;
+  cudaStream_t side_stream;  // mean-column branch of the CG graph
+  cudaEvent_t fork_ev[2], join_ev[2];
+  TcMaps maps;
   cudaGraph_t cg_graph;
   cudaGraphExec_t cg_exec;
   int *h_u;                 // pinned: CG steps executed
@@ -86,6 +89,16 @@ struct Carver {
   }
 };
 
+TcCfg make_tc(const Dims &d) {
+  TcCfg tc;
+  tc.NT = std::min(TC_NTMAX, (d.P + 15) / 16 * 16);
+  tc.slot = (tc.NT + 31) / 32 * 32;
+  tc.nacc = std::max(1, std::min(4, 512 / (2 * tc.slot)));
+  tc.stage_bytes = 2u * 128u * 128u + 2u * (unsigned)tc.NT * 128u;
+  tc.stages = std::max(2, std::min(4, (int)((200u * 1024u) / tc.stage_bytes)));
+  return tc;
+}
+
 bool make_dims(const cmtcs_problem *p, Dims *d, char *why) {
   if (!p) { snprintf(why, 256, "problem is NULL"); return false; }
   if (p->T < 1 || p->N < 4 || p->D < 4 || p->C < 1 || p->K < 1) { snprintf(why, 256, "need T>=1, N>=4, D>=4, C>=1, K>=1"); return false; }
@@ -117,7 +130,8 @@ bool make_dims(const cmtcs_problem *p, Dims *d, char *why) {
   d->nw = (p->D + 63) / 64;
   d->nRT1 = (p->N + OP_BR - 1) / OP_BR;
   d->nRT2 = (p->D + OP_BR - 1) / OP_BR;
-  d->nCT = (d->P + OP_BC - 1) / OP_BC;
+  const int NT = std::min(TC_NTMAX, (d->P + 15) / 16 * 16);
+  d->nCT = (d->P + NT - 1) / NT;
   {
     // split the stage-1 contraction over D until ≥ 2 CTAs per SM exist; S1 ∈ {1, 2, 4, 8} (the
     // cluster of split CTAs reduces its 128-row tile by rows) and every split ≥ 128 long
@@ -126,7 +140,7 @@ bool make_dims(const cmtcs_problem *p, Dims *d, char *why) {
     int s1 = 1;
     while (s1 < 8 && base * s1 < 2L * sms && p->D / (2 * s1) >= 128) s1 *= 2;
     int k1 = (p->D + s1 - 1) / s1;
-    k1 = (k1 + OP_BK - 1) / OP_BK * OP_BK;
+    k1 = (k1 + 31) / 32 * 32;   // whole 32-wide K stages of the tensor-core pipeline
     d->K1 = k1;
     d->S1 = s1;
     if ((p->D + k1 - 1) / k1 != s1) { snprintf(why, 256, "internal: bad split of D=%d", p->D); return false; }
@@ -145,15 +159,22 @@ size_t carve(const Dims &d, char *base, Bufs *b) {
   b->logpi = cv.take<double>(C);
   b->b64 = cv.take<double>(Tl * D);
   b->bnorm2 = cv.take<double>(Tl);
+  const size_t mats = d.shared_phi ? 1 : Tl;
+  b->Phh = cv.take<float>(mats * N * D);
+  b->Phl = cv.take<float>(mats * N * D);
+  b->PTh = cv.take<float>(mats * N * D);
+  b->PTl = cv.take<float>(mats * N * D);
   b->X = cv.take<float>(Tl * P * D);
   b->R = cv.take<float>(Tl * P * D);
-  b->Dv = cv.take<float>(Tl * P * D);
+  b->Dh = cv.take<float>(Tl * P * D);
+  b->Dl = cv.take<float>(Tl * P * D);
   b->W = cv.take<float>(Tl * P * D);
   b->Xm = cv.take<double>(Tl * C * D);
   b->Rm = cv.take<double>(Tl * C * D);
   b->Dm = cv.take<double>(Tl * C * D);
   b->Wm = cv.take<double>(Tl * C * D);
-  b->U = cv.take<float>(Tl * N * d.Pp);
+  b->Uh = cv.take<float>(Tl * d.Pp * N);
+  b->Ul = cv.take<float>(Tl * d.Pp * N);
   b->Um = cv.take<double>(Tl * N * C);
   b->rr = cv.take<double>(Tl * P);
   b->rrm = cv.take<double>(Tl * C);
@@ -212,6 +233,40 @@ cmtcs_status set_alpha(cmtcs_ctx *c, const double *alpha) {
   return CMTCS_OK;
 }
 
+typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                  const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+// 2-D fp32 tensor map over a row-major [rows][cols] array, box 32 × box_rows, 128-byte swizzle
+bool encode_2d(EncodeTiledFn enc, CUtensorMap *m, const float *ptr, long rows, long cols, int box_rows) {
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)cols * 4};
+  cuuint32_t box[2] = {32, (cuuint32_t)box_rows};
+  cuuint32_t es[2] = {1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void *)ptr, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+             CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
+         CUDA_SUCCESS;
+}
+
+cmtcs_status encode_maps(cmtcs_ctx *c) {
+  void *fn = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  CUDA_OK(c, cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+  if (!fn || q != cudaDriverEntryPointSuccess) return fail(c, CMTCS_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  EncodeTiledFn enc = (EncodeTiledFn)fn;
+  const Dims &d = c->kp.d;
+  const Bufs &b = c->kp.b;
+  const long mats = d.shared_phi ? 1 : d.Tl;
+  bool ok = encode_2d(enc, &c->maps.phi_h, b.Phh, mats * d.N, d.D, OP_BR) &&
+            encode_2d(enc, &c->maps.phi_l, b.Phl, mats * d.N, d.D, OP_BR) &&
+            encode_2d(enc, &c->maps.phit_h, b.PTh, mats * d.D, d.N, OP_BR) &&
+            encode_2d(enc, &c->maps.phit_l, b.PTl, mats * d.D, d.N, OP_BR) &&
+            encode_2d(enc, &c->maps.u_h, b.Uh, (long)d.Tl * d.Pp, d.N, c->kp.tc.NT) &&
+            encode_2d(enc, &c->maps.u_l, b.Ul, (long)d.Tl * d.Pp, d.N, c->kp.tc.NT);
+  if (!ok) return fail(c, CMTCS_ECUDA, "cuTensorMapEncodeTiled failed");
+  return CMTCS_OK;
+}
+
 const char *status_name(int code) {
   switch (code) {
     case ST_BREAKDOWN: return "CG breakdown (d'Ad <= 0)";
@@ -219,6 +274,25 @@ const char *status_name(int code) {
     case ST_NUMERIC: return "non-finite ell / softmax of all -inf";
     default: return "unknown";
   }
+}
+
+// One CG step: [tensor-core stage 1 ‖ mean-column stage 1] → [stage 2 ‖ mean stage 2] → update → advance.
+// The mean-column (fp64 SIMT) kernels run on a forked stream (a parallel graph branch).
+cudaError_t enqueue_cg_step(cmtcs_ctx *c, cudaStream_t s, cudaStream_t side, unsigned long long cond) {
+  const KParams &kp = c->kp;
+  cudaError_t e;
+  for (int stg = 0; stg < 2; ++stg) {
+    if ((e = cudaEventRecord(c->fork_ev[stg], s)) != cudaSuccess) return e;
+    if ((e = cudaStreamWaitEvent(side, c->fork_ev[stg], 0)) != cudaSuccess) return e;
+    e = stg == 0 ? launch_mu_stage1(kp, nullptr, false, side) : launch_mu_stage2(kp, side);
+    if (e != cudaSuccess) return e;
+    e = stg == 0 ? launch_stage1_tc(kp, c->maps, s) : launch_stage2_tc(kp, c->maps, s);
+    if (e != cudaSuccess) return e;
+    if ((e = cudaEventRecord(c->join_ev[stg], side)) != cudaSuccess) return e;
+    if ((e = cudaStreamWaitEvent(s, c->join_ev[stg], 0)) != cudaSuccess) return e;
+  }
+  if ((e = launch_update(kp, s)) != cudaSuccess) return e;
+  return launch_advance(kp, cond, s);
 }
 
 cmtcs_status build_cg_graph(cmtcs_ctx *c) {
@@ -237,10 +311,7 @@ cmtcs_status build_cg_graph(cmtcs_ctx *c) {
   CUDA_OK(c, cudaGraphAddNode(&node, g, nullptr, 0, &cp));
   cudaGraph_t body = cp.conditional.phGraph_out[0];
   CUDA_OK(c, cudaStreamBeginCaptureToGraph(c->cap_stream, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
-  cudaError_t e1 = launch_stage1(kp, nullptr, false, c->cap_stream);
-  cudaError_t e2 = e1 == cudaSuccess ? launch_stage2(kp, c->cap_stream) : e1;
-  cudaError_t e3 = e2 == cudaSuccess ? launch_update(kp, c->cap_stream) : e2;
-  cudaError_t e4 = e3 == cudaSuccess ? launch_advance(kp, (unsigned long long)h, c->cap_stream) : e3;
+  cudaError_t e4 = enqueue_cg_step(c, c->cap_stream, c->side_stream, (unsigned long long)h);
   cudaGraph_t captured = body;
   CUDA_OK(c, cudaStreamEndCapture(c->cap_stream, &captured));
   CUDA_OK(c, e4);
@@ -273,10 +344,7 @@ cmtcs_status one_em_iteration(cmtcs_ctx *c, const uint64_t *probe_bits, const do
     // profiling mode (CMTCS_NO_GRAPH=1): the same kernels launched from a host loop so that
     // per-launch tools (ncu) see them; convergence is checked every 8 steps
     for (int u = 0; u < d.cap; ++u) {
-      CUDA_OK(c, launch_stage1(kp, nullptr, false, s));
-      CUDA_OK(c, launch_stage2(kp, s));
-      CUDA_OK(c, launch_update(kp, s));
-      CUDA_OK(c, launch_advance(kp, 0ull, s));
+      CUDA_OK(c, enqueue_cg_step(c, s, c->side_stream, 0ull));
       if ((u & 7) == 7 || u + 1 == d.cap) {
         CUDA_OK(c, cudaMemcpyAsync(c->h_u, kp.b.alive + u, sizeof(int), cudaMemcpyDeviceToHost, s));
         CUDA_OK(c, cudaStreamSynchronize(s));
@@ -295,7 +363,7 @@ cmtcs_status one_em_iteration(cmtcs_ctx *c, const uint64_t *probe_bits, const do
   CUDA_OK(c, launch_diag(kp, s));
   CUDA_OK(c, launch_lanczos(kp.b.gam, kp.b.xi, kp.b.steps, d.Tl * d.P, d.cap, d.D, kp.b.tau, nullptr,
                             kp.b.status, s));
-  CUDA_OK(c, launch_stage1(kp, kp.b.Xm, true, s));
+  CUDA_OK(c, launch_mu_stage1(kp, kp.b.Xm, true, s));
   CUDA_OK(c, launch_estep_finish(kp, s));
   // ---- M-step (Eq. 4): local sums → all-reduce over ranks → α update ----
   CUDA_OK(c, launch_mstep_partial(kp, s));
@@ -324,8 +392,8 @@ cmtcs_status one_em_iteration(cmtcs_ctx *c, const uint64_t *probe_bits, const do
   c->launches += L;
   c->have_estep = true;
   const int steps_run = *c->h_u;
-  L += 4 * (int64_t)steps_run;  // stage1, stage2, update, advance per CG step inside the graph
-  c->launches += 4 * (int64_t)steps_run;
+  L += 6 * (int64_t)steps_run;  // stage1 (tc, mean), stage2 (tc, mean), update, advance per CG step
+  c->launches += 6 * (int64_t)steps_run;
   if (tm) {
     // per CG step: %globaltimer stamps of the first stage-1 CTA entry, the last stage-2 CTA exit
     // and the last update-warp exit (device clock, ns)
@@ -429,6 +497,7 @@ cmtcs_status cmtcs_init(cmtcs_ctx **out, const cmtcs_problem *p, const float *ph
   carve(d, (char *)workspace, &b);
   c->kp.d = d;
   c->kp.b = b;
+  c->kp.tc = make_tc(d);
   c->kp.phi = phi;
   c->kp.y = y;
   c->kp.beta = p->beta;
@@ -442,6 +511,11 @@ cmtcs_status cmtcs_init(cmtcs_ctx **out, const cmtcs_problem *p, const float *ph
   CUDA_OK(c, cudaMallocHost((void **)&c->h_out, 32 * sizeof(double)));
   CUDA_OK(c, cudaMallocHost((void **)&c->h_status, 8 * sizeof(int)));
   CUDA_OK(c, cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking));
+  CUDA_OK(c, cudaStreamCreateWithFlags(&c->side_stream, cudaStreamNonBlocking));
+  for (int i = 0; i < 2; ++i) {
+    CUDA_OK(c, cudaEventCreateWithFlags(&c->fork_ev[i], cudaEventDisableTiming));
+    CUDA_OK(c, cudaEventCreateWithFlags(&c->join_ev[i], cudaEventDisableTiming));
+  }
   CUDA_OK(c, cudaMallocHost((void **)&c->h_u, sizeof(int)));
   CUDA_OK(c, cudaMallocHost((void **)&c->h_ts, sizeof(unsigned long long) * 4 * d.cap));
   for (int i = 0; i < 3; ++i) CUDA_OK(c, cudaEventCreate(&c->tev[i]));
@@ -456,7 +530,12 @@ cmtcs_status cmtcs_init(cmtcs_ctx **out, const cmtcs_problem *p, const float *ph
   cmtcs_status st = set_alpha(c, alpha0);
   if (st != CMTCS_OK) { c->broken = true; return st; }
   CUDA_OK(c, launch_rhs(c->kp, c->stream));
-  c->launches += 3;
+  CUDA_OK(c, launch_split_phi(c->kp, c->stream));
+  c->launches += 4;
+  {
+    cmtcs_status st2 = encode_maps(c);
+    if (st2 != CMTCS_OK) return st2;
+  }
   CUDA_OK(c, cudaStreamSynchronize(c->stream));
   if (world > 1) {
     ncclUniqueId id;
@@ -540,6 +619,11 @@ void cmtcs_destroy(cmtcs_ctx *c) {
   if (c->cg_exec) cudaGraphExecDestroy(c->cg_exec);
   if (c->cg_graph) cudaGraphDestroy(c->cg_graph);
   if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
+  if (c->side_stream) cudaStreamDestroy(c->side_stream);
+  for (int i = 0; i < 2; ++i) {
+    if (c->fork_ev[i]) cudaEventDestroy(c->fork_ev[i]);
+    if (c->join_ev[i]) cudaEventDestroy(c->join_ev[i]);
+  }
   for (int i = 0; i < 3; ++i)
     if (c->tev[i]) cudaEventDestroy(c->tev[i]);
   if (c->h_u) cudaFreeHost(c->h_u);

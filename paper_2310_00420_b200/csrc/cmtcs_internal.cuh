@@ -1,6 +1,7 @@
 // Internal declarations shared by the libcmtcs translation units (not part of the C ABI).
 #pragma once
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -9,10 +10,11 @@
 namespace cmtcs {
 
 constexpr int MAXC = 16;        // clusters supported by the fp64 mean-column tiles
-constexpr int OP_BR = 128;      // operator CTA tile: rows (N in stage 1, D in stage 2)
-constexpr int OP_BC = 96;       // operator CTA tile: probe columns (8 warps x 12)
-constexpr int OP_BK = 16;       // contraction chunk
-constexpr int OP_THREADS = 256;
+constexpr int OP_BR = 128;      // operator tile rows (N in stage 1, D in stage 2)
+constexpr int OP_BK = 16;       // mean-column (SIMT) contraction chunk
+constexpr int OP_THREADS = 256; // mean-column kernels
+constexpr int TC_THREADS = 128; // tensor-core probe kernels (4 warps = 128 TMEM lanes)
+constexpr int TC_NTMAX = 256;   // widest probe-column tile (MMA N ≤ 256)
 constexpr int UPD_THREADS = 256;  // 8 warps = 8 columns per CTA
 
 // Sizes of one rank's problem.  Column index of probe (c, k) inside a task: col = c*K + k.
@@ -24,7 +26,7 @@ struct Dims {
   int nw;    // 64-bit probe words per column = ceil(D/64)
   int nRT1;  // stage-1 row tiles  = ceil(N / OP_BR)
   int nRT2;  // stage-2 row tiles  = ceil(D / OP_BR)
-  int nCT;   // probe column tiles = ceil(P / OP_BC)
+  int nCT;   // probe column tiles = ceil(P / TcCfg::NT)
   int S1;    // stage-1 split-K factor (fills the GPU when T·N is small)
   int K1;    // stage-1 contraction length per split (multiple of OP_BK)
   int shared_phi;
@@ -39,9 +41,12 @@ struct Bufs {
   double *logpi;     // [C]
   double *b64;       // [Tl][D]   βΦᵀy
   double *bnorm2;    // [Tl]      ‖b‖²
-  float *X, *R, *Dv, *W;     // probe columns [Tl][P][D]
+  float *X, *R, *W;  // probe columns [Tl][P][D]
+  float *Dh, *Dl;    // probe directions d = Dh + Dl exactly (Dh = tf32(d)) [Tl][P][D]
+  float *Phh, *Phl;  // Φ split: tf32 hi + fp32 lo   [Tl or 1][N][D]
+  float *PTh, *PTl;  // Φᵀ split                     [Tl or 1][D][N]
   double *Xm, *Rm, *Dm, *Wm; // mean columns  [Tl][C][D]
-  float *U;          // [Tl][N][Pp]  stage-1 output (compacted column order)
+  float *Uh, *Ul;    // stage-1 output split, [Tl][Pp][N] (row = compacted column j)
   double *Um;        // [Tl][N][C]
   double *rr;        // [Tl][P]
   double *rrm;       // [Tl][C]
@@ -71,9 +76,26 @@ struct Bufs {
   int *assign;       // [Tl]
 };
 
+// tensor-core operator configuration (chosen at init from P)
+struct TcCfg {
+  int NT;            // column tile width (multiple of 16, ≤ 256)
+  int slot;          // TMEM columns per accumulator (NT rounded up to 32)
+  int nacc;          // K-split accumulator pairs (2·nacc·slot ≤ 512)
+  int stages;        // smem pipeline depth
+  unsigned stage_bytes;
+};
+
+// TMA descriptors (host-encoded, passed as __grid_constant__ kernel parameters)
+struct TcMaps {
+  CUtensorMap phi_h, phi_l;    // [rows Tl·N][cols D], box 32 × 128
+  CUtensorMap phit_h, phit_l;  // [rows Tl·D][cols N], box 32 × 128
+  CUtensorMap u_h, u_l;        // [rows Tl·Pp][cols N], box 32 × NT
+};
+
 struct KParams {
   Dims d;
   Bufs b;
+  TcCfg tc;
   const float *phi;
   const float *y;
   double beta;
@@ -88,8 +110,12 @@ struct KParams {
 
 // launchers (return cudaGetLastError())
 cudaError_t launch_init_columns(const KParams &p, cudaStream_t s);
-cudaError_t launch_stage1(const KParams &p, const double *mu_src, bool mu_only, cudaStream_t s);
-cudaError_t launch_stage2(const KParams &p, cudaStream_t s);
+cudaError_t launch_stage1_tc(const KParams &p, const TcMaps &maps, cudaStream_t s);
+cudaError_t launch_stage2_tc(const KParams &p, const TcMaps &maps, cudaStream_t s);
+cudaError_t launch_split_phi(const KParams &p, cudaStream_t s);
+size_t tc_smem_bytes(const TcCfg &tc, int P);
+cudaError_t launch_mu_stage1(const KParams &p, const double *mu_src, bool mu_only, cudaStream_t s);
+cudaError_t launch_mu_stage2(const KParams &p, cudaStream_t s);
 cudaError_t launch_update(const KParams &p, cudaStream_t s);
 cudaError_t launch_advance(const KParams &p, unsigned long long cond_handle, cudaStream_t s);
 cudaError_t launch_rhs(const KParams &p, cudaStream_t s);

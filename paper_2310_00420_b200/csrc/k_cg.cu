@@ -26,6 +26,12 @@ __device__ __forceinline__ uint64_t probe_word(uint64_t seed, uint64_t w) {
   return mix64(seed + (w + 1ull) * 0x9E3779B97F4A7C15ull);
 }
 
+__device__ __forceinline__ float tf32_rn(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;\n" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
+
 __device__ __forceinline__ double block_sum(double v, double *sh) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
 #pragma unroll
@@ -77,7 +83,8 @@ __global__ void k_init_columns(KParams p) {
       const float v = ((wd >> (i & 63)) & 1ull) ? -1.f : 1.f;
       p.b.X[base + i] = 0.f;
       p.b.R[base + i] = v;
-      p.b.Dv[base + i] = v;
+      p.b.Dh[base + i] = v;     // ±1 is exact in tf32
+      p.b.Dl[base + i] = 0.f;
     }
     if (threadIdx.x == 0) {
       const size_t g = (size_t)t * d.P + slot;
@@ -144,12 +151,14 @@ __global__ void __launch_bounds__(UPD_THREADS) k_update(KParams p) {
     const double gam = rr / dAd;
     float4 *x4 = reinterpret_cast<float4 *>(p.b.X + g * d.D);
     float4 *r4 = reinterpret_cast<float4 *>(p.b.R + g * d.D);
-    float4 *d4 = reinterpret_cast<float4 *>(p.b.Dv + g * d.D);
+    float4 *dh4 = reinterpret_cast<float4 *>(p.b.Dh + g * d.D);
+    float4 *dl4 = reinterpret_cast<float4 *>(p.b.Dl + g * d.D);
     const float4 *w4 = reinterpret_cast<const float4 *>(p.b.W + g * d.D);
     const int n4 = d.D >> 2;
     double acc = 0.0;
     for (int i = lane; i < n4; i += 32) {
-      const float4 dv = d4[i], wv = w4[i];
+      const float4 dh = dh4[i], dl = dl4[i], wv = w4[i];
+      const float4 dv = make_float4(dh.x + dl.x, dh.y + dl.y, dh.z + dl.z, dh.w + dl.w);  // exact
       float4 xv = x4[i], rv = r4[i];
       xv.x = (float)fma(gam, (double)dv.x, (double)xv.x);
       xv.y = (float)fma(gam, (double)dv.y, (double)xv.y);
@@ -177,13 +186,17 @@ __global__ void __launch_bounds__(UPD_THREADS) k_update(KParams p) {
     }
     if (!stop) {
       for (int i = lane; i < n4; i += 32) {
-        const float4 rv = r4[i];
-        float4 dv = d4[i];
+        const float4 rv = r4[i], dh = dh4[i], dl = dl4[i];
+        float4 dv = make_float4(dh.x + dl.x, dh.y + dl.y, dh.z + dl.z, dh.w + dl.w);
         dv.x = (float)fma(xi, (double)dv.x, (double)rv.x);
         dv.y = (float)fma(xi, (double)dv.y, (double)rv.y);
         dv.z = (float)fma(xi, (double)dv.z, (double)rv.z);
         dv.w = (float)fma(xi, (double)dv.w, (double)rv.w);
-        d4[i] = dv;
+        // store d_{u+1} as the exact pair (tf32(d), d − tf32(d)) the tensor-core operator reads
+        float4 h4;
+        h4.x = tf32_rn(dv.x); h4.y = tf32_rn(dv.y); h4.z = tf32_rn(dv.z); h4.w = tf32_rn(dv.w);
+        dh4[i] = h4;
+        dl4[i] = make_float4(dv.x - h4.x, dv.y - h4.y, dv.z - h4.z, dv.w - h4.w);
       }
     }
   } else if (slot < d.P + d.C) {
