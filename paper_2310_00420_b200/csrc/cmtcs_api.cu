@@ -95,7 +95,7 @@ TcCfg make_tc(const Dims &d) {
   tc.slot = (tc.NT + 31) / 32 * 32;
   tc.nacc = std::max(1, std::min(4, 512 / (2 * tc.slot)));
   tc.stage_bytes = 2u * 128u * 128u + 2u * (unsigned)tc.NT * 128u;
-  tc.stages = std::max(2, std::min(4, (int)((200u * 1024u) / tc.stage_bytes)));
+  tc.stages = std::max(2, std::min(4, (int)((212u * 1024u) / tc.stage_bytes)));
   return tc;
 }
 

@@ -138,7 +138,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   const int nk = (ke - kb + TK - 1) / TK;
   const int arow = (d.shared_phi ? 0 : t * N) + n0;
   const uint32_t b_bytes = (uint32_t)tc.NT * 128;
-  const int slot = tc.slot, nacc = tc.nacc, S = tc.stages;
+  const int slot = tc.slot, nacc = min(tc.nacc, nk), S = tc.stages;  // every pair gets ≥ 1 chunk
   if (tid == 0) {
     for (int s = 0; s < S; ++s) { mbar_init(&tl.full[s], 1); mbar_init(&tl.empty[s], 1); }
     fence_mbar_init();
@@ -272,7 +272,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   const int arow = (d.shared_phi ? 0 : t * D) + d0;
   const int brow = t * d.Pp + j0;
   const uint32_t b_bytes = (uint32_t)tc.NT * 128;
-  const int slot = tc.slot, nacc = tc.nacc, S = tc.stages;
+  const int slot = tc.slot, nacc = min(tc.nacc, nk), S = tc.stages;  // every pair gets ≥ 1 chunk
   for (int j = tid; j < ncol; j += TC_THREADS) tl.act[j] = p.b.act[(size_t)t * P + j0 + j];
   if (tid == 0) {
     for (int s = 0; s < S; ++s) { mbar_init(&tl.full[s], 1); mbar_init(&tl.empty[s], 1); }
@@ -322,30 +322,42 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   mbar_wait(&tl.empty[(nk - 1) % S], ((nk - 1) / S) & 1);
   fence_after_sync();
 
-  // epilogue: W = β acc + α_c ⊙ d for row dd, fp64 partial dᵀW per column (this 128-row tile)
+  // epilogue: W = β acc + α_c ⊙ d for row dd, fp64 partial dᵀW per column (this 128-row tile).
+  // Per group of 16 columns all global loads are issued first, then the math, then the 16
+  // independent warp reductions (latency overlap instead of one dependent chain per column).
   const int r = warp * 32 + (tid & 31);
   const int dd = d0 + r;
   const bool rv = dd < D;
-  const double beta = p.beta;
+  const float betaf = (float)p.beta;
   for (int c0 = 0; c0 < nmma; c0 += 16) {
-    float tot[16];
-    acc_load16(tmem, warp, c0, nacc, slot, tot);
+    float tot[16], dh[16], dl[16], al[16];
+    size_t off[16];
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
       const int jj = c0 + i;
-      double dot = 0.0;
-      if (jj < ncol && rv) {
-        const int col = tl.act[jj];
-        const size_t o = ((size_t)t * P + col) * D + dd;
-        const float dv = p.b.Dh[o] + p.b.Dl[o];
-        const float w = fmaf((float)beta, tot[i], p.b.alpha32[(size_t)(col / d.K) * D + dd] * dv);
-        p.b.W[o] = w;
-        dot = (double)dv * (double)w;
-      }
-#pragma unroll
-      for (int o2 = 16; o2; o2 >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o2);
-      if ((tid & 31) == 0) tl.red[warp][jj] = dot;
+      const bool ok = jj < ncol && rv;
+      const int col = ok ? tl.act[jj] : 0;
+      off[i] = ((size_t)t * P + col) * D + dd;
+      dh[i] = ok ? p.b.Dh[off[i]] : 0.f;
+      dl[i] = ok ? p.b.Dl[off[i]] : 0.f;
+      al[i] = ok ? p.b.alpha32[(size_t)(col / d.K) * D + dd] : 0.f;
     }
+    acc_load16(tmem, warp, c0, nacc, slot, tot);
+    double dot[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const float dv = dh[i] + dl[i];
+      const float w = fmaf(betaf, tot[i], al[i] * dv);
+      if (c0 + i < ncol && rv) p.b.W[off[i]] = w;
+      dot[i] = (double)dv * (double)w;
+    }
+#pragma unroll
+    for (int o2 = 16; o2; o2 >>= 1)
+#pragma unroll
+      for (int i = 0; i < 16; ++i) dot[i] += __shfl_xor_sync(0xffffffffu, dot[i], o2);
+    if ((tid & 31) == 0)
+#pragma unroll
+      for (int i = 0; i < 16; ++i) tl.red[warp][c0 + i] = dot[i];
   }
   fence_before_sync();
   __syncthreads();
