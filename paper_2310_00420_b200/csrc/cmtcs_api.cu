@@ -133,12 +133,13 @@ bool make_dims(const cmtcs_problem *p, Dims *d, char *why) {
   const int NT = std::min(TC_NTMAX, (d->P + 15) / 16 * 16);
   d->nCT = (d->P + NT - 1) / NT;
   {
-    // split the stage-1 contraction over D until ≥ 2 CTAs per SM exist; S1 ∈ {1, 2, 4, 8} (the
-    // cluster of split CTAs reduces its 128-row tile by rows) and every split ≥ 128 long
+    // split the stage-1 contraction over D while the grid still fits one wave of 148 SMs (the
+    // tensor-core CTAs run one per SM); S1 ∈ {1, 2, 4, 8} (the cluster of split CTAs reduces its
+    // 128-row tile by rows) and every split keeps ≥ 128 of D
     const int sms = 148;
     const long base = (long)d->nCT * d->nRT1 * (p->task_end - p->task_begin);
     int s1 = 1;
-    while (s1 < 8 && base * s1 < 2L * sms && p->D / (2 * s1) >= 128) s1 *= 2;
+    while (s1 < 8 && base * s1 * 2 <= sms && p->D / (2 * s1) >= 128) s1 *= 2;
     int k1 = (p->D + s1 - 1) / s1;
     k1 = (k1 + 31) / 32 * 32;   // whole 32-wide K stages of the tensor-core pipeline
     d->K1 = k1;
