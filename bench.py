@@ -52,6 +52,14 @@ def fp32_peak_tflops(sm_mhz):
     return SM_COUNT * FP32_LANES_PER_SM * 2 * sm_mhz * 1e6 / 1e12
 
 
+def tf32x3_peak_tflops(peaks):
+    """fp32-equivalent peak of the 3xTF32 tensor-core operator: measured dense bf16 × (tf32/bf16 =
+    1.1/2.25 nominal, B200_PROFILING.md) ÷ 3 MMAs per product.  Burst figure: the operator kernels
+    are timed individually (device stamps), sustained is reported alongside."""
+    ratio = 1.1 / 2.25
+    return peaks["bf16_tflops"] * ratio / 3.0, peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"]) * ratio / 3.0
+
+
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -303,8 +311,12 @@ def cuda_arm(args):
     achieved_op = flops_rank / (op_ms_rank * 1e-3) / 1e12 if op_ms_rank > 0 else 0.0
     achieved_op = max_over_ranks(achieved_op) if world == 1 else sum_over_ranks(achieved_op) / world
     peaks, peaks_kind = measured_peaks()
-    peak = fp32_peak_tflops(peaks.get("sm_max_mhz", SM_MAX_MHZ))
-    em_roof_frac = (flops_all / world / (peak * 1e12)) / (total_ms * 1e-3 / args.steps * args.steps)
+    peak, peak_sust = tf32x3_peak_tflops(peaks)
+    # EM-step roofline (north_star): slower of Φ bytes at HBM bandwidth and FLOPs at peak, per CG step
+    steps_total = sum(i["cg_iters"] for i in infos)
+    phi_bytes = 4.0 * cfg.N * cfg.D * (1 if cfg.shared_phi else (e - b)) * steps_total
+    t_roof = max(flops_rank / (peak * 1e12), phi_bytes / (peaks["hbm_gbs"] * 1e9))
+    em_roof_frac = max_over_ranks(t_roof) / (total_ms * 1e-3)
 
     # ------------------------------ end to end through the public API (host buffers) --------
     e2e = None
@@ -345,7 +357,8 @@ def cuda_arm(args):
                 "T": cfg.T, "C": cfg.C, "N": cfg.N, "D": cfg.D, "K": cfg.K, "cg_cap": cfg.cg_cap,
                 "cg_tol": cfg.cg_tol, "em_iters_timed": f"{it0}..{it0 + args.steps - 1}",
                 "parallelism": f"task-sharded dp{world}" if world > 1 else "single GPU",
-                "precision": "probe columns f32 FFMA with f64 dots/scalars; mean columns, log-det, q, M-step f64",
+                "precision": "probe columns: fp32 vectors, operator on tcgen05 tensor cores as 3xTF32 "
+                             "(fp32-accurate), fp64 dots/scalars; mean columns, log-det, q, M-step fp64",
                 "l2": "flushed (zero-fill of 2xL2) between timed EM iterations",
                 "cg_steps_per_em_iter": [i["cg_iters"] for i in infos],
                 "active_col_iters_per_em_iter": [i["probe_col_iters"] + i["mean_col_iters"] for i in infos],
@@ -355,11 +368,13 @@ def cuda_arm(args):
                 "update_share_of_step": tm["update_ms"] / max(sum(step_ms), 1e-9),
                 "wall_s_timed": wall,
             },
-            "roofline": {"bound": "alu", "achieved": achieved_op, "peak": peak, "unit": "TFLOP/s",
+            "roofline": {"bound": "tensor", "achieved": achieved_op, "peak": peak, "unit": "TFLOP/s",
                          "frac": achieved_op / peak, "traffic": ncu_traffic(cfg.name),
-                         "kernel": "K1 operator (k_stage1 + k_stage2 launch pair per CG step)",
-                         "peak_source": f"derived: 148 SM x 128 FP32 lanes x 2 x {peaks.get('sm_max_mhz', SM_MAX_MHZ):.0f} MHz "
-                                        f"(sm_max_mhz of {peaks_kind} MEASURED_PEAKS.json); FFMA has no measured peak there"},
+                         "kernel": "K1 operator: k_stage1_tc + k_stage2_tc (tcgen05 3xTF32) per CG step, "
+                                   "achieved = algorithmic fp32 flop 4*N*D per active column / device-stamped duration",
+                         "peak_source": f"{peaks_kind} MEASURED_PEAKS.json bf16 {peaks['bf16_tflops']} TF/s x (1.1/2.25 "
+                                        f"tf32/bf16 nominal) / 3 passes; sustained-clock figure {peak_sust:.1f}",
+                         "fp32_ffma_peak": fp32_peak_tflops(peaks.get("sm_max_mhz", SM_MAX_MHZ))},
             "gpu_launches": int(launches),
             "clocks": clocks,
         }

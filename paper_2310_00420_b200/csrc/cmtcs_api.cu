@@ -95,7 +95,9 @@ TcCfg make_tc(const Dims &d) {
   tc.slot = (tc.NT + 31) / 32 * 32;
   tc.nacc = std::max(1, std::min(4, 512 / (2 * tc.slot)));
   tc.stage_bytes = 2u * 128u * 128u + 2u * (unsigned)tc.NT * 128u;
-  tc.stages = std::max(2, std::min(4, (int)((212u * 1024u) / tc.stage_bytes)));
+  // ≤ ~170 KB of ring so a mean-column CTA (≤ 37 KB) co-resides with a tensor-core CTA, whose
+  // 512 TMEM columns and > 114 KB of smem already pin it to one per SM
+  tc.stages = std::max(2, std::min(4, (int)((170u * 1024u) / tc.stage_bytes)));
   return tc;
 }
 

@@ -42,9 +42,42 @@ struct TcSmemTail {
   uint64_t full[MAXST], empty[MAXST];
   uint32_t tslot;
   int m;
-  int act[256];      // the tile's active columns
+  int act[256];        // the tile's active columns
+  long long off[256];  // stage 2: element offset of column j's vectors, ((t·P + col)·D)
+  int aoff[256];       // stage 2: offset of the column's α row, c·D
   double red[4][256];
 };
+
+// Sums v[0..15] over the 32 lanes of a warp with 16 shuffles (butterfly transpose-reduce); the
+// total of value index `idx` ends in the even lane with idx = bits 4..1 of the lane id.
+__device__ __forceinline__ double warp_reduce16(double *v, int lane, int *idx) {
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const bool up = lane & 16;
+    const double send = up ? v[i] : v[i + 8], keep = up ? v[i + 8] : v[i];
+    v[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const bool up = lane & 8;
+    const double send = up ? v[i] : v[i + 4], keep = up ? v[i + 4] : v[i];
+    v[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+  }
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const bool up = lane & 4;
+    const double send = up ? v[i] : v[i + 2], keep = up ? v[i + 2] : v[i];
+    v[i] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+  }
+  {
+    const bool up = lane & 2;
+    const double send = up ? v[0] : v[1], keep = up ? v[1] : v[0];
+    v[0] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
+  }
+  v[0] += __shfl_xor_sync(0xffffffffu, v[0], 1);
+  *idx = ((lane >> 4) & 1) * 8 + ((lane >> 3) & 1) * 4 + ((lane >> 2) & 1) * 2 + ((lane >> 1) & 1);
+  return v[0];
+}
 
 __device__ __forceinline__ unsigned char *stage_base(unsigned char *sm, int st, uint32_t stage_bytes) {
   return sm + (size_t)st * stage_bytes;
@@ -273,7 +306,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   const int brow = t * d.Pp + j0;
   const uint32_t b_bytes = (uint32_t)tc.NT * 128;
   const int slot = tc.slot, nacc = min(tc.nacc, nk), S = tc.stages;  // every pair gets ≥ 1 chunk
-  for (int j = tid; j < ncol; j += TC_THREADS) tl.act[j] = p.b.act[(size_t)t * P + j0 + j];
+  for (int j = tid; j < ncol; j += TC_THREADS) {
+    const int col = p.b.act[(size_t)t * P + j0 + j];
+    tl.act[j] = col;
+    tl.off[j] = ((long long)t * P + col) * D;
+    tl.aoff[j] = (col / d.K) * D;
+  }
   if (tid == 0) {
     for (int s = 0; s < S; ++s) { mbar_init(&tl.full[s], 1); mbar_init(&tl.empty[s], 1); }
     fence_mbar_init();
@@ -329,18 +367,16 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   const int dd = d0 + r;
   const bool rv = dd < D;
   const float betaf = (float)p.beta;
+  const int lane = tid & 31;
   for (int c0 = 0; c0 < nmma; c0 += 16) {
     float tot[16], dh[16], dl[16], al[16];
-    size_t off[16];
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
-      const int jj = c0 + i;
-      const bool ok = jj < ncol && rv;
-      const int col = ok ? tl.act[jj] : 0;
-      off[i] = ((size_t)t * P + col) * D + dd;
-      dh[i] = ok ? p.b.Dh[off[i]] : 0.f;
-      dl[i] = ok ? p.b.Dl[off[i]] : 0.f;
-      al[i] = ok ? p.b.alpha32[(size_t)(col / d.K) * D + dd] : 0.f;
+      const bool ok = c0 + i < ncol && rv;
+      const long long o = ok ? tl.off[c0 + i] + dd : 0;
+      dh[i] = ok ? p.b.Dh[o] : 0.f;
+      dl[i] = ok ? p.b.Dl[o] : 0.f;
+      al[i] = ok ? p.b.alpha32[tl.aoff[c0 + i] + dd] : 0.f;
     }
     acc_load16(tmem, warp, c0, nacc, slot, tot);
     double dot[16];
@@ -348,16 +384,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     for (int i = 0; i < 16; ++i) {
       const float dv = dh[i] + dl[i];
       const float w = fmaf(betaf, tot[i], al[i] * dv);
-      if (c0 + i < ncol && rv) p.b.W[off[i]] = w;
+      if (c0 + i < ncol && rv) p.b.W[tl.off[c0 + i] + dd] = w;
       dot[i] = (double)dv * (double)w;
     }
-#pragma unroll
-    for (int o2 = 16; o2; o2 >>= 1)
-#pragma unroll
-      for (int i = 0; i < 16; ++i) dot[i] += __shfl_xor_sync(0xffffffffu, dot[i], o2);
-    if ((tid & 31) == 0)
-#pragma unroll
-      for (int i = 0; i < 16; ++i) tl.red[warp][c0 + i] = dot[i];
+    int idx;
+    const double sum = warp_reduce16(dot, lane, &idx);
+    if ((lane & 1) == 0) tl.red[warp][c0 + idx] = sum;
   }
   fence_before_sync();
   __syncthreads();
