@@ -336,3 +336,23 @@ def test_single_step_config2(torch_cuda):
     assert conv.any() and e["s_conv"] <= S_TOL
     assert np.all(np.abs(post["logdet"] - orc["nu"]) <= nu_tol(orc["nu"]))
     assert e["L_abs"] <= L_TOL
+
+
+def test_task_shards_match_whole(torch_cuda):
+    """Two contexts holding tasks [0, 2) and [2, 4) of config 1 (the per-rank view of a 2-GPU run,
+    here on one GPU without NCCL) produce the same E-step as one context holding all 4 tasks."""
+    cfg = synthetic.CONFIGS[1]
+    data = synthetic.generate(cfg)
+    alpha = np.random.default_rng(4).uniform(0.5, 2.0, (cfg.C, cfg.D))
+    whole = make_gpu(data, alpha=alpha, em_iter0=5, cap=256)
+    whole.em_step(1)
+    pw = to_np(whole.posterior())
+    whole.close()
+    for b, e in [(0, 2), (2, 4)]:
+        part = synthetic.generate(cfg, range(b, e))
+        g = make_gpu(part, alpha=alpha, em_iter0=5, cap=256, T=cfg.T, task_begin=b)
+        g.em_step(1)
+        pp = to_np(g.posterior())
+        g.close()
+        for k in ("mu", "s", "logdet", "q"):
+            np.testing.assert_allclose(pp[k], pw[k][b:e], rtol=1e-12, atol=1e-12)
