@@ -45,6 +45,8 @@ struct cmtcs_ctx {
   cudaGraphExec_t cg_exec;
   int *h_u;                 // pinned: CG steps executed
   bool no_graph;            // CMTCS_NO_GRAPH=1: host-launched CG steps (for per-launch profilers)
+  bool serial_mean;         // CMTCS_SERIAL_MEAN=1: mean-column kernels on the main stream (no fork)
+  int unroll;               // CMTCS_GRAPH_UNROLL: CG steps per iteration of the WHILE body
 };
 
 namespace {
@@ -285,6 +287,13 @@ cudaError_t enqueue_cg_step(cmtcs_ctx *c, cudaStream_t s, cudaStream_t side, uns
   const KParams &kp = c->kp;
   cudaError_t e;
   for (int stg = 0; stg < 2; ++stg) {
+    if (c->serial_mean) {
+      e = stg == 0 ? launch_mu_stage1(kp, nullptr, false, s) : launch_mu_stage2(kp, s);
+      if (e != cudaSuccess) return e;
+      e = stg == 0 ? launch_stage1_tc(kp, c->maps, s) : launch_stage2_tc(kp, c->maps, s);
+      if (e != cudaSuccess) return e;
+      continue;
+    }
     if ((e = cudaEventRecord(c->fork_ev[stg], s)) != cudaSuccess) return e;
     if ((e = cudaStreamWaitEvent(side, c->fork_ev[stg], 0)) != cudaSuccess) return e;
     e = stg == 0 ? launch_mu_stage1(kp, nullptr, false, side) : launch_mu_stage2(kp, side);
@@ -314,7 +323,9 @@ cmtcs_status build_cg_graph(cmtcs_ctx *c) {
   CUDA_OK(c, cudaGraphAddNode(&node, g, nullptr, 0, &cp));
   cudaGraph_t body = cp.conditional.phGraph_out[0];
   CUDA_OK(c, cudaStreamBeginCaptureToGraph(c->cap_stream, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
-  cudaError_t e4 = enqueue_cg_step(c, c->cap_stream, c->side_stream, (unsigned long long)h);
+  cudaError_t e4 = cudaSuccess;
+  for (int r = 0; r < c->unroll && e4 == cudaSuccess; ++r)   // CG steps per WHILE iteration
+    e4 = enqueue_cg_step(c, c->cap_stream, c->side_stream, (unsigned long long)h);
   cudaGraph_t captured = body;
   CUDA_OK(c, cudaStreamEndCapture(c->cap_stream, &captured));
   CUDA_OK(c, e4);
@@ -496,6 +507,10 @@ cmtcs_status cmtcs_init(cmtcs_ctx **out, const cmtcs_problem *p, const float *ph
   {
     const char *ng = getenv("CMTCS_NO_GRAPH");
     c->no_graph = ng && ng[0] == '1';
+    const char *sm = getenv("CMTCS_SERIAL_MEAN");
+    c->serial_mean = sm && sm[0] == '1';
+    const char *ur = getenv("CMTCS_GRAPH_UNROLL");
+    c->unroll = ur ? std::max(1, std::min(8, atoi(ur))) : 1;
   }
   carve(d, (char *)workspace, &b);
   c->kp.d = d;

@@ -130,6 +130,7 @@ __device__ __forceinline__ double warp_sum(double v) {
 __global__ void __launch_bounds__(UPD_THREADS) k_update(KParams p) {
   const Dims &d = p.d;
   const int u = *p.b.u;
+  if (u >= d.cap) return;
   const int lane = threadIdx.x & 31;
   const int slot = blockIdx.x * (UPD_THREADS / 32) + (threadIdx.x >> 5), t = blockIdx.y;
   const double tol = p.tol;
@@ -260,8 +261,12 @@ __global__ void __launch_bounds__(UPD_THREADS) k_update(KParams p) {
 // while some column is still active and the cap is not reached.
 __global__ void k_advance(KParams p, cudaGraphConditionalHandle h) {
   const int u = *p.b.u;
+  if (u >= p.d.cap) {  // an unrolled body ran past the end: nothing left to do
+    cudaGraphSetConditional(h, 0u);
+    return;
+  }
   const int more = (p.b.alive[u] > 0) && (u + 1 < p.d.cap);
-  *p.b.u = u + 1;
+  *p.b.u = more ? u + 1 : p.d.cap;   // u = cap marks "done" for the remaining unrolled steps
   cudaGraphSetConditional(h, more ? 1u : 0u);
 }
 

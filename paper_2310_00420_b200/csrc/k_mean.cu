@@ -65,6 +65,7 @@ __global__ void __launch_bounds__(OP_THREADS) k_mu_stage1(KParams p, const doubl
     }
   };
   if (!mu_only) {
+    if (*p.b.u >= d.cap) return;               // past the end of an unrolled graph body
     int any = 0;
     for (int c = 0; c < C; ++c) any |= (p.b.flagm[t * C + c] == 1);
     if (!any) return;
@@ -149,6 +150,7 @@ __global__ void __launch_bounds__(OP_THREADS) k_mu_stage2(KParams p) {
 
 
   // ---------------- fp64 mean-column tile ---------------------------------------------------
+  if (*p.b.u >= d.cap) return;
   int any = 0;
   for (int c = 0; c < C; ++c) any |= (p.b.flagm[t * C + c] == 1);
   if (!any) return;

@@ -148,6 +148,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   const int rt = blockIdx.y / d.S1, sp = blockIdx.y % d.S1;
   const int N = d.N, D = d.D, P = d.P, C = d.C;
   const int u = *p.b.u;
+  if (u >= d.cap) return;                     // past the end of an unrolled graph body
   if (tid == 0) atomicMax(p.b.ts + 4 * u, ~globaltimer());  // ~t: max ⇔ min
   const int m = build_act(p.b.flag + (size_t)t * P, P, s_all, &tl.m);
   if (ct == 0 && blockIdx.y == 0) {
@@ -295,6 +296,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   TcSmemTail &tl = *reinterpret_cast<TcSmemTail *>(sm + (size_t)tc.stages * tc.stage_bytes);
   const int t = blockIdx.z, ct = blockIdx.x, rt = blockIdx.y, tid = threadIdx.x, warp = tid >> 5;
   const int N = d.N, D = d.D, P = d.P;
+  if (*p.b.u >= d.cap) return;
   const int m = p.b.m_act[t];
   const int j0 = ct * tc.NT;
   if (j0 >= m) return;

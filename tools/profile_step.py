@@ -31,8 +31,13 @@ for _ in range(a.warmup):
 m.set_timing(True)
 torch.cuda.synchronize()
 torch.cuda.profiler.start()
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+e0.record()
 for _ in range(a.steps):
     info = m.em_step(1)
+e1.record()
 torch.cuda.synchronize()
 torch.cuda.profiler.stop()
-print(json.dumps({"info": info, "timing": m.get_timing()}))
+ms = e0.elapsed_time(e1) / a.steps
+print(json.dumps({"em_ms": ms, "us_per_cg_step": 1e3 * ms / max(1, info["cg_iters"]), "info": info,
+                  "timing": m.get_timing()}))
