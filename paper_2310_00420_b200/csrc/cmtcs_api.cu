@@ -38,15 +38,12 @@ struct cmtcs_ctx {
   int64_t t_n[3];
   // the CG loop as one graph: WHILE(any column active) { stage1; stage2; update; advance }
   cudaStream_t cap_stream;
-  cudaStream_t side_stream;  // mean-column branch of the CG graph
-  cudaEvent_t fork_ev[2], join_ev[2];
   TcMaps maps;
   cudaGraph_t cg_graph;
   cudaGraphExec_t cg_exec;
   int *h_u;                 // pinned: CG steps executed
   bool no_graph;            // CMTCS_NO_GRAPH=1: host-launched CG steps (for per-launch profilers)
-  bool serial_mean;         // CMTCS_SERIAL_MEAN=1: mean-column kernels on the main stream (no fork)
-  int unroll;               // CMTCS_GRAPH_UNROLL: CG steps per iteration of the WHILE body
+  int unroll;               // CG steps per iteration of the WHILE body (CMTCS_GRAPH_UNROLL, default 4)
 };
 
 namespace {
@@ -96,10 +93,9 @@ TcCfg make_tc(const Dims &d) {
   tc.NT = std::min(TC_NTMAX, (d.P + 15) / 16 * 16);
   tc.slot = (tc.NT + 31) / 32 * 32;
   tc.nacc = std::max(1, std::min(4, 512 / (2 * tc.slot)));
-  tc.stage_bytes = 2u * 128u * 128u + 2u * (unsigned)tc.NT * 128u;
-  // ≤ ~170 KB of ring so a mean-column CTA (≤ 37 KB) co-resides with a tensor-core CTA, whose
-  // 512 TMEM columns and > 114 KB of smem already pin it to one per SM
-  tc.stages = std::max(2, std::min(4, (int)((170u * 1024u) / tc.stage_bytes)));
+  tc.stage_bytes = 2u * 128u * 128u + 2u * (unsigned)tc.NT * 128u + 4096u;  // + fp64 mean-column chunk
+  // one tensor-core CTA per SM (512 TMEM columns, > 114 KB of smem): the ring takes ≤ 208 KB
+  tc.stages = std::max(2, std::min(4, (int)((208u * 1024u) / tc.stage_bytes)));
   return tc;
 }
 
@@ -283,26 +279,12 @@ const char *status_name(int code) {
 
 // One CG step: [tensor-core stage 1 ‖ mean-column stage 1] → [stage 2 ‖ mean stage 2] → update → advance.
 // The mean-column (fp64 SIMT) kernels run on a forked stream (a parallel graph branch).
-cudaError_t enqueue_cg_step(cmtcs_ctx *c, cudaStream_t s, cudaStream_t side, unsigned long long cond) {
+// One CG step: tensor-core stage 1 (+ fp64 mean columns) → stage 2 (+ mean columns) → update → advance.
+cudaError_t enqueue_cg_step(cmtcs_ctx *c, cudaStream_t s, unsigned long long cond) {
   const KParams &kp = c->kp;
   cudaError_t e;
-  for (int stg = 0; stg < 2; ++stg) {
-    if (c->serial_mean) {
-      e = stg == 0 ? launch_mu_stage1(kp, nullptr, false, s) : launch_mu_stage2(kp, s);
-      if (e != cudaSuccess) return e;
-      e = stg == 0 ? launch_stage1_tc(kp, c->maps, s) : launch_stage2_tc(kp, c->maps, s);
-      if (e != cudaSuccess) return e;
-      continue;
-    }
-    if ((e = cudaEventRecord(c->fork_ev[stg], s)) != cudaSuccess) return e;
-    if ((e = cudaStreamWaitEvent(side, c->fork_ev[stg], 0)) != cudaSuccess) return e;
-    e = stg == 0 ? launch_mu_stage1(kp, nullptr, false, side) : launch_mu_stage2(kp, side);
-    if (e != cudaSuccess) return e;
-    e = stg == 0 ? launch_stage1_tc(kp, c->maps, s) : launch_stage2_tc(kp, c->maps, s);
-    if (e != cudaSuccess) return e;
-    if ((e = cudaEventRecord(c->join_ev[stg], side)) != cudaSuccess) return e;
-    if ((e = cudaStreamWaitEvent(s, c->join_ev[stg], 0)) != cudaSuccess) return e;
-  }
+  if ((e = launch_stage1_tc(kp, c->maps, s)) != cudaSuccess) return e;
+  if ((e = launch_stage2_tc(kp, c->maps, s)) != cudaSuccess) return e;
   if ((e = launch_update(kp, s)) != cudaSuccess) return e;
   return launch_advance(kp, cond, s);
 }
@@ -325,7 +307,7 @@ cmtcs_status build_cg_graph(cmtcs_ctx *c) {
   CUDA_OK(c, cudaStreamBeginCaptureToGraph(c->cap_stream, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
   cudaError_t e4 = cudaSuccess;
   for (int r = 0; r < c->unroll && e4 == cudaSuccess; ++r)   // CG steps per WHILE iteration
-    e4 = enqueue_cg_step(c, c->cap_stream, c->side_stream, (unsigned long long)h);
+    e4 = enqueue_cg_step(c, c->cap_stream, (unsigned long long)h);
   cudaGraph_t captured = body;
   CUDA_OK(c, cudaStreamEndCapture(c->cap_stream, &captured));
   CUDA_OK(c, e4);
@@ -358,7 +340,7 @@ cmtcs_status one_em_iteration(cmtcs_ctx *c, const uint64_t *probe_bits, const do
     // profiling mode (CMTCS_NO_GRAPH=1): the same kernels launched from a host loop so that
     // per-launch tools (ncu) see them; convergence is checked every 8 steps
     for (int u = 0; u < d.cap; ++u) {
-      CUDA_OK(c, enqueue_cg_step(c, s, c->side_stream, 0ull));
+      CUDA_OK(c, enqueue_cg_step(c, s, 0ull));
       if ((u & 7) == 7 || u + 1 == d.cap) {
         CUDA_OK(c, cudaMemcpyAsync(c->h_u, kp.b.alive + u, sizeof(int), cudaMemcpyDeviceToHost, s));
         CUDA_OK(c, cudaStreamSynchronize(s));
@@ -406,8 +388,8 @@ cmtcs_status one_em_iteration(cmtcs_ctx *c, const uint64_t *probe_bits, const do
   c->launches += L;
   c->have_estep = true;
   const int steps_run = *c->h_u;
-  L += 6 * (int64_t)steps_run;  // stage1 (tc, mean), stage2 (tc, mean), update, advance per CG step
-  c->launches += 6 * (int64_t)steps_run;
+  L += 4 * (int64_t)steps_run;  // stage 1, stage 2, update, advance per CG step
+  c->launches += 4 * (int64_t)steps_run;
   if (tm) {
     // per CG step: %globaltimer stamps of the first stage-1 CTA entry, the last stage-2 CTA exit
     // and the last update-warp exit (device clock, ns)
@@ -507,10 +489,8 @@ cmtcs_status cmtcs_init(cmtcs_ctx **out, const cmtcs_problem *p, const float *ph
   {
     const char *ng = getenv("CMTCS_NO_GRAPH");
     c->no_graph = ng && ng[0] == '1';
-    const char *sm = getenv("CMTCS_SERIAL_MEAN");
-    c->serial_mean = sm && sm[0] == '1';
     const char *ur = getenv("CMTCS_GRAPH_UNROLL");
-    c->unroll = ur ? std::max(1, std::min(8, atoi(ur))) : 1;
+    c->unroll = ur ? std::max(1, std::min(8, atoi(ur))) : 4;
   }
   carve(d, (char *)workspace, &b);
   c->kp.d = d;
@@ -529,11 +509,7 @@ cmtcs_status cmtcs_init(cmtcs_ctx **out, const cmtcs_problem *p, const float *ph
   CUDA_OK(c, cudaMallocHost((void **)&c->h_out, 32 * sizeof(double)));
   CUDA_OK(c, cudaMallocHost((void **)&c->h_status, 8 * sizeof(int)));
   CUDA_OK(c, cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking));
-  CUDA_OK(c, cudaStreamCreateWithFlags(&c->side_stream, cudaStreamNonBlocking));
-  for (int i = 0; i < 2; ++i) {
-    CUDA_OK(c, cudaEventCreateWithFlags(&c->fork_ev[i], cudaEventDisableTiming));
-    CUDA_OK(c, cudaEventCreateWithFlags(&c->join_ev[i], cudaEventDisableTiming));
-  }
+
   CUDA_OK(c, cudaMallocHost((void **)&c->h_u, sizeof(int)));
   CUDA_OK(c, cudaMallocHost((void **)&c->h_ts, sizeof(unsigned long long) * 4 * d.cap));
   for (int i = 0; i < 3; ++i) CUDA_OK(c, cudaEventCreate(&c->tev[i]));
@@ -637,11 +613,7 @@ void cmtcs_destroy(cmtcs_ctx *c) {
   if (c->cg_exec) cudaGraphExecDestroy(c->cg_exec);
   if (c->cg_graph) cudaGraphDestroy(c->cg_graph);
   if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
-  if (c->side_stream) cudaStreamDestroy(c->side_stream);
-  for (int i = 0; i < 2; ++i) {
-    if (c->fork_ev[i]) cudaEventDestroy(c->fork_ev[i]);
-    if (c->join_ev[i]) cudaEventDestroy(c->join_ev[i]);
-  }
+
   for (int i = 0; i < 3; ++i)
     if (c->tev[i]) cudaEventDestroy(c->tev[i]);
   if (c->h_u) cudaFreeHost(c->h_u);

@@ -115,7 +115,6 @@ cudaError_t launch_stage2_tc(const KParams &p, const TcMaps &maps, cudaStream_t 
 cudaError_t launch_split_phi(const KParams &p, cudaStream_t s);
 size_t tc_smem_bytes(const TcCfg &tc, int P);
 cudaError_t launch_mu_stage1(const KParams &p, const double *mu_src, bool mu_only, cudaStream_t s);
-cudaError_t launch_mu_stage2(const KParams &p, cudaStream_t s);
 cudaError_t launch_update(const KParams &p, cudaStream_t s);
 cudaError_t launch_advance(const KParams &p, unsigned long long cond_handle, cudaStream_t s);
 cudaError_t launch_rhs(const KParams &p, cudaStream_t s);

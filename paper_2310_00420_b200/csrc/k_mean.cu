@@ -1,10 +1,7 @@
-// K1 (mean columns) — the fp64 part of the batched operator W = βΦ_tᵀ(Φ_t V) + α_c ⊙ V for the C
-// mean systems A_tc μ_tc = βΦ_tᵀy_t of every task.  The mean columns stay in fp64
-// end to end: DFMA on fp32 Φ tiles streamed through a 3-stage cp.async ring.
-//   stage 1  Um[t][n][c] = Σ_d Φ_t[n][d] · src[t][c][d]   (split-K over S1 slices; the S1 CTAs of a
-//            row tile form a cluster and reduce over DSMEM in fixed order)
-//   stage 2  Wm[t][c][d] = β Σ_n Φ_t[n][d] · Um[t][n][c] + α_c ⊙ Dm, plus fp64 partial dᵀAd
-// They run on a parallel branch of the CG graph, concurrently with the tensor-core probe stages.
+// Φμ for ℓ (Eq. 3 via reading A1): Um[t][n][c] = Σ_d Φ_t[n][d] · μ_tc[d] in fp64 for the final means
+// of an E-step (inside the CG loop the mean columns are computed by the tensor-core kernels' CUDA
+// cores, k_operator_tc.cu).  DFMA on fp32 Φ tiles streamed through a 3-stage cp.async ring;
+// split-K over S1 slices, the S1 CTAs of a row tile form a cluster and reduce over DSMEM.
 #include <cooperative_groups.h>
 
 #include "cmtcs_internal.cuh"
@@ -19,17 +16,10 @@ constexpr int BR = OP_BR;       // 128 rows per CTA
 constexpr int BK = OP_BK;       // 16: contraction chunk
 constexpr int ST = 3;           // pipeline stages
 constexpr int A1LD = BK + 4;    // stage-1 A tile [r][k]
-constexpr int A2LD = BR + 4;    // stage-2 A tile [k][r]
 
 struct __align__(16) SmemM1 {
   float A[ST][BR][A1LD];
   double Bm[ST][BK][MAXC];
-};
-
-struct __align__(16) SmemM2 {
-  float A[ST][BK][A2LD];
-  double Bm[ST][BK][MAXC];
-  double red[2][4][MAXC / 2];
 };
 
 __device__ __forceinline__ void cp_async16(void *smem, const void *gmem, bool valid) {
@@ -125,102 +115,6 @@ __global__ void __launch_bounds__(OP_THREADS) k_mu_stage1(KParams p, const doubl
   return;
 }
 
-// stage 2:  grid (1, nRT2, Tl)
-__global__ void __launch_bounds__(OP_THREADS) k_mu_stage2(KParams p) {
-  extern __shared__ __align__(16) unsigned char dsm2[];
-  SmemM2 &sm = *reinterpret_cast<SmemM2 *>(dsm2);
-  const Dims &d = p.d;
-  const int t = blockIdx.z, rt = blockIdx.y, tid = threadIdx.x;
-  const int N = d.N, D = d.D, C = d.C;
-  const float *__restrict__ phi = p.phi + (size_t)t * d.phi_task_stride;
-  const int d0 = rt * BR;
-  const int nk = (N + BK - 1) / BK;
-  const double beta = p.beta;
-
-  // A tile: Φ[k0 + kk][d0 + 4q .. +3] → A[kk][4q..]  (2 × cp.async per thread)
-  auto loadA = [&](int buf, int k0) {
-#pragma unroll
-    for (int i = 0; i < 2; ++i) {
-      const int idx = tid + i * OP_THREADS, kk = idx >> 5, q = idx & 31;
-      const int n = k0 + kk, dd = d0 + 4 * q;
-      const bool ok = n < N && dd < D;
-      cp_async16(&sm.A[buf][kk][4 * q], ok ? phi + (size_t)n * D + dd : phi, ok);
-    }
-  };
-
-
-  // ---------------- fp64 mean-column tile ---------------------------------------------------
-  if (*p.b.u >= d.cap) return;
-  int any = 0;
-  for (int c = 0; c < C; ++c) any |= (p.b.flagm[t * C + c] == 1);
-  if (!any) return;
-  const int r = tid & (BR - 1), h = tid >> 7;
-  double acc[MAXC / 2];
-#pragma unroll
-  for (int i = 0; i < MAXC / 2; ++i) acc[i] = 0.0;
-  auto loadB = [&](int buf, int k0) {
-    if (tid < BK * C) {
-      const int kk = tid / C, c = tid % C;
-      sm.Bm[buf][kk][c] = (k0 + kk < N) ? p.b.Um[((size_t)t * N + k0 + kk) * C + c] : 0.0;
-    }
-  };
-#pragma unroll
-  for (int s = 0; s < ST - 1; ++s) {
-    if (s < nk) { loadA(s, s * BK); loadB(s, s * BK); }
-    cp_commit();
-  }
-  for (int kc = 0; kc < nk; ++kc) {
-    cp_wait<ST - 2>();
-    __syncthreads();
-    const int nx = kc + ST - 1;
-    if (nx < nk) { loadA(nx % ST, nx * BK); loadB(nx % ST, nx * BK); }
-    cp_commit();
-    const int buf = kc % ST;
-#pragma unroll 4
-    for (int kk = 0; kk < BK; ++kk) {
-      const double a = (double)sm.A[buf][kk][r];
-#pragma unroll
-      for (int i = 0; i < MAXC / 2; ++i)
-        if (h + 2 * i < C) acc[i] = fma(a, sm.Bm[buf][kk][h + 2 * i], acc[i]);
-    }
-  }
-  cp_wait<0>();
-  // epilogue: Wm = β acc + α ⊙ dm ; partial dᵀW over this row tile
-  const int dd = d0 + r;
-  double dot[MAXC / 2];
-#pragma unroll
-  for (int i = 0; i < MAXC / 2; ++i) {
-    dot[i] = 0.0;
-    const int c = h + 2 * i;
-    if (c < C && dd < D) {
-      const size_t o = ((size_t)t * C + c) * D + dd;
-      const double dv = p.b.Dm[o];
-      const double wv = fma(beta, acc[i], p.b.alpha64[(size_t)c * D + dd] * dv);
-      p.b.Wm[o] = wv;
-      dot[i] = dv * wv;
-    }
-  }
-  const int lane = tid & 31, wq = (tid >> 5) & 3;
-#pragma unroll
-  for (int i = 0; i < MAXC / 2; ++i) {
-    double v = dot[i];
-#pragma unroll
-    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    if (lane == 0) sm.red[h][wq][i] = v;
-  }
-  __syncthreads();
-  if (tid < MAXC) {
-    const int hh = tid & 1, i = tid >> 1, c = hh + 2 * i;
-    if (c < C) {
-      double v = 0.0;
-      for (int q = 0; q < 4; ++q) v += sm.red[hh][q][i];
-      p.b.dAdm[((size_t)t * C + c) * d.nRT2 + rt] = v;
-    }
-  }
-  if (tid == 0) atomicMax(p.b.ts + 4 * (*p.b.u) + 1, globaltimer());
-  return;
-}
-
 }  // namespace
 
 cudaError_t launch_mu_stage1(const KParams &p, const double *mu_src, bool mu_only, cudaStream_t s) {
@@ -243,17 +137,6 @@ cudaError_t launch_mu_stage1(const KParams &p, const double *mu_src, bool mu_onl
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, k_mu_stage1, p, mu_src ? mu_src : p.b.Dm, (int)(mu_only ? 1 : 0));
-}
-
-cudaError_t launch_mu_stage2(const KParams &p, cudaStream_t s) {
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(k_mu_stage2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(SmemM2));
-    if (e != cudaSuccess) return e;
-    configured = true;
-  }
-  k_mu_stage2<<<dim3(1, p.d.nRT2, p.d.Tl), OP_THREADS, sizeof(SmemM2), s>>>(p);
-  return cudaGetLastError();
 }
 
 }  // namespace cmtcs

@@ -45,7 +45,7 @@ struct TcSmemTail {
   int act[256];        // the tile's active columns
   long long off[256];  // stage 2: element offset of column j's vectors, ((t·P + col)·D)
   int aoff[256];       // stage 2: offset of the column's α row, c·D
-  double red[4][256];
+  double red[4][TC_NTMAX + MAXC];  // probe columns [0, NT), mean columns [TC_NTMAX, +C)
 };
 
 // Sums v[0..15] over the 32 lanes of a warp with 16 shuffles (butterfly transpose-reduce); the
@@ -133,8 +133,37 @@ __device__ int build_act(const int *flag, int P, int *s_act, int *s_m) {
   return *s_m;
 }
 
+// fp64 mean-column work on the A tile already in smem (CUDA cores, while the tensor core runs):
+// acc[c] += Σ_{k in stage} Φ[r][k] · B[c][k] for this thread's row r, Φ = hi + lo (exact in fp32).
+// Stage 1 reads B as [c][k] (k contiguous), stage 2 as [k][c].
+template <bool B_CK>
+__device__ __forceinline__ void mean_stage(const unsigned char *base, const double *mb, int r, int C, double *acc) {
+#pragma unroll
+  for (int cc = 0; cc < TK / 4; ++cc) {
+    const float4 h = *reinterpret_cast<const float4 *>(base + sw128_offset(r, cc));
+    const float4 l = *reinterpret_cast<const float4 *>(base + A_BYTES + sw128_offset(r, cc));
+    const double a[4] = {(double)(h.x + l.x), (double)(h.y + l.y), (double)(h.z + l.z), (double)(h.w + l.w)};
+#pragma unroll
+    for (int c = 0; c < MAXC; ++c) {
+      if (c < C) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const double bv = B_CK ? mb[c * TK + 4 * cc + i] : mb[(4 * cc + i) * C + c];
+          acc[c] = fma(a[i], bv, acc[c]);
+        }
+      }
+    }
+  }
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t *mbar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(mbar)) : "memory");
+}
+
 // ---------------------------------------------------------------------------------------------
 // stage 1:  grid (nCT, nRT1 * S1, Tl), cluster (1, S1, 1), 128 threads
+//   probe columns: U = Φ·D on the tensor core (3xTF32);  column tile 0 also computes the fp64
+//   mean columns Um = Φ·Dm on the CUDA cores from the same smem Φ tiles.
 // ---------------------------------------------------------------------------------------------
 __global__ void __launch_bounds__(TC_THREADS, 1)
     k_stage1_tc(KParams p, const __grid_constant__ CUtensorMap tPhiH, const __grid_constant__ CUtensorMap tPhiL) {
@@ -151,27 +180,28 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   if (u >= d.cap) return;                     // past the end of an unrolled graph body
   if (tid == 0) atomicMax(p.b.ts + 4 * u, ~globaltimer());  // ~t: max ⇔ min
   const int m = build_act(p.b.flag + (size_t)t * P, P, s_all, &tl.m);
-  if (ct == 0 && blockIdx.y == 0) {
+  int mc = 0;
+  for (int c = 0; c < C; ++c) mc += (p.b.flagm[t * C + c] == 1);
+  if (ct == 0 && blockIdx.y == 0 && tid == 0) {
     // task bookkeeping for this CG step: publish the act list and the step histograms
-    for (int j = tid; j < m; j += TC_THREADS) p.b.act[(size_t)t * P + j] = s_all[j];
-    if (tid == 0) {
-      p.b.m_act[t] = m;
-      int mc = 0;
-      for (int c = 0; c < C; ++c) mc += (p.b.flagm[t * C + c] == 1);
-      if (m) atomicAdd(p.b.hist + u, m);
-      if (mc) atomicAdd(p.b.histm + u, mc);
-      if (m + mc) atomicAdd(p.b.histt + u, 1);
-    }
+    p.b.m_act[t] = m;
+    if (m) atomicAdd(p.b.hist + u, m);
+    if (mc) atomicAdd(p.b.histm + u, mc);
+    if (m + mc) atomicAdd(p.b.histt + u, 1);
   }
+  if (ct == 0 && blockIdx.y == 0)
+    for (int j = tid; j < m; j += TC_THREADS) p.b.act[(size_t)t * P + j] = s_all[j];
   const int j0 = ct * tc.NT;
-  if (j0 >= m) return;                        // cluster-uniform (same t, ct)
-  const int ncol = min(tc.NT, m - j0);
+  const bool run_probe = j0 < m, run_mean = ct == 0 && mc > 0;
+  if (!run_probe && !run_mean) return;        // cluster-uniform (same t, ct)
+  const int ncol = run_probe ? min(tc.NT, m - j0) : 0;
   const int nmma = (ncol + 15) & ~15;
   const int n0 = rt * TM;
   const int kb = sp * d.K1, ke = min(D, kb + d.K1);
   const int nk = (ke - kb + TK - 1) / TK;
   const int arow = (d.shared_phi ? 0 : t * N) + n0;
   const uint32_t b_bytes = (uint32_t)tc.NT * 128;
+  const uint32_t mu_off = 2 * A_BYTES + 2 * b_bytes;   // fp64 mean-column chunk [C][32]
   const int slot = tc.slot, nacc = min(tc.nacc, nk), S = tc.stages;  // every pair gets ≥ 1 chunk
   if (tid == 0) {
     for (int s = 0; s < S; ++s) { mbar_init(&tl.full[s], 1); mbar_init(&tl.empty[s], 1); }
@@ -179,13 +209,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     prefetch_tmap(&tPhiH);
     prefetch_tmap(&tPhiL);
   }
-  if (warp == 0) tmem_alloc<512>(&tl.tslot);
+  if (warp == 0 && nmma) tmem_alloc<512>(&tl.tslot);
   fence_before_sync();
   __syncthreads();
   fence_after_sync();
   const uint32_t tmem = tl.tslot;
-  const uint32_t idesc = idesc_tf32(TM, nmma);
+  const uint32_t idesc = idesc_tf32(TM, nmma > 0 ? nmma : 16);
   const float *Dh = p.b.Dh + (size_t)t * P * D, *Dl = p.b.Dl + (size_t)t * P * D;
+  const double *Dm = p.b.Dm + (size_t)t * C * D;
 
   auto issue = [&](int st, int kc) {
     unsigned char *base = stage_base(sm, st, tc.stage_bytes);
@@ -205,7 +236,17 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       cp_async16(sb + sw128_offset(j, c), Dh + off, ok);
       cp_async16(sb + b_bytes + sw128_offset(j, c), Dl + off, ok);
     }
+    if (run_mean && tid < C * (TK / 2)) {     // Dm[c][k0 .. k0+31] → [c][k], 2 doubles per copy
+      const int c = tid / (TK / 2), k2 = tid % (TK / 2);
+      const int k = k0 + 2 * k2;
+      const bool ok = k < ke;
+      cp_async16(smem_u32(base + mu_off) + (uint32_t)(c * TK + 2 * k2) * 8, ok ? Dm + (size_t)c * D + k : Dm, ok);
+    }
   };
+  double macc[MAXC];
+#pragma unroll
+  for (int c = 0; c < MAXC; ++c) macc[c] = 0.0;
+  const int r = warp * 32 + (tid & 31);       // tile row = TMEM lane
   for (int s = 0; s < S - 1; ++s) {
     if (s < nk) issue(s, s);
     cp_commit();
@@ -216,17 +257,24 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     cp_wait_dyn(S - 2);
     fence_proxy_async();
     __syncthreads();
+    unsigned char *base = stage_base(sm, st, tc.stage_bytes);
     if (tid == 0) {
-      fence_after_sync();
-      const int q = (kc * nacc) / nk;
-      const int qfirst = (q * nk + nacc - 1) / nacc;
-      mma_stage(tmem, stage_base(sm, st, tc.stage_bytes), b_bytes, idesc, q, slot, kc == qfirst);
-      mma_commit(&tl.empty[st]);
+      if (nmma) {
+        fence_after_sync();
+        const int q = (kc * nacc) / nk;
+        const int qfirst = (q * nk + nacc - 1) / nacc;
+        mma_stage(tmem, base, b_bytes, idesc, q, slot, kc == qfirst);
+        mma_commit(&tl.empty[st]);
+      } else {
+        mbar_arrive(&tl.empty[st]);
+      }
     }
+    if (run_mean) mean_stage<true>(base, reinterpret_cast<const double *>(base + mu_off), r, C, macc);
     const int nx = kc + S - 1;
     if (nx < nk) {
       const int ns = nx % S;
       if (nx >= S) mbar_wait(&tl.empty[ns], ((nx - S) / S) & 1);
+      __syncthreads();                        // every thread is done reading stage ns (mean part)
       issue(ns, nx);
     }
     cp_commit();
@@ -234,7 +282,6 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   mbar_wait(&tl.empty[(nk - 1) % S], ((nk - 1) / S) & 1);
   fence_after_sync();
 
-  const int r = warp * 32 + (tid & 31);   // tile row = TMEM lane
   const int n = n0 + r;
   float *Uh = p.b.Uh + (size_t)t * d.Pp * N, *Ul = p.b.Ul + (size_t)t * d.Pp * N;
   if (d.S1 == 1) {
@@ -253,14 +300,26 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         }
       }
     }
+    if (run_mean && n < N) {
+#pragma unroll
+      for (int c = 0; c < MAXC; ++c)
+        if (c < C) p.b.Um[((size_t)t * N + n) * C + c] = macc[c];
+    }
   } else {
-    // split-K: partial tile part[c][r] in smem (aliases the drained ring), cluster DSMEM reduction
-    float *part = reinterpret_cast<float *>(sm);
+    // split-K: partial tiles in smem (aliases the drained ring), cluster DSMEM reduction
+    __syncthreads();
+    float *part = reinterpret_cast<float *>(sm);                         // [NT][128] fp32
+    double *partm = reinterpret_cast<double *>(sm + (size_t)tc.NT * TM * 4);  // [128][MAXC] fp64
     for (int c0 = 0; c0 < nmma; c0 += 16) {
       float tot[16];
       acc_load16(tmem, warp, c0, nacc, slot, tot);
 #pragma unroll
       for (int i = 0; i < 16; ++i) part[(c0 + i) * TM + r] = tot[i];
+    }
+    if (run_mean) {
+#pragma unroll
+      for (int c = 0; c < MAXC; ++c)
+        if (c < C) partm[r * MAXC + c] = macc[c];
     }
     cg::cluster_group cl = cg::this_cluster();
     cl.sync();
@@ -276,15 +335,24 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         Ul[(size_t)(j0 + c) * N + nn] = v - h;
       }
     }
+    if (run_mean)
+      for (int e = tid; e < rows * C; e += TC_THREADS) {
+        const int rr = rb + e / C, c = e % C;
+        double v = 0.0;
+        for (int src = 0; src < d.S1; ++src) v += cl.map_shared_rank(partm, src)[rr * MAXC + c];
+        if (n0 + rr < N) p.b.Um[((size_t)t * N + n0 + rr) * C + c] = v;
+      }
     cl.sync();
   }
   fence_before_sync();
   __syncthreads();
-  if (warp == 0) tmem_dealloc<512>(tmem);
+  if (warp == 0 && nmma) tmem_dealloc<512>(tmem);
 }
 
 // ---------------------------------------------------------------------------------------------
 // stage 2:  grid (nCT, nRT2, Tl), 128 threads
+//   probe columns: W = βΦᵀU + α⊙D (tensor core) and fp64 partial dᵀW;  column tile 0 also the fp64
+//   mean columns Wm = βΦᵀUm + α⊙Dm and dᵀW partials on the CUDA cores from the same Φᵀ tiles.
 // ---------------------------------------------------------------------------------------------
 __global__ void __launch_bounds__(TC_THREADS, 1)
     k_stage2_tc(KParams p, const __grid_constant__ CUtensorMap tPtH, const __grid_constant__ CUtensorMap tPtL,
@@ -295,18 +363,22 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   const TcCfg &tc = p.tc;
   TcSmemTail &tl = *reinterpret_cast<TcSmemTail *>(sm + (size_t)tc.stages * tc.stage_bytes);
   const int t = blockIdx.z, ct = blockIdx.x, rt = blockIdx.y, tid = threadIdx.x, warp = tid >> 5;
-  const int N = d.N, D = d.D, P = d.P;
+  const int N = d.N, D = d.D, P = d.P, C = d.C;
   if (*p.b.u >= d.cap) return;
   const int m = p.b.m_act[t];
+  int mc = 0;
+  for (int c = 0; c < C; ++c) mc += (p.b.flagm[t * C + c] == 1);
   const int j0 = ct * tc.NT;
-  if (j0 >= m) return;
-  const int ncol = min(tc.NT, m - j0);
+  const bool run_probe = j0 < m, run_mean = ct == 0 && mc > 0;
+  if (!run_probe && !run_mean) return;
+  const int ncol = run_probe ? min(tc.NT, m - j0) : 0;
   const int nmma = (ncol + 15) & ~15;
   const int d0 = rt * TM;
   const int nk = (N + TK - 1) / TK;
   const int arow = (d.shared_phi ? 0 : t * D) + d0;
   const int brow = t * d.Pp + j0;
   const uint32_t b_bytes = (uint32_t)tc.NT * 128;
+  const uint32_t mu_off = 2 * A_BYTES + 2 * b_bytes;   // fp64 mean-column chunk [32][C]
   const int slot = tc.slot, nacc = min(tc.nacc, nk), S = tc.stages;  // every pair gets ≥ 1 chunk
   for (int j = tid; j < ncol; j += TC_THREADS) {
     const int col = p.b.act[(size_t)t * P + j0 + j];
@@ -322,50 +394,75 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     prefetch_tmap(&tUH);
     prefetch_tmap(&tUL);
   }
-  if (warp == 0) tmem_alloc<512>(&tl.tslot);
+  if (warp == 0 && nmma) tmem_alloc<512>(&tl.tslot);
   fence_before_sync();
   __syncthreads();
   fence_after_sync();
   const uint32_t tmem = tl.tslot;
-  const uint32_t idesc = idesc_tf32(TM, nmma);
+  const uint32_t idesc = idesc_tf32(TM, nmma > 0 ? nmma : 16);
+  const double *Um = p.b.Um + (size_t)t * N * C;
 
   auto issue = [&](int st, int kc) {
+    unsigned char *base = stage_base(sm, st, tc.stage_bytes);
+    const int k0 = kc * TK;
     if (tid == 0) {
-      unsigned char *base = stage_base(sm, st, tc.stage_bytes);
-      const int k0 = kc * TK;
-      mbar_arrive_expect_tx(&tl.full[st], 2 * A_BYTES + 2 * b_bytes);
+      mbar_arrive_expect_tx(&tl.full[st], 2 * A_BYTES + (nmma ? 2 * b_bytes : 0));
       tma_load_2d(base, &tPtH, k0, arow, &tl.full[st]);
       tma_load_2d(base + A_BYTES, &tPtL, k0, arow, &tl.full[st]);
-      tma_load_2d(base + 2 * A_BYTES, &tUH, k0, brow, &tl.full[st]);
-      tma_load_2d(base + 2 * A_BYTES + b_bytes, &tUL, k0, brow, &tl.full[st]);
+      if (nmma) {
+        tma_load_2d(base + 2 * A_BYTES, &tUH, k0, brow, &tl.full[st]);
+        tma_load_2d(base + 2 * A_BYTES + b_bytes, &tUL, k0, brow, &tl.full[st]);
+      }
+    }
+    if (run_mean) {                            // Um[k0 .. k0+31][0..C) is contiguous: 32·C 8-byte copies
+      for (int e = tid; e < C * TK; e += TC_THREADS) {
+        const bool ok = k0 + e / C < N;
+        cp_async8(smem_u32(base + mu_off) + (uint32_t)e * 8, ok ? Um + (size_t)k0 * C + e : Um, ok);
+      }
     }
   };
-  for (int s = 0; s < S - 1; ++s)
+  double macc[MAXC];
+#pragma unroll
+  for (int c = 0; c < MAXC; ++c) macc[c] = 0.0;
+  const int r = warp * 32 + (tid & 31);
+  for (int s = 0; s < S - 1; ++s) {
     if (s < nk) issue(s, s);
+    cp_commit();
+  }
   for (int kc = 0; kc < nk; ++kc) {
     const int st = kc % S;
     mbar_wait(&tl.full[st], (kc / S) & 1);
+    cp_wait_dyn(S - 2);
+    fence_proxy_async();
+    __syncthreads();
+    unsigned char *base = stage_base(sm, st, tc.stage_bytes);
     if (tid == 0) {
-      fence_after_sync();
-      const int q = (kc * nacc) / nk;
-      const int qfirst = (q * nk + nacc - 1) / nacc;
-      mma_stage(tmem, stage_base(sm, st, tc.stage_bytes), b_bytes, idesc, q, slot, kc == qfirst);
-      mma_commit(&tl.empty[st]);
-      const int nx = kc + S - 1;
-      if (nx < nk) {
-        const int ns = nx % S;
-        if (nx >= S) mbar_wait(&tl.empty[ns], ((nx - S) / S) & 1);
-        issue(ns, nx);
+      if (nmma) {
+        fence_after_sync();
+        const int q = (kc * nacc) / nk;
+        const int qfirst = (q * nk + nacc - 1) / nacc;
+        mma_stage(tmem, base, b_bytes, idesc, q, slot, kc == qfirst);
+        mma_commit(&tl.empty[st]);
+      } else {
+        mbar_arrive(&tl.empty[st]);
       }
     }
+    if (run_mean) mean_stage<false>(base, reinterpret_cast<const double *>(base + mu_off), r, C, macc);
+    const int nx = kc + S - 1;
+    if (nx < nk) {
+      const int ns = nx % S;
+      if (nx >= S) mbar_wait(&tl.empty[ns], ((nx - S) / S) & 1);
+      __syncthreads();                        // every thread is done reading stage ns (mean part)
+      issue(ns, nx);
+    }
+    cp_commit();
   }
   mbar_wait(&tl.empty[(nk - 1) % S], ((nk - 1) / S) & 1);
   fence_after_sync();
 
   // epilogue: W = β acc + α_c ⊙ d for row dd, fp64 partial dᵀW per column (this 128-row tile).
-  // Per group of 16 columns all global loads are issued first, then the math, then the 16
-  // independent warp reductions (latency overlap instead of one dependent chain per column).
-  const int r = warp * 32 + (tid & 31);
+  // Per group of 16 columns all global loads are issued first, then the math, then a butterfly
+  // reduction of the 16 dot partials over the warp.
   const int dd = d0 + r;
   const bool rv = dd < D;
   const float betaf = (float)p.beta;
@@ -393,12 +490,34 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     const double sum = warp_reduce16(dot, lane, &idx);
     if ((lane & 1) == 0) tl.red[warp][c0 + idx] = sum;
   }
+  if (run_mean) {
+    // mean columns (fp64): Wm = β·acc + α ⊙ dm, partial dᵀWm over this row tile
+    double dot[16];
+#pragma unroll
+    for (int c = 0; c < 16; ++c) {
+      dot[c] = 0.0;
+      if (c < C && rv) {
+        const size_t o = ((size_t)t * C + c) * D + dd;
+        const double dmv = p.b.Dm[o];
+        const double wv = fma(p.beta, macc[c], p.b.alpha64[(size_t)c * D + dd] * dmv);
+        p.b.Wm[o] = wv;
+        dot[c] = dmv * wv;
+      }
+    }
+    int idx;
+    const double sum = warp_reduce16(dot, lane, &idx);
+    if ((lane & 1) == 0 && idx < C) tl.red[warp][TC_NTMAX + idx] = sum;
+  }
   fence_before_sync();
   __syncthreads();
   for (int jj = tid; jj < ncol; jj += TC_THREADS)
     p.b.dAd[((size_t)t * P + tl.act[jj]) * d.nRT2 + rt] = tl.red[0][jj] + tl.red[1][jj] + tl.red[2][jj] + tl.red[3][jj];
+  if (run_mean && tid < C) {
+    const int jj = TC_NTMAX + tid;
+    p.b.dAdm[((size_t)t * C + tid) * d.nRT2 + rt] = tl.red[0][jj] + tl.red[1][jj] + tl.red[2][jj] + tl.red[3][jj];
+  }
   if (tid == 0) atomicMax(p.b.ts + 4 * (*p.b.u) + 1, globaltimer());
-  if (warp == 0) tmem_dealloc<512>(tmem);
+  if (warp == 0 && nmma) tmem_dealloc<512>(tmem);
 }
 
 // Φ → (Φhi, Φlo) and the transposed pair (Φᵀhi, Φᵀlo), once at init.  32×32 smem-tiled transpose.
