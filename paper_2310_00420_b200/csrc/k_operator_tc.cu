@@ -236,12 +236,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       cp_async16(sb + sw128_offset(j, c), Dh + off, ok);
       cp_async16(sb + b_bytes + sw128_offset(j, c), Dl + off, ok);
     }
-    if (run_mean && tid < C * (TK / 2)) {     // Dm[c][k0 .. k0+31] → [c][k], 2 doubles per copy
-      const int c = tid / (TK / 2), k2 = tid % (TK / 2);
-      const int k = k0 + 2 * k2;
-      const bool ok = k < ke;
-      cp_async16(smem_u32(base + mu_off) + (uint32_t)(c * TK + 2 * k2) * 8, ok ? Dm + (size_t)c * D + k : Dm, ok);
-    }
+    if (run_mean)                             // Dm[c][k0 .. k0+31] → [c][k], 2 doubles per copy
+      for (int e = tid; e < C * (TK / 2); e += TC_THREADS) {
+        const int c = e / (TK / 2), k2 = e % (TK / 2);
+        const int k = k0 + 2 * k2;
+        const bool ok = k < ke;
+        cp_async16(smem_u32(base + mu_off) + (uint32_t)(c * TK + 2 * k2) * 8, ok ? Dm + (size_t)c * D + k : Dm, ok);
+      }
   };
   double macc[MAXC];
 #pragma unroll
