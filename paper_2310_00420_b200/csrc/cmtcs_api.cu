@@ -36,14 +36,10 @@ struct cmtcs_ctx {
   unsigned long long *h_ts;  // pinned [cap][4]
   double t_ms[3];
   int64_t t_n[3];
-  // the CG loop as one graph: WHILE(any column active) { stage1; stage2; update; advance }
-  cudaStream_t cap_stream;
+  // the CG loop: one persistent kernel per E-step (k_cg_persistent.cu), one CTA per SM
   TcMaps maps;
-  cudaGraph_t cg_graph;
-  cudaGraphExec_t cg_exec;
+  int grid;
   int *h_u;                 // pinned: CG steps executed
-  bool no_graph;            // CMTCS_NO_GRAPH=1: host-launched CG steps (for per-launch profilers)
-  int unroll;               // CG steps per iteration of the WHILE body (CMTCS_GRAPH_UNROLL, default 4)
 };
 
 namespace {
@@ -94,8 +90,19 @@ TcCfg make_tc(const Dims &d) {
   tc.slot = (tc.NT + 31) / 32 * 32;
   tc.nacc = std::max(1, std::min(4, 512 / (2 * tc.slot)));
   tc.stage_bytes = 2u * 128u * 128u + 2u * (unsigned)tc.NT * 128u + 4096u;  // + fp64 mean-column chunk
-  // one tensor-core CTA per SM (512 TMEM columns, > 114 KB of smem): the ring takes ≤ 208 KB
-  tc.stages = std::max(2, std::min(4, (int)((208u * 1024u) / tc.stage_bytes)));
+  // one CTA per SM (512 TMEM columns): ring (+ the stage-2 epilogue's d tile when ≥ 3 stages still fit)
+  // within ≤ 212 KB of the 227 KB of shared memory
+  const unsigned budget = 212u * 1024u;
+  tc.dtile_bytes = (unsigned)tc.NT * 128u * 4u;
+  const int st_with = (int)((budget - std::min(budget, tc.dtile_bytes)) / tc.stage_bytes);
+  if (st_with >= 3) {
+    tc.use_dtile = 1;
+    tc.stages = std::min(4, st_with);
+  } else {
+    tc.use_dtile = 0;
+    tc.dtile_bytes = 0;
+    tc.stages = std::max(2, std::min(4, (int)(budget / tc.stage_bytes)));
+  }
   return tc;
 }
 
@@ -126,6 +133,7 @@ bool make_dims(const cmtcs_problem *p, Dims *d, char *why) {
   d->K = p->K;
   d->P = p->C * p->K;
   d->Pp = (d->P + 3) & ~3;
+  d->Cp = (p->C + 1) & ~1;
   d->cap = p->cg_max_iters;
   d->nw = (p->D + 63) / 64;
   d->nRT1 = (p->N + OP_BR - 1) / OP_BR;
@@ -133,18 +141,26 @@ bool make_dims(const cmtcs_problem *p, Dims *d, char *why) {
   const int NT = std::min(TC_NTMAX, (d->P + 15) / 16 * 16);
   d->nCT = (d->P + NT - 1) / NT;
   {
-    // split the stage-1 contraction over D while the grid still fits one wave of 148 SMs (the
-    // tensor-core CTAs run one per SM); S1 ∈ {1, 2, 4, 8} (the cluster of split CTAs reduces its
-    // 128-row tile by rows) and every split keeps ≥ 128 of D
+    // split the stage-1 contraction over D (S1 ∈ {1, 2, 4, 8}, every split ≥ 128 of D) so that the
+    // stage-1 units fill the persistent grid (148 CTAs on a B200): minimise rounds × chunks per
+    // unit.  S1 > 1 only when all stage-1 units fit in one round: the split CTAs of a tile wait for
+    // one another to reduce their partial tiles (k_cg_persistent.cu).
     const int sms = 148;
     const long base = (long)d->nCT * d->nRT1 * (p->task_end - p->task_begin);
-    int s1 = 1;
-    while (s1 < 8 && base * s1 * 2 <= sms && p->D / (2 * s1) >= 128) s1 *= 2;
-    int k1 = (p->D + s1 - 1) / s1;
+    int best = 1;
+    long best_cost = -1;
+    for (int s1 = 1; s1 <= 8; s1 *= 2) {
+      if (s1 > 1 && (p->D / s1 < 128 || base * s1 > sms)) break;
+      const long rounds = (base * s1 + sms - 1) / sms;
+      const long chunks = ((p->D + s1 - 1) / s1 + 31) / 32;
+      const long cost = rounds * (chunks + 4);   // + fixed per-unit cost (prologue, epilogue, reduction)
+      if (best_cost < 0 || cost < best_cost) { best_cost = cost; best = s1; }
+    }
+    int k1 = (p->D + best - 1) / best;
     k1 = (k1 + 31) / 32 * 32;   // whole 32-wide K stages of the tensor-core pipeline
     d->K1 = k1;
-    d->S1 = s1;
-    if ((p->D + k1 - 1) / k1 != s1) { snprintf(why, 256, "internal: bad split of D=%d", p->D); return false; }
+    d->S1 = (p->D + k1 - 1) / k1;
+    if (d->S1 < 1 || d->S1 > 8) { snprintf(why, 256, "internal: bad split of D=%d", p->D); return false; }
   }
   d->shared_phi = p->shared_phi ? 1 : 0;
   d->phi_task_stride = p->shared_phi ? 0 : (int64_t)p->N * p->D;
@@ -169,6 +185,7 @@ size_t carve(const Dims &d, char *base, Bufs *b) {
   b->R = cv.take<float>(Tl * P * D);
   b->Dh = cv.take<float>(Tl * P * D);
   b->Dl = cv.take<float>(Tl * P * D);
+  b->D32 = cv.take<float>(Tl * P * D);
   b->W = cv.take<float>(Tl * P * D);
   b->Xm = cv.take<double>(Tl * C * D);
   b->Rm = cv.take<double>(Tl * C * D);
@@ -176,7 +193,7 @@ size_t carve(const Dims &d, char *base, Bufs *b) {
   b->Wm = cv.take<double>(Tl * C * D);
   b->Uh = cv.take<float>(Tl * d.Pp * N);
   b->Ul = cv.take<float>(Tl * d.Pp * N);
-  b->Um = cv.take<double>(Tl * N * C);
+  b->Um = cv.take<double>(Tl * N * d.Cp);
   b->rr = cv.take<double>(Tl * P);
   b->rrm = cv.take<double>(Tl * C);
   b->dAd = cv.take<double>(Tl * P * d.nRT2);
@@ -202,9 +219,14 @@ size_t carve(const Dims &d, char *base, Bufs *b) {
   b->histt = cv.take<int>(cap);
   b->status = cv.take<int>(8);
   b->u = cv.take<int>(1);
-  b->ts = cv.take<unsigned long long>((size_t)cap * 4);
+  b->ts = cv.take<unsigned long long>((size_t)cap * 4 + 256);   // + 256 diagnostic stamps
   b->stats = cv.take<double>(16);
   b->assign = cv.take<int>(Tl);
+  b->Upart = cv.take<float>(d.S1 > 1 ? Tl * d.S1 * d.Pp * N : 1);
+  b->Umpart = cv.take<double>(d.S1 > 1 ? Tl * d.S1 * N * d.Cp : 1);
+  b->tmark = cv.take<int>(Tl);
+  b->tilecnt = cv.take<int>(Tl * d.nCT * d.nRT1);
+  b->gridbar = cv.take<unsigned>(1);
   return cv.off;
 }
 
@@ -234,40 +256,6 @@ cmtcs_status set_alpha(cmtcs_ctx *c, const double *alpha) {
   return CMTCS_OK;
 }
 
-typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
-                                  const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
-                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-
-// 2-D fp32 tensor map over a row-major [rows][cols] array, box 32 × box_rows, 128-byte swizzle
-bool encode_2d(EncodeTiledFn enc, CUtensorMap *m, const float *ptr, long rows, long cols, int box_rows) {
-  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
-  cuuint64_t strides[1] = {(cuuint64_t)cols * 4};
-  cuuint32_t box[2] = {32, (cuuint32_t)box_rows};
-  cuuint32_t es[2] = {1, 1};
-  return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void *)ptr, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-             CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
-         CUDA_SUCCESS;
-}
-
-cmtcs_status encode_maps(cmtcs_ctx *c) {
-  void *fn = nullptr;
-  cudaDriverEntryPointQueryResult q;
-  CUDA_OK(c, cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
-  if (!fn || q != cudaDriverEntryPointSuccess) return fail(c, CMTCS_ECUDA, "cuTensorMapEncodeTiled unavailable");
-  EncodeTiledFn enc = (EncodeTiledFn)fn;
-  const Dims &d = c->kp.d;
-  const Bufs &b = c->kp.b;
-  const long mats = d.shared_phi ? 1 : d.Tl;
-  bool ok = encode_2d(enc, &c->maps.phi_h, b.Phh, mats * d.N, d.D, OP_BR) &&
-            encode_2d(enc, &c->maps.phi_l, b.Phl, mats * d.N, d.D, OP_BR) &&
-            encode_2d(enc, &c->maps.phit_h, b.PTh, mats * d.D, d.N, OP_BR) &&
-            encode_2d(enc, &c->maps.phit_l, b.PTl, mats * d.D, d.N, OP_BR) &&
-            encode_2d(enc, &c->maps.u_h, b.Uh, (long)d.Tl * d.Pp, d.N, c->kp.tc.NT) &&
-            encode_2d(enc, &c->maps.u_l, b.Ul, (long)d.Tl * d.Pp, d.N, c->kp.tc.NT);
-  if (!ok) return fail(c, CMTCS_ECUDA, "cuTensorMapEncodeTiled failed");
-  return CMTCS_OK;
-}
-
 const char *status_name(int code) {
   switch (code) {
     case ST_BREAKDOWN: return "CG breakdown (d'Ad <= 0)";
@@ -275,44 +263,6 @@ const char *status_name(int code) {
     case ST_NUMERIC: return "non-finite ell / softmax of all -inf";
     default: return "unknown";
   }
-}
-
-// One CG step: [tensor-core stage 1 ‖ mean-column stage 1] → [stage 2 ‖ mean stage 2] → update → advance.
-// The mean-column (fp64 SIMT) kernels run on a forked stream (a parallel graph branch).
-// One CG step: tensor-core stage 1 (+ fp64 mean columns) → stage 2 (+ mean columns) → update → advance.
-cudaError_t enqueue_cg_step(cmtcs_ctx *c, cudaStream_t s, unsigned long long cond) {
-  const KParams &kp = c->kp;
-  cudaError_t e;
-  if ((e = launch_stage1_tc(kp, c->maps, s)) != cudaSuccess) return e;
-  if ((e = launch_stage2_tc(kp, c->maps, s)) != cudaSuccess) return e;
-  if ((e = launch_update(kp, s)) != cudaSuccess) return e;
-  return launch_advance(kp, cond, s);
-}
-
-cmtcs_status build_cg_graph(cmtcs_ctx *c) {
-  const KParams &kp = c->kp;
-  cudaGraph_t g = nullptr;
-  CUDA_OK(c, cudaGraphCreate(&g, 0));
-  c->cg_graph = g;
-  cudaGraphConditionalHandle h;
-  CUDA_OK(c, cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault));
-  cudaGraphNodeParams cp = {};
-  cp.type = cudaGraphNodeTypeConditional;
-  cp.conditional.handle = h;
-  cp.conditional.type = cudaGraphCondTypeWhile;
-  cp.conditional.size = 1;
-  cudaGraphNode_t node;
-  CUDA_OK(c, cudaGraphAddNode(&node, g, nullptr, 0, &cp));
-  cudaGraph_t body = cp.conditional.phGraph_out[0];
-  CUDA_OK(c, cudaStreamBeginCaptureToGraph(c->cap_stream, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
-  cudaError_t e4 = cudaSuccess;
-  for (int r = 0; r < c->unroll && e4 == cudaSuccess; ++r)   // CG steps per WHILE iteration
-    e4 = enqueue_cg_step(c, c->cap_stream, (unsigned long long)h);
-  cudaGraph_t captured = body;
-  CUDA_OK(c, cudaStreamEndCapture(c->cap_stream, &captured));
-  CUDA_OK(c, e4);
-  CUDA_OK(c, cudaGraphInstantiate(&c->cg_exec, g, 0));
-  return CMTCS_OK;
 }
 
 cmtcs_status one_em_iteration(cmtcs_ctx *c, const uint64_t *probe_bits, const double *q_override,
@@ -328,38 +278,22 @@ cmtcs_status one_em_iteration(cmtcs_ctx *c, const uint64_t *probe_bits, const do
   CUDA_OK(c, cudaMemsetAsync(kp.b.hist, 0, sizeof(int) * d.cap, s));
   CUDA_OK(c, cudaMemsetAsync(kp.b.histm, 0, sizeof(int) * d.cap, s));
   CUDA_OK(c, cudaMemsetAsync(kp.b.histt, 0, sizeof(int) * d.cap, s));
+  CUDA_OK(c, cudaMemsetAsync(kp.b.tmark, 0, sizeof(int) * d.Tl, s));
   CUDA_OK(c, launch_init_columns(kp, s));
   L += 1;
   const bool tm = c->timing;
   if (tm) {
-    CUDA_OK(c, cudaMemsetAsync(kp.b.ts, 0, sizeof(unsigned long long) * 4 * d.cap, s));
+    CUDA_OK(c, cudaMemsetAsync(kp.b.ts, 0, sizeof(unsigned long long) * (4 * d.cap + 256), s));
     CUDA_OK(c, cudaEventRecord(c->tev[0], s));
   }
-  // ---- batched CG (Alg. 1) over all T_loc·C·(K+1) columns: one graph launch, device-side loop ----
-  if (c->no_graph) {
-    // profiling mode (CMTCS_NO_GRAPH=1): the same kernels launched from a host loop so that
-    // per-launch tools (ncu) see them; convergence is checked every 8 steps
-    for (int u = 0; u < d.cap; ++u) {
-      CUDA_OK(c, enqueue_cg_step(c, s, 0ull));
-      if ((u & 7) == 7 || u + 1 == d.cap) {
-        CUDA_OK(c, cudaMemcpyAsync(c->h_u, kp.b.alive + u, sizeof(int), cudaMemcpyDeviceToHost, s));
-        CUDA_OK(c, cudaStreamSynchronize(s));
-        if (*c->h_u == 0) break;
-      }
-    }
-  } else {
-    if (!c->cg_exec) {
-      cmtcs_status st = build_cg_graph(c);
-      if (st != CMTCS_OK) return st;
-    }
-    CUDA_OK(c, cudaGraphLaunch(c->cg_exec, s));
-  }
+  // ---- batched CG (Alg. 1) over all T_loc·C·(K+1) columns: one persistent kernel ----
+  CUDA_OK(c, launch_cg_persistent(kp, c->maps, c->grid, s));
   if (tm) CUDA_OK(c, cudaEventRecord(c->tev[1], s));
   // ---- estimators: s (Eq. 5), ν̄ (Eq. 7-9), Φμ for ℓ, q and log-lik (Eq. 3) ----
   CUDA_OK(c, launch_diag(kp, s));
   CUDA_OK(c, launch_lanczos(kp.b.gam, kp.b.xi, kp.b.steps, d.Tl * d.P, d.cap, d.D, kp.b.tau, nullptr,
                             kp.b.status, s));
-  CUDA_OK(c, launch_mu_stage1(kp, kp.b.Xm, true, s));
+  CUDA_OK(c, launch_mu_stage1(kp, kp.b.Xm, s));
   CUDA_OK(c, launch_estep_finish(kp, s));
   // ---- M-step (Eq. 4): local sums → all-reduce over ranks → α update ----
   CUDA_OK(c, launch_mstep_partial(kp, s));
@@ -377,7 +311,7 @@ cmtcs_status one_em_iteration(cmtcs_ctx *c, const uint64_t *probe_bits, const do
   L += 4;
   if (tm) {
     CUDA_OK(c, cudaEventRecord(c->tev[2], s));
-    CUDA_OK(c, cudaMemcpyAsync(c->h_ts, kp.b.ts, sizeof(unsigned long long) * 4 * d.cap, cudaMemcpyDeviceToHost, s));
+    CUDA_OK(c, cudaMemcpyAsync(c->h_ts, kp.b.ts, sizeof(unsigned long long) * (4 * d.cap + 256), cudaMemcpyDeviceToHost, s));
   }
   CUDA_OK(c, cudaMemcpyAsync(c->h_u, kp.b.u, sizeof(int), cudaMemcpyDeviceToHost, s));
   CUDA_OK(c, cudaMemcpyAsync(c->h_out, kp.b.stats, 16 * sizeof(double), cudaMemcpyDeviceToHost, s));
@@ -388,16 +322,40 @@ cmtcs_status one_em_iteration(cmtcs_ctx *c, const uint64_t *probe_bits, const do
   c->launches += L;
   c->have_estep = true;
   const int steps_run = *c->h_u;
-  L += 4 * (int64_t)steps_run;  // stage 1, stage 2, update, advance per CG step
-  c->launches += 4 * (int64_t)steps_run;
+  L += 1;                       // the persistent CG kernel
+  c->launches += 1;
   if (tm) {
-    // per CG step: %globaltimer stamps of the first stage-1 CTA entry, the last stage-2 CTA exit
-    // and the last update-warp exit (device clock, ns)
+    // per CG step: %globaltimer stamps taken by CTA 0 after the grid barriers: step start,
+    // operator (phases 1-2) done, update (phase 3) done (device clock, ns)
     for (int u = 0; u < steps_run; ++u) {
       const unsigned long long *q = c->h_ts + 4 * u;
-      const unsigned long long t0 = ~q[0], t1 = q[1], t2 = q[2];
-      if (q[0] && t1 >= t0) c->t_ms[0] += (t1 - t0) * 1e-6;
+      const unsigned long long t0 = q[0], t1 = q[1], t2 = q[2];
+      if (t0 && t1 >= t0) c->t_ms[0] += (t1 - t0) * 1e-6;
       if (t1 && t2 >= t1) c->t_ms[1] += (t2 - t1) * 1e-6;
+    }
+    if (getenv("CMTCS_PHASE_LOG")) {   // diagnostic: mean per-step phase durations (device stamps)
+      double ph[3] = {0, 0, 0};
+      for (int u = 0; u < steps_run; ++u) {
+        const unsigned long long *q = c->h_ts + 4 * u;
+        ph[0] += (q[3] - q[0]) * 1e-3;
+        ph[1] += (q[1] - q[3]) * 1e-3;
+        ph[2] += (q[2] - q[1]) * 1e-3;
+      }
+      fprintf(stderr, "[cmtcs] EM it %d: %d CG steps, per step us: phase1 %.2f phase2 %.2f update %.2f\n",
+              c->em_iter, steps_run, ph[0] / steps_run, ph[1] / steps_run, ph[2] / steps_run);
+      for (int ph = 0; ph < 2 && steps_run > 5; ++ph) {
+        const unsigned long long *g = c->h_ts + 4 * d.cap + 128 * ph;
+        const unsigned long long t0 = c->h_ts[4 * 5 + (ph ? 3 : 0)];
+        auto us = [&](int i) { return g[i] ? ((double)g[i] - (double)t0) * 1e-3 : -1.0; };
+        fprintf(stderr, "[cmtcs]   phase %d CTA0 unit0 (us): prod start %.2f epi start %.2f\n", ph + 1, us(84), us(83));
+        fprintf(stderr, "[cmtcs]     prod acq :"); for (int i = 0; i < 16; ++i) fprintf(stderr, " %.2f", us(i));
+        fprintf(stderr, "\n[cmtcs]     prod iss :"); for (int i = 16; i < 32; ++i) fprintf(stderr, " %.2f", us(i));
+        fprintf(stderr, "\n[cmtcs]     mma full :"); for (int i = 32; i < 48; ++i) fprintf(stderr, " %.2f", us(i));
+        fprintf(stderr, "\n[cmtcs]     epi full :"); for (int i = 64; i < 80; ++i) fprintf(stderr, " %.2f", us(i));
+        fprintf(stderr, "\n[cmtcs]     epi loopend %.2f meanepi %.2f tfull %.2f drained %.2f end %.2f\n", us(85), us(86), us(80), us(81), us(82));
+        fprintf(stderr, "[cmtcs]     drain    :"); for (int i = 90; i < 120; ++i) fprintf(stderr, " %.2f", us(i));
+        fprintf(stderr, "\n");
+      }
     }
     float ms = 0.f;
     CUDA_OK(c, cudaEventElapsedTime(&ms, c->tev[1], c->tev[2]));
@@ -486,12 +444,6 @@ cmtcs_status cmtcs_init(cmtcs_ctx **out, const cmtcs_problem *p, const float *ph
   c->rank = rank;
   c->world = world;
   c->em_iter = p->em_iter0;
-  {
-    const char *ng = getenv("CMTCS_NO_GRAPH");
-    c->no_graph = ng && ng[0] == '1';
-    const char *ur = getenv("CMTCS_GRAPH_UNROLL");
-    c->unroll = ur ? std::max(1, std::min(8, atoi(ur))) : 4;
-  }
   carve(d, (char *)workspace, &b);
   c->kp.d = d;
   c->kp.b = b;
@@ -505,17 +457,26 @@ cmtcs_status cmtcs_init(cmtcs_ctx **out, const cmtcs_problem *p, const float *ph
   c->kp.var_floor = p->var_floor;
   c->kp.empty_eps = p->empty_eps;
   c->kp.seed = p->probe_seed;
+  c->kp.dbg_flags = getenv("CMTCS_DBG") ? atoi(getenv("CMTCS_DBG")) : 0;
+  c->kp.lo_rn = getenv("CMTCS_LO_RN") ? atoi(getenv("CMTCS_LO_RN")) : 0;
   *out = c;  // from here on errors leave a (broken) ctx the caller destroys
   CUDA_OK(c, cudaMallocHost((void **)&c->h_out, 32 * sizeof(double)));
   CUDA_OK(c, cudaMallocHost((void **)&c->h_status, 8 * sizeof(int)));
-  CUDA_OK(c, cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking));
 
   CUDA_OK(c, cudaMallocHost((void **)&c->h_u, sizeof(int)));
-  CUDA_OK(c, cudaMallocHost((void **)&c->h_ts, sizeof(unsigned long long) * 4 * d.cap));
+  CUDA_OK(c, cudaMallocHost((void **)&c->h_ts, sizeof(unsigned long long) * (4 * d.cap + 256)));
   for (int i = 0; i < 3; ++i) CUDA_OK(c, cudaEventCreate(&c->tev[i]));
   CUDA_OK(c, cudaMemsetAsync(b.status, 0, 8 * sizeof(int), c->stream));
   CUDA_OK(c, cudaMemsetAsync(b.gam, 0, sizeof(double) * d.Tl * d.P * d.cap, c->stream));
   CUDA_OK(c, cudaMemsetAsync(b.xi, 0, sizeof(double) * d.Tl * d.P * d.cap, c->stream));
+  CUDA_OK(c, cudaMemsetAsync(b.Um, 0, sizeof(double) * (size_t)d.Tl * d.N * d.Cp, c->stream));
+  CUDA_OK(c, cudaMemsetAsync(b.tilecnt, 0, sizeof(int) * d.Tl * d.nCT * d.nRT1, c->stream));
+  c->grid = cg_grid_size(c->kp);
+  if (c->grid < 1) return fail(c, CMTCS_ECUDA, "persistent CG kernel cannot be made resident (smem %zu bytes)",
+                               tc_smem_bytes(c->kp.tc, d.P));
+  if (d.S1 > 1 && (long)d.Tl * d.nCT * d.nRT1 * d.S1 > c->grid)
+    return fail(c, CMTCS_ECUDA, "split-K stage 1 needs all %d units co-resident but the grid has %d CTAs",
+                d.Tl * d.nCT * d.nRT1 * d.S1, c->grid);
   // π: log π_c on device
   double *pi_dev = b.red;  // scratch: red is rewritten every M-step
   CUDA_OK(c, cudaMemcpyAsync(pi_dev, c->pi_host, sizeof(double) * p->C, cudaMemcpyHostToDevice, c->stream));
@@ -527,8 +488,8 @@ cmtcs_status cmtcs_init(cmtcs_ctx **out, const cmtcs_problem *p, const float *ph
   CUDA_OK(c, launch_split_phi(c->kp, c->stream));
   c->launches += 4;
   {
-    cmtcs_status st2 = encode_maps(c);
-    if (st2 != CMTCS_OK) return st2;
+    char why[256];
+    if (!encode_maps(c->kp, &c->maps, why)) return fail(c, CMTCS_ECUDA, "%s", why);
   }
   CUDA_OK(c, cudaStreamSynchronize(c->stream));
   if (world > 1) {
@@ -610,9 +571,6 @@ void cmtcs_destroy(cmtcs_ctx *c) {
   cudaSetDevice(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
   if (c->have_comm) ncclCommDestroy(c->comm);
-  if (c->cg_exec) cudaGraphExecDestroy(c->cg_exec);
-  if (c->cg_graph) cudaGraphDestroy(c->cg_graph);
-  if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
 
   for (int i = 0; i < 3; ++i)
     if (c->tev[i]) cudaEventDestroy(c->tev[i]);

@@ -15,19 +15,19 @@ constexpr int OP_BK = 16;       // mean-column (SIMT) contraction chunk
 constexpr int OP_THREADS = 256; // mean-column kernels
 constexpr int TC_THREADS = 128; // tensor-core probe kernels (4 warps = 128 TMEM lanes)
 constexpr int TC_NTMAX = 256;   // widest probe-column tile (MMA N ≤ 256)
-constexpr int UPD_THREADS = 256;  // 8 warps = 8 columns per CTA
 
 // Sizes of one rank's problem.  Column index of probe (c, k) inside a task: col = c*K + k.
 struct Dims {
   int T, Tl, t0, N, D, C, K;
   int P;     // probe columns per task = C*K
   int Pp;    // P rounded up to a multiple of 4 (row stride of U)
+  int Cp;    // C rounded up to even (row stride of Um: 16-byte TMA rows)
   int cap;   // CG step cap U
   int nw;    // 64-bit probe words per column = ceil(D/64)
   int nRT1;  // stage-1 row tiles  = ceil(N / OP_BR)
   int nRT2;  // stage-2 row tiles  = ceil(D / OP_BR)
   int nCT;   // probe column tiles = ceil(P / TcCfg::NT)
-  int S1;    // stage-1 split-K factor (fills the GPU when T·N is small)
+  int S1;    // stage-1 split-K factor (balances the persistent grid when T·N is small)
   int K1;    // stage-1 contraction length per split (multiple of OP_BK)
   int shared_phi;
   int64_t phi_task_stride;  // elements between Φ_t and Φ_{t+1} (0 if shared)
@@ -41,13 +41,14 @@ struct Bufs {
   double *logpi;     // [C]
   double *b64;       // [Tl][D]   βΦᵀy
   double *bnorm2;    // [Tl]      ‖b‖²
-  float *X, *R, *W;  // probe columns [Tl][P][D]
-  float *Dh, *Dl;    // probe directions d = Dh + Dl exactly (Dh = tf32(d)) [Tl][P][D]
+  float *X, *R, *W;  // probe columns [Tl][P][D]; W = Ad
+  float *Dh, *Dl;    // probe directions d = Dh + Dl exactly (Dh = tf32(d)) [Tl][P][D] (tensor-core operand)
+  float *D32;        // the same directions as plain fp32 [Tl][P][D] (epilogue / update operand)
   float *Phh, *Phl;  // Φ split: tf32 hi + fp32 lo   [Tl or 1][N][D]
   float *PTh, *PTl;  // Φᵀ split                     [Tl or 1][D][N]
   double *Xm, *Rm, *Dm, *Wm; // mean columns  [Tl][C][D]
   float *Uh, *Ul;    // stage-1 output split, [Tl][Pp][N] (row = compacted column j)
-  double *Um;        // [Tl][N][C]
+  double *Um;        // [Tl][N][Cp]
   double *rr;        // [Tl][P]
   double *rrm;       // [Tl][C]
   double *dAd;       // [Tl][P][nRT2]  per-row-tile partial dᵀAd
@@ -70,9 +71,14 @@ struct Bufs {
   int *histt;        // [cap]  tasks with an active column at step u
   int *status;       // [8]    first error: code, t, col, u
   int *u;            // [1]    current CG step (device-side loop counter of the CG graph)
-  unsigned long long *ts;  // [cap][4] per-step %globaltimer stamps: stage-1 first entry (min),
-                           //          stage-2 last exit, update last exit (max), unused
+  unsigned long long *ts;  // [cap][4] per-step %globaltimer stamps taken by CTA 0 after the grid
+                           //          barriers: step start, operator done, update done, unused
   double *stats;     // [16]   step statistics (filled by k_stats)
+  float *Upart;      // [Tl][S1][Pp][N]  stage-1 split-K partial tiles (S1 > 1)
+  double *Umpart;    // [Tl][S1][N][Cp]
+  int *tmark;        // [Tl]   last CG step (+1) at which the task had an active column
+  int *tilecnt;      // [Tl][nCT][nRT1]  split-K arrival counters (self re-arming)
+  unsigned *gridbar; // [1]    grid-barrier arrival counter of the persistent CG kernel
   int *assign;       // [Tl]
 };
 
@@ -83,13 +89,19 @@ struct TcCfg {
   int nacc;          // K-split accumulator pairs (2·nacc·slot ≤ 512)
   int stages;        // smem pipeline depth
   unsigned stage_bytes;
+  int use_dtile;     // stage-2 epilogue reads its d tile (NT × 128 fp32) from smem, staged by TMA
+  unsigned dtile_bytes;
 };
 
-// TMA descriptors (host-encoded, passed as __grid_constant__ kernel parameters)
+// TMA descriptors (host-encoded, passed as a __grid_constant__ kernel parameter)
 struct TcMaps {
-  CUtensorMap phi_h, phi_l;    // [rows Tl·N][cols D], box 32 × 128
-  CUtensorMap phit_h, phit_l;  // [rows Tl·D][cols N], box 32 × 128
-  CUtensorMap u_h, u_l;        // [rows Tl·Pp][cols N], box 32 × NT
+  CUtensorMap phi_h, phi_l;    // fp32 [rows Tl·N][cols D], box 32 × 128, SW128
+  CUtensorMap phit_h, phit_l;  // fp32 [rows Tl·D][cols N], box 32 × 128, SW128
+  CUtensorMap u_h, u_l;        // fp32 [rows Tl·Pp][cols N], box 32 × NT, SW128
+  CUtensorMap d_h, d_l;        // fp32 [rows Tl·P][cols D], box 32 × NT, SW128 (probe directions)
+  CUtensorMap dm;              // fp64 [rows Tl·C][cols D], box 32 × C (mean directions)
+  CUtensorMap um;              // fp64 [rows Tl·N][cols Cp], box Cp × 32 (Φ·d of the mean columns)
+  CUtensorMap d32;             // fp32 [rows Tl·P][cols D], box 128 × NT (probe directions, epilogue)
 };
 
 struct KParams {
@@ -106,17 +118,18 @@ struct KParams {
   int it;                      // global EM iteration index of this E-step
   const uint64_t *probe_bits;  // optional override
   const double *q_override;    // optional
+  int lo_rn;                   // tf32 split: lo rounded to nearest tf32 (1) or the exact fp32 remainder (0)
+  int dbg_flags;               // CMTCS_DBG (diagnostics only): 1 skip mean DFMA, 2 skip MMA, 4 skip B gather
 };
 
 // launchers (return cudaGetLastError())
 cudaError_t launch_init_columns(const KParams &p, cudaStream_t s);
-cudaError_t launch_stage1_tc(const KParams &p, const TcMaps &maps, cudaStream_t s);
-cudaError_t launch_stage2_tc(const KParams &p, const TcMaps &maps, cudaStream_t s);
 cudaError_t launch_split_phi(const KParams &p, cudaStream_t s);
 size_t tc_smem_bytes(const TcCfg &tc, int P);
-cudaError_t launch_mu_stage1(const KParams &p, const double *mu_src, bool mu_only, cudaStream_t s);
-cudaError_t launch_update(const KParams &p, cudaStream_t s);
-cudaError_t launch_advance(const KParams &p, unsigned long long cond_handle, cudaStream_t s);
+int cg_grid_size(const KParams &p);   // CTAs of the persistent CG kernel (one per SM), 0 on failure
+cudaError_t launch_cg_persistent(const KParams &p, const TcMaps &maps, int grid, cudaStream_t s);
+bool encode_maps(const KParams &p, TcMaps *maps, char *why);   // after the workspace is carved
+cudaError_t launch_mu_stage1(const KParams &p, const double *mu_src, cudaStream_t s);
 cudaError_t launch_rhs(const KParams &p, cudaStream_t s);
 cudaError_t launch_alpha_stats(const KParams &p, cudaStream_t s);
 cudaError_t launch_diag(const KParams &p, cudaStream_t s);

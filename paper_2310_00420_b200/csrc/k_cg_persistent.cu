@@ -1,0 +1,1103 @@
+// The batched conjugate-gradient loop of one E-step (Alg. 1, run for every task t,
+// cluster c and right-hand side of Alg. 2 lines 5-6) as ONE persistent kernel:
+// one CTA per SM, all CG steps of the EM iteration inside, three grid-wide phases per step.
+//
+//   phase 1 (K1, stage 1)  U[t][j][n] = Σ_d Φ_t[n][d] · D[t][j][d]                tensor cores (3xTF32)
+//   phase 2 (K1, stage 2)  W[t][j][d] = β Σ_n Φ_t[n][d] · U[t][j][n] + α_c ⊙ D   (PAPER.md:80, 157:
+//                          "A := βΦᵀΦ + diag(α)", ΦᵀΦ never formed) + fp64 partials of dᵀW
+//                          (dᵀAd is formed from the same W the residual update subtracts: computing it
+//                          as β‖Φd‖² + dᵀdiag(α)d instead is algebraically equal but inconsistent with
+//                          the rounded W, and measured 20x worse log-likelihood parity at C2)
+//   phase 3 (K4, update)   γ_u = rᵀr / dᵀAd; x += γd; r −= γAd; ξ_u = r'ᵀr'/rᵀr; d = r' + ξd;
+//                          convergence ‖r'‖ ≤ tol·‖b‖ (reading A5); transcript (γ_u, ξ_u)
+//
+// Phases are separated by a grid barrier (all CTAs co-resident: cooperative launch, one CTA per
+// SM); the work units of a phase (output tiles, columns) are dealt round-robin to the CTAs.  The
+// C fp64 mean columns of a task ride along with the task's column-tile-0 units: fp64 DFMA on the
+// CUDA cores, reading the same smem Φ tiles the tensor core reads.
+//
+// Warp roles in phases 1-2 (256 threads):
+//   warp 0     TMA producer: Φ/Φᵀ tiles (A), direction / U tiles (B), fp64 mean-column chunk
+//   warp 1     MMA issuer: tcgen05.mma kind::tf32, tcgen05.commit frees ring stages / the tile
+//   warp 2     TMEM owner (alloc / dealloc)
+//   warps 4-7  fp64 mean-column DFMA per ring stage, then the tile epilogue (TMEM → registers)
+// All operands arrive by TMA into an S-stage ring of 128-byte-swizzled K-major smem tiles, so no
+// CTA-wide barrier runs inside a K loop; the producer runs ahead into the next unit while the
+// epilogue of the previous one drains.  mbarriers: full[s] (TMA bytes), empty[s] (MMA done),
+// mdone[s] (fp64 warps done), tfull / tempty (accumulator handshake).
+//
+// 3xTF32: every operand x is the exact pair x = hi + lo with hi = tf32(x), and each K = 8 step issues
+//   acc_x += lo_A·hi_B + hi_A·lo_B ;  acc_m += hi_A·hi_B
+// into separate TMEM accumulators, themselves split over K into `nacc` pairs and summed in fp32 in
+// the epilogue (the tensor pipe's accumulation otherwise loses ~4 bits over long K;
+// tools/tc_gemm_test.cu measures 3.2e-5 → 5e-6 relative at K = 4096; fp32 serial FFMA: 2e-6).
+//
+// Columns are not compacted: a unit multiplies its whole column tile (retired columns included,
+// their results are ignored) and is skipped when none of its columns is active.  Stage 1 may split
+// the contraction over D (S1 > 1) to balance the grid; the S1 partial tiles are reduced through
+// global memory by the last-arriving CTA of the tile, in fixed order (deterministic).
+//
+// Memory ordering: every phase boundary is a grid barrier whose acquire fence (fence.acq_rel.gpu,
+// CCTL.IVALL in SASS) invalidates the SM's L1, so data written by other CTAs in earlier phases is
+// read with ordinary loads; TMA reads of such data follow fence.proxy.async.  Split-K partials,
+// exchanged within a phase, are read with ld.global.cg after the tile counter's acquire.
+#include <stdio.h>
+
+#include "cmtcs_internal.cuh"
+#include "umma.cuh"
+
+namespace cmtcs {
+
+using namespace umma;
+
+namespace {
+
+constexpr int TM = 128;                   // tile rows (MMA M)
+constexpr int TK = 32;                    // K per pipeline stage (one 128-byte swizzled row)
+constexpr uint32_t A_BYTES = TM * 128;    // 16 KB per hi / lo A tile
+constexpr int MAXST = 4;
+constexpr int NTHREADS = 256;
+constexpr int EPI0 = 128;                 // first thread of the epilogue / fp64 warps (4-7)
+
+struct PSmemTail {
+  uint64_t full[MAXST], empty[MAXST], mdone[MAXST];
+  uint64_t tfull, tempty;
+  uint64_t dfull, dempty;             // the stage-2 epilogue's d tile (TMA bytes / epilogue done)
+  uint32_t tslot;
+  uint32_t emask[4][TC_NTMAX / 32];   // per epilogue warp: active-column mask of its current tile
+  double red[4][TC_NTMAX + MAXC];     // per epilogue warp: dᵀAd partials, probe [0, NT), mean [NT_MAX, +C)
+};
+
+template <class T>
+__device__ __forceinline__ T ldv(const T *p) { return *p; }
+template <class T>
+__device__ __forceinline__ void stv(T *p, T v) { *p = v; }
+
+__device__ __forceinline__ void fence_proxy_async_global() {
+  asm volatile("fence.proxy.async.global;\n" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *mbar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(mbar)) : "memory");
+}
+// named barrier among the 4 epilogue warps
+__device__ __forceinline__ void epi_sync() { asm volatile("bar.sync 1, 128;\n" ::: "memory"); }
+
+// grid-wide barrier over the co-resident CTAs: a monotonically increasing arrival counter
+// (reset to 0 before every launch); epoch e completes when the counter reaches e·gridDim.x
+__device__ __forceinline__ void grid_sync(unsigned *bar, unsigned &epoch) {
+  fence_proxy_async_global();                 // this thread's generic writes → later TMA reads
+  __syncthreads();
+  epoch += 1;
+  if (threadIdx.x == 0) {
+    const unsigned target = epoch * gridDim.x;
+    __threadfence();
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;\n" ::"l"(bar) : "memory");
+    unsigned v;
+    do {   // relaxed polling (no L1 invalidation per poll), one acquire fence once released
+      asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(bar) : "memory");
+    } while (v < target);
+    asm volatile("fence.acq_rel.gpu;\n" ::: "memory");
+  }
+  __syncthreads();
+}
+
+// Sums v[0..15] over the 32 lanes of a warp with 16 shuffles (butterfly transpose-reduce); the
+// total of value index `idx` ends in the even lane with idx = bits 4..1 of the lane id.
+__device__ __forceinline__ double warp_reduce16(double *v, int lane, int *idx) {
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const bool up = lane & 16;
+    const double send = up ? v[i] : v[i + 8], keep = up ? v[i + 8] : v[i];
+    v[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const bool up = lane & 8;
+    const double send = up ? v[i] : v[i + 4], keep = up ? v[i + 4] : v[i];
+    v[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+  }
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const bool up = lane & 4;
+    const double send = up ? v[i] : v[i + 2], keep = up ? v[i + 2] : v[i];
+    v[i] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+  }
+  {
+    const bool up = lane & 2;
+    const double send = up ? v[0] : v[1], keep = up ? v[1] : v[0];
+    v[0] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
+  }
+  v[0] += __shfl_xor_sync(0xffffffffu, v[0], 1);
+  *idx = ((lane >> 4) & 1) * 8 + ((lane >> 3) & 1) * 4 + ((lane >> 2) & 1) * 2 + ((lane >> 1) & 1);
+  return v[0];
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// low part of the tf32 split x = hi + lo: exact fp32 remainder (the tensor core then truncates it to
+// tf32) or, with lrn, the remainder rounded to nearest tf32 (unbiased; x = hi + lo to 2^-22 relative)
+__device__ __forceinline__ float tf32_lo(float x, float hi, int lrn) {
+  const float r = x - hi;
+  return lrn ? tf32_hi(r) : r;
+}
+
+// K-split accumulator pairs of a tile: one for short contractions (K ≤ 512), else up to tc.nacc
+__device__ __forceinline__ int unit_nacc(const TcCfg &tc, int nk, int dbg) {
+  return (nk <= 16 && !(dbg & 8)) ? 1 : min(tc.nacc, nk);
+}
+
+// TMEM accumulator column of pair q, term x (0 = main hi·hi, 1 = cross terms)
+__device__ __forceinline__ uint32_t acc_col(int q, int x, int slot) { return (uint32_t)((2 * q + x) * slot); }
+
+// issue the 3xTF32 MMAs of one K = 32 stage (one thread)
+__device__ __forceinline__ void mma_stage(uint32_t tmem, unsigned char *base, uint32_t b_bytes, uint32_t idesc,
+                                          int q, int slot, bool first_of_acc) {
+  const uint64_t ah = desc_sw128(smem_u32(base)), al = desc_sw128(smem_u32(base + A_BYTES));
+  const uint64_t bh = desc_sw128(smem_u32(base + 2 * A_BYTES));
+  const uint64_t bl = desc_sw128(smem_u32(base + 2 * A_BYTES + b_bytes));
+  const uint32_t tm_m = tmem + acc_col(q, 0, slot), tm_x = tmem + acc_col(q, 1, slot);
+#pragma unroll
+  for (int k8 = 0; k8 < TK / 8; ++k8) {
+    const uint64_t o = (uint64_t)(k8 * 32) >> 4;  // +32 bytes per K = 8 step inside the swizzled row
+    const uint32_t acc = (first_of_acc && k8 == 0) ? 0u : 1u;
+    mma_tf32(tm_x, al + o, bh + o, idesc, acc);
+    mma_tf32(tm_x, ah + o, bl + o, idesc, 1u);
+    mma_tf32(tm_m, ah + o, bh + o, idesc, acc);
+  }
+}
+
+// 16 accumulator columns [c0, c0+16) of this thread's row, summed over the K-split pairs: all
+// tcgen05.ld of the group are issued before one wait::ld
+__device__ __forceinline__ void tmem_ld16_nowait(uint32_t taddr, uint32_t *r) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void acc_load16(uint32_t tmem, int ew, int c0, int nacc, int slot, float *tot) {
+  const uint32_t lane_base = tmem + ((uint32_t)(ew * 32) << 16) + c0;
+  uint32_t m0[16], x0[16];
+  tmem_ld16_nowait(lane_base + acc_col(0, 1, slot), x0);
+  tmem_ld16_nowait(lane_base + acc_col(0, 0, slot), m0);
+  if (nacc == 1) {
+    asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 16; ++i) tot[i] = __uint_as_float(x0[i]) + __uint_as_float(m0[i]);
+    return;
+  }
+  uint32_t m1[16], x1[16];
+  tmem_ld16_nowait(lane_base + acc_col(1, 1, slot), x1);
+  tmem_ld16_nowait(lane_base + acc_col(1, 0, slot), m1);
+  asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 16; ++i) tot[i] = __uint_as_float(x0[i]) + __uint_as_float(x1[i]);   // cross terms first
+  for (int q = 2; q < nacc; ++q) {
+    tmem_ld16_nowait(lane_base + acc_col(q, 1, slot), x1);
+    asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 16; ++i) tot[i] += __uint_as_float(x1[i]);
+  }
+#pragma unroll
+  for (int i = 0; i < 16; ++i) tot[i] += __uint_as_float(m0[i]);
+#pragma unroll
+  for (int i = 0; i < 16; ++i) tot[i] += __uint_as_float(m1[i]);
+  for (int q = 2; q < nacc; ++q) {
+    tmem_ld16_nowait(lane_base + acc_col(q, 0, slot), m1);
+    asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 16; ++i) tot[i] += __uint_as_float(m1[i]);
+  }
+}
+
+// Active-column bitmask of a column tile (bit c ⇔ column j0+c has flag 1), computed by one warp
+// from flags written by other CTAs in the previous update phase; NT ≤ 256 → 8 words.
+__device__ __forceinline__ int tile_mask(const int *flag, int ncol, int lane, uint32_t *mask) {
+  int cnt = 0;
+#pragma unroll
+  for (int w = 0; w < TC_NTMAX / 32; ++w) {
+    const int c = w * 32 + lane;
+    const int f = (c < ncol) ? (ldv(flag + c) == 1) : 0;
+    mask[w] = __ballot_sync(0xffffffffu, f);
+    cnt += __popc(mask[w]);
+  }
+  return cnt;
+}
+__device__ __forceinline__ int mean_count(const int *flagm, int C, int lane) {
+  const int f = (lane < C) ? (ldv(flagm + lane) == 1) : 0;
+  return __popc(__ballot_sync(0xffffffffu, f));
+}
+
+__device__ __forceinline__ float4 lds128(uint32_t a) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];\n" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ double2 lds_d2(uint32_t a) {
+  double2 v;
+  asm volatile("ld.shared.v2.f64 {%0,%1}, [%2];\n" : "=d"(v.x), "=d"(v.y) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ double lds_d(uint32_t a) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1];\n" : "=d"(v) : "r"(a));
+  return v;
+}
+
+// fp64 mean-column work of one ring stage for tile row r: acc[c] += Σ_k Φ[r][k]·B(c, k), Φ = hi + lo
+// exactly (fp32).  Stage 1 reads B as [c][32] (Dm chunk), stage 2 as [32][Cp] (Um chunk).
+// CC ≥ C is a compile-time bound (fully unrolled, accumulators in registers, c ≥ C predicated off).
+template <bool B_CK, int CC>
+__device__ __forceinline__ void mean_stage(uint32_t a_hi, uint32_t mb, int r, int C, int Cp, double *acc) {
+#pragma unroll
+  for (int cc = 0; cc < TK / 4; ++cc) {
+    const float4 h = lds128(a_hi + sw128_offset(r, cc));
+    const float4 l = lds128(a_hi + A_BYTES + sw128_offset(r, cc));
+    const double a[4] = {(double)(h.x + l.x), (double)(h.y + l.y), (double)(h.z + l.z), (double)(h.w + l.w)};
+#pragma unroll
+    for (int c = 0; c < CC; ++c) {
+      if (c < C) {
+        if (B_CK) {
+          const double2 b01 = lds_d2(mb + (uint32_t)(c * TK + 4 * cc) * 8);
+          const double2 b23 = lds_d2(mb + (uint32_t)(c * TK + 4 * cc + 2) * 8);
+          acc[c] = fma(a[0], b01.x, acc[c]);
+          acc[c] = fma(a[1], b01.y, acc[c]);
+          acc[c] = fma(a[2], b23.x, acc[c]);
+          acc[c] = fma(a[3], b23.y, acc[c]);
+        } else {
+#pragma unroll
+          for (int i = 0; i < 4; ++i) acc[c] = fma(a[i], lds_d(mb + (uint32_t)((4 * cc + i) * Cp + c) * 8), acc[c]);
+        }
+      }
+    }
+  }
+}
+
+// Per-unit geometry shared by all roles (computed redundantly by every warp).
+struct Unit {
+  int stage;          // 1 or 2
+  int t, ct, rt, sp;
+  int ncol;           // columns of the tile (≤ NT)
+  int nmma;           // MMA N (0: no probe work)
+  bool mean;          // fp64 mean columns ride along
+  int nk;             // K chunks
+  int k0;             // first K element
+  int arow, brow;     // TMA row coordinates of A and B
+};
+
+__device__ void report(int *status, int code, int t, int col, int u) {
+  if (atomicCAS(status, 0, code) == 0) {
+    status[1] = t;
+    status[2] = col;
+    status[3] = u;
+  }
+}
+
+// ---- phase 3 -----------------------------------------------------------------------------------
+// Alg. 1 lines 3-7 for one probe column by one warp (fp32 vectors, fp64 scalars and dots)
+__device__ void update_probe(const KParams &p, int t, int col, int u, int lane) {
+  const Dims &d = p.d;
+  const size_t g = (size_t)t * d.P + col;
+  double dAd = 0.0;
+  for (int i = 0; i < d.nRT2; ++i) dAd += ldv(p.b.dAd + g * d.nRT2 + i);
+  const double rr = ldv(p.b.rr + g);
+  if (!(dAd > 0.0)) {  // Alg. 1 line 3 breakdown
+    if (lane == 0) {
+      report(p.b.status, ST_BREAKDOWN, d.t0 + t, col, u + 1);
+      p.b.flag[g] = 0;
+    }
+    return;
+  }
+  const double gam = rr / dAd;
+  float4 *x4 = reinterpret_cast<float4 *>(p.b.X + g * d.D);
+  float4 *r4 = reinterpret_cast<float4 *>(p.b.R + g * d.D);
+  float4 *dh4 = reinterpret_cast<float4 *>(p.b.Dh + g * d.D);
+  float4 *dl4 = reinterpret_cast<float4 *>(p.b.Dl + g * d.D);
+  float4 *d4 = reinterpret_cast<float4 *>(p.b.D32 + g * d.D);
+  const float4 *w4 = reinterpret_cast<const float4 *>(p.b.W + g * d.D);
+  const int n4 = d.D >> 2;
+  double acc = 0.0;
+  constexpr int U = 2;   // float4 per lane in flight (per array)
+  for (int i0 = lane; i0 < n4; i0 += 32 * U) {
+    float4 dd[U], wv[U], xv[U], rv[U];
+#pragma unroll
+    for (int v = 0; v < U; ++v) {
+      const int i = i0 + 32 * v;
+      if (i < n4) { dd[v] = ldv(d4 + i); wv[v] = ldv(w4 + i); xv[v] = ldv(x4 + i); rv[v] = ldv(r4 + i); }
+    }
+#pragma unroll
+    for (int v = 0; v < U; ++v) {
+      const int i = i0 + 32 * v;
+      if (i < n4) {
+        const float4 dv = dd[v];
+        const float4 ad = wv[v];            // Ad from the operator's epilogue
+        float4 x = xv[v], r = rv[v];
+        x.x = (float)fma(gam, (double)dv.x, (double)x.x);
+        x.y = (float)fma(gam, (double)dv.y, (double)x.y);
+        x.z = (float)fma(gam, (double)dv.z, (double)x.z);
+        x.w = (float)fma(gam, (double)dv.w, (double)x.w);
+        r.x = (float)fma(-gam, (double)ad.x, (double)r.x);
+        r.y = (float)fma(-gam, (double)ad.y, (double)r.y);
+        r.z = (float)fma(-gam, (double)ad.z, (double)r.z);
+        r.w = (float)fma(-gam, (double)ad.w, (double)r.w);
+        stv(x4 + i, x);
+        stv(r4 + i, r);
+        acc += (double)r.x * r.x + (double)r.y * r.y + (double)r.z * r.z + (double)r.w * r.w;
+      }
+    }
+  }
+  const double rrn = warp_sum(acc);
+  const double xi = rrn / rr;
+  const bool conv = sqrt(rrn) <= p.tol * sqrt((double)d.D);
+  const bool stop = conv || (u + 1 >= d.cap);
+  if (lane == 0) {
+    p.b.gam[g * d.cap + u] = gam;
+    p.b.xi[g * d.cap + u] = xi;
+    p.b.steps[g] = u + 1;
+    p.b.rr[g] = rrn;
+    if (stop) p.b.flag[g] = conv ? 0 : 2;
+    else atomicAdd(p.b.alive + u, 1);
+  }
+  if (!stop) {
+    __syncwarp();
+    const int lrn = p.lo_rn;
+    for (int i0 = lane; i0 < n4; i0 += 32 * U) {
+      float4 rv[U], dd[U];
+#pragma unroll
+      for (int v = 0; v < U; ++v) {
+        const int i = i0 + 32 * v;
+        if (i < n4) { rv[v] = ldv(r4 + i); dd[v] = ldv(d4 + i); }
+      }
+#pragma unroll
+      for (int v = 0; v < U; ++v) {
+        const int i = i0 + 32 * v;
+        if (i < n4) {
+          float4 dv = dd[v];
+          dv.x = (float)fma(xi, (double)dv.x, (double)rv[v].x);
+          dv.y = (float)fma(xi, (double)dv.y, (double)rv[v].y);
+          dv.z = (float)fma(xi, (double)dv.z, (double)rv[v].z);
+          dv.w = (float)fma(xi, (double)dv.w, (double)rv[v].w);
+          // store d_{u+1} as the exact pair (tf32(d), d − tf32(d)) the tensor-core operator reads
+          float4 h4;
+          h4.x = tf32_hi(dv.x); h4.y = tf32_hi(dv.y); h4.z = tf32_hi(dv.z); h4.w = tf32_hi(dv.w);
+          stv(dh4 + i, h4);
+          stv(d4 + i, dv);
+          stv(dl4 + i, make_float4(tf32_lo(dv.x, h4.x, lrn), tf32_lo(dv.y, h4.y, lrn), tf32_lo(dv.z, h4.z, lrn), tf32_lo(dv.w, h4.w, lrn)));
+        }
+      }
+    }
+  }
+}
+
+// the same for one fp64 mean column
+__device__ void update_mean(const KParams &p, int t, int c, int u, int lane) {
+  const Dims &d = p.d;
+  const size_t g = (size_t)t * d.C + c;
+  double dAd = 0.0;
+  for (int i = 0; i < d.nRT2; ++i) dAd += ldv(p.b.dAdm + g * d.nRT2 + i);
+  const double rr = ldv(p.b.rrm + g);
+  if (!(dAd > 0.0)) {
+    if (lane == 0) {
+      report(p.b.status, ST_BREAKDOWN, d.t0 + t, -1 - c, u + 1);
+      p.b.flagm[g] = 0;
+    }
+    return;
+  }
+  const double gam = rr / dAd;
+  double2 *x = reinterpret_cast<double2 *>(p.b.Xm + g * d.D);
+  double2 *r = reinterpret_cast<double2 *>(p.b.Rm + g * d.D);
+  double2 *dv = reinterpret_cast<double2 *>(p.b.Dm + g * d.D);
+  const double2 *w = reinterpret_cast<const double2 *>(p.b.Wm + g * d.D);
+  const int n2 = d.D >> 1;
+  double acc = 0.0;
+  constexpr int U = 4;
+  for (int i0 = lane; i0 < n2; i0 += 32 * U) {
+    double2 dd[U], ww[U], xx[U], rn[U];
+#pragma unroll
+    for (int v = 0; v < U; ++v) {
+      const int i = i0 + 32 * v;
+      if (i < n2) { dd[v] = ldv(dv + i); ww[v] = ldv(w + i); xx[v] = ldv(x + i); rn[v] = ldv(r + i); }
+    }
+#pragma unroll
+    for (int v = 0; v < U; ++v) {
+      const int i = i0 + 32 * v;
+      if (i < n2) {
+        const double adx = ww[v].x, ady = ww[v].y;
+        xx[v].x = fma(gam, dd[v].x, xx[v].x);
+        xx[v].y = fma(gam, dd[v].y, xx[v].y);
+        rn[v].x = fma(-gam, adx, rn[v].x);
+        rn[v].y = fma(-gam, ady, rn[v].y);
+        stv(x + i, xx[v]);
+        stv(r + i, rn[v]);
+        acc = fma(rn[v].x, rn[v].x, acc);
+        acc = fma(rn[v].y, rn[v].y, acc);
+      }
+    }
+  }
+  const double rrn = warp_sum(acc);
+  const double xi = rrn / rr;
+  const bool conv = sqrt(rrn) <= p.tol_mean * sqrt(p.b.bnorm2[t]);
+  const bool stop = conv || (u + 1 >= d.cap);
+  if (lane == 0) {
+    p.b.stepsm[g] = u + 1;
+    p.b.rrm[g] = rrn;
+    if (stop) p.b.flagm[g] = conv ? 0 : 2;
+    else atomicAdd(p.b.alive + u, 1);
+  }
+  if (!stop) {
+    __syncwarp();
+    for (int i0 = lane; i0 < n2; i0 += 32 * U) {
+      double2 rn[U], dd[U];
+#pragma unroll
+      for (int v = 0; v < U; ++v) {
+        const int i = i0 + 32 * v;
+        if (i < n2) { rn[v] = ldv(r + i); dd[v] = ldv(dv + i); }
+      }
+#pragma unroll
+      for (int v = 0; v < U; ++v) {
+        const int i = i0 + 32 * v;
+        if (i < n2) {
+          dd[v].x = fma(xi, dd[v].x, rn[v].x);
+          dd[v].y = fma(xi, dd[v].y, rn[v].y);
+          stv(dv + i, dd[v]);
+        }
+      }
+    }
+  }
+}
+
+// ---- unit geometry ---------------------------------------------------------------------------
+__device__ __forceinline__ Unit make_unit1(const Dims &d, const TcCfg &tc, int w) {
+  Unit x;
+  x.stage = 1;
+  if (d.shared_phi) {     // task fastest: concurrent units share the Φ tile in L2
+    x.t = w % d.Tl;
+    int r = w / d.Tl;
+    x.sp = r % d.S1; r /= d.S1;
+    x.rt = r % d.nRT1;
+    x.ct = r / d.nRT1;
+  } else {
+    x.sp = w % d.S1;
+    int r = w / d.S1;
+    x.rt = r % d.nRT1; r /= d.nRT1;
+    x.ct = r % d.nCT;
+    x.t = r / d.nCT;
+  }
+  const int j0 = x.ct * tc.NT;
+  x.ncol = min(tc.NT, d.P - j0);
+  x.k0 = x.sp * d.K1;
+  const int ke = min(d.D, x.k0 + d.K1);
+  x.nk = (ke - x.k0 + TK - 1) / TK;
+  x.arow = (d.shared_phi ? 0 : x.t * d.N) + x.rt * TM;
+  x.brow = x.t * d.P + j0;
+  return x;
+}
+__device__ __forceinline__ Unit make_unit2(const Dims &d, const TcCfg &tc, int w) {
+  Unit x;
+  x.stage = 2;
+  x.sp = 0;
+  if (d.shared_phi) {
+    x.t = w % d.Tl;
+    const int r = w / d.Tl;
+    x.rt = r % d.nRT2;
+    x.ct = r / d.nRT2;
+  } else {
+    x.rt = w % d.nRT2;
+    const int r = w / d.nRT2;
+    x.ct = r % d.nCT;
+    x.t = r / d.nCT;
+  }
+  const int j0 = x.ct * tc.NT;
+  x.ncol = min(tc.NT, d.P - j0);
+  x.k0 = 0;
+  x.nk = (d.N + TK - 1) / TK;
+  x.arow = (d.shared_phi ? 0 : x.t * d.D) + x.rt * TM;
+  x.brow = x.t * d.Pp + j0;
+  return x;
+}
+
+// which work the unit has (every warp evaluates it from the same settled flags)
+__device__ __forceinline__ void unit_work(const KParams &p, Unit &x, int lane, uint32_t *mask) {
+  const Dims &d = p.d;
+  const int j0 = x.ct * p.tc.NT;
+  const int m = tile_mask(p.b.flag + (size_t)x.t * d.P + j0, x.ncol, lane, mask);
+  x.nmma = m ? ((x.ncol + 15) & ~15) : 0;
+  x.mean = x.ct == 0 && mean_count(p.b.flagm + (size_t)x.t * d.C, d.C, lane) > 0;
+}
+
+// ring: chunk G lives in stage G % S; full / empty / mdone phase of chunk G is G / S
+struct RingCtl {
+  int S;
+  uint32_t g;      // chunks handled so far by this role
+  uint32_t ti;     // accumulator tiles handled so far (tfull / tempty phases)
+  uint32_t di;     // stage-2 d tiles handled so far (dfull / dempty phases)
+};
+
+// ---- producer (warp 0, one lane) ---------------------------------------------------------------
+__device__ __forceinline__ void produce(const KParams &p, const TcMaps &mp, unsigned char *sm, PSmemTail &tl,
+                                        RingCtl &rc, const Unit &x, unsigned long long *tr) {
+  if (tr) tr[84] = globaltimer();
+  const uint32_t b_bytes = (uint32_t)p.tc.NT * 128;
+  const uint32_t mean_tx = x.stage == 1 ? (uint32_t)p.d.C * TK * 8 : (uint32_t)TK * p.d.Cp * 8;
+  const uint32_t bytes = 2 * A_BYTES + (x.nmma ? 2 * b_bytes : 0) + (x.mean ? mean_tx : 0);
+  if (x.stage == 2 && x.nmma && p.tc.use_dtile) {
+    // the epilogue's d tile: rows d0..d0+127 of the tile's NT direction columns
+    if (rc.di > 0) mbar_wait(&tl.dempty, (rc.di - 1) & 1);
+    unsigned char *dt = sm + (size_t)rc.S * p.tc.stage_bytes;
+    mbar_arrive_expect_tx(&tl.dfull, p.tc.dtile_bytes);
+    tma_load_2d(dt, &mp.d32, x.rt * TM, x.t * p.d.P + x.ct * p.tc.NT, &tl.dfull);
+    rc.di++;
+  }
+  for (int kc = 0; kc < x.nk; ++kc) {
+    const uint32_t G = rc.g++;
+    const int st = G % rc.S;
+    if (G >= (uint32_t)rc.S) {
+      const uint32_t ph = ((G - rc.S) / rc.S) & 1;
+      mbar_wait(&tl.empty[st], ph);
+      mbar_wait(&tl.mdone[st], ph);
+    }
+    if (tr && kc < 16) tr[kc] = globaltimer();
+    unsigned char *base = sm + (size_t)st * p.tc.stage_bytes;
+    uint64_t *fb = &tl.full[st];
+    mbar_arrive_expect_tx(fb, bytes);
+    const int k = x.k0 + kc * TK;
+    if (x.stage == 1) {
+      tma_load_2d(base, &mp.phi_h, k, x.arow, fb);
+      tma_load_2d(base + A_BYTES, &mp.phi_l, k, x.arow, fb);
+      if (x.nmma) {
+        tma_load_2d(base + 2 * A_BYTES, &mp.d_h, k, x.brow, fb);
+        tma_load_2d(base + 2 * A_BYTES + b_bytes, &mp.d_l, k, x.brow, fb);
+      }
+      if (x.mean) tma_load_2d(base + 2 * A_BYTES + 2 * b_bytes, &mp.dm, k, x.t * p.d.C, fb);
+    } else {
+      tma_load_2d(base, &mp.phit_h, k, x.arow, fb);
+      tma_load_2d(base + A_BYTES, &mp.phit_l, k, x.arow, fb);
+      if (x.nmma) {
+        tma_load_2d(base + 2 * A_BYTES, &mp.u_h, k, x.brow, fb);
+        tma_load_2d(base + 2 * A_BYTES + b_bytes, &mp.u_l, k, x.brow, fb);
+      }
+      if (x.mean) tma_load_2d(base + 2 * A_BYTES + 2 * b_bytes, &mp.um, 0, x.t * p.d.N + k, fb);
+    }
+    if (tr && kc < 16) tr[16 + kc] = globaltimer();
+  }
+}
+
+// ---- MMA issuer (warp 1, one lane) ---------------------------------------------------------------
+__device__ __forceinline__ void mma_unit(const KParams &p, unsigned char *sm, PSmemTail &tl, RingCtl &rc,
+                                         uint32_t tmem, const Unit &x, unsigned long long *tr) {
+  const TcCfg &tc = p.tc;
+  const uint32_t b_bytes = (uint32_t)tc.NT * 128;
+  const int nacc = unit_nacc(tc, x.nk, p.dbg_flags);
+  const uint32_t idesc = idesc_tf32(TM, x.nmma > 0 ? x.nmma : 16);
+  if (x.nmma && rc.ti > 0) {
+    mbar_wait(&tl.tempty, (rc.ti - 1) & 1);   // the epilogue has drained the previous tile
+    fence_after_sync();
+  }
+  for (int kc = 0; kc < x.nk; ++kc) {
+    const uint32_t G = rc.g++;
+    const int st = G % rc.S;
+    mbar_wait(&tl.full[st], (G / rc.S) & 1);
+    if (tr && kc < 16) tr[32 + kc] = globaltimer();
+    if (x.nmma && !(p.dbg_flags & 2)) {
+      fence_after_sync();
+      const int q = (kc * nacc) / x.nk;
+      const int qfirst = (q * x.nk + nacc - 1) / nacc;
+      mma_stage(tmem, sm + (size_t)st * tc.stage_bytes, b_bytes, idesc, q, tc.slot, kc == qfirst);
+      mma_commit(&tl.empty[st]);
+    } else {
+      mbar_arrive(&tl.empty[st]);
+    }
+  }
+  if (x.nmma) {
+    if (p.dbg_flags & 2) mbar_arrive(&tl.tfull);
+    else mma_commit(&tl.tfull);              // all MMAs of the tile complete → accumulator ready
+    rc.ti++;
+  }
+}
+
+// ---- epilogue + fp64 warps (warps 4-7) ---------------------------------------------------------
+template <int CC>
+__device__ void epilogue_unit(const KParams &p, unsigned char *sm, PSmemTail &tl, RingCtl &rc, uint32_t tmem,
+                              const Unit &x, const uint32_t *mask_in, unsigned long long *tr) {
+  if (tr && threadIdx.x != EPI0) tr = nullptr;
+  if (tr) tr[83] = globaltimer();
+  const Dims &d = p.d;
+  const TcCfg &tc = p.tc;
+  const int et = threadIdx.x - EPI0, ew = et >> 5, lane = et & 31;
+  const int r = et;                          // tile row = TMEM lane
+  const int N = d.N, D = d.D, P = d.P, C = d.C;
+  const uint32_t b_bytes = (uint32_t)tc.NT * 128;
+  const uint32_t mu_off = 2 * A_BYTES + 2 * b_bytes;
+  const int nacc = unit_nacc(tc, x.nk, p.dbg_flags);
+  const int j0 = x.ct * tc.NT;
+  if (lane < TC_NTMAX / 32) {
+    uint32_t v = 0;
+#pragma unroll
+    for (int i = 0; i < TC_NTMAX / 32; ++i)
+      if (i == lane) v = mask_in[i];
+    tl.emask[ew][lane] = v;
+  }
+  __syncwarp();
+  const uint32_t *mask = tl.emask[ew];
+  double macc[CC];
+#pragma unroll
+  for (int c = 0; c < CC; ++c) macc[c] = 0.0;
+  // mainloop: fp64 mean-column DFMA on each stage (or just release it)
+  for (int kc = 0; kc < x.nk; ++kc) {
+    const uint32_t G = rc.g++;
+    const int st = G % rc.S;
+    mbar_wait(&tl.full[st], (G / rc.S) & 1);
+    if (tr && kc < 16) tr[64 + kc] = globaltimer();
+    if (x.mean && !(p.dbg_flags & 1)) {
+      const uint32_t base = smem_u32(sm) + (uint32_t)st * tc.stage_bytes;
+      if (x.stage == 1) mean_stage<true, CC>(base, base + mu_off, r, C, d.Cp, macc);
+      else mean_stage<false, CC>(base, base + mu_off, r, C, d.Cp, macc);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&tl.mdone[st]);
+  }
+  if (tr) tr[85] = globaltimer();
+  if (x.stage == 1) {
+    const int n = x.rt * TM + r;
+    float *Uh = p.b.Uh + (size_t)x.t * d.Pp * N, *Ul = p.b.Ul + (size_t)x.t * d.Pp * N;
+    float *part = p.b.Upart + ((size_t)x.t * d.S1 + x.sp) * d.Pp * N;
+    if (x.nmma) {
+      mbar_wait(&tl.tfull, rc.ti & 1);
+      if (tr) tr[80] = globaltimer();
+      fence_after_sync();
+      for (int c0 = 0; c0 < x.nmma; c0 += 16) {
+        float tot[16];
+        acc_load16(tmem, ew, c0, nacc, tc.slot, tot);
+        if (tr && c0 < 128) tr[90 + (c0 >> 4) * 2] = globaltimer();
+        if (n < N) {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const int c = c0 + i;
+            if (c < x.ncol) {
+              const size_t o = (size_t)(j0 + c) * N + n;
+              if (d.S1 == 1) {
+                const float h = tf32_hi(tot[i]);
+                Uh[o] = h;
+                Ul[o] = tf32_lo(tot[i], h, p.lo_rn);
+              } else {
+                stv(part + o, tot[i]);
+              }
+            }
+          }
+        }
+        if (tr && c0 < 128) tr[91 + (c0 >> 4) * 2] = globaltimer();
+      }
+      fence_before_sync();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tl.tempty);  // the MMA warp may overwrite the accumulator
+      rc.ti++;
+      if (tr) tr[81] = globaltimer();
+    }
+    if (x.mean && n < N) {
+#pragma unroll
+      for (int c = 0; c < CC; ++c)
+        if (c < C) {
+          if (d.S1 == 1) p.b.Um[((size_t)x.t * N + n) * d.Cp + c] = macc[c];
+          else stv(p.b.Umpart + (((size_t)x.t * d.S1 + x.sp) * N + n) * d.Cp + c, macc[c]);
+        }
+    }
+    if (d.S1 > 1) {
+      // The S1 split CTAs of this tile run in the same round (the host picks S1 > 1 only when all
+      // stage-1 units fit the grid): each arrives on the tile counter, waits for all S1 partials,
+      // then sums its 1/S1 share of the tile's rows in split order (deterministic).
+      __threadfence();
+      epi_sync();
+      if (et == 0) {
+        int *cnt = p.b.tilecnt + ((size_t)x.t * d.nCT + x.ct) * d.nRT1 + x.rt;
+        const int ticket = atomicAdd(cnt, 1);
+        const int target = (ticket / d.S1 + 1) * d.S1;
+        int v;
+        do {
+          asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];\n" : "=r"(v) : "l"(cnt) : "memory");
+        } while (v < target);
+        asm volatile("fence.acq_rel.gpu;\n" ::: "memory");
+      }
+      epi_sync();
+      if (tr) tr[86] = globaltimer();
+      const int n0 = x.rt * TM, rows = min(TM, N - n0);
+      const int rs = ((rows + d.S1 - 1) / d.S1 + 3) & ~3;     // rows of this split's share (×4)
+      const int rb = x.sp * rs, re = min(rows, rb + rs);
+      if (re > rb) {
+        const int r4n = (re - rb) >> 2;
+        const size_t split = (size_t)d.Pp * N;
+        const float *base = p.b.Upart + (size_t)x.t * d.S1 * split;
+        if (x.nmma) {
+          const int tot4 = x.ncol * r4n;
+          constexpr int V = 4;
+          for (int e0 = et; e0 < tot4; e0 += 128 * V) {
+            float4 acc4[V];
+            size_t off[V];
+#pragma unroll
+            for (int v = 0; v < V; ++v) {
+              const int e = min(e0 + 128 * v, tot4 - 1);
+              off[v] = (size_t)(j0 + e / r4n) * N + n0 + rb + 4 * (e % r4n);
+              acc4[v] = __ldcg(reinterpret_cast<const float4 *>(base + off[v]));
+            }
+            for (int sidx = 1; sidx < d.S1; ++sidx) {
+              float4 pv[V];
+#pragma unroll
+              for (int v = 0; v < V; ++v) pv[v] = __ldcg(reinterpret_cast<const float4 *>(base + sidx * split + off[v]));
+#pragma unroll
+              for (int v = 0; v < V; ++v) {
+                acc4[v].x += pv[v].x; acc4[v].y += pv[v].y; acc4[v].z += pv[v].z; acc4[v].w += pv[v].w;
+              }
+            }
+#pragma unroll
+            for (int v = 0; v < V; ++v) {
+              if (e0 + 128 * v < tot4) {
+                float4 h;
+                h.x = tf32_hi(acc4[v].x); h.y = tf32_hi(acc4[v].y); h.z = tf32_hi(acc4[v].z); h.w = tf32_hi(acc4[v].w);
+                *reinterpret_cast<float4 *>(Uh + off[v]) = h;
+                *reinterpret_cast<float4 *>(Ul + off[v]) =
+                    make_float4(tf32_lo(acc4[v].x, h.x, p.lo_rn), tf32_lo(acc4[v].y, h.y, p.lo_rn), tf32_lo(acc4[v].z, h.z, p.lo_rn), tf32_lo(acc4[v].w, h.w, p.lo_rn));
+              }
+            }
+          }
+        }
+        if (x.mean) {
+          const int nm = (re - rb) * d.Cp / 2;   // double2 elements of this share of Um
+          const double *mbase = p.b.Umpart + (size_t)x.t * d.S1 * N * d.Cp;
+          for (int e = et; e < nm; e += 128) {
+            const size_t o = (size_t)(n0 + rb) * d.Cp + 2 * e;
+            double2 v = make_double2(0.0, 0.0);
+            for (int sidx = 0; sidx < d.S1; ++sidx) {
+              const double2 pv = __ldcg(reinterpret_cast<const double2 *>(mbase + (size_t)sidx * N * d.Cp + o));
+              v.x += pv.x;
+              v.y += pv.y;
+            }
+            *reinterpret_cast<double2 *>(p.b.Um + (size_t)x.t * N * d.Cp + o) = v;
+          }
+        }
+      }
+    }
+    if (tr) tr[82] = globaltimer();
+    return;
+  }
+  // ---- stage 2 epilogue: W = β acc + α_c ⊙ d for row dd, fp64 partial dᵀW per column (this tile) ----
+  const int dd = x.rt * TM + r;
+  const bool rv = dd < D;
+  const float betaf = (float)p.beta;
+  if (x.mean) {
+    // mean columns (fp64): Wm = β·acc + α ⊙ dm, partial dᵀWm over this row tile
+    double dot[16];
+#pragma unroll
+    for (int c = 0; c < 16; ++c) {
+      dot[c] = 0.0;
+      if (c < CC && c < C && rv) {
+        const size_t o = ((size_t)x.t * C + c) * D + dd;
+        const double dmv = ldv(p.b.Dm + o);
+        const double wv = fma(p.beta, macc[c], p.b.alpha64[(size_t)c * D + dd] * dmv);
+        stv(p.b.Wm + o, wv);
+        dot[c] = dmv * wv;
+      }
+    }
+    int idx;
+    const double sum = warp_reduce16(dot, lane, &idx);
+    if ((lane & 1) == 0 && idx < C) tl.red[ew][TC_NTMAX + idx] = sum;
+  }
+  if (tr) tr[86] = globaltimer();
+  if (x.nmma) {
+    mbar_wait(&tl.tfull, rc.ti & 1);
+    if (tr) tr[80] = globaltimer();
+    fence_after_sync();
+    const size_t colbase = ((size_t)x.t * P + j0) * D + dd;
+    float aC[CC];                             // α_c at this row for the clusters of the tile's columns
+#pragma unroll
+    for (int c = 0; c < CC; ++c) aC[c] = (c < C && rv) ? p.b.alpha32[(size_t)c * D + dd] : 0.f;
+    const bool dts = tc.use_dtile;
+    const float *dtile = reinterpret_cast<const float *>(sm + (size_t)rc.S * tc.stage_bytes);
+    if (dts) {
+      mbar_wait(&tl.dfull, rc.di & 1);
+      rc.di++;
+    }
+    for (int c0 = 0; c0 < x.nmma; c0 += 16) {
+      float dv[16], al[16], tot[16];
+      const uint32_t mk = (mask[c0 >> 5] >> (c0 & 31)) & 0xFFFFu;
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const bool ok = ((mk >> i) & 1u) && rv;
+        dv[i] = ok ? (dts ? dtile[(c0 + i) * TM + r] : ldv(p.b.D32 + colbase + (size_t)(c0 + i) * D)) : 0.f;
+        const int cl = (j0 + c0 + i) / d.K;
+        float a = 0.f;
+#pragma unroll
+        for (int c = 0; c < CC; ++c) a = (c == cl) ? aC[c] : a;
+        al[i] = a;
+      }
+      if (tr && c0 < 128) tr[90 + (c0 >> 4) * 3] = globaltimer();
+      acc_load16(tmem, ew, c0, nacc, tc.slot, tot);
+      if (tr && c0 < 128) tr[91 + (c0 >> 4) * 3] = globaltimer();
+      double dot[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const float w = fmaf(betaf, tot[i], al[i] * dv[i]);
+        if (((mk >> i) & 1u) && rv) stv(p.b.W + colbase + (size_t)(c0 + i) * D, w);
+        dot[i] = (double)dv[i] * (double)w;
+      }
+      int idx;
+      const double sum = warp_reduce16(dot, lane, &idx);
+      if ((lane & 1) == 0) tl.red[ew][c0 + idx] = sum;
+      if (tr && c0 < 128) tr[92 + (c0 >> 4) * 3] = globaltimer();
+    }
+    fence_before_sync();
+    __syncwarp();
+    if (lane == 0) {
+      mbar_arrive(&tl.tempty);
+      if (dts) mbar_arrive(&tl.dempty);
+    }
+    rc.ti++;
+    if (tr) tr[81] = globaltimer();
+  }
+  epi_sync();
+  if (x.nmma)
+    for (int c = et; c < x.ncol; c += 128)
+      if ((mask[c >> 5] >> (c & 31)) & 1u)
+        stv(p.b.dAd + ((size_t)x.t * P + j0 + c) * d.nRT2 + x.rt,
+               tl.red[0][c] + tl.red[1][c] + tl.red[2][c] + tl.red[3][c]);
+  if (x.mean && et < C) {
+    const int jj = TC_NTMAX + et;
+    stv(p.b.dAdm + ((size_t)x.t * C + et) * d.nRT2 + x.rt, tl.red[0][jj] + tl.red[1][jj] + tl.red[2][jj] + tl.red[3][jj]);
+  }
+  epi_sync();                                 // tl.red is reused by the next unit
+  if (tr) tr[82] = globaltimer();
+}
+
+// ---------------------------------------------------------------------------------------------
+// the persistent CG kernel: grid = #SMs (cooperative), 256 threads, one CTA per SM
+// ---------------------------------------------------------------------------------------------
+template <int CC>
+__global__ void __launch_bounds__(NTHREADS, 1) k_cg_persistent(KParams p, const __grid_constant__ TcMaps mp) {
+  extern __shared__ __align__(1024) unsigned char tc_raw[];
+  unsigned char *sm = reinterpret_cast<unsigned char *>((reinterpret_cast<uintptr_t>(tc_raw) + 1023) & ~(uintptr_t)1023);
+  const Dims &d = p.d;
+  const TcCfg &tc = p.tc;
+  PSmemTail &tl = *reinterpret_cast<PSmemTail *>(sm + (size_t)tc.stages * tc.stage_bytes + tc.dtile_bytes);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int G = gridDim.x, b = blockIdx.x;
+  if (tid == 0) {
+    for (int s = 0; s < tc.stages; ++s) {
+      mbar_init(&tl.full[s], 1);
+      mbar_init(&tl.empty[s], 1);
+      mbar_init(&tl.mdone[s], 4);
+    }
+    mbar_init(&tl.tfull, 1);
+    mbar_init(&tl.tempty, 4);
+    mbar_init(&tl.dfull, 1);
+    mbar_init(&tl.dempty, 4);
+    fence_mbar_init();
+  }
+  if (warp == 0 && lane == 0) {
+    prefetch_tmap(&mp.phi_h); prefetch_tmap(&mp.phi_l); prefetch_tmap(&mp.phit_h); prefetch_tmap(&mp.phit_l);
+    prefetch_tmap(&mp.u_h); prefetch_tmap(&mp.u_l); prefetch_tmap(&mp.d_h); prefetch_tmap(&mp.d_l);
+    prefetch_tmap(&mp.dm); prefetch_tmap(&mp.um); prefetch_tmap(&mp.d32);
+  }
+  if (warp == 2) tmem_alloc<512>(&tl.tslot);
+  fence_before_sync();
+  __syncthreads();
+  fence_after_sync();
+  const uint32_t tmem = tl.tslot;
+  RingCtl rc{tc.stages, 0u, 0u, 0u};
+  unsigned epoch = 0;
+  unsigned *bar = p.b.gridbar;
+  const int n1 = d.Tl * d.nCT * d.nRT1 * d.S1, n2 = d.Tl * d.nCT * d.nRT2;
+  const int ncols = d.Tl * (d.P + d.C);
+  const bool producer = warp == 0 && lane == 0, issuer = warp == 1 && lane == 0, epi = warp >= 4;
+  const bool tile_role = warp == 0 || warp == 1 || epi;
+  for (int u = 0; u < d.cap; ++u) {
+    if (b == 0 && tid == 0) p.b.ts[4 * u + 0] = globaltimer();
+    // diagnostic trace of CTA 0's first unit of each phase at CG step 5 (CMTCS_PHASE_LOG)
+    unsigned long long *tr1 = (b == 0 && u == 5) ? p.b.ts + 4 * d.cap : nullptr;
+    unsigned long long *tr2 = tr1 ? tr1 + 128 : nullptr;
+    // ---- phase 1: U = Φ D ----
+    if (tile_role) {
+      for (int w = b; w < n1; w += G, tr1 = nullptr) {
+        Unit x = make_unit1(d, tc, w);
+        uint32_t mask[TC_NTMAX / 32];
+        unit_work(p, x, lane, mask);
+        if (!x.nmma && !x.mean) continue;
+        if (producer) produce(p, mp, sm, tl, rc, x, tr1);
+        else if (issuer) mma_unit(p, sm, tl, rc, tmem, x, tr1);
+        else if (epi) epilogue_unit<CC>(p, sm, tl, rc, tmem, x, mask, tr1);
+      }
+    }
+    grid_sync(bar, epoch);
+    if (b == 0 && tid == 0) p.b.ts[4 * u + 3] = globaltimer();
+    // ---- phase 2: W = βΦᵀU + αD, dᵀW partials ----
+    if (tile_role) {
+      for (int w = b; w < n2; w += G, tr2 = nullptr) {
+        Unit x = make_unit2(d, tc, w);
+        uint32_t mask[TC_NTMAX / 32];
+        unit_work(p, x, lane, mask);
+        if (!x.nmma && !x.mean) continue;
+        if (producer) produce(p, mp, sm, tl, rc, x, tr2);
+        else if (issuer) mma_unit(p, sm, tl, rc, tmem, x, tr2);
+        else if (epi) epilogue_unit<CC>(p, sm, tl, rc, tmem, x, mask, tr2);
+      }
+    }
+    grid_sync(bar, epoch);
+    if (b == 0 && tid == 0) p.b.ts[4 * u + 1] = globaltimer();
+    // ---- phase 3: CG update, one warp per active column ----
+    for (int w = b * (NTHREADS / 32) + warp; w < ncols; w += G * (NTHREADS / 32)) {
+      const int t = w / (d.P + d.C), j = w % (d.P + d.C);
+      bool active;
+      if (j < d.P) {
+        active = ldv(p.b.flag + (size_t)t * d.P + j) == 1;
+        if (active) {
+          if (lane == 0) atomicAdd(p.b.hist + u, 1);
+          update_probe(p, t, j, u, lane);
+        }
+      } else {
+        active = ldv(p.b.flagm + (size_t)t * d.C + (j - d.P)) == 1;
+        if (active) {
+          if (lane == 0) atomicAdd(p.b.histm + u, 1);
+          update_mean(p, t, j - d.P, u, lane);
+        }
+      }
+      if (active && lane == 0 && atomicMax(p.b.tmark + t, u + 1) < u + 1) atomicAdd(p.b.histt + u, 1);
+    }
+    grid_sync(bar, epoch);
+    if (b == 0 && tid == 0) {
+      p.b.ts[4 * u + 2] = globaltimer();
+      *p.b.u = u + 1;                          // CG steps executed
+    }
+    if (ldv(p.b.alive + u) == 0) break;     // grid-uniform: every CTA reads the settled count
+  }
+  fence_before_sync();
+  __syncthreads();
+  if (warp == 2) tmem_dealloc<512>(tmem);
+}
+
+// Φ → (Φhi, Φlo) and the transposed pair (Φᵀhi, Φᵀlo), once at init.  32×32 smem-tiled transpose.
+__global__ void k_split_phi(const float *__restrict__ phi, int rows, int cols, int mats, float *hi, float *lo,
+                            float *thi, float *tlo, int lrn) {
+  __shared__ float tile[32][33];
+  const int mat = blockIdx.z;
+  const int c0 = blockIdx.x * 32, r0 = blockIdx.y * 32;
+  const float *src = phi + (size_t)mat * rows * cols;
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int r = r0 + i, c = c0 + threadIdx.x;
+    float v = 0.f;
+    if (r < rows && c < cols) {
+      v = src[(size_t)r * cols + c];
+      const float h = tf32_hi(v);
+      hi[(size_t)mat * rows * cols + (size_t)r * cols + c] = h;
+      lo[(size_t)mat * rows * cols + (size_t)r * cols + c] = tf32_lo(v, h, lrn);
+    }
+    tile[i][threadIdx.x] = v;
+  }
+  __syncthreads();
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int c = c0 + i, r = r0 + threadIdx.x;   // transposed: row c, column r
+    if (c < cols && r < rows) {
+      const float v = tile[threadIdx.x][i];
+      const float h = tf32_hi(v);
+      thi[(size_t)mat * rows * cols + (size_t)c * rows + r] = h;
+      tlo[(size_t)mat * rows * cols + (size_t)c * rows + r] = tf32_lo(v, h, lrn);
+    }
+  }
+}
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                  const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+// 2-D tensor map over a row-major [rows][cols] array; box box_cols × box_rows
+bool encode_2d(EncodeTiledFn enc, CUtensorMap *m, const void *ptr, CUtensorMapDataType dt, int esize, long rows,
+               long cols, int box_cols, int box_rows, bool swizzle) {
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)cols * esize};
+  cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
+  cuuint32_t es[2] = {1, 1};
+  return enc(m, dt, 2, const_cast<void *>(ptr), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+             swizzle ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+}  // namespace
+
+size_t tc_smem_bytes(const TcCfg &tc, int P) {
+  (void)P;
+  return 1024 + (size_t)tc.stages * tc.stage_bytes + tc.dtile_bytes + sizeof(PSmemTail);
+}
+
+bool encode_maps(const KParams &p, TcMaps *m, char *why) {
+  void *fn = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn ||
+      q != cudaDriverEntryPointSuccess) {
+    snprintf(why, 256, "cuTensorMapEncodeTiled unavailable");
+    return false;
+  }
+  EncodeTiledFn enc = (EncodeTiledFn)fn;
+  const Dims &d = p.d;
+  const Bufs &b = p.b;
+  const long mats = d.shared_phi ? 1 : d.Tl;
+  const CUtensorMapDataType F32 = CU_TENSOR_MAP_DATA_TYPE_FLOAT32, F64 = CU_TENSOR_MAP_DATA_TYPE_FLOAT64;
+  const int NT = p.tc.NT;
+  const bool ok = encode_2d(enc, &m->phi_h, b.Phh, F32, 4, mats * d.N, d.D, 32, TM, true) &&
+                  encode_2d(enc, &m->phi_l, b.Phl, F32, 4, mats * d.N, d.D, 32, TM, true) &&
+                  encode_2d(enc, &m->phit_h, b.PTh, F32, 4, mats * d.D, d.N, 32, TM, true) &&
+                  encode_2d(enc, &m->phit_l, b.PTl, F32, 4, mats * d.D, d.N, 32, TM, true) &&
+                  encode_2d(enc, &m->u_h, b.Uh, F32, 4, (long)d.Tl * d.Pp, d.N, 32, NT, true) &&
+                  encode_2d(enc, &m->u_l, b.Ul, F32, 4, (long)d.Tl * d.Pp, d.N, 32, NT, true) &&
+                  encode_2d(enc, &m->d_h, b.Dh, F32, 4, (long)d.Tl * d.P, d.D, 32, NT, true) &&
+                  encode_2d(enc, &m->d_l, b.Dl, F32, 4, (long)d.Tl * d.P, d.D, 32, NT, true) &&
+                  encode_2d(enc, &m->dm, b.Dm, F64, 8, (long)d.Tl * d.C, d.D, TK, d.C, false) &&
+                  encode_2d(enc, &m->um, b.Um, F64, 8, (long)d.Tl * d.N, d.Cp, d.Cp, TK, false) &&
+                  encode_2d(enc, &m->d32, b.D32, F32, 4, (long)d.Tl * d.P, d.D, TM, NT, false);
+  if (!ok) snprintf(why, 256, "cuTensorMapEncodeTiled failed");
+  return ok;
+}
+
+// kernel instantiation for the cluster count: CC ∈ {4, 8, 16} bounds C at compile time
+typedef void (*CgKernel)(KParams, const TcMaps);
+CgKernel cg_kernel(int C) {
+  if (C <= 4) return k_cg_persistent<4>;
+  if (C <= 8) return k_cg_persistent<8>;
+  return k_cg_persistent<16>;
+}
+
+int cg_grid_size(const KParams &p) {
+  int dev = 0, sms = 0, occ = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 0;
+  if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return 0;
+  const size_t smem = tc_smem_bytes(p.tc, p.d.P);
+  const CgKernel k = cg_kernel(p.d.C);
+  if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) return 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, NTHREADS, smem) != cudaSuccess) return 0;
+  return occ >= 1 ? sms : 0;   // one CTA per SM (512 TMEM columns each)
+}
+
+cudaError_t launch_split_phi(const KParams &p, cudaStream_t s) {
+  const int mats = p.d.shared_phi ? 1 : p.d.Tl;
+  dim3 grid((p.d.D + 31) / 32, (p.d.N + 31) / 32, mats);
+  k_split_phi<<<grid, dim3(32, 8), 0, s>>>(p.phi, p.d.N, p.d.D, mats, p.b.Phh, p.b.Phl, p.b.PTh, p.b.PTl, p.lo_rn);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_cg_persistent(const KParams &p, const TcMaps &maps, int grid, cudaStream_t s) {
+  const size_t smem = tc_smem_bytes(p.tc, p.d.P);
+  cudaError_t e = cudaMemsetAsync(p.b.gridbar, 0, sizeof(unsigned), s);
+  if (e != cudaSuccess) return e;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(NTHREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;   // co-residency of all CTAs (grid barriers)
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, cg_kernel(p.d.C), p, maps);
+}
+
+}  // namespace cmtcs

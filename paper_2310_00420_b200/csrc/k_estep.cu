@@ -170,7 +170,7 @@ __global__ void k_estep_finish(KParams p) {
     quad = block_sum(quad, sh);
     double res = 0.0;
     for (int n = tid; n < d.N; n += blockDim.x) {
-      const double rv = (double)p.y[(size_t)t * d.N + n] - p.b.Um[((size_t)t * d.N + n) * d.C + c];
+      const double rv = (double)p.y[(size_t)t * d.N + n] - p.b.Um[((size_t)t * d.N + n) * d.Cp + c];
       res = fma(rv, rv, res);
     }
     res = block_sum(res, sh);

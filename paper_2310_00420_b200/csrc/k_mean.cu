@@ -1,6 +1,6 @@
 // Φμ for ℓ (Eq. 3 via reading A1): Um[t][n][c] = Σ_d Φ_t[n][d] · μ_tc[d] in fp64 for the final means
-// of an E-step (inside the CG loop the mean columns are computed by the tensor-core kernels' CUDA
-// cores, k_operator_tc.cu).  DFMA on fp32 Φ tiles streamed through a 3-stage cp.async ring;
+// of an E-step (inside the CG loop the mean columns are computed on the CUDA cores of the persistent
+// CG kernel, k_cg_persistent.cu).  DFMA on fp32 Φ tiles streamed through a 3-stage cp.async ring;
 // split-K over S1 slices, the S1 CTAs of a row tile form a cluster and reduce over DSMEM.
 #include <cooperative_groups.h>
 
@@ -32,7 +32,7 @@ template <int N>
 __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
 // stage 1:  grid (1, nRT1 * S1, Tl), clusters of (1, S1, 1)
-__global__ void __launch_bounds__(OP_THREADS) k_mu_stage1(KParams p, const double *__restrict__ mu_src, int mu_only) {
+__global__ void __launch_bounds__(OP_THREADS) k_mu_stage1(KParams p, const double *__restrict__ mu_src) {
   extern __shared__ __align__(16) unsigned char dsm1[];
   SmemM1 &sm = *reinterpret_cast<SmemM1 *>(dsm1);
   const Dims &d = p.d;
@@ -54,13 +54,6 @@ __global__ void __launch_bounds__(OP_THREADS) k_mu_stage1(KParams p, const doubl
       cp_async16(&sm.A[buf][r][4 * q], ok ? phi + (size_t)n * D + k : phi, ok);
     }
   };
-  if (!mu_only) {
-    if (*p.b.u >= d.cap) return;               // past the end of an unrolled graph body
-    int any = 0;
-    for (int c = 0; c < C; ++c) any |= (p.b.flagm[t * C + c] == 1);
-    if (!any) return;
-    if (tid == 0) atomicMax(p.b.ts + 4 * (*p.b.u), ~globaltimer());
-  }
   const double *src = mu_src + (size_t)t * C * D;
   const int r = tid & (BR - 1), h = tid >> 7;
   double acc[MAXC / 2];
@@ -109,7 +102,7 @@ __global__ void __launch_bounds__(OP_THREADS) k_mu_stage1(KParams p, const doubl
       const double *pp = d.S1 > 1 ? cl.map_shared_rank(part, q) : part;
       v += pp[rr * MAXC + c];
     }
-    if (n0 + rr < N) p.b.Um[((size_t)t * N + n0 + rr) * C + c] = v;
+    if (n0 + rr < N) p.b.Um[((size_t)t * N + n0 + rr) * d.Cp + c] = v;
   }
   if (d.S1 > 1) cl.sync();
   return;
@@ -117,7 +110,7 @@ __global__ void __launch_bounds__(OP_THREADS) k_mu_stage1(KParams p, const doubl
 
 }  // namespace
 
-cudaError_t launch_mu_stage1(const KParams &p, const double *mu_src, bool mu_only, cudaStream_t s) {
+cudaError_t launch_mu_stage1(const KParams &p, const double *mu_src, cudaStream_t s) {
   static bool configured = false;
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(k_mu_stage1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(SmemM1));
@@ -136,7 +129,7 @@ cudaError_t launch_mu_stage1(const KParams &p, const double *mu_src, bool mu_onl
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, k_mu_stage1, p, mu_src ? mu_src : p.b.Dm, (int)(mu_only ? 1 : 0));
+  return cudaLaunchKernelEx(&cfg, k_mu_stage1, p, mu_src);
 }
 
 }  // namespace cmtcs
