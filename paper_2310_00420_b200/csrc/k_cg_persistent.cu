@@ -248,31 +248,43 @@ __device__ __forceinline__ double lds_d(uint32_t a) {
   return v;
 }
 
-// fp64 mean-column work of one ring stage for tile row r: acc[c] += Σ_k Φ[r][k]·B(c, k), Φ = hi + lo
-// exactly (fp32).  Stage 1 reads B as [c][32] (Dm chunk), stage 2 as [32][Cp] (Um chunk).
-// CC ≥ C is a compile-time bound (fully unrolled, accumulators in registers, c ≥ C predicated off).
-template <bool B_CK, int CC>
-__device__ __forceinline__ void mean_stage(uint32_t a_hi, uint32_t mb, int r, int C, int Cp, double *acc) {
+__device__ __forceinline__ float lds_f32(uint32_t a) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1];\n" : "=f"(v) : "r"(a));
+  return v;
+}
+
+// D(8×8) += A(8×4) · B(4×8) on the FP64 tensor path; lane holds A[lane/4][lane%4], B[lane%4][lane/4]
+// and D[lane/4][2·(lane%4) + {0, 1}]
+__device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c[0]), "+d"(c[1])
+               : "d"(a), "d"(b));
+}
+
+// fp64 mean-column work of one ring stage, one warp, rows [32·ew, 32·ew + 32) of the tile:
+// acc += Φ[rows][k-chunk] · B[k-chunk][C] exactly in fp64 (Φ = hi + lo is the fp32 Φ).  Stage 1 reads
+// B from the Dm chunk laid out [c][32], stage 2 from the Um chunk laid out [32][Cp].  Accumulator
+// fragment acc[mt][nt] holds rows 32·ew + 8·mt + lane/4, columns 8·nt + 2·(lane%4) + {0, 1}.
+template <bool B_CK, int NTC>
+__device__ __forceinline__ void mean_stage(uint32_t a_hi, uint32_t mb, int ew, int lane, int C, int Cp,
+                                           double (&acc)[4][NTC][2]) {
+  const int g = lane >> 2, q = lane & 3;
 #pragma unroll
-  for (int cc = 0; cc < TK / 4; ++cc) {
-    const float4 h = lds128(a_hi + sw128_offset(r, cc));
-    const float4 l = lds128(a_hi + A_BYTES + sw128_offset(r, cc));
-    const double a[4] = {(double)(h.x + l.x), (double)(h.y + l.y), (double)(h.z + l.z), (double)(h.w + l.w)};
+  for (int ks = 0; ks < TK / 4; ++ks) {
+    const int k = 4 * ks + q;
+    double bf[NTC];
 #pragma unroll
-    for (int c = 0; c < CC; ++c) {
-      if (c < C) {
-        if (B_CK) {
-          const double2 b01 = lds_d2(mb + (uint32_t)(c * TK + 4 * cc) * 8);
-          const double2 b23 = lds_d2(mb + (uint32_t)(c * TK + 4 * cc + 2) * 8);
-          acc[c] = fma(a[0], b01.x, acc[c]);
-          acc[c] = fma(a[1], b01.y, acc[c]);
-          acc[c] = fma(a[2], b23.x, acc[c]);
-          acc[c] = fma(a[3], b23.y, acc[c]);
-        } else {
+    for (int nt = 0; nt < NTC; ++nt) {
+      const int n = 8 * nt + g;
+      bf[nt] = (n < C) ? lds_d(mb + (uint32_t)(B_CK ? n * TK + k : k * Cp + n) * 8) : 0.0;
+    }
 #pragma unroll
-          for (int i = 0; i < 4; ++i) acc[c] = fma(a[i], lds_d(mb + (uint32_t)((4 * cc + i) * Cp + c) * 8), acc[c]);
-        }
-      }
+    for (int mt = 0; mt < 4; ++mt) {
+      const uint32_t off = sw128_offset(32 * ew + 8 * mt + g, ks) + (uint32_t)q * 4;
+      const double a = (double)(lds_f32(a_hi + off) + lds_f32(a_hi + A_BYTES + off));
+#pragma unroll
+      for (int nt = 0; nt < NTC; ++nt) dmma(acc[mt][nt], a, bf[nt]);
     }
   }
 }
@@ -643,9 +655,13 @@ __device__ void epilogue_unit(const KParams &p, unsigned char *sm, PSmemTail &tl
   }
   __syncwarp();
   const uint32_t *mask = tl.emask[ew];
-  double macc[CC];
+  constexpr int NTC = (CC + 7) / 8;         // 8-column fp64 MMA tiles covering the C mean columns
+  double macc[4][NTC][2];
 #pragma unroll
-  for (int c = 0; c < CC; ++c) macc[c] = 0.0;
+  for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < NTC; ++nt) macc[mt][nt][0] = macc[mt][nt][1] = 0.0;
+  const int fg = lane >> 2, fq = lane & 3;   // fragment row group / column pair of this lane
   // mainloop: fp64 mean-column DFMA on each stage (or just release it)
   for (int kc = 0; kc < x.nk; ++kc) {
     const uint32_t G = rc.g++;
@@ -654,8 +670,8 @@ __device__ void epilogue_unit(const KParams &p, unsigned char *sm, PSmemTail &tl
     if (tr && kc < 16) tr[64 + kc] = globaltimer();
     if (x.mean && !(p.dbg_flags & 1)) {
       const uint32_t base = smem_u32(sm) + (uint32_t)st * tc.stage_bytes;
-      if (x.stage == 1) mean_stage<true, CC>(base, base + mu_off, r, C, d.Cp, macc);
-      else mean_stage<false, CC>(base, base + mu_off, r, C, d.Cp, macc);
+      if (x.stage == 1) mean_stage<true, NTC>(base, base + mu_off, ew, lane, C, d.Cp, macc);
+      else mean_stage<false, NTC>(base, base + mu_off, ew, lane, C, d.Cp, macc);
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&tl.mdone[st]);
@@ -697,13 +713,19 @@ __device__ void epilogue_unit(const KParams &p, unsigned char *sm, PSmemTail &tl
       rc.ti++;
       if (tr) tr[81] = globaltimer();
     }
-    if (x.mean && n < N) {
+    if (x.mean) {
+      double *dst = d.S1 == 1 ? p.b.Um + (size_t)x.t * N * d.Cp
+                              : p.b.Umpart + ((size_t)x.t * d.S1 + x.sp) * N * d.Cp;
 #pragma unroll
-      for (int c = 0; c < CC; ++c)
-        if (c < C) {
-          if (d.S1 == 1) p.b.Um[((size_t)x.t * N + n) * d.Cp + c] = macc[c];
-          else stv(p.b.Umpart + (((size_t)x.t * d.S1 + x.sp) * N + n) * d.Cp + c, macc[c]);
+      for (int mt = 0; mt < 4; ++mt) {
+        const int nn = x.rt * TM + 32 * ew + 8 * mt + fg;
+#pragma unroll
+        for (int nt = 0; nt < NTC; ++nt) {
+          const int c = 8 * nt + 2 * fq;       // Cp is even: columns c, c+1 are both < Cp or both ≥ C
+          if (nn < N && c < C) stv(reinterpret_cast<double2 *>(dst + (size_t)nn * d.Cp + c),
+                                   make_double2(macc[mt][nt][0], macc[mt][nt][1]));
         }
+      }
     }
     if (d.S1 > 1) {
       // The S1 split CTAs of this tile run in the same round (the host picks S1 > 1 only when all
@@ -787,22 +809,30 @@ __device__ void epilogue_unit(const KParams &p, unsigned char *sm, PSmemTail &tl
   const bool rv = dd < D;
   const float betaf = (float)p.beta;
   if (x.mean) {
-    // mean columns (fp64): Wm = β·acc + α ⊙ dm, partial dᵀWm over this row tile
-    double dot[16];
+    // mean columns (fp64): Wm = β·acc + α ⊙ dm on this lane's fragment rows / columns, and the
+    // partial dᵀWm per column over the tile (fragment rows, then the 8 row groups of the warp)
 #pragma unroll
-    for (int c = 0; c < 16; ++c) {
-      dot[c] = 0.0;
-      if (c < CC && c < C && rv) {
-        const size_t o = ((size_t)x.t * C + c) * D + dd;
-        const double dmv = ldv(p.b.Dm + o);
-        const double wv = fma(p.beta, macc[c], p.b.alpha64[(size_t)c * D + dd] * dmv);
-        stv(p.b.Wm + o, wv);
-        dot[c] = dmv * wv;
+    for (int nt = 0; nt < NTC; ++nt) {
+      double dot[2] = {0.0, 0.0};
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int c = 8 * nt + 2 * fq + e;
+#pragma unroll
+        for (int mt = 0; mt < 4; ++mt) {
+          const int de = x.rt * TM + 32 * ew + 8 * mt + fg;
+          if (c < C && de < D) {
+            const size_t o = ((size_t)x.t * C + c) * D + de;
+            const double dmv = ldv(p.b.Dm + o);
+            const double wv = fma(p.beta, macc[mt][nt][e], p.b.alpha64[(size_t)c * D + de] * dmv);
+            stv(p.b.Wm + o, wv);
+            dot[e] = fma(dmv, wv, dot[e]);
+          }
+        }
+#pragma unroll
+        for (int o = 4; o < 32; o <<= 1) dot[e] += __shfl_xor_sync(0xffffffffu, dot[e], o);
+        if (fg == 0 && c < C) tl.red[ew][TC_NTMAX + c] = dot[e];
       }
     }
-    int idx;
-    const double sum = warp_reduce16(dot, lane, &idx);
-    if ((lane & 1) == 0 && idx < C) tl.red[ew][TC_NTMAX + idx] = sum;
   }
   if (tr) tr[86] = globaltimer();
   if (x.nmma) {
