@@ -31,7 +31,7 @@ Every function below is pinned by tests/test_oracle_pins.py (closed forms, invar
 from __future__ import annotations
 
 import math
-from typing import Callable, Optional
+from typing import Callable, Optional, Sequence
 
 import numpy as np
 
@@ -260,11 +260,18 @@ def _phi_of(data, i):
 
 def cofem_task(phi: np.ndarray, y: np.ndarray, beta: float, alpha: np.ndarray, pi: np.ndarray,
                P: np.ndarray, tol: float, cap: int, mu_tol: Optional[float] = None,
-               mu_cap: Optional[int] = None) -> dict:
+               mu_cap: Optional[int] = None, clusters: Optional[Sequence[int]] = None) -> dict:
     """Alg. 2 lines 4-12 for one task t and every cluster c.
 
     P: probes [C, K, D] (line 5).  Line 6: CG on A_tc μ = βΦᵀy and A_tc x_k = p_k.  mu_tol/mu_cap
-    optionally solve the mean system to a different tolerance (parity protocol)."""
+    optionally solve the mean system to a different tolerance (parity protocol).
+    clusters: evaluate lines 6-9 (μ, s, ν̄) for these clusters only — every (t, c) block is an
+    independent computation; q and the log-likelihood (line 10) need all clusters and are omitted."""
+    if clusters is not None:
+        sel = np.asarray(list(clusters), dtype=np.int64)
+        full = cofem_task(phi, y, beta, alpha[sel], np.full(sel.size, 1.0 / sel.size), P[sel], tol, cap,
+                          mu_tol, mu_cap)
+        return {k: full[k] for k in ("mu", "s", "nu", "tau", "mu_steps", "probe_steps", "gamma", "xi")}
     phi64 = np.asarray(phi, dtype=np.float64)
     C, K, Dn = P.shape
     N = phi64.shape[0]

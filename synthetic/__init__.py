@@ -128,9 +128,11 @@ def z_true(cfg: Config, t: int, sup=None, lab=None) -> np.ndarray:
 
 
 def measurements(cfg: Config, t: int, phi_t: np.ndarray, z: np.ndarray) -> np.ndarray:
-    """y_t = fp32(Phi_t z_t + eps_t), computed in fp64 then rounded once (A21)."""
+    """y_t = fp32(Phi_t z_t + eps_t), computed in fp64 then rounded once (A21).  phi_t may be given
+    already widened to fp64 (the shared-Phi config widens it once for all tasks)."""
     eps = _rng(cfg, 3, t).standard_normal(cfg.N) * cfg.sigma
-    return (phi_t.astype(np.float64) @ z + eps).astype(np.float32)
+    p64 = phi_t if phi_t.dtype == np.float64 else phi_t.astype(np.float64)
+    return (p64 @ z + eps).astype(np.float32)
 
 
 def generate(cfg: Config, tasks: Optional[Sequence[int]] = None) -> dict:
@@ -148,13 +150,14 @@ def generate(cfg: Config, tasks: Optional[Sequence[int]] = None) -> dict:
     lab = labels(cfg)
     if cfg.shared_phi:
         ph = phi(cfg, 0)
+        ph64 = ph.astype(np.float64)
         phis = None
     else:
         phis = np.empty((len(tasks), cfg.N, cfg.D), dtype=np.float32)
     ys = np.empty((len(tasks), cfg.N), dtype=np.float32)
     zs = np.empty((len(tasks), cfg.D), dtype=np.float64)
     for i, t in enumerate(tasks):
-        p = ph if cfg.shared_phi else phi(cfg, int(t))
+        p = ph64 if cfg.shared_phi else phi(cfg, int(t))
         if not cfg.shared_phi:
             phis[i] = p
         zs[i] = z_true(cfg, int(t), sup, lab)

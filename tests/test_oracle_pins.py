@@ -350,3 +350,15 @@ def test_readout_ties_lowest_and_nmse():
     assert list(a) == [0, 1]
     np.testing.assert_array_equal(z, [mu[0, 0], mu[1, 1]])
     assert O.nmse(np.ones(4), 2 * np.ones(4)) == pytest.approx(0.25)
+
+
+def test_cluster_subset_equals_full_computation():
+    """Every (t, c) block of Alg. 2 lines 6-9 is an independent computation: evaluating a subset of
+    clusters (used for the full-size sampled parity tests) reproduces the full call's μ, s, ν̄."""
+    data = synthetic.small_problem(T=1, C=3, N=10, D=20, K=5, seed=11)
+    alpha = np.random.default_rng(3).uniform(0.5, 3.0, (3, 20))
+    P = O.probe_signs(9, 0, 1, 0, 3, 5, 20)
+    full = O.cofem_task(data["phi"][0], data["y"][0], data["beta"], alpha, data["pi"], P, 1e-8, 80)
+    sub = O.cofem_task(data["phi"][0], data["y"][0], data["beta"], alpha, data["pi"], P, 1e-8, 80, clusters=[2, 0])
+    for k in ("mu", "s", "nu"):
+        np.testing.assert_array_equal(sub[k], full[k][[2, 0]])
