@@ -86,7 +86,10 @@ struct Carver {
 
 TcCfg make_tc(const Dims &d) {
   TcCfg tc;
-  tc.NT = std::min(TC_NTMAX, (d.P + 15) / 16 * 16);
+  // column tile: up to 256 columns; 128 with a shared Φ (its re-reads per column tile hit L2), which
+  // leaves TMEM room for two K-split accumulator pairs (precision of the long K = D contraction)
+  const int ntmax = d.shared_phi ? 128 : TC_NTMAX;
+  tc.NT = std::min(ntmax, (d.P + 15) / 16 * 16);
   tc.slot = (tc.NT + 31) / 32 * 32;
   tc.nacc = std::max(1, std::min(4, 512 / (2 * tc.slot)));
   tc.stage_bytes = 2u * 128u * 128u + 2u * (unsigned)tc.NT * 128u + 4096u;  // + fp64 mean-column chunk
@@ -138,7 +141,7 @@ bool make_dims(const cmtcs_problem *p, Dims *d, char *why) {
   d->nw = (p->D + 63) / 64;
   d->nRT1 = (p->N + OP_BR - 1) / OP_BR;
   d->nRT2 = (p->D + OP_BR - 1) / OP_BR;
-  const int NT = std::min(TC_NTMAX, (d->P + 15) / 16 * 16);
+  const int NT = std::min(p->shared_phi ? 128 : TC_NTMAX, (d->P + 15) / 16 * 16);   // = make_tc's NT
   d->nCT = (d->P + NT - 1) / NT;
   {
     // split the stage-1 contraction over D (S1 ∈ {1, 2, 4, 8}, every split ≥ 128 of D) so that the
@@ -177,22 +180,16 @@ size_t carve(const Dims &d, char *base, Bufs *b) {
   b->b64 = cv.take<double>(Tl * D);
   b->bnorm2 = cv.take<double>(Tl);
   const size_t mats = d.shared_phi ? 1 : Tl;
-  b->Phh = cv.take<float>(mats * N * D);
-  b->Phl = cv.take<float>(mats * N * D);
-  b->PTh = cv.take<float>(mats * N * D);
-  b->PTl = cv.take<float>(mats * N * D);
+  b->PT = cv.take<float>(mats * N * D);
   b->X = cv.take<float>(Tl * P * D);
   b->R = cv.take<float>(Tl * P * D);
-  b->Dh = cv.take<float>(Tl * P * D);
-  b->Dl = cv.take<float>(Tl * P * D);
   b->D32 = cv.take<float>(Tl * P * D);
   b->W = cv.take<float>(Tl * P * D);
   b->Xm = cv.take<double>(Tl * C * D);
   b->Rm = cv.take<double>(Tl * C * D);
   b->Dm = cv.take<double>(Tl * C * D);
   b->Wm = cv.take<double>(Tl * C * D);
-  b->Uh = cv.take<float>(Tl * d.Pp * N);
-  b->Ul = cv.take<float>(Tl * d.Pp * N);
+  b->U = cv.take<float>(Tl * d.Pp * N);
   b->Um = cv.take<double>(Tl * N * d.Cp);
   b->rr = cv.take<double>(Tl * P);
   b->rrm = cv.take<double>(Tl * C);
@@ -458,7 +455,6 @@ cmtcs_status cmtcs_init(cmtcs_ctx **out, const cmtcs_problem *p, const float *ph
   c->kp.empty_eps = p->empty_eps;
   c->kp.seed = p->probe_seed;
   c->kp.dbg_flags = getenv("CMTCS_DBG") ? atoi(getenv("CMTCS_DBG")) : 0;
-  c->kp.lo_rn = getenv("CMTCS_LO_RN") ? atoi(getenv("CMTCS_LO_RN")) : 0;
   *out = c;  // from here on errors leave a (broken) ctx the caller destroys
   CUDA_OK(c, cudaMallocHost((void **)&c->h_out, 32 * sizeof(double)));
   CUDA_OK(c, cudaMallocHost((void **)&c->h_status, 8 * sizeof(int)));

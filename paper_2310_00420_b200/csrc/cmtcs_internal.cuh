@@ -42,12 +42,10 @@ struct Bufs {
   double *b64;       // [Tl][D]   βΦᵀy
   double *bnorm2;    // [Tl]      ‖b‖²
   float *X, *R, *W;  // probe columns [Tl][P][D]; W = Ad
-  float *Dh, *Dl;    // probe directions d = Dh + Dl exactly (Dh = tf32(d)) [Tl][P][D] (tensor-core operand)
-  float *D32;        // the same directions as plain fp32 [Tl][P][D] (epilogue / update operand)
-  float *Phh, *Phl;  // Φ split: tf32 hi + fp32 lo   [Tl or 1][N][D]
-  float *PTh, *PTl;  // Φᵀ split                     [Tl or 1][D][N]
+  float *D32;        // probe directions d [Tl][P][D]
+  float *PT;         // Φᵀ fp32 [Tl or 1][D][N] (stage-2 A operand; stage 1 reads the caller's Φ)
   double *Xm, *Rm, *Dm, *Wm; // mean columns  [Tl][C][D]
-  float *Uh, *Ul;    // stage-1 output split, [Tl][Pp][N] (row = compacted column j)
+  float *U;          // stage-1 output U = ΦD, [Tl][Pp][N] (row = column j)
   double *Um;        // [Tl][N][Cp]
   double *rr;        // [Tl][P]
   double *rrm;       // [Tl][C]
@@ -95,10 +93,10 @@ struct TcCfg {
 
 // TMA descriptors (host-encoded, passed as a __grid_constant__ kernel parameter)
 struct TcMaps {
-  CUtensorMap phi_h, phi_l;    // fp32 [rows Tl·N][cols D], box 32 × 128, SW128
-  CUtensorMap phit_h, phit_l;  // fp32 [rows Tl·D][cols N], box 32 × 128, SW128
-  CUtensorMap u_h, u_l;        // fp32 [rows Tl·Pp][cols N], box 32 × NT, SW128
-  CUtensorMap d_h, d_l;        // fp32 [rows Tl·P][cols D], box 32 × NT, SW128 (probe directions)
+  CUtensorMap phi;             // fp32 Φ (the caller's) [rows Tl·N][cols D], box 32 × 128, SW128
+  CUtensorMap phit;            // fp32 Φᵀ [rows Tl·D][cols N], box 32 × 128, SW128
+  CUtensorMap u;               // fp32 U = ΦD [rows Tl·Pp][cols N], box 32 × NT, SW128
+  CUtensorMap dir;             // fp32 directions [rows Tl·P][cols D], box 32 × NT, SW128
   CUtensorMap dm;              // fp64 [rows Tl·C][cols D], box 32 × C (mean directions)
   CUtensorMap um;              // fp64 [rows Tl·N][cols Cp], box Cp × 32 (Φ·d of the mean columns)
   CUtensorMap d32;             // fp32 [rows Tl·P][cols D], box 128 × NT (probe directions, epilogue)
@@ -118,7 +116,6 @@ struct KParams {
   int it;                      // global EM iteration index of this E-step
   const uint64_t *probe_bits;  // optional override
   const double *q_override;    // optional
-  int lo_rn;                   // tf32 split: lo rounded to nearest tf32 (1) or the exact fp32 remainder (0)
   int dbg_flags;               // CMTCS_DBG (diagnostics only): 1 skip mean DFMA, 2 skip MMA, 4 skip B gather
 };
 

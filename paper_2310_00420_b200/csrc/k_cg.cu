@@ -69,8 +69,6 @@ __global__ void k_init_columns(KParams p) {
       const float v = ((wd >> (i & 63)) & 1ull) ? -1.f : 1.f;
       p.b.X[base + i] = 0.f;
       p.b.R[base + i] = v;
-      p.b.Dh[base + i] = v;     // ±1 is exact in tf32
-      p.b.Dl[base + i] = 0.f;
       p.b.D32[base + i] = v;
     }
     if (threadIdx.x == 0) {

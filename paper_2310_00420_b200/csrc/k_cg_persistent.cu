@@ -17,14 +17,20 @@
 // CUDA cores, reading the same smem Φ tiles the tensor core reads.
 //
 // Warp roles in phases 1-2 (256 threads):
-//   warp 0     TMA producer: Φ/Φᵀ tiles (A), direction / U tiles (B), fp64 mean-column chunk
+//   warp 0     TMA producer: fp32 Φ/Φᵀ tiles (A), direction / U tiles (B), fp64 mean-column chunk
 //   warp 1     MMA issuer: tcgen05.mma kind::tf32, tcgen05.commit frees ring stages / the tile
 //   warp 2     TMEM owner (alloc / dealloc)
-//   warps 4-7  fp64 mean-column DFMA per ring stage, then the tile epilogue (TMEM → registers)
+//   warps 4-7  per ring stage: tf32 split of A and B, then the fp64 mean-column MMAs (DMMA);
+//              per tile: the epilogue (TMEM → registers)
 // All operands arrive by TMA into an S-stage ring of 128-byte-swizzled K-major smem tiles, so no
 // CTA-wide barrier runs inside a K loop; the producer runs ahead into the next unit while the
-// epilogue of the previous one drains.  mbarriers: full[s] (TMA bytes), empty[s] (MMA done),
-// mdone[s] (fp64 warps done), tfull / tempty (accumulator handshake).
+// epilogue of the previous one drains.  mbarriers: full[s] (TMA bytes), conv[s] (split done),
+// empty[s] (MMA done), mdone[s] (fp64 warps done), tfull / tempty (accumulator handshake).
+//
+// Operands live in HBM as plain fp32 (Φ itself, its transpose, the directions, U) and arrive by TMA;
+// the epilogue warps split each staged tile in shared memory into the exact pair x = hi + lo,
+// hi = tf32(x) (in place) and lo = x − hi (a second tile), so the operator reads every operand
+// byte once per use (mbarrier conv[s]: split done → the MMA warp may issue).
 //
 // 3xTF32: every operand x is the exact pair x = hi + lo with hi = tf32(x), and each K = 8 step issues
 //   acc_x += lo_A·hi_B + hi_A·lo_B ;  acc_m += hi_A·hi_B
@@ -60,7 +66,7 @@ constexpr int NTHREADS = 256;
 constexpr int EPI0 = 128;                 // first thread of the epilogue / fp64 warps (4-7)
 
 struct PSmemTail {
-  uint64_t full[MAXST], empty[MAXST], mdone[MAXST];
+  uint64_t full[MAXST], conv[MAXST], empty[MAXST], mdone[MAXST];
   uint64_t tfull, tempty;
   uint64_t dfull, dempty;             // the stage-2 epilogue's d tile (TMA bytes / epilogue done)
   uint32_t tslot;
@@ -136,13 +142,6 @@ __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
   for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   return v;
-}
-
-// low part of the tf32 split x = hi + lo: exact fp32 remainder (the tensor core then truncates it to
-// tf32) or, with lrn, the remainder rounded to nearest tf32 (unbiased; x = hi + lo to 2^-22 relative)
-__device__ __forceinline__ float tf32_lo(float x, float hi, int lrn) {
-  const float r = x - hi;
-  return lrn ? tf32_hi(r) : r;
 }
 
 // K-split accumulator pairs of a tile: one for short contractions (K ≤ 512), else up to tc.nacc
@@ -289,6 +288,36 @@ __device__ __forceinline__ void mean_stage(uint32_t a_hi, uint32_t mb, int ew, i
   }
 }
 
+__device__ __forceinline__ void sts128(uint32_t a, float4 v) {
+  asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};\n" ::"r"(a), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w) : "memory");
+}
+
+// tf32 rounding to nearest (ties away from zero, = cvt.rna.tf32.f32 for finite x) on the integer pipe
+__device__ __forceinline__ float tf32_rna(float x) {
+  return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xFFFFE000u);
+}
+
+// Split rows r, r+128, ... (nrows of them) of a staged 128-byte-swizzled fp32 tile into the exact
+// pair x = hi + lo: hi = tf32(x) written in place, lo = x − hi written to the same offsets of `lo`.
+// The swizzle permutes 16-byte chunks within a row only, so a whole row is 8 chunks at fixed
+// offsets; lane r visits them in the order c ^ (r & 7), which spreads a warp over all 32 banks.
+__device__ __forceinline__ void split_rows(uint32_t hi, uint32_t lo, int r, int nrows) {
+  for (int i = 0; i < nrows; ++i, r += 128) {
+    const uint32_t row = (uint32_t)(r >> 3) * 1024 + (uint32_t)(r & 7) * 128;
+    float4 v[8];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) v[c] = lds128(hi + row + (uint32_t)((c ^ r) & 7) * 16);
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const uint32_t off = row + (uint32_t)((c ^ r) & 7) * 16;
+      float4 h;
+      h.x = tf32_rna(v[c].x); h.y = tf32_rna(v[c].y); h.z = tf32_rna(v[c].z); h.w = tf32_rna(v[c].w);
+      sts128(hi + off, h);
+      sts128(lo + off, make_float4(v[c].x - h.x, v[c].y - h.y, v[c].z - h.z, v[c].w - h.w));
+    }
+  }
+}
+
 // Per-unit geometry shared by all roles (computed redundantly by every warp).
 struct Unit {
   int stage;          // 1 or 2
@@ -327,8 +356,6 @@ __device__ void update_probe(const KParams &p, int t, int col, int u, int lane) 
   const double gam = rr / dAd;
   float4 *x4 = reinterpret_cast<float4 *>(p.b.X + g * d.D);
   float4 *r4 = reinterpret_cast<float4 *>(p.b.R + g * d.D);
-  float4 *dh4 = reinterpret_cast<float4 *>(p.b.Dh + g * d.D);
-  float4 *dl4 = reinterpret_cast<float4 *>(p.b.Dl + g * d.D);
   float4 *d4 = reinterpret_cast<float4 *>(p.b.D32 + g * d.D);
   const float4 *w4 = reinterpret_cast<const float4 *>(p.b.W + g * d.D);
   const int n4 = d.D >> 2;
@@ -376,7 +403,6 @@ __device__ void update_probe(const KParams &p, int t, int col, int u, int lane) 
   }
   if (!stop) {
     __syncwarp();
-    const int lrn = p.lo_rn;
     for (int i0 = lane; i0 < n4; i0 += 32 * U) {
       float4 rv[U], dd[U];
 #pragma unroll
@@ -393,12 +419,7 @@ __device__ void update_probe(const KParams &p, int t, int col, int u, int lane) 
           dv.y = (float)fma(xi, (double)dv.y, (double)rv[v].y);
           dv.z = (float)fma(xi, (double)dv.z, (double)rv[v].z);
           dv.w = (float)fma(xi, (double)dv.w, (double)rv[v].w);
-          // store d_{u+1} as the exact pair (tf32(d), d − tf32(d)) the tensor-core operator reads
-          float4 h4;
-          h4.x = tf32_hi(dv.x); h4.y = tf32_hi(dv.y); h4.z = tf32_hi(dv.z); h4.w = tf32_hi(dv.w);
-          stv(dh4 + i, h4);
           stv(d4 + i, dv);
-          stv(dl4 + i, make_float4(tf32_lo(dv.x, h4.x, lrn), tf32_lo(dv.y, h4.y, lrn), tf32_lo(dv.z, h4.z, lrn), tf32_lo(dv.w, h4.w, lrn)));
         }
       }
     }
@@ -555,7 +576,7 @@ __device__ __forceinline__ void produce(const KParams &p, const TcMaps &mp, unsi
   if (tr) tr[84] = globaltimer();
   const uint32_t b_bytes = (uint32_t)p.tc.NT * 128;
   const uint32_t mean_tx = x.stage == 1 ? (uint32_t)p.d.C * TK * 8 : (uint32_t)TK * p.d.Cp * 8;
-  const uint32_t bytes = 2 * A_BYTES + (x.nmma ? 2 * b_bytes : 0) + (x.mean ? mean_tx : 0);
+  const uint32_t bytes = A_BYTES + (x.nmma ? b_bytes : 0) + (x.mean ? mean_tx : 0);
   if (x.stage == 2 && x.nmma && p.tc.use_dtile) {
     // the epilogue's d tile: rows d0..d0+127 of the tile's NT direction columns
     if (rc.di > 0) mbar_wait(&tl.dempty, (rc.di - 1) & 1);
@@ -577,21 +598,14 @@ __device__ __forceinline__ void produce(const KParams &p, const TcMaps &mp, unsi
     uint64_t *fb = &tl.full[st];
     mbar_arrive_expect_tx(fb, bytes);
     const int k = x.k0 + kc * TK;
+    // fp32 tiles into the hi slots (split in place by the epilogue warps, lo into the lo slots)
     if (x.stage == 1) {
-      tma_load_2d(base, &mp.phi_h, k, x.arow, fb);
-      tma_load_2d(base + A_BYTES, &mp.phi_l, k, x.arow, fb);
-      if (x.nmma) {
-        tma_load_2d(base + 2 * A_BYTES, &mp.d_h, k, x.brow, fb);
-        tma_load_2d(base + 2 * A_BYTES + b_bytes, &mp.d_l, k, x.brow, fb);
-      }
+      tma_load_2d(base, &mp.phi, k, x.arow, fb);
+      if (x.nmma) tma_load_2d(base + 2 * A_BYTES, &mp.dir, k, x.brow, fb);
       if (x.mean) tma_load_2d(base + 2 * A_BYTES + 2 * b_bytes, &mp.dm, k, x.t * p.d.C, fb);
     } else {
-      tma_load_2d(base, &mp.phit_h, k, x.arow, fb);
-      tma_load_2d(base + A_BYTES, &mp.phit_l, k, x.arow, fb);
-      if (x.nmma) {
-        tma_load_2d(base + 2 * A_BYTES, &mp.u_h, k, x.brow, fb);
-        tma_load_2d(base + 2 * A_BYTES + b_bytes, &mp.u_l, k, x.brow, fb);
-      }
+      tma_load_2d(base, &mp.phit, k, x.arow, fb);
+      if (x.nmma) tma_load_2d(base + 2 * A_BYTES, &mp.u, k, x.brow, fb);
       if (x.mean) tma_load_2d(base + 2 * A_BYTES + 2 * b_bytes, &mp.um, 0, x.t * p.d.N + k, fb);
     }
     if (tr && kc < 16) tr[16 + kc] = globaltimer();
@@ -612,7 +626,7 @@ __device__ __forceinline__ void mma_unit(const KParams &p, unsigned char *sm, PS
   for (int kc = 0; kc < x.nk; ++kc) {
     const uint32_t G = rc.g++;
     const int st = G % rc.S;
-    mbar_wait(&tl.full[st], (G / rc.S) & 1);
+    mbar_wait(&tl.conv[st], (G / rc.S) & 1);      // operands staged and split
     if (tr && kc < 16) tr[32 + kc] = globaltimer();
     if (x.nmma && !(p.dbg_flags & 2)) {
       fence_after_sync();
@@ -668,6 +682,15 @@ __device__ void epilogue_unit(const KParams &p, unsigned char *sm, PSmemTail &tl
     const int st = G % rc.S;
     mbar_wait(&tl.full[st], (G / rc.S) & 1);
     if (tr && kc < 16) tr[64 + kc] = globaltimer();
+    {
+      // tf32 split of the staged fp32 tiles: A (128 rows, this thread's row) and B (x.ncol rows)
+      const uint32_t base = smem_u32(sm) + (uint32_t)st * tc.stage_bytes;
+      split_rows(base, base + A_BYTES, et, 1);
+      if (x.nmma) split_rows(base + 2 * A_BYTES, base + 2 * A_BYTES + b_bytes, et, (x.nmma + 127 - et) / 128);
+      fence_proxy_async();                    // generic smem writes → tensor-core (async proxy) reads
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tl.conv[st]);
+    }
     if (x.mean && !(p.dbg_flags & 1)) {
       const uint32_t base = smem_u32(sm) + (uint32_t)st * tc.stage_bytes;
       if (x.stage == 1) mean_stage<true, NTC>(base, base + mu_off, ew, lane, C, d.Cp, macc);
@@ -679,7 +702,7 @@ __device__ void epilogue_unit(const KParams &p, unsigned char *sm, PSmemTail &tl
   if (tr) tr[85] = globaltimer();
   if (x.stage == 1) {
     const int n = x.rt * TM + r;
-    float *Uh = p.b.Uh + (size_t)x.t * d.Pp * N, *Ul = p.b.Ul + (size_t)x.t * d.Pp * N;
+    float *Ut = p.b.U + (size_t)x.t * d.Pp * N;
     float *part = p.b.Upart + ((size_t)x.t * d.S1 + x.sp) * d.Pp * N;
     if (x.nmma) {
       mbar_wait(&tl.tfull, rc.ti & 1);
@@ -696,9 +719,7 @@ __device__ void epilogue_unit(const KParams &p, unsigned char *sm, PSmemTail &tl
             if (c < x.ncol) {
               const size_t o = (size_t)(j0 + c) * N + n;
               if (d.S1 == 1) {
-                const float h = tf32_hi(tot[i]);
-                Uh[o] = h;
-                Ul[o] = tf32_lo(tot[i], h, p.lo_rn);
+                Ut[o] = tot[i];
               } else {
                 stv(part + o, tot[i]);
               }
@@ -776,11 +797,7 @@ __device__ void epilogue_unit(const KParams &p, unsigned char *sm, PSmemTail &tl
 #pragma unroll
             for (int v = 0; v < V; ++v) {
               if (e0 + 128 * v < tot4) {
-                float4 h;
-                h.x = tf32_hi(acc4[v].x); h.y = tf32_hi(acc4[v].y); h.z = tf32_hi(acc4[v].z); h.w = tf32_hi(acc4[v].w);
-                *reinterpret_cast<float4 *>(Uh + off[v]) = h;
-                *reinterpret_cast<float4 *>(Ul + off[v]) =
-                    make_float4(tf32_lo(acc4[v].x, h.x, p.lo_rn), tf32_lo(acc4[v].y, h.y, p.lo_rn), tf32_lo(acc4[v].z, h.z, p.lo_rn), tf32_lo(acc4[v].w, h.w, p.lo_rn));
+                *reinterpret_cast<float4 *>(Ut + off[v]) = acc4[v];
               }
             }
           }
@@ -915,6 +932,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_cg_persistent(KParams p, const 
   if (tid == 0) {
     for (int s = 0; s < tc.stages; ++s) {
       mbar_init(&tl.full[s], 1);
+      mbar_init(&tl.conv[s], 4);
       mbar_init(&tl.empty[s], 1);
       mbar_init(&tl.mdone[s], 4);
     }
@@ -925,8 +943,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_cg_persistent(KParams p, const 
     fence_mbar_init();
   }
   if (warp == 0 && lane == 0) {
-    prefetch_tmap(&mp.phi_h); prefetch_tmap(&mp.phi_l); prefetch_tmap(&mp.phit_h); prefetch_tmap(&mp.phit_l);
-    prefetch_tmap(&mp.u_h); prefetch_tmap(&mp.u_l); prefetch_tmap(&mp.d_h); prefetch_tmap(&mp.d_l);
+    prefetch_tmap(&mp.phi); prefetch_tmap(&mp.phit); prefetch_tmap(&mp.u); prefetch_tmap(&mp.dir);
     prefetch_tmap(&mp.dm); prefetch_tmap(&mp.um); prefetch_tmap(&mp.d32);
   }
   if (warp == 2) tmem_alloc<512>(&tl.tslot);
@@ -1005,33 +1022,20 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_cg_persistent(KParams p, const 
   if (warp == 2) tmem_dealloc<512>(tmem);
 }
 
-// Φ → (Φhi, Φlo) and the transposed pair (Φᵀhi, Φᵀlo), once at init.  32×32 smem-tiled transpose.
-__global__ void k_split_phi(const float *__restrict__ phi, int rows, int cols, int mats, float *hi, float *lo,
-                            float *thi, float *tlo, int lrn) {
+// Φᵀ (fp32) of every task, once at init: the K-major A operand of stage 2.  32×32 smem-tiled transpose.
+__global__ void k_transpose_phi(const float *__restrict__ phi, int rows, int cols, float *__restrict__ phit) {
   __shared__ float tile[32][33];
   const int mat = blockIdx.z;
   const int c0 = blockIdx.x * 32, r0 = blockIdx.y * 32;
   const float *src = phi + (size_t)mat * rows * cols;
   for (int i = threadIdx.y; i < 32; i += blockDim.y) {
     const int r = r0 + i, c = c0 + threadIdx.x;
-    float v = 0.f;
-    if (r < rows && c < cols) {
-      v = src[(size_t)r * cols + c];
-      const float h = tf32_hi(v);
-      hi[(size_t)mat * rows * cols + (size_t)r * cols + c] = h;
-      lo[(size_t)mat * rows * cols + (size_t)r * cols + c] = tf32_lo(v, h, lrn);
-    }
-    tile[i][threadIdx.x] = v;
+    tile[i][threadIdx.x] = (r < rows && c < cols) ? src[(size_t)r * cols + c] : 0.f;
   }
   __syncthreads();
   for (int i = threadIdx.y; i < 32; i += blockDim.y) {
     const int c = c0 + i, r = r0 + threadIdx.x;   // transposed: row c, column r
-    if (c < cols && r < rows) {
-      const float v = tile[threadIdx.x][i];
-      const float h = tf32_hi(v);
-      thi[(size_t)mat * rows * cols + (size_t)c * rows + r] = h;
-      tlo[(size_t)mat * rows * cols + (size_t)c * rows + r] = tf32_lo(v, h, lrn);
-    }
+    if (c < cols && r < rows) phit[(size_t)mat * rows * cols + (size_t)c * rows + r] = tile[threadIdx.x][i];
   }
 }
 
@@ -1072,14 +1076,10 @@ bool encode_maps(const KParams &p, TcMaps *m, char *why) {
   const long mats = d.shared_phi ? 1 : d.Tl;
   const CUtensorMapDataType F32 = CU_TENSOR_MAP_DATA_TYPE_FLOAT32, F64 = CU_TENSOR_MAP_DATA_TYPE_FLOAT64;
   const int NT = p.tc.NT;
-  const bool ok = encode_2d(enc, &m->phi_h, b.Phh, F32, 4, mats * d.N, d.D, 32, TM, true) &&
-                  encode_2d(enc, &m->phi_l, b.Phl, F32, 4, mats * d.N, d.D, 32, TM, true) &&
-                  encode_2d(enc, &m->phit_h, b.PTh, F32, 4, mats * d.D, d.N, 32, TM, true) &&
-                  encode_2d(enc, &m->phit_l, b.PTl, F32, 4, mats * d.D, d.N, 32, TM, true) &&
-                  encode_2d(enc, &m->u_h, b.Uh, F32, 4, (long)d.Tl * d.Pp, d.N, 32, NT, true) &&
-                  encode_2d(enc, &m->u_l, b.Ul, F32, 4, (long)d.Tl * d.Pp, d.N, 32, NT, true) &&
-                  encode_2d(enc, &m->d_h, b.Dh, F32, 4, (long)d.Tl * d.P, d.D, 32, NT, true) &&
-                  encode_2d(enc, &m->d_l, b.Dl, F32, 4, (long)d.Tl * d.P, d.D, 32, NT, true) &&
+  const bool ok = encode_2d(enc, &m->phi, p.phi, F32, 4, mats * d.N, d.D, 32, TM, true) &&
+                  encode_2d(enc, &m->phit, b.PT, F32, 4, mats * d.D, d.N, 32, TM, true) &&
+                  encode_2d(enc, &m->u, b.U, F32, 4, (long)d.Tl * d.Pp, d.N, 32, NT, true) &&
+                  encode_2d(enc, &m->dir, b.D32, F32, 4, (long)d.Tl * d.P, d.D, 32, NT, true) &&
                   encode_2d(enc, &m->dm, b.Dm, F64, 8, (long)d.Tl * d.C, d.D, TK, d.C, false) &&
                   encode_2d(enc, &m->um, b.Um, F64, 8, (long)d.Tl * d.N, d.Cp, d.Cp, TK, false) &&
                   encode_2d(enc, &m->d32, b.D32, F32, 4, (long)d.Tl * d.P, d.D, TM, NT, false);
@@ -1109,7 +1109,7 @@ int cg_grid_size(const KParams &p) {
 cudaError_t launch_split_phi(const KParams &p, cudaStream_t s) {
   const int mats = p.d.shared_phi ? 1 : p.d.Tl;
   dim3 grid((p.d.D + 31) / 32, (p.d.N + 31) / 32, mats);
-  k_split_phi<<<grid, dim3(32, 8), 0, s>>>(p.phi, p.d.N, p.d.D, mats, p.b.Phh, p.b.Phl, p.b.PTh, p.b.PTl, p.lo_rn);
+  k_transpose_phi<<<grid, dim3(32, 8), 0, s>>>(p.phi, p.d.N, p.d.D, p.b.PT);
   return cudaGetLastError();
 }
 
