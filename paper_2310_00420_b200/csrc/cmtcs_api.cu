@@ -84,12 +84,17 @@ struct Carver {
   }
 };
 
+// widest column tile: 256 columns, or 128 with a shared Φ (its re-reads per column tile hit L2)
+// which leaves TMEM room for double-buffered or K-split accumulators (CMTCS_NTMAX overrides)
+int nt_max(int shared_phi) {
+  const char *e = getenv("CMTCS_NTMAX");
+  if (e) return std::max(16, std::min(TC_NTMAX, atoi(e) / 16 * 16));
+  return shared_phi ? 128 : TC_NTMAX;
+}
+
 TcCfg make_tc(const Dims &d) {
   TcCfg tc;
-  // column tile: up to 256 columns; 128 with a shared Φ (its re-reads per column tile hit L2), which
-  // leaves TMEM room for two K-split accumulator pairs (precision of the long K = D contraction)
-  const int ntmax = d.shared_phi ? 128 : TC_NTMAX;
-  tc.NT = std::min(ntmax, (d.P + 15) / 16 * 16);
+  tc.NT = std::min(nt_max(d.shared_phi), (d.P + 15) / 16 * 16);
   tc.slot = (tc.NT + 31) / 32 * 32;
   tc.nacc = std::max(1, std::min(4, 512 / (2 * tc.slot)));
   tc.stage_bytes = 2u * 128u * 128u + 2u * (unsigned)tc.NT * 128u + 4096u;  // + fp64 mean-column chunk
@@ -141,7 +146,7 @@ bool make_dims(const cmtcs_problem *p, Dims *d, char *why) {
   d->nw = (p->D + 63) / 64;
   d->nRT1 = (p->N + OP_BR - 1) / OP_BR;
   d->nRT2 = (p->D + OP_BR - 1) / OP_BR;
-  const int NT = std::min(p->shared_phi ? 128 : TC_NTMAX, (d->P + 15) / 16 * 16);   // = make_tc's NT
+  const int NT = std::min(nt_max(p->shared_phi), (d->P + 15) / 16 * 16);   // = make_tc's NT
   d->nCT = (d->P + NT - 1) / NT;
   {
     // split the stage-1 contraction over D (S1 ∈ {1, 2, 4, 8}, every split ≥ 128 of D) so that the
@@ -445,6 +450,7 @@ cmtcs_status cmtcs_init(cmtcs_ctx **out, const cmtcs_problem *p, const float *ph
   c->kp.d = d;
   c->kp.b = b;
   c->kp.tc = make_tc(d);
+  c->kp.tc.pf = getenv("CMTCS_PF") ? atoi(getenv("CMTCS_PF")) : 6;
   c->kp.phi = phi;
   c->kp.y = y;
   c->kp.beta = p->beta;

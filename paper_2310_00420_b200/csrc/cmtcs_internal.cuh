@@ -87,6 +87,7 @@ struct TcCfg {
   int nacc;          // K-split accumulator pairs (2·nacc·slot ≤ 512)
   int stages;        // smem pipeline depth
   unsigned stage_bytes;
+  int pf;            // L2 prefetch distance of the producer (chunks ahead; 0 = off)
   int use_dtile;     // stage-2 epilogue reads its d tile (NT × 128 fp32) from smem, staged by TMA
   unsigned dtile_bytes;
 };

@@ -16,19 +16,20 @@
 // C fp64 mean columns of a task ride along with the task's column-tile-0 units: fp64 DFMA on the
 // CUDA cores, reading the same smem Φ tiles the tensor core reads.
 //
-// Warp roles in phases 1-2 (256 threads):
+// Warp roles in phases 1-2 (384 threads):
 //   warp 0     TMA producer: fp32 Φ/Φᵀ tiles (A), direction / U tiles (B), fp64 mean-column chunk
 //   warp 1     MMA issuer: tcgen05.mma kind::tf32, tcgen05.commit frees ring stages / the tile
-//   warp 2     TMEM owner (alloc / dealloc)
-//   warps 4-7  per ring stage: tf32 split of A and B, then the fp64 mean-column MMAs (DMMA);
-//              per tile: the epilogue (TMEM → registers)
+//   warps 2-3  converters: tf32 split of A and B of every staged chunk (warp 2 also owns TMEM)
+//   warps 4-7  the fp64 mean columns: per ring stage DMMA on the split Φ tile, per tile their outputs
+//   warps 8-11 the epilogue (TMEM → registers → U / W, dᵀAd partials), overlapping the next tile's
+//              K loop when the accumulators are double-buffered in TMEM
 // All operands arrive by TMA into an S-stage ring of 128-byte-swizzled K-major smem tiles, so no
 // CTA-wide barrier runs inside a K loop; the producer runs ahead into the next unit while the
 // epilogue of the previous one drains.  mbarriers: full[s] (TMA bytes), conv[s] (split done),
 // empty[s] (MMA done), mdone[s] (fp64 warps done), tfull / tempty (accumulator handshake).
 //
 // Operands live in HBM as plain fp32 (Φ itself, its transpose, the directions, U) and arrive by TMA;
-// the epilogue warps split each staged tile in shared memory into the exact pair x = hi + lo,
+// the converter warps split each staged tile in shared memory into the exact pair x = hi + lo,
 // hi = tf32(x) (in place) and lo = x − hi (a second tile), so the operator reads every operand
 // byte once per use (mbarrier conv[s]: split done → the MMA warp may issue).
 //
@@ -62,16 +63,18 @@ constexpr int TM = 128;                   // tile rows (MMA M)
 constexpr int TK = 32;                    // K per pipeline stage (one 128-byte swizzled row)
 constexpr uint32_t A_BYTES = TM * 128;    // 16 KB per hi / lo A tile
 constexpr int MAXST = 4;
-constexpr int NTHREADS = 256;
-constexpr int EPI0 = 128;                 // first thread of the epilogue / fp64 warps (4-7)
+constexpr int NTHREADS = 384;
+constexpr int MEAN0 = 128;                // first thread of the mean (fp64) warps 4-7
+constexpr int EPI0 = 256;                 // first thread of the epilogue warps 8-11
 
 struct PSmemTail {
-  uint64_t full[MAXST], conv[MAXST], empty[MAXST], mdone[MAXST];
-  uint64_t tfull, tempty;
+  uint64_t full[MAXST], conv[MAXST], convm[MAXST], empty[MAXST], mdone[MAXST];
+  uint64_t tfull[2], tempty[2];      // TMEM accumulator buffers: MMA done / epilogue drained
   uint64_t dfull, dempty;             // the stage-2 epilogue's d tile (TMA bytes / epilogue done)
   uint32_t tslot;
   uint32_t emask[4][TC_NTMAX / 32];   // per epilogue warp: active-column mask of its current tile
-  double red[4][TC_NTMAX + MAXC];     // per epilogue warp: dᵀAd partials, probe [0, NT), mean [NT_MAX, +C)
+  double red[4][TC_NTMAX];            // per epilogue warp: dᵀAd partials of the probe columns
+  double redm[4][MAXC];               // per mean warp: dᵀAd partials of the mean columns
 };
 
 template <class T>
@@ -82,11 +85,18 @@ __device__ __forceinline__ void stv(T *p, T v) { *p = v; }
 __device__ __forceinline__ void fence_proxy_async_global() {
   asm volatile("fence.proxy.async.global;\n" ::: "memory");
 }
+// TMA prefetch of a tile into L2 (no shared memory, no completion tracking)
+__device__ __forceinline__ void tma_prefetch_2d(const CUtensorMap *map, int x, int y) {
+  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];\n" ::"l"(
+                   reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y)
+               : "memory");
+}
+
 __device__ __forceinline__ void mbar_arrive(uint64_t *mbar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(mbar)) : "memory");
 }
 // named barrier among the 4 epilogue warps
-__device__ __forceinline__ void epi_sync() { asm volatile("bar.sync 1, 128;\n" ::: "memory"); }
+__device__ __forceinline__ void epi_sync() { asm volatile("bar.sync 2, 128;\n" ::: "memory"); }
 
 // grid-wide barrier over the co-resident CTAs: a monotonically increasing arrival counter
 // (reset to 0 before every launch); epoch e completes when the counter reaches e·gridDim.x
@@ -145,7 +155,13 @@ __device__ __forceinline__ double warp_sum(double v) {
 }
 
 // K-split accumulator pairs of a tile: one for short contractions (K ≤ 512), else up to tc.nacc
+// Double-buffered accumulators (two 256-column TMEM buffers, one accumulator pair each) for tiles of
+// up to 128 columns and K ≤ 2048; longer contractions keep K-split pairs in one 512-column buffer.
+__device__ __forceinline__ bool unit_dbl(const TcCfg &tc, int nk, int dbg) {
+  return tc.slot <= 128 && nk <= 64 && !(dbg & 16);
+}
 __device__ __forceinline__ int unit_nacc(const TcCfg &tc, int nk, int dbg) {
+  if (unit_dbl(tc, nk, dbg)) return 1;
   return (nk <= 16 && !(dbg & 8)) ? 1 : min(tc.nacc, nk);
 }
 
@@ -297,12 +313,13 @@ __device__ __forceinline__ float tf32_rna(float x) {
   return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xFFFFE000u);
 }
 
-// Split rows r, r+128, ... (nrows of them) of a staged 128-byte-swizzled fp32 tile into the exact
-// pair x = hi + lo: hi = tf32(x) written in place, lo = x − hi written to the same offsets of `lo`.
-// The swizzle permutes 16-byte chunks within a row only, so a whole row is 8 chunks at fixed
-// offsets; lane r visits them in the order c ^ (r & 7), which spreads a warp over all 32 banks.
-__device__ __forceinline__ void split_rows(uint32_t hi, uint32_t lo, int r, int nrows) {
-  for (int i = 0; i < nrows; ++i, r += 128) {
+// Split rows of a staged 128-byte-swizzled fp32 tile into the exact pair x = hi + lo: hi = tf32(x)
+// written in place, lo = x − hi written to the same offsets of `lo`.  The swizzle permutes 16-byte
+// chunks within a row only, so a whole row is 8 chunks at fixed offsets; lane r visits them in the
+// order c ^ (r & 7), which spreads a warp over all 32 banks.  Rows r, r + 64, ... below nrows
+// (64 converter threads).
+__device__ __forceinline__ void split_rows64(uint32_t hi, uint32_t lo, int r, int nrows) {
+  for (; r < nrows; r += 64) {
     const uint32_t row = (uint32_t)(r >> 3) * 1024 + (uint32_t)(r & 7) * 128;
     float4 v[8];
 #pragma unroll
@@ -447,7 +464,7 @@ __device__ void update_mean(const KParams &p, int t, int c, int u, int lane) {
   const double2 *w = reinterpret_cast<const double2 *>(p.b.Wm + g * d.D);
   const int n2 = d.D >> 1;
   double acc = 0.0;
-  constexpr int U = 4;
+  constexpr int U = 2;
   for (int i0 = lane; i0 < n2; i0 += 32 * U) {
     double2 dd[U], ww[U], xx[U], rn[U];
 #pragma unroll
@@ -566,8 +583,17 @@ __device__ __forceinline__ void unit_work(const KParams &p, Unit &x, int lane, u
 struct RingCtl {
   int S;
   uint32_t g;      // chunks handled so far by this role
-  uint32_t ti;     // accumulator tiles handled so far (tfull / tempty phases)
+  int st;          // = g % S (kept incrementally: no integer division in the K loops)
+  uint32_t ph;     // = (g / S) & 1
+  __device__ __forceinline__ void next() {
+    ++g;
+    if (++st == S) { st = 0; ph ^= 1u; }
+  }
+  uint32_t ti;     // accumulator tiles handled so far
+  uint32_t tuse[2];  // uses of each TMEM accumulator buffer (tfull / tempty phases)
   uint32_t di;     // stage-2 d tiles handled so far (dfull / dempty phases)
+  uint32_t smean;  // producer: bit s = the chunk last placed in slot s belongs to a mean unit
+  uint32_t mcnt[MAXST];  // producer: mean chunks placed in each slot (mdone phases)
 };
 
 // ---- producer (warp 0, one lane) ---------------------------------------------------------------
@@ -577,28 +603,46 @@ __device__ __forceinline__ void produce(const KParams &p, const TcMaps &mp, unsi
   const uint32_t b_bytes = (uint32_t)p.tc.NT * 128;
   const uint32_t mean_tx = x.stage == 1 ? (uint32_t)p.d.C * TK * 8 : (uint32_t)TK * p.d.Cp * 8;
   const uint32_t bytes = A_BYTES + (x.nmma ? b_bytes : 0) + (x.mean ? mean_tx : 0);
-  if (x.stage == 2 && x.nmma && p.tc.use_dtile) {
-    // the epilogue's d tile: rows d0..d0+127 of the tile's NT direction columns
-    if (rc.di > 0) mbar_wait(&tl.dempty, (rc.di - 1) & 1);
-    unsigned char *dt = sm + (size_t)rc.S * p.tc.stage_bytes;
-    mbar_arrive_expect_tx(&tl.dfull, p.tc.dtile_bytes);
-    tma_load_2d(dt, &mp.d32, x.rt * TM, x.t * p.d.P + x.ct * p.tc.NT, &tl.dfull);
-    rc.di++;
-  }
   for (int kc = 0; kc < x.nk; ++kc) {
-    const uint32_t G = rc.g++;
-    const int st = G % rc.S;
+    const uint32_t G = rc.g;
+    const int st = rc.st;
+    const uint32_t cph = rc.ph;
+    rc.next();
     if (G >= (uint32_t)rc.S) {
-      const uint32_t ph = ((G - rc.S) / rc.S) & 1;
-      mbar_wait(&tl.empty[st], ph);
-      mbar_wait(&tl.mdone[st], ph);
+      mbar_wait(&tl.empty[st], cph ^ 1u);      // MMAs of chunk G − S (same slot) done
+      if ((rc.smean >> st) & 1u) mbar_wait(&tl.mdone[st], (rc.mcnt[st] - 1) & 1);   // its fp64 work too
+    }
+    if (x.mean) {
+      rc.smean |= 1u << st;
+      rc.mcnt[st]++;
+    } else {
+      rc.smean &= ~(1u << st);
     }
     if (tr && kc < 16) tr[kc] = globaltimer();
     unsigned char *base = sm + (size_t)st * p.tc.stage_bytes;
     uint64_t *fb = &tl.full[st];
     mbar_arrive_expect_tx(fb, bytes);
     const int k = x.k0 + kc * TK;
-    // fp32 tiles into the hi slots (split in place by the epilogue warps, lo into the lo slots)
+    // L2 prefetch PF chunks ahead: HBM latency is hidden beyond the depth of the smem ring
+    const int kp = kc + p.tc.pf;
+    if (p.tc.pf && kp < x.nk) {
+      const int kk = x.k0 + kp * TK;
+      if (x.stage == 1) {
+        tma_prefetch_2d(&mp.phi, kk, x.arow);
+        if (x.nmma) tma_prefetch_2d(&mp.dir, kk, x.brow);
+      } else {
+        tma_prefetch_2d(&mp.phit, kk, x.arow);
+        if (x.nmma) tma_prefetch_2d(&mp.u, kk, x.brow);
+      }
+    }
+    if (kc == 0 && p.tc.pf) {                 // the first chunks of the unit
+      for (int k2 = 1; k2 < min(p.tc.pf, x.nk); ++k2) {
+        const int kk = x.k0 + k2 * TK;
+        tma_prefetch_2d(x.stage == 1 ? &mp.phi : &mp.phit, kk, x.arow);
+        if (x.nmma) tma_prefetch_2d(x.stage == 1 ? &mp.dir : &mp.u, kk, x.brow);
+      }
+    }
+    // fp32 tiles into the hi slots (split in place by the converter warps, lo into the lo slots)
     if (x.stage == 1) {
       tma_load_2d(base, &mp.phi, k, x.arow, fb);
       if (x.nmma) tma_load_2d(base + 2 * A_BYTES, &mp.dir, k, x.brow, fb);
@@ -610,6 +654,15 @@ __device__ __forceinline__ void produce(const KParams &p, const TcMaps &mp, unsi
     }
     if (tr && kc < 16) tr[16 + kc] = globaltimer();
   }
+  if (x.stage == 2 && x.nmma && p.tc.use_dtile) {
+    // the epilogue's d tile (rows d0..d0+127 of the tile's NT direction columns), after the K loop
+    // so the ring keeps streaming while the previous tile's epilogue still reads its d tile
+    if (rc.di > 0) mbar_wait(&tl.dempty, (rc.di - 1) & 1);
+    unsigned char *dt = sm + (size_t)rc.S * p.tc.stage_bytes;
+    mbar_arrive_expect_tx(&tl.dfull, p.tc.dtile_bytes);
+    tma_load_2d(dt, &mp.d32, x.rt * TM, x.t * p.d.P + x.ct * p.tc.NT, &tl.dfull);
+    rc.di++;
+  }
 }
 
 // ---- MMA issuer (warp 1, one lane) ---------------------------------------------------------------
@@ -619,46 +672,210 @@ __device__ __forceinline__ void mma_unit(const KParams &p, unsigned char *sm, PS
   const uint32_t b_bytes = (uint32_t)tc.NT * 128;
   const int nacc = unit_nacc(tc, x.nk, p.dbg_flags);
   const uint32_t idesc = idesc_tf32(TM, x.nmma > 0 ? x.nmma : 16);
-  if (x.nmma && rc.ti > 0) {
-    mbar_wait(&tl.tempty, (rc.ti - 1) & 1);   // the epilogue has drained the previous tile
+  const bool dbl = unit_dbl(tc, x.nk, p.dbg_flags);
+  const int bi = dbl ? (int)(rc.ti & 1) : 0;
+  const uint32_t tacc = tmem + (uint32_t)(bi * 256);
+  if (x.nmma) {
+    // the epilogue has drained this buffer's previous tile (both buffers for a 512-column tile)
+    if (rc.tuse[bi] > 0) mbar_wait(&tl.tempty[bi], (rc.tuse[bi] - 1) & 1);
+    if (!dbl && rc.tuse[1] > 0) mbar_wait(&tl.tempty[1], (rc.tuse[1] - 1) & 1);
     fence_after_sync();
   }
   for (int kc = 0; kc < x.nk; ++kc) {
-    const uint32_t G = rc.g++;
-    const int st = G % rc.S;
-    mbar_wait(&tl.conv[st], (G / rc.S) & 1);      // operands staged and split
+    const int st = rc.st;
+    mbar_wait(&tl.conv[st], rc.ph);           // operands staged and split
+    rc.next();
     if (tr && kc < 16) tr[32 + kc] = globaltimer();
     if (x.nmma && !(p.dbg_flags & 2)) {
       fence_after_sync();
       const int q = (kc * nacc) / x.nk;
       const int qfirst = (q * x.nk + nacc - 1) / nacc;
-      mma_stage(tmem, sm + (size_t)st * tc.stage_bytes, b_bytes, idesc, q, tc.slot, kc == qfirst);
+      mma_stage(tacc, sm + (size_t)st * tc.stage_bytes, b_bytes, idesc, q, tc.slot, kc == qfirst);
       mma_commit(&tl.empty[st]);
     } else {
       mbar_arrive(&tl.empty[st]);
     }
   }
   if (x.nmma) {
-    if (p.dbg_flags & 2) mbar_arrive(&tl.tfull);
-    else mma_commit(&tl.tfull);              // all MMAs of the tile complete → accumulator ready
+    if (p.dbg_flags & 2) mbar_arrive(&tl.tfull[bi]);
+    else mma_commit(&tl.tfull[bi]);          // all MMAs of the tile complete → accumulator ready
+    rc.tuse[bi]++;
     rc.ti++;
   }
 }
 
-// ---- epilogue + fp64 warps (warps 4-7) ---------------------------------------------------------
+// ---- converter warps (2-3): tf32 split of every staged chunk --------------------------------------
+__device__ __forceinline__ void convert_unit(const KParams &p, unsigned char *sm, PSmemTail &tl, RingCtl &rc,
+                                             const Unit &x) {
+  const int ct = threadIdx.x - 64;            // 0..63
+  const uint32_t b_bytes = (uint32_t)p.tc.NT * 128;
+  for (int kc = 0; kc < x.nk; ++kc) {
+    const int st = rc.st;
+    mbar_wait(&tl.full[st], rc.ph);
+    rc.next();
+    const uint32_t base = smem_u32(sm) + (uint32_t)st * p.tc.stage_bytes;
+    if (!(p.dbg_flags & 4)) {
+      split_rows64(base, base + A_BYTES, ct, TM);                     // A: 128 rows
+      if (x.nmma) split_rows64(base + 2 * A_BYTES, base + 2 * A_BYTES + b_bytes, ct, x.nmma);   // B rows
+    }
+    fence_proxy_async();                      // generic smem writes → tensor-core (async proxy) reads
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0) {
+      mbar_arrive(&tl.conv[st]);
+      if (x.mean) mbar_arrive(&tl.convm[st]);  // the mean warps follow mean chunks only
+    }
+  }
+}
+
+// named barriers: 1 = mean warps (4-7), 2 = epilogue warps (8-11), 3 = both groups (256 threads)
+__device__ __forceinline__ void mean_sync() { asm volatile("bar.sync 1, 128;\n" ::: "memory"); }
+__device__ __forceinline__ void pair_sync() { asm volatile("bar.sync 3, 256;\n" ::: "memory"); }
+
+// Split-K handoff of a stage-1 tile (S1 > 1): every split CTA arrives on the tile counter and waits
+// until all S1 partials are written (the host picks S1 > 1 only when all stage-1 units are
+// co-resident).  Called by the mean and the epilogue warps together (256 threads).
+__device__ __forceinline__ void split_handoff(const KParams &p, const Unit &x) {
+  __threadfence();
+  pair_sync();
+  if (threadIdx.x == EPI0) {
+    int *cnt = p.b.tilecnt + ((size_t)x.t * p.d.nCT + x.ct) * p.d.nRT1 + x.rt;
+    const int ticket = atomicAdd(cnt, 1);
+    const int target = (ticket / p.d.S1 + 1) * p.d.S1;
+    int v;
+    do {
+      asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];\n" : "=r"(v) : "l"(cnt) : "memory");
+    } while (v < target);
+    asm volatile("fence.acq_rel.gpu;\n" ::: "memory");
+  }
+  pair_sync();
+}
+
+// rows [rb, re) of a stage-1 tile summed over the S1 split partials (this split's share)
+__device__ __forceinline__ void split_share(const Dims &d, const Unit &x, int *rb, int *re) {
+  const int n0 = x.rt * TM, rows = min(TM, d.N - n0);
+  const int rs = ((rows + d.S1 - 1) / d.S1 + 3) & ~3;       // rows per share (×4: float4 rows)
+  *rb = min(rows, x.sp * rs);
+  *re = min(rows, *rb + rs);
+}
+
+// ---- mean warps (4-7): fp64 mean columns on the FP64 tensor path --------------------------------
 template <int CC>
-__device__ void epilogue_unit(const KParams &p, unsigned char *sm, PSmemTail &tl, RingCtl &rc, uint32_t tmem,
-                              const Unit &x, const uint32_t *mask_in, unsigned long long *tr) {
+__device__ void mean_unit(const KParams &p, unsigned char *sm, PSmemTail &tl, RingCtl &rc, const Unit &x) {
+  const Dims &d = p.d;
+  const TcCfg &tc = p.tc;
+  const int mt0 = threadIdx.x - MEAN0, mw = mt0 >> 5, lane = mt0 & 31;
+  const int N = d.N, D = d.D, C = d.C;
+  const uint32_t b_bytes = (uint32_t)tc.NT * 128;
+  const uint32_t mu_off = 2 * A_BYTES + 2 * b_bytes;
+  constexpr int NTC = (CC + 7) / 8;         // 8-column fp64 MMA tiles covering the C mean columns
+  double macc[4][NTC][2];
+#pragma unroll
+  for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < NTC; ++nt) macc[mt][nt][0] = macc[mt][nt][1] = 0.0;
+  const int fg = lane >> 2, fq = lane & 3;   // fragment row group / column pair of this lane
+  // only chunks of mean units are waited for (convm: one phase per mean chunk of the slot; the
+  // producer refills a slot holding a mean chunk only after mdone, so phases cannot alias) and
+  // released through mdone; the ring position still advances over every chunk
+  for (int kc = 0; kc < x.nk; ++kc) {
+    const int st = rc.st;
+    rc.next();
+    if (x.mean) {
+      mbar_wait(&tl.convm[st], rc.mcnt[st] & 1);
+      rc.mcnt[st]++;
+      if (!(p.dbg_flags & 1)) {
+        const uint32_t base = smem_u32(sm) + (uint32_t)st * tc.stage_bytes;
+        if (x.stage == 1) mean_stage<true, NTC>(base, base + mu_off, mw, lane, C, d.Cp, macc);
+        else mean_stage<false, NTC>(base, base + mu_off, mw, lane, C, d.Cp, macc);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tl.mdone[st]);
+    }
+  }
+  if (x.stage == 1) {
+    if (x.mean) {
+      double *dst = d.S1 == 1 ? p.b.Um + (size_t)x.t * N * d.Cp
+                              : p.b.Umpart + ((size_t)x.t * d.S1 + x.sp) * N * d.Cp;
+#pragma unroll
+      for (int mt = 0; mt < 4; ++mt) {
+        const int nn = x.rt * TM + 32 * mw + 8 * mt + fg;
+#pragma unroll
+        for (int nt = 0; nt < NTC; ++nt) {
+          const int c = 8 * nt + 2 * fq;       // Cp is even: columns c, c+1 are both < Cp or both ≥ C
+          if (nn < N && c < C) stv(reinterpret_cast<double2 *>(dst + (size_t)nn * d.Cp + c),
+                                   make_double2(macc[mt][nt][0], macc[mt][nt][1]));
+        }
+      }
+    }
+    if (d.S1 > 1) {
+      split_handoff(p, x);
+      int rb, re;
+      split_share(d, x, &rb, &re);
+      if (x.mean && re > rb) {
+        const int n0 = x.rt * TM;
+        const int nm = (re - rb) * d.Cp / 2;   // double2 elements of this share of Um
+        const double *mbase = p.b.Umpart + (size_t)x.t * d.S1 * N * d.Cp;
+        for (int e = mt0; e < nm; e += 128) {
+          const size_t o = (size_t)(n0 + rb) * d.Cp + 2 * e;
+          double2 v = make_double2(0.0, 0.0);
+          for (int sidx = 0; sidx < d.S1; ++sidx) {
+            const double2 pv = __ldcg(reinterpret_cast<const double2 *>(mbase + (size_t)sidx * N * d.Cp + o));
+            v.x += pv.x;
+            v.y += pv.y;
+          }
+          *reinterpret_cast<double2 *>(p.b.Um + (size_t)x.t * N * d.Cp + o) = v;
+        }
+      }
+    }
+    return;
+  }
+  if (!x.mean) return;
+  // stage 2: Wm = β·acc + α ⊙ dm on this lane's fragment rows / columns, and the partial dᵀWm per
+  // column over the tile (fragment rows, the 8 row groups of the warp, then the 4 warps)
+#pragma unroll
+  for (int nt = 0; nt < NTC; ++nt) {
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int c = 8 * nt + 2 * fq + e;
+      double dot = 0.0;
+#pragma unroll
+      for (int mt = 0; mt < 4; ++mt) {
+        const int de = x.rt * TM + 32 * mw + 8 * mt + fg;
+        if (c < C && de < D) {
+          const size_t o = ((size_t)x.t * C + c) * D + de;
+          const double dmv = ldv(p.b.Dm + o);
+          const double wv = fma(p.beta, macc[mt][nt][e], p.b.alpha64[(size_t)c * D + de] * dmv);
+          stv(p.b.Wm + o, wv);
+          dot = fma(dmv, wv, dot);
+        }
+      }
+#pragma unroll
+      for (int o = 4; o < 32; o <<= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
+      if (fg == 0 && c < C) tl.redm[mw][c] = dot;
+    }
+  }
+  mean_sync();
+  if (mt0 < C)
+    stv(p.b.dAdm + ((size_t)x.t * C + mt0) * d.nRT2 + x.rt, tl.redm[0][mt0] + tl.redm[1][mt0] + tl.redm[2][mt0] + tl.redm[3][mt0]);
+  mean_sync();                                // tl.redm is reused by the next unit
+}
+
+// ---- epilogue warps (8-11): the probe columns' accumulator tile ------------------------------
+// TMEM accumulator buffer of a tile: two buffers (columns [0, 256) and [256, 512)) when the tile's
+// accumulators fit in 256 columns, so the MMA warp starts the next tile while this one drains
+__device__ __forceinline__ int acc_buf(const RingCtl &rc, bool dbl) { return dbl ? (int)(rc.ti & 1) : 0; }
+
+template <int CC>
+__device__ void probe_epilogue(const KParams &p, unsigned char *sm, PSmemTail &tl, RingCtl &rc, uint32_t tmem,
+                               const Unit &x, const uint32_t *mask_in, unsigned long long *tr) {
   if (tr && threadIdx.x != EPI0) tr = nullptr;
-  if (tr) tr[83] = globaltimer();
   const Dims &d = p.d;
   const TcCfg &tc = p.tc;
   const int et = threadIdx.x - EPI0, ew = et >> 5, lane = et & 31;
   const int r = et;                          // tile row = TMEM lane
   const int N = d.N, D = d.D, P = d.P, C = d.C;
-  const uint32_t b_bytes = (uint32_t)tc.NT * 128;
-  const uint32_t mu_off = 2 * A_BYTES + 2 * b_bytes;
   const int nacc = unit_nacc(tc, x.nk, p.dbg_flags);
+  const bool dbl = unit_dbl(tc, x.nk, p.dbg_flags);
   const int j0 = x.ct * tc.NT;
   if (lane < TC_NTMAX / 32) {
     uint32_t v = 0;
@@ -669,250 +886,145 @@ __device__ void epilogue_unit(const KParams &p, unsigned char *sm, PSmemTail &tl
   }
   __syncwarp();
   const uint32_t *mask = tl.emask[ew];
-  constexpr int NTC = (CC + 7) / 8;         // 8-column fp64 MMA tiles covering the C mean columns
-  double macc[4][NTC][2];
-#pragma unroll
-  for (int mt = 0; mt < 4; ++mt)
-#pragma unroll
-    for (int nt = 0; nt < NTC; ++nt) macc[mt][nt][0] = macc[mt][nt][1] = 0.0;
-  const int fg = lane >> 2, fq = lane & 3;   // fragment row group / column pair of this lane
-  // mainloop: fp64 mean-column DFMA on each stage (or just release it)
-  for (int kc = 0; kc < x.nk; ++kc) {
-    const uint32_t G = rc.g++;
-    const int st = G % rc.S;
-    mbar_wait(&tl.full[st], (G / rc.S) & 1);
-    if (tr && kc < 16) tr[64 + kc] = globaltimer();
-    {
-      // tf32 split of the staged fp32 tiles: A (128 rows, this thread's row) and B (x.ncol rows)
-      const uint32_t base = smem_u32(sm) + (uint32_t)st * tc.stage_bytes;
-      split_rows(base, base + A_BYTES, et, 1);
-      if (x.nmma) split_rows(base + 2 * A_BYTES, base + 2 * A_BYTES + b_bytes, et, (x.nmma + 127 - et) / 128);
-      fence_proxy_async();                    // generic smem writes → tensor-core (async proxy) reads
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&tl.conv[st]);
-    }
-    if (x.mean && !(p.dbg_flags & 1)) {
-      const uint32_t base = smem_u32(sm) + (uint32_t)st * tc.stage_bytes;
-      if (x.stage == 1) mean_stage<true, NTC>(base, base + mu_off, ew, lane, C, d.Cp, macc);
-      else mean_stage<false, NTC>(base, base + mu_off, ew, lane, C, d.Cp, macc);
-    }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&tl.mdone[st]);
+  uint32_t tacc = tmem;                      // this tile's accumulator buffer
+  if (x.nmma) {
+    const int bi = acc_buf(rc, dbl);
+    tacc = tmem + (uint32_t)(bi * 256);
+    mbar_wait(&tl.tfull[bi], rc.tuse[bi] & 1);
+    if (tr) tr[80] = globaltimer();
+    fence_after_sync();
   }
-  if (tr) tr[85] = globaltimer();
   if (x.stage == 1) {
     const int n = x.rt * TM + r;
     float *Ut = p.b.U + (size_t)x.t * d.Pp * N;
     float *part = p.b.Upart + ((size_t)x.t * d.S1 + x.sp) * d.Pp * N;
     if (x.nmma) {
-      mbar_wait(&tl.tfull, rc.ti & 1);
-      if (tr) tr[80] = globaltimer();
-      fence_after_sync();
       for (int c0 = 0; c0 < x.nmma; c0 += 16) {
         float tot[16];
-        acc_load16(tmem, ew, c0, nacc, tc.slot, tot);
-        if (tr && c0 < 128) tr[90 + (c0 >> 4) * 2] = globaltimer();
+        acc_load16(tacc, ew, c0, nacc, tc.slot, tot);
         if (n < N) {
 #pragma unroll
           for (int i = 0; i < 16; ++i) {
             const int c = c0 + i;
             if (c < x.ncol) {
               const size_t o = (size_t)(j0 + c) * N + n;
-              if (d.S1 == 1) {
-                Ut[o] = tot[i];
-              } else {
-                stv(part + o, tot[i]);
-              }
+              if (d.S1 == 1) Ut[o] = tot[i];
+              else stv(part + o, tot[i]);
             }
           }
         }
-        if (tr && c0 < 128) tr[91 + (c0 >> 4) * 2] = globaltimer();
       }
       fence_before_sync();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&tl.tempty);  // the MMA warp may overwrite the accumulator
+      const int bi = acc_buf(rc, dbl);
+      if (lane == 0) mbar_arrive(&tl.tempty[bi]);  // the MMA warp may overwrite the accumulator
+      rc.tuse[bi]++;
       rc.ti++;
       if (tr) tr[81] = globaltimer();
     }
-    if (x.mean) {
-      double *dst = d.S1 == 1 ? p.b.Um + (size_t)x.t * N * d.Cp
-                              : p.b.Umpart + ((size_t)x.t * d.S1 + x.sp) * N * d.Cp;
-#pragma unroll
-      for (int mt = 0; mt < 4; ++mt) {
-        const int nn = x.rt * TM + 32 * ew + 8 * mt + fg;
-#pragma unroll
-        for (int nt = 0; nt < NTC; ++nt) {
-          const int c = 8 * nt + 2 * fq;       // Cp is even: columns c, c+1 are both < Cp or both ≥ C
-          if (nn < N && c < C) stv(reinterpret_cast<double2 *>(dst + (size_t)nn * d.Cp + c),
-                                   make_double2(macc[mt][nt][0], macc[mt][nt][1]));
-        }
-      }
-    }
     if (d.S1 > 1) {
-      // The S1 split CTAs of this tile run in the same round (the host picks S1 > 1 only when all
-      // stage-1 units fit the grid): each arrives on the tile counter, waits for all S1 partials,
-      // then sums its 1/S1 share of the tile's rows in split order (deterministic).
-      __threadfence();
-      epi_sync();
-      if (et == 0) {
-        int *cnt = p.b.tilecnt + ((size_t)x.t * d.nCT + x.ct) * d.nRT1 + x.rt;
-        const int ticket = atomicAdd(cnt, 1);
-        const int target = (ticket / d.S1 + 1) * d.S1;
-        int v;
-        do {
-          asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];\n" : "=r"(v) : "l"(cnt) : "memory");
-        } while (v < target);
-        asm volatile("fence.acq_rel.gpu;\n" ::: "memory");
-      }
-      epi_sync();
-      if (tr) tr[86] = globaltimer();
-      const int n0 = x.rt * TM, rows = min(TM, N - n0);
-      const int rs = ((rows + d.S1 - 1) / d.S1 + 3) & ~3;     // rows of this split's share (×4)
-      const int rb = x.sp * rs, re = min(rows, rb + rs);
-      if (re > rb) {
-        const int r4n = (re - rb) >> 2;
+      split_handoff(p, x);
+      int rb, re;
+      split_share(d, x, &rb, &re);
+      if (x.nmma && re > rb) {
+        const int n0 = x.rt * TM, r4n = (re - rb) >> 2;
         const size_t split = (size_t)d.Pp * N;
         const float *base = p.b.Upart + (size_t)x.t * d.S1 * split;
-        if (x.nmma) {
-          const int tot4 = x.ncol * r4n;
-          constexpr int V = 4;
-          for (int e0 = et; e0 < tot4; e0 += 128 * V) {
-            float4 acc4[V];
-            size_t off[V];
+        const int tot4 = x.ncol * r4n;
+        constexpr int V = 4;
+        for (int e0 = et; e0 < tot4; e0 += 128 * V) {
+          float4 acc4[V];
+          size_t off[V];
+#pragma unroll
+          for (int v = 0; v < V; ++v) {
+            const int e = min(e0 + 128 * v, tot4 - 1);
+            off[v] = (size_t)(j0 + e / r4n) * N + n0 + rb + 4 * (e % r4n);
+            acc4[v] = __ldcg(reinterpret_cast<const float4 *>(base + off[v]));
+          }
+          for (int sidx = 1; sidx < d.S1; ++sidx) {
+            float4 pv[V];
+#pragma unroll
+            for (int v = 0; v < V; ++v) pv[v] = __ldcg(reinterpret_cast<const float4 *>(base + sidx * split + off[v]));
 #pragma unroll
             for (int v = 0; v < V; ++v) {
-              const int e = min(e0 + 128 * v, tot4 - 1);
-              off[v] = (size_t)(j0 + e / r4n) * N + n0 + rb + 4 * (e % r4n);
-              acc4[v] = __ldcg(reinterpret_cast<const float4 *>(base + off[v]));
-            }
-            for (int sidx = 1; sidx < d.S1; ++sidx) {
-              float4 pv[V];
-#pragma unroll
-              for (int v = 0; v < V; ++v) pv[v] = __ldcg(reinterpret_cast<const float4 *>(base + sidx * split + off[v]));
-#pragma unroll
-              for (int v = 0; v < V; ++v) {
-                acc4[v].x += pv[v].x; acc4[v].y += pv[v].y; acc4[v].z += pv[v].z; acc4[v].w += pv[v].w;
-              }
-            }
-#pragma unroll
-            for (int v = 0; v < V; ++v) {
-              if (e0 + 128 * v < tot4) {
-                *reinterpret_cast<float4 *>(Ut + off[v]) = acc4[v];
-              }
+              acc4[v].x += pv[v].x; acc4[v].y += pv[v].y; acc4[v].z += pv[v].z; acc4[v].w += pv[v].w;
             }
           }
-        }
-        if (x.mean) {
-          const int nm = (re - rb) * d.Cp / 2;   // double2 elements of this share of Um
-          const double *mbase = p.b.Umpart + (size_t)x.t * d.S1 * N * d.Cp;
-          for (int e = et; e < nm; e += 128) {
-            const size_t o = (size_t)(n0 + rb) * d.Cp + 2 * e;
-            double2 v = make_double2(0.0, 0.0);
-            for (int sidx = 0; sidx < d.S1; ++sidx) {
-              const double2 pv = __ldcg(reinterpret_cast<const double2 *>(mbase + (size_t)sidx * N * d.Cp + o));
-              v.x += pv.x;
-              v.y += pv.y;
-            }
-            *reinterpret_cast<double2 *>(p.b.Um + (size_t)x.t * N * d.Cp + o) = v;
-          }
+#pragma unroll
+          for (int v = 0; v < V; ++v)
+            if (e0 + 128 * v < tot4) *reinterpret_cast<float4 *>(Ut + off[v]) = acc4[v];
         }
       }
     }
     if (tr) tr[82] = globaltimer();
     return;
   }
-  // ---- stage 2 epilogue: W = β acc + α_c ⊙ d for row dd, fp64 partial dᵀW per column (this tile) ----
+  if (!x.nmma) return;
+  // ---- stage 2: W = β acc + α_c ⊙ d for row dd, fp64 partial dᵀW per column (this tile) ----
   const int dd = x.rt * TM + r;
   const bool rv = dd < D;
   const float betaf = (float)p.beta;
-  if (x.mean) {
-    // mean columns (fp64): Wm = β·acc + α ⊙ dm on this lane's fragment rows / columns, and the
-    // partial dᵀWm per column over the tile (fragment rows, then the 8 row groups of the warp)
+  const size_t colbase = ((size_t)x.t * P + j0) * D + dd;
+  float aC[CC];                               // α_c at this row for the clusters of the tile's columns
 #pragma unroll
-    for (int nt = 0; nt < NTC; ++nt) {
-      double dot[2] = {0.0, 0.0};
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int c = 8 * nt + 2 * fq + e;
-#pragma unroll
-        for (int mt = 0; mt < 4; ++mt) {
-          const int de = x.rt * TM + 32 * ew + 8 * mt + fg;
-          if (c < C && de < D) {
-            const size_t o = ((size_t)x.t * C + c) * D + de;
-            const double dmv = ldv(p.b.Dm + o);
-            const double wv = fma(p.beta, macc[mt][nt][e], p.b.alpha64[(size_t)c * D + de] * dmv);
-            stv(p.b.Wm + o, wv);
-            dot[e] = fma(dmv, wv, dot[e]);
-          }
-        }
-#pragma unroll
-        for (int o = 4; o < 32; o <<= 1) dot[e] += __shfl_xor_sync(0xffffffffu, dot[e], o);
-        if (fg == 0 && c < C) tl.red[ew][TC_NTMAX + c] = dot[e];
-      }
-    }
+  for (int c = 0; c < CC; ++c) aC[c] = (c < C && rv) ? p.b.alpha32[(size_t)c * D + dd] : 0.f;
+  const bool dts = tc.use_dtile;
+  const float *dtile = reinterpret_cast<const float *>(sm + (size_t)rc.S * tc.stage_bytes);
+  if (dts) {
+    mbar_wait(&tl.dfull, rc.di & 1);
+    rc.di++;
   }
-  if (tr) tr[86] = globaltimer();
-  if (x.nmma) {
-    mbar_wait(&tl.tfull, rc.ti & 1);
-    if (tr) tr[80] = globaltimer();
-    fence_after_sync();
-    const size_t colbase = ((size_t)x.t * P + j0) * D + dd;
-    float aC[CC];                             // α_c at this row for the clusters of the tile's columns
+  // d of the next 16-column group is loaded while the current one is processed (global loads when
+  // the d tile does not fit in shared memory)
+  float dnx[16];
+  auto load_d = [&](int c0, float *dst) {
+    const uint32_t mk = c0 < x.nmma ? (mask[c0 >> 5] >> (c0 & 31)) & 0xFFFFu : 0u;
 #pragma unroll
-    for (int c = 0; c < CC; ++c) aC[c] = (c < C && rv) ? p.b.alpha32[(size_t)c * D + dd] : 0.f;
-    const bool dts = tc.use_dtile;
-    const float *dtile = reinterpret_cast<const float *>(sm + (size_t)rc.S * tc.stage_bytes);
-    if (dts) {
-      mbar_wait(&tl.dfull, rc.di & 1);
-      rc.di++;
+    for (int i = 0; i < 16; ++i) {
+      const bool ok = ((mk >> i) & 1u) && rv;
+      dst[i] = ok ? (dts ? dtile[(c0 + i) * TM + r] : ldv(p.b.D32 + colbase + (size_t)(c0 + i) * D)) : 0.f;
     }
-    for (int c0 = 0; c0 < x.nmma; c0 += 16) {
-      float dv[16], al[16], tot[16];
-      const uint32_t mk = (mask[c0 >> 5] >> (c0 & 31)) & 0xFFFFu;
+  };
+  load_d(0, dnx);
+  for (int c0 = 0; c0 < x.nmma; c0 += 16) {
+    float dv[16], tot[16];
 #pragma unroll
-      for (int i = 0; i < 16; ++i) {
-        const bool ok = ((mk >> i) & 1u) && rv;
-        dv[i] = ok ? (dts ? dtile[(c0 + i) * TM + r] : ldv(p.b.D32 + colbase + (size_t)(c0 + i) * D)) : 0.f;
-        const int cl = (j0 + c0 + i) / d.K;
-        float a = 0.f;
+    for (int i = 0; i < 16; ++i) dv[i] = dnx[i];
+    load_d(c0 + 16, dnx);
+    const uint32_t mk = (mask[c0 >> 5] >> (c0 & 31)) & 0xFFFFu;
+    acc_load16(tacc, ew, c0, nacc, tc.slot, tot);
+    double dot[16];
 #pragma unroll
-        for (int c = 0; c < CC; ++c) a = (c == cl) ? aC[c] : a;
-        al[i] = a;
-      }
-      if (tr && c0 < 128) tr[90 + (c0 >> 4) * 3] = globaltimer();
-      acc_load16(tmem, ew, c0, nacc, tc.slot, tot);
-      if (tr && c0 < 128) tr[91 + (c0 >> 4) * 3] = globaltimer();
-      double dot[16];
+    for (int i = 0; i < 16; ++i) {
+      const int cl = (j0 + c0 + i) / d.K;
+      float a = 0.f;
 #pragma unroll
-      for (int i = 0; i < 16; ++i) {
-        const float w = fmaf(betaf, tot[i], al[i] * dv[i]);
-        if (((mk >> i) & 1u) && rv) stv(p.b.W + colbase + (size_t)(c0 + i) * D, w);
-        dot[i] = (double)dv[i] * (double)w;
-      }
-      int idx;
-      const double sum = warp_reduce16(dot, lane, &idx);
-      if ((lane & 1) == 0) tl.red[ew][c0 + idx] = sum;
-      if (tr && c0 < 128) tr[92 + (c0 >> 4) * 3] = globaltimer();
+      for (int c = 0; c < CC; ++c) a = (c == cl) ? aC[c] : a;
+      const float w = fmaf(betaf, tot[i], a * dv[i]);
+      if (((mk >> i) & 1u) && rv) stv(p.b.W + colbase + (size_t)(c0 + i) * D, w);
+      dot[i] = (double)dv[i] * (double)w;
     }
-    fence_before_sync();
-    __syncwarp();
+    int idx;
+    const double sum = warp_reduce16(dot, lane, &idx);
+    if ((lane & 1) == 0) tl.red[ew][c0 + idx] = sum;
+  }
+  fence_before_sync();
+  __syncwarp();
+  {
+    const int bi = acc_buf(rc, dbl);
     if (lane == 0) {
-      mbar_arrive(&tl.tempty);
+      mbar_arrive(&tl.tempty[bi]);
       if (dts) mbar_arrive(&tl.dempty);
     }
+    rc.tuse[bi]++;
     rc.ti++;
-    if (tr) tr[81] = globaltimer();
   }
+  if (tr) tr[81] = globaltimer();
   epi_sync();
-  if (x.nmma)
-    for (int c = et; c < x.ncol; c += 128)
-      if ((mask[c >> 5] >> (c & 31)) & 1u)
-        stv(p.b.dAd + ((size_t)x.t * P + j0 + c) * d.nRT2 + x.rt,
-               tl.red[0][c] + tl.red[1][c] + tl.red[2][c] + tl.red[3][c]);
-  if (x.mean && et < C) {
-    const int jj = TC_NTMAX + et;
-    stv(p.b.dAdm + ((size_t)x.t * C + et) * d.nRT2 + x.rt, tl.red[0][jj] + tl.red[1][jj] + tl.red[2][jj] + tl.red[3][jj]);
-  }
+  for (int c = et; c < x.ncol; c += 128)
+    if ((mask[c >> 5] >> (c & 31)) & 1u)
+      stv(p.b.dAd + ((size_t)x.t * P + j0 + c) * d.nRT2 + x.rt,
+          tl.red[0][c] + tl.red[1][c] + tl.red[2][c] + tl.red[3][c]);
   epi_sync();                                 // tl.red is reused by the next unit
   if (tr) tr[82] = globaltimer();
 }
@@ -932,12 +1044,15 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_cg_persistent(KParams p, const 
   if (tid == 0) {
     for (int s = 0; s < tc.stages; ++s) {
       mbar_init(&tl.full[s], 1);
-      mbar_init(&tl.conv[s], 4);
+      mbar_init(&tl.conv[s], 2);
+      mbar_init(&tl.convm[s], 2);
       mbar_init(&tl.empty[s], 1);
       mbar_init(&tl.mdone[s], 4);
     }
-    mbar_init(&tl.tfull, 1);
-    mbar_init(&tl.tempty, 4);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tl.tfull[i], 1);
+      mbar_init(&tl.tempty[i], 4);
+    }
     mbar_init(&tl.dfull, 1);
     mbar_init(&tl.dempty, 4);
     fence_mbar_init();
@@ -951,13 +1066,14 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_cg_persistent(KParams p, const 
   __syncthreads();
   fence_after_sync();
   const uint32_t tmem = tl.tslot;
-  RingCtl rc{tc.stages, 0u, 0u, 0u};
+  RingCtl rc{tc.stages, 0u, 0, 0u, 0u, {0u, 0u}, 0u, 0u, {0u, 0u, 0u, 0u}};
   unsigned epoch = 0;
   unsigned *bar = p.b.gridbar;
   const int n1 = d.Tl * d.nCT * d.nRT1 * d.S1, n2 = d.Tl * d.nCT * d.nRT2;
   const int ncols = d.Tl * (d.P + d.C);
-  const bool producer = warp == 0 && lane == 0, issuer = warp == 1 && lane == 0, epi = warp >= 4;
-  const bool tile_role = warp == 0 || warp == 1 || epi;
+  const bool producer = warp == 0 && lane == 0, issuer = warp == 1 && lane == 0;
+  const bool conv = warp == 2 || warp == 3, meanw = warp >= 4 && warp < 8, epi = warp >= 8;
+  const bool tile_role = true;
   for (int u = 0; u < d.cap; ++u) {
     if (b == 0 && tid == 0) p.b.ts[4 * u + 0] = globaltimer();
     // diagnostic trace of CTA 0's first unit of each phase at CG step 5 (CMTCS_PHASE_LOG)
@@ -972,7 +1088,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_cg_persistent(KParams p, const 
         if (!x.nmma && !x.mean) continue;
         if (producer) produce(p, mp, sm, tl, rc, x, tr1);
         else if (issuer) mma_unit(p, sm, tl, rc, tmem, x, tr1);
-        else if (epi) epilogue_unit<CC>(p, sm, tl, rc, tmem, x, mask, tr1);
+        else if (conv) convert_unit(p, sm, tl, rc, x);
+        else if (meanw) mean_unit<CC>(p, sm, tl, rc, x);
+        else if (epi) probe_epilogue<CC>(p, sm, tl, rc, tmem, x, mask, tr1);
       }
     }
     grid_sync(bar, epoch);
@@ -986,7 +1104,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_cg_persistent(KParams p, const 
         if (!x.nmma && !x.mean) continue;
         if (producer) produce(p, mp, sm, tl, rc, x, tr2);
         else if (issuer) mma_unit(p, sm, tl, rc, tmem, x, tr2);
-        else if (epi) epilogue_unit<CC>(p, sm, tl, rc, tmem, x, mask, tr2);
+        else if (conv) convert_unit(p, sm, tl, rc, x);
+        else if (meanw) mean_unit<CC>(p, sm, tl, rc, x);
+        else if (epi) probe_epilogue<CC>(p, sm, tl, rc, tmem, x, mask, tr2);
       }
     }
     grid_sync(bar, epoch);
