@@ -203,14 +203,15 @@ def reference_arm(args):
 # CUDA arm
 # --------------------------------------------------------------------------------------------
 def ncu_traffic(cfg_name):
-    """dram bytes per operator launch pair from the committed ncu --set full summary, if any."""
+    """DRAM bytes (read + write) of the persistent CG kernel per CG step, from the committed
+    ncu --set full capture (profiles/ncu_summary.json), if any: the same unit as `achieved`."""
     p = os.path.join(ROOT, "profiles", "ncu_summary.json")
     if not os.path.exists(p):
         return None
     try:
         with open(p) as f:
             j = json.load(f)
-        return j.get("traffic_bytes_per_launch", {}).get(cfg_name)
+        return j.get("traffic_bytes_per_cg_step", {}).get(cfg_name)
     except Exception:
         return None
 
@@ -370,6 +371,7 @@ def cuda_arm(args):
             },
             "roofline": {"bound": "tensor", "achieved": achieved_op, "peak": peak, "unit": "TFLOP/s",
                          "frac": achieved_op / peak, "traffic": ncu_traffic(cfg.name),
+                         "traffic_unit": "DRAM bytes per CG step (ncu --set full of k_cg_persistent / its CG steps)",
                          "kernel": "K1 operator = phases 1-2 of the persistent CG kernel k_cg_persistent (tcgen05 3xTF32), "
                                    "achieved = algorithmic fp32 flop 4*N*D per active column per CG step / the "
                                    "device-stamped (%globaltimer, grid-barrier to grid-barrier) duration of those phases",
