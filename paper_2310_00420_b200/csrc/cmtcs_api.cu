@@ -450,7 +450,7 @@ cmtcs_status cmtcs_init(cmtcs_ctx **out, const cmtcs_problem *p, const float *ph
   c->kp.d = d;
   c->kp.b = b;
   c->kp.tc = make_tc(d);
-  c->kp.tc.pf = getenv("CMTCS_PF") ? atoi(getenv("CMTCS_PF")) : 6;
+  c->kp.tc.pf = getenv("CMTCS_PF") ? atoi(getenv("CMTCS_PF")) : 0;
   c->kp.phi = phi;
   c->kp.y = y;
   c->kp.beta = p->beta;

@@ -521,15 +521,33 @@ __device__ void update_mean(const KParams &p, int t, int c, int u, int lane) {
 }
 
 // ---- unit geometry ---------------------------------------------------------------------------
+// Shared Φ: the units of a phase form one large GEMM (rows of Φ/Φᵀ × all tasks' columns).  Units
+// are rasterised in bands of RB row tiles: inside a band the row tile varies fastest, then the
+// column tile, then the task, so a wave of ~148 concurrent units reads RB row tiles of Φ and
+// ~148 / RB column tiles of the tasks' operands at each K step (L2 reuse of both operands).
+constexpr int RB = 8;
+__device__ __forceinline__ void decode_banded(int w, int Tl, int nCT, int nRT, int *t, int *ct, int *rt) {
+  const int full = nRT / RB;                       // complete bands
+  const int per_band = Tl * nCT * RB;
+  int band = w / per_band, rb = RB;
+  int r = w - band * per_band;
+  if (band >= full) {                              // the last, partial band
+    band = full;
+    rb = nRT - full * RB;
+    r = w - full * per_band;
+  }
+  *rt = band * RB + r % rb;
+  r /= rb;
+  *ct = r % nCT;
+  *t = r / nCT;
+}
+
 __device__ __forceinline__ Unit make_unit1(const Dims &d, const TcCfg &tc, int w) {
   Unit x;
   x.stage = 1;
-  if (d.shared_phi) {     // task fastest: concurrent units share the Φ tile in L2
-    x.t = w % d.Tl;
-    int r = w / d.Tl;
-    x.sp = r % d.S1; r /= d.S1;
-    x.rt = r % d.nRT1;
-    x.ct = r / d.nRT1;
+  if (d.shared_phi) {
+    x.sp = w % d.S1;
+    decode_banded(w / d.S1, d.Tl, d.nCT, d.nRT1, &x.t, &x.ct, &x.rt);
   } else {
     x.sp = w % d.S1;
     int r = w / d.S1;
@@ -551,10 +569,7 @@ __device__ __forceinline__ Unit make_unit2(const Dims &d, const TcCfg &tc, int w
   x.stage = 2;
   x.sp = 0;
   if (d.shared_phi) {
-    x.t = w % d.Tl;
-    const int r = w / d.Tl;
-    x.rt = r % d.nRT2;
-    x.ct = r / d.nRT2;
+    decode_banded(w, d.Tl, d.nCT, d.nRT2, &x.t, &x.ct, &x.rt);
   } else {
     x.rt = w % d.nRT2;
     const int r = w / d.nRT2;
@@ -974,32 +989,21 @@ __device__ void probe_epilogue(const KParams &p, unsigned char *sm, PSmemTail &t
     mbar_wait(&tl.dfull, rc.di & 1);
     rc.di++;
   }
-  // d of the next 16-column group is loaded while the current one is processed (global loads when
-  // the d tile does not fit in shared memory)
-  float dnx[16];
-  auto load_d = [&](int c0, float *dst) {
-    const uint32_t mk = c0 < x.nmma ? (mask[c0 >> 5] >> (c0 & 31)) & 0xFFFFu : 0u;
-#pragma unroll
-    for (int i = 0; i < 16; ++i) {
-      const bool ok = ((mk >> i) & 1u) && rv;
-      dst[i] = ok ? (dts ? dtile[(c0 + i) * TM + r] : ldv(p.b.D32 + colbase + (size_t)(c0 + i) * D)) : 0.f;
-    }
-  };
-  load_d(0, dnx);
-  for (int c0 = 0; c0 < x.nmma; c0 += 16) {
-    float dv[16], tot[16];
-#pragma unroll
-    for (int i = 0; i < 16; ++i) dv[i] = dnx[i];
-    load_d(c0 + 16, dnx);
+  if (tr) tr[86] = globaltimer();
+  // per 16-column group: W = β·acc + α_c ⊙ d, dot partials; the cluster of column j0 + c0 + i is
+  // tracked incrementally (no integer division per column)
+  auto group = [&](int c0, const float *dv) {
     const uint32_t mk = (mask[c0 >> 5] >> (c0 & 31)) & 0xFFFFu;
+    float tot[16];
     acc_load16(tacc, ew, c0, nacc, tc.slot, tot);
+    int cl = (j0 + c0) / d.K, rem = (j0 + c0) - cl * d.K;
     double dot[16];
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
-      const int cl = (j0 + c0 + i) / d.K;
       float a = 0.f;
 #pragma unroll
       for (int c = 0; c < CC; ++c) a = (c == cl) ? aC[c] : a;
+      if (++rem == d.K) { rem = 0; ++cl; }
       const float w = fmaf(betaf, tot[i], a * dv[i]);
       if (((mk >> i) & 1u) && rv) stv(p.b.W + colbase + (size_t)(c0 + i) * D, w);
       dot[i] = (double)dv[i] * (double)w;
@@ -1007,6 +1011,31 @@ __device__ void probe_epilogue(const KParams &p, unsigned char *sm, PSmemTail &t
     int idx;
     const double sum = warp_reduce16(dot, lane, &idx);
     if ((lane & 1) == 0) tl.red[ew][c0 + idx] = sum;
+  };
+  if (dts) {
+    for (int c0 = 0; c0 < x.nmma; c0 += 16) {
+      float dv[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) dv[i] = rv ? dtile[(c0 + i) * TM + r] : 0.f;
+      group(c0, dv);
+    }
+  } else {
+    // global loads of d: the next group's are issued while the current one is processed
+    float dnx[16];
+    auto load_d = [&](int c0, float *dst) {
+      const uint32_t mk = c0 < x.nmma ? (mask[c0 >> 5] >> (c0 & 31)) & 0xFFFFu : 0u;
+#pragma unroll
+      for (int i = 0; i < 16; ++i)
+        dst[i] = (((mk >> i) & 1u) && rv) ? ldv(p.b.D32 + colbase + (size_t)(c0 + i) * D) : 0.f;
+    };
+    load_d(0, dnx);
+    for (int c0 = 0; c0 < x.nmma; c0 += 16) {
+      float dv[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) dv[i] = dnx[i];
+      load_d(c0 + 16, dnx);
+      group(c0, dv);
+    }
   }
   fence_before_sync();
   __syncwarp();
