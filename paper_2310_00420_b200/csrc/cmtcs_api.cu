@@ -97,19 +97,24 @@ TcCfg make_tc(const Dims &d) {
   tc.NT = std::min(nt_max(d.shared_phi), (d.P + 15) / 16 * 16);
   tc.slot = (tc.NT + 31) / 32 * 32;
   tc.nacc = std::max(1, std::min(4, 512 / (2 * tc.slot)));
-  tc.stage_bytes = 2u * 128u * 128u + 2u * (unsigned)tc.NT * 128u + 4096u;  // + fp64 mean-column chunk
-  // one CTA per SM (512 TMEM columns): ring (+ the stage-2 epilogue's d tile when ≥ 3 stages still fit)
-  // within ≤ 212 KB of the 227 KB of shared memory
+  // ring stage: A hi/lo (2 × 16 KB), B hi/lo (2 × NT × 128 B), fp64 mean-column chunk (≤ 32 × Cp × 8 B)
+  const unsigned mean_bytes = (256u * (unsigned)d.Cp + 1023u) & ~1023u;
+  tc.stage_bytes = 2u * 128u * 128u + 2u * (unsigned)tc.NT * 128u + mean_bytes;
+  // one CTA per SM (512 TMEM columns) within ≤ 212 KB of the 227 KB of shared memory: the stage-2
+  // epilogue's d tile (NT × 128 fp32) when ≥ 3 ring stages still fit (measured at C3: a 4th stage
+  // instead of the d tile does not help, the K loop is bound by shared-memory traffic)
   const unsigned budget = 212u * 1024u;
-  tc.dtile_bytes = (unsigned)tc.NT * 128u * 4u;
-  const int st_with = (int)((budget - std::min(budget, tc.dtile_bytes)) / tc.stage_bytes);
+  const unsigned dtile = (unsigned)tc.NT * 128u * 4u;
+  const int st_with = (int)((budget - std::min(budget, dtile)) / tc.stage_bytes);
+  const int st_without = std::min(4, (int)(budget / tc.stage_bytes));
   if (st_with >= 3) {
     tc.use_dtile = 1;
+    tc.dtile_bytes = dtile;
     tc.stages = std::min(4, st_with);
   } else {
     tc.use_dtile = 0;
     tc.dtile_bytes = 0;
-    tc.stages = std::max(2, std::min(4, (int)(budget / tc.stage_bytes)));
+    tc.stages = std::max(2, st_without);
   }
   return tc;
 }
