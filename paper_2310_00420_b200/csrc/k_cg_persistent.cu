@@ -360,8 +360,10 @@ __device__ void report(int *status, int code, int t, int col, int u) {
 __device__ void update_probe(const KParams &p, int t, int col, int u, int lane) {
   const Dims &d = p.d;
   const size_t g = (size_t)t * d.P + col;
-  double dAd = 0.0;
-  for (int i = 0; i < d.nRT2; ++i) dAd += ldv(p.b.dAd + g * d.nRT2 + i);
+  // the per-row-tile partials of dᵀAd: one load per lane, then the warp's fixed-order butterfly
+  double dpart = 0.0;
+  for (int i = lane; i < d.nRT2; i += 32) dpart += ldv(p.b.dAd + g * d.nRT2 + i);
+  const double dAd = warp_sum(dpart);
   const double rr = ldv(p.b.rr + g);
   if (!(dAd > 0.0)) {  // Alg. 1 line 3 breakdown
     if (lane == 0) {
@@ -447,8 +449,9 @@ __device__ void update_probe(const KParams &p, int t, int col, int u, int lane) 
 __device__ void update_mean(const KParams &p, int t, int c, int u, int lane) {
   const Dims &d = p.d;
   const size_t g = (size_t)t * d.C + c;
-  double dAd = 0.0;
-  for (int i = 0; i < d.nRT2; ++i) dAd += ldv(p.b.dAdm + g * d.nRT2 + i);
+  double dpart = 0.0;
+  for (int i = lane; i < d.nRT2; i += 32) dpart += ldv(p.b.dAdm + g * d.nRT2 + i);
+  const double dAd = warp_sum(dpart);
   const double rr = ldv(p.b.rrm + g);
   if (!(dAd > 0.0)) {
     if (lane == 0) {
@@ -980,9 +983,6 @@ __device__ void probe_epilogue(const KParams &p, unsigned char *sm, PSmemTail &t
   const bool rv = dd < D;
   const float betaf = (float)p.beta;
   const size_t colbase = ((size_t)x.t * P + j0) * D + dd;
-  float aC[CC];                               // α_c at this row for the clusters of the tile's columns
-#pragma unroll
-  for (int c = 0; c < CC; ++c) aC[c] = (c < C && rv) ? p.b.alpha32[(size_t)c * D + dd] : 0.f;
   const bool dts = tc.use_dtile;
   const float *dtile = reinterpret_cast<const float *>(sm + (size_t)rc.S * tc.stage_bytes);
   if (dts) {
@@ -992,25 +992,38 @@ __device__ void probe_epilogue(const KParams &p, unsigned char *sm, PSmemTail &t
   if (tr) tr[86] = globaltimer();
   // per 16-column group: W = β·acc + α_c ⊙ d, dot partials; the cluster of column j0 + c0 + i is
   // tracked incrementally (no integer division per column)
-  auto group = [&](int c0, const float *dv) {
+  const float *__restrict__ arow = p.b.alpha32 + dd;
+  float *__restrict__ Wc = p.b.W + colbase;
+  auto group_tot = [&](int c0, const float *dv, const float *tot) {
+    // independent steps over the 16 columns (one epilogue warp per scheduler: ILP, not TLP, hides
+    // latency): α loads, W, stores, exact fp64 products, then the butterfly reduction
     const uint32_t mk = (mask[c0 >> 5] >> (c0 & 31)) & 0xFFFFu;
-    float tot[16];
-    acc_load16(tacc, ew, c0, nacc, tc.slot, tot);
     int cl = (j0 + c0) / d.K, rem = (j0 + c0) - cl * d.K;
-    double dot[16];
+    float a[16], w[16];
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
-      float a = 0.f;
-#pragma unroll
-      for (int c = 0; c < CC; ++c) a = (c == cl) ? aC[c] : a;
+      // α_c at this row (read-only during the E-step: the non-coherent path, mostly L1 hits)
+      a[i] = rv ? __ldg(arow + (size_t)min(cl, C - 1) * D) : 0.f;
       if (++rem == d.K) { rem = 0; ++cl; }
-      const float w = fmaf(betaf, tot[i], a * dv[i]);
-      if (((mk >> i) & 1u) && rv) stv(p.b.W + colbase + (size_t)(c0 + i) * D, w);
-      dot[i] = (double)dv[i] * (double)w;
     }
+#pragma unroll
+    for (int i = 0; i < 16; ++i) w[i] = fmaf(betaf, tot[i], a[i] * dv[i]);
+    if (rv) {
+#pragma unroll
+      for (int i = 0; i < 16; ++i)
+        if ((mk >> i) & 1u) Wc[(size_t)(c0 + i) * D] = w[i];
+    }
+    double dot[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) dot[i] = (double)dv[i] * (double)w[i];
     int idx;
     const double sum = warp_reduce16(dot, lane, &idx);
     if ((lane & 1) == 0) tl.red[ew][c0 + idx] = sum;
+  };
+  auto group = [&](int c0, const float *dv) {
+    float tot[16];
+    acc_load16(tacc, ew, c0, nacc, tc.slot, tot);
+    group_tot(c0, dv, tot);
   };
   if (dts) {
     for (int c0 = 0; c0 < x.nmma; c0 += 16) {
