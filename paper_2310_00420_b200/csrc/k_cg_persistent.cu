@@ -373,10 +373,10 @@ __device__ void update_probe(const KParams &p, int t, int col, int u, int lane) 
     return;
   }
   const double gam = rr / dAd;
-  float4 *x4 = reinterpret_cast<float4 *>(p.b.X + g * d.D);
-  float4 *r4 = reinterpret_cast<float4 *>(p.b.R + g * d.D);
-  float4 *d4 = reinterpret_cast<float4 *>(p.b.D32 + g * d.D);
-  const float4 *w4 = reinterpret_cast<const float4 *>(p.b.W + g * d.D);
+  float4 *__restrict__ x4 = reinterpret_cast<float4 *>(p.b.X + g * d.D);
+  float4 *__restrict__ r4 = reinterpret_cast<float4 *>(p.b.R + g * d.D);
+  float4 *__restrict__ d4 = reinterpret_cast<float4 *>(p.b.D32 + g * d.D);
+  const float4 *__restrict__ w4 = reinterpret_cast<const float4 *>(p.b.W + g * d.D);
   const int n4 = d.D >> 2;
   double acc = 0.0;
   constexpr int U = 2;   // float4 per lane in flight (per array)

@@ -317,11 +317,32 @@ def test_full_run_config1(torch_cuda):
     capfree = np.array([i["n_cap_hit"] == 0 and c == 0 for i, c in zip(infos, caps_orc)])
     print("L gaps", gaps, "cap-free iterations", capfree, "nmse", nm_gpu, orc["nmse"])
     # At config 1's cap (64 = D) fp32 probe CG needs more steps than fp64 (finite-precision delay,
-    # SURVEY.md §0.2 / DESIGN.md §6), so cap-limited iterations are reported, not asserted here;
-    # tests/test_gpu_fp64.py asserts every iteration with fp64 probe columns.
+    # SURVEY.md §0.2 / DESIGN.md §6), so cap-limited iterations are reported, not asserted here.
     # L is compared step by step from identical states in the single-step tests; across a run the
     # states drift apart after cap-limited iterations, so here it is reported only.
     assert capfree.sum() >= 5
+
+
+def test_full_run_config2(torch_cuda):
+    """The bench configuration's whole run (config 2, 30 EM iterations from alpha0 = 1): identical
+    argmax assignments and |ΔNMSE| ≤ 1e-3 (north_star) against the fp64 oracle's run, stored by
+    tests/golden/make_c2_full_run.py (oracle only); |ΔL| per iteration reported."""
+    import json
+    import os
+    with open(os.path.join(os.path.dirname(__file__), "golden", "c2_full_run.json")) as f:
+        gold = json.load(f)
+    cfg = synthetic.CONFIGS[2]
+    data = synthetic.generate(cfg)
+    g = make_gpu(data)
+    infos = [g.em_step(1) for _ in range(cfg.em_iters)]
+    post = to_np(g.posterior())
+    g.close()
+    nm_gpu = O.nmse(post["recon"], data["z"])
+    gaps = np.abs(np.array([i["loglik"] for i in infos]) - np.array(gold["L"]))
+    print("C2 full run: assign", list(post["assign"]), "oracle", gold["assign"], "nmse", nm_gpu, gold["nmse"],
+          "max |dL|", gaps.max(), "GPU cap hits", [i["n_cap_hit"] for i in infos])
+    assert list(post["assign"]) == gold["assign"]
+    assert abs(nm_gpu - gold["nmse"]) <= 1e-3
 
 
 def test_single_step_config2(torch_cuda):
