@@ -96,7 +96,7 @@ TcCfg make_tc(const Dims &d) {
   TcCfg tc;
   tc.NT = std::min(nt_max(d.shared_phi), (d.P + 15) / 16 * 16);
   tc.slot = (tc.NT + 31) / 32 * 32;
-  tc.nacc = std::max(1, std::min(4, 512 / (2 * tc.slot)));
+  tc.nacc = std::max(1, std::min(4, 512 / tc.slot - 1));   // main accumulators besides the cross one
   // ring stage: A hi/lo (2 × 16 KB), B hi/lo (2 × NT × 128 B), fp64 mean-column chunk (≤ 32 × Cp × 8 B)
   const unsigned mean_bytes = (256u * (unsigned)d.Cp + 1023u) & ~1023u;
   tc.stage_bytes = 2u * 128u * 128u + 2u * (unsigned)tc.NT * 128u + mean_bytes;
@@ -155,15 +155,16 @@ bool make_dims(const cmtcs_problem *p, Dims *d, char *why) {
   d->nCT = (d->P + NT - 1) / NT;
   {
     // split the stage-1 contraction over D (S1 ∈ {1, 2, 4, 8}, every split ≥ 128 of D) so that the
-    // stage-1 units fill the persistent grid (148 CTAs on a B200): minimise rounds × chunks per
-    // unit.  S1 > 1 only when all stage-1 units fit in one round: the split CTAs of a tile wait for
-    // one another to reduce their partial tiles (k_cg_persistent.cu).
+    // stage-1 units fill and balance the persistent grid (148 CTAs on a B200): minimise rounds ×
+    // (chunks per unit + a fixed per-unit cost).  The split partial tiles are reduced cooperatively
+    // when all stage-1 units fit in one round, else by the last-arriving split CTA
+    // (k_cg_persistent.cu).
     const int sms = 148;
     const long base = (long)d->nCT * d->nRT1 * (p->task_end - p->task_begin);
     int best = 1;
     long best_cost = -1;
     for (int s1 = 1; s1 <= 8; s1 *= 2) {
-      if (s1 > 1 && (p->D / s1 < 128 || base * s1 > sms)) break;
+      if (s1 > 1 && p->D / s1 < 128) break;
       const long rounds = (base * s1 + sms - 1) / sms;
       const long chunks = ((p->D + s1 - 1) / s1 + 31) / 32;
       const long cost = rounds * (chunks + 4);   // + fixed per-unit cost (prologue, epilogue, reduction)
@@ -173,6 +174,7 @@ bool make_dims(const cmtcs_problem *p, Dims *d, char *why) {
     k1 = (k1 + 31) / 32 * 32;   // whole 32-wide K stages of the tensor-core pipeline
     d->K1 = k1;
     d->S1 = (p->D + k1 - 1) / k1;
+    d->split_coop = d->S1 > 1 && base * d->S1 <= sms;
     if (d->S1 < 1 || d->S1 > 8) { snprintf(why, 256, "internal: bad split of D=%d", p->D); return false; }
   }
   d->shared_phi = p->shared_phi ? 1 : 0;
@@ -481,8 +483,8 @@ cmtcs_status cmtcs_init(cmtcs_ctx **out, const cmtcs_problem *p, const float *ph
   c->grid = cg_grid_size(c->kp);
   if (c->grid < 1) return fail(c, CMTCS_ECUDA, "persistent CG kernel cannot be made resident (smem %zu bytes)",
                                tc_smem_bytes(c->kp.tc, d.P));
-  if (d.S1 > 1 && (long)d.Tl * d.nCT * d.nRT1 * d.S1 > c->grid)
-    return fail(c, CMTCS_ECUDA, "split-K stage 1 needs all %d units co-resident but the grid has %d CTAs",
+  if (d.split_coop && (long)d.Tl * d.nCT * d.nRT1 * d.S1 > c->grid)
+    return fail(c, CMTCS_ECUDA, "cooperative split-K needs all %d stage-1 units co-resident but the grid has %d CTAs",
                 d.Tl * d.nCT * d.nRT1 * d.S1, c->grid);
   // π: log π_c on device
   double *pi_dev = b.red;  // scratch: red is rewritten every M-step

@@ -29,6 +29,7 @@ struct Dims {
   int nCT;   // probe column tiles = ceil(P / TcCfg::NT)
   int S1;    // stage-1 split-K factor (balances the persistent grid when T·N is small)
   int K1;    // stage-1 contraction length per split (multiple of OP_BK)
+  int split_coop;  // S1 > 1 with every stage-1 unit co-resident: split CTAs reduce cooperatively
   int shared_phi;
   int64_t phi_task_stride;  // elements between Φ_t and Φ_{t+1} (0 if shared)
 };
@@ -84,7 +85,7 @@ struct Bufs {
 struct TcCfg {
   int NT;            // column tile width (multiple of 16, ≤ 256)
   int slot;          // TMEM columns per accumulator (NT rounded up to 32)
-  int nacc;          // K-split accumulator pairs (2·nacc·slot ≤ 512)
+  int nacc;          // K-split main accumulators ((1 + nacc)·slot ≤ 512 TMEM columns)
   int stages;        // smem pipeline depth
   unsigned stage_bytes;
   int pf;            // L2 prefetch distance of the producer (chunks ahead; 0 = off)

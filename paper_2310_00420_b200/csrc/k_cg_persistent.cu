@@ -35,7 +35,7 @@
 //
 // 3xTF32: every operand x is the exact pair x = hi + lo with hi = tf32(x), and each K = 8 step issues
 //   acc_x += lo_A·hi_B + hi_A·lo_B ;  acc_m += hi_A·hi_B
-// into separate TMEM accumulators, themselves split over K into `nacc` pairs and summed in fp32 in
+// into separate TMEM accumulators, the main one split over K into up to 4 and summed in fp32 in
 // the epilogue (the tensor pipe's accumulation otherwise loses ~4 bits over long K;
 // tools/tc_gemm_test.cu measures 3.2e-5 → 5e-6 relative at K = 4096; fp32 serial FFMA: 2e-6).
 //
@@ -72,6 +72,7 @@ struct PSmemTail {
   uint64_t tfull[2], tempty[2];      // TMEM accumulator buffers: MMA done / epilogue drained
   uint64_t dfull, dempty;             // the stage-2 epilogue's d tile (TMA bytes / epilogue done)
   uint32_t tslot;
+  int last;                           // split-K: this CTA reduces the tile (last-arriver mode)
   uint32_t emask[4][TC_NTMAX / 32];   // per epilogue warp: active-column mask of its current tile
   double red[4][TC_NTMAX];            // per epilogue warp: dᵀAd partials of the probe columns
   double redm[4][MAXC];               // per mean warp: dᵀAd partials of the mean columns
@@ -154,34 +155,33 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
-// K-split accumulator pairs of a tile: one for short contractions (K ≤ 512), else up to tc.nacc
-// Double-buffered accumulators (two 256-column TMEM buffers, one accumulator pair each) for tiles of
-// up to 128 columns and K ≤ 2048; longer contractions keep K-split pairs in one 512-column buffer.
+// TMEM accumulators of a tile: the cross terms (lo·hi + hi·lo, ~2^-11 of the product) in one
+// accumulator at column 0, the main terms (hi·hi) split over K into `nacc` accumulators at columns
+// (1 + q)·slot, summed in fp32 in the epilogue (the tensor pipe's fp32 accumulation loses bits over
+// long K).  Short contractions (≤ 32 chunks, K ≤ 1024) use one main accumulator and two 256-column
+// buffers (double buffering: the MMA warp starts the next tile while the epilogue drains this one);
+// longer ones up to tc.nacc main accumulators in one 512-column buffer.
 __device__ __forceinline__ bool unit_dbl(const TcCfg &tc, int nk, int dbg) {
-  return tc.slot <= 128 && nk <= 64 && !(dbg & 16);
+  return 2 * tc.slot <= 256 && nk <= (dbg & 32 ? 64 : 32) && !(dbg & 16);
 }
 __device__ __forceinline__ int unit_nacc(const TcCfg &tc, int nk, int dbg) {
   if (unit_dbl(tc, nk, dbg)) return 1;
   return (nk <= 16 && !(dbg & 8)) ? 1 : min(tc.nacc, nk);
 }
 
-// TMEM accumulator column of pair q, term x (0 = main hi·hi, 1 = cross terms)
-__device__ __forceinline__ uint32_t acc_col(int q, int x, int slot) { return (uint32_t)((2 * q + x) * slot); }
-
-// issue the 3xTF32 MMAs of one K = 32 stage (one thread)
+// issue the 3xTF32 MMAs of one K = 32 stage (one thread) into main accumulator q
 __device__ __forceinline__ void mma_stage(uint32_t tmem, unsigned char *base, uint32_t b_bytes, uint32_t idesc,
-                                          int q, int slot, bool first_of_acc) {
+                                          int q, int slot, bool first_main, bool first_cross) {
   const uint64_t ah = desc_sw128(smem_u32(base)), al = desc_sw128(smem_u32(base + A_BYTES));
   const uint64_t bh = desc_sw128(smem_u32(base + 2 * A_BYTES));
   const uint64_t bl = desc_sw128(smem_u32(base + 2 * A_BYTES + b_bytes));
-  const uint32_t tm_m = tmem + acc_col(q, 0, slot), tm_x = tmem + acc_col(q, 1, slot);
+  const uint32_t tm_m = tmem + (uint32_t)((1 + q) * slot), tm_x = tmem;
 #pragma unroll
   for (int k8 = 0; k8 < TK / 8; ++k8) {
     const uint64_t o = (uint64_t)(k8 * 32) >> 4;  // +32 bytes per K = 8 step inside the swizzled row
-    const uint32_t acc = (first_of_acc && k8 == 0) ? 0u : 1u;
-    mma_tf32(tm_x, al + o, bh + o, idesc, acc);
+    mma_tf32(tm_x, al + o, bh + o, idesc, (first_cross && k8 == 0) ? 0u : 1u);
     mma_tf32(tm_x, ah + o, bl + o, idesc, 1u);
-    mma_tf32(tm_m, ah + o, bh + o, idesc, acc);
+    mma_tf32(tm_m, ah + o, bh + o, idesc, (first_main && k8 == 0) ? 0u : 1u);
   }
 }
 
@@ -196,36 +196,17 @@ __device__ __forceinline__ void tmem_ld16_nowait(uint32_t taddr, uint32_t *r) {
 }
 __device__ __forceinline__ void acc_load16(uint32_t tmem, int ew, int c0, int nacc, int slot, float *tot) {
   const uint32_t lane_base = tmem + ((uint32_t)(ew * 32) << 16) + c0;
-  uint32_t m0[16], x0[16];
-  tmem_ld16_nowait(lane_base + acc_col(0, 1, slot), x0);
-  tmem_ld16_nowait(lane_base + acc_col(0, 0, slot), m0);
-  if (nacc == 1) {
-    asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
-#pragma unroll
-    for (int i = 0; i < 16; ++i) tot[i] = __uint_as_float(x0[i]) + __uint_as_float(m0[i]);
-    return;
-  }
-  uint32_t m1[16], x1[16];
-  tmem_ld16_nowait(lane_base + acc_col(1, 1, slot), x1);
-  tmem_ld16_nowait(lane_base + acc_col(1, 0, slot), m1);
+  uint32_t x0[16], m0[16];
+  tmem_ld16_nowait(lane_base, x0);                          // cross terms
+  tmem_ld16_nowait(lane_base + (uint32_t)slot, m0);         // main terms, K part 0
   asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
 #pragma unroll
-  for (int i = 0; i < 16; ++i) tot[i] = __uint_as_float(x0[i]) + __uint_as_float(x1[i]);   // cross terms first
-  for (int q = 2; q < nacc; ++q) {
-    tmem_ld16_nowait(lane_base + acc_col(q, 1, slot), x1);
+  for (int i = 0; i < 16; ++i) tot[i] = __uint_as_float(x0[i]) + __uint_as_float(m0[i]);
+  for (int q = 1; q < nacc; ++q) {
+    tmem_ld16_nowait(lane_base + (uint32_t)((1 + q) * slot), m0);
     asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
 #pragma unroll
-    for (int i = 0; i < 16; ++i) tot[i] += __uint_as_float(x1[i]);
-  }
-#pragma unroll
-  for (int i = 0; i < 16; ++i) tot[i] += __uint_as_float(m0[i]);
-#pragma unroll
-  for (int i = 0; i < 16; ++i) tot[i] += __uint_as_float(m1[i]);
-  for (int q = 2; q < nacc; ++q) {
-    tmem_ld16_nowait(lane_base + acc_col(q, 0, slot), m1);
-    asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
-#pragma unroll
-    for (int i = 0; i < 16; ++i) tot[i] += __uint_as_float(m1[i]);
+    for (int i = 0; i < 16; ++i) tot[i] += __uint_as_float(m0[i]);
   }
 }
 
@@ -708,7 +689,7 @@ __device__ __forceinline__ void mma_unit(const KParams &p, unsigned char *sm, PS
       fence_after_sync();
       const int q = (kc * nacc) / x.nk;
       const int qfirst = (q * x.nk + nacc - 1) / nacc;
-      mma_stage(tacc, sm + (size_t)st * tc.stage_bytes, b_bytes, idesc, q, tc.slot, kc == qfirst);
+      mma_stage(tacc, sm + (size_t)st * tc.stage_bytes, b_bytes, idesc, q, tc.slot, kc == qfirst, kc == 0);
       mma_commit(&tl.empty[st]);
     } else {
       mbar_arrive(&tl.empty[st]);
@@ -749,31 +730,41 @@ __device__ __forceinline__ void convert_unit(const KParams &p, unsigned char *sm
 __device__ __forceinline__ void mean_sync() { asm volatile("bar.sync 1, 128;\n" ::: "memory"); }
 __device__ __forceinline__ void pair_sync() { asm volatile("bar.sync 3, 256;\n" ::: "memory"); }
 
-// Split-K handoff of a stage-1 tile (S1 > 1): every split CTA arrives on the tile counter and waits
-// until all S1 partials are written (the host picks S1 > 1 only when all stage-1 units are
-// co-resident).  Called by the mean and the epilogue warps together (256 threads).
-__device__ __forceinline__ void split_handoff(const KParams &p, const Unit &x) {
+// Split-K handoff of a stage-1 tile (S1 > 1), called by the mean and the epilogue warps together
+// (256 threads) once this CTA's partial tile is written; returns the rows [rb, re) of the tile
+// this CTA sums over the S1 partials, in split order (deterministic):
+//  * cooperative (all stage-1 units co-resident, small configs): every split CTA waits on the tile
+//    counter for all S1 partials and reduces its 1/S1 share of the rows;
+//  * last arriver (several units per CTA): the CTA that completes the tile's S1 arrivals of this
+//    step reduces the whole tile, the others move on.
+// The tile counters only grow (S1 arrivals per active tile and step, zeroed at init).
+__device__ __forceinline__ void split_handoff(const KParams &p, const Unit &x, PSmemTail &tl, int *rb, int *re) {
+  const Dims &d = p.d;
   __threadfence();
   pair_sync();
+  int *cnt = p.b.tilecnt + ((size_t)x.t * d.nCT + x.ct) * d.nRT1 + x.rt;
   if (threadIdx.x == EPI0) {
-    int *cnt = p.b.tilecnt + ((size_t)x.t * p.d.nCT + x.ct) * p.d.nRT1 + x.rt;
     const int ticket = atomicAdd(cnt, 1);
-    const int target = (ticket / p.d.S1 + 1) * p.d.S1;
-    int v;
-    do {
-      asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];\n" : "=r"(v) : "l"(cnt) : "memory");
-    } while (v < target);
+    if (d.split_coop) {
+      const int target = (ticket / d.S1 + 1) * d.S1;
+      int v;
+      do {
+        asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];\n" : "=r"(v) : "l"(cnt) : "memory");
+      } while (v < target);
+    }
+    tl.last = (ticket % d.S1) == d.S1 - 1;
     asm volatile("fence.acq_rel.gpu;\n" ::: "memory");
   }
   pair_sync();
-}
-
-// rows [rb, re) of a stage-1 tile summed over the S1 split partials (this split's share)
-__device__ __forceinline__ void split_share(const Dims &d, const Unit &x, int *rb, int *re) {
   const int n0 = x.rt * TM, rows = min(TM, d.N - n0);
-  const int rs = ((rows + d.S1 - 1) / d.S1 + 3) & ~3;       // rows per share (×4: float4 rows)
-  *rb = min(rows, x.sp * rs);
-  *re = min(rows, *rb + rs);
+  if (d.split_coop) {
+    const int rs = ((rows + d.S1 - 1) / d.S1 + 3) & ~3;     // rows per share (×4: float4 rows)
+    *rb = min(rows, x.sp * rs);
+    *re = min(rows, *rb + rs);
+  } else {
+    *rb = 0;
+    *re = tl.last ? rows : 0;
+  }
 }
 
 // ---- mean warps (4-7): fp64 mean columns on the FP64 tensor path --------------------------------
@@ -826,9 +817,8 @@ __device__ void mean_unit(const KParams &p, unsigned char *sm, PSmemTail &tl, Ri
       }
     }
     if (d.S1 > 1) {
-      split_handoff(p, x);
       int rb, re;
-      split_share(d, x, &rb, &re);
+      split_handoff(p, x, tl, &rb, &re);
       if (x.mean && re > rb) {
         const int n0 = x.rt * TM;
         const int nm = (re - rb) * d.Cp / 2;   // double2 elements of this share of Um
@@ -941,9 +931,8 @@ __device__ void probe_epilogue(const KParams &p, unsigned char *sm, PSmemTail &t
       if (tr) tr[81] = globaltimer();
     }
     if (d.S1 > 1) {
-      split_handoff(p, x);
       int rb, re;
-      split_share(d, x, &rb, &re);
+      split_handoff(p, x, tl, &rb, &re);
       if (x.nmma && re > rb) {
         const int n0 = x.rt * TM, r4n = (re - rb) >> 2;
         const size_t split = (size_t)d.Pp * N;
