@@ -148,6 +148,19 @@ def test_single_em_step_ragged_shapes(torch_cuda):
     assert np.all(np.abs(post["logdet"] - orc["nu"]) <= nu_tol(orc["nu"]))
 
 
+def test_single_em_step_multiround_split_k(torch_cuda):
+    """80 tasks with N = 256, D = 512: stage 1 splits K in two (S1 = 2) over 320 units, more than one
+    round of the 148-CTA grid, so the split partial tiles are reduced by the last-arriving CTA;
+    stage 2 has 320 units of 4 chunks each (double-buffered accumulators)."""
+    data = synthetic.small_problem(T=80, C=2, N=256, D=512, K=4, sigma=0.01, seed=13, support=20)
+    alpha = np.random.default_rng(5).uniform(0.5, 4.0, (2, 512))
+    post, info, orc, a_next, conv = _single_step(data, alpha, 2, cap=1024, tol=1e-7)
+    e = compare_step(post, info, orc, a_next, conv)
+    print("multiround split-K", e, "converged", conv.sum(), "/", conv.size)
+    assert e["mu"] <= MU_TOL and conv.any() and e["s_conv"] <= S_TOL and e["q_abs"] <= Q_TOL and e["L_abs"] <= L_TOL
+    assert np.all(np.abs(post["logdet"] - orc["nu"]) <= nu_tol(orc["nu"]))
+
+
 def test_single_em_step_many_column_tiles(torch_cuda):
     """P = C·K = 16·9 = 144 > two 64-column tiles, C = 16 (the maximum), 1 task per... ."""
     data = synthetic.small_problem(T=2, C=16, N=48, D=128, K=9, sigma=0.05, seed=12, support=5)
