@@ -196,12 +196,15 @@ size_t carve(const Dims &d, char *base, Bufs *b) {
   b->X = cv.take<float>(Tl * P * D);
   b->R = cv.take<float>(Tl * P * D);
   b->D32 = cv.take<float>(Tl * P * D);
+  b->Dh = cv.take<float>(Tl * P * D);
+  b->Dl = cv.take<float>(Tl * P * D);
   b->W = cv.take<float>(Tl * P * D);
   b->Xm = cv.take<double>(Tl * C * D);
   b->Rm = cv.take<double>(Tl * C * D);
   b->Dm = cv.take<double>(Tl * C * D);
   b->Wm = cv.take<double>(Tl * C * D);
-  b->U = cv.take<float>(Tl * d.Pp * N);
+  b->Uh = cv.take<float>(Tl * d.Pp * N);
+  b->Ul = cv.take<float>(Tl * d.Pp * N);
   b->Um = cv.take<double>(Tl * N * d.Cp);
   b->rr = cv.take<double>(Tl * P);
   b->rrm = cv.take<double>(Tl * C);

@@ -43,10 +43,11 @@ struct Bufs {
   double *b64;       // [Tl][D]   βΦᵀy
   double *bnorm2;    // [Tl]      ‖b‖²
   float *X, *R, *W;  // probe columns [Tl][P][D]; W = Ad
-  float *D32;        // probe directions d [Tl][P][D]
+  float *D32;        // probe directions d [Tl][P][D] (fp32: the epilogue's d tile, the update)
+  float *Dh, *Dl;    // the same as the exact tf32 pair d = Dh + Dl (stage-1 B operand) [Tl][P][D]
   float *PT;         // Φᵀ fp32 [Tl or 1][D][N] (stage-2 A operand; stage 1 reads the caller's Φ)
   double *Xm, *Rm, *Dm, *Wm; // mean columns  [Tl][C][D]
-  float *U;          // stage-1 output U = ΦD, [Tl][Pp][N] (row = column j)
+  float *Uh, *Ul;    // stage-1 output U = ΦD as the exact tf32 pair (stage-2 B operand), [Tl][Pp][N]
   double *Um;        // [Tl][N][Cp]
   double *rr;        // [Tl][P]
   double *rrm;       // [Tl][C]
@@ -97,8 +98,8 @@ struct TcCfg {
 struct TcMaps {
   CUtensorMap phi;             // fp32 Φ (the caller's) [rows Tl·N][cols D], box 32 × 128, SW128
   CUtensorMap phit;            // fp32 Φᵀ [rows Tl·D][cols N], box 32 × 128, SW128
-  CUtensorMap u;               // fp32 U = ΦD [rows Tl·Pp][cols N], box 32 × NT, SW128
-  CUtensorMap dir;             // fp32 directions [rows Tl·P][cols D], box 32 × NT, SW128
+  CUtensorMap u_h, u_l;        // U = ΦD split [rows Tl·Pp][cols N], box 32 × NT, SW128
+  CUtensorMap d_h, d_l;        // directions split [rows Tl·P][cols D], box 32 × NT, SW128
   CUtensorMap dm;              // fp64 [rows Tl·C][cols D], box 32 × C (mean directions)
   CUtensorMap um;              // fp64 [rows Tl·N][cols Cp], box Cp × 32 (Φ·d of the mean columns)
   CUtensorMap d32;             // fp32 [rows Tl·P][cols D], box 128 × NT (probe directions, epilogue)

@@ -28,10 +28,11 @@
 // epilogue of the previous one drains.  mbarriers: full[s] (TMA bytes), conv[s] (split done),
 // empty[s] (MMA done), mdone[s] (fp64 warps done), tfull / tempty (accumulator handshake).
 //
-// Operands live in HBM as plain fp32 (Φ itself, its transpose, the directions, U) and arrive by TMA;
-// the converter warps split each staged tile in shared memory into the exact pair x = hi + lo,
-// hi = tf32(x) (in place) and lo = x − hi (a second tile), so the operator reads every operand
-// byte once per use (mbarrier conv[s]: split done → the MMA warp may issue).
+// The A operands (Φ itself and its transpose) live in HBM as plain fp32 and arrive by TMA; the
+// converter warps split each staged tile in shared memory into the exact pair x = hi + lo,
+// hi = tf32(x) (in place) and lo = x − hi (a second tile), so Φ is read once per use (mbarrier
+// conv[s]: split done → the MMA warp may issue).  The B operands (directions, U — small next to Φ
+// and re-read by every row tile) are written by their producers as tf32 pairs and staged as such.
 //
 // 3xTF32: every operand x is the exact pair x = hi + lo with hi = tf32(x), and each K = 8 step issues
 //   acc_x += lo_A·hi_B + hi_A·lo_B ;  acc_m += hi_A·hi_B
@@ -357,6 +358,8 @@ __device__ void update_probe(const KParams &p, int t, int col, int u, int lane) 
   float4 *__restrict__ x4 = reinterpret_cast<float4 *>(p.b.X + g * d.D);
   float4 *__restrict__ r4 = reinterpret_cast<float4 *>(p.b.R + g * d.D);
   float4 *__restrict__ d4 = reinterpret_cast<float4 *>(p.b.D32 + g * d.D);
+  float4 *__restrict__ dh4 = reinterpret_cast<float4 *>(p.b.Dh + g * d.D);
+  float4 *__restrict__ dl4 = reinterpret_cast<float4 *>(p.b.Dl + g * d.D);
   const float4 *__restrict__ w4 = reinterpret_cast<const float4 *>(p.b.W + g * d.D);
   const int n4 = d.D >> 2;
   double acc = 0.0;
@@ -420,6 +423,10 @@ __device__ void update_probe(const KParams &p, int t, int col, int u, int lane) 
           dv.z = (float)fma(xi, (double)dv.z, (double)rv[v].z);
           dv.w = (float)fma(xi, (double)dv.w, (double)rv[v].w);
           stv(d4 + i, dv);
+          float4 h4;
+          h4.x = tf32_rna(dv.x); h4.y = tf32_rna(dv.y); h4.z = tf32_rna(dv.z); h4.w = tf32_rna(dv.w);
+          stv(dh4 + i, h4);
+          stv(dl4 + i, make_float4(dv.x - h4.x, dv.y - h4.y, dv.z - h4.z, dv.w - h4.w));
         }
       }
     }
@@ -601,7 +608,7 @@ __device__ __forceinline__ void produce(const KParams &p, const TcMaps &mp, unsi
   if (tr) tr[84] = globaltimer();
   const uint32_t b_bytes = (uint32_t)p.tc.NT * 128;
   const uint32_t mean_tx = x.stage == 1 ? (uint32_t)p.d.C * TK * 8 : (uint32_t)TK * p.d.Cp * 8;
-  const uint32_t bytes = A_BYTES + (x.nmma ? b_bytes : 0) + (x.mean ? mean_tx : 0);
+  const uint32_t bytes = A_BYTES + (x.nmma ? 2 * b_bytes : 0) + (x.mean ? mean_tx : 0);
   for (int kc = 0; kc < x.nk; ++kc) {
     const uint32_t G = rc.g;
     const int st = rc.st;
@@ -628,27 +635,33 @@ __device__ __forceinline__ void produce(const KParams &p, const TcMaps &mp, unsi
       const int kk = x.k0 + kp * TK;
       if (x.stage == 1) {
         tma_prefetch_2d(&mp.phi, kk, x.arow);
-        if (x.nmma) tma_prefetch_2d(&mp.dir, kk, x.brow);
+        if (x.nmma) tma_prefetch_2d(&mp.d_h, kk, x.brow);
       } else {
         tma_prefetch_2d(&mp.phit, kk, x.arow);
-        if (x.nmma) tma_prefetch_2d(&mp.u, kk, x.brow);
+        if (x.nmma) tma_prefetch_2d(&mp.u_h, kk, x.brow);
       }
     }
     if (kc == 0 && p.tc.pf) {                 // the first chunks of the unit
       for (int k2 = 1; k2 < min(p.tc.pf, x.nk); ++k2) {
         const int kk = x.k0 + k2 * TK;
         tma_prefetch_2d(x.stage == 1 ? &mp.phi : &mp.phit, kk, x.arow);
-        if (x.nmma) tma_prefetch_2d(x.stage == 1 ? &mp.dir : &mp.u, kk, x.brow);
+        if (x.nmma) tma_prefetch_2d(x.stage == 1 ? &mp.d_h : &mp.u_h, kk, x.brow);
       }
     }
     // fp32 tiles into the hi slots (split in place by the converter warps, lo into the lo slots)
     if (x.stage == 1) {
       tma_load_2d(base, &mp.phi, k, x.arow, fb);
-      if (x.nmma) tma_load_2d(base + 2 * A_BYTES, &mp.dir, k, x.brow, fb);
+      if (x.nmma) {
+        tma_load_2d(base + 2 * A_BYTES, &mp.d_h, k, x.brow, fb);
+        tma_load_2d(base + 2 * A_BYTES + b_bytes, &mp.d_l, k, x.brow, fb);
+      }
       if (x.mean) tma_load_2d(base + 2 * A_BYTES + 2 * b_bytes, &mp.dm, k, x.t * p.d.C, fb);
     } else {
       tma_load_2d(base, &mp.phit, k, x.arow, fb);
-      if (x.nmma) tma_load_2d(base + 2 * A_BYTES, &mp.u, k, x.brow, fb);
+      if (x.nmma) {
+        tma_load_2d(base + 2 * A_BYTES, &mp.u_h, k, x.brow, fb);
+        tma_load_2d(base + 2 * A_BYTES + b_bytes, &mp.u_l, k, x.brow, fb);
+      }
       if (x.mean) tma_load_2d(base + 2 * A_BYTES + 2 * b_bytes, &mp.um, 0, x.t * p.d.N + k, fb);
     }
     if (tr && kc < 16) tr[16 + kc] = globaltimer();
@@ -715,7 +728,7 @@ __device__ __forceinline__ void convert_unit(const KParams &p, unsigned char *sm
     const uint32_t base = smem_u32(sm) + (uint32_t)st * p.tc.stage_bytes;
     if (!(p.dbg_flags & 4)) {
       split_rows64(base, base + A_BYTES, ct, TM);                     // A: 128 rows
-      if (x.nmma) split_rows64(base + 2 * A_BYTES, base + 2 * A_BYTES + b_bytes, ct, x.nmma);   // B rows
+      // B (directions / U) arrives already split: stored as tf32 pairs by their producers
     }
     fence_proxy_async();                      // generic smem writes → tensor-core (async proxy) reads
     __syncwarp();
@@ -904,7 +917,7 @@ __device__ void probe_epilogue(const KParams &p, unsigned char *sm, PSmemTail &t
   }
   if (x.stage == 1) {
     const int n = x.rt * TM + r;
-    float *Ut = p.b.U + (size_t)x.t * d.Pp * N;
+    float *Uh = p.b.Uh + (size_t)x.t * d.Pp * N, *Ul = p.b.Ul + (size_t)x.t * d.Pp * N;
     float *part = p.b.Upart + ((size_t)x.t * d.S1 + x.sp) * d.Pp * N;
     if (x.nmma) {
       for (int c0 = 0; c0 < x.nmma; c0 += 16) {
@@ -916,8 +929,13 @@ __device__ void probe_epilogue(const KParams &p, unsigned char *sm, PSmemTail &t
             const int c = c0 + i;
             if (c < x.ncol) {
               const size_t o = (size_t)(j0 + c) * N + n;
-              if (d.S1 == 1) Ut[o] = tot[i];
-              else stv(part + o, tot[i]);
+              if (d.S1 == 1) {
+                const float h = tf32_rna(tot[i]);
+                Uh[o] = h;
+                Ul[o] = tot[i] - h;
+              } else {
+                stv(part + o, tot[i]);
+              }
             }
           }
         }
@@ -959,7 +977,13 @@ __device__ void probe_epilogue(const KParams &p, unsigned char *sm, PSmemTail &t
           }
 #pragma unroll
           for (int v = 0; v < V; ++v)
-            if (e0 + 128 * v < tot4) *reinterpret_cast<float4 *>(Ut + off[v]) = acc4[v];
+            if (e0 + 128 * v < tot4) {
+              float4 h;
+              h.x = tf32_rna(acc4[v].x); h.y = tf32_rna(acc4[v].y); h.z = tf32_rna(acc4[v].z); h.w = tf32_rna(acc4[v].w);
+              *reinterpret_cast<float4 *>(Uh + off[v]) = h;
+              *reinterpret_cast<float4 *>(Ul + off[v]) =
+                  make_float4(acc4[v].x - h.x, acc4[v].y - h.y, acc4[v].z - h.z, acc4[v].w - h.w);
+            }
         }
       }
     }
@@ -1089,7 +1113,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_cg_persistent(KParams p, const 
     fence_mbar_init();
   }
   if (warp == 0 && lane == 0) {
-    prefetch_tmap(&mp.phi); prefetch_tmap(&mp.phit); prefetch_tmap(&mp.u); prefetch_tmap(&mp.dir);
+    prefetch_tmap(&mp.phi); prefetch_tmap(&mp.phit); prefetch_tmap(&mp.u_h); prefetch_tmap(&mp.u_l);
+    prefetch_tmap(&mp.d_h); prefetch_tmap(&mp.d_l);
     prefetch_tmap(&mp.dm); prefetch_tmap(&mp.um); prefetch_tmap(&mp.d32);
   }
   if (warp == 2) tmem_alloc<512>(&tl.tslot);
@@ -1229,8 +1254,10 @@ bool encode_maps(const KParams &p, TcMaps *m, char *why) {
   const int NT = p.tc.NT;
   const bool ok = encode_2d(enc, &m->phi, p.phi, F32, 4, mats * d.N, d.D, 32, TM, true) &&
                   encode_2d(enc, &m->phit, b.PT, F32, 4, mats * d.D, d.N, 32, TM, true) &&
-                  encode_2d(enc, &m->u, b.U, F32, 4, (long)d.Tl * d.Pp, d.N, 32, NT, true) &&
-                  encode_2d(enc, &m->dir, b.D32, F32, 4, (long)d.Tl * d.P, d.D, 32, NT, true) &&
+                  encode_2d(enc, &m->u_h, b.Uh, F32, 4, (long)d.Tl * d.Pp, d.N, 32, NT, true) &&
+                  encode_2d(enc, &m->u_l, b.Ul, F32, 4, (long)d.Tl * d.Pp, d.N, 32, NT, true) &&
+                  encode_2d(enc, &m->d_h, b.Dh, F32, 4, (long)d.Tl * d.P, d.D, 32, NT, true) &&
+                  encode_2d(enc, &m->d_l, b.Dl, F32, 4, (long)d.Tl * d.P, d.D, 32, NT, true) &&
                   encode_2d(enc, &m->dm, b.Dm, F64, 8, (long)d.Tl * d.C, d.D, TK, d.C, false) &&
                   encode_2d(enc, &m->um, b.Um, F64, 8, (long)d.Tl * d.N, d.Cp, d.Cp, TK, false) &&
                   encode_2d(enc, &m->d32, b.D32, F32, 4, (long)d.Tl * d.P, d.D, TM, NT, false);
