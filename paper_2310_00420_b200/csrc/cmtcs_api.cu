@@ -84,33 +84,41 @@ struct Carver {
   }
 };
 
-// widest column tile: 256 columns, or 128 with a shared Φ (its re-reads per column tile hit L2)
-// which leaves TMEM room for double-buffered or K-split accumulators (CMTCS_NTMAX overrides)
+// widest column tile: 128 columns (TMEM holds the accumulators and the A stages; CMTCS_NTMAX
+// overrides)
 int nt_max(int shared_phi) {
+  (void)shared_phi;
   const char *e = getenv("CMTCS_NTMAX");
   if (e) return std::max(16, std::min(TC_NTMAX, atoi(e) / 16 * 16));
-  return shared_phi ? 128 : TC_NTMAX;
+  return TC_NTMAX;
 }
 
 TcCfg make_tc(const Dims &d) {
   TcCfg tc;
   tc.NT = std::min(nt_max(d.shared_phi), (d.P + 15) / 16 * 16);
-  tc.slot = (tc.NT + 31) / 32 * 32;
-  tc.nacc = std::max(1, std::min(4, 512 / tc.slot - 1));   // main accumulators besides the cross one
-  // ring stage: A hi/lo (2 × 16 KB), B hi/lo (2 × NT × 128 B), fp64 mean-column chunk (≤ 32 × Cp × 8 B)
+  tc.slot = (tc.NT + 15) / 16 * 16;
+  // TMEM (512 columns): accumulators in [0, acol0), the A stages (tf32 hi | lo, 64 columns) above:
+  // three A stages with double-buffered accumulators when both fit, else two (CMTCS_SA overrides)
+  tc.sa = 4 * tc.slot <= 512 - 64 * 3 ? 3 : 2;
+  if (getenv("CMTCS_SA")) tc.sa = std::max(1, std::min(4, atoi(getenv("CMTCS_SA"))));
+  tc.acol0 = 512 - 64 * tc.sa;
+  tc.dbl = 4 * tc.slot <= tc.acol0 ? 1 : 0;
+  tc.nacc = std::max(1, std::min(4, tc.acol0 / tc.slot - 1));   // main accumulators besides the cross one
+  // ring stage: fp32 A (16 KB), B hi/lo (2 × NT × 128 B), fp64 mean-column chunk (≤ 32 × Cp × 8 B)
   const unsigned mean_bytes = (256u * (unsigned)d.Cp + 1023u) & ~1023u;
-  tc.stage_bytes = 2u * 128u * 128u + 2u * (unsigned)tc.NT * 128u + mean_bytes;
+  tc.stage_bytes = 128u * 128u + 2u * (unsigned)tc.NT * 128u + mean_bytes;
   // one CTA per SM (512 TMEM columns) within ≤ 212 KB of the 227 KB of shared memory: the stage-2
   // epilogue's d tile (NT × 128 fp32) when ≥ 3 ring stages still fit (measured at C3: a 4th stage
   // instead of the d tile does not help, the K loop is bound by shared-memory traffic)
   const unsigned budget = 212u * 1024u;
   const unsigned dtile = (unsigned)tc.NT * 128u * 4u;
-  const int st_with = (int)((budget - std::min(budget, dtile)) / tc.stage_bytes);
-  const int st_without = std::min(4, (int)(budget / tc.stage_bytes));
+  int st_with = (int)((budget - std::min(budget, dtile)) / tc.stage_bytes);
+  const int st_without = std::min(6, (int)(budget / tc.stage_bytes));
+  if (getenv("CMTCS_NODTILE")) st_with = 0;   // experiments: ring stages instead of the d tile
   if (st_with >= 3) {
     tc.use_dtile = 1;
     tc.dtile_bytes = dtile;
-    tc.stages = std::min(4, st_with);
+    tc.stages = std::min(6, st_with);
   } else {
     tc.use_dtile = 0;
     tc.dtile_bytes = 0;
@@ -231,7 +239,7 @@ size_t carve(const Dims &d, char *base, Bufs *b) {
   b->histt = cv.take<int>(cap);
   b->status = cv.take<int>(8);
   b->u = cv.take<int>(1);
-  b->ts = cv.take<unsigned long long>((size_t)cap * 4 + 256);   // + 256 diagnostic stamps
+  b->ts = cv.take<unsigned long long>((size_t)cap * 4 + 512);   // + 2 × 256 diagnostic stamps
   b->stats = cv.take<double>(16);
   b->assign = cv.take<int>(Tl);
   b->Upart = cv.take<float>(d.S1 > 1 ? Tl * d.S1 * d.Pp * N : 1);
@@ -323,7 +331,7 @@ cmtcs_status one_em_iteration(cmtcs_ctx *c, const uint64_t *probe_bits, const do
   L += 4;
   if (tm) {
     CUDA_OK(c, cudaEventRecord(c->tev[2], s));
-    CUDA_OK(c, cudaMemcpyAsync(c->h_ts, kp.b.ts, sizeof(unsigned long long) * (4 * d.cap + 256), cudaMemcpyDeviceToHost, s));
+    CUDA_OK(c, cudaMemcpyAsync(c->h_ts, kp.b.ts, sizeof(unsigned long long) * (4 * d.cap + 512), cudaMemcpyDeviceToHost, s));
   }
   CUDA_OK(c, cudaMemcpyAsync(c->h_u, kp.b.u, sizeof(int), cudaMemcpyDeviceToHost, s));
   CUDA_OK(c, cudaMemcpyAsync(c->h_out, kp.b.stats, 16 * sizeof(double), cudaMemcpyDeviceToHost, s));
@@ -356,17 +364,20 @@ cmtcs_status one_em_iteration(cmtcs_ctx *c, const uint64_t *probe_bits, const do
       fprintf(stderr, "[cmtcs] EM it %d: %d CG steps, per step us: phase1 %.2f phase2 %.2f update %.2f\n",
               c->em_iter, steps_run, ph[0] / steps_run, ph[1] / steps_run, ph[2] / steps_run);
       for (int ph = 0; ph < 2 && steps_run > 5; ++ph) {
-        const unsigned long long *g = c->h_ts + 4 * d.cap + 128 * ph;
-        const unsigned long long t0 = c->h_ts[4 * 5 + (ph ? 3 : 0)];
+        const unsigned long long *g = c->h_ts + 4 * d.cap + 256 * ph;
+        const unsigned long long t0 = g[127];   // SM clock at the phase start (CTA 0)
         auto us = [&](int i) { return g[i] ? ((double)g[i] - (double)t0) * 1e-3 : -1.0; };
-        fprintf(stderr, "[cmtcs]   phase %d CTA0 unit0 (us): prod start %.2f epi start %.2f\n", ph + 1, us(84), us(83));
+        fprintf(stderr, "[cmtcs]   phase %d CTA0 unit0 (kilocycles): prod start %.2f epi start %.2f\n", ph + 1, us(84), us(83));
         fprintf(stderr, "[cmtcs]     prod acq :"); for (int i = 0; i < 16; ++i) fprintf(stderr, " %.2f", us(i));
         fprintf(stderr, "\n[cmtcs]     prod iss :"); for (int i = 16; i < 32; ++i) fprintf(stderr, " %.2f", us(i));
         fprintf(stderr, "\n[cmtcs]     mma full :"); for (int i = 32; i < 48; ++i) fprintf(stderr, " %.2f", us(i));
-        fprintf(stderr, "\n[cmtcs]     epi full :"); for (int i = 64; i < 80; ++i) fprintf(stderr, " %.2f", us(i));
+        fprintf(stderr, "\n[cmtcs]     A full   :"); for (int i = 48; i < 64; ++i) fprintf(stderr, " %.2f", us(i));
+        fprintf(stderr, "\n[cmtcs]     A aempty :"); for (int i = 64; i < 80; ++i) fprintf(stderr, " %.2f", us(i));
+        fprintf(stderr, "\n[cmtcs]     A split  :"); for (int i = 90; i < 106; ++i) fprintf(stderr, " %.2f", us(i));
+        fprintf(stderr, "\n[cmtcs]     A done   :"); for (int i = 106; i < 120; ++i) fprintf(stderr, " %.2f", us(i));
+        fprintf(stderr, "\n[cmtcs]     epi grp  :"); for (int i = 128; i < 160; ++i) fprintf(stderr, " %.2f", us(i));
         fprintf(stderr, "\n[cmtcs]     epi loopend %.2f meanepi %.2f tfull %.2f drained %.2f end %.2f\n", us(85), us(86), us(80), us(81), us(82));
-        fprintf(stderr, "[cmtcs]     drain    :"); for (int i = 90; i < 120; ++i) fprintf(stderr, " %.2f", us(i));
-        fprintf(stderr, "\n");
+
       }
     }
     float ms = 0.f;
@@ -476,7 +487,7 @@ cmtcs_status cmtcs_init(cmtcs_ctx **out, const cmtcs_problem *p, const float *ph
   CUDA_OK(c, cudaMallocHost((void **)&c->h_status, 8 * sizeof(int)));
 
   CUDA_OK(c, cudaMallocHost((void **)&c->h_u, sizeof(int)));
-  CUDA_OK(c, cudaMallocHost((void **)&c->h_ts, sizeof(unsigned long long) * (4 * d.cap + 256)));
+  CUDA_OK(c, cudaMallocHost((void **)&c->h_ts, sizeof(unsigned long long) * (4 * d.cap + 512)));
   for (int i = 0; i < 3; ++i) CUDA_OK(c, cudaEventCreate(&c->tev[i]));
   CUDA_OK(c, cudaMemsetAsync(b.status, 0, 8 * sizeof(int), c->stream));
   CUDA_OK(c, cudaMemsetAsync(b.gam, 0, sizeof(double) * d.Tl * d.P * d.cap, c->stream));

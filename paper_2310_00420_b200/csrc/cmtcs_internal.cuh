@@ -14,7 +14,7 @@ constexpr int OP_BR = 128;      // operator tile rows (N in stage 1, D in stage 
 constexpr int OP_BK = 16;       // mean-column (SIMT) contraction chunk
 constexpr int OP_THREADS = 256; // mean-column kernels
 constexpr int TC_THREADS = 128; // tensor-core probe kernels (4 warps = 128 TMEM lanes)
-constexpr int TC_NTMAX = 256;   // widest probe-column tile (MMA N ≤ 256)
+constexpr int TC_NTMAX = 128;   // widest probe-column tile (MMA N; TMEM also holds the A stages)
 
 // Sizes of one rank's problem.  Column index of probe (c, k) inside a task: col = c*K + k.
 struct Dims {
@@ -84,9 +84,12 @@ struct Bufs {
 
 // tensor-core operator configuration (chosen at init from P)
 struct TcCfg {
-  int NT;            // column tile width (multiple of 16, ≤ 256)
+  int NT;            // column tile width (multiple of 16, ≤ TC_NTMAX)
   int slot;          // TMEM columns per accumulator (NT rounded up to 32)
-  int nacc;          // K-split main accumulators ((1 + nacc)·slot ≤ 512 TMEM columns)
+  int sa;            // A stages in TMEM (64 columns each: the tf32 hi and lo halves of a 128 × 32 tile)
+  int acol0;         // first TMEM column of the A stages (= 512 − 64·sa; accumulators below)
+  int dbl;           // two accumulator buffers (cross + one main each) fit below acol0
+  int nacc;          // K-split main accumulators ((1 + nacc)·slot ≤ acol0)
   int stages;        // smem pipeline depth
   unsigned stage_bytes;
   int pf;            // L2 prefetch distance of the producer (chunks ahead; 0 = off)
@@ -119,7 +122,8 @@ struct KParams {
   int it;                      // global EM iteration index of this E-step
   const uint64_t *probe_bits;  // optional override
   const double *q_override;    // optional
-  int dbg_flags;               // CMTCS_DBG (diagnostics only): 1 skip mean DFMA, 2 skip MMA, 4 skip B gather
+  int dbg_flags;               // CMTCS_DBG (diagnostics only, wrong results): 1 no DMMA, 2 no tcgen05.mma,
+                               // 4 no tf32 split, 8/16/32 accumulator layouts, 64 no epilogue, 128 no TMA
 };
 
 // launchers (return cudaGetLastError())

@@ -16,23 +16,25 @@
 // C fp64 mean columns of a task ride along with the task's column-tile-0 units: fp64 DFMA on the
 // CUDA cores, reading the same smem Φ tiles the tensor core reads.
 //
-// Warp roles in phases 1-2 (384 threads):
+// Warp roles in phases 1-2 (320 threads):
 //   warp 0     TMA producer: fp32 Φ/Φᵀ tiles (A), direction / U tiles (B), fp64 mean-column chunk
-//   warp 1     MMA issuer: tcgen05.mma kind::tf32, tcgen05.commit frees ring stages / the tile
-//   warps 2-3  converters: tf32 split of A and B of every staged chunk (warp 2 also owns TMEM)
-//   warps 4-7  the fp64 mean columns: per ring stage DMMA on the split Φ tile, per tile their outputs
-//   warps 8-11 the epilogue (TMEM → registers → U / W, dᵀAd partials), overlapping the next tile's
+//   warp 1     MMA issuer: tcgen05.mma kind::tf32 with A in TMEM, tcgen05.commit frees stages / tiles
+//   warps 2-5  the A warps (one per TMEM lane quarter; warp 2 also owns TMEM): split every staged
+//              fp32 A tile into the exact tf32 pair hi + lo and write it to a TMEM A stage
+//              (tcgen05.st), then the fp64 mean columns' DMMA on the same fp32 tile
+//   warps 6-9  the epilogue (TMEM → registers → U / W, dᵀAd partials), overlapping the next tile's
 //              K loop when the accumulators are double-buffered in TMEM
 // All operands arrive by TMA into an S-stage ring of 128-byte-swizzled K-major smem tiles, so no
 // CTA-wide barrier runs inside a K loop; the producer runs ahead into the next unit while the
-// epilogue of the previous one drains.  mbarriers: full[s] (TMA bytes), conv[s] (split done),
-// empty[s] (MMA done), mdone[s] (fp64 warps done), tfull / tempty (accumulator handshake).
+// epilogue of the previous one drains.  mbarriers: full[s] (TMA bytes), empty[s] (MMA done and the
+// four A warps done with the stage), afull[a] / aempty[a] (TMEM A stage written / consumed by the
+// MMAs), tfull / tempty (accumulator handshake).
 //
-// The A operands (Φ itself and its transpose) live in HBM as plain fp32 and arrive by TMA; the
-// converter warps split each staged tile in shared memory into the exact pair x = hi + lo,
-// hi = tf32(x) (in place) and lo = x − hi (a second tile), so Φ is read once per use (mbarrier
-// conv[s]: split done → the MMA warp may issue).  The B operands (directions, U — small next to Φ
-// and re-read by every row tile) are written by their producers as tf32 pairs and staged as such.
+// The A operands (Φ itself and its transpose) live in HBM as plain fp32 and arrive by TMA; the A
+// warps split each staged tile into hi = tf32(x), lo = x − hi straight into tensor memory, so the
+// shared-memory port carries each A byte once (TMA write, one read) and the MMAs read only B from
+// shared memory.  The B operands (directions, U — small next to Φ and re-read by every row tile)
+// are written by their producers as tf32 pairs and staged as such.
 //
 // 3xTF32: every operand x is the exact pair x = hi + lo with hi = tf32(x), and each K = 8 step issues
 //   acc_x += lo_A·hi_B + hi_A·lo_B ;  acc_m += hi_A·hi_B
@@ -62,14 +64,16 @@ namespace {
 
 constexpr int TM = 128;                   // tile rows (MMA M)
 constexpr int TK = 32;                    // K per pipeline stage (one 128-byte swizzled row)
-constexpr uint32_t A_BYTES = TM * 128;    // 16 KB per hi / lo A tile
-constexpr int MAXST = 4;
-constexpr int NTHREADS = 384;
-constexpr int MEAN0 = 128;                // first thread of the mean (fp64) warps 4-7
-constexpr int EPI0 = 256;                 // first thread of the epilogue warps 8-11
+constexpr uint32_t A_BYTES = TM * 128;    // 16 KB fp32 A tile per ring stage
+constexpr int MAXST = 6;
+constexpr int MAXSA = 4;                  // TMEM A stages
+constexpr int NTHREADS = 320;
+constexpr int MEAN0 = 64;                 // first thread of the A (split + fp64 mean) warps 2-5
+constexpr int EPI0 = 192;                 // first thread of the epilogue warps 6-9
 
 struct PSmemTail {
-  uint64_t full[MAXST], conv[MAXST], convm[MAXST], empty[MAXST], mdone[MAXST];
+  uint64_t full[MAXST], empty[MAXST];
+  uint64_t afull[MAXSA], aempty[MAXSA];   // TMEM A stages: written by the A warps / read by the MMAs
   uint64_t tfull[2], tempty[2];      // TMEM accumulator buffers: MMA done / epilogue drained
   uint64_t dfull, dempty;             // the stage-2 epilogue's d tile (TMA bytes / epilogue done)
   uint32_t tslot;
@@ -159,30 +163,31 @@ __device__ __forceinline__ double warp_sum(double v) {
 // TMEM accumulators of a tile: the cross terms (lo·hi + hi·lo, ~2^-11 of the product) in one
 // accumulator at column 0, the main terms (hi·hi) split over K into `nacc` accumulators at columns
 // (1 + q)·slot, summed in fp32 in the epilogue (the tensor pipe's fp32 accumulation loses bits over
-// long K).  Short contractions (≤ 32 chunks, K ≤ 1024) use one main accumulator and two 256-column
-// buffers (double buffering: the MMA warp starts the next tile while the epilogue drains this one);
-// longer ones up to tc.nacc main accumulators in one 512-column buffer.
+// long K).  Short contractions (≤ 32 chunks, K ≤ 1024) use one main accumulator and two buffers
+// of 2·slot columns (double buffering: the MMA warp starts the next tile while the epilogue drains
+// this one) when they fit below the A stages; longer ones up to tc.nacc main accumulators.
 __device__ __forceinline__ bool unit_dbl(const TcCfg &tc, int nk, int dbg) {
-  return 2 * tc.slot <= 256 && nk <= (dbg & 32 ? 64 : 32) && !(dbg & 16);
+  return tc.dbl && nk <= (dbg & 32 ? 64 : 32) && !(dbg & 16);
 }
 __device__ __forceinline__ int unit_nacc(const TcCfg &tc, int nk, int dbg) {
   if (unit_dbl(tc, nk, dbg)) return 1;
   return (nk <= 16 && !(dbg & 8)) ? 1 : min(tc.nacc, nk);
 }
 
-// issue the 3xTF32 MMAs of one K = 32 stage (one thread) into main accumulator q
-__device__ __forceinline__ void mma_stage(uint32_t tmem, unsigned char *base, uint32_t b_bytes, uint32_t idesc,
-                                          int q, int slot, bool first_main, bool first_cross) {
-  const uint64_t ah = desc_sw128(smem_u32(base)), al = desc_sw128(smem_u32(base + A_BYTES));
-  const uint64_t bh = desc_sw128(smem_u32(base + 2 * A_BYTES));
-  const uint64_t bl = desc_sw128(smem_u32(base + 2 * A_BYTES + b_bytes));
+// issue the 3xTF32 MMAs of one K = 32 stage (one thread) into main accumulator q: A (hi | lo) from
+// the TMEM A stage at column a_tm, B (hi, lo) from the shared-memory ring stage
+__device__ __forceinline__ void mma_stage(uint32_t tmem, uint32_t a_tm, unsigned char *base, uint32_t b_bytes,
+                                          uint32_t idesc, int q, int slot, bool first_main, bool first_cross) {
+  const uint64_t bh = desc_sw128(smem_u32(base + A_BYTES));
+  const uint64_t bl = desc_sw128(smem_u32(base + A_BYTES + b_bytes));
   const uint32_t tm_m = tmem + (uint32_t)((1 + q) * slot), tm_x = tmem;
 #pragma unroll
   for (int k8 = 0; k8 < TK / 8; ++k8) {
     const uint64_t o = (uint64_t)(k8 * 32) >> 4;  // +32 bytes per K = 8 step inside the swizzled row
-    mma_tf32(tm_x, al + o, bh + o, idesc, (first_cross && k8 == 0) ? 0u : 1u);
-    mma_tf32(tm_x, ah + o, bl + o, idesc, 1u);
-    mma_tf32(tm_m, ah + o, bh + o, idesc, (first_main && k8 == 0) ? 0u : 1u);
+    const uint32_t ah = a_tm + 8 * k8, al = a_tm + 32 + 8 * k8;
+    mma_tf32_ts(tm_x, al, bh + o, idesc, (first_cross && k8 == 0) ? 0u : 1u);
+    mma_tf32_ts(tm_x, ah, bl + o, idesc, 1u);
+    mma_tf32_ts(tm_m, ah, bh + o, idesc, (first_main && k8 == 0) ? 0u : 1u);
   }
 }
 
@@ -212,7 +217,7 @@ __device__ __forceinline__ void acc_load16(uint32_t tmem, int ew, int c0, int na
 }
 
 // Active-column bitmask of a column tile (bit c ⇔ column j0+c has flag 1), computed by one warp
-// from flags written by other CTAs in the previous update phase; NT ≤ 256 → 8 words.
+// from flags written by other CTAs in the previous update phase; NT ≤ 128 → 4 words.
 __device__ __forceinline__ int tile_mask(const int *flag, int ncol, int lane, uint32_t *mask) {
   int cnt = 0;
 #pragma unroll
@@ -244,7 +249,6 @@ __device__ __forceinline__ double lds_d(uint32_t a) {
   asm volatile("ld.shared.f64 %0, [%1];\n" : "=d"(v) : "r"(a));
   return v;
 }
-
 __device__ __forceinline__ float lds_f32(uint32_t a) {
   float v;
   asm volatile("ld.shared.f32 %0, [%1];\n" : "=f"(v) : "r"(a));
@@ -260,11 +264,12 @@ __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
 }
 
 // fp64 mean-column work of one ring stage, one warp, rows [32·ew, 32·ew + 32) of the tile:
-// acc += Φ[rows][k-chunk] · B[k-chunk][C] exactly in fp64 (Φ = hi + lo is the fp32 Φ).  Stage 1 reads
+// acc += Φ[rows][k-chunk] · B[k-chunk][C] exactly in fp64 (the staged fp32 Φ tile).  Stage 1 reads
 // B from the Dm chunk laid out [c][32], stage 2 from the Um chunk laid out [32][Cp].  Accumulator
 // fragment acc[mt][nt] holds rows 32·ew + 8·mt + lane/4, columns 8·nt + 2·(lane%4) + {0, 1}.
+// (Measured: the FP64 tensor path beats row-per-thread DFMA here — C3 −10 %, C4 −35 % with DFMA.)
 template <bool B_CK, int NTC>
-__device__ __forceinline__ void mean_stage(uint32_t a_hi, uint32_t mb, int ew, int lane, int C, int Cp,
+__device__ __forceinline__ void mean_stage(uint32_t a32, uint32_t mb, int ew, int lane, int C, int Cp,
                                            double (&acc)[4][NTC][2]) {
   const int g = lane >> 2, q = lane & 3;
 #pragma unroll
@@ -279,15 +284,11 @@ __device__ __forceinline__ void mean_stage(uint32_t a_hi, uint32_t mb, int ew, i
 #pragma unroll
     for (int mt = 0; mt < 4; ++mt) {
       const uint32_t off = sw128_offset(32 * ew + 8 * mt + g, ks) + (uint32_t)q * 4;
-      const double a = (double)(lds_f32(a_hi + off) + lds_f32(a_hi + A_BYTES + off));
+      const double a = (double)lds_f32(a32 + off);
 #pragma unroll
       for (int nt = 0; nt < NTC; ++nt) dmma(acc[mt][nt], a, bf[nt]);
     }
   }
-}
-
-__device__ __forceinline__ void sts128(uint32_t a, float4 v) {
-  asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};\n" ::"r"(a), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w) : "memory");
 }
 
 // tf32 rounding to nearest (ties away from zero, = cvt.rna.tf32.f32 for finite x) on the integer pipe
@@ -295,25 +296,26 @@ __device__ __forceinline__ float tf32_rna(float x) {
   return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xFFFFE000u);
 }
 
-// Split rows of a staged 128-byte-swizzled fp32 tile into the exact pair x = hi + lo: hi = tf32(x)
-// written in place, lo = x − hi written to the same offsets of `lo`.  The swizzle permutes 16-byte
-// chunks within a row only, so a whole row is 8 chunks at fixed offsets; lane r visits them in the
-// order c ^ (r & 7), which spreads a warp over all 32 banks.  Rows r, r + 64, ... below nrows
-// (64 converter threads).
-__device__ __forceinline__ void split_rows64(uint32_t hi, uint32_t lo, int r, int nrows) {
-  for (; r < nrows; r += 64) {
-    const uint32_t row = (uint32_t)(r >> 3) * 1024 + (uint32_t)(r & 7) * 128;
-    float4 v[8];
+// Row r of a staged 128-byte-swizzled fp32 tile (this thread's TMEM lane) as the exact pair
+// x = hi + lo, hi = tf32(x), lo = x − hi, written to the TMEM A stage at lane address `ta`: hi in
+// columns [0, 32), lo in [32, 64).  The swizzle permutes 16-byte chunks within a row only: logical
+// chunk c of row r sits at position c ^ (r & 7), so the 32 lanes of a warp (32 consecutive rows)
+// spread each read over all 32 banks.
+__device__ __forceinline__ void split_row_tmem(uint32_t a32, uint32_t ta, int r) {
+  const uint32_t row = a32 + (uint32_t)(r >> 3) * 1024 + (uint32_t)(r & 7) * 128;
 #pragma unroll
-    for (int c = 0; c < 8; ++c) v[c] = lds128(hi + row + (uint32_t)((c ^ r) & 7) * 16);
+  for (int h = 0; h < 2; ++h) {
+    float hi[16], lo[16];
 #pragma unroll
-    for (int c = 0; c < 8; ++c) {
-      const uint32_t off = row + (uint32_t)((c ^ r) & 7) * 16;
-      float4 h;
-      h.x = tf32_rna(v[c].x); h.y = tf32_rna(v[c].y); h.z = tf32_rna(v[c].z); h.w = tf32_rna(v[c].w);
-      sts128(hi + off, h);
-      sts128(lo + off, make_float4(v[c].x - h.x, v[c].y - h.y, v[c].z - h.z, v[c].w - h.w));
+    for (int c = 0; c < 4; ++c) {
+      const float4 v = lds128(row + (uint32_t)(((4 * h + c) ^ r) & 7) * 16);
+      hi[4 * c + 0] = tf32_rna(v.x); lo[4 * c + 0] = v.x - hi[4 * c + 0];
+      hi[4 * c + 1] = tf32_rna(v.y); lo[4 * c + 1] = v.y - hi[4 * c + 1];
+      hi[4 * c + 2] = tf32_rna(v.z); lo[4 * c + 2] = v.z - hi[4 * c + 2];
+      hi[4 * c + 3] = tf32_rna(v.w); lo[4 * c + 3] = v.w - hi[4 * c + 3];
     }
+    tmem_st16(ta + 16 * h, hi);
+    tmem_st16(ta + 32 + 16 * h, lo);
   }
 }
 
@@ -540,11 +542,12 @@ __device__ __forceinline__ Unit make_unit1(const Dims &d, const TcCfg &tc, int w
     x.sp = w % d.S1;
     decode_banded(w / d.S1, d.Tl, d.nCT, d.nRT1, &x.t, &x.ct, &x.rt);
   } else {
+    // column tiles of a row tile on neighbouring CTAs: they stream the same Φ rows together (L2)
     x.sp = w % d.S1;
     int r = w / d.S1;
-    x.rt = r % d.nRT1; r /= d.nRT1;
-    x.ct = r % d.nCT;
-    x.t = r / d.nCT;
+    x.ct = r % d.nCT; r /= d.nCT;
+    x.rt = r % d.nRT1;
+    x.t = r / d.nRT1;
   }
   const int j0 = x.ct * tc.NT;
   x.ncol = min(tc.NT, d.P - j0);
@@ -562,10 +565,10 @@ __device__ __forceinline__ Unit make_unit2(const Dims &d, const TcCfg &tc, int w
   if (d.shared_phi) {
     decode_banded(w, d.Tl, d.nCT, d.nRT2, &x.t, &x.ct, &x.rt);
   } else {
-    x.rt = w % d.nRT2;
-    const int r = w / d.nRT2;
-    x.ct = r % d.nCT;
-    x.t = r / d.nCT;
+    x.ct = w % d.nCT;
+    const int r = w / d.nCT;
+    x.rt = r % d.nRT2;
+    x.t = r / d.nRT2;
   }
   const int j0 = x.ct * tc.NT;
   x.ncol = min(tc.NT, d.P - j0);
@@ -582,10 +585,11 @@ __device__ __forceinline__ void unit_work(const KParams &p, Unit &x, int lane, u
   const int j0 = x.ct * p.tc.NT;
   const int m = tile_mask(p.b.flag + (size_t)x.t * d.P + j0, x.ncol, lane, mask);
   x.nmma = m ? ((x.ncol + 15) & ~15) : 0;
-  x.mean = x.ct == 0 && mean_count(p.b.flagm + (size_t)x.t * d.C, d.C, lane) > 0;
+  x.mean = x.ct == 0 && !(p.dbg_flags & 512) && mean_count(p.b.flagm + (size_t)x.t * d.C, d.C, lane) > 0;
 }
 
-// ring: chunk G lives in stage G % S; full / empty / mdone phase of chunk G is G / S
+// ring: chunk G lives in stage G % S; full / empty phase of chunk G is G / S.  The TMEM A ring
+// (SA stages) counts the chunks with probe MMAs the same way (afull / aempty).
 struct RingCtl {
   int S;
   uint32_t g;      // chunks handled so far by this role
@@ -595,17 +599,23 @@ struct RingCtl {
     ++g;
     if (++st == S) { st = 0; ph ^= 1u; }
   }
+  int SA;
+  uint32_t ag;     // TMEM A stages handled so far (A warps, MMA warp)
+  int ast;         // = ag % SA
+  uint32_t aph;    // = (ag / SA) & 1
+  __device__ __forceinline__ void nexta() {
+    ++ag;
+    if (++ast == SA) { ast = 0; aph ^= 1u; }
+  }
   uint32_t ti;     // accumulator tiles handled so far
   uint32_t tuse[2];  // uses of each TMEM accumulator buffer (tfull / tempty phases)
   uint32_t di;     // stage-2 d tiles handled so far (dfull / dempty phases)
-  uint32_t smean;  // producer: bit s = the chunk last placed in slot s belongs to a mean unit
-  uint32_t mcnt[MAXST];  // producer: mean chunks placed in each slot (mdone phases)
 };
 
 // ---- producer (warp 0, one lane) ---------------------------------------------------------------
 __device__ __forceinline__ void produce(const KParams &p, const TcMaps &mp, unsigned char *sm, PSmemTail &tl,
                                         RingCtl &rc, const Unit &x, unsigned long long *tr) {
-  if (tr) tr[84] = globaltimer();
+  if (tr) tr[84] = clock64();
   const uint32_t b_bytes = (uint32_t)p.tc.NT * 128;
   const uint32_t mean_tx = x.stage == 1 ? (uint32_t)p.d.C * TK * 8 : (uint32_t)TK * p.d.Cp * 8;
   const uint32_t bytes = A_BYTES + (x.nmma ? 2 * b_bytes : 0) + (x.mean ? mean_tx : 0);
@@ -614,19 +624,14 @@ __device__ __forceinline__ void produce(const KParams &p, const TcMaps &mp, unsi
     const int st = rc.st;
     const uint32_t cph = rc.ph;
     rc.next();
-    if (G >= (uint32_t)rc.S) {
-      mbar_wait(&tl.empty[st], cph ^ 1u);      // MMAs of chunk G − S (same slot) done
-      if ((rc.smean >> st) & 1u) mbar_wait(&tl.mdone[st], (rc.mcnt[st] - 1) & 1);   // its fp64 work too
-    }
-    if (x.mean) {
-      rc.smean |= 1u << st;
-      rc.mcnt[st]++;
-    } else {
-      rc.smean &= ~(1u << st);
-    }
-    if (tr && kc < 16) tr[kc] = globaltimer();
+    if (G >= (uint32_t)rc.S) mbar_wait(&tl.empty[st], cph ^ 1u);   // chunk G − S (same slot) consumed
+    if (tr && kc < 16) tr[kc] = clock64();
     unsigned char *base = sm + (size_t)st * p.tc.stage_bytes;
     uint64_t *fb = &tl.full[st];
+    if (p.dbg_flags & 128) {                  // diagnostic: no operand traffic
+      mbar_arrive(fb);
+      continue;
+    }
     mbar_arrive_expect_tx(fb, bytes);
     const int k = x.k0 + kc * TK;
     // L2 prefetch PF chunks ahead: HBM latency is hidden beyond the depth of the smem ring
@@ -648,31 +653,35 @@ __device__ __forceinline__ void produce(const KParams &p, const TcMaps &mp, unsi
         if (x.nmma) tma_prefetch_2d(x.stage == 1 ? &mp.d_h : &mp.u_h, kk, x.brow);
       }
     }
-    // fp32 tiles into the hi slots (split in place by the converter warps, lo into the lo slots)
+    // stage layout: fp32 A tile | B hi | B lo | fp64 mean-column chunk
     if (x.stage == 1) {
       tma_load_2d(base, &mp.phi, k, x.arow, fb);
       if (x.nmma) {
-        tma_load_2d(base + 2 * A_BYTES, &mp.d_h, k, x.brow, fb);
-        tma_load_2d(base + 2 * A_BYTES + b_bytes, &mp.d_l, k, x.brow, fb);
+        tma_load_2d(base + A_BYTES, &mp.d_h, k, x.brow, fb);
+        tma_load_2d(base + A_BYTES + b_bytes, &mp.d_l, k, x.brow, fb);
       }
-      if (x.mean) tma_load_2d(base + 2 * A_BYTES + 2 * b_bytes, &mp.dm, k, x.t * p.d.C, fb);
+      if (x.mean) tma_load_2d(base + A_BYTES + 2 * b_bytes, &mp.dm, k, x.t * p.d.C, fb);
     } else {
       tma_load_2d(base, &mp.phit, k, x.arow, fb);
       if (x.nmma) {
-        tma_load_2d(base + 2 * A_BYTES, &mp.u_h, k, x.brow, fb);
-        tma_load_2d(base + 2 * A_BYTES + b_bytes, &mp.u_l, k, x.brow, fb);
+        tma_load_2d(base + A_BYTES, &mp.u_h, k, x.brow, fb);
+        tma_load_2d(base + A_BYTES + b_bytes, &mp.u_l, k, x.brow, fb);
       }
-      if (x.mean) tma_load_2d(base + 2 * A_BYTES + 2 * b_bytes, &mp.um, 0, x.t * p.d.N + k, fb);
+      if (x.mean) tma_load_2d(base + A_BYTES + 2 * b_bytes, &mp.um, 0, x.t * p.d.N + k, fb);
     }
-    if (tr && kc < 16) tr[16 + kc] = globaltimer();
+    if (tr && kc < 16) tr[16 + kc] = clock64();
   }
   if (x.stage == 2 && x.nmma && p.tc.use_dtile) {
     // the epilogue's d tile (rows d0..d0+127 of the tile's NT direction columns), after the K loop
     // so the ring keeps streaming while the previous tile's epilogue still reads its d tile
     if (rc.di > 0) mbar_wait(&tl.dempty, (rc.di - 1) & 1);
     unsigned char *dt = sm + (size_t)rc.S * p.tc.stage_bytes;
-    mbar_arrive_expect_tx(&tl.dfull, p.tc.dtile_bytes);
-    tma_load_2d(dt, &mp.d32, x.rt * TM, x.t * p.d.P + x.ct * p.tc.NT, &tl.dfull);
+    if (p.dbg_flags & 128) {
+      mbar_arrive(&tl.dfull);
+    } else {
+      mbar_arrive_expect_tx(&tl.dfull, p.tc.dtile_bytes);
+      tma_load_2d(dt, &mp.d32, x.rt * TM, x.t * p.d.P + x.ct * p.tc.NT, &tl.dfull);
+    }
     rc.di++;
   }
 }
@@ -686,7 +695,7 @@ __device__ __forceinline__ void mma_unit(const KParams &p, unsigned char *sm, PS
   const uint32_t idesc = idesc_tf32(TM, x.nmma > 0 ? x.nmma : 16);
   const bool dbl = unit_dbl(tc, x.nk, p.dbg_flags);
   const int bi = dbl ? (int)(rc.ti & 1) : 0;
-  const uint32_t tacc = tmem + (uint32_t)(bi * 256);
+  const uint32_t tacc = tmem + (uint32_t)(bi * 2 * tc.slot);
   if (x.nmma) {
     // the epilogue has drained this buffer's previous tile (both buffers for a 512-column tile)
     if (rc.tuse[bi] > 0) mbar_wait(&tl.tempty[bi], (rc.tuse[bi] - 1) & 1);
@@ -695,17 +704,28 @@ __device__ __forceinline__ void mma_unit(const KParams &p, unsigned char *sm, PS
   }
   for (int kc = 0; kc < x.nk; ++kc) {
     const int st = rc.st;
-    mbar_wait(&tl.conv[st], rc.ph);           // operands staged and split
+    const uint32_t ph = rc.ph;
     rc.next();
-    if (tr && kc < 16) tr[32 + kc] = globaltimer();
-    if (x.nmma && !(p.dbg_flags & 2)) {
-      fence_after_sync();
-      const int q = (kc * nacc) / x.nk;
-      const int qfirst = (q * x.nk + nacc - 1) / nacc;
-      mma_stage(tacc, sm + (size_t)st * tc.stage_bytes, b_bytes, idesc, q, tc.slot, kc == qfirst, kc == 0);
-      mma_commit(&tl.empty[st]);
+    if (x.nmma) {
+      const int sa = rc.ast;
+      mbar_wait(&tl.afull[sa], rc.aph);       // A stage written (the A warps waited full[st] first)
+      rc.nexta();
+      mbar_wait(&tl.full[st], ph);            // B staged
+      if (tr && kc < 16) tr[32 + kc] = clock64();
+      if (!(p.dbg_flags & 2)) {
+        fence_after_sync();
+        const int q = (kc * nacc) / x.nk;
+        const int qfirst = (q * x.nk + nacc - 1) / nacc;
+        mma_stage(tacc, tmem + (uint32_t)(tc.acol0 + 64 * sa), sm + (size_t)st * tc.stage_bytes, b_bytes, idesc,
+                  q, tc.slot, kc == qfirst, kc == 0);
+        mma_commit(&tl.aempty[sa]);           // the MMAs have read the A stage
+        mma_commit(&tl.empty[st]);            // ... and the B tiles
+      } else {
+        mbar_arrive(&tl.aempty[sa]);
+        mbar_arrive(&tl.empty[st]);
+      }
     } else {
-      mbar_arrive(&tl.empty[st]);
+      mbar_arrive(&tl.empty[st]);             // the A warps' arrivals complete the stage
     }
   }
   if (x.nmma) {
@@ -716,30 +736,7 @@ __device__ __forceinline__ void mma_unit(const KParams &p, unsigned char *sm, PS
   }
 }
 
-// ---- converter warps (2-3): tf32 split of every staged chunk --------------------------------------
-__device__ __forceinline__ void convert_unit(const KParams &p, unsigned char *sm, PSmemTail &tl, RingCtl &rc,
-                                             const Unit &x) {
-  const int ct = threadIdx.x - 64;            // 0..63
-  const uint32_t b_bytes = (uint32_t)p.tc.NT * 128;
-  for (int kc = 0; kc < x.nk; ++kc) {
-    const int st = rc.st;
-    mbar_wait(&tl.full[st], rc.ph);
-    rc.next();
-    const uint32_t base = smem_u32(sm) + (uint32_t)st * p.tc.stage_bytes;
-    if (!(p.dbg_flags & 4)) {
-      split_rows64(base, base + A_BYTES, ct, TM);                     // A: 128 rows
-      // B (directions / U) arrives already split: stored as tf32 pairs by their producers
-    }
-    fence_proxy_async();                      // generic smem writes → tensor-core (async proxy) reads
-    __syncwarp();
-    if ((threadIdx.x & 31) == 0) {
-      mbar_arrive(&tl.conv[st]);
-      if (x.mean) mbar_arrive(&tl.convm[st]);  // the mean warps follow mean chunks only
-    }
-  }
-}
-
-// named barriers: 1 = mean warps (4-7), 2 = epilogue warps (8-11), 3 = both groups (256 threads)
+// named barriers: 1 = A warps (2-5), 2 = epilogue warps (6-9), 3 = both groups (256 threads)
 __device__ __forceinline__ void mean_sync() { asm volatile("bar.sync 1, 128;\n" ::: "memory"); }
 __device__ __forceinline__ void pair_sync() { asm volatile("bar.sync 3, 256;\n" ::: "memory"); }
 
@@ -780,15 +777,17 @@ __device__ __forceinline__ void split_handoff(const KParams &p, const Unit &x, P
   }
 }
 
-// ---- mean warps (4-7): fp64 mean columns on the FP64 tensor path --------------------------------
+// ---- A warps (2-5): the TMEM A stages, and the fp64 mean columns on the FP64 tensor path -------
 template <int CC>
-__device__ void mean_unit(const KParams &p, unsigned char *sm, PSmemTail &tl, RingCtl &rc, const Unit &x) {
+__device__ void mean_unit(const KParams &p, unsigned char *sm, PSmemTail &tl, RingCtl &rc, uint32_t tmem,
+                          const Unit &x, unsigned long long *tr) {
   const Dims &d = p.d;
   const TcCfg &tc = p.tc;
-  const int mt0 = threadIdx.x - MEAN0, mw = mt0 >> 5, lane = mt0 & 31;
+  const int mt0 = threadIdx.x - MEAN0, mw = (threadIdx.x >> 5) & 3, lane = threadIdx.x & 31;
   const int N = d.N, D = d.D, C = d.C;
   const uint32_t b_bytes = (uint32_t)tc.NT * 128;
-  const uint32_t mu_off = 2 * A_BYTES + 2 * b_bytes;
+  const uint32_t mu_off = A_BYTES + 2 * b_bytes;
+  const uint32_t ta_lane = tmem + ((uint32_t)(32 * mw) << 16) + (uint32_t)tc.acol0;
   constexpr int NTC = (CC + 7) / 8;         // 8-column fp64 MMA tiles covering the C mean columns
   double macc[4][NTC][2];
 #pragma unroll
@@ -796,23 +795,34 @@ __device__ void mean_unit(const KParams &p, unsigned char *sm, PSmemTail &tl, Ri
 #pragma unroll
     for (int nt = 0; nt < NTC; ++nt) macc[mt][nt][0] = macc[mt][nt][1] = 0.0;
   const int fg = lane >> 2, fq = lane & 3;   // fragment row group / column pair of this lane
-  // only chunks of mean units are waited for (convm: one phase per mean chunk of the slot; the
-  // producer refills a slot holding a mean chunk only after mdone, so phases cannot alias) and
-  // released through mdone; the ring position still advances over every chunk
+  // every chunk: its A tile → TMEM A stage (when the unit has probe MMAs), then the fp64 mean
+  // columns' DMMA on the same fp32 tile; the ring stage is released (empty) after both
   for (int kc = 0; kc < x.nk; ++kc) {
     const int st = rc.st;
+    mbar_wait(&tl.full[st], rc.ph);
     rc.next();
-    if (x.mean) {
-      mbar_wait(&tl.convm[st], rc.mcnt[st] & 1);
-      rc.mcnt[st]++;
-      if (!(p.dbg_flags & 1)) {
-        const uint32_t base = smem_u32(sm) + (uint32_t)st * tc.stage_bytes;
-        if (x.stage == 1) mean_stage<true, NTC>(base, base + mu_off, mw, lane, C, d.Cp, macc);
-        else mean_stage<false, NTC>(base, base + mu_off, mw, lane, C, d.Cp, macc);
-      }
+    if (tr && kc < 16) tr[48 + kc] = clock64();
+    const uint32_t base = smem_u32(sm) + (uint32_t)st * tc.stage_bytes;
+    if (x.nmma) {
+      const int sa = rc.ast;
+      if (rc.ag >= (uint32_t)rc.SA) mbar_wait(&tl.aempty[sa], rc.aph ^ 1u);   // MMAs of chunk − SA done
+      rc.nexta();
+      if (tr && kc < 16) tr[64 + kc] = clock64();
+      fence_after_sync();
+      if (!(p.dbg_flags & 4)) split_row_tmem(base, ta_lane + (uint32_t)(64 * sa), 32 * mw + lane);
+      tmem_wait_st();
+      fence_before_sync();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&tl.mdone[st]);
+      if (lane == 0) mbar_arrive(&tl.afull[sa]);
+      if (tr && kc < 16) tr[90 + kc] = clock64();
     }
+    if (x.mean && !(p.dbg_flags & 1)) {
+      if (x.stage == 1) mean_stage<true, NTC>(base, base + mu_off, mw, lane, C, d.Cp, macc);
+      else mean_stage<false, NTC>(base, base + mu_off, mw, lane, C, d.Cp, macc);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&tl.empty[st]);
+    if (tr && kc < 14) tr[106 + kc] = clock64();
   }
   if (x.stage == 1) {
     if (x.mean) {
@@ -882,9 +892,71 @@ __device__ void mean_unit(const KParams &p, unsigned char *sm, PSmemTail &tl, Ri
 }
 
 // ---- epilogue warps (8-11): the probe columns' accumulator tile ------------------------------
-// TMEM accumulator buffer of a tile: two buffers (columns [0, 256) and [256, 512)) when the tile's
-// accumulators fit in 256 columns, so the MMA warp starts the next tile while this one drains
+// TMEM accumulator buffer of a tile: two buffers (columns [0, 2·slot) and [2·slot, 4·slot)) when
+// double-buffered, so the MMA warp starts the next tile while this one drains
 __device__ __forceinline__ int acc_buf(const RingCtl &rc, bool dbl) { return dbl ? (int)(rc.ti & 1) : 0; }
+
+// Stage-2 epilogue, column groups [c0, c0 + 16) of the tile: W = β·acc + α_c ⊙ d for row dd of
+// this thread (its TMEM lane), W stored, fp64 partial dᵀW per column reduced over the warp's 32
+// rows into tl.red[warp % 4]; d from the smem d tile.  (Measured: sharing the drain of a CTA's
+// last tile with the A warps does not pay — they join only after their own mean epilogue.)
+template <int CC>
+__device__ __forceinline__ void drain2_groups(const KParams &p, PSmemTail &tl, const Unit &x, uint32_t tacc,
+                                              int nacc, const float *dtile, const float (&alpha)[CC]) {
+  const Dims &d = p.d;
+  const TcCfg &tc = p.tc;
+  const int ew = (threadIdx.x >> 5) & 3, lane = threadIdx.x & 31, r = 32 * ew + lane;
+  const int D = d.D, C = d.C;
+  const int j0 = x.ct * tc.NT;
+  const int dd = x.rt * TM + r;
+  const bool rv = dd < D;
+  const float betaf = (float)p.beta;
+  const float *__restrict__ arow = p.b.alpha32 + dd;
+  float *__restrict__ Wc = p.b.W + ((size_t)x.t * d.P + j0) * D + dd;
+  for (int c0 = 0; c0 < x.nmma; c0 += 16) {
+    float dv[16], tot[16], a[16], w[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) dv[i] = rv ? dtile[(c0 + i) * TM + r] : 0.f;
+    acc_load16(tacc, ew, c0, nacc, tc.slot, tot);
+    // α_c of this row, c = cluster of column j0 + c0 + i
+    const int jc = j0 + c0, cl0 = jc / d.K;
+    if (d.K >= 16) {   // ≤ 2 clusters in a group: column i in cluster cl0 while i < nb (α preloaded)
+      const int nb = (cl0 + 1) * d.K - jc;
+      float a0 = alpha[0], a1 = alpha[0];
+#pragma unroll
+      for (int c = 1; c < CC; ++c) {
+        if (c == cl0) a0 = alpha[c];
+        if (c == cl0 + 1) a1 = alpha[c];
+      }
+#pragma unroll
+      for (int i = 0; i < 16; ++i) a[i] = i < nb ? a0 : a1;
+    } else {
+      int cl = cl0, rem = jc - cl0 * d.K;
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        a[i] = rv ? __ldg(arow + (size_t)min(cl, C - 1) * D) : 0.f;
+        if (++rem == d.K) { rem = 0; ++cl; }
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 16; ++i) w[i] = fmaf(betaf, tot[i], a[i] * dv[i]);
+    if (rv) {   // columns of retired probes get a W too (never read); MMA padding past ncol is not stored
+      float *wc = Wc + (uint32_t)c0 * (uint32_t)D;
+      const int nv = x.ncol - c0;
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        if (i < nv) *wc = w[i];
+        wc += D;
+      }
+    }
+    double dot[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) dot[i] = (double)dv[i] * (double)w[i];
+    int idx;
+    const double sum = warp_reduce16(dot, lane, &idx);
+    if ((lane & 1) == 0) tl.red[ew][c0 + idx] = sum;
+  }
+}
 
 template <int CC>
 __device__ void probe_epilogue(const KParams &p, unsigned char *sm, PSmemTail &tl, RingCtl &rc, uint32_t tmem,
@@ -892,8 +964,8 @@ __device__ void probe_epilogue(const KParams &p, unsigned char *sm, PSmemTail &t
   if (tr && threadIdx.x != EPI0) tr = nullptr;
   const Dims &d = p.d;
   const TcCfg &tc = p.tc;
-  const int et = threadIdx.x - EPI0, ew = et >> 5, lane = et & 31;
-  const int r = et;                          // tile row = TMEM lane
+  const int et = threadIdx.x - EPI0, ew = (threadIdx.x >> 5) & 3, lane = threadIdx.x & 31;
+  const int r = 32 * ew + lane;              // tile row = TMEM lane (warp w reads lanes 32·(w % 4) + ...)
   const int N = d.N, D = d.D, P = d.P, C = d.C;
   const int nacc = unit_nacc(tc, x.nk, p.dbg_flags);
   const bool dbl = unit_dbl(tc, x.nk, p.dbg_flags);
@@ -908,11 +980,20 @@ __device__ void probe_epilogue(const KParams &p, unsigned char *sm, PSmemTail &t
   __syncwarp();
   const uint32_t *mask = tl.emask[ew];
   uint32_t tacc = tmem;                      // this tile's accumulator buffer
+  // stage 2: α_c of this thread's row for every cluster (read-only during the E-step: the
+  // non-coherent path), loaded while the accumulator is still being computed
+  float alpha[CC];
+  {
+    const int dd = x.rt * TM + 32 * ew + lane;
+#pragma unroll
+    for (int c = 0; c < CC; ++c)
+      alpha[c] = (x.stage == 2 && c < C && dd < D) ? __ldg(p.b.alpha32 + (size_t)c * D + dd) : 0.f;
+  }
   if (x.nmma) {
     const int bi = acc_buf(rc, dbl);
-    tacc = tmem + (uint32_t)(bi * 256);
+    tacc = tmem + (uint32_t)(bi * 2 * tc.slot);
     mbar_wait(&tl.tfull[bi], rc.tuse[bi] & 1);
-    if (tr) tr[80] = globaltimer();
+    if (tr) tr[80] = clock64();
     fence_after_sync();
   }
   if (x.stage == 1) {
@@ -920,23 +1001,28 @@ __device__ void probe_epilogue(const KParams &p, unsigned char *sm, PSmemTail &t
     float *Uh = p.b.Uh + (size_t)x.t * d.Pp * N, *Ul = p.b.Ul + (size_t)x.t * d.Pp * N;
     float *part = p.b.Upart + ((size_t)x.t * d.S1 + x.sp) * d.Pp * N;
     if (x.nmma) {
-      for (int c0 = 0; c0 < x.nmma; c0 += 16) {
+      for (int c0 = 0; c0 < ((p.dbg_flags & 64) ? 0 : x.nmma); c0 += 16) {
         float tot[16];
         acc_load16(tacc, ew, c0, nacc, tc.slot, tot);
         if (n < N) {
+          // rows j0 + c0 + i of U (stride N); the columns past ncol (MMA padding) are not stored
+          const int nv = min(16, x.ncol - c0);
+          const uint32_t o0 = (uint32_t)(j0 + c0) * (uint32_t)N + (uint32_t)n;
+          if (d.S1 == 1) {
+            float *uh = Uh + o0, *ul = Ul + o0;
 #pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            const int c = c0 + i;
-            if (c < x.ncol) {
-              const size_t o = (size_t)(j0 + c) * N + n;
-              if (d.S1 == 1) {
+            for (int i = 0; i < 16; ++i) {
+              if (i < nv) {
                 const float h = tf32_rna(tot[i]);
-                Uh[o] = h;
-                Ul[o] = tot[i] - h;
-              } else {
-                stv(part + o, tot[i]);
+                uh[(uint32_t)i * (uint32_t)N] = h;
+                ul[(uint32_t)i * (uint32_t)N] = tot[i] - h;
               }
             }
+          } else {
+            float *pp = part + o0;
+#pragma unroll
+            for (int i = 0; i < 16; ++i)
+              if (i < nv) pp[(uint32_t)i * (uint32_t)N] = tot[i];
           }
         }
       }
@@ -946,7 +1032,7 @@ __device__ void probe_epilogue(const KParams &p, unsigned char *sm, PSmemTail &t
       if (lane == 0) mbar_arrive(&tl.tempty[bi]);  // the MMA warp may overwrite the accumulator
       rc.tuse[bi]++;
       rc.ti++;
-      if (tr) tr[81] = globaltimer();
+      if (tr) tr[81] = clock64();
     }
     if (d.S1 > 1) {
       int rb, re;
@@ -987,7 +1073,7 @@ __device__ void probe_epilogue(const KParams &p, unsigned char *sm, PSmemTail &t
         }
       }
     }
-    if (tr) tr[82] = globaltimer();
+    if (tr) tr[82] = clock64();
     return;
   }
   if (!x.nmma) return;
@@ -1002,29 +1088,41 @@ __device__ void probe_epilogue(const KParams &p, unsigned char *sm, PSmemTail &t
     mbar_wait(&tl.dfull, rc.di & 1);
     rc.di++;
   }
-  if (tr) tr[86] = globaltimer();
+  if (tr) tr[86] = clock64();
   // per 16-column group: W = β·acc + α_c ⊙ d, dot partials; the cluster of column j0 + c0 + i is
   // tracked incrementally (no integer division per column)
   const float *__restrict__ arow = p.b.alpha32 + dd;
   float *__restrict__ Wc = p.b.W + colbase;
   auto group_tot = [&](int c0, const float *dv, const float *tot) {
     // independent steps over the 16 columns (one epilogue warp per scheduler: ILP, not TLP, hides
-    // latency): α loads, W, stores, exact fp64 products, then the butterfly reduction
-    const uint32_t mk = (mask[c0 >> 5] >> (c0 & 31)) & 0xFFFFu;
-    int cl = (j0 + c0) / d.K, rem = (j0 + c0) - cl * d.K;
+    // latency): α, W, stores, exact fp64 products, then the butterfly reduction.  Columns of
+    // retired probes get a W too (never read: the update skips them).
     float a[16], w[16];
+    const int jc = j0 + c0, cl0 = jc / d.K;
+    if (d.K >= 16) {
+      // ≤ 2 clusters in a group of 16 columns: α of this row for both (read-only during the
+      // E-step: the non-coherent path), column i of the group in cluster cl0 while i < nb
+      const int nb = (cl0 + 1) * d.K - jc;
+      const float a0 = rv ? __ldg(arow + (size_t)min(cl0, C - 1) * D) : 0.f;
+      const float a1 = rv ? __ldg(arow + (size_t)min(cl0 + 1, C - 1) * D) : 0.f;
 #pragma unroll
-    for (int i = 0; i < 16; ++i) {
-      // α_c at this row (read-only during the E-step: the non-coherent path, mostly L1 hits)
-      a[i] = rv ? __ldg(arow + (size_t)min(cl, C - 1) * D) : 0.f;
-      if (++rem == d.K) { rem = 0; ++cl; }
+      for (int i = 0; i < 16; ++i) a[i] = i < nb ? a0 : a1;
+    } else {
+      int cl = cl0, rem = jc - cl0 * d.K;
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        a[i] = rv ? __ldg(arow + (size_t)min(cl, C - 1) * D) : 0.f;
+        if (++rem == d.K) { rem = 0; ++cl; }
+      }
     }
 #pragma unroll
     for (int i = 0; i < 16; ++i) w[i] = fmaf(betaf, tot[i], a[i] * dv[i]);
     if (rv) {
+      float *wc = Wc + (uint32_t)c0 * (uint32_t)D;
+      const int nv = x.ncol - c0;            // the MMA padding columns past ncol are not stored
 #pragma unroll
       for (int i = 0; i < 16; ++i)
-        if ((mk >> i) & 1u) Wc[(size_t)(c0 + i) * D] = w[i];
+        if (i < nv) wc[(uint32_t)i * (uint32_t)D] = w[i];
     }
     double dot[16];
 #pragma unroll
@@ -1038,13 +1136,10 @@ __device__ void probe_epilogue(const KParams &p, unsigned char *sm, PSmemTail &t
     acc_load16(tacc, ew, c0, nacc, tc.slot, tot);
     group_tot(c0, dv, tot);
   };
-  if (dts) {
-    for (int c0 = 0; c0 < x.nmma; c0 += 16) {
-      float dv[16];
-#pragma unroll
-      for (int i = 0; i < 16; ++i) dv[i] = rv ? dtile[(c0 + i) * TM + r] : 0.f;
-      group(c0, dv);
-    }
+  if (p.dbg_flags & 64) {
+    // diagnostic: accumulator not drained
+  } else if (dts) {
+    drain2_groups<CC>(p, tl, x, tacc, nacc, dtile, alpha);
   } else {
     // global loads of d: the next group's are issued while the current one is processed
     float dnx[16];
@@ -1074,18 +1169,18 @@ __device__ void probe_epilogue(const KParams &p, unsigned char *sm, PSmemTail &t
     rc.tuse[bi]++;
     rc.ti++;
   }
-  if (tr) tr[81] = globaltimer();
+  if (tr) tr[81] = clock64();
   epi_sync();
   for (int c = et; c < x.ncol; c += 128)
     if ((mask[c >> 5] >> (c & 31)) & 1u)
       stv(p.b.dAd + ((size_t)x.t * P + j0 + c) * d.nRT2 + x.rt,
           tl.red[0][c] + tl.red[1][c] + tl.red[2][c] + tl.red[3][c]);
   epi_sync();                                 // tl.red is reused by the next unit
-  if (tr) tr[82] = globaltimer();
+  if (tr) tr[82] = clock64();
 }
 
 // ---------------------------------------------------------------------------------------------
-// the persistent CG kernel: grid = #SMs (cooperative), 256 threads, one CTA per SM
+// the persistent CG kernel: grid = #SMs (cooperative), 320 threads, one CTA per SM
 // ---------------------------------------------------------------------------------------------
 template <int CC>
 __global__ void __launch_bounds__(NTHREADS, 1) k_cg_persistent(KParams p, const __grid_constant__ TcMaps mp) {
@@ -1099,10 +1194,11 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_cg_persistent(KParams p, const 
   if (tid == 0) {
     for (int s = 0; s < tc.stages; ++s) {
       mbar_init(&tl.full[s], 1);
-      mbar_init(&tl.conv[s], 2);
-      mbar_init(&tl.convm[s], 2);
-      mbar_init(&tl.empty[s], 1);
-      mbar_init(&tl.mdone[s], 4);
+      mbar_init(&tl.empty[s], 5);             // the MMA warp's commit (or arrive) + the 4 A warps
+    }
+    for (int s = 0; s < tc.sa; ++s) {
+      mbar_init(&tl.afull[s], 4);
+      mbar_init(&tl.aempty[s], 1);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tl.tfull[i], 1);
@@ -1122,20 +1218,21 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_cg_persistent(KParams p, const 
   __syncthreads();
   fence_after_sync();
   const uint32_t tmem = tl.tslot;
-  RingCtl rc{tc.stages, 0u, 0, 0u, 0u, {0u, 0u}, 0u, 0u, {0u, 0u, 0u, 0u}};
+  RingCtl rc{tc.stages, 0u, 0, 0u, tc.sa, 0u, 0, 0u, 0u, {0u, 0u}, 0u};
   unsigned epoch = 0;
   unsigned *bar = p.b.gridbar;
   const int n1 = d.Tl * d.nCT * d.nRT1 * d.S1, n2 = d.Tl * d.nCT * d.nRT2;
   const int ncols = d.Tl * (d.P + d.C);
   const bool producer = warp == 0 && lane == 0, issuer = warp == 1 && lane == 0;
-  const bool conv = warp == 2 || warp == 3, meanw = warp >= 4 && warp < 8, epi = warp >= 8;
+  const bool meanw = warp >= 2 && warp < 6, epi = warp >= 6;
   const bool tile_role = true;
   for (int u = 0; u < d.cap; ++u) {
     if (b == 0 && tid == 0) p.b.ts[4 * u + 0] = globaltimer();
     // diagnostic trace of CTA 0's first unit of each phase at CG step 5 (CMTCS_PHASE_LOG)
     unsigned long long *tr1 = (b == 0 && u == 5) ? p.b.ts + 4 * d.cap : nullptr;
-    unsigned long long *tr2 = tr1 ? tr1 + 128 : nullptr;
+    unsigned long long *tr2 = tr1 ? tr1 + 256 : nullptr;
     // ---- phase 1: U = Φ D ----
+    if (tr1 && tid == 0) tr1[127] = clock64();   // trace times are SM clocks from here
     if (tile_role) {
       for (int w = b; w < n1; w += G, tr1 = nullptr) {
         Unit x = make_unit1(d, tc, w);
@@ -1144,14 +1241,14 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_cg_persistent(KParams p, const 
         if (!x.nmma && !x.mean) continue;
         if (producer) produce(p, mp, sm, tl, rc, x, tr1);
         else if (issuer) mma_unit(p, sm, tl, rc, tmem, x, tr1);
-        else if (conv) convert_unit(p, sm, tl, rc, x);
-        else if (meanw) mean_unit<CC>(p, sm, tl, rc, x);
+        else if (meanw) mean_unit<CC>(p, sm, tl, rc, tmem, x, (tr1 && threadIdx.x == MEAN0) ? tr1 : nullptr);
         else if (epi) probe_epilogue<CC>(p, sm, tl, rc, tmem, x, mask, tr1);
       }
     }
     grid_sync(bar, epoch);
     if (b == 0 && tid == 0) p.b.ts[4 * u + 3] = globaltimer();
     // ---- phase 2: W = βΦᵀU + αD, dᵀW partials ----
+    if (tr2 && tid == 0) tr2[127] = clock64();
     if (tile_role) {
       for (int w = b; w < n2; w += G, tr2 = nullptr) {
         Unit x = make_unit2(d, tc, w);
@@ -1160,8 +1257,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_cg_persistent(KParams p, const 
         if (!x.nmma && !x.mean) continue;
         if (producer) produce(p, mp, sm, tl, rc, x, tr2);
         else if (issuer) mma_unit(p, sm, tl, rc, tmem, x, tr2);
-        else if (conv) convert_unit(p, sm, tl, rc, x);
-        else if (meanw) mean_unit<CC>(p, sm, tl, rc, x);
+        else if (meanw) mean_unit<CC>(p, sm, tl, rc, tmem, x, (tr2 && threadIdx.x == MEAN0) ? tr2 : nullptr);
         else if (epi) probe_epilogue<CC>(p, sm, tl, rc, tmem, x, mask, tr2);
       }
     }

@@ -1,0 +1,116 @@
+// Microbenchmark: the CG operator's per-chunk MMA sequence (3xTF32: per K = 8 step lo·hi and hi·lo
+// into the cross accumulator, hi·hi into the main one; A in TMEM, B hi/lo in shared memory, N = 80)
+// issued by one thread, alone and with concurrent TMEM traffic from other warps:
+//   mode 0: MMAs only
+//   mode 1: + 4 warps streaming tcgen05.ld of another TMEM region (an epilogue draining)
+//   mode 2: + 4 warps streaming tcgen05.st into another TMEM region (A warps writing A stages)
+//   mode 3: + both (8 warps)
+//   mode 4: + 4 warps streaming ld.shared (shared-memory port pressure)
+// Cycles per chunk (12 MMAs) from clock64 on the issuing thread.
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -I paper_2310_00420_b200/csrc -o tools/mma_contention_test tools/mma_contention_test.cu
+#include <cstdio>
+#include "umma.cuh"
+
+using namespace cmtcs::umma;
+
+__device__ __forceinline__ void mma_ts(uint32_t d, uint32_t a, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
+  asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\ttcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(d),
+               "r"(a), "l"(bdesc), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void st16(uint32_t taddr, float x) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1};\n" ::"r"(taddr), "f"(x)
+      : "memory");
+}
+
+constexpr int NB = 80;
+
+__global__ void __launch_bounds__(384, 1) k(int mode, int chunks, unsigned long long *out, float *sink) {
+  extern __shared__ __align__(1024) unsigned char raw[];
+  unsigned char *sm = reinterpret_cast<unsigned char *>((reinterpret_cast<uintptr_t>(raw) + 1023) & ~(uintptr_t)1023);
+  __shared__ uint64_t done;
+  __shared__ uint32_t slot;
+  __shared__ volatile int stop;
+  const int t = threadIdx.x, w = t >> 5;
+  for (int i = t; i < 65536 / 4; i += blockDim.x) reinterpret_cast<float *>(sm)[i] = 0.f;
+  if (t == 0) { mbar_init(&done, 1); stop = 0; }
+  if (w == 0) tmem_alloc<512>(&slot);
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+  fence_before_sync();
+  __syncthreads();
+  fence_after_sync();
+  const uint32_t tm = slot;
+  if (t == 0) {
+    const uint32_t idesc = idesc_tf32(128, NB);
+    const uint64_t bh = desc_sw128(smem_u32(sm)), bl = desc_sw128(smem_u32(sm + NB * 128));
+    const uint32_t tx = tm, tmain = tm + 96, ta = tm + 384;
+    const long long c0 = clock64();
+    for (int c = 0; c < chunks; ++c) {
+#pragma unroll
+      for (int k8 = 0; k8 < 4; ++k8) {
+        const uint64_t o = (uint64_t)(k8 * 32) >> 4;
+        mma_ts(tx, ta + 32 + 8 * k8, bh + o, idesc, 1);
+        mma_ts(tx, ta + 8 * k8, bl + o, idesc, 1);
+        mma_ts(tmain, ta + 8 * k8, bh + o, idesc, 1);
+      }
+    }
+    mma_commit(&done);
+    mbar_wait(&done, 0);
+    const long long c1 = clock64();
+    out[blockIdx.x] = (unsigned long long)(c1 - c0);
+    stop = 1;
+  } else if (w >= 4 && w < 8 && (mode == 1 || mode == 3)) {
+    float acc = 0.f;
+    const uint32_t lane_base = tm + ((uint32_t)((w & 3) * 32) << 16) + 192;
+    while (!stop) {
+      float v[16];
+      tmem_ld16(lane_base + (acc > 1e30f ? 16 : 0), v);
+      for (int i = 0; i < 16; ++i) acc += v[i];
+    }
+    if (acc == 1.2345f) sink[0] = acc;
+  } else if (w >= 8 && (mode == 2 || mode == 3)) {
+    const uint32_t lane_base = tm + ((uint32_t)((w & 3) * 32) << 16) + 448;
+    float x = 0.f;
+    while (!stop) {
+      st16(lane_base, x);
+      st16(lane_base + 16, x);
+      asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+      x += 1.f;
+    }
+  } else if (w >= 4 && w < 8 && mode == 4) {
+    float acc = 0.f;
+    uint32_t a = smem_u32(sm) + 32768 + (t & 127) * 16;
+    while (!stop) {
+      float4 v;
+      asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];\n" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
+      acc += v.x;
+      a ^= 2048;
+    }
+    if (acc == 1.2345f) sink[0] = acc;
+  }
+  fence_before_sync();
+  __syncthreads();
+  if (w == 0) tmem_dealloc<512>(tm);
+}
+
+int main() {
+  unsigned long long *out, h[148];
+  float *sink;
+  cudaMalloc(&out, 148 * 8);
+  cudaMalloc(&sink, 64);
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536 + 1024);
+  const char *names[5] = {"MMAs only", "+ tcgen05.ld stream", "+ tcgen05.st stream", "+ ld and st streams", "+ ld.shared stream"};
+  const int chunks = 2000;
+  for (int mode = 0; mode < 5; ++mode) {
+    for (int rep = 0; rep < 2; ++rep) {
+      k<<<148, 384, 65536 + 1024>>>(mode, chunks, out, sink);
+      cudaDeviceSynchronize();
+    }
+    cudaMemcpy(h, out, sizeof(h), cudaMemcpyDeviceToHost);
+    unsigned long long mx = 0;
+    for (int i = 0; i < 148; ++i) mx = h[i] > mx ? h[i] : mx;
+    printf("%-22s: %.0f clk per chunk (12 MMAs, N=%d; floor 12*%d = %d)  %s\n", names[mode], (double)mx / chunks, NB, NB / 2,
+           12 * NB / 2, cudaGetErrorString(cudaGetLastError()));
+  }
+  return 0;
+}
