@@ -535,7 +535,17 @@ __device__ __forceinline__ void decode_banded(int w, int Tl, int nCT, int nRT, i
   *t = r / nCT;
 }
 
-__device__ __forceinline__ Unit make_unit1(const Dims &d, const TcCfg &tc, int w) {
+// Column tile of unit w when the column tiles of a row tile sit on neighbouring CTAs: rotated by
+// the round k = w / G so that a CTA alternates between column tiles (the fp64 mean columns ride
+// with column tile 0: without the rotation, G being a multiple of the group, every CTA would see
+// the same column tile in every round — all the mean work on half of the CTAs).  A bijection
+// whenever the group (the nCT consecutive units sharing everything but ct) never straddles a
+// round boundary, i.e. G % group == 0.
+__device__ __forceinline__ int rotate_ct(int c, int w, int G, int group, int nCT) {
+  return (G % group == 0) ? (c + w / G) % nCT : c;
+}
+
+__device__ __forceinline__ Unit make_unit1(const Dims &d, const TcCfg &tc, int w, int G) {
   Unit x;
   x.stage = 1;
   if (d.shared_phi) {
@@ -545,7 +555,8 @@ __device__ __forceinline__ Unit make_unit1(const Dims &d, const TcCfg &tc, int w
     // column tiles of a row tile on neighbouring CTAs: they stream the same Φ rows together (L2)
     x.sp = w % d.S1;
     int r = w / d.S1;
-    x.ct = r % d.nCT; r /= d.nCT;
+    x.ct = rotate_ct(r % d.nCT, w, G, d.S1 * d.nCT, d.nCT);
+    r /= d.nCT;
     x.rt = r % d.nRT1;
     x.t = r / d.nRT1;
   }
@@ -558,14 +569,14 @@ __device__ __forceinline__ Unit make_unit1(const Dims &d, const TcCfg &tc, int w
   x.brow = x.t * d.P + j0;
   return x;
 }
-__device__ __forceinline__ Unit make_unit2(const Dims &d, const TcCfg &tc, int w) {
+__device__ __forceinline__ Unit make_unit2(const Dims &d, const TcCfg &tc, int w, int G) {
   Unit x;
   x.stage = 2;
   x.sp = 0;
   if (d.shared_phi) {
     decode_banded(w, d.Tl, d.nCT, d.nRT2, &x.t, &x.ct, &x.rt);
   } else {
-    x.ct = w % d.nCT;
+    x.ct = rotate_ct(w % d.nCT, w, G, d.nCT, d.nCT);
     const int r = w / d.nCT;
     x.rt = r % d.nRT2;
     x.t = r / d.nRT2;
@@ -1235,7 +1246,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_cg_persistent(KParams p, const 
     if (tr1 && tid == 0) tr1[127] = clock64();   // trace times are SM clocks from here
     if (tile_role) {
       for (int w = b; w < n1; w += G, tr1 = nullptr) {
-        Unit x = make_unit1(d, tc, w);
+        Unit x = make_unit1(d, tc, w, G);
         uint32_t mask[TC_NTMAX / 32];
         unit_work(p, x, lane, mask);
         if (!x.nmma && !x.mean) continue;
@@ -1251,7 +1262,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_cg_persistent(KParams p, const 
     if (tr2 && tid == 0) tr2[127] = clock64();
     if (tile_role) {
       for (int w = b; w < n2; w += G, tr2 = nullptr) {
-        Unit x = make_unit2(d, tc, w);
+        Unit x = make_unit2(d, tc, w, G);
         uint32_t mask[TC_NTMAX / 32];
         unit_work(p, x, lane, mask);
         if (!x.nmma && !x.mean) continue;
