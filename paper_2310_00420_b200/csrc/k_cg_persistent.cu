@@ -341,7 +341,12 @@ __device__ void report(int *status, int code, int t, int col, int u) {
 
 // ---- phase 3 -----------------------------------------------------------------------------------
 // Alg. 1 lines 3-7 for one probe column by one warp (fp32 vectors, fp64 scalars and dots)
-__device__ void update_probe(const KParams &p, int t, int col, int u, int lane) {
+// With `stg` (this warp's 2·D floats of shared memory, when D is small enough: the ring is idle in
+// this phase) the first pass also parks d and the new r there, so the direction update re-reads
+// shared memory instead of global memory (one dependent global round trip per 256 elements less).
+__device__ void update_probe(const KParams &p, int t, int col, int u, int lane, float4 *stg,
+                             unsigned long long *tr) {
+  if (tr) tr[0] = clock64();
   const Dims &d = p.d;
   const size_t g = (size_t)t * d.P + col;
   // the per-row-tile partials of dᵀAd: one load per lane, then the warp's fixed-order butterfly
@@ -356,7 +361,11 @@ __device__ void update_probe(const KParams &p, int t, int col, int u, int lane) 
     }
     return;
   }
-  const double gam = rr / dAd;
+  // the step sizes act in fp32 (the vectors' precision; fp32 FMAs: F2F.F64.F32 runs at 2 lanes / clk
+  // per SM sub-partition, tools/dmma_test.cu) and the transcript records the values applied
+  const float gamf = (float)(rr / dAd);
+  const double gam = (double)gamf;
+  if (tr) tr[1] = clock64();
   float4 *__restrict__ x4 = reinterpret_cast<float4 *>(p.b.X + g * d.D);
   float4 *__restrict__ r4 = reinterpret_cast<float4 *>(p.b.R + g * d.D);
   float4 *__restrict__ d4 = reinterpret_cast<float4 *>(p.b.D32 + g * d.D);
@@ -380,22 +389,29 @@ __device__ void update_probe(const KParams &p, int t, int col, int u, int lane) 
         const float4 dv = dd[v];
         const float4 ad = wv[v];            // Ad from the operator's epilogue
         float4 x = xv[v], r = rv[v];
-        x.x = (float)fma(gam, (double)dv.x, (double)x.x);
-        x.y = (float)fma(gam, (double)dv.y, (double)x.y);
-        x.z = (float)fma(gam, (double)dv.z, (double)x.z);
-        x.w = (float)fma(gam, (double)dv.w, (double)x.w);
-        r.x = (float)fma(-gam, (double)ad.x, (double)r.x);
-        r.y = (float)fma(-gam, (double)ad.y, (double)r.y);
-        r.z = (float)fma(-gam, (double)ad.z, (double)r.z);
-        r.w = (float)fma(-gam, (double)ad.w, (double)r.w);
+        x.x = fmaf(gamf, dv.x, x.x);
+        x.y = fmaf(gamf, dv.y, x.y);
+        x.z = fmaf(gamf, dv.z, x.z);
+        x.w = fmaf(gamf, dv.w, x.w);
+        r.x = fmaf(-gamf, ad.x, r.x);
+        r.y = fmaf(-gamf, ad.y, r.y);
+        r.z = fmaf(-gamf, ad.z, r.z);
+        r.w = fmaf(-gamf, ad.w, r.w);
         stv(x4 + i, x);
         stv(r4 + i, r);
-        acc += (double)r.x * r.x + (double)r.y * r.y + (double)r.z * r.z + (double)r.w * r.w;
+        if (stg) {
+          stg[i] = dv;
+          stg[n4 + i] = r;
+        }
+        acc += (double)fmaf(r.w, r.w, fmaf(r.z, r.z, fmaf(r.y, r.y, r.x * r.x)));   // fp64 across float4s
       }
     }
   }
+  if (tr) tr[2] = clock64();
   const double rrn = warp_sum(acc);
-  const double xi = rrn / rr;
+  const float xif = (float)(rrn / rr);
+  const double xi = (double)xif;
+  if (tr) tr[3] = clock64();
   const bool conv = sqrt(rrn) <= p.tol * sqrt((double)d.D);
   const bool stop = conv || (u + 1 >= d.cap);
   if (lane == 0) {
@@ -413,17 +429,20 @@ __device__ void update_probe(const KParams &p, int t, int col, int u, int lane) 
 #pragma unroll
       for (int v = 0; v < U; ++v) {
         const int i = i0 + 32 * v;
-        if (i < n4) { rv[v] = ldv(r4 + i); dd[v] = ldv(d4 + i); }
+        if (i < n4) {
+          if (stg) { rv[v] = stg[n4 + i]; dd[v] = stg[i]; }   // this lane's own stores: no sync needed
+          else { rv[v] = ldv(r4 + i); dd[v] = ldv(d4 + i); }
+        }
       }
 #pragma unroll
       for (int v = 0; v < U; ++v) {
         const int i = i0 + 32 * v;
         if (i < n4) {
           float4 dv = dd[v];
-          dv.x = (float)fma(xi, (double)dv.x, (double)rv[v].x);
-          dv.y = (float)fma(xi, (double)dv.y, (double)rv[v].y);
-          dv.z = (float)fma(xi, (double)dv.z, (double)rv[v].z);
-          dv.w = (float)fma(xi, (double)dv.w, (double)rv[v].w);
+          dv.x = fmaf(xif, dv.x, rv[v].x);
+          dv.y = fmaf(xif, dv.y, rv[v].y);
+          dv.z = fmaf(xif, dv.z, rv[v].z);
+          dv.w = fmaf(xif, dv.w, rv[v].w);
           stv(d4 + i, dv);
           float4 h4;
           h4.x = tf32_rna(dv.x); h4.y = tf32_rna(dv.y); h4.z = tf32_rna(dv.z); h4.w = tf32_rna(dv.w);
@@ -433,6 +452,7 @@ __device__ void update_probe(const KParams &p, int t, int col, int u, int lane) 
       }
     }
   }
+  if (tr) tr[4] = clock64();
 }
 
 // the same for one fp64 mean column
@@ -1275,6 +1295,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_cg_persistent(KParams p, const 
     grid_sync(bar, epoch);
     if (b == 0 && tid == 0) p.b.ts[4 * u + 1] = globaltimer();
     // ---- phase 3: CG update, one warp per active column ----
+    unsigned long long *tr3 = (b == 0 && u == 5 && warp == 0) ? p.b.ts + 4 * d.cap + 160 : nullptr;
+    if (tr3 && lane == 0) tr3[8] = clock64();
+    float4 *stage_d = (size_t)NTHREADS / 32 * 2 * d.D * 4 <= (size_t)tc.stages * tc.stage_bytes
+                          ? reinterpret_cast<float4 *>(sm) + (size_t)warp * (d.D / 2) : nullptr;
     for (int w = b * (NTHREADS / 32) + warp; w < ncols; w += G * (NTHREADS / 32)) {
       const int t = w / (d.P + d.C), j = w % (d.P + d.C);
       bool active;
@@ -1282,7 +1306,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_cg_persistent(KParams p, const 
         active = ldv(p.b.flag + (size_t)t * d.P + j) == 1;
         if (active) {
           if (lane == 0) atomicAdd(p.b.hist + u, 1);
-          update_probe(p, t, j, u, lane);
+          update_probe(p, t, j, u, lane, stage_d, (tr3 && w == b * (NTHREADS / 32) + warp && lane == 0) ? tr3 : nullptr);
         }
       } else {
         active = ldv(p.b.flagm + (size_t)t * d.C + (j - d.P)) == 1;
