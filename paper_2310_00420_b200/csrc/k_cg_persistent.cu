@@ -154,6 +154,47 @@ __device__ __forceinline__ double warp_reduce16(double *v, int lane, int *idx) {
   return v[0];
 }
 
+// The same in fp32 with an error-free product split: v = p + e exactly per element (p = d·w rounded,
+// e = fma(d, w, −p)), the p's and e's butterflied separately (fp32 shuffles are one SHFL, fp64
+// two, and the fp64 conversions cost as much as the MMAs: tools/dmma_test.cu); the total is
+// returned in fp64 as p_sum + e_sum.
+__device__ __forceinline__ double warp_reduce16_f(float *p, float *e, int lane, int *idx) {
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const bool up = lane & 16;
+    const float sp = up ? p[i] : p[i + 8], kp = up ? p[i + 8] : p[i];
+    const float se = up ? e[i] : e[i + 8], ke = up ? e[i + 8] : e[i];
+    p[i] = kp + __shfl_xor_sync(0xffffffffu, sp, 16);
+    e[i] = ke + __shfl_xor_sync(0xffffffffu, se, 16);
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const bool up = lane & 8;
+    const float sp = up ? p[i] : p[i + 4], kp = up ? p[i + 4] : p[i];
+    const float se = up ? e[i] : e[i + 4], ke = up ? e[i + 4] : e[i];
+    p[i] = kp + __shfl_xor_sync(0xffffffffu, sp, 8);
+    e[i] = ke + __shfl_xor_sync(0xffffffffu, se, 8);
+  }
+  // from here fp64: 4 → 1 values per lane pair, few conversions
+  double pd[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) pd[i] = (double)p[i] + (double)e[i];
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const bool up = lane & 4;
+    const double send = up ? pd[i] : pd[i + 2], keep = up ? pd[i + 2] : pd[i];
+    pd[i] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+  }
+  {
+    const bool up = lane & 2;
+    const double send = up ? pd[0] : pd[1], keep = up ? pd[1] : pd[0];
+    pd[0] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
+  }
+  pd[0] += __shfl_xor_sync(0xffffffffu, pd[0], 1);
+  *idx = ((lane >> 4) & 1) * 8 + ((lane >> 3) & 1) * 4 + ((lane >> 2) & 1) * 2 + ((lane >> 1) & 1);
+  return pd[0];
+}
+
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
   for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -980,11 +1021,14 @@ __device__ __forceinline__ void drain2_groups(const KParams &p, PSmemTail &tl, c
         wc += D;
       }
     }
-    double dot[16];
+    float dp[16], de[16];
 #pragma unroll
-    for (int i = 0; i < 16; ++i) dot[i] = (double)dv[i] * (double)w[i];
+    for (int i = 0; i < 16; ++i) {
+      dp[i] = dv[i] * w[i];
+      de[i] = fmaf(dv[i], w[i], -dp[i]);
+    }
     int idx;
-    const double sum = warp_reduce16(dot, lane, &idx);
+    const double sum = warp_reduce16_f(dp, de, lane, &idx);
     if ((lane & 1) == 0) tl.red[ew][c0 + idx] = sum;
   }
 }
