@@ -3,7 +3,13 @@
 // NW warps per CTA doing it (one per SMSP when 4), 148 CTAs.
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/dmma_test tools/dmma_test.cu
 #include <cstdio>
-template <int NACC, bool CVT>
+#include <cstdint>
+__device__ __forceinline__ double f2d_int(float x) {
+  const uint32_t u = __float_as_uint(x), m = u & 0x7fffffffu, s = u & 0x80000000u;
+  const uint32_t hi = m ? (s | ((m >> 3) + 0x38000000u)) : s;
+  return __hiloint2double((int)hi, (int)(m << 29));
+}
+template <int NACC, int CVT>
 __global__ void k(int iters, int nw, float *src, unsigned long long *out) {
   const int w = threadIdx.x >> 5;
   double acc[NACC][2];
@@ -17,7 +23,7 @@ __global__ void k(int iters, int nw, float *src, unsigned long long *out) {
     for (int it = 0; it < iters; ++it) {
 #pragma unroll
       for (int i = 0; i < NACC; ++i) {
-        const double a = CVT ? (double)fa[i] : da[i];
+        const double a = CVT == 2 ? f2d_int(fa[i]) : CVT == 1 ? (double)fa[i] : da[i];
         asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                      : "+d"(acc[i][0]), "+d"(acc[i][1]) : "d"(a), "d"(b));
       }
@@ -31,7 +37,7 @@ __global__ void k(int iters, int nw, float *src, unsigned long long *out) {
   if (s == 1.2345) src[0] = 0;
   if (threadIdx.x == 0) out[blockIdx.x] = c1 - c0;
 }
-template <int NACC, bool CVT>
+template <int NACC, int CVT>
 void run(int nw) {
   float *src;
   unsigned long long *out, h[148];
@@ -47,7 +53,7 @@ void run(int nw) {
 }
 int main() {
   for (int nw : {1, 4, 8}) {
-    run<4, false>(nw); run<4, true>(nw); run<8, false>(nw); run<8, true>(nw);
+    run<4, 0>(nw); run<4, 1>(nw); run<4, 2>(nw); run<8, 0>(nw); run<8, 1>(nw); run<8, 2>(nw);
   }
   return 0;
 }
