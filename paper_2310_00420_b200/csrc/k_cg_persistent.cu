@@ -21,14 +21,17 @@
 //   warp 1     MMA issuer: tcgen05.mma kind::tf32 with A in TMEM, tcgen05.commit frees stages / tiles
 //   warps 2-5  the A warps (one per TMEM lane quarter; warp 2 also owns TMEM): split every staged
 //              fp32 A tile into the exact tf32 pair hi + lo and write it to a TMEM A stage
-//              (tcgen05.st), then the fp64 mean columns' DMMA on the same fp32 tile
-//   warps 6-9  the epilogue (TMEM → registers → U / W, dᵀAd partials), overlapping the next tile's
-//              K loop when the accumulators are double-buffered in TMEM
+//              (tcgen05.st)
+//   warps 6-9  the epilogue: the fp64 mean columns' DMMA on the staged fp32 tiles during a unit's
+//              K loop (the FP64 pipe of each SM sub-partition, beside the A warps' split), then the
+//              unit's outputs (TMEM → registers → U / W, dᵀAd partials); with double-buffered TMEM
+//              accumulators the MMAs of the next unit run while the epilogue drains
 // All operands arrive by TMA into an S-stage ring of 128-byte-swizzled K-major smem tiles, so no
 // CTA-wide barrier runs inside a K loop; the producer runs ahead into the next unit while the
 // epilogue of the previous one drains.  mbarriers: full[s] (TMA bytes), empty[s] (MMA done and the
-// four A warps done with the stage), afull[a] / aempty[a] (TMEM A stage written / consumed by the
-// MMAs), tfull / tempty (accumulator handshake).
+// four A warps done with the stage), mdone[s] (the epilogue warps' fp64 work on a mean chunk done),
+// afull[a] / aempty[a] (TMEM A stage written / consumed by the MMAs), tfull / tempty (accumulator
+// handshake).
 //
 // The A operands (Φ itself and its transpose) live in HBM as plain fp32 and arrive by TMA; the A
 // warps split each staged tile into hi = tf32(x), lo = x − hi straight into tensor memory, so the
@@ -68,11 +71,11 @@ constexpr uint32_t A_BYTES = TM * 128;    // 16 KB fp32 A tile per ring stage
 constexpr int MAXST = 6;
 constexpr int MAXSA = 4;                  // TMEM A stages
 constexpr int NTHREADS = 320;
-constexpr int MEAN0 = 64;                 // first thread of the A (split + fp64 mean) warps 2-5
+constexpr int AW0 = 64;                   // first thread of the A (split) warps 2-5
 constexpr int EPI0 = 192;                 // first thread of the epilogue warps 6-9
 
 struct PSmemTail {
-  uint64_t full[MAXST], empty[MAXST];
+  uint64_t full[MAXST], empty[MAXST], mdone[MAXST];
   uint64_t afull[MAXSA], aempty[MAXSA];   // TMEM A stages: written by the A warps / read by the MMAs
   uint64_t tfull[2], tempty[2];      // TMEM accumulator buffers: MMA done / epilogue drained
   uint64_t dfull, dempty;             // the stage-2 epilogue's d tile (TMA bytes / epilogue done)
@@ -215,7 +218,8 @@ __device__ __forceinline__ int unit_nacc(const TcCfg &tc, int nk, int dbg) {
   return (nk <= 16 && !(dbg & 8)) ? 1 : min(tc.nacc, nk);
 }
 
-// issue the 3xTF32 MMAs of one K = 32 stage (one thread) into main accumulator q: A (hi | lo) from
+// issue the 3xTF32 MMAs of one K = 32 stage (the whole MMA warp, one elected lane issuing) into main
+// accumulator q: A (hi | lo) from
 // the TMEM A stage at column a_tm, B (hi, lo) from the shared-memory ring stage
 __device__ __forceinline__ void mma_stage(uint32_t tmem, uint32_t a_tm, unsigned char *base, uint32_t b_bytes,
                                           uint32_t idesc, int q, int slot, bool first_main, bool first_cross) {
@@ -226,9 +230,9 @@ __device__ __forceinline__ void mma_stage(uint32_t tmem, uint32_t a_tm, unsigned
   for (int k8 = 0; k8 < TK / 8; ++k8) {
     const uint64_t o = (uint64_t)(k8 * 32) >> 4;  // +32 bytes per K = 8 step inside the swizzled row
     const uint32_t ah = a_tm + 8 * k8, al = a_tm + 32 + 8 * k8;
-    mma_tf32_ts(tm_x, al, bh + o, idesc, (first_cross && k8 == 0) ? 0u : 1u);
-    mma_tf32_ts(tm_x, ah, bl + o, idesc, 1u);
-    mma_tf32_ts(tm_m, ah, bh + o, idesc, (first_main && k8 == 0) ? 0u : 1u);
+    mma_tf32_ts_warp(tm_x, al, bh + o, idesc, (first_cross && k8 == 0) ? 0u : 1u);
+    mma_tf32_ts_warp(tm_x, ah, bl + o, idesc, 1u);
+    mma_tf32_ts_warp(tm_m, ah, bh + o, idesc, (first_main && k8 == 0) ? 0u : 1u);
   }
 }
 
@@ -682,6 +686,8 @@ struct RingCtl {
   uint32_t ti;     // accumulator tiles handled so far
   uint32_t tuse[2];  // uses of each TMEM accumulator buffer (tfull / tempty phases)
   uint32_t di;     // stage-2 d tiles handled so far (dfull / dempty phases)
+  uint32_t smean;  // producer: bit s = the chunk last placed in slot s belongs to a mean unit
+  uint32_t mcnt[MAXST];  // producer: mean chunks placed in each slot (mdone phases)
 };
 
 // ---- producer (warp 0, one lane) ---------------------------------------------------------------
@@ -696,7 +702,16 @@ __device__ __forceinline__ void produce(const KParams &p, const TcMaps &mp, unsi
     const int st = rc.st;
     const uint32_t cph = rc.ph;
     rc.next();
-    if (G >= (uint32_t)rc.S) mbar_wait(&tl.empty[st], cph ^ 1u);   // chunk G − S (same slot) consumed
+    if (G >= (uint32_t)rc.S) {
+      mbar_wait(&tl.empty[st], cph ^ 1u);     // chunk G − S (same slot): MMAs and split done
+      if ((rc.smean >> st) & 1u) mbar_wait(&tl.mdone[st], (rc.mcnt[st] - 1) & 1);   // its fp64 work too
+    }
+    if (x.mean) {
+      rc.smean |= 1u << st;
+      rc.mcnt[st]++;
+    } else {
+      rc.smean &= ~(1u << st);
+    }
     if (tr && kc < 16) tr[kc] = clock64();
     unsigned char *base = sm + (size_t)st * p.tc.stage_bytes;
     uint64_t *fb = &tl.full[st];
@@ -758,10 +773,11 @@ __device__ __forceinline__ void produce(const KParams &p, const TcMaps &mp, unsi
   }
 }
 
-// ---- MMA issuer (warp 1, one lane) ---------------------------------------------------------------
+// ---- MMA issuer (warp 1, converged; one elected lane issues) ------------------------------------
 __device__ __forceinline__ void mma_unit(const KParams &p, unsigned char *sm, PSmemTail &tl, RingCtl &rc,
                                          uint32_t tmem, const Unit &x, unsigned long long *tr) {
   const TcCfg &tc = p.tc;
+  const int lane = threadIdx.x & 31;
   const uint32_t b_bytes = (uint32_t)tc.NT * 128;
   const int nacc = unit_nacc(tc, x.nk, p.dbg_flags);
   const uint32_t idesc = idesc_tf32(TM, x.nmma > 0 ? x.nmma : 16);
@@ -783,37 +799,39 @@ __device__ __forceinline__ void mma_unit(const KParams &p, unsigned char *sm, PS
       mbar_wait(&tl.afull[sa], rc.aph);       // A stage written (the A warps waited full[st] first)
       rc.nexta();
       mbar_wait(&tl.full[st], ph);            // B staged
-      if (tr && kc < 16) tr[32 + kc] = clock64();
+      if (tr && kc < 16 && lane == 0) tr[32 + kc] = clock64();
       if (!(p.dbg_flags & 2)) {
         fence_after_sync();
         const int q = (kc * nacc) / x.nk;
         const int qfirst = (q * x.nk + nacc - 1) / nacc;
         mma_stage(tacc, tmem + (uint32_t)(tc.acol0 + 64 * sa), sm + (size_t)st * tc.stage_bytes, b_bytes, idesc,
                   q, tc.slot, kc == qfirst, kc == 0);
-        mma_commit(&tl.aempty[sa]);           // the MMAs have read the A stage
-        mma_commit(&tl.empty[st]);            // ... and the B tiles
-      } else {
+        mma_commit_warp(&tl.aempty[sa]);      // the MMAs have read the A stage
+        mma_commit_warp(&tl.empty[st]);       // ... and the B tiles
+      } else if (lane == 0) {
         mbar_arrive(&tl.aempty[sa]);
         mbar_arrive(&tl.empty[st]);
       }
-    } else {
+    } else if (lane == 0) {
       mbar_arrive(&tl.empty[st]);             // the A warps' arrivals complete the stage
     }
+    __syncwarp();
   }
   if (x.nmma) {
-    if (p.dbg_flags & 2) mbar_arrive(&tl.tfull[bi]);
-    else mma_commit(&tl.tfull[bi]);          // all MMAs of the tile complete → accumulator ready
+    if (p.dbg_flags & 2) {
+      if (lane == 0) mbar_arrive(&tl.tfull[bi]);
+    } else {
+      mma_commit_warp(&tl.tfull[bi]);        // all MMAs of the tile complete → accumulator ready
+    }
     rc.tuse[bi]++;
     rc.ti++;
   }
 }
 
-// named barriers: 1 = A warps (2-5), 2 = epilogue warps (6-9), 3 = both groups (256 threads)
-__device__ __forceinline__ void mean_sync() { asm volatile("bar.sync 1, 128;\n" ::: "memory"); }
-__device__ __forceinline__ void pair_sync() { asm volatile("bar.sync 3, 256;\n" ::: "memory"); }
+// named barrier 2: the epilogue warps (6-9)
 
-// Split-K handoff of a stage-1 tile (S1 > 1), called by the mean and the epilogue warps together
-// (256 threads) once this CTA's partial tile is written; returns the rows [rb, re) of the tile
+// Split-K handoff of a stage-1 tile (S1 > 1), called by the epilogue warps once this CTA's partial
+// tiles (probe and mean columns) are written; returns the rows [rb, re) of the tile
 // this CTA sums over the S1 partials, in split order (deterministic):
 //  * cooperative (all stage-1 units co-resident, small configs): every split CTA waits on the tile
 //    counter for all S1 partials and reduces its 1/S1 share of the rows;
@@ -823,7 +841,7 @@ __device__ __forceinline__ void pair_sync() { asm volatile("bar.sync 3, 256;\n" 
 __device__ __forceinline__ void split_handoff(const KParams &p, const Unit &x, PSmemTail &tl, int *rb, int *re) {
   const Dims &d = p.d;
   __threadfence();
-  pair_sync();
+  epi_sync();
   int *cnt = p.b.tilecnt + ((size_t)x.t * d.nCT + x.ct) * d.nRT1 + x.rt;
   if (threadIdx.x == EPI0) {
     const int ticket = atomicAdd(cnt, 1);
@@ -837,7 +855,7 @@ __device__ __forceinline__ void split_handoff(const KParams &p, const Unit &x, P
     tl.last = (ticket % d.S1) == d.S1 - 1;
     asm volatile("fence.acq_rel.gpu;\n" ::: "memory");
   }
-  pair_sync();
+  epi_sync();
   const int n0 = x.rt * TM, rows = min(TM, d.N - n0);
   if (d.split_coop) {
     const int rs = ((rows + d.S1 - 1) / d.S1 + 3) & ~3;     // rows per share (×4: float4 rows)
@@ -849,121 +867,71 @@ __device__ __forceinline__ void split_handoff(const KParams &p, const Unit &x, P
   }
 }
 
-// ---- A warps (2-5): the TMEM A stages, and the fp64 mean columns on the FP64 tensor path -------
-template <int CC>
-__device__ void mean_unit(const KParams &p, unsigned char *sm, PSmemTail &tl, RingCtl &rc, uint32_t tmem,
-                          const Unit &x, unsigned long long *tr) {
-  const Dims &d = p.d;
+// ---- A warps (2-5): the TMEM A stages ------------------------------------------------------------
+__device__ void a_unit(const KParams &p, unsigned char *sm, PSmemTail &tl, RingCtl &rc, uint32_t tmem, const Unit &x,
+                       unsigned long long *tr, unsigned long long *tr4) {
   const TcCfg &tc = p.tc;
-  const int mt0 = threadIdx.x - MEAN0, mw = (threadIdx.x >> 5) & 3, lane = threadIdx.x & 31;
-  const int N = d.N, D = d.D, C = d.C;
-  const uint32_t b_bytes = (uint32_t)tc.NT * 128;
-  const uint32_t mu_off = A_BYTES + 2 * b_bytes;
-  const uint32_t ta_lane = tmem + ((uint32_t)(32 * mw) << 16) + (uint32_t)tc.acol0;
-  constexpr int NTC = (CC + 7) / 8;         // 8-column fp64 MMA tiles covering the C mean columns
-  double macc[4][NTC][2];
-#pragma unroll
-  for (int mt = 0; mt < 4; ++mt)
-#pragma unroll
-    for (int nt = 0; nt < NTC; ++nt) macc[mt][nt][0] = macc[mt][nt][1] = 0.0;
-  const int fg = lane >> 2, fq = lane & 3;   // fragment row group / column pair of this lane
-  // every chunk: its A tile → TMEM A stage (when the unit has probe MMAs), then the fp64 mean
-  // columns' DMMA on the same fp32 tile; the ring stage is released (empty) after both
+  const int aq = (threadIdx.x >> 5) & 3, lane = threadIdx.x & 31;   // TMEM lane quarter of this warp
+  const uint32_t ta_lane = tmem + ((uint32_t)(32 * aq) << 16) + (uint32_t)tc.acol0;
   for (int kc = 0; kc < x.nk; ++kc) {
     const int st = rc.st;
     mbar_wait(&tl.full[st], rc.ph);
     rc.next();
     if (tr && kc < 16) tr[48 + kc] = clock64();
-    const uint32_t base = smem_u32(sm) + (uint32_t)st * tc.stage_bytes;
     if (x.nmma) {
+      const uint32_t base = smem_u32(sm) + (uint32_t)st * tc.stage_bytes;
       const int sa = rc.ast;
       if (rc.ag >= (uint32_t)rc.SA) mbar_wait(&tl.aempty[sa], rc.aph ^ 1u);   // MMAs of chunk − SA done
       rc.nexta();
       if (tr && kc < 16) tr[64 + kc] = clock64();
       fence_after_sync();
-      if (!(p.dbg_flags & 4)) split_row_tmem(base, ta_lane + (uint32_t)(64 * sa), 32 * mw + lane);
+      if (!(p.dbg_flags & 4)) split_row_tmem(base, ta_lane + (uint32_t)(64 * sa), 32 * aq + lane);
       tmem_wait_st();
       fence_before_sync();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tl.afull[sa]);
       if (tr && kc < 16) tr[90 + kc] = clock64();
-    }
-    if (x.mean && !(p.dbg_flags & 1)) {
-      if (x.stage == 1) mean_stage<true, NTC>(base, base + mu_off, mw, lane, C, d.Cp, macc);
-      else mean_stage<false, NTC>(base, base + mu_off, mw, lane, C, d.Cp, macc);
+      if (tr4 && lane == 0 && kc < 16) tr4[16 * aq + kc] = clock64();
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&tl.empty[st]);
     if (tr && kc < 14) tr[106 + kc] = clock64();
   }
-  if (x.stage == 1) {
-    if (x.mean) {
-      double *dst = d.S1 == 1 ? p.b.Um + (size_t)x.t * N * d.Cp
-                              : p.b.Umpart + ((size_t)x.t * d.S1 + x.sp) * N * d.Cp;
-#pragma unroll
-      for (int mt = 0; mt < 4; ++mt) {
-        const int nn = x.rt * TM + 32 * mw + 8 * mt + fg;
-#pragma unroll
-        for (int nt = 0; nt < NTC; ++nt) {
-          const int c = 8 * nt + 2 * fq;       // Cp is even: columns c, c+1 are both < Cp or both ≥ C
-          if (nn < N && c < C) stv(reinterpret_cast<double2 *>(dst + (size_t)nn * d.Cp + c),
-                                   make_double2(macc[mt][nt][0], macc[mt][nt][1]));
-        }
-      }
-    }
-    if (d.S1 > 1) {
-      int rb, re;
-      split_handoff(p, x, tl, &rb, &re);
-      if (x.mean && re > rb) {
-        const int n0 = x.rt * TM;
-        const int nm = (re - rb) * d.Cp / 2;   // double2 elements of this share of Um
-        const double *mbase = p.b.Umpart + (size_t)x.t * d.S1 * N * d.Cp;
-        for (int e = mt0; e < nm; e += 128) {
-          const size_t o = (size_t)(n0 + rb) * d.Cp + 2 * e;
-          double2 v = make_double2(0.0, 0.0);
-          for (int sidx = 0; sidx < d.S1; ++sidx) {
-            const double2 pv = __ldcg(reinterpret_cast<const double2 *>(mbase + (size_t)sidx * N * d.Cp + o));
-            v.x += pv.x;
-            v.y += pv.y;
-          }
-          *reinterpret_cast<double2 *>(p.b.Um + (size_t)x.t * N * d.Cp + o) = v;
-        }
-      }
-    }
-    return;
-  }
-  if (!x.mean) return;
-  // stage 2: Wm = β·acc + α ⊙ dm on this lane's fragment rows / columns, and the partial dᵀWm per
-  // column over the tile (fragment rows, the 8 row groups of the warp, then the 4 warps)
-#pragma unroll
-  for (int nt = 0; nt < NTC; ++nt) {
-#pragma unroll
-    for (int e = 0; e < 2; ++e) {
-      const int c = 8 * nt + 2 * fq + e;
-      double dot = 0.0;
-#pragma unroll
-      for (int mt = 0; mt < 4; ++mt) {
-        const int de = x.rt * TM + 32 * mw + 8 * mt + fg;
-        if (c < C && de < D) {
-          const size_t o = ((size_t)x.t * C + c) * D + de;
-          const double dmv = ldv(p.b.Dm + o);
-          const double wv = fma(p.beta, macc[mt][nt][e], p.b.alpha64[(size_t)c * D + de] * dmv);
-          stv(p.b.Wm + o, wv);
-          dot = fma(dmv, wv, dot);
-        }
-      }
-#pragma unroll
-      for (int o = 4; o < 32; o <<= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
-      if (fg == 0 && c < C) tl.redm[mw][c] = dot;
-    }
-  }
-  mean_sync();
-  if (mt0 < C)
-    stv(p.b.dAdm + ((size_t)x.t * C + mt0) * d.nRT2 + x.rt, tl.redm[0][mt0] + tl.redm[1][mt0] + tl.redm[2][mt0] + tl.redm[3][mt0]);
-  mean_sync();                                // tl.redm is reused by the next unit
 }
 
-// ---- epilogue warps (8-11): the probe columns' accumulator tile ------------------------------
+// ---- epilogue warps, K loop of a unit: the fp64 mean columns on the FP64 tensor path -----------
+// Only chunks of mean units are waited for and released (mdone; the producer refills a slot that
+// held a mean chunk only after mdone, so full's phase parity cannot alias); the ring position still
+// advances over every chunk.
+template <int NTC>
+__device__ __forceinline__ void mean_kloop(const KParams &p, unsigned char *sm, PSmemTail &tl, RingCtl &rc,
+                                           const Unit &x, double (&macc)[4][NTC][2], unsigned long long *trm) {
+  const TcCfg &tc = p.tc;
+  const int ew = (threadIdx.x >> 5) & 3, lane = threadIdx.x & 31;
+  const uint32_t mu_off = A_BYTES + 2 * (uint32_t)tc.NT * 128;
+#pragma unroll
+  for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < NTC; ++nt) macc[mt][nt][0] = macc[mt][nt][1] = 0.0;
+  for (int kc = 0; kc < x.nk; ++kc) {
+    const int st = rc.st;
+    const uint32_t ph = rc.ph;
+    rc.next();
+    if (x.mean) {
+      mbar_wait(&tl.full[st], ph);
+      if (!(p.dbg_flags & 1)) {
+        const uint32_t base = smem_u32(sm) + (uint32_t)st * tc.stage_bytes;
+        if (x.stage == 1) mean_stage<true, NTC>(base, base + mu_off, ew, lane, p.d.C, p.d.Cp, macc);
+        else mean_stage<false, NTC>(base, base + mu_off, ew, lane, p.d.C, p.d.Cp, macc);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tl.mdone[st]);
+      if (trm && threadIdx.x == EPI0 && kc < 16) trm[kc] = clock64();
+    }
+  }
+}
+
+// ---- epilogue warps (6-9): a unit's fp64 mean columns and its probe accumulator tile ----------
 // TMEM accumulator buffer of a tile: two buffers (columns [0, 2·slot) and [2·slot, 4·slot)) when
 // double-buffered, so the MMA warp starts the next tile while this one drains
 __device__ __forceinline__ int acc_buf(const RingCtl &rc, bool dbl) { return dbl ? (int)(rc.ti & 1) : 0; }
@@ -1054,6 +1022,54 @@ __device__ void probe_epilogue(const KParams &p, unsigned char *sm, PSmemTail &t
   }
   __syncwarp();
   const uint32_t *mask = tl.emask[ew];
+  // the fp64 mean columns' share of the K loop (DMMA on the staged tiles, beside the A warps' split)
+  constexpr int NTC = (CC + 7) / 8;
+  double macc[4][NTC][2];
+  mean_kloop<NTC>(p, sm, tl, rc, x, macc, tr ? tr + 224 : nullptr);
+  const int fg = lane >> 2, fq = lane & 3;   // DMMA fragment row group / column pair of this lane
+  if (x.stage == 1 && x.mean) {              // Um = Φ·Dm rows of this tile (or this split's partial)
+    double *dst = d.S1 == 1 ? p.b.Um + (size_t)x.t * N * d.Cp : p.b.Umpart + ((size_t)x.t * d.S1 + x.sp) * N * d.Cp;
+#pragma unroll
+    for (int mt = 0; mt < 4; ++mt) {
+      const int nn = x.rt * TM + 32 * ew + 8 * mt + fg;
+#pragma unroll
+      for (int nt = 0; nt < NTC; ++nt) {
+        const int c = 8 * nt + 2 * fq;         // Cp is even: columns c, c+1 are both < Cp or both ≥ C
+        if (nn < N && c < C)
+          stv(reinterpret_cast<double2 *>(dst + (size_t)nn * d.Cp + c), make_double2(macc[mt][nt][0], macc[mt][nt][1]));
+      }
+    }
+  }
+  if (x.stage == 2 && x.mean) {
+    // Wm = β·acc + α ⊙ dm on this lane's fragment rows / columns, and the partial dᵀWm per column
+    // over the tile (fragment rows, the 8 row groups of the warp, then the 4 warps)
+#pragma unroll
+    for (int nt = 0; nt < NTC; ++nt) {
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int c = 8 * nt + 2 * fq + e;
+        double dot = 0.0;
+#pragma unroll
+        for (int mt = 0; mt < 4; ++mt) {
+          const int de = x.rt * TM + 32 * ew + 8 * mt + fg;
+          if (c < C && de < D) {
+            const size_t o = ((size_t)x.t * C + c) * D + de;
+            const double dmv = ldv(p.b.Dm + o);
+            const double wv = fma(p.beta, macc[mt][nt][e], p.b.alpha64[(size_t)c * D + de] * dmv);
+            stv(p.b.Wm + o, wv);
+            dot = fma(dmv, wv, dot);
+          }
+        }
+#pragma unroll
+        for (int o = 4; o < 32; o <<= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
+        if (fg == 0 && c < C) tl.redm[ew][c] = dot;
+      }
+    }
+    epi_sync();
+    if (et < C)
+      stv(p.b.dAdm + ((size_t)x.t * C + et) * d.nRT2 + x.rt, tl.redm[0][et] + tl.redm[1][et] + tl.redm[2][et] + tl.redm[3][et]);
+    epi_sync();                               // tl.redm is reused by the next unit
+  }
   uint32_t tacc = tmem;                      // this tile's accumulator buffer
   // stage 2: α_c of this thread's row for every cluster (read-only during the E-step: the
   // non-coherent path), loaded while the accumulator is still being computed
@@ -1112,6 +1128,21 @@ __device__ void probe_epilogue(const KParams &p, unsigned char *sm, PSmemTail &t
     if (d.S1 > 1) {
       int rb, re;
       split_handoff(p, x, tl, &rb, &re);
+      if (x.mean && re > rb) {                 // Um: this CTA's share of the split partials
+        const int n0 = x.rt * TM;
+        const int nm = (re - rb) * d.Cp / 2;   // double2 elements of this share of Um
+        const double *mbase = p.b.Umpart + (size_t)x.t * d.S1 * N * d.Cp;
+        for (int e = et; e < nm; e += 128) {
+          const size_t o = (size_t)(n0 + rb) * d.Cp + 2 * e;
+          double2 v = make_double2(0.0, 0.0);
+          for (int sidx = 0; sidx < d.S1; ++sidx) {
+            const double2 pv = __ldcg(reinterpret_cast<const double2 *>(mbase + (size_t)sidx * N * d.Cp + o));
+            v.x += pv.x;
+            v.y += pv.y;
+          }
+          *reinterpret_cast<double2 *>(p.b.Um + (size_t)x.t * N * d.Cp + o) = v;
+        }
+      }
       if (x.nmma && re > rb) {
         const int n0 = x.rt * TM, r4n = (re - rb) >> 2;
         const size_t split = (size_t)d.Pp * N;
@@ -1270,6 +1301,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_cg_persistent(KParams p, const 
     for (int s = 0; s < tc.stages; ++s) {
       mbar_init(&tl.full[s], 1);
       mbar_init(&tl.empty[s], 5);             // the MMA warp's commit (or arrive) + the 4 A warps
+      mbar_init(&tl.mdone[s], 4);             // the 4 epilogue warps' fp64 work on a mean chunk
     }
     for (int s = 0; s < tc.sa; ++s) {
       mbar_init(&tl.afull[s], 4);
@@ -1293,13 +1325,13 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_cg_persistent(KParams p, const 
   __syncthreads();
   fence_after_sync();
   const uint32_t tmem = tl.tslot;
-  RingCtl rc{tc.stages, 0u, 0, 0u, tc.sa, 0u, 0, 0u, 0u, {0u, 0u}, 0u};
+  RingCtl rc{tc.stages, 0u, 0, 0u, tc.sa, 0u, 0, 0u, 0u, {0u, 0u}, 0u, 0u, {0u, 0u, 0u, 0u, 0u, 0u}};
   unsigned epoch = 0;
   unsigned *bar = p.b.gridbar;
   const int n1 = d.Tl * d.nCT * d.nRT1 * d.S1, n2 = d.Tl * d.nCT * d.nRT2;
   const int ncols = d.Tl * (d.P + d.C);
-  const bool producer = warp == 0 && lane == 0, issuer = warp == 1 && lane == 0;
-  const bool meanw = warp >= 2 && warp < 6, epi = warp >= 6;
+  const bool producer = warp == 0 && lane == 0, issuer = warp == 1;
+  const bool aw = warp >= 2 && warp < 6, epi = warp >= 6;
   const bool tile_role = true;
   for (int u = 0; u < d.cap; ++u) {
     if (b == 0 && tid == 0) p.b.ts[4 * u + 0] = globaltimer();
@@ -1316,7 +1348,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_cg_persistent(KParams p, const 
         if (!x.nmma && !x.mean) continue;
         if (producer) produce(p, mp, sm, tl, rc, x, tr1);
         else if (issuer) mma_unit(p, sm, tl, rc, tmem, x, tr1);
-        else if (meanw) mean_unit<CC>(p, sm, tl, rc, tmem, x, (tr1 && threadIdx.x == MEAN0) ? tr1 : nullptr);
+        else if (aw) a_unit(p, sm, tl, rc, tmem, x, (tr1 && threadIdx.x == AW0) ? tr1 : nullptr, nullptr);
         else if (epi) probe_epilogue<CC>(p, sm, tl, rc, tmem, x, mask, tr1);
       }
     }
@@ -1332,7 +1364,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_cg_persistent(KParams p, const 
         if (!x.nmma && !x.mean) continue;
         if (producer) produce(p, mp, sm, tl, rc, x, tr2);
         else if (issuer) mma_unit(p, sm, tl, rc, tmem, x, tr2);
-        else if (meanw) mean_unit<CC>(p, sm, tl, rc, tmem, x, (tr2 && threadIdx.x == MEAN0) ? tr2 : nullptr);
+        else if (aw) a_unit(p, sm, tl, rc, tmem, x, (tr2 && threadIdx.x == AW0) ? tr2 : nullptr, tr2 ? tr2 + 160 : nullptr);
         else if (epi) probe_epilogue<CC>(p, sm, tl, rc, tmem, x, mask, tr2);
       }
     }

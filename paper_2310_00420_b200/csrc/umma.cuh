@@ -100,6 +100,25 @@ __device__ __forceinline__ void mma_tf32_ts(uint32_t tmem_d, uint32_t tmem_a, ui
       "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate));
 }
 
+// The same two issued by one elected lane of a converged warp (all 32 lanes call it with the same
+// operands): the operands stay warp-uniform, so no per-instruction register → uniform-register
+// moves and elect loops (tools/mma_contention_test.cu: 480 vs 637 clk for 12 N = 80 MMAs)
+__device__ __forceinline__ void mma_tf32_ts_warp(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc,
+                                                 uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void mma_commit_warp(uint64_t *mbar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}\n" ::"r"(smem_u32(mbar))
+      : "memory");
+}
+
 // 16 consecutive 32-bit columns of this thread's TMEM lane (warp w writes lanes 32(w%4)..+31);
 // completion is awaited with tmem_wait_st()
 __device__ __forceinline__ void tmem_st16(uint32_t taddr, const float *v) {
