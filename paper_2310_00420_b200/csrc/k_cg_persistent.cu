@@ -690,10 +690,10 @@ struct RingCtl {
   uint32_t mcnt[MAXST];  // producer: mean chunks placed in each slot (mdone phases)
 };
 
-// ---- producer (warp 0, one lane) ---------------------------------------------------------------
+// ---- producer (warp 0, converged; one elected lane issues) ---------------------------------------------------------------
 __device__ __forceinline__ void produce(const KParams &p, const TcMaps &mp, unsigned char *sm, PSmemTail &tl,
                                         RingCtl &rc, const Unit &x, unsigned long long *tr) {
-  if (tr) tr[84] = clock64();
+  if (tr && (threadIdx.x & 31) == 0) tr[84] = clock64();
   const uint32_t b_bytes = (uint32_t)p.tc.NT * 128;
   const uint32_t mean_tx = x.stage == 1 ? (uint32_t)p.d.C * TK * 8 : (uint32_t)TK * p.d.Cp * 8;
   const uint32_t bytes = A_BYTES + (x.nmma ? 2 * b_bytes : 0) + (x.mean ? mean_tx : 0);
@@ -712,18 +712,18 @@ __device__ __forceinline__ void produce(const KParams &p, const TcMaps &mp, unsi
     } else {
       rc.smean &= ~(1u << st);
     }
-    if (tr && kc < 16) tr[kc] = clock64();
+    if (tr && kc < 16 && (threadIdx.x & 31) == 0) tr[kc] = clock64();
     unsigned char *base = sm + (size_t)st * p.tc.stage_bytes;
     uint64_t *fb = &tl.full[st];
     if (p.dbg_flags & 128) {                  // diagnostic: no operand traffic
-      mbar_arrive(fb);
+      if ((threadIdx.x & 31) == 0) mbar_arrive(fb);
       continue;
     }
-    mbar_arrive_expect_tx(fb, bytes);
+    mbar_arrive_expect_tx_warp(fb, bytes);
     const int k = x.k0 + kc * TK;
     // L2 prefetch PF chunks ahead: HBM latency is hidden beyond the depth of the smem ring
     const int kp = kc + p.tc.pf;
-    if (p.tc.pf && kp < x.nk) {
+    if (p.tc.pf && kp < x.nk && (threadIdx.x & 31) == 0) {
       const int kk = x.k0 + kp * TK;
       if (x.stage == 1) {
         tma_prefetch_2d(&mp.phi, kk, x.arow);
@@ -733,7 +733,7 @@ __device__ __forceinline__ void produce(const KParams &p, const TcMaps &mp, unsi
         if (x.nmma) tma_prefetch_2d(&mp.u_h, kk, x.brow);
       }
     }
-    if (kc == 0 && p.tc.pf) {                 // the first chunks of the unit
+    if (kc == 0 && p.tc.pf && (threadIdx.x & 31) == 0) {   // the first chunks of the unit
       for (int k2 = 1; k2 < min(p.tc.pf, x.nk); ++k2) {
         const int kk = x.k0 + k2 * TK;
         tma_prefetch_2d(x.stage == 1 ? &mp.phi : &mp.phit, kk, x.arow);
@@ -742,21 +742,21 @@ __device__ __forceinline__ void produce(const KParams &p, const TcMaps &mp, unsi
     }
     // stage layout: fp32 A tile | B hi | B lo | fp64 mean-column chunk
     if (x.stage == 1) {
-      tma_load_2d(base, &mp.phi, k, x.arow, fb);
+      tma_load_2d_warp(base, &mp.phi, k, x.arow, fb);
       if (x.nmma) {
-        tma_load_2d(base + A_BYTES, &mp.d_h, k, x.brow, fb);
-        tma_load_2d(base + A_BYTES + b_bytes, &mp.d_l, k, x.brow, fb);
+        tma_load_2d_warp(base + A_BYTES, &mp.d_h, k, x.brow, fb);
+        tma_load_2d_warp(base + A_BYTES + b_bytes, &mp.d_l, k, x.brow, fb);
       }
-      if (x.mean) tma_load_2d(base + A_BYTES + 2 * b_bytes, &mp.dm, k, x.t * p.d.C, fb);
+      if (x.mean) tma_load_2d_warp(base + A_BYTES + 2 * b_bytes, &mp.dm, k, x.t * p.d.C, fb);
     } else {
-      tma_load_2d(base, &mp.phit, k, x.arow, fb);
+      tma_load_2d_warp(base, &mp.phit, k, x.arow, fb);
       if (x.nmma) {
-        tma_load_2d(base + A_BYTES, &mp.u_h, k, x.brow, fb);
-        tma_load_2d(base + A_BYTES + b_bytes, &mp.u_l, k, x.brow, fb);
+        tma_load_2d_warp(base + A_BYTES, &mp.u_h, k, x.brow, fb);
+        tma_load_2d_warp(base + A_BYTES + b_bytes, &mp.u_l, k, x.brow, fb);
       }
-      if (x.mean) tma_load_2d(base + A_BYTES + 2 * b_bytes, &mp.um, 0, x.t * p.d.N + k, fb);
+      if (x.mean) tma_load_2d_warp(base + A_BYTES + 2 * b_bytes, &mp.um, 0, x.t * p.d.N + k, fb);
     }
-    if (tr && kc < 16) tr[16 + kc] = clock64();
+    if (tr && kc < 16 && (threadIdx.x & 31) == 0) tr[16 + kc] = clock64();
   }
   if (x.stage == 2 && x.nmma && p.tc.use_dtile) {
     // the epilogue's d tile (rows d0..d0+127 of the tile's NT direction columns), after the K loop
@@ -764,10 +764,10 @@ __device__ __forceinline__ void produce(const KParams &p, const TcMaps &mp, unsi
     if (rc.di > 0) mbar_wait(&tl.dempty, (rc.di - 1) & 1);
     unsigned char *dt = sm + (size_t)rc.S * p.tc.stage_bytes;
     if (p.dbg_flags & 128) {
-      mbar_arrive(&tl.dfull);
+      if ((threadIdx.x & 31) == 0) mbar_arrive(&tl.dfull);
     } else {
-      mbar_arrive_expect_tx(&tl.dfull, p.tc.dtile_bytes);
-      tma_load_2d(dt, &mp.d32, x.rt * TM, x.t * p.d.P + x.ct * p.tc.NT, &tl.dfull);
+      mbar_arrive_expect_tx_warp(&tl.dfull, p.tc.dtile_bytes);
+      tma_load_2d_warp(dt, &mp.d32, x.rt * TM, x.t * p.d.P + x.ct * p.tc.NT, &tl.dfull);
     }
     rc.di++;
   }
@@ -1330,7 +1330,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_cg_persistent(KParams p, const 
   unsigned *bar = p.b.gridbar;
   const int n1 = d.Tl * d.nCT * d.nRT1 * d.S1, n2 = d.Tl * d.nCT * d.nRT2;
   const int ncols = d.Tl * (d.P + d.C);
-  const bool producer = warp == 0 && lane == 0, issuer = warp == 1;
+  const bool producer = warp == 0, issuer = warp == 1;
   const bool aw = warp >= 2 && warp < 6, epi = warp >= 6;
   const bool tile_role = true;
   for (int u = 0; u < d.cap; ++u) {
