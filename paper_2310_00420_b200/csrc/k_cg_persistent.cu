@@ -317,23 +317,29 @@ template <bool B_CK, int NTC>
 __device__ __forceinline__ void mean_stage(uint32_t a32, uint32_t mb, int ew, int lane, int C, int Cp,
                                            double (&acc)[4][NTC][2]) {
   const int g = lane >> 2, q = lane & 3;
+  // all shared-memory operands of the stage first (32 A values, 8·NTC B values per lane), so the
+  // FP64 pipe (F2F + DMMA, the binding resource of the mean columns) runs without load gaps
+  float af[TK / 4][4];
+  double bf[TK / 4][NTC];
 #pragma unroll
   for (int ks = 0; ks < TK / 4; ++ks) {
     const int k = 4 * ks + q;
-    double bf[NTC];
 #pragma unroll
     for (int nt = 0; nt < NTC; ++nt) {
       const int n = 8 * nt + g;
-      bf[nt] = (n < C) ? lds_d(mb + (uint32_t)(B_CK ? n * TK + k : k * Cp + n) * 8) : 0.0;
+      bf[ks][nt] = (n < C) ? lds_d(mb + (uint32_t)(B_CK ? n * TK + k : k * Cp + n) * 8) : 0.0;
     }
+#pragma unroll
+    for (int mt = 0; mt < 4; ++mt) af[ks][mt] = lds_f32(a32 + sw128_offset(32 * ew + 8 * mt + g, ks) + (uint32_t)q * 4);
+  }
+#pragma unroll
+  for (int ks = 0; ks < TK / 4; ++ks)
 #pragma unroll
     for (int mt = 0; mt < 4; ++mt) {
-      const uint32_t off = sw128_offset(32 * ew + 8 * mt + g, ks) + (uint32_t)q * 4;
-      const double a = (double)lds_f32(a32 + off);
+      const double a = (double)af[ks][mt];
 #pragma unroll
-      for (int nt = 0; nt < NTC; ++nt) dmma(acc[mt][nt], a, bf[nt]);
+      for (int nt = 0; nt < NTC; ++nt) dmma(acc[mt][nt], a, bf[ks][nt]);
     }
-  }
 }
 
 // tf32 rounding to nearest (ties away from zero, = cvt.rna.tf32.f32 for finite x) on the integer pipe
