@@ -80,6 +80,7 @@ struct PSmemTail {
   uint64_t tfull[2], tempty[2];      // TMEM accumulator buffers: MMA done / epilogue drained
   uint64_t dfull, dempty;             // the stage-2 epilogue's d tile (TMA bytes / epilogue done)
   uint32_t tslot;
+  uint32_t help_tacc;                 // the accumulator buffer of a tile drained by A + epilogue warps
   int last;                           // split-K: this CTA reduces the tile (last-arriver mode)
   uint32_t emask[4][TC_NTMAX / 32];   // per epilogue warp: active-column mask of its current tile
   double red[4][TC_NTMAX];            // per epilogue warp: dᵀAd partials of the probe columns
@@ -106,6 +107,8 @@ __device__ __forceinline__ void mbar_arrive(uint64_t *mbar) {
 }
 // named barrier among the 4 epilogue warps
 __device__ __forceinline__ void epi_sync() { asm volatile("bar.sync 2, 128;\n" ::: "memory"); }
+// named barrier among the A warps and the epilogue warps (a CTA's last stage-2 tile, drained by both)
+__device__ __forceinline__ void pair_sync() { asm volatile("bar.sync 3, 256;\n" ::: "memory"); }
 
 // grid-wide barrier over the co-resident CTAs: a monotonically increasing arrival counter
 // (reset to 0 before every launch); epoch e completes when the counter reaches e·gridDim.x
@@ -948,7 +951,8 @@ __device__ __forceinline__ int acc_buf(const RingCtl &rc, bool dbl) { return dbl
 // last tile with the A warps does not pay — they join only after their own mean epilogue.)
 template <int CC>
 __device__ __forceinline__ void drain2_groups(const KParams &p, PSmemTail &tl, const Unit &x, uint32_t tacc,
-                                              int nacc, const float *dtile, const float (&alpha)[CC]) {
+                                              int nacc, const float *dtile, const float (&alpha)[CC], int g0,
+                                              int gstep) {
   const Dims &d = p.d;
   const TcCfg &tc = p.tc;
   const int ew = (threadIdx.x >> 5) & 3, lane = threadIdx.x & 31, r = 32 * ew + lane;
@@ -959,7 +963,7 @@ __device__ __forceinline__ void drain2_groups(const KParams &p, PSmemTail &tl, c
   const float betaf = (float)p.beta;
   const float *__restrict__ arow = p.b.alpha32 + dd;
   float *__restrict__ Wc = p.b.W + ((size_t)x.t * d.P + j0) * D + dd;
-  for (int c0 = 0; c0 < x.nmma; c0 += 16) {
+  for (int c0 = 16 * g0; c0 < x.nmma; c0 += 16 * gstep) {
     float dv[16], tot[16], a[16], w[16];
 #pragma unroll
     for (int i = 0; i < 16; ++i) dv[i] = rv ? dtile[(c0 + i) * TM + r] : 0.f;
@@ -1007,9 +1011,25 @@ __device__ __forceinline__ void drain2_groups(const KParams &p, PSmemTail &tl, c
   }
 }
 
+// A warps: the odd column groups of a CTA's last stage-2 tile of the phase (the A warps are idle
+// once its K loop is split; the epilogue warps take the even groups after their fp64 mean work)
+template <int CC>
+__device__ void a_help_drain2(const KParams &p, unsigned char *sm, PSmemTail &tl, const RingCtl &rc, const Unit &x) {
+  const Dims &d = p.d;
+  const TcCfg &tc = p.tc;
+  float alpha[CC];
+  const int dd = x.rt * TM + 32 * ((threadIdx.x >> 5) & 3) + (threadIdx.x & 31);
+#pragma unroll
+  for (int c = 0; c < CC; ++c) alpha[c] = (c < d.C && dd < d.D) ? __ldg(p.b.alpha32 + (size_t)c * d.D + dd) : 0.f;
+  pair_sync();
+  drain2_groups<CC>(p, tl, x, tl.help_tacc, unit_nacc(tc, x.nk, p.dbg_flags),
+                    reinterpret_cast<const float *>(sm + (size_t)rc.S * tc.stage_bytes), alpha, 1, 2);
+  pair_sync();
+}
+
 template <int CC>
 __device__ void probe_epilogue(const KParams &p, unsigned char *sm, PSmemTail &tl, RingCtl &rc, uint32_t tmem,
-                               const Unit &x, const uint32_t *mask_in, unsigned long long *tr) {
+                               const Unit &x, const uint32_t *mask_in, unsigned long long *tr, bool helped) {
   if (tr && threadIdx.x != EPI0) tr = nullptr;
   const Dims &d = p.d;
   const TcCfg &tc = p.tc;
@@ -1251,7 +1271,14 @@ __device__ void probe_epilogue(const KParams &p, unsigned char *sm, PSmemTail &t
   if (p.dbg_flags & 64) {
     // diagnostic: accumulator not drained
   } else if (dts) {
-    drain2_groups<CC>(p, tl, x, tacc, nacc, dtile, alpha);
+    if (helped) {                             // the A warps take every other column group
+      if (threadIdx.x == EPI0) tl.help_tacc = tacc;
+      pair_sync();
+      drain2_groups<CC>(p, tl, x, tacc, nacc, dtile, alpha, 0, 2);
+      pair_sync();
+    } else {
+      drain2_groups<CC>(p, tl, x, tacc, nacc, dtile, alpha, 0, 1);
+    }
   } else {
     // global loads of d: the next group's are issued while the current one is processed
     float dnx[16];
@@ -1339,6 +1366,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_cg_persistent(KParams p, const 
   const bool producer = warp == 0, issuer = warp == 1;
   const bool aw = warp >= 2 && warp < 6, epi = warp >= 6;
   const bool tile_role = true;
+  // the A warps help drain a CTA's last stage-2 tile (the d tile path; not under diagnostics)
+  const bool help2 = tc.use_dtile && !(p.dbg_flags & 64);
   for (int u = 0; u < d.cap; ++u) {
     if (b == 0 && tid == 0) p.b.ts[4 * u + 0] = globaltimer();
     // diagnostic trace of CTA 0's first unit of each phase at CG step 5 (CMTCS_PHASE_LOG)
@@ -1355,7 +1384,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_cg_persistent(KParams p, const 
         if (producer) produce(p, mp, sm, tl, rc, x, tr1);
         else if (issuer) mma_unit(p, sm, tl, rc, tmem, x, tr1);
         else if (aw) a_unit(p, sm, tl, rc, tmem, x, (tr1 && threadIdx.x == AW0) ? tr1 : nullptr, nullptr);
-        else if (epi) probe_epilogue<CC>(p, sm, tl, rc, tmem, x, mask, tr1);
+        else if (epi) probe_epilogue<CC>(p, sm, tl, rc, tmem, x, mask, tr1, false);
       }
     }
     grid_sync(bar, epoch);
@@ -1370,8 +1399,11 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_cg_persistent(KParams p, const 
         if (!x.nmma && !x.mean) continue;
         if (producer) produce(p, mp, sm, tl, rc, x, tr2);
         else if (issuer) mma_unit(p, sm, tl, rc, tmem, x, tr2);
-        else if (aw) a_unit(p, sm, tl, rc, tmem, x, (tr2 && threadIdx.x == AW0) ? tr2 : nullptr, tr2 ? tr2 + 160 : nullptr);
-        else if (epi) probe_epilogue<CC>(p, sm, tl, rc, tmem, x, mask, tr2);
+        else if (aw) {
+          a_unit(p, sm, tl, rc, tmem, x, (tr2 && threadIdx.x == AW0) ? tr2 : nullptr, tr2 ? tr2 + 160 : nullptr);
+          if (help2 && w + G >= n2 && x.nmma) a_help_drain2<CC>(p, sm, tl, rc, x);
+        }
+        else if (epi) probe_epilogue<CC>(p, sm, tl, rc, tmem, x, mask, tr2, help2 && w + G >= n2);
       }
     }
     grid_sync(bar, epoch);
