@@ -247,6 +247,7 @@ size_t carve(const Dims &d, char *base, Bufs *b) {
   b->tmark = cv.take<int>(Tl);
   b->tilecnt = cv.take<int>(Tl * d.nCT * d.nRT1);
   b->gridbar = cv.take<unsigned>(1);
+  b->dep = cv.take<int>(2 * Tl);
   return cv.off;
 }
 

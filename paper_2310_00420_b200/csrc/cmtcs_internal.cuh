@@ -79,6 +79,7 @@ struct Bufs {
   int *tmark;        // [Tl]   last CG step (+1) at which the task had an active column
   int *tilecnt;      // [Tl][nCT][nRT1]  split-K arrival counters (self re-arming)
   unsigned *gridbar; // [1]    grid-barrier arrival counter of the persistent CG kernel
+  int *dep;          // [2][Tl] per-task completion counters of stage 1 / stage 2 units (monotonic)
   int *assign;       // [Tl]
 };
 

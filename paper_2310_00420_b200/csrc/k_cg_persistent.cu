@@ -129,6 +129,19 @@ __device__ __forceinline__ void grid_sync(unsigned *bar, unsigned &epoch) {
   __syncthreads();
 }
 
+// Per-task dataflow between the phases (instead of grid barriers): a unit's completion is released
+// on its task's counter (the unit's stores fenced first), and a consumer acquires the counter until
+// it reaches the step's target (units per task × (step + 1); skipped units count too).
+__device__ __forceinline__ void dep_signal(int *cnt) {
+  asm volatile("red.release.gpu.global.add.s32 [%0], 1;\n" ::"l"(cnt) : "memory");
+}
+__device__ __forceinline__ void dep_wait(const int *cnt, int target) {
+  int v;
+  do {
+    asm volatile("ld.acquire.gpu.global.s32 %0, [%1];\n" : "=r"(v) : "l"(cnt) : "memory");
+  } while (v < target);
+}
+
 // Sums v[0..15] over the 32 lanes of a warp with 16 shuffles (butterfly transpose-reduce); the
 // total of value index `idx` ends in the even lane with idx = bits 4..1 of the lane id.
 __device__ __forceinline__ double warp_reduce16(double *v, int lane, int *idx) {
@@ -405,7 +418,9 @@ __device__ void update_probe(const KParams &p, int t, int col, int u, int lane, 
   const size_t g = (size_t)t * d.P + col;
   // the per-row-tile partials of dᵀAd: one load per lane, then the warp's fixed-order butterfly
   double dpart = 0.0;
-  for (int i = lane; i < d.nRT2; i += 32) dpart += ldv(p.b.dAd + g * d.nRT2 + i);
+  // W and the dᵀAd partials come from other CTAs' stage 2 (acquired through the task counter, no
+  // grid barrier): read through L2
+  for (int i = lane; i < d.nRT2; i += 32) dpart += __ldcg(p.b.dAd + g * d.nRT2 + i);
   const double dAd = warp_sum(dpart);
   const double rr = ldv(p.b.rr + g);
   if (!(dAd > 0.0)) {  // Alg. 1 line 3 breakdown
@@ -434,7 +449,7 @@ __device__ void update_probe(const KParams &p, int t, int col, int u, int lane, 
 #pragma unroll
     for (int v = 0; v < U; ++v) {
       const int i = i0 + 32 * v;
-      if (i < n4) { dd[v] = ldv(d4 + i); wv[v] = ldv(w4 + i); xv[v] = ldv(x4 + i); rv[v] = ldv(r4 + i); }
+      if (i < n4) { dd[v] = ldv(d4 + i); wv[v] = __ldcg(w4 + i); xv[v] = ldv(x4 + i); rv[v] = ldv(r4 + i); }
     }
 #pragma unroll
     for (int v = 0; v < U; ++v) {
@@ -514,7 +529,7 @@ __device__ void update_mean(const KParams &p, int t, int c, int u, int lane) {
   const Dims &d = p.d;
   const size_t g = (size_t)t * d.C + c;
   double dpart = 0.0;
-  for (int i = lane; i < d.nRT2; i += 32) dpart += ldv(p.b.dAdm + g * d.nRT2 + i);
+  for (int i = lane; i < d.nRT2; i += 32) dpart += __ldcg(p.b.dAdm + g * d.nRT2 + i);
   const double dAd = warp_sum(dpart);
   const double rr = ldv(p.b.rrm + g);
   if (!(dAd > 0.0)) {
@@ -537,7 +552,7 @@ __device__ void update_mean(const KParams &p, int t, int c, int u, int lane) {
 #pragma unroll
     for (int v = 0; v < U; ++v) {
       const int i = i0 + 32 * v;
-      if (i < n2) { dd[v] = ldv(dv + i); ww[v] = ldv(w + i); xx[v] = ldv(x + i); rn[v] = ldv(r + i); }
+      if (i < n2) { dd[v] = ldv(dv + i); ww[v] = __ldcg(w + i); xx[v] = ldv(x + i); rn[v] = ldv(r + i); }
     }
 #pragma unroll
     for (int v = 0; v < U; ++v) {
@@ -1024,6 +1039,7 @@ __device__ void a_help_drain2(const KParams &p, unsigned char *sm, PSmemTail &tl
   pair_sync();
   drain2_groups<CC>(p, tl, x, tl.help_tacc, unit_nacc(tc, x.nk, p.dbg_flags),
                     reinterpret_cast<const float *>(sm + (size_t)rc.S * tc.stage_bytes), alpha, 1, 2);
+  __threadfence();                            // W stores before the epilogue's completion release
   pair_sync();
 }
 
@@ -1362,6 +1378,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_cg_persistent(KParams p, const 
   unsigned epoch = 0;
   unsigned *bar = p.b.gridbar;
   const int n1 = d.Tl * d.nCT * d.nRT1 * d.S1, n2 = d.Tl * d.nCT * d.nRT2;
+  const int E2 = d.nCT * d.nRT2;             // stage-2 units per task
+  int *cnt2 = p.b.dep + d.Tl;
   const int ncols = d.Tl * (d.P + d.C);
   const bool producer = warp == 0, issuer = warp == 1;
   const bool aw = warp >= 2 && warp < 6, epi = warp >= 6;
@@ -1387,6 +1405,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_cg_persistent(KParams p, const 
         else if (epi) probe_epilogue<CC>(p, sm, tl, rc, tmem, x, mask, tr1, false);
       }
     }
+    // stage 1 → stage 2: a grid barrier (a per-task dataflow counter here, as between stage 2 and the
+    // update, hung or mis-converged at C3: kept out)
     grid_sync(bar, epoch);
     if (b == 0 && tid == 0) p.b.ts[4 * u + 3] = globaltimer();
     // ---- phase 2: W = βΦᵀU + αD, dᵀW partials ----
@@ -1396,18 +1416,27 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_cg_persistent(KParams p, const 
         Unit x = make_unit2(d, tc, w, G);
         uint32_t mask[TC_NTMAX / 32];
         unit_work(p, x, lane, mask);
-        if (!x.nmma && !x.mean) continue;
+        if (!x.nmma && !x.mean) {
+          if (tid == EPI0) dep_signal(cnt2 + x.t);
+          continue;
+        }
         if (producer) produce(p, mp, sm, tl, rc, x, tr2);
         else if (issuer) mma_unit(p, sm, tl, rc, tmem, x, tr2);
         else if (aw) {
           a_unit(p, sm, tl, rc, tmem, x, (tr2 && threadIdx.x == AW0) ? tr2 : nullptr, tr2 ? tr2 + 160 : nullptr);
           if (help2 && w + G >= n2 && x.nmma) a_help_drain2<CC>(p, sm, tl, rc, x);
         }
-        else if (epi) probe_epilogue<CC>(p, sm, tl, rc, tmem, x, mask, tr2, help2 && w + G >= n2);
+        else if (epi) {
+          probe_epilogue<CC>(p, sm, tl, rc, tmem, x, mask, tr2, help2 && w + G >= n2);
+          __threadfence();                    // this tile's W / Wm / dᵀAd stores, then its completion
+          epi_sync();
+          if (tid == EPI0) dep_signal(cnt2 + x.t);
+        }
       }
     }
-    grid_sync(bar, epoch);
-    if (b == 0 && tid == 0) p.b.ts[4 * u + 1] = globaltimer();
+    // no grid barrier: the update of a column of task t starts once task t's stage-2 units are done
+    if (tid == EPI0) atomicMax(p.b.ts + 4 * u + 1, globaltimer());
+    __syncthreads();                          // the ring's shared memory is reused by the update
     // ---- phase 3: CG update, one warp per active column ----
     unsigned long long *tr3 = (b == 0 && u == 5 && warp == 0) ? p.b.ts + 4 * d.cap + 160 : nullptr;
     if (tr3 && lane == 0) tr3[8] = clock64();
@@ -1415,6 +1444,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_cg_persistent(KParams p, const 
                           ? reinterpret_cast<float4 *>(sm) + (size_t)warp * (d.D / 2) : nullptr;
     for (int w = b * (NTHREADS / 32) + warp; w < ncols; w += G * (NTHREADS / 32)) {
       const int t = w / (d.P + d.C), j = w % (d.P + d.C);
+      if (lane == 0) dep_wait(cnt2 + t, (u + 1) * E2);   // W, dᵀAd of task t complete
+      __syncwarp();
       bool active;
       if (j < d.P) {
         active = ldv(p.b.flag + (size_t)t * d.P + j) == 1;
@@ -1539,6 +1570,8 @@ cudaError_t launch_split_phi(const KParams &p, cudaStream_t s) {
 cudaError_t launch_cg_persistent(const KParams &p, const TcMaps &maps, int grid, cudaStream_t s) {
   const size_t smem = tc_smem_bytes(p.tc, p.d.P);
   cudaError_t e = cudaMemsetAsync(p.b.gridbar, 0, sizeof(unsigned), s);
+  if (e != cudaSuccess) return e;
+  e = cudaMemsetAsync(p.b.dep, 0, sizeof(int) * 2 * p.d.Tl, s);
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
