@@ -1177,6 +1177,7 @@ __device__ void probe_epilogue(const KParams &p, unsigned char *sm, PSmemTail &t
         for (int e = et; e < nm; e += 128) {
           const size_t o = (size_t)(n0 + rb) * d.Cp + 2 * e;
           double2 v = make_double2(0.0, 0.0);
+#pragma unroll 4
           for (int sidx = 0; sidx < d.S1; ++sidx) {
             const double2 pv = __ldcg(reinterpret_cast<const double2 *>(mbase + (size_t)sidx * N * d.Cp + o));
             v.x += pv.x;
@@ -1200,6 +1201,7 @@ __device__ void probe_epilogue(const KParams &p, unsigned char *sm, PSmemTail &t
             off[v] = (size_t)(j0 + e / r4n) * N + n0 + rb + 4 * (e % r4n);
             acc4[v] = __ldcg(reinterpret_cast<const float4 *>(base + off[v]));
           }
+#pragma unroll 3
           for (int sidx = 1; sidx < d.S1; ++sidx) {
             float4 pv[V];
 #pragma unroll
