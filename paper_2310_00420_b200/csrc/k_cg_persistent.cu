@@ -708,7 +708,9 @@ struct RingCtl {
     if (++ast == SA) { ast = 0; aph ^= 1u; }
   }
   uint32_t ti;     // accumulator tiles handled so far
-  uint32_t tuse[2];  // uses of each TMEM accumulator buffer (tfull / tempty phases)
+  uint32_t tf[2];  // tiles committed to / drained from each TMEM accumulator buffer (tfull phases)
+  uint32_t te[2];  // MMA warp: tempty completions expected per buffer (a single-buffered tile in the
+                   // double-buffer layout spans both buffers and is released on both)
   uint32_t di;     // stage-2 d tiles handled so far (dfull / dempty phases)
   uint32_t smean;  // producer: bit s = the chunk last placed in slot s belongs to a mean unit
   uint32_t mcnt[MAXST];  // producer: mean chunks placed in each slot (mdone phases)
@@ -810,8 +812,8 @@ __device__ __forceinline__ void mma_unit(const KParams &p, unsigned char *sm, PS
   const uint32_t tacc = tmem + (uint32_t)(bi * 2 * tc.slot);
   if (x.nmma) {
     // the epilogue has drained this buffer's previous tile (both buffers for a 512-column tile)
-    if (rc.tuse[bi] > 0) mbar_wait(&tl.tempty[bi], (rc.tuse[bi] - 1) & 1);
-    if (!dbl && rc.tuse[1] > 0) mbar_wait(&tl.tempty[1], (rc.tuse[1] - 1) & 1);
+    if (rc.te[bi] > 0) mbar_wait(&tl.tempty[bi], (rc.te[bi] - 1) & 1);
+    if (!dbl && rc.te[1] > 0) mbar_wait(&tl.tempty[1], (rc.te[1] - 1) & 1);
     fence_after_sync();
   }
   for (int kc = 0; kc < x.nk; ++kc) {
@@ -847,7 +849,9 @@ __device__ __forceinline__ void mma_unit(const KParams &p, unsigned char *sm, PS
     } else {
       mma_commit_warp(&tl.tfull[bi]);        // all MMAs of the tile complete → accumulator ready
     }
-    rc.tuse[bi]++;
+    rc.tf[bi]++;
+    rc.te[bi]++;
+    if (!dbl && tc.dbl) rc.te[1]++;          // the tile also covers buffer 1's columns
     rc.ti++;
   }
 }
@@ -1125,7 +1129,7 @@ __device__ void probe_epilogue(const KParams &p, unsigned char *sm, PSmemTail &t
   if (x.nmma) {
     const int bi = acc_buf(rc, dbl);
     tacc = tmem + (uint32_t)(bi * 2 * tc.slot);
-    mbar_wait(&tl.tfull[bi], rc.tuse[bi] & 1);
+    mbar_wait(&tl.tfull[bi], rc.tf[bi] & 1);
     if (tr) tr[80] = clock64();
     fence_after_sync();
   }
@@ -1162,8 +1166,11 @@ __device__ void probe_epilogue(const KParams &p, unsigned char *sm, PSmemTail &t
       fence_before_sync();
       __syncwarp();
       const int bi = acc_buf(rc, dbl);
-      if (lane == 0) mbar_arrive(&tl.tempty[bi]);  // the MMA warp may overwrite the accumulator
-      rc.tuse[bi]++;
+      if (lane == 0) {                         // the MMA warp may overwrite the accumulator
+        mbar_arrive(&tl.tempty[bi]);
+        if (!dbl && tc.dbl) mbar_arrive(&tl.tempty[1]);
+      }
+      rc.tf[bi]++;
       rc.ti++;
       if (tr) tr[81] = clock64();
     }
@@ -1321,9 +1328,10 @@ __device__ void probe_epilogue(const KParams &p, unsigned char *sm, PSmemTail &t
     const int bi = acc_buf(rc, dbl);
     if (lane == 0) {
       mbar_arrive(&tl.tempty[bi]);
+      if (!dbl && tc.dbl) mbar_arrive(&tl.tempty[1]);
       if (dts) mbar_arrive(&tl.dempty);
     }
-    rc.tuse[bi]++;
+    rc.tf[bi]++;
     rc.ti++;
   }
   if (tr) tr[81] = clock64();
@@ -1376,12 +1384,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_cg_persistent(KParams p, const 
   __syncthreads();
   fence_after_sync();
   const uint32_t tmem = tl.tslot;
-  RingCtl rc{tc.stages, 0u, 0, 0u, tc.sa, 0u, 0, 0u, 0u, {0u, 0u}, 0u, 0u, {0u, 0u, 0u, 0u, 0u, 0u}};
+  RingCtl rc{tc.stages, 0u, 0, 0u, tc.sa, 0u, 0, 0u, 0u, {0u, 0u}, {0u, 0u}, 0u, 0u, {0u, 0u, 0u, 0u, 0u, 0u}};
   unsigned epoch = 0;
   unsigned *bar = p.b.gridbar;
   const int n1 = d.Tl * d.nCT * d.nRT1 * d.S1, n2 = d.Tl * d.nCT * d.nRT2;
-  const int E2 = d.nCT * d.nRT2;             // stage-2 units per task
-  int *cnt2 = p.b.dep + d.Tl;
+  const int E1 = d.nCT * d.nRT1 * d.S1, E2 = d.nCT * d.nRT2;   // units per task and stage
+  int *cnt1 = p.b.dep, *cnt2 = p.b.dep + d.Tl;
   const int ncols = d.Tl * (d.P + d.C);
   const bool producer = warp == 0, issuer = warp == 1;
   const bool aw = warp >= 2 && warp < 6, epi = warp >= 6;
@@ -1400,17 +1408,23 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_cg_persistent(KParams p, const 
         Unit x = make_unit1(d, tc, w, G);
         uint32_t mask[TC_NTMAX / 32];
         unit_work(p, x, lane, mask);
-        if (!x.nmma && !x.mean) continue;
+        if (!x.nmma && !x.mean) {
+          if (tid == EPI0) dep_signal(cnt1 + x.t);
+          continue;
+        }
         if (producer) produce(p, mp, sm, tl, rc, x, tr1);
         else if (issuer) mma_unit(p, sm, tl, rc, tmem, x, tr1);
         else if (aw) a_unit(p, sm, tl, rc, tmem, x, (tr1 && threadIdx.x == AW0) ? tr1 : nullptr, nullptr);
-        else if (epi) probe_epilogue<CC>(p, sm, tl, rc, tmem, x, mask, tr1, false);
+        else if (epi) {
+          probe_epilogue<CC>(p, sm, tl, rc, tmem, x, mask, tr1, false);
+          __threadfence();                    // this tile's U / Um stores, then its completion
+          epi_sync();
+          if (tid == EPI0) dep_signal(cnt1 + x.t);
+        }
       }
     }
-    // stage 1 → stage 2: a grid barrier (a per-task dataflow counter here, as between stage 2 and the
-    // update, hung or mis-converged at C3: kept out)
-    grid_sync(bar, epoch);
-    if (b == 0 && tid == 0) p.b.ts[4 * u + 3] = globaltimer();
+    // no grid barrier: a stage-2 unit of task t starts once task t's stage-1 units are complete
+    if (tid == EPI0) atomicMax(p.b.ts + 4 * u + 3, globaltimer());
     // ---- phase 2: W = βΦᵀU + αD, dᵀW partials ----
     if (tr2 && tid == 0) tr2[127] = clock64();
     if (tile_role) {
@@ -1422,7 +1436,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_cg_persistent(KParams p, const 
           if (tid == EPI0) dep_signal(cnt2 + x.t);
           continue;
         }
-        if (producer) produce(p, mp, sm, tl, rc, x, tr2);
+        if (producer) {
+          if (lane == 0) dep_wait(cnt1 + x.t, (u + 1) * E1);   // U, Um of task t complete
+          __syncwarp();
+          fence_proxy_async_global();         // the acquired generic writes → this warp's TMA reads
+          produce(p, mp, sm, tl, rc, x, tr2);
+        }
         else if (issuer) mma_unit(p, sm, tl, rc, tmem, x, tr2);
         else if (aw) {
           a_unit(p, sm, tl, rc, tmem, x, (tr2 && threadIdx.x == AW0) ? tr2 : nullptr, tr2 ? tr2 + 160 : nullptr);

@@ -1,3 +1,4 @@
 timeout 600 python -m pytest tests/test_gpu_parity.py -x -q 2>&1 | tail -1
 CMTCS_PHASE_LOG=1 timeout 120 python bench.py --config 2 --steps 1 --warmup 0 --no-e2e --no-cpu-baseline 2>&1 | grep -E "cmtcs\] EM"
 CMTCS_PHASE_LOG=1 timeout 120 python bench.py --config 3 --steps 1 --warmup 0 --no-e2e --no-cpu-baseline 2>&1 | grep -E "cmtcs\] EM"
+timeout 900 python -m pytest tests/test_gpu_fullsize.py -x -q 2>&1 | tail -2
