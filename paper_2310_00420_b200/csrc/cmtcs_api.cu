@@ -364,7 +364,7 @@ cmtcs_status one_em_iteration(cmtcs_ctx *c, const uint64_t *probe_bits, const do
       }
       fprintf(stderr, "[cmtcs] EM it %d: %d CG steps, per step us: phase1 %.2f phase2 %.2f update %.2f\n",
               c->em_iter, steps_run, ph[0] / steps_run, ph[1] / steps_run, ph[2] / steps_run);
-      for (int ph = 0; ph < 2 && steps_run > 5; ++ph) {
+      for (int ph = 0; ph < 2 && steps_run > c->kp.trace_step; ++ph) {
         const unsigned long long *g = c->h_ts + 4 * d.cap + 256 * ph;
         const unsigned long long t0 = g[127];   // SM clock at the phase start (CTA 0)
         auto us = [&](int i) { return g[i] ? ((double)g[i] - (double)t0) * 1e-3 : -1.0; };
@@ -488,6 +488,7 @@ cmtcs_status cmtcs_init(cmtcs_ctx **out, const cmtcs_problem *p, const float *ph
   c->kp.empty_eps = p->empty_eps;
   c->kp.seed = p->probe_seed;
   c->kp.dbg_flags = getenv("CMTCS_DBG") ? atoi(getenv("CMTCS_DBG")) : 0;
+  c->kp.trace_step = getenv("CMTCS_TRACE_STEP") ? atoi(getenv("CMTCS_TRACE_STEP")) : 5;
   *out = c;  // from here on errors leave a (broken) ctx the caller destroys
   CUDA_OK(c, cudaMallocHost((void **)&c->h_out, 32 * sizeof(double)));
   CUDA_OK(c, cudaMallocHost((void **)&c->h_status, 8 * sizeof(int)));

@@ -1398,8 +1398,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_cg_persistent(KParams p, const 
   const bool help2 = tc.use_dtile && !(p.dbg_flags & 64);
   for (int u = 0; u < d.cap; ++u) {
     if (b == 0 && tid == 0) p.b.ts[4 * u + 0] = globaltimer();
-    // diagnostic trace of CTA 0's first unit of each phase at CG step 5 (CMTCS_PHASE_LOG)
-    unsigned long long *tr1 = (b == 0 && u == 5) ? p.b.ts + 4 * d.cap : nullptr;
+    // diagnostic trace of CTA 0's first unit of each phase at CG step trace_step (CMTCS_PHASE_LOG)
+    unsigned long long *tr1 = (b == 0 && u == p.trace_step) ? p.b.ts + 4 * d.cap : nullptr;
     unsigned long long *tr2 = tr1 ? tr1 + 256 : nullptr;
     // ---- phase 1: U = Φ D ----
     if (tr1 && tid == 0) tr1[127] = clock64();   // trace times are SM clocks from here
@@ -1459,7 +1459,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_cg_persistent(KParams p, const 
     if (tid == EPI0) atomicMax(p.b.ts + 4 * u + 1, globaltimer());
     __syncthreads();                          // the ring's shared memory is reused by the update
     // ---- phase 3: CG update, one warp per active column ----
-    unsigned long long *tr3 = (b == 0 && u == 5 && warp == 0) ? p.b.ts + 4 * d.cap + 160 : nullptr;
+    unsigned long long *tr3 = (b == 0 && u == p.trace_step && warp == 0) ? p.b.ts + 4 * d.cap + 160 : nullptr;
     if (tr3 && lane == 0) tr3[8] = clock64();
     float4 *stage_d = (size_t)NTHREADS / 32 * 2 * d.D * 4 <= (size_t)tc.stages * tc.stage_bytes
                           ? reinterpret_cast<float4 *>(sm) + (size_t)warp * (d.D / 2) : nullptr;

@@ -12,6 +12,9 @@
 //   mode 8: MMAs + commit after every chunk, waiting for it before the next chunk (issue → done)
 //   mode 9: as mode 0, but the whole warp runs the issue loop and one elected lane issues each MMA
 //           (warp-uniform operands: no per-MMA register → uniform-register moves)
+//   mode 10: as mode 9 with the main accumulator at TMEM column 80 (16- but not 32-aligned)
+//   mode 11: as mode 9 plus the kernel's per-chunk overhead: two completed-mbarrier waits,
+//            tcgen05.fence::after_thread_sync, two integer divisions, two commits
 // Cycles per chunk (12 MMAs) from clock64 on the issuing thread.
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -I paper_2310_00420_b200/csrc -o tools/mma_contention_test tools/mma_contention_test.cu
 #include <cstdio>
@@ -51,10 +54,38 @@ __global__ void __launch_bounds__(384, 1) k(int mode, int chunks, unsigned long 
   __syncthreads();
   fence_after_sync();
   const uint32_t tm = slot;
-  if (mode == 9 && w == 0) {
+  if (mode == 11 && w == 0) {
     const uint32_t idesc = idesc_tf32(128, NB);
     const uint64_t bh = desc_sw128(smem_u32(sm)), bl = desc_sw128(smem_u32(sm + NB * 128));
     const uint32_t tx = tm, tmain = tm + 96, ta = tm + 384;
+    __shared__ uint64_t pre;
+    if (t == 0) { mbar_init(&pre, 1); asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(&pre)) : "memory"); }
+    __syncwarp();
+    const long long c0 = clock64();
+    int nk = chunks, nacc = 1;
+    for (int c = 0; c < chunks; ++c) {
+      mbar_wait(&pre, 0);
+      mbar_wait(&pre, 0);
+      fence_after_sync();
+      const int q = (c * nacc) / nk;
+      const int qfirst = (q * nk + nacc - 1) / nacc;
+#pragma unroll
+      for (int k8 = 0; k8 < 4; ++k8) {
+        const uint64_t o = (uint64_t)(k8 * 32) >> 4;
+        mma_ts_elect(tx, ta + 32 + 8 * k8, bh + o, idesc, 1);
+        mma_ts_elect(tx, ta + 8 * k8, bl + o, idesc, 1);
+        mma_ts_elect(tmain + 0 * q, ta + 8 * k8, bh + o, idesc, (c == qfirst && k8 == 0) ? 0u : 1u);
+      }
+      asm volatile("{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}\n" ::"r"(smem_u32(&done)) : "memory");
+      asm volatile("{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}\n" ::"r"(smem_u32(&done)) : "memory");
+      __syncwarp();
+    }
+    const long long c1 = clock64();
+    if (t == 0) { out[blockIdx.x] = (unsigned long long)(c1 - c0); stop = 1; }
+  } else if ((mode == 9 || mode == 10) && w == 0) {
+    const uint32_t idesc = idesc_tf32(128, NB);
+    const uint64_t bh = desc_sw128(smem_u32(sm)), bl = desc_sw128(smem_u32(sm + NB * 128));
+    const uint32_t tx = tm, tmain = tm + (mode == 10 ? 80 : 96), ta = tm + 384;
     const long long c0 = clock64();
     for (int c = 0; c < chunks; ++c) {
 #pragma unroll
@@ -69,7 +100,7 @@ __global__ void __launch_bounds__(384, 1) k(int mode, int chunks, unsigned long 
     mbar_wait(&done, 0);
     const long long c1 = clock64();
     if (t == 0) { out[blockIdx.x] = (unsigned long long)(c1 - c0); stop = 1; }
-  } else if (t == 0 && mode != 9) {
+  } else if (t == 0 && mode < 9) {
     const uint32_t idesc = idesc_tf32(128, NB);
     const uint64_t bh = desc_sw128(smem_u32(sm)), bl = desc_sw128(smem_u32(sm + NB * 128));
     const uint32_t tx = tm, tmain = tm + 96, ta = tm + 384;
@@ -144,11 +175,11 @@ int main() {
   cudaMalloc(&out, 148 * 8);
   cudaMalloc(&sink, 64);
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536 + 1024);
-  const char *names[10] = {"MMAs only", "+ tcgen05.ld stream", "+ tcgen05.st stream", "+ ld and st streams", "+ ld.shared stream",
+  const char *names[12] = {"MMAs only", "+ tcgen05.ld stream", "+ tcgen05.st stream", "+ ld and st streams", "+ ld.shared stream",
                           "+ DMMA stream", "+ F2F + DMMA stream", "commit per chunk", "commit + wait per chunk",
-                          "whole warp, elect.sync"};
+                          "whole warp, elect.sync", "elect, main acc at col 80", "elect + kernel overheads"};
   const int chunks = 2000;
-  for (int mode = 0; mode < 10; ++mode) {
+  for (int mode = 0; mode < 12; ++mode) {
     for (int rep = 0; rep < 2; ++rep) {
       k<<<148, 384, 65536 + 1024>>>(mode, chunks, out, sink);
       cudaDeviceSynchronize();
