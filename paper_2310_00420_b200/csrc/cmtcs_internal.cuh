@@ -107,6 +107,8 @@ struct TcMaps {
   CUtensorMap dm;              // fp64 [rows Tl·C][cols D], box 32 × C (mean directions)
   CUtensorMap um;              // fp64 [rows Tl·N][cols Cp], box Cp × 32 (Φ·d of the mean columns)
   CUtensorMap d32;             // fp32 [rows Tl·P][cols D], box 128 × NT (probe directions, epilogue)
+  CUtensorMap u_hl, d_hl;      // the hi and lo arrays as one 3-D tensor [2][rows][cols], box 32 × NT × 2:
+                               // both B tiles of a stage with one TMA (hi tile, then lo tile)
 };
 
 struct KParams {

@@ -769,17 +769,11 @@ __device__ __forceinline__ void produce(const KParams &p, const TcMaps &mp, unsi
     // stage layout: fp32 A tile | B hi | B lo | fp64 mean-column chunk
     if (x.stage == 1) {
       tma_load_2d_warp(base, &mp.phi, k, x.arow, fb);
-      if (x.nmma) {
-        tma_load_2d_warp(base + A_BYTES, &mp.d_h, k, x.brow, fb);
-        tma_load_2d_warp(base + A_BYTES + b_bytes, &mp.d_l, k, x.brow, fb);
-      }
+      if (x.nmma) tma_load_3d_warp(base + A_BYTES, &mp.d_hl, k, x.brow, 0, fb);   // hi | lo tiles
       if (x.mean) tma_load_2d_warp(base + A_BYTES + 2 * b_bytes, &mp.dm, k, x.t * p.d.C, fb);
     } else {
       tma_load_2d_warp(base, &mp.phit, k, x.arow, fb);
-      if (x.nmma) {
-        tma_load_2d_warp(base + A_BYTES, &mp.u_h, k, x.brow, fb);
-        tma_load_2d_warp(base + A_BYTES + b_bytes, &mp.u_l, k, x.brow, fb);
-      }
+      if (x.nmma) tma_load_3d_warp(base + A_BYTES, &mp.u_hl, k, x.brow, 0, fb);
       if (x.mean) tma_load_2d_warp(base + A_BYTES + 2 * b_bytes, &mp.um, 0, x.t * p.d.N + k, fb);
     }
     if (tr && kc < 16 && (threadIdx.x & 31) == 0) tr[16 + kc] = clock64();
@@ -1528,6 +1522,21 @@ bool encode_2d(EncodeTiledFn enc, CUtensorMap *m, const void *ptr, CUtensorMapDa
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// 3-D view [2][rows][cols] of two equally shaped row-major fp32 arrays (hi at `hi`, lo at `lo`,
+// lo − hi a multiple of 16 bytes), box box_cols × box_rows × 2, 128-byte swizzle
+bool encode_hilo(EncodeTiledFn enc, CUtensorMap *m, const float *hi, const float *lo, long rows, long cols, int box_cols,
+                 int box_rows) {
+  const long long gap = (long long)((const char *)lo - (const char *)hi);
+  if (gap <= 0 || gap % 16) return false;
+  cuuint64_t dims[3] = {(cuuint64_t)cols, (cuuint64_t)rows, 2};
+  cuuint64_t strides[2] = {(cuuint64_t)cols * 4, (cuuint64_t)gap};
+  cuuint32_t box[3] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows, 2};
+  cuuint32_t es[3] = {1, 1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float *>(hi), dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 }  // namespace
 
 size_t tc_smem_bytes(const TcCfg &tc, int P) {
@@ -1557,7 +1566,9 @@ bool encode_maps(const KParams &p, TcMaps *m, char *why) {
                   encode_2d(enc, &m->d_l, b.Dl, F32, 4, (long)d.Tl * d.P, d.D, 32, NT, true) &&
                   encode_2d(enc, &m->dm, b.Dm, F64, 8, (long)d.Tl * d.C, d.D, TK, d.C, false) &&
                   encode_2d(enc, &m->um, b.Um, F64, 8, (long)d.Tl * d.N, d.Cp, d.Cp, TK, false) &&
-                  encode_2d(enc, &m->d32, b.D32, F32, 4, (long)d.Tl * d.P, d.D, TM, NT, false);
+                  encode_2d(enc, &m->d32, b.D32, F32, 4, (long)d.Tl * d.P, d.D, TM, NT, false) &&
+                  encode_hilo(enc, &m->u_hl, b.Uh, b.Ul, (long)d.Tl * d.Pp, d.N, 32, NT) &&
+                  encode_hilo(enc, &m->d_hl, b.Dh, b.Dl, (long)d.Tl * d.P, d.D, 32, NT);
   if (!ok) snprintf(why, 256, "cuTensorMapEncodeTiled failed");
   return ok;
 }

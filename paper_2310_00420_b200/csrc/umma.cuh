@@ -148,6 +148,14 @@ __device__ __forceinline__ void tma_load_2d_warp(void *smem, const CUtensorMap *
       "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(smem_u32(mbar))
       : "memory");
 }
+__device__ __forceinline__ void tma_load_3d_warp(void *smem, const CUtensorMap *map, int x, int y, int z, uint64_t *mbar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];\n\t}\n" ::"r"(
+          smem_u32(smem)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(mbar))
+      : "memory");
+}
 __device__ __forceinline__ void mbar_arrive_expect_tx_warp(uint64_t *mbar, uint32_t bytes) {
   asm volatile(
       "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"

@@ -1,1 +1,3 @@
-CMTCS_TRACE_STEP=40 CMTCS_PHASE_LOG=1 timeout 120 python bench.py --config 2 --steps 1 --warmup 0 --no-e2e --no-cpu-baseline 2>&1 | grep -E "cmtcs\]" | grep -E "EM it|phase |prod|mma full|A full|A split|afull q0|mdone|epi loop" | cut -c1-180
+timeout 1500 python -m pytest tests -m gpu -x -q 2>&1 | tail -2
+python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" 2>&1 | tail -1
+timeout 300 python bench.py 2>&1 | tail -1 | cut -c1-300
