@@ -161,6 +161,22 @@ def test_single_em_step_multiround_split_k(torch_cuda):
     assert np.all(np.abs(post["logdet"] - orc["nu"]) <= nu_tol(orc["nu"]))
 
 
+def test_single_em_step_mixed_accumulator_layouts(torch_cuda):
+    """40 tasks with N = 256, D = 4096: stage 1 is unsplit (80 units of 128 chunks: single-buffered,
+    K-split TMEM accumulators) and stage 2 double-buffered (8 chunks), and without a grid barrier
+    between the stages a CTA's stage-2 tile follows its stage-1 tile in TMEM: the single-buffered
+    tile is released on both buffers before a double-buffered one reuses them.  (Parity of the
+    mixed layouts; the race the release order prevents is timing-dependent — it showed at C3 full
+    size, covered by test_gpu_fullsize.py — and did not trigger at this size.)"""
+    data = synthetic.small_problem(T=40, C=2, N=256, D=4096, K=4, sigma=0.01, seed=17, support=20)
+    alpha = np.random.default_rng(9).uniform(0.5, 4.0, (2, 4096))
+    post, info, orc, a_next, conv = _single_step(data, alpha, 2, cap=600, tol=1e-7)
+    e = compare_step(post, info, orc, a_next, conv)
+    print("mixed TMEM layouts", e, "converged", conv.sum(), "/", conv.size)
+    assert e["mu"] <= MU_TOL and conv.any() and e["s_conv"] <= S_TOL and e["q_abs"] <= Q_TOL and e["L_abs"] <= L_TOL
+    assert np.all(np.abs(post["logdet"] - orc["nu"]) <= nu_tol(orc["nu"]))
+
+
 def test_single_em_step_many_column_tiles(torch_cuda):
     """P = C·K = 16·9 = 144 > two 64-column tiles, C = 16 (the maximum), 1 task per... ."""
     data = synthetic.small_problem(T=2, C=16, N=48, D=128, K=9, sigma=0.05, seed=12, support=5)
