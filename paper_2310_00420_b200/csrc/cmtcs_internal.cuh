@@ -86,7 +86,7 @@ struct Bufs {
 // tensor-core operator configuration (chosen at init from P)
 struct TcCfg {
   int NT;            // column tile width (multiple of 16, ≤ TC_NTMAX)
-  int slot;          // TMEM columns per accumulator (NT rounded up to 32)
+  int slot;          // TMEM columns per accumulator (NT rounded up to 16)
   int sa;            // A stages in TMEM (64 columns each: the tf32 hi and lo halves of a 128 × 32 tile)
   int acol0;         // first TMEM column of the A stages (= 512 − 64·sa; accumulators below)
   int dbl;           // two accumulator buffers (cross + one main each) fit below acol0
