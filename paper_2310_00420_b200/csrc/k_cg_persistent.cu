@@ -252,6 +252,23 @@ __device__ __forceinline__ void mma_stage(uint32_t tmem, uint32_t a_tm, unsigned
   }
 }
 
+// The same for a full double-buffered tile (N = NT, slot = NT, one main accumulator) in 2 MMAs per
+// K = 8 step instead of 3: the B hi and lo tiles are adjacent in shared memory, so one N = 2·NT MMA
+// computes hi_A·[hi_B | lo_B] into [main | cross] (columns [0, NT) and [NT, 2·NT) of the buffer, the
+// same regions the 3-MMA form uses for cross and main — the epilogue sums both either way), and a
+// second adds lo_A·hi_B to the cross region.  Fewer MMA instructions per chunk for the issuing warp.
+__device__ __forceinline__ void mma_stage_cat(uint32_t tmem, uint32_t a_tm, unsigned char *base, uint32_t idesc2,
+                                              uint32_t idesc, int nt, bool first) {
+  const uint64_t bh = desc_sw128(smem_u32(base + A_BYTES));
+#pragma unroll
+  for (int k8 = 0; k8 < TK / 8; ++k8) {
+    const uint64_t o = (uint64_t)(k8 * 32) >> 4;
+    const uint32_t ah = a_tm + 8 * k8, al = a_tm + 32 + 8 * k8;
+    mma_tf32_ts_warp(tmem, ah, bh + o, idesc2, (first && k8 == 0) ? 0u : 1u);
+    mma_tf32_ts_warp(tmem + (uint32_t)nt, al, bh + o, idesc, 1u);
+  }
+}
+
 // 16 accumulator columns [c0, c0+16) of this thread's row, summed over the K-split pairs: all
 // tcgen05.ld of the group are issued before one wait::ld
 __device__ __forceinline__ void tmem_ld16_nowait(uint32_t taddr, uint32_t *r) {
@@ -802,6 +819,9 @@ __device__ __forceinline__ void mma_unit(const KParams &p, unsigned char *sm, PS
   const int nacc = unit_nacc(tc, x.nk, p.dbg_flags);
   const uint32_t idesc = idesc_tf32(TM, x.nmma > 0 ? x.nmma : 16);
   const bool dbl = unit_dbl(tc, x.nk, p.dbg_flags);
+  // a full double-buffered tile: the 2-MMA form (N = 2·NT ≤ 256)
+  const bool cat = dbl && x.nmma == tc.NT && tc.slot == tc.NT && 2 * tc.NT <= 256 && !(p.dbg_flags & 4096);
+  const uint32_t idesc2 = idesc_tf32(TM, cat ? 2 * tc.NT : 16);
   const int bi = dbl ? (int)(rc.ti & 1) : 0;
   const uint32_t tacc = tmem + (uint32_t)(bi * 2 * tc.slot);
   if (x.nmma) {
@@ -824,8 +844,12 @@ __device__ __forceinline__ void mma_unit(const KParams &p, unsigned char *sm, PS
         fence_after_sync();
         const int q = (kc * nacc) / x.nk;
         const int qfirst = (q * x.nk + nacc - 1) / nacc;
-        mma_stage(tacc, tmem + (uint32_t)(tc.acol0 + 64 * sa), sm + (size_t)st * tc.stage_bytes, b_bytes, idesc,
-                  q, tc.slot, kc == qfirst, kc == 0);
+        if (cat)
+          mma_stage_cat(tacc, tmem + (uint32_t)(tc.acol0 + 64 * sa), sm + (size_t)st * tc.stage_bytes, idesc2, idesc,
+                        tc.NT, kc == 0);
+        else
+          mma_stage(tacc, tmem + (uint32_t)(tc.acol0 + 64 * sa), sm + (size_t)st * tc.stage_bytes, b_bytes, idesc,
+                    q, tc.slot, kc == qfirst, kc == 0);
         mma_commit_warp(&tl.aempty[sa]);      // the MMAs have read the A stage
         mma_commit_warp(&tl.empty[st]);       // ... and the B tiles
       } else if (lane == 0) {
