@@ -234,22 +234,6 @@ __device__ __forceinline__ int unit_nacc(const TcCfg &tc, int nk, int dbg) {
   return (nk <= 16 && !(dbg & 8)) ? 1 : min(tc.nacc, nk);
 }
 
-// 2-MMA form of a unit (mma_stage_cat): full column tile, N = 2·NT ≤ 256; its accumulators are
-// `pairs` [main | cross] pairs (K split over the pairs; one pair when double-buffered, else as many
-// as fit below the A stages, at least 2 — otherwise the 3-MMA form keeps a K-split main)
-__device__ __forceinline__ int unit_cat_pairs(const TcCfg &tc, int nmma, int nk, int dbg) {
-  if (nmma != tc.NT || tc.slot != tc.NT || 2 * tc.NT > 256 || (dbg & 4096)) return 0;
-  if (unit_dbl(tc, nk, dbg)) return 1;
-  const int pairs = min(min(4, tc.acol0 / (2 * tc.slot)), nk);
-  return pairs >= 2 ? pairs : 0;
-}
-// accumulator regions of a unit beyond the first (the acc_load16 count): 2·pairs − 1 in the 2-MMA
-// form, else the cross region plus nacc mains
-__device__ __forceinline__ int unit_regions(const TcCfg &tc, int nmma, int nk, int dbg) {
-  const int pairs = unit_cat_pairs(tc, nmma, nk, dbg);
-  return pairs ? 2 * pairs - 1 : unit_nacc(tc, nk, dbg);
-}
-
 // issue the 3xTF32 MMAs of one K = 32 stage (the whole MMA warp, one elected lane issuing) into main
 // accumulator q: A (hi | lo) from
 // the TMEM A stage at column a_tm, B (hi, lo) from the shared-memory ring stage
@@ -835,9 +819,8 @@ __device__ __forceinline__ void mma_unit(const KParams &p, unsigned char *sm, PS
   const int nacc = unit_nacc(tc, x.nk, p.dbg_flags);
   const uint32_t idesc = idesc_tf32(TM, x.nmma > 0 ? x.nmma : 16);
   const bool dbl = unit_dbl(tc, x.nk, p.dbg_flags);
-  // a full tile: the 2-MMA form (N = 2·NT ≤ 256) over `pairs` [main | cross] accumulator pairs
-  const int pairs = unit_cat_pairs(tc, x.nmma, x.nk, p.dbg_flags);
-  const bool cat = pairs > 0;
+  // a full double-buffered tile: the 2-MMA form (N = 2·NT ≤ 256)
+  const bool cat = dbl && x.nmma == tc.NT && tc.slot == tc.NT && 2 * tc.NT <= 256 && !(p.dbg_flags & 4096);
   const uint32_t idesc2 = idesc_tf32(TM, cat ? 2 * tc.NT : 16);
   const int bi = dbl ? (int)(rc.ti & 1) : 0;
   const uint32_t tacc = tmem + (uint32_t)(bi * 2 * tc.slot);
@@ -861,15 +844,12 @@ __device__ __forceinline__ void mma_unit(const KParams &p, unsigned char *sm, PS
         fence_after_sync();
         const int q = (kc * nacc) / x.nk;
         const int qfirst = (q * x.nk + nacc - 1) / nacc;
-        if (cat) {
-          const int qc = (kc * pairs) / x.nk;
-          const int qcfirst = (qc * x.nk + pairs - 1) / pairs;
-          mma_stage_cat(tacc + (uint32_t)(qc * 2 * tc.slot), tmem + (uint32_t)(tc.acol0 + 64 * sa),
-                        sm + (size_t)st * tc.stage_bytes, idesc2, idesc, tc.NT, kc == qcfirst);
-        } else {
+        if (cat)
+          mma_stage_cat(tacc, tmem + (uint32_t)(tc.acol0 + 64 * sa), sm + (size_t)st * tc.stage_bytes, idesc2, idesc,
+                        tc.NT, kc == 0);
+        else
           mma_stage(tacc, tmem + (uint32_t)(tc.acol0 + 64 * sa), sm + (size_t)st * tc.stage_bytes, b_bytes, idesc,
                     q, tc.slot, kc == qfirst, kc == 0);
-        }
         mma_commit_warp(&tl.aempty[sa]);      // the MMAs have read the A stage
         mma_commit_warp(&tl.empty[st]);       // ... and the B tiles
       } else if (lane == 0) {
@@ -1079,7 +1059,7 @@ __device__ void a_help_drain2(const KParams &p, unsigned char *sm, PSmemTail &tl
 #pragma unroll
   for (int c = 0; c < CC; ++c) alpha[c] = (c < d.C && dd < d.D) ? __ldg(p.b.alpha32 + (size_t)c * d.D + dd) : 0.f;
   pair_sync();
-  drain2_groups<CC>(p, tl, x, tl.help_tacc, unit_regions(tc, x.nmma, x.nk, p.dbg_flags),
+  drain2_groups<CC>(p, tl, x, tl.help_tacc, unit_nacc(tc, x.nk, p.dbg_flags),
                     reinterpret_cast<const float *>(sm + (size_t)rc.S * tc.stage_bytes), alpha, 1, 2);
   __threadfence();                            // W stores before the epilogue's completion release
   pair_sync();
@@ -1094,7 +1074,7 @@ __device__ void probe_epilogue(const KParams &p, unsigned char *sm, PSmemTail &t
   const int et = threadIdx.x - EPI0, ew = (threadIdx.x >> 5) & 3, lane = threadIdx.x & 31;
   const int r = 32 * ew + lane;              // tile row = TMEM lane (warp w reads lanes 32·(w % 4) + ...)
   const int N = d.N, D = d.D, P = d.P, C = d.C;
-  const int nacc = unit_regions(tc, x.nmma, x.nk, p.dbg_flags);   // accumulator regions − 1
+  const int nacc = unit_nacc(tc, x.nk, p.dbg_flags);
   const bool dbl = unit_dbl(tc, x.nk, p.dbg_flags);
   const int j0 = x.ct * tc.NT;
   if (lane < TC_NTMAX / 32) {

@@ -1,6 +1,6 @@
-for c in 2 3; do timeout 300 python bench.py --config $c --no-e2e --no-cpu-baseline $( [ $c = 3 ] && echo "--steps 3 --warmup 3") 2>&1 | python -c "import sys,json
+timeout 600 python -m pytest tests/test_gpu_parity.py -x -q -s 2>&1 | grep -E "parity|multiround|mixed|passed|failed" | cut -c1-250
+CMTCS_PHASE_LOG=1 timeout 120 python bench.py --config 2 --steps 1 --warmup 0 --no-e2e --no-cpu-baseline 2>&1 | grep -E "cmtcs\] EM|rror" | head -3
+CMTCS_PHASE_LOG=1 timeout 120 python bench.py --config 3 --steps 1 --warmup 0 --no-e2e --no-cpu-baseline 2>&1 | grep -E "cmtcs\] EM|rror" | head -3
+timeout 300 python bench.py --no-e2e --no-cpu-baseline 2>&1 | python -c "import sys,json
 for l in sys.stdin:
-    if l.startswith('{'): j=json.loads(l); print('C$c', round(j['value'],4), j['roofline']['frac'])"; done
-timeout 300 python bench.py --config 4 --steps 1 --warmup 1 --no-e2e --no-cpu-baseline 2>&1 | python -c "import sys,json
-for l in sys.stdin:
-    if l.startswith('{'): j=json.loads(l); print('C4', round(j['value'],4), j['roofline']['frac'], j.get('clocks',{}).get('sm_mhz'))"
+    if l.startswith('{'): j=json.loads(l); print('C2', round(j['value'],3), j['roofline']['frac'])"
