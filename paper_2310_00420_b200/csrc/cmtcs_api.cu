@@ -382,7 +382,7 @@ cmtcs_status one_em_iteration(cmtcs_ctx *c, const uint64_t *probe_bits, const do
           fprintf(stderr, "\n[cmtcs]     mdone    :"); for (int i = 0; i < 16; ++i) fprintf(stderr, " %.2f", us(224 + i));
         }
         if (ph == 0) { fprintf(stderr, "\n[cmtcs]     update (kcyc from phase start): start %.2f gam %.2f pass1 %.2f xi %.2f end %.2f", (g[160]-g[168])*1e-3, (g[161]-g[168])*1e-3, (g[162]-g[168])*1e-3, (g[163]-g[168])*1e-3, (g[164]-g[168])*1e-3); }
-        fprintf(stderr, "\n[cmtcs]     epi loopend %.2f meanepi %.2f tfull %.2f drained %.2f end %.2f\n", us(85), us(86), us(80), us(81), us(82));
+        fprintf(stderr, "\n[cmtcs]     epi loopend %.2f meanepi %.2f tfull %.2f drained %.2f handoff %.2f end %.2f\n", us(85), us(86), us(80), us(81), us(87), us(82));
 
       }
     }

@@ -886,11 +886,13 @@ __device__ __forceinline__ void mma_unit(const KParams &p, unsigned char *sm, PS
 // The tile counters only grow (S1 arrivals per active tile and step, zeroed at init).
 __device__ __forceinline__ void split_handoff(const KParams &p, const Unit &x, PSmemTail &tl, int *rb, int *re) {
   const Dims &d = p.d;
-  __threadfence();
+  // the epilogue warps' partial stores are ordered before EPI0's release by the barrier (a
+  // gpu-scope release is cumulative over what the releasing thread has observed)
   epi_sync();
   int *cnt = p.b.tilecnt + ((size_t)x.t * d.nCT + x.ct) * d.nRT1 + x.rt;
   if (threadIdx.x == EPI0) {
-    const int ticket = atomicAdd(cnt, 1);
+    int ticket;
+    asm volatile("atom.add.release.gpu.global.s32 %0, [%1], 1;\n" : "=r"(ticket) : "l"(cnt) : "memory");
     if (d.split_coop) {
       const int target = (ticket / d.S1 + 1) * d.S1;
       int v;
@@ -1061,8 +1063,7 @@ __device__ void a_help_drain2(const KParams &p, unsigned char *sm, PSmemTail &tl
   pair_sync();
   drain2_groups<CC>(p, tl, x, tl.help_tacc, unit_nacc(tc, x.nk, p.dbg_flags),
                     reinterpret_cast<const float *>(sm + (size_t)rc.S * tc.stage_bytes), alpha, 1, 2);
-  __threadfence();                            // W stores before the epilogue's completion release
-  pair_sync();
+  pair_sync();                                // W stores ordered before the epilogue's completion release
 }
 
 template <int CC>
@@ -1195,6 +1196,7 @@ __device__ void probe_epilogue(const KParams &p, unsigned char *sm, PSmemTail &t
     if (d.S1 > 1) {
       int rb, re;
       split_handoff(p, x, tl, &rb, &re);
+      if (tr) tr[87] = clock64();
       if (x.mean && re > rb) {                 // Um: this CTA's share of the split partials
         const int n0 = x.rt * TM;
         const int nm = (re - rb) * d.Cp / 2;   // double2 elements of this share of Um
@@ -1435,8 +1437,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_cg_persistent(KParams p, const 
         else if (aw) a_unit(p, sm, tl, rc, tmem, x, (tr1 && threadIdx.x == AW0) ? tr1 : nullptr, nullptr);
         else if (epi) {
           probe_epilogue<CC>(p, sm, tl, rc, tmem, x, mask, tr1, false);
-          __threadfence();                    // this tile's U / Um stores, then its completion
-          epi_sync();
+          epi_sync();                         // this tile's U / Um stores, then EPI0's release
           if (tid == EPI0) dep_signal(cnt1 + x.t);
         }
       }
@@ -1467,8 +1468,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_cg_persistent(KParams p, const 
         }
         else if (epi) {
           probe_epilogue<CC>(p, sm, tl, rc, tmem, x, mask, tr2, help2 && w + G >= n2);
-          __threadfence();                    // this tile's W / Wm / dᵀAd stores, then its completion
-          epi_sync();
+          epi_sync();                         // this tile's W / Wm / dᵀAd stores, then EPI0's release
           if (tid == EPI0) dep_signal(cnt2 + x.t);
         }
       }
