@@ -389,7 +389,7 @@ def cuda_arm(args):
                          "traffic_unit": "DRAM bytes per CG step (ncu --set full of k_cg_persistent / its CG steps)",
                          "kernel": "K1 operator = phases 1-2 of the persistent CG kernel k_cg_persistent (tcgen05 3xTF32), "
                                    "achieved = algorithmic fp32 flop 4*N*D per active column per CG step / the "
-                                   "device-stamped (%globaltimer, grid-barrier to grid-barrier) duration of those phases",
+                                   "device-stamped (%globaltimer) time from the step's grid barrier to the last CTA's end of stage 2",
                          "peak_source": f"{peaks_kind} MEASURED_PEAKS.json bf16 {peaks['bf16_tflops']} TF/s x (1.1/2.25 "
                                         f"tf32/bf16 nominal) / 3 passes; sustained-clock figure {peak_sust:.1f}",
                          "fp32_ffma_peak": fp32_peak_tflops(peaks.get("sm_max_mhz", SM_MAX_MHZ))},
