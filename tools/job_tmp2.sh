@@ -1,1 +1,2 @@
-CMTCS_TRACE_STEP=40 CMTCS_PHASE_LOG=1 timeout 120 python bench.py --config 2 --steps 1 --warmup 0 --no-e2e --no-cpu-baseline 2>&1 | grep -E "cmtcs\]" | grep -E "EM it|epi loop" | head -2 | cut -c1-180
+timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -2
+bash tools/job_ab.sh
