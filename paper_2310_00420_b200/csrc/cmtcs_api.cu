@@ -379,6 +379,7 @@ cmtcs_status one_em_iteration(cmtcs_ctx *c, const uint64_t *probe_bits, const do
         fprintf(stderr, "\n[cmtcs]     epi grp  :"); for (int i = 128; i < 160; ++i) fprintf(stderr, " %.2f", us(i));
         if (ph == 1) {
           for (int q = 0; q < 4; ++q) { fprintf(stderr, "\n[cmtcs]     afull q%d :", q); for (int i = 0; i < 16; ++i) fprintf(stderr, " %.2f", us(160 + 16 * q + i)); }
+          fprintf(stderr, "\n[cmtcs]     mfull    :"); for (int i = 0; i < 16; ++i) fprintf(stderr, " %.2f", us(240 + i));
           fprintf(stderr, "\n[cmtcs]     mdone    :"); for (int i = 0; i < 16; ++i) fprintf(stderr, " %.2f", us(224 + i));
         }
         if (ph == 0) { fprintf(stderr, "\n[cmtcs]     update (kcyc from phase start): start %.2f gam %.2f pass1 %.2f xi %.2f end %.2f", (g[160]-g[168])*1e-3, (g[161]-g[168])*1e-3, (g[162]-g[168])*1e-3, (g[163]-g[168])*1e-3, (g[164]-g[168])*1e-3); }

@@ -127,7 +127,8 @@ struct KParams {
   const double *q_override;    // optional
   int trace_step;              // CMTCS_TRACE_STEP (default 5): the CG step CMTCS_PHASE_LOG traces
   int dbg_flags;               // CMTCS_DBG (diagnostics only, wrong results): 1 no DMMA, 2 no tcgen05.mma,
-                               // 4 no tf32 split, 8/16/32 accumulator layouts, 64 no epilogue, 128 no TMA
+                               // 4 no tf32 split, 8/16/32 accumulator layouts, 64 no epilogue, 128 no TMA;
+                               // (results unchanged:) 4096 no 2-MMA form, 16384 no A-warp drain help on mean units
 };
 
 // launchers (return cudaGetLastError())

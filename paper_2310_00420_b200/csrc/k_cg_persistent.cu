@@ -967,6 +967,7 @@ __device__ __forceinline__ void mean_kloop(const KParams &p, unsigned char *sm, 
     rc.next();
     if (x.mean) {
       mbar_wait(&tl.full[st], ph);
+      if (trm && threadIdx.x == EPI0 && kc < 16) trm[16 + kc] = clock64();
       if (!(p.dbg_flags & 1)) {
         const uint32_t base = smem_u32(sm) + (uint32_t)st * tc.stage_bytes;
         if (x.stage == 1) mean_stage<true, NTC>(base, base + mu_off, ew, lane, p.d.C, p.d.Cp, macc);
@@ -1050,8 +1051,15 @@ __device__ __forceinline__ void drain2_groups(const KParams &p, PSmemTail &tl, c
   }
 }
 
-// A warps: the odd column groups of a CTA's last stage-2 tile of the phase (the A warps are idle
-// once its K loop is split; the epilogue warps take the even groups after their fp64 mean work)
+// A warps: the odd column groups of a CTA's last stage-2 tile of the phase, and of every long
+// stage-2 tile carrying fp64 mean columns (help_mean), while the epilogue warps take the even
+// groups after their fp64 mean work.  A long mean unit's pace is the epilogue warps' (DMMA K loop
+// ≈ 1.4-1.7k clk per chunk against ≈ 0.5k of tcgen05 MMAs, then the drain), so the A warps, idle
+// for most of it, halve the drain; on short units (C2: 8 chunks) the MMA warp would stall on the
+// next unit's splits instead (measured C3 +1.9 %, C2 −0.5 % when applied to all mean units).
+__device__ __forceinline__ bool help_mean(const KParams &p, const Unit &x) {
+  return x.mean && x.nk >= 16 && !(p.dbg_flags & 16384);
+}
 template <int CC>
 __device__ void a_help_drain2(const KParams &p, unsigned char *sm, PSmemTail &tl, const RingCtl &rc, const Unit &x) {
   const Dims &d = p.d;
@@ -1464,10 +1472,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_cg_persistent(KParams p, const 
         else if (issuer) mma_unit(p, sm, tl, rc, tmem, x, tr2);
         else if (aw) {
           a_unit(p, sm, tl, rc, tmem, x, (tr2 && threadIdx.x == AW0) ? tr2 : nullptr, tr2 ? tr2 + 160 : nullptr);
-          if (help2 && w + G >= n2 && x.nmma) a_help_drain2<CC>(p, sm, tl, rc, x);
+          if (help2 && x.nmma && (w + G >= n2 || help_mean(p, x))) a_help_drain2<CC>(p, sm, tl, rc, x);
         }
         else if (epi) {
-          probe_epilogue<CC>(p, sm, tl, rc, tmem, x, mask, tr2, help2 && w + G >= n2);
+          probe_epilogue<CC>(p, sm, tl, rc, tmem, x, mask, tr2, help2 && (w + G >= n2 || (x.nmma && help_mean(p, x))));
           epi_sync();                         // this tile's W / Wm / dᵀAd stores, then EPI0's release
           if (tid == EPI0) dep_signal(cnt2 + x.t);
         }

@@ -52,6 +52,7 @@ void run(int nw) {
          cudaGetErrorString(cudaGetLastError()));
 }
 int main() {
+  run<1, 0>(1); run<2, 0>(1); run<1, 0>(4); run<2, 0>(4);   // NACC = 1: the dependent-chain latency
   for (int nw : {1, 4, 8}) {
     run<4, 0>(nw); run<4, 1>(nw); run<4, 2>(nw); run<8, 0>(nw); run<8, 1>(nw); run<8, 2>(nw);
   }
