@@ -177,6 +177,18 @@ def test_single_em_step_mixed_accumulator_layouts(torch_cuda):
     assert np.all(np.abs(post["logdet"] - orc["nu"]) <= nu_tol(orc["nu"]))
 
 
+def test_single_em_step_long_mean_tiles(torch_cuda):
+    """N = 600 (ragged, 19 stage-2 chunks ≥ 16): every stage-2 tile carrying the fp64 mean columns
+    is drained by the epilogue and A warps together (help_mean), not only a CTA's last tile."""
+    data = synthetic.small_problem(T=12, C=2, N=600, D=1024, K=6, sigma=0.01, seed=19, support=30)
+    alpha = np.random.default_rng(11).uniform(0.5, 4.0, (2, 1024))
+    post, info, orc, a_next, conv = _single_step(data, alpha, 1, cap=800, tol=1e-7)
+    e = compare_step(post, info, orc, a_next, conv)
+    print("long mean tiles", e, "converged", conv.sum(), "/", conv.size)
+    assert e["mu"] <= MU_TOL and conv.any() and e["s_conv"] <= S_TOL and e["q_abs"] <= Q_TOL and e["L_abs"] <= L_TOL
+    assert np.all(np.abs(post["logdet"] - orc["nu"]) <= nu_tol(orc["nu"]))
+
+
 def test_single_em_step_many_column_tiles(torch_cuda):
     """P = C·K = 16·9 = 144 > two 64-column tiles, C = 16 (the maximum), 1 task per... ."""
     data = synthetic.small_problem(T=2, C=16, N=48, D=128, K=9, sigma=0.05, seed=12, support=5)
