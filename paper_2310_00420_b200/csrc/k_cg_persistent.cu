@@ -118,7 +118,7 @@ __device__ __forceinline__ void grid_sync(unsigned *bar, unsigned &epoch) {
   epoch += 1;
   if (threadIdx.x == 0) {
     const unsigned target = epoch * gridDim.x;
-    __threadfence();
+    // the release is cumulative over the CTA's writes ordered before it by the barrier above
     asm volatile("red.release.gpu.global.add.u32 [%0], 1;\n" ::"l"(bar) : "memory");
     unsigned v;
     do {   // relaxed polling (no L1 invalidation per poll), one acquire fence once released
@@ -1491,23 +1491,25 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_cg_persistent(KParams p, const 
                           ? reinterpret_cast<float4 *>(sm) + (size_t)warp * (d.D / 2) : nullptr;
     for (int w = b * (NTHREADS / 32) + warp; w < ncols; w += G * (NTHREADS / 32)) {
       const int t = w / (d.P + d.C), j = w % (d.P + d.C);
+      // the column's flag is written only by this warp's own update (the same column every step):
+      // read it before the wait, and issue the task-activity mark early (its result is used last)
+      const bool active = j < d.P ? ldv(p.b.flag + (size_t)t * d.P + j) == 1
+                                  : ldv(p.b.flagm + (size_t)t * d.C + (j - d.P)) == 1;
+      const int tm_old = (active && lane == 0) ? atomicMax(p.b.tmark + t, u + 1) : u + 1;
       if (lane == 0) dep_wait(cnt2 + t, (u + 1) * E2);   // W, dᵀAd of task t complete
       __syncwarp();
-      bool active;
       if (j < d.P) {
-        active = ldv(p.b.flag + (size_t)t * d.P + j) == 1;
         if (active) {
           if (lane == 0) atomicAdd(p.b.hist + u, 1);
           update_probe(p, t, j, u, lane, stage_d, (tr3 && w == b * (NTHREADS / 32) + warp && lane == 0) ? tr3 : nullptr);
         }
       } else {
-        active = ldv(p.b.flagm + (size_t)t * d.C + (j - d.P)) == 1;
         if (active) {
           if (lane == 0) atomicAdd(p.b.histm + u, 1);
           update_mean(p, t, j - d.P, u, lane);
         }
       }
-      if (active && lane == 0 && atomicMax(p.b.tmark + t, u + 1) < u + 1) atomicAdd(p.b.histt + u, 1);
+      if (tm_old < u + 1) atomicAdd(p.b.histt + u, 1);
     }
     grid_sync(bar, epoch);
     if (b == 0 && tid == 0) {
