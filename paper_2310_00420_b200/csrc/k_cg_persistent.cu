@@ -433,6 +433,22 @@ __device__ void update_probe(const KParams &p, int t, int col, int u, int lane, 
   if (tr) tr[0] = clock64();
   const Dims &d = p.d;
   const size_t g = (size_t)t * d.P + col;
+  float4 *__restrict__ x4 = reinterpret_cast<float4 *>(p.b.X + g * d.D);
+  float4 *__restrict__ r4 = reinterpret_cast<float4 *>(p.b.R + g * d.D);
+  float4 *__restrict__ d4 = reinterpret_cast<float4 *>(p.b.D32 + g * d.D);
+  float4 *__restrict__ dh4 = reinterpret_cast<float4 *>(p.b.Dh + g * d.D);
+  float4 *__restrict__ dl4 = reinterpret_cast<float4 *>(p.b.Dl + g * d.D);
+  const float4 *__restrict__ w4 = reinterpret_cast<const float4 *>(p.b.W + g * d.D);
+  const int n4 = d.D >> 2;
+  constexpr int U = 2;   // float4 per lane in flight (per array)
+  // the first block of the pass is loaded before the dᵀAd reduction (independent of it: one
+  // dependent global round trip less per column)
+  float4 dd[U], wv[U], xv[U], rv[U];
+#pragma unroll
+  for (int v = 0; v < U; ++v) {
+    const int i = lane + 32 * v;
+    if (i < n4) { dd[v] = ldv(d4 + i); wv[v] = __ldcg(w4 + i); xv[v] = ldv(x4 + i); rv[v] = ldv(r4 + i); }
+  }
   // the per-row-tile partials of dᵀAd: one load per lane, then the warp's fixed-order butterfly
   double dpart = 0.0;
   // W and the dᵀAd partials come from other CTAs' stage 2 (acquired through the task counter, no
@@ -452,21 +468,14 @@ __device__ void update_probe(const KParams &p, int t, int col, int u, int lane, 
   const float gamf = (float)(rr / dAd);
   const double gam = (double)gamf;
   if (tr) tr[1] = clock64();
-  float4 *__restrict__ x4 = reinterpret_cast<float4 *>(p.b.X + g * d.D);
-  float4 *__restrict__ r4 = reinterpret_cast<float4 *>(p.b.R + g * d.D);
-  float4 *__restrict__ d4 = reinterpret_cast<float4 *>(p.b.D32 + g * d.D);
-  float4 *__restrict__ dh4 = reinterpret_cast<float4 *>(p.b.Dh + g * d.D);
-  float4 *__restrict__ dl4 = reinterpret_cast<float4 *>(p.b.Dl + g * d.D);
-  const float4 *__restrict__ w4 = reinterpret_cast<const float4 *>(p.b.W + g * d.D);
-  const int n4 = d.D >> 2;
   double acc = 0.0;
-  constexpr int U = 2;   // float4 per lane in flight (per array)
   for (int i0 = lane; i0 < n4; i0 += 32 * U) {
-    float4 dd[U], wv[U], xv[U], rv[U];
+    if (i0 != lane) {
 #pragma unroll
-    for (int v = 0; v < U; ++v) {
-      const int i = i0 + 32 * v;
-      if (i < n4) { dd[v] = ldv(d4 + i); wv[v] = __ldcg(w4 + i); xv[v] = ldv(x4 + i); rv[v] = ldv(r4 + i); }
+      for (int v = 0; v < U; ++v) {
+        const int i = i0 + 32 * v;
+        if (i < n4) { dd[v] = ldv(d4 + i); wv[v] = __ldcg(w4 + i); xv[v] = ldv(x4 + i); rv[v] = ldv(r4 + i); }
+      }
     }
 #pragma unroll
     for (int v = 0; v < U; ++v) {
