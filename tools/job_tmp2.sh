@@ -1,3 +1,2 @@
-python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" 2>&1 | tail -1
-bash tools/job_profile.sh
-timeout 300 python bench.py --config 1 --steps 10 --warmup 5 --no-cpu-baseline > gpurun_out/bench_c1.json 2> gpurun_out/bench_c1.err
+timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -2
+bash tools/job_ab_small.sh
