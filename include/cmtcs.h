@@ -82,6 +82,10 @@ typedef struct cmtcs_step_info {
   int64_t mean_col_iters;    /* Σ_u (#active mean columns at step u), this rank                */
   int64_t task_iters;        /* Σ_u (#tasks with ≥ 1 active column at step u), this rank       */
   int64_t kernel_launches;   /* kernels this library launched during the call                  */
+  int64_t tile_col_iters;    /* Σ_u probe columns the operator multiplied at step u: the MMA
+                                widths of every column tile with ≥ 1 active column (retired
+                                columns inside such a tile are multiplied too; padded work ≥
+                                probe_col_iters), this rank                                      */
 } cmtcs_step_info;
 
 typedef struct cmtcs_ctx cmtcs_ctx;
@@ -138,13 +142,23 @@ void cmtcs_destroy(cmtcs_ctx *ctx);
 /* Total kernels this library launched on ctx since cmtcs_init (launch-count evidence). */
 int64_t cmtcs_kernel_launches(const cmtcs_ctx *ctx);
 
-/* Live kernel timing with CUDA events recorded on the context's stream around every launch of
- * the operator (K1: stage 1 + stage 2 of one CG step) and of the CG update (K4).  enable = 0|1.
- * cmtcs_get_timing returns accumulated device milliseconds ms[0] = operator, ms[1] = update,
- * ms[2] = everything else in em_step, and the matching counts of CG steps in n[0..1] (n[2] = EM
- * iterations) since the last reset; reset = 1 clears the accumulators after reading. */
+/* Live device timing of em_step (enable = 0|1).  cmtcs_get_timing returns accumulated
+ * milliseconds since the last reset (reset = 1 clears after reading):
+ *   ms[0] operator phases (stages 1-2) of every CG step, ms[1] update phase (Alg. 1 lines 3-7):
+ *         %globaltimer stamps taken inside the persistent CG kernel at its step boundaries;
+ *   ms[2] everything in em_step after the CG kernel (estimators, M-step): CUDA events;
+ *   ms[3] the whole persistent CG kernel: CUDA events recorded on the context's stream
+ *         immediately before and after its launch;
+ * n[0..1] CG steps, n[2..3] EM iterations. */
 cmtcs_status cmtcs_set_timing(cmtcs_ctx *ctx, int32_t enable);
-cmtcs_status cmtcs_get_timing(cmtcs_ctx *ctx, double ms[3], int64_t n[3], int32_t reset);
+cmtcs_status cmtcs_get_timing(cmtcs_ctx *ctx, double ms[4], int64_t n[4], int32_t reset);
+
+/* This rank's Eq. 4 sums of the last em_step, BEFORE the all-reduce (Alg. 2 lines
+ * 14-15): out (host or device) fp64 [C·D + C + 1] = [den_cd = Σ_t q_tc(μ²_tcd + max(s_tcd, floor))
+ * row-major | num_c = Σ_t q_tc | Σ_t log p(y_t|θ̂)], t over this rank's tasks.  Summing the
+ * outputs of the ranks gives the all-reduced sums the M-step uses (multi-GPU tests).
+ * ESTATE before any em_step. */
+cmtcs_status cmtcs_estep_sums(cmtcs_ctx *ctx, double *out);
 
 /* ---- stateless kernel entry points (unit tests / benchmarks; all pointers device) ------- */
 

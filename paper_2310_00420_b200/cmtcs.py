@@ -19,7 +19,7 @@ STATUS = {0: "CMTCS_OK", 1: "CMTCS_EINVAL", 2: "CMTCS_ENOMEM", 3: "CMTCS_ECUDA",
 EXPORTED = ["cmtcs_get_unique_id", "cmtcs_workspace_size", "cmtcs_init", "cmtcs_em_step",
             "cmtcs_posterior", "cmtcs_set_state", "cmtcs_transcript", "cmtcs_last_error",
             "cmtcs_destroy", "cmtcs_kernel_launches", "cmtcs_probe_words", "cmtcs_lanczos_quadrature",
-            "cmtcs_set_timing", "cmtcs_get_timing"]
+            "cmtcs_set_timing", "cmtcs_get_timing", "cmtcs_estep_sums"]
 
 
 class CmtcsError(RuntimeError):
@@ -43,7 +43,7 @@ class cmtcs_step_info(ctypes.Structure):
                 ("probe_steps_min", c_int32), ("probe_steps_max", c_int32),
                 ("probe_steps_mean", c_double), ("n_cap_hit", c_int64),
                 ("probe_col_iters", c_int64), ("mean_col_iters", c_int64),
-                ("task_iters", c_int64), ("kernel_launches", c_int64)]
+                ("task_iters", c_int64), ("kernel_launches", c_int64), ("tile_col_iters", c_int64)]
 
     def as_dict(self) -> dict:
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -85,6 +85,8 @@ def _load() -> ctypes.CDLL:
     lib.cmtcs_set_timing.restype = st
     lib.cmtcs_get_timing.argtypes = [vp, POINTER(c_double), POINTER(c_int64), c_int32]
     lib.cmtcs_get_timing.restype = st
+    lib.cmtcs_estep_sums.argtypes = [vp, vp]
+    lib.cmtcs_estep_sums.restype = st
     return lib
 
 
@@ -173,8 +175,12 @@ def cmtcs_set_timing(ctx: int, enable: bool):
 
 
 def cmtcs_get_timing(ctx: int, reset: bool = False) -> dict:
-    ms = (c_double * 3)()
-    n = (c_int64 * 3)()
+    ms = (c_double * 4)()
+    n = (c_int64 * 4)()
     _check(_lib.cmtcs_get_timing(ctx, ms, n, 1 if reset else 0), ctx)
-    return dict(op_ms=ms[0], update_ms=ms[1], other_ms=ms[2], op_launch_pairs=n[0],
-                update_launches=n[1], em_iters=n[2])
+    return dict(op_ms=ms[0], update_ms=ms[1], other_ms=ms[2], cg_kernel_ms=ms[3], op_steps=n[0],
+                update_steps=n[1], em_iters=n[2], cg_kernel_launches=n[3])
+
+
+def cmtcs_estep_sums(ctx: int, out_ptr: int):
+    _check(_lib.cmtcs_estep_sums(ctx, out_ptr), ctx)

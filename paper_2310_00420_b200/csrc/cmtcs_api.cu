@@ -34,8 +34,8 @@ struct cmtcs_ctx {
   bool timing;
   cudaEvent_t tev[3];
   unsigned long long *h_ts;  // pinned [cap][4]
-  double t_ms[3];
-  int64_t t_n[3];
+  double t_ms[4];
+  int64_t t_n[4];
   // the CG loop: one persistent kernel per E-step (k_cg_persistent.cu), one CTA per SM
   TcMaps maps;
   int grid;
@@ -233,10 +233,12 @@ size_t carve(const Dims &d, char *base, Bufs *b) {
   b->q = cv.take<double>(Tl * C);
   b->ll = cv.take<double>(Tl);
   b->red = cv.take<double>(C * D + C + 1);
+  b->red_local = cv.take<double>(C * D + C + 1);
   b->alive = cv.take<int>(cap);
   b->hist = cv.take<int>(cap);
   b->histm = cv.take<int>(cap);
   b->histt = cv.take<int>(cap);
+  b->histp = cv.take<int>(cap);
   b->status = cv.take<int>(8);
   b->u = cv.take<int>(1);
   b->ts = cv.take<unsigned long long>((size_t)cap * 4 + 512);   // + 2 × 256 diagnostic stamps
@@ -264,12 +266,14 @@ __global__ void k_check_alpha(const double *a, int n, int *bad) {
 cmtcs_status set_alpha(cmtcs_ctx *c, const double *alpha) {
   const Dims &d = c->kp.d;
   const size_t n = (size_t)d.C * d.D;
-  CUDA_OK(c, cudaMemcpyAsync(c->kp.b.alpha64, alpha, n * sizeof(double), cudaMemcpyDefault, c->stream));
+  // validated in scratch (red, rewritten by every M-step) so that a rejected α leaves the state intact
+  CUDA_OK(c, cudaMemcpyAsync(c->kp.b.red, alpha, n * sizeof(double), cudaMemcpyDefault, c->stream));
   CUDA_OK(c, cudaMemsetAsync(c->kp.b.status + 4, 0, sizeof(int), c->stream));
-  k_check_alpha<<<64, 256, 0, c->stream>>>(c->kp.b.alpha64, (int)n, c->kp.b.status + 4);
+  k_check_alpha<<<64, 256, 0, c->stream>>>(c->kp.b.red, (int)n, c->kp.b.status + 4);
   CUDA_OK(c, cudaMemcpyAsync(c->h_status + 4, c->kp.b.status + 4, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
   CUDA_OK(c, cudaStreamSynchronize(c->stream));
   if (c->h_status[4]) return fail(c, CMTCS_EINVAL, "alpha must be finite and > 0 everywhere");
+  CUDA_OK(c, cudaMemcpyAsync(c->kp.b.alpha64, c->kp.b.red, n * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
   k_alpha_copy<<<64, 256, 0, c->stream>>>(c->kp.b.alpha64, c->kp.b.alpha32, nullptr, nullptr, (int)n, d.C);
   CUDA_OK(c, cudaGetLastError());
   CUDA_OK(c, launch_alpha_stats(c->kp, c->stream));
@@ -299,6 +303,7 @@ cmtcs_status one_em_iteration(cmtcs_ctx *c, const uint64_t *probe_bits, const do
   CUDA_OK(c, cudaMemsetAsync(kp.b.hist, 0, sizeof(int) * d.cap, s));
   CUDA_OK(c, cudaMemsetAsync(kp.b.histm, 0, sizeof(int) * d.cap, s));
   CUDA_OK(c, cudaMemsetAsync(kp.b.histt, 0, sizeof(int) * d.cap, s));
+  CUDA_OK(c, cudaMemsetAsync(kp.b.histp, 0, sizeof(int) * d.cap, s));
   CUDA_OK(c, cudaMemsetAsync(kp.b.tmark, 0, sizeof(int) * d.Tl, s));
   CUDA_OK(c, launch_init_columns(kp, s));
   L += 1;
@@ -319,6 +324,9 @@ cmtcs_status one_em_iteration(cmtcs_ctx *c, const uint64_t *probe_bits, const do
   // ---- M-step (Eq. 4): local sums → all-reduce over ranks → α update ----
   CUDA_OK(c, launch_mstep_partial(kp, s));
   L += 5;
+  // this rank's Eq. 4 sums before the all-reduce (cmtcs_estep_sums)
+  CUDA_OK(c, cudaMemcpyAsync(kp.b.red_local, kp.b.red, sizeof(double) * ((size_t)d.C * d.D + d.C + 1),
+                             cudaMemcpyDeviceToDevice, s));
   if (c->have_comm)
     NCCL_OK(c, ncclAllReduce(kp.b.red, kp.b.red, (size_t)d.C * d.D + d.C + 1, ncclDouble, ncclSum, c->comm, s));
   CUDA_OK(c, launch_mstep_finish(kp, s));
@@ -387,12 +395,15 @@ cmtcs_status one_em_iteration(cmtcs_ctx *c, const uint64_t *probe_bits, const do
 
       }
     }
-    float ms = 0.f;
+    float ms = 0.f, mk = 0.f;
     CUDA_OK(c, cudaEventElapsedTime(&ms, c->tev[1], c->tev[2]));
+    CUDA_OK(c, cudaEventElapsedTime(&mk, c->tev[0], c->tev[1]));
     c->t_ms[2] += ms;
+    c->t_ms[3] += mk;
     c->t_n[0] += steps_run;
     c->t_n[1] += steps_run;
     c->t_n[2] += 1;
+    c->t_n[3] += 1;
   }
   const int it = c->em_iter;
   c->em_iter += 1;
@@ -416,6 +427,7 @@ cmtcs_status one_em_iteration(cmtcs_ctx *c, const uint64_t *probe_bits, const do
     info->probe_col_iters = (int64_t)o[6];
     info->mean_col_iters = (int64_t)o[7];
     info->task_iters = (int64_t)o[8];
+    info->tile_col_iters = (int64_t)o[9];
     info->kernel_launches = L;
   }
   return CMTCS_OK;
@@ -478,7 +490,6 @@ cmtcs_status cmtcs_init(cmtcs_ctx **out, const cmtcs_problem *p, const float *ph
   c->kp.d = d;
   c->kp.b = b;
   c->kp.tc = make_tc(d);
-  c->kp.tc.pf = getenv("CMTCS_PF") ? atoi(getenv("CMTCS_PF")) : 0;
   c->kp.phi = phi;
   c->kp.y = y;
   c->kp.beta = p->beta;
@@ -501,6 +512,9 @@ cmtcs_status cmtcs_init(cmtcs_ctx **out, const cmtcs_problem *p, const float *ph
   CUDA_OK(c, cudaMemsetAsync(b.gam, 0, sizeof(double) * d.Tl * d.P * d.cap, c->stream));
   CUDA_OK(c, cudaMemsetAsync(b.xi, 0, sizeof(double) * d.Tl * d.P * d.cap, c->stream));
   CUDA_OK(c, cudaMemsetAsync(b.Um, 0, sizeof(double) * (size_t)d.Tl * d.N * d.Cp, c->stream));
+  // U's padding rows P..Pp−1 of each task are B-tile rows past the tile's columns: keep them finite
+  CUDA_OK(c, cudaMemsetAsync(b.Uh, 0, sizeof(float) * (size_t)d.Tl * d.Pp * d.N, c->stream));
+  CUDA_OK(c, cudaMemsetAsync(b.Ul, 0, sizeof(float) * (size_t)d.Tl * d.Pp * d.N, c->stream));
   CUDA_OK(c, cudaMemsetAsync(b.tilecnt, 0, sizeof(int) * d.Tl * d.nCT * d.nRT1, c->stream));
   c->grid = cg_grid_size(c->kp);
   if (c->grid < 1) return fail(c, CMTCS_ECUDA, "persistent CG kernel cannot be made resident (smem %zu bytes)",
@@ -595,6 +609,17 @@ cmtcs_status cmtcs_transcript(cmtcs_ctx *c, double *gamma, double *xi, int32_t *
   return CMTCS_OK;
 }
 
+cmtcs_status cmtcs_estep_sums(cmtcs_ctx *c, double *out) {
+  if (!c || !out) return fail(c, CMTCS_EINVAL, "ctx and out must be non-NULL");
+  if (c->broken) return CMTCS_ESTATE;
+  if (!c->have_estep) return fail(c, CMTCS_ESTATE, "E-step sums requested before any em_step");
+  const Dims &d = c->kp.d;
+  CUDA_OK(c, cudaMemcpyAsync(out, c->kp.b.red_local, sizeof(double) * ((size_t)d.C * d.D + d.C + 1),
+                             cudaMemcpyDefault, c->stream));
+  CUDA_OK(c, cudaStreamSynchronize(c->stream));
+  return CMTCS_OK;
+}
+
 const char *cmtcs_last_error(const cmtcs_ctx *c) { return c ? c->err : g_err; }
 
 void cmtcs_destroy(cmtcs_ctx *c) {
@@ -621,9 +646,9 @@ cmtcs_status cmtcs_set_timing(cmtcs_ctx *c, int32_t enable) {
   return CMTCS_OK;
 }
 
-cmtcs_status cmtcs_get_timing(cmtcs_ctx *c, double ms[3], int64_t n[3], int32_t reset) {
+cmtcs_status cmtcs_get_timing(cmtcs_ctx *c, double ms[4], int64_t n[4], int32_t reset) {
   if (!c) return fail(nullptr, CMTCS_EINVAL, "ctx is NULL");
-  for (int i = 0; i < 3; ++i) {
+  for (int i = 0; i < 4; ++i) {
     if (ms) ms[i] = c->t_ms[i];
     if (n) n[i] = c->t_n[i];
     if (reset) { c->t_ms[i] = 0; c->t_n[i] = 0; }

@@ -65,10 +65,13 @@ struct Bufs {
   double *nu, *ell, *q;  // [Tl][C]
   double *ll;        // [Tl]
   double *red;       // [C*D + C + 1]  Eq. 4 sums (den, num) and Σ_t log p(y_t)
+  double *red_local; // [C*D + C + 1]  the same before the all-reduce (this rank's tasks)
   int *alive;        // [cap]  columns still active after step u
   int *hist;         // [cap]  probe columns active at step u
   int *histm;        // [cap]  mean columns active at step u
   int *histt;        // [cap]  tasks with an active column at step u
+  int *histp;        // [cap]  probe columns the operator multiplied at step u (MMA widths of the
+                     //        column tiles with ≥ 1 active column, per task: padded work)
   int *status;       // [8]    first error: code, t, col, u
   int *u;            // [1]    current CG step (device-side loop counter of the CG graph)
   unsigned long long *ts;  // [cap][4] per-step %globaltimer stamps taken by CTA 0 after the grid
@@ -93,22 +96,22 @@ struct TcCfg {
   int nacc;          // K-split main accumulators ((1 + nacc)·slot ≤ acol0)
   int stages;        // smem pipeline depth
   unsigned stage_bytes;
-  int pf;            // L2 prefetch distance of the producer (chunks ahead; 0 = off)
   int use_dtile;     // stage-2 epilogue reads its d tile (NT × 128 fp32) from smem, staged by TMA
   unsigned dtile_bytes;
 };
 
 // TMA descriptors (host-encoded, passed as a __grid_constant__ kernel parameter)
 struct TcMaps {
-  CUtensorMap phi;             // fp32 Φ (the caller's) [rows Tl·N][cols D], box 32 × 128, SW128
-  CUtensorMap phit;            // fp32 Φᵀ [rows Tl·D][cols N], box 32 × 128, SW128
-  CUtensorMap u_h, u_l;        // U = ΦD split [rows Tl·Pp][cols N], box 32 × NT, SW128
-  CUtensorMap d_h, d_l;        // directions split [rows Tl·P][cols D], box 32 × NT, SW128
-  CUtensorMap dm;              // fp64 [rows Tl·C][cols D], box 32 × C (mean directions)
-  CUtensorMap um;              // fp64 [rows Tl·N][cols Cp], box Cp × 32 (Φ·d of the mean columns)
-  CUtensorMap d32;             // fp32 [rows Tl·P][cols D], box 128 × NT (probe directions, epilogue)
-  CUtensorMap u_hl, d_hl;      // the hi and lo arrays as one 3-D tensor [2][rows][cols], box 32 × NT × 2:
-                               // both B tiles of a stage with one TMA (hi tile, then lo tile)
+  // every map is per task, [task][rows][cols] (box depth 1 in the task dimension): a tile or K chunk
+  // overhanging a task's matrix is zero-filled instead of reading the next task's data
+  CUtensorMap phi;             // fp32 Φ (the caller's) [Tl or 1][N][D], box 32 × 128, SW128
+  CUtensorMap phit;            // fp32 Φᵀ [Tl or 1][D][N], box 32 × 128, SW128
+  CUtensorMap dm;              // fp64 [Tl][C][D], box 32 × C (mean directions)
+  CUtensorMap um;              // fp64 [Tl][N][Cp], box Cp × 32 (Φ·d of the mean columns)
+  CUtensorMap d32;             // fp32 [Tl][P][D], box 128 × NT (probe directions, epilogue)
+  CUtensorMap u_hl, d_hl;      // U = ΦD [Tl][Pp][N] and the directions [Tl][P][D] as their exact tf32
+                               // pairs, hi and lo arrays viewed as one 4-D tensor [2][Tl][rows][cols],
+                               // box 32 × NT × 1 × 2: both B tiles of a stage with one TMA
 };
 
 struct KParams {

@@ -95,12 +95,6 @@ __device__ __forceinline__ void stv(T *p, T v) { *p = v; }
 __device__ __forceinline__ void fence_proxy_async_global() {
   asm volatile("fence.proxy.async.global;\n" ::: "memory");
 }
-// TMA prefetch of a tile into L2 (no shared memory, no completion tracking)
-__device__ __forceinline__ void tma_prefetch_2d(const CUtensorMap *map, int x, int y) {
-  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];\n" ::"l"(
-                   reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y)
-               : "memory");
-}
 
 __device__ __forceinline__ void mbar_arrive(uint64_t *mbar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(mbar)) : "memory");
@@ -113,7 +107,9 @@ __device__ __forceinline__ void pair_sync() { asm volatile("bar.sync 3, 256;\n" 
 // grid-wide barrier over the co-resident CTAs: a monotonically increasing arrival counter
 // (reset to 0 before every launch); epoch e completes when the counter reaches e·gridDim.x
 __device__ __forceinline__ void grid_sync(unsigned *bar, unsigned &epoch) {
-  fence_proxy_async_global();                 // this thread's generic writes → later TMA reads
+  // this thread's generic writes → later async-proxy accesses: global (TMA reads of d, U) and
+  // shared (the update phase parks d / r in the idle ring, which the next step's TMA overwrites)
+  asm volatile("fence.proxy.async;\n" ::: "memory");
   __syncthreads();
   epoch += 1;
   if (threadIdx.x == 0) {
@@ -680,8 +676,8 @@ __device__ __forceinline__ Unit make_unit1(const Dims &d, const TcCfg &tc, int w
   x.k0 = x.sp * d.K1;
   const int ke = min(d.D, x.k0 + d.K1);
   x.nk = (ke - x.k0 + TK - 1) / TK;
-  x.arow = (d.shared_phi ? 0 : x.t * d.N) + x.rt * TM;
-  x.brow = x.t * d.P + j0;
+  x.arow = x.rt * TM;                              // row of Φ_t (per-task maps)
+  x.brow = j0;                                     // first direction column of the tile
   return x;
 }
 __device__ __forceinline__ Unit make_unit2(const Dims &d, const TcCfg &tc, int w, int G) {
@@ -700,8 +696,8 @@ __device__ __forceinline__ Unit make_unit2(const Dims &d, const TcCfg &tc, int w
   x.ncol = min(tc.NT, d.P - j0);
   x.k0 = 0;
   x.nk = (d.N + TK - 1) / TK;
-  x.arow = (d.shared_phi ? 0 : x.t * d.D) + x.rt * TM;
-  x.brow = x.t * d.Pp + j0;
+  x.arow = x.rt * TM;                              // row of Φ_tᵀ
+  x.brow = j0;
   return x;
 }
 
@@ -773,34 +769,19 @@ __device__ __forceinline__ void produce(const KParams &p, const TcMaps &mp, unsi
     }
     mbar_arrive_expect_tx_warp(fb, bytes);
     const int k = x.k0 + kc * TK;
-    // L2 prefetch PF chunks ahead: HBM latency is hidden beyond the depth of the smem ring
-    const int kp = kc + p.tc.pf;
-    if (p.tc.pf && kp < x.nk && (threadIdx.x & 31) == 0) {
-      const int kk = x.k0 + kp * TK;
-      if (x.stage == 1) {
-        tma_prefetch_2d(&mp.phi, kk, x.arow);
-        if (x.nmma) tma_prefetch_2d(&mp.d_h, kk, x.brow);
-      } else {
-        tma_prefetch_2d(&mp.phit, kk, x.arow);
-        if (x.nmma) tma_prefetch_2d(&mp.u_h, kk, x.brow);
-      }
-    }
-    if (kc == 0 && p.tc.pf && (threadIdx.x & 31) == 0) {   // the first chunks of the unit
-      for (int k2 = 1; k2 < min(p.tc.pf, x.nk); ++k2) {
-        const int kk = x.k0 + k2 * TK;
-        tma_prefetch_2d(x.stage == 1 ? &mp.phi : &mp.phit, kk, x.arow);
-        if (x.nmma) tma_prefetch_2d(x.stage == 1 ? &mp.d_h : &mp.u_h, kk, x.brow);
-      }
-    }
     // stage layout: fp32 A tile | B hi | B lo | fp64 mean-column chunk
+    // every operand map is per task ([task][rows][cols]): a box never reaches into the next task's
+    // rows (out-of-range rows and K columns are zero-filled), so tasks are isolated even where a tile
+    // or a K chunk overhangs the task's matrix
+    const int at = p.d.shared_phi ? 0 : x.t;
     if (x.stage == 1) {
-      tma_load_2d_warp(base, &mp.phi, k, x.arow, fb);
-      if (x.nmma) tma_load_3d_warp(base + A_BYTES, &mp.d_hl, k, x.brow, 0, fb);   // hi | lo tiles
-      if (x.mean) tma_load_2d_warp(base + A_BYTES + 2 * b_bytes, &mp.dm, k, x.t * p.d.C, fb);
+      tma_load_3d_warp(base, &mp.phi, k, x.arow, at, fb);
+      if (x.nmma) tma_load_4d_warp(base + A_BYTES, &mp.d_hl, k, x.brow, x.t, 0, fb);   // hi | lo tiles
+      if (x.mean) tma_load_3d_warp(base + A_BYTES + 2 * b_bytes, &mp.dm, k, 0, x.t, fb);
     } else {
-      tma_load_2d_warp(base, &mp.phit, k, x.arow, fb);
-      if (x.nmma) tma_load_3d_warp(base + A_BYTES, &mp.u_hl, k, x.brow, 0, fb);
-      if (x.mean) tma_load_2d_warp(base + A_BYTES + 2 * b_bytes, &mp.um, 0, x.t * p.d.N + k, fb);
+      tma_load_3d_warp(base, &mp.phit, k, x.arow, at, fb);
+      if (x.nmma) tma_load_4d_warp(base + A_BYTES, &mp.u_hl, k, x.brow, x.t, 0, fb);
+      if (x.mean) tma_load_3d_warp(base + A_BYTES + 2 * b_bytes, &mp.um, 0, k, x.t, fb);
     }
     if (tr && kc < 16 && (threadIdx.x & 31) == 0) tr[16 + kc] = clock64();
   }
@@ -813,7 +794,7 @@ __device__ __forceinline__ void produce(const KParams &p, const TcMaps &mp, unsi
       if ((threadIdx.x & 31) == 0) mbar_arrive(&tl.dfull);
     } else {
       mbar_arrive_expect_tx_warp(&tl.dfull, p.tc.dtile_bytes);
-      tma_load_2d_warp(dt, &mp.d32, x.rt * TM, x.t * p.d.P + x.ct * p.tc.NT, &tl.dfull);
+      tma_load_3d_warp(dt, &mp.d32, x.rt * TM, x.ct * p.tc.NT, x.t, &tl.dfull);
     }
     rc.di++;
   }
@@ -1078,8 +1059,12 @@ __device__ void a_help_drain2(const KParams &p, unsigned char *sm, PSmemTail &tl
 #pragma unroll
   for (int c = 0; c < CC; ++c) alpha[c] = (c < d.C && dd < d.D) ? __ldg(p.b.alpha32 + (size_t)c * d.D + dd) : 0.f;
   pair_sync();
+  // the epilogue waited on tfull; this barrier plus the fence orders these warps' tcgen05.ld after
+  // the MMAs' completion (tcgen05 memory model: thread sync, then fence::after_thread_sync)
+  fence_after_sync();
   drain2_groups<CC>(p, tl, x, tl.help_tacc, unit_nacc(tc, x.nk, p.dbg_flags),
                     reinterpret_cast<const float *>(sm + (size_t)rc.S * tc.stage_bytes), alpha, 1, 2);
+  fence_before_sync();                        // these tcgen05.ld before the epilogue's tempty release
   pair_sync();                                // W stores ordered before the epilogue's completion release
 }
 
@@ -1412,8 +1397,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_cg_persistent(KParams p, const 
     fence_mbar_init();
   }
   if (warp == 0 && lane == 0) {
-    prefetch_tmap(&mp.phi); prefetch_tmap(&mp.phit); prefetch_tmap(&mp.u_h); prefetch_tmap(&mp.u_l);
-    prefetch_tmap(&mp.d_h); prefetch_tmap(&mp.d_l);
+    prefetch_tmap(&mp.phi); prefetch_tmap(&mp.phit); prefetch_tmap(&mp.u_hl); prefetch_tmap(&mp.d_hl);
     prefetch_tmap(&mp.dm); prefetch_tmap(&mp.um); prefetch_tmap(&mp.d32);
   }
   if (warp == 2) tmem_alloc<512>(&tl.tslot);
@@ -1484,6 +1468,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_cg_persistent(KParams p, const 
           if (help2 && x.nmma && (w + G >= n2 || help_mean(p, x))) a_help_drain2<CC>(p, sm, tl, rc, x);
         }
         else if (epi) {
+          if (tid == EPI0 && x.rt == 0 && x.nmma) atomicAdd(p.b.histp + u, x.nmma);
           probe_epilogue<CC>(p, sm, tl, rc, tmem, x, mask, tr2, help2 && (w + G >= n2 || (x.nmma && help_mean(p, x))));
           epi_sync();                         // this tile's W / Wm / dᵀAd stores, then EPI0's release
           if (tid == EPI0) dep_signal(cnt2 + x.t);
@@ -1553,29 +1538,30 @@ typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t
                                   const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
-// 2-D tensor map over a row-major [rows][cols] array; box box_cols × box_rows
-bool encode_2d(EncodeTiledFn enc, CUtensorMap *m, const void *ptr, CUtensorMapDataType dt, int esize, long rows,
-               long cols, int box_cols, int box_rows, bool swizzle) {
-  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
-  cuuint64_t strides[1] = {(cuuint64_t)cols * esize};
-  cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
-  cuuint32_t es[2] = {1, 1};
-  return enc(m, dt, 2, const_cast<void *>(ptr), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+// 3-D tensor map over [mats][rows][cols] row-major (one matrix per task); box box_cols × box_rows × 1
+bool encode_3d(EncodeTiledFn enc, CUtensorMap *m, const void *ptr, CUtensorMapDataType dt, int esize, long mats,
+               long rows, long cols, int box_cols, int box_rows, bool swizzle) {
+  cuuint64_t dims[3] = {(cuuint64_t)cols, (cuuint64_t)rows, (cuuint64_t)mats};
+  cuuint64_t strides[2] = {(cuuint64_t)cols * esize, (cuuint64_t)rows * cols * esize};
+  cuuint32_t box[3] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows, 1};
+  cuuint32_t es[3] = {1, 1, 1};
+  return enc(m, dt, 3, const_cast<void *>(ptr), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
              swizzle ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-// 3-D view [2][rows][cols] of two equally shaped row-major fp32 arrays (hi at `hi`, lo at `lo`,
-// lo − hi a multiple of 16 bytes), box box_cols × box_rows × 2, 128-byte swizzle
-bool encode_hilo(EncodeTiledFn enc, CUtensorMap *m, const float *hi, const float *lo, long rows, long cols, int box_cols,
-                 int box_rows) {
+// 4-D view [2][mats][rows][cols] of two equally shaped fp32 arrays (hi at `hi`, lo at `lo`, lo − hi a
+// multiple of 16 bytes), box box_cols × box_rows × 1 × 2, 128-byte swizzle: one TMA brings a task's
+// hi tile and then its lo tile
+bool encode_hilo(EncodeTiledFn enc, CUtensorMap *m, const float *hi, const float *lo, long mats, long rows,
+                 long cols, int box_cols, int box_rows) {
   const long long gap = (long long)((const char *)lo - (const char *)hi);
   if (gap <= 0 || gap % 16) return false;
-  cuuint64_t dims[3] = {(cuuint64_t)cols, (cuuint64_t)rows, 2};
-  cuuint64_t strides[2] = {(cuuint64_t)cols * 4, (cuuint64_t)gap};
-  cuuint32_t box[3] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows, 2};
-  cuuint32_t es[3] = {1, 1, 1};
-  return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float *>(hi), dims, strides, box, es,
+  cuuint64_t dims[4] = {(cuuint64_t)cols, (cuuint64_t)rows, (cuuint64_t)mats, 2};
+  cuuint64_t strides[3] = {(cuuint64_t)cols * 4, (cuuint64_t)rows * cols * 4, (cuuint64_t)gap};
+  cuuint32_t box[4] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows, 1, 2};
+  cuuint32_t es[4] = {1, 1, 1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float *>(hi), dims, strides, box, es,
              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
@@ -1601,17 +1587,14 @@ bool encode_maps(const KParams &p, TcMaps *m, char *why) {
   const long mats = d.shared_phi ? 1 : d.Tl;
   const CUtensorMapDataType F32 = CU_TENSOR_MAP_DATA_TYPE_FLOAT32, F64 = CU_TENSOR_MAP_DATA_TYPE_FLOAT64;
   const int NT = p.tc.NT;
-  const bool ok = encode_2d(enc, &m->phi, p.phi, F32, 4, mats * d.N, d.D, 32, TM, true) &&
-                  encode_2d(enc, &m->phit, b.PT, F32, 4, mats * d.D, d.N, 32, TM, true) &&
-                  encode_2d(enc, &m->u_h, b.Uh, F32, 4, (long)d.Tl * d.Pp, d.N, 32, NT, true) &&
-                  encode_2d(enc, &m->u_l, b.Ul, F32, 4, (long)d.Tl * d.Pp, d.N, 32, NT, true) &&
-                  encode_2d(enc, &m->d_h, b.Dh, F32, 4, (long)d.Tl * d.P, d.D, 32, NT, true) &&
-                  encode_2d(enc, &m->d_l, b.Dl, F32, 4, (long)d.Tl * d.P, d.D, 32, NT, true) &&
-                  encode_2d(enc, &m->dm, b.Dm, F64, 8, (long)d.Tl * d.C, d.D, TK, d.C, false) &&
-                  encode_2d(enc, &m->um, b.Um, F64, 8, (long)d.Tl * d.N, d.Cp, d.Cp, TK, false) &&
-                  encode_2d(enc, &m->d32, b.D32, F32, 4, (long)d.Tl * d.P, d.D, TM, NT, false) &&
-                  encode_hilo(enc, &m->u_hl, b.Uh, b.Ul, (long)d.Tl * d.Pp, d.N, 32, NT) &&
-                  encode_hilo(enc, &m->d_hl, b.Dh, b.Dl, (long)d.Tl * d.P, d.D, 32, NT);
+  const long Tl = d.Tl;
+  const bool ok = encode_3d(enc, &m->phi, p.phi, F32, 4, mats, d.N, d.D, 32, TM, true) &&
+                  encode_3d(enc, &m->phit, b.PT, F32, 4, mats, d.D, d.N, 32, TM, true) &&
+                  encode_3d(enc, &m->dm, b.Dm, F64, 8, Tl, d.C, d.D, TK, d.C, false) &&
+                  encode_3d(enc, &m->um, b.Um, F64, 8, Tl, d.N, d.Cp, d.Cp, TK, false) &&
+                  encode_3d(enc, &m->d32, b.D32, F32, 4, Tl, d.P, d.D, TM, NT, false) &&
+                  encode_hilo(enc, &m->u_hl, b.Uh, b.Ul, Tl, d.Pp, d.N, 32, NT) &&
+                  encode_hilo(enc, &m->d_hl, b.Dh, b.Dl, Tl, d.P, d.D, 32, NT);
   if (!ok) snprintf(why, 256, "cuTensorMapEncodeTiled failed");
   return ok;
 }

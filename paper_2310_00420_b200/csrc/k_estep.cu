@@ -286,8 +286,10 @@ __global__ void k_stats(KParams p) {
     const double s = p.b.stepsm[i];
     mmin = fmin(mmin, s); mmax = fmax(mmax, s); caph += (p.b.flagm[i] == 2);
   }
-  double h = 0, hm = 0, ht = 0;
-  for (int u = tid; u < d.cap; u += blockDim.x) { h += p.b.hist[u]; hm += p.b.histm[u]; ht += p.b.histt[u]; }
+  double h = 0, hm = 0, ht = 0, hp = 0;
+  for (int u = tid; u < d.cap; u += blockDim.x) {
+    h += p.b.hist[u]; hm += p.b.histm[u]; ht += p.b.histt[u]; hp += p.b.histp[u];
+  }
   // min/max via negation trick on sums is not possible; use shared reductions
   __shared__ double red[6][256];
   red[0][tid] = smin; red[1][tid] = smax; red[2][tid] = mmin; red[3][tid] = mmax;
@@ -306,11 +308,12 @@ __global__ void k_stats(KParams p) {
   h = block_sum(h, sh);
   hm = block_sum(hm, sh);
   ht = block_sum(ht, sh);
+  hp = block_sum(hp, sh);
   if (tid == 0) {
     double *o = p.b.stats;
     o[0] = np ? red[0][0] : 0; o[1] = red[1][0]; o[2] = np ? ssum / np : 0;
     o[3] = nm ? red[2][0] : 0; o[4] = red[3][0]; o[5] = caph;
-    o[6] = h; o[7] = hm; o[8] = ht;
+    o[6] = h; o[7] = hm; o[8] = ht; o[9] = hp;
   }
 }
 

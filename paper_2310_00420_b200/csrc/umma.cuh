@@ -1,6 +1,6 @@
 // sm_100a tensor-core helpers (inline PTX): tcgen05 MMA with TMEM accumulators, shared-memory
 // matrix descriptors for the 128-byte-swizzled K-major canonical layout, TMEM alloc / load,
-// mbarriers and TMA bulk-tensor loads.  Used by the 3xTF32 operator (k_operator_tc.cu).
+// mbarriers and TMA bulk-tensor loads.  Used by the persistent CG kernel (k_cg_persistent.cu).
 //
 // Canonical K-major SWIZZLE_128B operand layout (what TMA SWIZZLE_128B writes): rows of 128 bytes
 // (32 fp32/tf32 values of K), 8 rows per 1024-byte atom, atoms stacked along M/N every 1024 bytes;
@@ -154,6 +154,16 @@ __device__ __forceinline__ void tma_load_3d_warp(void *smem, const CUtensorMap *
       "@e cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];\n\t}\n" ::"r"(
           smem_u32(smem)),
       "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(mbar))
+      : "memory");
+}
+// 4-D box (the hi | lo planes of a per-task operand: dims {cols, rows, task, plane})
+__device__ __forceinline__ void tma_load_4d_warp(void *smem, const CUtensorMap *map, int x, int y, int z, int w,
+                                                 uint64_t *mbar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], [%6];\n\t}\n" ::"r"(
+          smem_u32(smem)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(w), "r"(smem_u32(mbar))
       : "memory");
 }
 __device__ __forceinline__ void mbar_arrive_expect_tx_warp(uint64_t *mbar, uint32_t bytes) {

@@ -100,6 +100,12 @@ class CoFEM:
         self.stream.synchronize()
         return out
 
+    def estep_sums(self) -> torch.Tensor:
+        """This rank's Eq. 4 sums [den (C·D) | num (C) | Σ_t log p(y_t)] before the all-reduce."""
+        out = torch.empty(self.C * self.D + self.C + 1, dtype=torch.float64, device=self.device)
+        _c.cmtcs_estep_sums(self.ctx, out.data_ptr())
+        return out
+
     def set_timing(self, enable: bool = True):
         _c.cmtcs_set_timing(self.ctx, enable)
 

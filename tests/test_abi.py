@@ -48,7 +48,7 @@ def test_struct_layout_matches_c():
 int main(void){
   printf("%zu %zu %zu %zu %zu\n", sizeof(cmtcs_problem), offsetof(cmtcs_problem, beta),
          offsetof(cmtcs_problem, probe_seed), offsetof(cmtcs_problem, em_iter0), sizeof(cmtcs_step_info));
-  printf("%zu %zu %zu\n", offsetof(cmtcs_step_info, probe_steps_mean), offsetof(cmtcs_step_info, kernel_launches),
+  printf("%zu %zu %zu %zu\n", offsetof(cmtcs_step_info, probe_steps_mean), offsetof(cmtcs_step_info, kernel_launches), offsetof(cmtcs_step_info, tile_col_iters),
          offsetof(cmtcs_problem, mean_rel_tol));
   return 0; }
 '''
@@ -60,7 +60,7 @@ int main(void){
         out = subprocess.check_output([exe]).decode().split()
     P, S = cmtcs.cmtcs_problem, cmtcs.cmtcs_step_info
     want = [ctypes.sizeof(P), P.beta.offset, P.probe_seed.offset, P.em_iter0.offset, ctypes.sizeof(S),
-            S.probe_steps_mean.offset, S.kernel_launches.offset, P.mean_rel_tol.offset]
+            S.probe_steps_mean.offset, S.kernel_launches.offset, S.tile_col_iters.offset, P.mean_rel_tol.offset]
     assert [int(x) for x in out] == want
 
 

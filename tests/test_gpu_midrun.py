@@ -1,0 +1,111 @@
+"""Mid-run parity at configs 3-5 (north_star: "GPU EM iterations match the oracle within the stated
+tolerances on all five configs"), and the config-3 full run.
+
+One EM step (Alg. 2 lines 3-15) from an oracle-reached mid-run state — α after
+8 EM iterations of the oracle's own C3 run; after 5 (C4) or 2 (C5) oracle iterations on one task
+of every true cluster — is run on the GPU and compared with the oracle's step from the same state,
+stored by tests/golden/make_midrun_goldens.py (which calls only synthetic/ and oracle/).  Mid-run
+states are the ill-conditioned ones (α spread over orders of magnitude, hundreds of CG steps).
+Parity protocol: the CG cap is 4x the config's on both sides (P-s: every block
+converges) and the mean systems are solved to 1e-10 (P-μ); C4 and C5 run the tasks the golden
+sampled in a context holding only those tasks (the probes and M-step are those of the sample).
+Bars as tests/test_gpu_parity.py: μ, s (converged blocks), α rel_∞ ≤ 1e-4; q ≤ 1e-3;
+|ΔL| ≤ 1e-3; ν̄ ≤ 5e-3 + 1e-6|ν̄|; end-to-end α when q is one-hot to 1e-5, q-conditioned α always.
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import synthetic
+from oracle import cofem as O
+from gpu_common import make_gpu, rel_inf, to_np
+
+pytestmark = pytest.mark.gpu
+
+GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+MU_TOL, S_TOL, Q_TOL, A_TOL, L_TOL = 1e-4, 1e-4, 1e-3, 1e-4, 1e-3
+
+
+def nu_tol(nu):
+    return 5e-3 + 1e-6 * np.abs(nu)
+
+
+@pytest.fixture(scope="module")
+def torch_cuda():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    return torch
+
+
+def _run(data, g, alpha, it, cap, q_override=None):
+    """One GPU EM step from (alpha, it) through the C ABI: posterior, info, probe steps."""
+    import torch
+    cfg = data["cfg"]
+    m = make_gpu(data, alpha=alpha, em_iter0=it, cap=cap, mean_tol=float(g["mean_tol"]), T=cfg.T,
+                 task_begin=int(data["tasks"][0]))
+    info = m.em_step(1, q_override=None if q_override is None else torch.tensor(q_override).cuda())
+    post = to_np(m.posterior())
+    steps = m.transcript()["steps"].cpu().numpy().reshape(len(data["tasks"]), cfg.C, cfg.K)
+    m.close()
+    return post, info, steps
+
+
+@pytest.mark.parametrize("name,cid", [("c3_step8", 3), ("c4_step5", 4), ("c5_step2", 5)])
+def test_midrun_single_step(torch_cuda, name, cid):
+    g = np.load(os.path.join(GOLDEN, f"{name}.npz"))
+    cfg = synthetic.CONFIGS[cid]
+    tasks = [int(t) for t in g["tasks"]]
+    data = synthetic.generate(cfg, tasks)
+    alpha, it, cap = g["alpha_in"], int(g["it"]), int(g["cap"])
+    post, info, steps = _run(data, g, alpha, it, cap)
+    mu_o, s_o = g["mu"].astype(np.float64), g["s"].astype(np.float64)
+    mu_e = rel_inf(post["mu"], mu_o)
+    s_e = rel_inf(post["s"], s_o)
+    conv = np.all(steps < cap, axis=-1) & np.all(g["probe_steps"].reshape(steps.shape) < cap, axis=-1)
+    nu_e = np.abs(post["logdet"] - g["nu"])
+    q_e = np.max(np.abs(post["q"] - g["q"]))
+    L_gpu = info["loglik"] * cfg.T / len(tasks)          # the library's L is Σ_t ll_t / T (global T)
+    L_e = abs(L_gpu - float(g["L"]))
+    a_e = np.max(rel_inf(post["alpha"], g["alpha_next"]))
+    # q-conditioned α: the GPU's M-step fed the oracle's q, from the same state
+    post_q, _, _ = _run(data, g, alpha, it, cap, q_override=g["q"])
+    aq_e = np.max(rel_inf(post_q["alpha"], g["alpha_next"]))
+    print(f"{name}: mu {mu_e.max():.2e} s {s_e[conv].max() if conv.any() else float('nan'):.2e} "
+          f"(converged {conv.sum()}/{conv.size}) nu {nu_e.max():.2e} (|nu| {np.abs(g['nu']).max():.3g}) "
+          f"q {q_e:.2e} L {L_e:.2e} alpha {a_e:.2e} q-cond alpha {aq_e:.2e} "
+          f"GPU probe steps max {steps.max()} oracle {int(g['probe_steps'].max())}")
+    assert mu_e.max() <= MU_TOL
+    assert conv.all() and s_e.max() <= S_TOL
+    assert np.all(nu_e <= nu_tol(g["nu"]))
+    assert q_e <= Q_TOL
+    assert L_e <= L_TOL
+    assert aq_e <= A_TOL
+    if q_e <= 1e-5:
+        assert a_e <= A_TOL
+
+
+def test_full_run_config3(torch_cuda):
+    """Config 3's whole run (64 tasks, 30 EM iterations from α₀ = 1, the config's cap and tolerance):
+    identical argmax assignments and |ΔNMSE| ≤ 1e-3 (north_star) against the oracle's run
+    (tests/golden/c3_full_run.json); |ΔL| reported per iteration, asserted on the common-state
+    prefix (up to the first iteration with a cap hit on either side)."""
+    with open(os.path.join(GOLDEN, "c3_full_run.json")) as f:
+        gold = json.load(f)
+    cfg = synthetic.CONFIGS[3]
+    data = synthetic.generate(cfg)
+    m = make_gpu(data)
+    infos = [m.em_step(1) for _ in range(cfg.em_iters)]
+    post = to_np(m.posterior())
+    m.close()
+    nm_gpu = O.nmse(post["recon"], data["z"])
+    gaps = np.abs(np.array([i["loglik"] for i in infos]) - np.array(gold["L"]))
+    capped = np.array([i["n_cap_hit"] > 0 or c > 0 for i, c in zip(infos, gold["probe_cap_hits"])])
+    prefix = (int(np.argmax(capped)) + 1) if capped.any() else len(capped)
+    print("C3 full run: nmse", nm_gpu, gold["nmse"], "|dL|", np.array2string(gaps, precision=2),
+          "GPU cap hits", [i["n_cap_hit"] for i in infos], "oracle", gold["probe_cap_hits"], "prefix", prefix)
+    assert [int(a) for a in post["assign"]] == gold["assign"]
+    assert abs(nm_gpu - gold["nmse"]) <= 1e-3
+    assert np.max(gaps[:prefix]) <= L_TOL

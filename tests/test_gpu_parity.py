@@ -199,24 +199,28 @@ def test_single_em_step_many_column_tiles(torch_cuda):
     assert e["mu"] <= MU_TOL and e["s_conv"] <= S_TOL and e["q_abs"] <= Q_TOL and e["L_abs"] <= L_TOL
 
 
-@pytest.mark.parametrize("it", [
-    pytest.param(4, marks=pytest.mark.xfail(reason="fp32 probe columns at C1's kappa: rel_inf(alpha) 1.3e-4 "
-                                                     "(eps32*kappa floor, DESIGN.md §6); strict in fp64 mode",
-                                             strict=False)),
-    15])
+@pytest.mark.parametrize("it", [4, 15])
 def test_q_conditioned_alpha(torch_cuda, it):
-    """The GPU M-step fed the oracle's q (reading of P-α)."""
+    """The GPU M-step fed the oracle's q (reading of P-α): rel_∞(α) ≤ 1e-4 always.
+
+    Both sides solve the mean systems to 1e-10 (reading A5 / P-μ, as every μ parity check here):
+    at the config tolerance a rounding-level difference in ‖r‖ moves the stopping step of a mean
+    column, which moves μ by up to ~1e-4 on BOTH fp64 sides alike — the α error this test saw
+    at it = 4 in round 1 (1.3e-4) came from μ, not from the fp32 probe columns (an fp32
+    emulation of the probe solves alone gives 3e-6 there)."""
     import torch
     cfg = synthetic.CONFIGS[1]
     data = synthetic.generate(cfg)
     alpha = oracle_state(data, it, mode="cofem")
-    orc = O.e_step(data, alpha, it, mode="cofem", cap=4 * cfg.cg_cap)
-    g = make_gpu(data, cap=4 * cfg.cg_cap, alpha=alpha, em_iter0=it)
+    orc = O.e_step(data, alpha, it, mode="cofem", cap=4 * cfg.cg_cap, mu_tol=MEAN_TOL, mu_cap=4 * cfg.cg_cap)
+    g = make_gpu(data, cap=4 * cfg.cg_cap, alpha=alpha, em_iter0=it, mean_tol=MEAN_TOL)
     g.em_step(1, q_override=torch.tensor(orc["q"]).cuda())
     post = to_np(g.posterior())
     g.close()
     a_next = O.m_step(orc["q"], orc["mu"], orc["s"], alpha)
-    assert np.max(rel_inf(post["alpha"], a_next)) <= A_TOL
+    err = np.max(rel_inf(post["alpha"], a_next))
+    print("q-conditioned alpha C1 it", it, err)
+    assert err <= A_TOL
 
 
 def test_probe_override_matches_hash(torch_cuda):
@@ -358,9 +362,14 @@ def test_full_run_config1(torch_cuda):
     capfree = np.array([i["n_cap_hit"] == 0 and c == 0 for i, c in zip(infos, caps_orc)])
     print("L gaps", gaps, "cap-free iterations", capfree, "nmse", nm_gpu, orc["nmse"])
     # At config 1's cap (64 = D) fp32 probe CG needs more steps than fp64 (finite-precision delay,
-    # SURVEY.md §0.2 / DESIGN.md §6), so cap-limited iterations are reported, not asserted here.
-    # L is compared step by step from identical states in the single-step tests; across a run the
-    # states drift apart after cap-limited iterations, so here it is reported only.
+    # SURVEY.md §0.2 / DESIGN.md §6): a cap-limited iteration leaves the two runs in different
+    # states (the capped columns' x differ by more than rounding), so L(θ̂) of the entry state is
+    # asserted on the common-state prefix — every iteration up to and including the first one
+    # in which either side hit the cap — and reported after it.
+    capped = np.array([not c for c in capfree])
+    prefix = (int(np.argmax(capped)) + 1) if capped.any() else len(capfree)
+    print("common-state prefix", prefix, "iterations; max |dL| there", gaps[:prefix].max())
+    assert prefix >= 1 and np.max(gaps[:prefix]) <= L_TOL
     assert capfree.sum() >= 5
 
 
@@ -397,7 +406,20 @@ def test_single_step_config2(torch_cuda):
     assert e["mu"] <= MU_TOL
     assert conv.any() and e["s_conv"] <= S_TOL
     assert np.all(np.abs(post["logdet"] - orc["nu"]) <= nu_tol(orc["nu"]))
+    assert e["q_abs"] <= Q_TOL
     assert e["L_abs"] <= L_TOL
+    # end-to-end α when q is one-hot to 1e-5 (P-α), and always the q-conditioned α: the GPU
+    # M-step fed the oracle's q, from the same state
+    if np.max(np.abs(post["q"] - orc["q"])) <= 1e-5:
+        assert e["alpha"] <= A_TOL
+    import torch
+    g = make_gpu(data, cap=4 * cfg.cg_cap, alpha=alpha, em_iter0=3, mean_tol=MEAN_TOL)
+    g.em_step(1, q_override=torch.tensor(orc["q"]).cuda())
+    pq = to_np(g.posterior())
+    g.close()
+    errq = np.max(rel_inf(pq["alpha"], a_next))
+    print("C2 q-conditioned alpha", errq)
+    assert errq <= A_TOL
 
 
 def test_task_shards_match_whole(torch_cuda):
@@ -409,12 +431,23 @@ def test_task_shards_match_whole(torch_cuda):
     whole = make_gpu(data, alpha=alpha, em_iter0=5, cap=256)
     whole.em_step(1)
     pw = to_np(whole.posterior())
+    sums_w = whole.estep_sums().cpu().numpy()
+    alpha_w = pw["alpha"]
     whole.close()
+    sums = []
     for b, e in [(0, 2), (2, 4)]:
         part = synthetic.generate(cfg, range(b, e))
         g = make_gpu(part, alpha=alpha, em_iter0=5, cap=256, T=cfg.T, task_begin=b)
         g.em_step(1)
         pp = to_np(g.posterior())
+        sums.append(g.estep_sums().cpu().numpy())
         g.close()
         for k in ("mu", "s", "logdet", "q"):
             np.testing.assert_allclose(pp[k], pw[k][b:e], rtol=1e-12, atol=1e-12)
+    # the library's per-rank Eq. 4 sums (what each rank contributes to the all-reduce) add up to
+    # the whole problem's, and finishing them gives the whole problem's α (Eq. 4)
+    tot = sums[0] + sums[1]
+    np.testing.assert_allclose(tot, sums_w, rtol=1e-13)
+    CD = cfg.C * cfg.D
+    a_fin = O.m_step_finish(tot[CD:CD + cfg.C], tot[:CD].reshape(cfg.C, cfg.D), alpha)
+    np.testing.assert_allclose(a_fin, alpha_w, rtol=1e-13)
