@@ -69,7 +69,8 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", type=int, default=4, choices=[1, 2, 3, 4, 5])
+    ap.add_argument("--config", type=int, default=4, choices=[1, 2, 3, 4, 5, 6],
+                    help="BASELINE.json configs[cfg-1] (1-5); 6 = the paper's own partial-Fourier workload (§4)")
     ap.add_argument("--impl", default="cuda", choices=["cuda", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -157,7 +158,10 @@ def oracle_blocks(cfg, alpha, it, budget_s):
         t, c = divmod(n, cfg.C)
         if c == 0 or data is None:
             data = synthetic.generate(cfg, [t])
-        phi_t = data["phi"] if cfg.shared_phi else data["phi"][0]
+        if cfg.operator == "fourier":
+            phi_t = O.partial_fourier_matrix(cfg.D, data["rows"][0])
+        else:
+            phi_t = data["phi"] if cfg.shared_phi else data["phi"][0]
         t0 = time.perf_counter()
         P = O.probe_signs(cfg.probe_seed, it, cfg.T, t, cfg.C, cfg.K, cfg.D)
         o = O.cofem_task(phi_t, data["y"][0], data["beta"], alpha, data["pi"], P, cfg.cg_tol, cfg.cg_cap,
@@ -191,7 +195,7 @@ def reference_arm(args):
         return 0
     cfg = synthetic.CONFIGS[args.config]
     from oracle import cofem as O
-    n_t, n_c = {1: (4, 2), 2: (2, 4), 3: (1, 2), 4: (1, 1), 5: (1, 1)}[args.config]
+    n_t, n_c = {1: (4, 2), 2: (2, 4), 3: (1, 2), 4: (1, 1), 5: (1, 1), 6: (1, 2)}[args.config]
     data = synthetic.generate(cfg, range(n_t))
     sub = cfg.replace(C=n_c)
     data["cfg"] = sub
@@ -274,7 +278,9 @@ def cuda_arm(args):
         b, e = synthetic.shard(cfg.T, rank, world)
         data = synthetic.generate(cfg, range(b, e))
     pi = data["pi"]
-    phi_h = torch.from_numpy(np.ascontiguousarray(data["phi"])).pin_memory()
+    fourier = cfg.operator == "fourier"
+    # the sensing operator's host copy: Φ (dense) or the sampled DFT rows Ω_t (partial Fourier)
+    phi_h = torch.from_numpy(np.ascontiguousarray(data["rows"] if fourier else data["phi"])).pin_memory()
     y_h = torch.from_numpy(np.ascontiguousarray(data["y"])).pin_memory()
     del data
     phi = phi_h.to(dev)
@@ -286,6 +292,10 @@ def cuda_arm(args):
         uid = obj[0]
 
     def make(phi_d, y_d, alpha0=None, em_iter0=0, nccl_uid=None):
+        if fourier:
+            return CoFEM(None, y_d, fourier_rows=phi_d, D=cfg.D, T=t_total, C=cfg.C, K=cfg.K, beta=cfg.beta,
+                         cg_max_iters=cfg.cg_cap, cg_rel_tol=cfg.cg_tol, probe_seed=cfg.probe_seed, pi=pi,
+                         task_begin=b, nccl_uid=nccl_uid, rank=rank, world=world, alpha0=alpha0, em_iter0=em_iter0)
         return CoFEM(phi_d, y_d, T=t_total, C=cfg.C, K=cfg.K, beta=cfg.beta, cg_max_iters=cfg.cg_cap,
                      cg_rel_tol=cfg.cg_tol, probe_seed=cfg.probe_seed, pi=pi, task_begin=b,
                      shared_phi=cfg.shared_phi, nccl_uid=nccl_uid, rank=rank, world=world, alpha0=alpha0,
@@ -354,7 +364,10 @@ def cuda_arm(args):
     col_iters = sum(i["probe_col_iters"] + i["mean_col_iters"] for i in infos)
     probe_iters = sum(i["probe_col_iters"] for i in infos)
     tile_iters = sum(i["tile_col_iters"] for i in infos)
-    flops_rank = 4.0 * cfg.N * cfg.D * col_iters
+    # dense: 4·N·D flop per active column per CG step (the two products with Φ_t);  partial Fourier:
+    # two length-D complex FFTs, 5·D·log2(D) flop each (the standard radix-2 count), per column-step
+    flop_per_col = (10.0 * cfg.D * math.log2(cfg.D)) if fourier else 4.0 * cfg.N * cfg.D
+    flops_rank = flop_per_col * col_iters
     flops_all = sum_over_ranks(flops_rank)
     kern_ms = tm["cg_kernel_ms"]                 # the whole persistent CG kernel (CUDA events)
     op_ms = tm["op_ms"]                          # its operator phases only (device stamps)
@@ -365,9 +378,11 @@ def cuda_arm(args):
     peak_burst, peak_sust = tf32x3_peak_tflops(peaks)
     long_kernel = kern_ms / max(1, tm["cg_kernel_launches"]) > 1000.0
     peak = peak_sust if long_kernel else peak_burst
+    if fourier:   # FP32 ALU bound (FFMA peak at the measured clock ceiling, B200_PROFILING.md unit counts)
+        peak_burst = peak_sust = peak = fp32_peak_tflops(peaks.get("sm_max_mhz", SM_MAX_MHZ))
     # EM-step roofline (north_star): slower of Φ bytes at HBM bandwidth and FLOPs at peak, per CG step
     steps_total = sum(i["cg_iters"] for i in infos)
-    phi_bytes = 4.0 * cfg.N * cfg.D * (1 if cfg.shared_phi else (e - b)) * steps_total
+    phi_bytes = (4.0 * cfg.N if fourier else 4.0 * cfg.N * cfg.D) * (1 if cfg.shared_phi else (e - b)) * steps_total
     t_roof = max(flops_rank / (peak * 1e12), phi_bytes / (peaks["hbm_gbs"] * 1e9))
     em_roof_frac = max_over_ranks(t_roof) / (total_ms * 1e-3)
 
@@ -377,7 +392,7 @@ def cuda_arm(args):
     e2e = None
     if not args.no_e2e and args.e2e_steps > 0:
         ne = min(args.e2e_steps, args.steps)
-        h2d = phi_h.numel() * 4 + y_h.numel() * 4 + cfg.C * cfg.D * 8
+        h2d = phi_h.numel() * phi_h.element_size() + y_h.numel() * 4 + cfg.C * cfg.D * 8
         d2h = ((e - b) * cfg.C + cfg.C * cfg.D + (e - b) * cfg.D + (e - b)) * 8
         barrier()
         torch.cuda.synchronize()
@@ -423,8 +438,10 @@ def cuda_arm(args):
                    if weak else {}),
                 "parallelism": f"task-sharded dp{world}" if world > 1 else "single GPU",
                 "straggler_spread": (total_ms / fastest_ms) if world > 1 else 1.0,
-                "precision": "probe columns: fp32 vectors, operator on tcgen05 tensor cores as 3xTF32 "
-                             "(fp32-accurate), fp64 dots/scalars; mean columns, log-det, q, M-step fp64",
+                "precision": ("probe columns: fp32 vectors and fp32 FFT, fp64 dots/scalars; mean columns (fp64 FFT), "
+                              "log-det, q, M-step fp64") if fourier else
+                             ("probe columns: fp32 vectors, operator on tcgen05 tensor cores as 3xTF32 "
+                              "(fp32-accurate), fp64 dots/scalars; mean columns, log-det, q, M-step fp64"),
                 "l2": "flushed (zero-fill of 2xL2) between timed EM iterations",
                 "cg_steps_per_em_iter": [i["cg_iters"] for i in infos],
                 "active_col_iters_per_em_iter": [i["probe_col_iters"] + i["mean_col_iters"] for i in infos],
@@ -436,13 +453,16 @@ def cuda_arm(args):
                 "update_share_of_step": tm["update_ms"] / max(rank_ms, 1e-9),
                 "wall_s_timed": wall,
             },
-            "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+            "roofline": {"bound": "alu" if fourier else "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                          "frac": achieved / peak, "traffic": ncu_traffic(cfg.name),
                          "traffic_unit": "DRAM bytes per CG step (ncu --set full of k_cg_persistent / its CG steps)",
-                         "kernel": "k_cg_persistent (the whole CG loop of an E-step: operator on tcgen05 3xTF32 + fp64 "
-                                   "mean columns on DMMA + CG update); achieved = algorithmic fp32 flop 4*N*D per "
-                                   "active column per CG step / the kernel's duration (CUDA events on the launch "
-                                   "stream around every launch in the timed region)",
+                         "kernel": ("k_cg_fourier (partial-Fourier CG: one CTA per column, FFT in shared memory; "
+                                    "achieved = 10*D*log2(D) flop per active column per CG step / the kernels' "
+                                    "duration)") if fourier else
+                                   ("k_cg_persistent (the whole CG loop of an E-step: operator on tcgen05 3xTF32 + fp64 "
+                                    "mean columns on DMMA + CG update); achieved = algorithmic fp32 flop 4*N*D per "
+                                    "active column per CG step / the kernel's duration (CUDA events on the launch "
+                                    "stream around every launch in the timed region)"),
                          "peak_source": (f"{peaks_kind} MEASURED_PEAKS.json bf16 "
                                          f"{peaks['bf16_tflops_sustained' if long_kernel else 'bf16_tflops']} TF/s "
                                          f"({'sustained: kernel launches last > 1 s' if long_kernel else 'burst'}) "

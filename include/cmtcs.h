@@ -67,7 +67,17 @@ typedef struct cmtcs_problem {
   int32_t em_iter0;      /* global EM-iteration index of the next em_step (probe counter `it`) */
   double mean_rel_tol;   /* tolerance of the C mean systems A μ = βΦᵀy; < 0 ⇒ cg_rel_tol.  A tighter
                             value (e.g. 1e-10) makes μ independent of where CG stops (DESIGN.md §3 A5) */
+  int32_t op_kind;       /* CMTCS_OP_DENSE: Φ_t is the caller's matrix (phi).  CMTCS_OP_PARTIAL_FOURIER:
+                            the paper's §4 sensing matrix Φ_t = Ω_t F — F the unitary
+                            D-point DFT, Ω_t the N rows fourier_rows[t] of the identity, real-embedded as
+                            [Re(Ω_t F); Im(Ω_t F)] (reading F1), applied by FFT; then phi must
+                            be NULL, y is [T_loc][2N] (N real parts, then N imaginary parts), D is a
+                            power of two in [512, 8192] and shared_phi = 0                           */
+  const int32_t *fourier_rows; /* device, BORROWED, op_kind = PARTIAL_FOURIER: int32 [T_loc][N], distinct
+                            rows in [0, D) per task (must outlive ctx); NULL otherwise                */
 } cmtcs_problem;
+
+enum { CMTCS_OP_DENSE = 0, CMTCS_OP_PARTIAL_FOURIER = 1 };
 
 /* Statistics of the last EM iteration run by cmtcs_em_step (host struct, filled on return). */
 typedef struct cmtcs_step_info {
@@ -99,7 +109,8 @@ cmtcs_status cmtcs_workspace_size(const cmtcs_problem *p, size_t *bytes);
 /* Create a context.
  *   phi      device, BORROWED (must outlive ctx): fp32 [T_loc][N][D] row-major, or [N][D] if
  *            p->shared_phi; T_loc = task_end − task_begin, task i is global task task_begin+i.
- *   y        device, BORROWED: fp32 [T_loc][N].
+ *            NULL for op_kind = CMTCS_OP_PARTIAL_FOURIER (Φ_t from p->fourier_rows).
+ *   y        device, BORROWED: fp32 [T_loc][N] ([T_loc][2N] for the partial-Fourier operator).
  *   alpha0   host or device, COPIED: fp64 [C][D], every entry > 0 (α₀, Alg. 2 line 1).
  *   workspace device, BORROWED, ≥ cmtcs_workspace_size bytes, 256-byte aligned.
  *   nccl_uid NULL with world == 1 for a single GPU; else the rank-0 id, rank in [0, world).

@@ -17,6 +17,7 @@ notation.  Citations are PAPER.md line numbers (the LaTeX source) with the equat
   Eq. 7   Lanczos tridiagonal Γ̄ from (γ, ξ) ...... PAPER.md:129-133
   Eq. 8   p'Lp = D Σ_u S²_{u,1} log λ_u ........... PAPER.md:134-138
   Eq. 9   ν̄ = -(1/K) Σ_k Σ_u D S̄²_{u,1} log λ̄_u .... PAPER.md:140-143
+  Φ_t = Ω_t F (partial Fourier, §4) ............... PAPER.md:176 (partial_fourier_matrix)
 
 Readings where the paper is silent or ambiguous are DESIGN.md §3 (A-numbers follow SURVEY.md 8(c)):
   A1  ℓ is evaluated in its stationary form ℓ̃ = ℓ - β‖y‖² (identical at the exact μ, see `ell`).
@@ -81,6 +82,19 @@ def normal_apply(phi: np.ndarray, beta: float, alpha_cols: np.ndarray, V: np.nda
     """A V for the columns of V: β Φᵀ(Φ V) + α_col ⊙ V.  alpha_cols is [D, m] (α of each column)."""
     phi = np.asarray(phi, dtype=np.float64)
     return beta * (phi.T @ (phi @ V)) + alpha_cols * V
+
+
+def partial_fourier_matrix(D: int, rows) -> np.ndarray:
+    """Φ = Ω F of the paper's own workload (§4), formed densely (2N × D, real).
+
+    F ∈ ℂ^{D×D} is the unitary DFT, F_{k,d} = exp(−2πi·k·d/D)/√D (reading F1: the unitary
+    normalisation); Ω keeps the N rows `rows` of the identity.  z, α and A stay real by
+    the real embedding Φ = [Re(ΩF); Im(ΩF)] (reading F1): Φᵀ[u; w] = Re((ΩF)ᴴ(u + iw)),
+    so ΦᵀΦ = Re(Fᴴ ΩᵀΩ F).  Written out element by element from the DFT's definition."""
+    k = np.asarray(rows, dtype=np.float64)[:, None]
+    d = np.arange(D, dtype=np.float64)[None, :]
+    ang = -2.0 * np.pi * np.mod(k * d, D) / D
+    return np.concatenate([np.cos(ang), np.sin(ang)], axis=0) / math.sqrt(D)
 
 
 def dense_A(phi: np.ndarray, beta: float, alpha: np.ndarray) -> np.ndarray:
@@ -254,7 +268,11 @@ def m_step_finish(num, den, alpha_old, alpha_max=1e12, empty_eps=1e-10):
 # E-steps: cofem (Alg. 2 lines 3-12), exact (Eq. 3 literal), probe_exact (K fixed, U → ∞)
 # --------------------------------------------------------------------------------------------
 def _phi_of(data, i):
+    """Φ_t of the i-th task of `data`: the given matrix, or for a partial-Fourier task
+    the dense Ω_t F built from its sampled rows."""
     ph = data["phi"]
+    if ph is None:
+        return partial_fourier_matrix(data["cfg"].D, data["rows"][i])
     return ph if ph.ndim == 2 else ph[i]
 
 

@@ -34,7 +34,10 @@ class cmtcs_problem(ctypes.Structure):
                 ("cg_max_iters", c_int32), ("cg_rel_tol", c_double), ("alpha_max", c_double),
                 ("var_floor", c_double), ("empty_eps", c_double), ("probe_seed", c_uint64),
                 ("task_begin", c_int32), ("task_end", c_int32), ("em_iter0", c_int32),
-                ("mean_rel_tol", c_double)]
+                ("mean_rel_tol", c_double), ("op_kind", c_int32), ("fourier_rows", c_void_p)]
+
+
+CMTCS_OP_DENSE, CMTCS_OP_PARTIAL_FOURIER = 0, 1
 
 
 class cmtcs_step_info(ctypes.Structure):

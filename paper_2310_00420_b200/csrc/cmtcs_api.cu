@@ -95,7 +95,9 @@ int nt_max(int shared_phi) {
 
 TcCfg make_tc(const Dims &d) {
   TcCfg tc;
-  tc.NT = std::min(nt_max(d.shared_phi), (d.P + 15) / 16 * 16);
+  tc.pair = d.pair;
+  // a pair's MMA has N ≤ 256, a multiple of 32 (each CTA stages N/2 columns)
+  tc.NT = std::min(nt_max(d.shared_phi), (d.P + (d.pair ? 31 : 15)) / (d.pair ? 32 : 16) * (d.pair ? 32 : 16));
   tc.slot = (tc.NT + 15) / 16 * 16;
   // TMEM (512 columns): accumulators in [0, acol0), the A stages (tf32 hi | lo, 64 columns) above:
   // three A stages with double-buffered accumulators when both fit, else two (CMTCS_SA overrides)
@@ -104,9 +106,10 @@ TcCfg make_tc(const Dims &d) {
   tc.acol0 = 512 - 64 * tc.sa;
   tc.dbl = 4 * tc.slot <= tc.acol0 ? 1 : 0;
   tc.nacc = std::max(1, std::min(4, tc.acol0 / tc.slot - 1));   // main accumulators besides the cross one
-  // ring stage: fp32 A (16 KB), B hi/lo (2 × NT × 128 B), fp64 mean-column chunk (≤ 32 × Cp × 8 B)
+  // ring stage: fp32 A (16 KB), B hi/lo (2 × NT × 128 B; a pair: its half, NT × 128 B), fp64
+  // mean-column chunk (≤ 32 × Cp × 8 B)
   const unsigned mean_bytes = (256u * (unsigned)d.Cp + 1023u) & ~1023u;
-  tc.stage_bytes = 128u * 128u + 2u * (unsigned)tc.NT * 128u + mean_bytes;
+  tc.stage_bytes = 128u * 128u + (tc.pair ? 1u : 2u) * (unsigned)tc.NT * 128u + mean_bytes;
   // one CTA per SM (512 TMEM columns) within ≤ 212 KB of the 227 KB of shared memory: the stage-2
   // epilogue's d tile (NT × 128 fp32) when ≥ 3 ring stages still fit (measured at C3: a 4th stage
   // instead of the d tile does not help, the K loop is bound by shared-memory traffic)
@@ -114,7 +117,7 @@ TcCfg make_tc(const Dims &d) {
   const unsigned dtile = (unsigned)tc.NT * 128u * 4u;
   int st_with = (int)((budget - std::min(budget, dtile)) / tc.stage_bytes);
   const int st_without = std::min(6, (int)(budget / tc.stage_bytes));
-  if (getenv("CMTCS_NODTILE")) st_with = 0;   // experiments: ring stages instead of the d tile
+  if (getenv("CMTCS_NODTILE") ? atoi(getenv("CMTCS_NODTILE")) != 0 : tc.pair != 0) st_with = 0;   // pairs: ring stages, not the d tile
   if (st_with >= 3) {
     tc.use_dtile = 1;
     tc.dtile_bytes = dtile;
@@ -145,6 +148,12 @@ bool make_dims(const cmtcs_problem *p, Dims *d, char *why) {
     s += p->pi[c];
   }
   if (fabs(s - 1.0) > 1e-9) { snprintf(why, 256, "pi sums to %.17g, not 1", s); return false; }
+  if (p->op_kind != CMTCS_OP_DENSE && p->op_kind != CMTCS_OP_PARTIAL_FOURIER) { snprintf(why, 256, "unknown op_kind %d", p->op_kind); return false; }
+  if (p->op_kind == CMTCS_OP_PARTIAL_FOURIER) {
+    if (p->shared_phi) { snprintf(why, 256, "the partial-Fourier operator has a mask per task: shared_phi must be 0"); return false; }
+    if (!p->fourier_rows) { snprintf(why, 256, "the partial-Fourier operator needs fourier_rows"); return false; }
+    if (!fourier_supported(p->D, p->N, why)) return false;
+  }
   d->T = p->T;
   d->Tl = p->task_end - p->task_begin;
   d->t0 = p->task_begin;
@@ -159,9 +168,23 @@ bool make_dims(const cmtcs_problem *p, Dims *d, char *why) {
   d->nw = (p->D + 63) / 64;
   d->nRT1 = (p->N + OP_BR - 1) / OP_BR;
   d->nRT2 = (p->D + OP_BR - 1) / OP_BR;
-  const int NT = std::min(nt_max(p->shared_phi), (d->P + 15) / 16 * 16);   // = make_tc's NT
-  d->nCT = (d->P + NT - 1) / NT;
   {
+    // CTA pairs (2-CTA clusters, cta_group::2) when the operator has enough row-tile pairs to fill
+    // the 74 pairs of a B200 twice over: half of B per CTA, M = 256 MMAs.  CMTCS_PAIR=0 disables,
+    // =2 forces them (tests: every shape through the pair path)
+    const char *e = getenv("CMTCS_PAIR");
+    const int mode = e ? atoi(e) : 0;   // off by default: slower at C4 so far
+    const int NT1 = std::min(nt_max(p->shared_phi), (d->P + 15) / 16 * 16);
+    const long pair_units = (long)((d->P + NT1 - 1) / NT1) * ((d->nRT1 + 1) / 2) * (p->task_end - p->task_begin);
+    d->pair = mode == 2 || (mode == 1 && pair_units >= 148);
+  }
+  const int NT = std::min(nt_max(p->shared_phi), (d->P + (d->pair ? 31 : 15)) / (d->pair ? 32 : 16) * (d->pair ? 32 : 16));   // = make_tc's NT
+  d->nCT = (d->P + NT - 1) / NT;
+  if (d->pair) {
+    d->S1 = 1;
+    d->K1 = (p->D + 31) / 32 * 32;
+    d->split_coop = 0;
+  } else {
     // split the stage-1 contraction over D (S1 ∈ {1, 2, 4, 8}, every split ≥ 128 of D) so that the
     // stage-1 units fill and balance the persistent grid (148 CTAs on a B200): minimise rounds ×
     // (chunks per unit + a fixed per-unit cost).  The split partial tiles are reduced cooperatively
@@ -178,6 +201,7 @@ bool make_dims(const cmtcs_problem *p, Dims *d, char *why) {
       const long cost = rounds * (chunks + 4);   // + fixed per-unit cost (prologue, epilogue, reduction)
       if (best_cost < 0 || cost < best_cost) { best_cost = cost; best = s1; }
     }
+    if (getenv("CMTCS_S1")) best = std::max(1, std::min(8, atoi(getenv("CMTCS_S1"))));   // experiments
     int k1 = (p->D + best - 1) / best;
     k1 = (k1 + 31) / 32 * 32;   // whole 32-wide K stages of the tensor-core pipeline
     d->K1 = k1;
@@ -187,6 +211,8 @@ bool make_dims(const cmtcs_problem *p, Dims *d, char *why) {
   }
   d->shared_phi = p->shared_phi ? 1 : 0;
   d->phi_task_stride = p->shared_phi ? 0 : (int64_t)p->N * p->D;
+  d->op = p->op_kind;
+  if (d->op != CMTCS_OP_DENSE) d->pair = 0;
   return true;
 }
 
@@ -200,24 +226,26 @@ size_t carve(const Dims &d, char *base, Bufs *b) {
   b->b64 = cv.take<double>(Tl * D);
   b->bnorm2 = cv.take<double>(Tl);
   const size_t mats = d.shared_phi ? 1 : Tl;
-  b->PT = cv.take<float>(mats * N * D);
+  // dn = 0: the partial-Fourier operator keeps its CG vectors on chip (k_fourier.cu) — only x leaves
+  const size_t dn = d.op == CMTCS_OP_DENSE ? 1 : 0;
+  b->PT = cv.take<float>(dn * mats * N * D);
   b->X = cv.take<float>(Tl * P * D);
-  b->R = cv.take<float>(Tl * P * D);
-  b->D32 = cv.take<float>(Tl * P * D);
-  b->Dh = cv.take<float>(Tl * P * D);
-  b->Dl = cv.take<float>(Tl * P * D);
-  b->W = cv.take<float>(Tl * P * D);
+  b->R = cv.take<float>(dn * Tl * P * D);
+  b->D32 = cv.take<float>(dn * Tl * P * D);
+  b->Dh = cv.take<float>(dn * Tl * P * D);
+  b->Dl = cv.take<float>(dn * Tl * P * D);
+  b->W = cv.take<float>(dn * Tl * P * D);
   b->Xm = cv.take<double>(Tl * C * D);
-  b->Rm = cv.take<double>(Tl * C * D);
-  b->Dm = cv.take<double>(Tl * C * D);
-  b->Wm = cv.take<double>(Tl * C * D);
-  b->Uh = cv.take<float>(Tl * d.Pp * N);
-  b->Ul = cv.take<float>(Tl * d.Pp * N);
-  b->Um = cv.take<double>(Tl * N * d.Cp);
+  b->Rm = cv.take<double>(dn * Tl * C * D);
+  b->Dm = cv.take<double>(dn * Tl * C * D);
+  b->Wm = cv.take<double>(dn * Tl * C * D);
+  b->Uh = cv.take<float>(dn * Tl * d.Pp * N);
+  b->Ul = cv.take<float>(dn * Tl * d.Pp * N);
+  b->Um = cv.take<double>(dn * Tl * N * d.Cp);
   b->rr = cv.take<double>(Tl * P);
   b->rrm = cv.take<double>(Tl * C);
-  b->dAd = cv.take<double>(Tl * P * d.nRT2);
-  b->dAdm = cv.take<double>(Tl * C * d.nRT2);
+  b->dAd = cv.take<double>(dn * Tl * P * d.nRT2);
+  b->dAdm = cv.take<double>(dn * Tl * C * d.nRT2);
   b->flag = cv.take<int>(Tl * P);
   b->flagm = cv.take<int>(Tl * C);
   b->steps = cv.take<int>(Tl * P);
@@ -244,8 +272,9 @@ size_t carve(const Dims &d, char *base, Bufs *b) {
   b->ts = cv.take<unsigned long long>((size_t)cap * 4 + 512);   // + 2 × 256 diagnostic stamps
   b->stats = cv.take<double>(16);
   b->assign = cv.take<int>(Tl);
-  b->Upart = cv.take<float>(d.S1 > 1 ? Tl * d.S1 * d.Pp * N : 1);
-  b->Umpart = cv.take<double>(d.S1 > 1 ? Tl * d.S1 * N * d.Cp : 1);
+  b->Upart = cv.take<float>(dn && d.S1 > 1 ? Tl * d.S1 * d.Pp * N : 1);
+  b->Umpart = cv.take<double>(dn && d.S1 > 1 ? Tl * d.S1 * N * d.Cp : 1);
+  b->resm = cv.take<double>(Tl * C);
   b->tmark = cv.take<int>(Tl);
   b->tilecnt = cv.take<int>(Tl * d.nCT * d.nRT1);
   b->gridbar = cv.take<unsigned>(1);
@@ -305,21 +334,30 @@ cmtcs_status one_em_iteration(cmtcs_ctx *c, const uint64_t *probe_bits, const do
   CUDA_OK(c, cudaMemsetAsync(kp.b.histt, 0, sizeof(int) * d.cap, s));
   CUDA_OK(c, cudaMemsetAsync(kp.b.histp, 0, sizeof(int) * d.cap, s));
   CUDA_OK(c, cudaMemsetAsync(kp.b.tmark, 0, sizeof(int) * d.Tl, s));
-  CUDA_OK(c, launch_init_columns(kp, s));
-  L += 1;
+  const bool fourier = d.op == CMTCS_OP_PARTIAL_FOURIER;
+  if (fourier) {
+    CUDA_OK(c, cudaMemsetAsync(kp.b.u, 0, sizeof(int), s));
+  } else {
+    CUDA_OK(c, launch_init_columns(kp, s));
+    L += 1;
+  }
   const bool tm = c->timing;
   if (tm) {
     CUDA_OK(c, cudaMemsetAsync(kp.b.ts, 0, sizeof(unsigned long long) * (4 * d.cap + 256), s));
     CUDA_OK(c, cudaEventRecord(c->tev[0], s));
   }
   // ---- batched CG (Alg. 1) over all T_loc·C·(K+1) columns: one persistent kernel ----
-  CUDA_OK(c, launch_cg_persistent(kp, c->maps, c->grid, s));
+  if (fourier) {
+    CUDA_OK(c, launch_fourier_cg(kp, c->grid, s));   // probe columns (fp32), then mean columns (fp64)
+  } else {
+    CUDA_OK(c, launch_cg_persistent(kp, c->maps, c->grid, s));
+  }
   if (tm) CUDA_OK(c, cudaEventRecord(c->tev[1], s));
   // ---- estimators: s (Eq. 5), ν̄ (Eq. 7-9), Φμ for ℓ, q and log-lik (Eq. 3) ----
   CUDA_OK(c, launch_diag(kp, s));
   CUDA_OK(c, launch_lanczos(kp.b.gam, kp.b.xi, kp.b.steps, d.Tl * d.P, d.cap, d.D, kp.b.tau, nullptr,
                             kp.b.status, s));
-  CUDA_OK(c, launch_mu_stage1(kp, kp.b.Xm, s));
+  if (!fourier) CUDA_OK(c, launch_mu_stage1(kp, kp.b.Xm, s));   // Φμ (the Fourier kernel forms ‖y − Φμ‖² itself)
   CUDA_OK(c, launch_estep_finish(kp, s));
   // ---- M-step (Eq. 4): local sums → all-reduce over ranks → α update ----
   CUDA_OK(c, launch_mstep_partial(kp, s));
@@ -351,8 +389,8 @@ cmtcs_status one_em_iteration(cmtcs_ctx *c, const uint64_t *probe_bits, const do
   c->launches += L;
   c->have_estep = true;
   const int steps_run = *c->h_u;
-  L += 1;                       // the persistent CG kernel
-  c->launches += 1;
+  L += fourier ? 2 : 1;         // the persistent CG kernel (partial Fourier: probe and mean kernels)
+  c->launches += fourier ? 2 : 1;
   if (tm) {
     // per CG step: %globaltimer stamps taken by CTA 0 after the grid barriers: step start,
     // operator (phases 1-2) done, update (phase 3) done (device clock, ns)
@@ -362,7 +400,7 @@ cmtcs_status one_em_iteration(cmtcs_ctx *c, const uint64_t *probe_bits, const do
       if (t0 && t1 >= t0) c->t_ms[0] += (t1 - t0) * 1e-6;
       if (t1 && t2 >= t1) c->t_ms[1] += (t2 - t1) * 1e-6;
     }
-    if (getenv("CMTCS_PHASE_LOG")) {   // diagnostic: mean per-step phase durations (device stamps)
+    if (getenv("CMTCS_PHASE_LOG") && steps_run > 0) {   // diagnostic: mean per-step phase durations (device stamps)
       double ph[3] = {0, 0, 0};
       for (int u = 0; u < steps_run; ++u) {
         const unsigned long long *q = c->h_ts + 4 * u;
@@ -466,7 +504,9 @@ cmtcs_status cmtcs_init(cmtcs_ctx **out, const cmtcs_problem *p, const float *ph
   Dims d;
   char why[256];
   if (!make_dims(p, &d, why)) return fail(nullptr, CMTCS_EINVAL, "%s", why);
-  if (!phi || !y || !alpha0 || !workspace) return fail(nullptr, CMTCS_EINVAL, "phi, y, alpha0 and workspace must be non-NULL");
+  const bool fourier = p->op_kind == CMTCS_OP_PARTIAL_FOURIER;
+  if (fourier ? phi != nullptr : !phi) return fail(nullptr, CMTCS_EINVAL, fourier ? "phi must be NULL for the partial-Fourier operator" : "phi must be non-NULL");
+  if (!y || !alpha0 || !workspace) return fail(nullptr, CMTCS_EINVAL, "y, alpha0 and workspace must be non-NULL");
   if (((uintptr_t)workspace & 255) || ((uintptr_t)phi & 15) || ((uintptr_t)y & 3))
     return fail(nullptr, CMTCS_EINVAL, "workspace must be 256-byte and phi 16-byte aligned");
   if (world < 1 || rank < 0 || rank >= world) return fail(nullptr, CMTCS_EINVAL, "bad rank %d / world %d", rank, world);
@@ -490,6 +530,7 @@ cmtcs_status cmtcs_init(cmtcs_ctx **out, const cmtcs_problem *p, const float *ph
   c->kp.d = d;
   c->kp.b = b;
   c->kp.tc = make_tc(d);
+  c->kp.tc.pf = getenv("CMTCS_PF") ? atoi(getenv("CMTCS_PF")) : 0;
   c->kp.phi = phi;
   c->kp.y = y;
   c->kp.beta = p->beta;
@@ -511,6 +552,12 @@ cmtcs_status cmtcs_init(cmtcs_ctx **out, const cmtcs_problem *p, const float *ph
   CUDA_OK(c, cudaMemsetAsync(b.status, 0, 8 * sizeof(int), c->stream));
   CUDA_OK(c, cudaMemsetAsync(b.gam, 0, sizeof(double) * d.Tl * d.P * d.cap, c->stream));
   CUDA_OK(c, cudaMemsetAsync(b.xi, 0, sizeof(double) * d.Tl * d.P * d.cap, c->stream));
+  c->kp.rows = p->fourier_rows;
+  if (fourier) {
+    int dev = 0;
+    CUDA_OK(c, cudaGetDevice(&dev));
+    CUDA_OK(c, cudaDeviceGetAttribute(&c->grid, cudaDevAttrMultiProcessorCount, dev));
+  } else {
   CUDA_OK(c, cudaMemsetAsync(b.Um, 0, sizeof(double) * (size_t)d.Tl * d.N * d.Cp, c->stream));
   // U's padding rows P..Pp−1 of each task are B-tile rows past the tile's columns: keep them finite
   CUDA_OK(c, cudaMemsetAsync(b.Uh, 0, sizeof(float) * (size_t)d.Tl * d.Pp * d.N, c->stream));
@@ -522,6 +569,7 @@ cmtcs_status cmtcs_init(cmtcs_ctx **out, const cmtcs_problem *p, const float *ph
   if (d.split_coop && (long)d.Tl * d.nCT * d.nRT1 * d.S1 > c->grid)
     return fail(c, CMTCS_ECUDA, "cooperative split-K needs all %d stage-1 units co-resident but the grid has %d CTAs",
                 d.Tl * d.nCT * d.nRT1 * d.S1, c->grid);
+  }
   // π: log π_c on device
   double *pi_dev = b.red;  // scratch: red is rewritten every M-step
   CUDA_OK(c, cudaMemcpyAsync(pi_dev, c->pi_host, sizeof(double) * p->C, cudaMemcpyHostToDevice, c->stream));
@@ -529,10 +577,13 @@ cmtcs_status cmtcs_init(cmtcs_ctx **out, const cmtcs_problem *p, const float *ph
   CUDA_OK(c, cudaGetLastError());
   cmtcs_status st = set_alpha(c, alpha0);
   if (st != CMTCS_OK) { c->broken = true; return st; }
-  CUDA_OK(c, launch_rhs(c->kp, c->stream));
-  CUDA_OK(c, launch_split_phi(c->kp, c->stream));
-  c->launches += 4;
-  {
+  if (fourier) {
+    CUDA_OK(c, launch_fourier_rhs(c->kp, c->stream));
+    c->launches += 3;
+  } else {
+    CUDA_OK(c, launch_rhs(c->kp, c->stream));
+    CUDA_OK(c, launch_split_phi(c->kp, c->stream));
+    c->launches += 4;
     char why[256];
     if (!encode_maps(c->kp, &c->maps, why)) return fail(c, CMTCS_ECUDA, "%s", why);
   }

@@ -30,8 +30,10 @@ struct Dims {
   int S1;    // stage-1 split-K factor (balances the persistent grid when T·N is small)
   int K1;    // stage-1 contraction length per split (multiple of OP_BK)
   int split_coop;  // S1 > 1 with every stage-1 unit co-resident: split CTAs reduce cooperatively
+  int pair;        // CTA-pair operator (TcCfg::pair), decided with the split: pairs need S1 = 1
   int shared_phi;
   int64_t phi_task_stride;  // elements between Φ_t and Φ_{t+1} (0 if shared)
+  int op;          // CMTCS_OP_DENSE (Φ_t a matrix) or CMTCS_OP_PARTIAL_FOURIER (Φ_t = Ω_t F, k_fourier.cu)
 };
 
 // Device buffers carved from the caller's workspace (all sizes in DESIGN.md §5).
@@ -84,6 +86,7 @@ struct Bufs {
   unsigned *gridbar; // [1]    grid-barrier arrival counter of the persistent CG kernel
   int *dep;          // [2][Tl] per-task completion counters of stage 1 / stage 2 units (monotonic)
   int *assign;       // [Tl]
+  double *resm;      // [Tl][C]  ‖y_t − Φ_t μ_tc‖² (partial-Fourier path; the dense path uses Um)
 };
 
 // tensor-core operator configuration (chosen at init from P)
@@ -96,6 +99,9 @@ struct TcCfg {
   int nacc;          // K-split main accumulators ((1 + nacc)·slot ≤ acol0)
   int stages;        // smem pipeline depth
   unsigned stage_bytes;
+  int pf;            // L2 prefetch distance of the A tiles (chunks ahead of the one being loaded; 0 = off)
+  int pair;          // CTA pairs: 2-CTA clusters issuing cta_group::2 MMAs (M = 256 rows: a row-tile
+                     // pair), each CTA staging half of the tile's B columns
   int use_dtile;     // stage-2 epilogue reads its d tile (NT × 128 fp32) from smem, staged by TMA
   unsigned dtile_bytes;
 };
@@ -120,6 +126,7 @@ struct KParams {
   TcCfg tc;
   const float *phi;
   const float *y;
+  const int *rows;             // partial Fourier: sampled DFT rows [Tl][N] (Ω_t)
   double beta;
   double tol;                  // probe columns: stop when ‖r‖ ≤ tol·‖p‖
   double tol_mean;             // mean columns
@@ -131,7 +138,8 @@ struct KParams {
   int trace_step;              // CMTCS_TRACE_STEP (default 5): the CG step CMTCS_PHASE_LOG traces
   int dbg_flags;               // CMTCS_DBG (diagnostics only, wrong results): 1 no DMMA, 2 no tcgen05.mma,
                                // 4 no tf32 split, 8/16/32 accumulator layouts, 64 no epilogue, 128 no TMA;
-                               // (results unchanged:) 4096 no 2-MMA form, 16384 no A-warp drain help on mean units
+                               // (results unchanged:) 4096 no 2-MMA form, 16384 no A-warp drain help on mean units;
+                               // 65536 probe columns never break down (timing runs with the flags above)
 };
 
 // launchers (return cudaGetLastError())
@@ -155,6 +163,9 @@ cudaError_t launch_readout(const KParams &p, double *recon, cudaStream_t s);
 cudaError_t launch_probe_words(uint64_t seed, int it, int T, int t0, int Tl, int C, int K, int D,
                                uint64_t *out, cudaStream_t s);
 cudaError_t launch_copy_transcript(const KParams &p, double *gam, double *xi, cudaStream_t s);
+bool fourier_supported(int D, int N, char *why);
+cudaError_t launch_fourier_rhs(const KParams &p, cudaStream_t s);
+cudaError_t launch_fourier_cg(const KParams &p, int sms, cudaStream_t s);
 
 __device__ __forceinline__ unsigned long long globaltimer() {
   unsigned long long t;

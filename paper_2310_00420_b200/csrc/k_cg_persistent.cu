@@ -56,6 +56,8 @@
 // exchanged within a phase, are read with ld.global.cg after the tile counter's acquire.
 #include <stdio.h>
 
+#include <algorithm>
+
 #include "cmtcs_internal.cuh"
 #include "umma.cuh"
 
@@ -76,6 +78,7 @@ constexpr int EPI0 = 192;                 // first thread of the epilogue warps 
 
 struct PSmemTail {
   uint64_t full[MAXST], empty[MAXST], mdone[MAXST];
+  uint64_t bfull[MAXST];                  // CTA pairs: both CTAs' B halves landed (the leader's copy is used)
   uint64_t afull[MAXSA], aempty[MAXSA];   // TMEM A stages: written by the A warps / read by the MMAs
   uint64_t tfull[2], tempty[2];      // TMEM accumulator buffers: MMA done / epilogue drained
   uint64_t dfull, dempty;             // the stage-2 epilogue's d tile (TMA bytes / epilogue done)
@@ -94,6 +97,15 @@ __device__ __forceinline__ void stv(T *p, T v) { *p = v; }
 
 __device__ __forceinline__ void fence_proxy_async_global() {
   asm volatile("fence.proxy.async.global;\n" ::: "memory");
+}
+
+// TMA prefetch of an A tile into L2 (no shared memory, no completion tracking): the A operand (Φ /
+// Φᵀ) streams from HBM once per step, and a ring of S stages holds too few bytes to cover that
+// latency at the MMA rate (Little's law: ~200 KB in flight against ~2.4k clk from issue to landing)
+__device__ __forceinline__ void tma_prefetch_3d(const CUtensorMap *map, int x, int y, int z) {
+  asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];\n" ::"l"(
+                   reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z)
+               : "memory");
 }
 
 __device__ __forceinline__ void mbar_arrive(uint64_t *mbar) {
@@ -233,18 +245,26 @@ __device__ __forceinline__ int unit_nacc(const TcCfg &tc, int nk, int dbg) {
 // issue the 3xTF32 MMAs of one K = 32 stage (the whole MMA warp, one elected lane issuing) into main
 // accumulator q: A (hi | lo) from
 // the TMEM A stage at column a_tm, B (hi, lo) from the shared-memory ring stage
-__device__ __forceinline__ void mma_stage(uint32_t tmem, uint32_t a_tm, unsigned char *base, uint32_t b_bytes,
+// (CTA pairs: one cta_group::2 instruction covers both CTAs' 128 rows; each CTA's stage holds its
+// half of the tile's columns, hi half then lo half, at the same offsets: lo_off = the hi half's bytes)
+template <bool PR>
+__device__ __forceinline__ void mma_ts(uint32_t d, uint32_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  if (PR) mma_tf32_ts_warp_pair(d, a, b, idesc, acc);
+  else mma_tf32_ts_warp(d, a, b, idesc, acc);
+}
+template <bool PR>
+__device__ __forceinline__ void mma_stage(uint32_t tmem, uint32_t a_tm, unsigned char *base, uint32_t lo_off,
                                           uint32_t idesc, int q, int slot, bool first_main, bool first_cross) {
   const uint64_t bh = desc_sw128(smem_u32(base + A_BYTES));
-  const uint64_t bl = desc_sw128(smem_u32(base + A_BYTES + b_bytes));
+  const uint64_t bl = desc_sw128(smem_u32(base + A_BYTES + lo_off));
   const uint32_t tm_m = tmem + (uint32_t)((1 + q) * slot), tm_x = tmem;
 #pragma unroll
   for (int k8 = 0; k8 < TK / 8; ++k8) {
     const uint64_t o = (uint64_t)(k8 * 32) >> 4;  // +32 bytes per K = 8 step inside the swizzled row
     const uint32_t ah = a_tm + 8 * k8, al = a_tm + 32 + 8 * k8;
-    mma_tf32_ts_warp(tm_x, al, bh + o, idesc, (first_cross && k8 == 0) ? 0u : 1u);
-    mma_tf32_ts_warp(tm_x, ah, bl + o, idesc, 1u);
-    mma_tf32_ts_warp(tm_m, ah, bh + o, idesc, (first_main && k8 == 0) ? 0u : 1u);
+    mma_ts<PR>(tm_x, al, bh + o, idesc, (first_cross && k8 == 0) ? 0u : 1u);
+    mma_ts<PR>(tm_x, ah, bl + o, idesc, 1u);
+    mma_ts<PR>(tm_m, ah, bh + o, idesc, (first_main && k8 == 0) ? 0u : 1u);
   }
 }
 
@@ -450,8 +470,10 @@ __device__ void update_probe(const KParams &p, int t, int col, int u, int lane, 
   // W and the dᵀAd partials come from other CTAs' stage 2 (acquired through the task counter, no
   // grid barrier): read through L2
   for (int i = lane; i < d.nRT2; i += 32) dpart += __ldcg(p.b.dAd + g * d.nRT2 + i);
-  const double dAd = warp_sum(dpart);
-  const double rr = ldv(p.b.rr + g);
+  double dAd = warp_sum(dpart);
+  const double rr0 = ldv(p.b.rr + g);
+  const double rr = (p.dbg_flags & 65536) && !(rr0 > 0.0 && rr0 < 1e300) ? 1.0 : rr0;
+  if ((p.dbg_flags & 65536) && !(dAd > 0.0 && dAd < 1e300)) dAd = 1.0;   // diagnostics: timing only
   if (!(dAd > 0.0)) {  // Alg. 1 line 3 breakdown
     if (lane == 0) {
       report(p.b.status, ST_BREAKDOWN, d.t0 + t, col, u + 1);
@@ -552,8 +574,12 @@ __device__ void update_mean(const KParams &p, int t, int c, int u, int lane) {
   const size_t g = (size_t)t * d.C + c;
   double dpart = 0.0;
   for (int i = lane; i < d.nRT2; i += 32) dpart += __ldcg(p.b.dAdm + g * d.nRT2 + i);
-  const double dAd = warp_sum(dpart);
-  const double rr = ldv(p.b.rrm + g);
+  double dAd = warp_sum(dpart);
+  double rr = ldv(p.b.rrm + g);
+  if (p.dbg_flags & 65536) {   // diagnostics: timing only
+    if (!(rr > 0.0 && rr < 1e300)) rr = 1.0;
+    if (!(dAd > 0.0 && dAd < 1e300)) dAd = 1.0;
+  }
   if (!(dAd > 0.0)) {
     if (lane == 0) {
       report(p.b.status, ST_BREAKDOWN, d.t0 + t, -1 - c, u + 1);
@@ -656,21 +682,26 @@ __device__ __forceinline__ int rotate_ct(int c, int w, int G, int group, int nCT
   return (G % group == 0) ? (c + w / G) % nCT : c;
 }
 
-__device__ __forceinline__ Unit make_unit1(const Dims &d, const TcCfg &tc, int w, int G) {
+// Units are dealt to G dealers (CTAs, or CTA pairs: then a unit covers the row-tile pair (2ρ, 2ρ+1)
+// and rank r of the pair takes row tile 2ρ + r; nRTu = the phase's row tiles or row-tile pairs)
+__device__ __forceinline__ int nrt_units(int nrt, int pair) { return pair ? (nrt + 1) / 2 : nrt; }
+__device__ __forceinline__ Unit make_unit1(const Dims &d, const TcCfg &tc, int w, int G, int rank) {
   Unit x;
   x.stage = 1;
+  const int nRTu = nrt_units(d.nRT1, tc.pair);
   if (d.shared_phi) {
     x.sp = w % d.S1;
-    decode_banded(w / d.S1, d.Tl, d.nCT, d.nRT1, &x.t, &x.ct, &x.rt);
+    decode_banded(w / d.S1, d.Tl, d.nCT, nRTu, &x.t, &x.ct, &x.rt);
   } else {
     // column tiles of a row tile on neighbouring CTAs: they stream the same Φ rows together (L2)
     x.sp = w % d.S1;
     int r = w / d.S1;
     x.ct = rotate_ct(r % d.nCT, w, G, d.S1 * d.nCT, d.nCT);
     r /= d.nCT;
-    x.rt = r % d.nRT1;
-    x.t = r / d.nRT1;
+    x.rt = r % nRTu;
+    x.t = r / nRTu;
   }
+  if (tc.pair) x.rt = 2 * x.rt + rank;
   const int j0 = x.ct * tc.NT;
   x.ncol = min(tc.NT, d.P - j0);
   x.k0 = x.sp * d.K1;
@@ -680,18 +711,20 @@ __device__ __forceinline__ Unit make_unit1(const Dims &d, const TcCfg &tc, int w
   x.brow = j0;                                     // first direction column of the tile
   return x;
 }
-__device__ __forceinline__ Unit make_unit2(const Dims &d, const TcCfg &tc, int w, int G) {
+__device__ __forceinline__ Unit make_unit2(const Dims &d, const TcCfg &tc, int w, int G, int rank) {
   Unit x;
   x.stage = 2;
   x.sp = 0;
+  const int nRTu = nrt_units(d.nRT2, tc.pair);
   if (d.shared_phi) {
-    decode_banded(w, d.Tl, d.nCT, d.nRT2, &x.t, &x.ct, &x.rt);
+    decode_banded(w, d.Tl, d.nCT, nRTu, &x.t, &x.ct, &x.rt);
   } else {
     x.ct = rotate_ct(w % d.nCT, w, G, d.nCT, d.nCT);
     const int r = w / d.nCT;
-    x.rt = r % d.nRT2;
-    x.t = r / d.nRT2;
+    x.rt = r % nRTu;
+    x.t = r / nRTu;
   }
+  if (tc.pair) x.rt = 2 * x.rt + rank;
   const int j0 = x.ct * tc.NT;
   x.ncol = min(tc.NT, d.P - j0);
   x.k0 = 0;
@@ -706,7 +739,8 @@ __device__ __forceinline__ void unit_work(const KParams &p, Unit &x, int lane, u
   const Dims &d = p.d;
   const int j0 = x.ct * p.tc.NT;
   const int m = tile_mask(p.b.flag + (size_t)x.t * d.P + j0, x.ncol, lane, mask);
-  x.nmma = m ? ((x.ncol + 15) & ~15) : 0;
+  // a pair's MMA spans the whole tile (each CTA stages NT/2 columns; padding columns are zero-filled)
+  x.nmma = m ? (p.tc.pair ? p.tc.NT : ((x.ncol + 15) & ~15)) : 0;
   x.mean = x.ct == 0 && !(p.dbg_flags & 512) && mean_count(p.b.flagm + (size_t)x.t * d.C, d.C, lane) > 0;
 }
 
@@ -739,12 +773,16 @@ struct RingCtl {
 };
 
 // ---- producer (warp 0, converged; one elected lane issues) ---------------------------------------------------------------
+template <bool PR>
 __device__ __forceinline__ void produce(const KParams &p, const TcMaps &mp, unsigned char *sm, PSmemTail &tl,
-                                        RingCtl &rc, const Unit &x, unsigned long long *tr) {
+                                        RingCtl &rc, const Unit &x, unsigned long long *tr, uint32_t rank) {
   if (tr && (threadIdx.x & 31) == 0) tr[84] = clock64();
-  const uint32_t b_bytes = (uint32_t)p.tc.NT * 128;
+  const uint32_t b_bytes = (uint32_t)p.tc.NT * 128;       // one plane (hi or lo) of the tile's B
   const uint32_t mean_tx = x.stage == 1 ? (uint32_t)p.d.C * TK * 8 : (uint32_t)TK * p.d.Cp * 8;
-  const uint32_t bytes = A_BYTES + (x.nmma ? 2 * b_bytes : 0) + (x.mean ? mean_tx : 0);
+  // the local full barrier counts the A tile and mean chunk (and B when unpaired); a pair's B halves
+  // (hi | lo planes of NT/2 rows each per CTA) count on the leader's bfull
+  const uint32_t bytes = A_BYTES + ((x.nmma && !PR) ? 2 * b_bytes : 0) + (x.mean ? mean_tx : 0);
+  const uint32_t b_stage = PR ? b_bytes : 2 * b_bytes;    // B bytes in this CTA's stage
   for (int kc = 0; kc < x.nk; ++kc) {
     const uint32_t G = rc.g;
     const int st = rc.st;
@@ -764,7 +802,10 @@ __device__ __forceinline__ void produce(const KParams &p, const TcMaps &mp, unsi
     unsigned char *base = sm + (size_t)st * p.tc.stage_bytes;
     uint64_t *fb = &tl.full[st];
     if (p.dbg_flags & 128) {                  // diagnostic: no operand traffic
-      if ((threadIdx.x & 31) == 0) mbar_arrive(fb);
+      if ((threadIdx.x & 31) == 0) {
+        mbar_arrive(fb);
+        if (PR && x.nmma && rank == 0) mbar_arrive(&tl.bfull[st]);
+      }
       continue;
     }
     mbar_arrive_expect_tx_warp(fb, bytes);
@@ -774,14 +815,25 @@ __device__ __forceinline__ void produce(const KParams &p, const TcMaps &mp, unsi
     // rows (out-of-range rows and K columns are zero-filled), so tasks are isolated even where a tile
     // or a K chunk overhangs the task's matrix
     const int at = p.d.shared_phi ? 0 : x.t;
+    if (p.tc.pf && (threadIdx.x & 31) == 0) {   // A tiles PF chunks ahead into L2
+      const CUtensorMap *am = x.stage == 1 ? &mp.phi : &mp.phit;
+      for (int k2 = (kc == 0 ? rc.S : kc + p.tc.pf); k2 <= kc + p.tc.pf && k2 < x.nk; ++k2)
+        tma_prefetch_3d(am, x.k0 + k2 * TK, x.arow, at);
+    }
+    const CUtensorMap *bmap = x.stage == 1 ? &mp.d_hl : &mp.u_hl;
+    if (PR && x.nmma) {
+      const uint32_t bl = mapa_shared(smem_u32(&tl.bfull[st]), 0);
+      if (rank == 0) mbar_arrive_expect_tx_warp(&tl.bfull[st], 2 * b_bytes);
+      tma_load_4d_warp_pair(base + A_BYTES, bmap, k, x.brow + (int)rank * (p.tc.NT / 2), x.t, 0, bl);
+    }
     if (x.stage == 1) {
       tma_load_3d_warp(base, &mp.phi, k, x.arow, at, fb);
-      if (x.nmma) tma_load_4d_warp(base + A_BYTES, &mp.d_hl, k, x.brow, x.t, 0, fb);   // hi | lo tiles
-      if (x.mean) tma_load_3d_warp(base + A_BYTES + 2 * b_bytes, &mp.dm, k, 0, x.t, fb);
+      if (x.nmma && !PR) tma_load_4d_warp(base + A_BYTES, bmap, k, x.brow, x.t, 0, fb);   // hi | lo tiles
+      if (x.mean) tma_load_3d_warp(base + A_BYTES + b_stage, &mp.dm, k, 0, x.t, fb);
     } else {
       tma_load_3d_warp(base, &mp.phit, k, x.arow, at, fb);
-      if (x.nmma) tma_load_4d_warp(base + A_BYTES, &mp.u_hl, k, x.brow, x.t, 0, fb);
-      if (x.mean) tma_load_3d_warp(base + A_BYTES + 2 * b_bytes, &mp.um, 0, k, x.t, fb);
+      if (x.nmma && !PR) tma_load_4d_warp(base + A_BYTES, bmap, k, x.brow, x.t, 0, fb);
+      if (x.mean) tma_load_3d_warp(base + A_BYTES + b_stage, &mp.um, 0, k, x.t, fb);
     }
     if (tr && kc < 16 && (threadIdx.x & 31) == 0) tr[16 + kc] = clock64();
   }
@@ -801,16 +853,34 @@ __device__ __forceinline__ void produce(const KParams &p, const TcMaps &mp, unsi
 }
 
 // ---- MMA issuer (warp 1, converged; one elected lane issues) ------------------------------------
+// (CTA pairs: run by the leader's MMA warp only; its commits arrive on both CTAs' barriers)
+template <bool PR>
 __device__ __forceinline__ void mma_unit(const KParams &p, unsigned char *sm, PSmemTail &tl, RingCtl &rc,
-                                         uint32_t tmem, const Unit &x, unsigned long long *tr) {
+                                         uint32_t tmem, const Unit &x, unsigned long long *tr, uint32_t rank) {
   const TcCfg &tc = p.tc;
   const int lane = threadIdx.x & 31;
-  const uint32_t b_bytes = (uint32_t)tc.NT * 128;
+  if (PR && rank != 0) {
+    // a pair's peer: the leader issues the MMAs (and its commits release this CTA's stages); this
+    // warp only keeps its ring position and releases its slots of mean-only units (see below)
+    for (int kc = 0; kc < x.nk; ++kc) {
+      const int st = rc.st;
+      const uint32_t ph = rc.ph;
+      rc.next();
+      if (!x.nmma) {
+        mbar_wait(&tl.full[st], ph);
+        if (lane == 0) mbar_arrive(&tl.empty[st]);
+      }
+      __syncwarp();
+    }
+    return;
+  }
+  const uint32_t lo_off = (uint32_t)tc.NT * 128 / (PR ? 2 : 1);
   const int nacc = unit_nacc(tc, x.nk, p.dbg_flags);
-  const uint32_t idesc = idesc_tf32(TM, x.nmma > 0 ? x.nmma : 16);
+  const uint32_t idesc = idesc_tf32(PR ? 2 * TM : TM, x.nmma > 0 ? x.nmma : 32);
   const bool dbl = unit_dbl(tc, x.nk, p.dbg_flags);
-  // a full double-buffered tile: the 2-MMA form (N = 2·NT ≤ 256)
-  const bool cat = dbl && x.nmma == tc.NT && tc.slot == tc.NT && 2 * tc.NT <= 256 && !(p.dbg_flags & 4096);
+  // a full double-buffered tile: the 2-MMA form (N = 2·NT ≤ 256; unpaired only: a pair's stage
+  // holds half of the hi and of the lo plane, not a contiguous [hi | lo])
+  const bool cat = !PR && dbl && x.nmma == tc.NT && tc.slot == tc.NT && 2 * tc.NT <= 256 && !(p.dbg_flags & 4096);
   const uint32_t idesc2 = idesc_tf32(TM, cat ? 2 * tc.NT : 16);
   const int bi = dbl ? (int)(rc.ti & 1) : 0;
   const uint32_t tacc = tmem + (uint32_t)(bi * 2 * tc.slot);
@@ -828,7 +898,7 @@ __device__ __forceinline__ void mma_unit(const KParams &p, unsigned char *sm, PS
       const int sa = rc.ast;
       mbar_wait(&tl.afull[sa], rc.aph);       // A stage written (the A warps waited full[st] first)
       rc.nexta();
-      mbar_wait(&tl.full[st], ph);            // B staged
+      mbar_wait(PR ? &tl.bfull[st] : &tl.full[st], ph);   // B staged (a pair: both halves)
       if (tr && kc < 16 && lane == 0) tr[32 + kc] = clock64();
       if (!(p.dbg_flags & 2)) {
         fence_after_sync();
@@ -838,22 +908,41 @@ __device__ __forceinline__ void mma_unit(const KParams &p, unsigned char *sm, PS
           mma_stage_cat(tacc, tmem + (uint32_t)(tc.acol0 + 64 * sa), sm + (size_t)st * tc.stage_bytes, idesc2, idesc,
                         tc.NT, kc == 0);
         else
-          mma_stage(tacc, tmem + (uint32_t)(tc.acol0 + 64 * sa), sm + (size_t)st * tc.stage_bytes, b_bytes, idesc,
-                    q, tc.slot, kc == qfirst, kc == 0);
-        mma_commit_warp(&tl.aempty[sa]);      // the MMAs have read the A stage
-        mma_commit_warp(&tl.empty[st]);       // ... and the B tiles
+          mma_stage<PR>(tacc, tmem + (uint32_t)(tc.acol0 + 64 * sa), sm + (size_t)st * tc.stage_bytes, lo_off, idesc,
+                        q, tc.slot, kc == qfirst, kc == 0);
+        if (PR) {
+          mma_commit_warp_pair(&tl.aempty[sa]);   // both CTAs: the MMAs have read their A stages
+          mma_commit_warp_pair(&tl.empty[st]);    // ... and their B halves
+        } else {
+          mma_commit_warp(&tl.aempty[sa]);      // the MMAs have read the A stage
+          mma_commit_warp(&tl.empty[st]);       // ... and the B tiles
+        }
       } else if (lane == 0) {
         mbar_arrive(&tl.aempty[sa]);
         mbar_arrive(&tl.empty[st]);
+        if (PR) {
+          mbar_arrive_cluster(mapa_shared(smem_u32(&tl.aempty[sa]), 1));
+          mbar_arrive_cluster(mapa_shared(smem_u32(&tl.empty[st]), 1));
+        }
       }
-    } else if (lane == 0) {
-      mbar_arrive(&tl.empty[st]);             // the A warps' arrivals complete the stage
+    } else {
+      // no probe work in this unit (mean columns only): the MMA warp's share of empty[st] — after
+      // full[st], so it never runs ahead of the ring (an arrival for chunk G + S landing in chunk G's
+      // phase would complete that phase early and shift every later one: a hang).  A pair's CTAs
+      // each release their own slot here (the peer's MMA warp runs this path too).
+      mbar_wait(&tl.full[st], ph);
+      if (lane == 0) mbar_arrive(&tl.empty[st]);
     }
     __syncwarp();
   }
   if (x.nmma) {
     if (p.dbg_flags & 2) {
-      if (lane == 0) mbar_arrive(&tl.tfull[bi]);
+      if (lane == 0) {
+        mbar_arrive(&tl.tfull[bi]);
+        if (PR) mbar_arrive_cluster(mapa_shared(smem_u32(&tl.tfull[bi]), 1));
+      }
+    } else if (PR) {
+      mma_commit_warp_pair(&tl.tfull[bi]);   // both CTAs' accumulators ready
     } else {
       mma_commit_warp(&tl.tfull[bi]);        // all MMAs of the tile complete → accumulator ready
     }
@@ -906,6 +995,7 @@ __device__ __forceinline__ void split_handoff(const KParams &p, const Unit &x, P
 }
 
 // ---- A warps (2-5): the TMEM A stages ------------------------------------------------------------
+template <bool PR>
 __device__ void a_unit(const KParams &p, unsigned char *sm, PSmemTail &tl, RingCtl &rc, uint32_t tmem, const Unit &x,
                        unsigned long long *tr, unsigned long long *tr4) {
   const TcCfg &tc = p.tc;
@@ -927,7 +1017,10 @@ __device__ void a_unit(const KParams &p, unsigned char *sm, PSmemTail &tl, RingC
       tmem_wait_st();
       fence_before_sync();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&tl.afull[sa]);
+      if (lane == 0) {   // a pair's leader issues the MMA: its afull counts both CTAs' A warps
+        if (PR) mbar_arrive_cluster(mapa_shared(smem_u32(&tl.afull[sa]), 0));
+        else mbar_arrive(&tl.afull[sa]);
+      }
       if (tr && kc < 16) tr[90 + kc] = clock64();
       if (tr4 && lane == 0 && kc < 16) tr4[16 * aq + kc] = clock64();
     }
@@ -946,7 +1039,7 @@ __device__ __forceinline__ void mean_kloop(const KParams &p, unsigned char *sm, 
                                            const Unit &x, double (&macc)[4][NTC][2], unsigned long long *trm) {
   const TcCfg &tc = p.tc;
   const int ew = (threadIdx.x >> 5) & 3, lane = threadIdx.x & 31;
-  const uint32_t mu_off = A_BYTES + 2 * (uint32_t)tc.NT * 128;
+  const uint32_t mu_off = A_BYTES + (tc.pair ? 1u : 2u) * (uint32_t)tc.NT * 128;
 #pragma unroll
   for (int mt = 0; mt < 4; ++mt)
 #pragma unroll
@@ -1068,7 +1161,19 @@ __device__ void a_help_drain2(const KParams &p, unsigned char *sm, PSmemTail &tl
   pair_sync();                                // W stores ordered before the epilogue's completion release
 }
 
-template <int CC>
+// the accumulator buffer drained: the MMA warp (a pair's leader) may overwrite it
+template <bool PR>
+__device__ __forceinline__ void tempty_arrive(PSmemTail &tl, int bi, bool both) {
+  if (PR) {
+    mbar_arrive_cluster(mapa_shared(smem_u32(&tl.tempty[bi]), 0));
+    if (both) mbar_arrive_cluster(mapa_shared(smem_u32(&tl.tempty[1]), 0));
+  } else {
+    mbar_arrive(&tl.tempty[bi]);
+    if (both) mbar_arrive(&tl.tempty[1]);
+  }
+}
+
+template <int CC, bool PR>
 __device__ void probe_epilogue(const KParams &p, unsigned char *sm, PSmemTail &tl, RingCtl &rc, uint32_t tmem,
                                const Unit &x, const uint32_t *mask_in, unsigned long long *tr, bool helped) {
   if (tr && threadIdx.x != EPI0) tr = nullptr;
@@ -1133,7 +1238,7 @@ __device__ void probe_epilogue(const KParams &p, unsigned char *sm, PSmemTail &t
       }
     }
     epi_sync();
-    if (et < C)
+    if (et < C && x.rt < d.nRT2)
       stv(p.b.dAdm + ((size_t)x.t * C + et) * d.nRT2 + x.rt, tl.redm[0][et] + tl.redm[1][et] + tl.redm[2][et] + tl.redm[3][et]);
     epi_sync();                               // tl.redm is reused by the next unit
   }
@@ -1187,10 +1292,7 @@ __device__ void probe_epilogue(const KParams &p, unsigned char *sm, PSmemTail &t
       fence_before_sync();
       __syncwarp();
       const int bi = acc_buf(rc, dbl);
-      if (lane == 0) {                         // the MMA warp may overwrite the accumulator
-        mbar_arrive(&tl.tempty[bi]);
-        if (!dbl && tc.dbl) mbar_arrive(&tl.tempty[1]);
-      }
+      if (lane == 0) tempty_arrive<PR>(tl, bi, !dbl && tc.dbl);   // the MMA warp may overwrite the accumulator
       rc.tf[bi]++;
       rc.ti++;
       if (tr) tr[81] = clock64();
@@ -1349,8 +1451,7 @@ __device__ void probe_epilogue(const KParams &p, unsigned char *sm, PSmemTail &t
   {
     const int bi = acc_buf(rc, dbl);
     if (lane == 0) {
-      mbar_arrive(&tl.tempty[bi]);
-      if (!dbl && tc.dbl) mbar_arrive(&tl.tempty[1]);
+      tempty_arrive<PR>(tl, bi, !dbl && tc.dbl);
       if (dts) mbar_arrive(&tl.dempty);
     }
     rc.tf[bi]++;
@@ -1358,7 +1459,7 @@ __device__ void probe_epilogue(const KParams &p, unsigned char *sm, PSmemTail &t
   }
   if (tr) tr[81] = clock64();
   epi_sync();
-  for (int c = et; c < x.ncol; c += 128)
+  for (int c = et; c < x.ncol && x.rt < d.nRT2; c += 128)
     if ((mask[c >> 5] >> (c & 31)) & 1u)
       stv(p.b.dAd + ((size_t)x.t * P + j0 + c) * d.nRT2 + x.rt,
           tl.red[0][c] + tl.red[1][c] + tl.red[2][c] + tl.red[3][c]);
@@ -1369,7 +1470,8 @@ __device__ void probe_epilogue(const KParams &p, unsigned char *sm, PSmemTail &t
 // ---------------------------------------------------------------------------------------------
 // the persistent CG kernel: grid = #SMs (cooperative), 320 threads, one CTA per SM
 // ---------------------------------------------------------------------------------------------
-template <int CC>
+// PR: CTA pairs (2-CTA clusters, cta_group::2 MMAs of M = 256, each CTA staging half of B)
+template <int CC, bool PR>
 __global__ void __launch_bounds__(NTHREADS, 1) k_cg_persistent(KParams p, const __grid_constant__ TcMaps mp) {
   extern __shared__ __align__(1024) unsigned char tc_raw[];
   unsigned char *sm = reinterpret_cast<unsigned char *>((reinterpret_cast<uintptr_t>(tc_raw) + 1023) & ~(uintptr_t)1023);
@@ -1378,19 +1480,23 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_cg_persistent(KParams p, const 
   PSmemTail &tl = *reinterpret_cast<PSmemTail *>(sm + (size_t)tc.stages * tc.stage_bytes + tc.dtile_bytes);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int G = gridDim.x, b = blockIdx.x;
+  // units are dealt to GU dealers: the CTAs, or the CTA pairs (both CTAs of a pair walk the same units)
+  const uint32_t rank = PR ? cluster_rank() : 0u;
+  const int GU = PR ? G / 2 : G, bu = PR ? b / 2 : b;
   if (tid == 0) {
     for (int s = 0; s < tc.stages; ++s) {
       mbar_init(&tl.full[s], 1);
+      mbar_init(&tl.bfull[s], 1);             // a pair's leader: its expect_tx; bytes of both CTAs' B halves
       mbar_init(&tl.empty[s], 5);             // the MMA warp's commit (or arrive) + the 4 A warps
       mbar_init(&tl.mdone[s], 4);             // the 4 epilogue warps' fp64 work on a mean chunk
     }
     for (int s = 0; s < tc.sa; ++s) {
-      mbar_init(&tl.afull[s], 4);
+      mbar_init(&tl.afull[s], PR ? 8 : 4);    // a pair's leader counts both CTAs' A warps
       mbar_init(&tl.aempty[s], 1);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tl.tfull[i], 1);
-      mbar_init(&tl.tempty[i], 4);
+      mbar_init(&tl.tempty[i], PR ? 8 : 4);   // both CTAs' epilogue warps (leader's copy)
     }
     mbar_init(&tl.dfull, 1);
     mbar_init(&tl.dempty, 4);
@@ -1400,16 +1506,22 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_cg_persistent(KParams p, const 
     prefetch_tmap(&mp.phi); prefetch_tmap(&mp.phit); prefetch_tmap(&mp.u_hl); prefetch_tmap(&mp.d_hl);
     prefetch_tmap(&mp.dm); prefetch_tmap(&mp.um); prefetch_tmap(&mp.d32);
   }
-  if (warp == 2) tmem_alloc<512>(&tl.tslot);
+  if (warp == 2) {
+    if (PR) tmem_alloc_pair<512>(&tl.tslot);
+    else tmem_alloc<512>(&tl.tslot);
+  }
   fence_before_sync();
   __syncthreads();
+  if (PR) cluster_sync_all();                 // the peer's barriers exist before any remote arrive
   fence_after_sync();
   const uint32_t tmem = tl.tslot;
   RingCtl rc{tc.stages, 0u, 0, 0u, tc.sa, 0u, 0, 0u, 0u, {0u, 0u}, {0u, 0u}, 0u, 0u, {0u, 0u, 0u, 0u, 0u, 0u}};
   unsigned epoch = 0;
   unsigned *bar = p.b.gridbar;
-  const int n1 = d.Tl * d.nCT * d.nRT1 * d.S1, n2 = d.Tl * d.nCT * d.nRT2;
-  const int E1 = d.nCT * d.nRT1 * d.S1, E2 = d.nCT * d.nRT2;   // units per task and stage
+  const int nRTu1 = nrt_units(d.nRT1, PR), nRTu2 = nrt_units(d.nRT2, PR);
+  const int n1 = d.Tl * d.nCT * nRTu1 * d.S1, n2 = d.Tl * d.nCT * nRTu2;
+  // completion signals per task and stage (one per CTA and unit: a pair unit signals twice)
+  const int E1 = d.nCT * nRTu1 * d.S1 * (PR ? 2 : 1), E2 = d.nCT * nRTu2 * (PR ? 2 : 1);
   int *cnt1 = p.b.dep, *cnt2 = p.b.dep + d.Tl;
   const int ncols = d.Tl * (d.P + d.C);
   const bool producer = warp == 0, issuer = warp == 1;
@@ -1425,19 +1537,19 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_cg_persistent(KParams p, const 
     // ---- phase 1: U = Φ D ----
     if (tr1 && tid == 0) tr1[127] = clock64();   // trace times are SM clocks from here
     if (tile_role) {
-      for (int w = b; w < n1; w += G, tr1 = nullptr) {
-        Unit x = make_unit1(d, tc, w, G);
+      for (int w = bu; w < n1; w += GU, tr1 = nullptr) {
+        Unit x = make_unit1(d, tc, w, GU, (int)rank);
         uint32_t mask[TC_NTMAX / 32];
         unit_work(p, x, lane, mask);
         if (!x.nmma && !x.mean) {
           if (tid == EPI0) dep_signal(cnt1 + x.t);
           continue;
         }
-        if (producer) produce(p, mp, sm, tl, rc, x, tr1);
-        else if (issuer) mma_unit(p, sm, tl, rc, tmem, x, tr1);
-        else if (aw) a_unit(p, sm, tl, rc, tmem, x, (tr1 && threadIdx.x == AW0) ? tr1 : nullptr, nullptr);
+        if (producer) produce<PR>(p, mp, sm, tl, rc, x, tr1, rank);
+        else if (issuer) mma_unit<PR>(p, sm, tl, rc, tmem, x, tr1, rank);
+        else if (aw) a_unit<PR>(p, sm, tl, rc, tmem, x, (tr1 && threadIdx.x == AW0) ? tr1 : nullptr, nullptr);
         else if (epi) {
-          probe_epilogue<CC>(p, sm, tl, rc, tmem, x, mask, tr1, false);
+          probe_epilogue<CC, PR>(p, sm, tl, rc, tmem, x, mask, tr1, false);
           epi_sync();                         // this tile's U / Um stores, then EPI0's release
           if (tid == EPI0) dep_signal(cnt1 + x.t);
         }
@@ -1448,8 +1560,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_cg_persistent(KParams p, const 
     // ---- phase 2: W = βΦᵀU + αD, dᵀW partials ----
     if (tr2 && tid == 0) tr2[127] = clock64();
     if (tile_role) {
-      for (int w = b; w < n2; w += G, tr2 = nullptr) {
-        Unit x = make_unit2(d, tc, w, G);
+      for (int w = bu; w < n2; w += GU, tr2 = nullptr) {
+        Unit x = make_unit2(d, tc, w, GU, (int)rank);
         uint32_t mask[TC_NTMAX / 32];
         unit_work(p, x, lane, mask);
         if (!x.nmma && !x.mean) {
@@ -1460,16 +1572,16 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_cg_persistent(KParams p, const 
           if (lane == 0) dep_wait(cnt1 + x.t, (u + 1) * E1);   // U, Um of task t complete
           __syncwarp();
           fence_proxy_async_global();         // the acquired generic writes → this warp's TMA reads
-          produce(p, mp, sm, tl, rc, x, tr2);
+          produce<PR>(p, mp, sm, tl, rc, x, tr2, rank);
         }
-        else if (issuer) mma_unit(p, sm, tl, rc, tmem, x, tr2);
+        else if (issuer) mma_unit<PR>(p, sm, tl, rc, tmem, x, tr2, rank);
         else if (aw) {
-          a_unit(p, sm, tl, rc, tmem, x, (tr2 && threadIdx.x == AW0) ? tr2 : nullptr, tr2 ? tr2 + 160 : nullptr);
-          if (help2 && x.nmma && (w + G >= n2 || help_mean(p, x))) a_help_drain2<CC>(p, sm, tl, rc, x);
+          a_unit<PR>(p, sm, tl, rc, tmem, x, (tr2 && threadIdx.x == AW0) ? tr2 : nullptr, tr2 ? tr2 + 160 : nullptr);
+          if (help2 && x.nmma && (w + GU >= n2 || help_mean(p, x))) a_help_drain2<CC>(p, sm, tl, rc, x);
         }
         else if (epi) {
           if (tid == EPI0 && x.rt == 0 && x.nmma) atomicAdd(p.b.histp + u, x.nmma);
-          probe_epilogue<CC>(p, sm, tl, rc, tmem, x, mask, tr2, help2 && (w + G >= n2 || (x.nmma && help_mean(p, x))));
+          probe_epilogue<CC, PR>(p, sm, tl, rc, tmem, x, mask, tr2, help2 && (w + GU >= n2 || (x.nmma && help_mean(p, x))));
           epi_sync();                         // this tile's W / Wm / dᵀAd stores, then EPI0's release
           if (tid == EPI0) dep_signal(cnt2 + x.t);
         }
@@ -1514,7 +1626,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) k_cg_persistent(KParams p, const 
   }
   fence_before_sync();
   __syncthreads();
-  if (warp == 2) tmem_dealloc<512>(tmem);
+  if (PR) {
+    cluster_sync_all();                       // the peer is done with this pair's tensor memory
+    if (warp == 2) tmem_dealloc_pair<512>(tmem);
+  } else if (warp == 2) {
+    tmem_dealloc<512>(tmem);
+  }
 }
 
 // Φᵀ (fp32) of every task, once at init: the K-major A operand of stage 2.  32×32 smem-tiled transpose.
@@ -1593,18 +1710,23 @@ bool encode_maps(const KParams &p, TcMaps *m, char *why) {
                   encode_3d(enc, &m->dm, b.Dm, F64, 8, Tl, d.C, d.D, TK, d.C, false) &&
                   encode_3d(enc, &m->um, b.Um, F64, 8, Tl, d.N, d.Cp, d.Cp, TK, false) &&
                   encode_3d(enc, &m->d32, b.D32, F32, 4, Tl, d.P, d.D, TM, NT, false) &&
-                  encode_hilo(enc, &m->u_hl, b.Uh, b.Ul, Tl, d.Pp, d.N, 32, NT) &&
-                  encode_hilo(enc, &m->d_hl, b.Dh, b.Dl, Tl, d.P, d.D, 32, NT);
+                  encode_hilo(enc, &m->u_hl, b.Uh, b.Ul, Tl, d.Pp, d.N, 32, p.tc.pair ? NT / 2 : NT) &&
+                  encode_hilo(enc, &m->d_hl, b.Dh, b.Dl, Tl, d.P, d.D, 32, p.tc.pair ? NT / 2 : NT);
   if (!ok) snprintf(why, 256, "cuTensorMapEncodeTiled failed");
   return ok;
 }
 
 // kernel instantiation for the cluster count: CC ∈ {4, 8, 16} bounds C at compile time
 typedef void (*CgKernel)(KParams, const TcMaps);
-CgKernel cg_kernel(int C) {
-  if (C <= 4) return k_cg_persistent<4>;
-  if (C <= 8) return k_cg_persistent<8>;
-  return k_cg_persistent<16>;
+CgKernel cg_kernel(int C, int pair) {
+  if (pair) {
+    if (C <= 4) return k_cg_persistent<4, true>;
+    if (C <= 8) return k_cg_persistent<8, true>;
+    return k_cg_persistent<16, true>;
+  }
+  if (C <= 4) return k_cg_persistent<4, false>;
+  if (C <= 8) return k_cg_persistent<8, false>;
+  return k_cg_persistent<16, false>;
 }
 
 int cg_grid_size(const KParams &p) {
@@ -1612,10 +1734,27 @@ int cg_grid_size(const KParams &p) {
   if (cudaGetDevice(&dev) != cudaSuccess) return 0;
   if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return 0;
   const size_t smem = tc_smem_bytes(p.tc, p.d.P);
-  const CgKernel k = cg_kernel(p.d.C);
+  const CgKernel k = cg_kernel(p.d.C, p.tc.pair);
   if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) return 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, NTHREADS, smem) != cudaSuccess) return 0;
-  return occ >= 1 ? sms : 0;   // one CTA per SM (512 TMEM columns each)
+  if (occ < 1) return 0;
+  if (!p.tc.pair) return sms;  // one CTA per SM (512 TMEM columns each)
+  // CTA pairs: as many 2-CTA clusters as can be co-resident (every CTA must be resident: grid barrier)
+  if (cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 0) != cudaSuccess) return 0;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(sms / 2 * 2);
+  cfg.blockDim = dim3(NTHREADS);
+  cfg.dynamicSmemBytes = smem;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int clusters = 0;
+  if (cudaOccupancyMaxActiveClusters(&clusters, k, &cfg) != cudaSuccess) return 0;
+  return std::min(sms / 2, clusters) * 2;
 }
 
 cudaError_t launch_split_phi(const KParams &p, cudaStream_t s) {
@@ -1636,12 +1775,19 @@ cudaError_t launch_cg_persistent(const KParams &p, const TcMaps &maps, int grid,
   cfg.blockDim = dim3(NTHREADS);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeCooperative;   // co-residency of all CTAs (grid barriers)
   attr[0].val.cooperative = 1;
+  int na = 1;
+  if (p.tc.pair) {   // 2-CTA clusters (the grid is sized to the co-resident cluster count)
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+  }
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, cg_kernel(p.d.C), p, maps);
+  cfg.numAttrs = na;
+  return cudaLaunchKernelEx(&cfg, cg_kernel(p.d.C, p.tc.pair), p, maps);
 }
 
 }  // namespace cmtcs

@@ -169,11 +169,15 @@ __global__ void k_estep_finish(KParams p) {
     for (int i = tid; i < d.D; i += blockDim.x) quad = fma(al[i] * mu[i], mu[i], quad);
     quad = block_sum(quad, sh);
     double res = 0.0;
-    for (int n = tid; n < d.N; n += blockDim.x) {
-      const double rv = (double)p.y[(size_t)t * d.N + n] - p.b.Um[((size_t)t * d.N + n) * d.Cp + c];
-      res = fma(rv, rv, res);
+    if (d.op == CMTCS_OP_DENSE) {
+      for (int n = tid; n < d.N; n += blockDim.x) {
+        const double rv = (double)p.y[(size_t)t * d.N + n] - p.b.Um[((size_t)t * d.N + n) * d.Cp + c];
+        res = fma(rv, rv, res);
+      }
+      res = block_sum(res, sh);
+    } else {
+      res = p.b.resm[(size_t)t * d.C + c];   // computed with μ by the partial-Fourier CG kernel
     }
-    res = block_sum(res, sh);
     if (tid == 0) {
       double tsum = 0.0;
       for (int k = 0; k < d.K; ++k) tsum += p.b.tau[(size_t)t * d.P + c * d.K + k];
@@ -200,7 +204,9 @@ __global__ void k_estep_finish(KParams p) {
     double se = 0.0;
     for (int c = 0; c < d.C; ++c) se += exp(a[c] - mx);
     for (int c = 0; c < d.C; ++c) p.b.q[t * d.C + c] = exp(a[c] - mx) / se;
-    p.b.ll[t] = mx + log(se) + 0.5 * d.N * log(beta / (2.0 * 3.14159265358979323846));
+    // N real measurements per task (the partial-Fourier operator's real embedding has 2N: reading F1)
+    const double nmeas = d.op == CMTCS_OP_PARTIAL_FOURIER ? 2.0 * d.N : (double)d.N;
+    p.b.ll[t] = mx + log(se) + 0.5 * nmeas * log(beta / (2.0 * 3.14159265358979323846));
   }
 }
 

@@ -16,6 +16,8 @@ class CoFEM:
 
     phi: cuda fp32 [T_loc, N, D] (or [N, D] with shared_phi), y: cuda fp32 [T_loc, N].
     Tasks of this rank are global tasks task_begin .. task_begin + T_loc - 1 of T.
+    Partial-Fourier sensing (the paper's §4 workload): phi=None, fourier_rows = cuda
+    int32 [T_loc, N] sampled DFT rows, y = cuda fp32 [T_loc, 2N] (real parts, then imaginary), D given.
     """
 
     def __init__(self, phi: torch.Tensor, y: torch.Tensor, *, T: int, C: int, K: int, beta: float,
@@ -23,15 +25,25 @@ class CoFEM:
                  task_begin: int = 0, shared_phi: bool = False, em_iter0: int = 0,
                  alpha_max: float = 1e12, var_floor: float = 1e-12, empty_eps: float = 1e-10,
                  mean_rel_tol: float = -1.0,
-                 nccl_uid: bytes | None = None, rank: int = 0, world: int = 1, stream=None):
-        if not (phi.is_cuda and y.is_cuda):
-            raise ValueError("phi and y must be CUDA tensors (no CPU path exists)")
-        self.phi = phi.contiguous() if phi.dtype == torch.float32 else phi.float().contiguous()
+                 nccl_uid: bytes | None = None, rank: int = 0, world: int = 1, stream=None,
+                 fourier_rows: torch.Tensor | None = None, D: int | None = None):
+        fourier = fourier_rows is not None
+        if not (y.is_cuda and (fourier_rows.is_cuda if fourier else phi.is_cuda)):
+            raise ValueError("phi (or fourier_rows) and y must be CUDA tensors (no CPU path exists)")
         self.y = y.contiguous() if y.dtype == torch.float32 else y.float().contiguous()
-        self.device = self.phi.device
+        self.device = self.y.device
         T_loc = self.y.shape[0]
-        N = self.y.shape[1]
-        D = self.phi.shape[-1]
+        if fourier:
+            self.phi = None
+            self.rows = fourier_rows.to(torch.int32).contiguous()
+            N = self.rows.shape[1]
+            if D is None:
+                raise ValueError("the partial-Fourier operator needs D")
+        else:
+            self.phi = phi.contiguous() if phi.dtype == torch.float32 else phi.float().contiguous()
+            self.rows = None
+            N = self.y.shape[1]
+            D = self.phi.shape[-1]
         self.T, self.T_loc, self.N, self.D, self.C, self.K = T, T_loc, N, D, C, K
         self._pi = np.ascontiguousarray(np.full(C, 1.0 / C) if pi is None else np.asarray(pi, np.float64))
         self.problem = _c.cmtcs_problem(
@@ -40,7 +52,9 @@ class CoFEM:
             cg_rel_tol=float(cg_rel_tol), alpha_max=float(alpha_max), var_floor=float(var_floor),
             empty_eps=float(empty_eps), probe_seed=int(probe_seed) & ((1 << 64) - 1),
             task_begin=int(task_begin), task_end=int(task_begin) + T_loc, em_iter0=int(em_iter0),
-            mean_rel_tol=float(mean_rel_tol))
+            mean_rel_tol=float(mean_rel_tol),
+            op_kind=_c.CMTCS_OP_PARTIAL_FOURIER if fourier else _c.CMTCS_OP_DENSE,
+            fourier_rows=self.rows.data_ptr() if fourier else None)
         a0 = torch.ones(C, D, dtype=torch.float64, device=self.device) if alpha0 is None else \
             torch.as_tensor(np.asarray(alpha0, np.float64) if not torch.is_tensor(alpha0) else alpha0,
                             dtype=torch.float64).to(self.device).contiguous()
@@ -48,7 +62,7 @@ class CoFEM:
         self.workspace = torch.empty(self.ws_bytes + 256, dtype=torch.uint8, device=self.device)
         ws_ptr = (self.workspace.data_ptr() + 255) & ~255
         self.stream = torch.cuda.current_stream(self.device) if stream is None else stream
-        self.ctx = _c.cmtcs_init(self.problem, self.phi.data_ptr(), self.y.data_ptr(), a0.data_ptr(),
+        self.ctx = _c.cmtcs_init(self.problem, None if fourier else self.phi.data_ptr(), self.y.data_ptr(), a0.data_ptr(),
                                  ws_ptr, self.ws_bytes, nccl_uid, rank, world,
                                  self.device.index if self.device.index is not None else 0,
                                  self.stream.cuda_stream)

@@ -15,6 +15,11 @@ on its own and is bit-identical to the same tasks of the full set.
 Streams of numpy.random.SeedSequence([ROOT, cfg_id, stream, t]):
     0 supports (per config, t = 0)      1 Phi_t (t = task; shared Phi uses t = 0)
     2 nonzero values of z_t             3 noise eps_t            4 task labels (t = 0)
+    5 sampled Fourier rows of task t (partial-Fourier configs)
+
+Config 6 is the paper's own §4 workload: Phi_t = Omega_t F, the unitary DFT F
+undersampled by a random row mask Omega_t per task (N = D/4 rows), real-embedded as
+[Re(Omega_t F); Im(Omega_t F)] (reading F1), 5 % sparse N(0,1) signals, sigma = 0.05.
 """
 from __future__ import annotations
 
@@ -45,6 +50,7 @@ class Config:
     overlap_core: int = 0         # indices shared by every cluster's support (C2: 20 % overlap)
     values: str = "normal"        # "normal": N(0,1) nonzeros; "sign": +-1 with random sign
     shared_phi: bool = False      # C5: one Phi for all tasks
+    operator: str = "dense"       # "dense": Phi_t given as a matrix; "fourier": Phi_t = Omega_t F (C6)
 
     @property
     def beta(self) -> float:
@@ -75,6 +81,10 @@ CONFIGS: Dict[int, Config] = {
               cg_tol=1e-6, cluster_sizes=(32,) * 8, support=200, values="sign"),
     5: Config(5, "C5-sharedPhi", T=512, C=16, N=4096, D=16384, K=20, sigma=0.01, em_iters=10,
               cg_cap=300, cg_tol=1e-6, cluster_sizes=(32,) * 16, support=400, shared_phi=True),
+    # the paper's §4 workload: partial DFT, N = D/4 sampled rows, 5 % support,
+    # sigma = 0.05, K = 15 probes, U = 50 CG steps; T/C in the range of Fig. 1(e, f)
+    6: Config(6, "C6-partialFourier", T=64, C=4, N=2048, D=8192, K=15, sigma=0.05, em_iters=30,
+              cg_cap=50, cg_tol=1e-6, cluster_sizes=(16,) * 4, support=410, operator="fourier"),
 }
 
 
@@ -114,6 +124,18 @@ def phi(cfg: Config, t: int) -> np.ndarray:
     return a
 
 
+def fourier_rows(cfg: Config, t: int) -> np.ndarray:
+    """Omega_t: N distinct DFT rows of [0, D), drawn uniformly per task, sorted."""
+    return np.sort(_rng(cfg, 5, t).choice(cfg.D, size=cfg.N, replace=False)).astype(np.int32)
+
+
+def fourier_measure(cfg: Config, rows: np.ndarray, z: np.ndarray) -> np.ndarray:
+    """The forward model Phi_t z for Phi_t = [Re(Omega F); Im(Omega F)], F the unitary DFT (the
+    data model of Eq. 1 evaluated with numpy's FFT; fp64)."""
+    f = np.fft.fft(z) / math.sqrt(cfg.D)
+    return np.concatenate([f.real[rows], f.imag[rows]])
+
+
 def z_true(cfg: Config, t: int, sup=None, lab=None) -> np.ndarray:
     sup = supports(cfg) if sup is None else sup
     lab = labels(cfg) if lab is None else lab
@@ -138,7 +160,8 @@ def measurements(cfg: Config, t: int, phi_t: np.ndarray, z: np.ndarray) -> np.nd
 def generate(cfg: Config, tasks: Optional[Sequence[int]] = None) -> dict:
     """Data of the tasks in `tasks` (default: all).  Returns a dict:
 
-    phi   float32 [T_sel, N, D]   (shared_phi: [N, D])
+    phi   float32 [T_sel, N, D]   (shared_phi: [N, D]; None for the partial-Fourier config, whose
+                                   Phi_t is given by `rows` int32 [T_sel, N] and y has 2N entries)
     y     float32 [T_sel, N]
     z     float64 [T_sel, D]      true signals
     labels int32  [T_sel]         true clusters
@@ -148,6 +171,14 @@ def generate(cfg: Config, tasks: Optional[Sequence[int]] = None) -> dict:
     tasks = np.arange(cfg.T) if tasks is None else np.asarray(list(tasks), dtype=np.int64)
     sup = supports(cfg)
     lab = labels(cfg)
+    if cfg.operator == "fourier":
+        rows = np.stack([fourier_rows(cfg, int(t)) for t in tasks])
+        zs = np.stack([z_true(cfg, int(t), sup, lab) for t in tasks])
+        ys = np.stack([(fourier_measure(cfg, rows[i], zs[i])
+                        + _rng(cfg, 3, int(t)).standard_normal(2 * cfg.N) * cfg.sigma).astype(np.float32)
+                       for i, t in enumerate(tasks)])
+        return dict(phi=None, rows=rows, y=ys, z=zs, labels=lab[tasks], tasks=tasks, beta=cfg.beta,
+                    pi=np.full(cfg.C, 1.0 / cfg.C), alpha0=np.ones((cfg.C, cfg.D)), cfg=cfg)
     if cfg.shared_phi:
         ph = phi(cfg, 0)
         ph64 = ph.astype(np.float64)

@@ -20,9 +20,11 @@ def make_gpu(data, *, K=None, tol=None, cap=None, alpha=None, em_iter0=0, task_b
     import torch
     from paper_2310_00420_b200 import CoFEM
     cfg = data["cfg"]
-    phi = torch.from_numpy(np.ascontiguousarray(data["phi"])).cuda()
+    fourier = data.get("phi") is None
+    phi = None if fourier else torch.from_numpy(np.ascontiguousarray(data["phi"])).cuda()
+    rows = torch.from_numpy(np.ascontiguousarray(data["rows"])).cuda() if fourier else None
     y = torch.from_numpy(np.ascontiguousarray(data["y"])).cuda()
-    return CoFEM(phi, y, T=cfg.T if T is None else T, C=data["alpha0"].shape[0],
+    return CoFEM(phi, y, fourier_rows=rows, D=cfg.D, T=cfg.T if T is None else T, C=data["alpha0"].shape[0],
                  K=cfg.K if K is None else K, beta=data["beta"],
                  cg_max_iters=cfg.cg_cap if cap is None else cap,
                  cg_rel_tol=cfg.cg_tol if tol is None else tol,

@@ -50,6 +50,7 @@ int main(void){
          offsetof(cmtcs_problem, probe_seed), offsetof(cmtcs_problem, em_iter0), sizeof(cmtcs_step_info));
   printf("%zu %zu %zu %zu\n", offsetof(cmtcs_step_info, probe_steps_mean), offsetof(cmtcs_step_info, kernel_launches), offsetof(cmtcs_step_info, tile_col_iters),
          offsetof(cmtcs_problem, mean_rel_tol));
+  printf("%zu %zu %d\n", offsetof(cmtcs_problem, op_kind), offsetof(cmtcs_problem, fourier_rows), (int)CMTCS_OP_PARTIAL_FOURIER);
   return 0; }
 '''
     with tempfile.TemporaryDirectory() as d:
@@ -60,7 +61,8 @@ int main(void){
         out = subprocess.check_output([exe]).decode().split()
     P, S = cmtcs.cmtcs_problem, cmtcs.cmtcs_step_info
     want = [ctypes.sizeof(P), P.beta.offset, P.probe_seed.offset, P.em_iter0.offset, ctypes.sizeof(S),
-            S.probe_steps_mean.offset, S.kernel_launches.offset, S.tile_col_iters.offset, P.mean_rel_tol.offset]
+            S.probe_steps_mean.offset, S.kernel_launches.offset, S.tile_col_iters.offset, P.mean_rel_tol.offset,
+            P.op_kind.offset, P.fourier_rows.offset, cmtcs.CMTCS_OP_PARTIAL_FOURIER]
     assert [int(x) for x in out] == want
 
 

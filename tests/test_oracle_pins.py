@@ -362,3 +362,56 @@ def test_cluster_subset_equals_full_computation():
     sub = O.cofem_task(data["phi"][0], data["y"][0], data["beta"], alpha, data["pi"], P, 1e-8, 80, clusters=[2, 0])
     for k in ("mu", "s", "nu"):
         np.testing.assert_array_equal(sub[k], full[k][[2, 0]])
+
+
+# ---------------------------------------------------- partial-Fourier Φ = Ω F ----
+def test_partial_fourier_equals_library_fft():
+    """Φv = [Re(F v)[rows]; Im(F v)[rows]] with F the unitary DFT: numpy's FFT (pocketfft) of v
+    divided by √D, restricted to the sampled rows (the paper's Ω), real-embedded."""
+    rng = np.random.default_rng(31)
+    for D in (8, 64, 100, 256):
+        rows = np.sort(rng.choice(D, size=D // 4, replace=False))
+        v = rng.standard_normal(D)
+        f = np.fft.fft(v) / math.sqrt(D)
+        want = np.concatenate([f.real[rows], f.imag[rows]])
+        np.testing.assert_allclose(O.partial_fourier_matrix(D, rows) @ v, want, rtol=0, atol=1e-12)
+
+
+def test_partial_fourier_dc_row_and_full_mask_unitary():
+    """D = 4, Ω = the DC row, v = 1 → Φv = [4/√4, 0] = [2, 0].  Ω = I → ΦᵀΦ = I
+    (F unitary: Parseval), the real embedding preserving it."""
+    np.testing.assert_allclose(O.partial_fourier_matrix(4, [0]) @ np.ones(4), [2.0, 0.0], atol=1e-15)
+    for D in (4, 16, 30):
+        P = O.partial_fourier_matrix(D, np.arange(D))
+        np.testing.assert_allclose(P.T @ P, np.eye(D), atol=1e-12)
+
+
+def test_partial_fourier_normal_operator_spectrum():
+    """ΦᵀΦ = Re(Fᴴ ΩᵀΩ F) is the circulant whose symbol is m_sym(k) = (m(k) + m(−k mod D))/2 for the
+    0/1 mask m of the sampled rows (convolution theorem), so its eigenvalues are exactly the D values
+    m_sym(k) ∈ {0, ½, 1} — e.g. frequency k alone (k ≠ 0, D/2) contributes ½ twice."""
+    rng = np.random.default_rng(32)
+    for D in (16, 64, 90):
+        rows = np.sort(rng.choice(D, size=D // 4, replace=False))
+        m = np.zeros(D)
+        m[rows] = 1.0
+        msym = 0.5 * (m + m[(-np.arange(D)) % D])
+        P = O.partial_fourier_matrix(D, rows)
+        lam = np.linalg.eigvalsh(P.T @ P)
+        np.testing.assert_allclose(np.sort(lam), np.sort(msym), atol=1e-12)
+
+
+def test_partial_fourier_task_data_follow_the_model():
+    """Config 6 data (synthetic): y_t − Φ_t z_t is the N(0, σ²) noise of Eq. 1, with
+    Φ_t = Ω_t F the oracle's dense real-embedded partial DFT, and the oracle E-step at a tiny D runs
+    on it (Φ built from the task's rows)."""
+    cfg = synthetic.CONFIGS[6]
+    d = synthetic.generate(cfg, [3])
+    P = O.partial_fourier_matrix(cfg.D, d["rows"][0])
+    res = d["y"][0].astype(np.float64) - P @ d["z"][0]
+    assert abs(np.std(res) / cfg.sigma - 1.0) < 0.05 and abs(np.mean(res)) < 5 * cfg.sigma / np.sqrt(res.size)
+    small = cfg.replace(D=64, N=16, T=2, support=4, cluster_sizes=(1, 1), C=2)
+    ds = synthetic.generate(small)
+    e = O.e_step(ds, np.ones((2, 64)), 0, cap=200)
+    ex = O.e_step(ds, np.ones((2, 64)), 0, mode="exact")
+    np.testing.assert_allclose(e["mu"], ex["mu"], rtol=1e-5, atol=1e-8)
