@@ -401,6 +401,21 @@ __device__ __forceinline__ float tf32_rna(float x) {
 // columns [0, 32), lo in [32, 64).  The swizzle permutes 16-byte chunks within a row only: logical
 // chunk c of row r sits at position c ^ (r & 7), so the 32 lanes of a warp (32 consecutive rows)
 // spread each read over all 32 banks.
+__device__ __forceinline__ void split_row_tmem32(uint32_t a32, uint32_t ta, int r) {
+  // the same with one 32-column store per plane (fewer, larger TMEM writes)
+  const uint32_t row = a32 + (uint32_t)(r >> 3) * 1024 + (uint32_t)(r & 7) * 128;
+  float hi[32], lo[32];
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    const float4 v = lds128(row + (uint32_t)((c ^ r) & 7) * 16);
+    hi[4 * c + 0] = tf32_rna(v.x); lo[4 * c + 0] = v.x - hi[4 * c + 0];
+    hi[4 * c + 1] = tf32_rna(v.y); lo[4 * c + 1] = v.y - hi[4 * c + 1];
+    hi[4 * c + 2] = tf32_rna(v.z); lo[4 * c + 2] = v.z - hi[4 * c + 2];
+    hi[4 * c + 3] = tf32_rna(v.w); lo[4 * c + 3] = v.w - hi[4 * c + 3];
+  }
+  tmem_st32(ta, hi);
+  tmem_st32(ta + 32, lo);
+}
 __device__ __forceinline__ void split_row_tmem(uint32_t a32, uint32_t ta, int r) {
   const uint32_t row = a32 + (uint32_t)(r >> 3) * 1024 + (uint32_t)(r & 7) * 128;
 #pragma unroll
@@ -1013,7 +1028,28 @@ __device__ void a_unit(const KParams &p, unsigned char *sm, PSmemTail &tl, RingC
       rc.nexta();
       if (tr && kc < 16) tr[64 + kc] = clock64();
       fence_after_sync();
-      if (!(p.dbg_flags & 4)) split_row_tmem(base, ta_lane + (uint32_t)(64 * sa), 32 * aq + lane);
+      if (p.dbg_flags & (131072 | 262144)) {
+        // diagnostics (timing only): 131072 split constants into TMEM (no smem reads), 262144 read and
+        // split the tile but do not store it to TMEM (a value sink keeps the work)
+        if (p.dbg_flags & 131072) {
+          float z[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) z[i] = (float)i;
+          const uint32_t ta = ta_lane + (uint32_t)(64 * sa);
+          tmem_st16(ta, z); tmem_st16(ta + 16, z); tmem_st16(ta + 32, z); tmem_st16(ta + 48, z);
+        } else {
+          const uint32_t row = base + (uint32_t)((32 * aq + lane) >> 3) * 1024 + (uint32_t)((32 * aq + lane) & 7) * 128;
+          float acc = 0.f;
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            const float4 v = lds128(row + (uint32_t)((c ^ lane) & 7) * 16);
+            acc += (v.x - tf32_rna(v.x)) + (v.y - tf32_rna(v.y)) + (v.z - tf32_rna(v.z)) + (v.w - tf32_rna(v.w));
+          }
+          if (acc == 1.2345e-30f) p.b.status[7] = 1;
+        }
+      } else if (p.dbg_flags & 524288) {
+        split_row_tmem32(base, ta_lane + (uint32_t)(64 * sa), 32 * aq + lane);
+      } else if (!(p.dbg_flags & 4)) split_row_tmem(base, ta_lane + (uint32_t)(64 * sa), 32 * aq + lane);
       tmem_wait_st();
       fence_before_sync();
       __syncwarp();

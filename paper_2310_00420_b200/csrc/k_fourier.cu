@@ -101,22 +101,25 @@ __device__ void ifft_dit(C2<R> *buf, const C2<R> *tw, int D, int logD) {
 
 __device__ __forceinline__ int brev(int k, int logD) { return (int)(__brev((unsigned)k) >> (32 - logD)); }
 
-// Shared memory: buf C2<R>[D] | tw C2<R>[D/2] | msym_br float[D] | red double[FT/32] | misc
+// Shared memory: buf C2<R>[D] | tw C2<R>[D/2] | msym2 uint8[D] | red double[FT/32] | misc
+// (fp32 at D = 8192: 104 KB — two CTAs per SM)
 template <class R>
 __host__ __device__ constexpr size_t fourier_smem(int D) {
-  return (size_t)D * sizeof(C2<R>) + (size_t)(D / 2) * sizeof(C2<R>) + (size_t)D * sizeof(float) +
-         (FT / 32) * sizeof(double) + 64;
+  return (size_t)D * sizeof(C2<R>) + (size_t)(D / 2) * sizeof(C2<R>) + (size_t)D + (FT / 32) * sizeof(double) + 64;
 }
 
-// m_sym of task t in bit-reversed order: each sampled row k adds ½ at k and at −k mod D
-__device__ void build_mask(const int *rows, int N, int D, int logD, float *msym_br) {
-  for (int i = threadIdx.x; i < D; i += FT) msym_br[i] = 0.f;
+// 2·m_sym of task t in bit-reversed order (0, 1 or 2): each sampled row k counts at k and at −k mod D.
+// The counts are formed in `scratch` (D ints: the FFT buffer, free between columns).
+__device__ void build_mask(const int *rows, int N, int D, int logD, int *scratch, unsigned char *msym2) {
+  for (int i = threadIdx.x; i < D; i += FT) scratch[i] = 0;
   __syncthreads();
   for (int i = threadIdx.x; i < N; i += FT) {
     const int k = rows[i];
-    atomicAdd(msym_br + brev(k, logD), 0.5f);
-    atomicAdd(msym_br + brev((D - k) & (D - 1), logD), 0.5f);
+    atomicAdd(scratch + brev(k, logD), 1);
+    atomicAdd(scratch + brev((D - k) & (D - 1), logD), 1);
   }
+  __syncthreads();
+  for (int i = threadIdx.x; i < D; i += FT) msym2[i] = (unsigned char)scratch[i];
   __syncthreads();
 }
 
@@ -125,14 +128,14 @@ __device__ void build_mask(const int *rows, int N, int D, int logD, float *msym_
 // (j = tid + FT·e), which only it reads back after the inverse pass, so no barrier is needed between
 // the caller's reads of one application and the writes of the next.
 template <class R, int E>
-__device__ __forceinline__ void apply_normal(const R (&dv)[E], C2<R> *buf, const C2<R> *tw, const float *msym_br,
-                                             int D, int logD) {
+__device__ __forceinline__ void apply_normal(const R (&dv)[E], C2<R> *buf, const C2<R> *tw,
+                                             const unsigned char *msym2, int D, int logD) {
 #pragma unroll
   for (int e = 0; e < E; ++e) buf[threadIdx.x + FT * e] = {dv[e], (R)0};
   __syncthreads();
   fft_dif<R>(buf, tw, D, logD);
   for (int q = threadIdx.x; q < D; q += FT) {
-    const R m = (R)msym_br[q];
+    const R m = (R)0.5 * (R)msym2[q];
     buf[q] = {buf[q].x * m, buf[q].y * m};
   }
   __syncthreads();
@@ -182,8 +185,8 @@ __global__ void __launch_bounds__(FT, 1) k_cg_fourier(KParams p) {
   const int D = d.D, N = d.N, logD = __ffs(D) - 1;
   C2<R> *buf = reinterpret_cast<C2<R> *>(fsm);
   C2<R> *tw = buf + D;
-  float *msym_br = reinterpret_cast<float *>(tw + D / 2);
-  double *red = reinterpret_cast<double *>(msym_br + D);
+  unsigned char *msym2 = reinterpret_cast<unsigned char *>(tw + D / 2);
+  double *red = reinterpret_cast<double *>(msym2 + D);
   for (int k = threadIdx.x; k < D / 2; k += FT) {
     double s, c;
     sincospi(-2.0 * k / D, &s, &c);
@@ -197,7 +200,7 @@ __global__ void __launch_bounds__(FT, 1) k_cg_fourier(KParams p) {
     const int t = g / per_task, j = g % per_task;
     const int c = MEAN ? j : j / d.K, k = MEAN ? 0 : j % d.K;
     if (t != mask_t) {
-      build_mask(p.rows + (size_t)t * N, N, D, logD, msym_br);
+      build_mask(p.rows + (size_t)t * N, N, D, logD, reinterpret_cast<int *>(buf), msym2);
       mask_t = t;
     }
     R x[E], r[E], dv[E];
@@ -229,7 +232,7 @@ __global__ void __launch_bounds__(FT, 1) k_cg_fourier(KParams p) {
     const double tol = MEAN ? p.tol_mean : p.tol;
     int steps = 0, flag = rr > 0.0 ? 1 : 0;   // zero right-hand side: x = 0 in 0 steps (A8)
     for (int u = 0; u < d.cap && flag == 1; ++u) {
-      apply_normal<R, E>(dv, buf, tw, msym_br, D, logD);
+      apply_normal<R, E>(dv, buf, tw, msym2, D, logD);
       double dad = 0.0;
 #pragma unroll
       for (int e = 0; e < E; ++e) {
