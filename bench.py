@@ -75,8 +75,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="oracle sample budget")
-    ap.add_argument("--e2e-steps", type=int, default=3,
-                    help="EM iterations of the end-to-end leg (init from host buffers + steps + readback)")
+    ap.add_argument("--e2e-steps", type=int, default=0,
+                    help="EM iterations of the end-to-end leg (init from host buffers + steps + readback); 0 = all K")
     ap.add_argument("--scaling", default="strong", choices=["weak", "strong"],
                     help="N > 1: strong = the config's tasks sharded (default), weak = a config-sized block per rank")
     return ap.parse_args()
@@ -390,8 +390,8 @@ def cuda_arm(args):
     # the user's call sequence from pinned host memory: upload Φ, y; cmtcs_init (b = βΦᵀy, Φᵀ,
     # TMA maps) at the timed iterations' entry state; E EM iterations; posterior read back to host
     e2e = None
-    if not args.no_e2e and args.e2e_steps > 0:
-        ne = min(args.e2e_steps, args.steps)
+    if not args.no_e2e:
+        ne = min(args.e2e_steps, args.steps) if args.e2e_steps > 0 else args.steps
         h2d = phi_h.numel() * phi_h.element_size() + y_h.numel() * 4 + cfg.C * cfg.D * 8
         d2h = ((e - b) * cfg.C + cfg.C * cfg.D + (e - b) * cfg.D + (e - b)) * 8
         barrier()

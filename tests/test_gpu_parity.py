@@ -451,3 +451,24 @@ def test_task_shards_match_whole(torch_cuda):
     CD = cfg.C * cfg.D
     a_fin = O.m_step_finish(tot[CD:CD + cfg.C], tot[:CD].reshape(cfg.C, cfg.D), alpha)
     np.testing.assert_allclose(a_fin, alpha_w, rtol=1e-13)
+
+
+def test_cta_pair_mode_parity(torch_cuda, monkeypatch):
+    """The CTA-pair operator (2-CTA clusters issuing cta_group::2 MMAs, each CTA staging half of the
+    B columns; off by default) forced on a ragged multi-tile shape and on config 1:
+    the same bars as the single-CTA path."""
+    monkeypatch.setenv("CMTCS_PAIR", "2")
+    cfg = synthetic.CONFIGS[1]
+    data = synthetic.generate(cfg)
+    alpha = oracle_state(data, 6, mode="cofem")
+    post, info, orc, a_next, conv = _single_step(data, alpha, 6, cap=4 * cfg.cg_cap)
+    e = compare_step(post, info, orc, a_next, conv)
+    print("pair C1", e)
+    assert e["mu"] <= MU_TOL and conv.all() and e["s_conv"] <= S_TOL and e["q_abs"] <= Q_TOL and e["L_abs"] <= L_TOL
+    data = synthetic.small_problem(T=5, C=3, N=300, D=260, K=5, sigma=0.05, seed=27, support=6)
+    alpha = np.random.default_rng(8).uniform(0.3, 4.0, (3, 260))
+    post, info, orc, a_next, conv = _single_step(data, alpha, 1, cap=600, tol=1e-7)
+    e = compare_step(post, info, orc, a_next, conv)
+    print("pair ragged", e)
+    assert e["mu"] <= MU_TOL and conv.all() and e["s_conv"] <= S_TOL and e["q_abs"] <= Q_TOL and e["L_abs"] <= L_TOL
+    assert np.all(np.abs(post["logdet"] - orc["nu"]) <= nu_tol(orc["nu"]))

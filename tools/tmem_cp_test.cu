@@ -129,16 +129,22 @@ __global__ void __launch_bounds__(384, 1) k_rate(int mode, int chunks, unsigned 
     const long long c1 = clock64();
     out[blockIdx.x] = (unsigned long long)(c1 - c0);
     stop = 1;
-  } else if (w >= 8 && mode == 1) {
-    const uint32_t lane_base = tm + ((uint32_t)((w & 3) * 32) << 16) + 256;
+  } else if (w >= 8 && (mode == 1 || mode >= 3)) {
+    // mode 1: stores to columns 256..319 (away from the A operand); mode 3: to the OTHER A stage
+    // (384 + 64·((c+1)&1) — what the kernel's A warps do); mode 4: into the A stage being read
+    const uint32_t col = mode == 1 ? 256u : 384u;
+    const uint32_t lane_base = tm + ((uint32_t)((w & 3) * 32) << 16) + col;
     float x = 0.f;
+    int it = 0;
     while (!stop) {
-      st16(lane_base, x);
-      st16(lane_base + 16, x);
-      st16(lane_base + 32, x);
-      st16(lane_base + 48, x);
+      const uint32_t off = mode == 1 ? 0u : (mode == 3 ? 64u * (uint32_t)((it + 1) & 1) : 64u * (uint32_t)(it & 1));
+      st16(lane_base + off, x);
+      st16(lane_base + off + 16, x);
+      st16(lane_base + off + 32, x);
+      st16(lane_base + off + 48, x);
       asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
       x += 1.f;
+      ++it;
     }
   }
   fence_before_sync();
@@ -178,9 +184,10 @@ int main() {
   unsigned long long *out, h[148];
   cudaMalloc(&out, 148 * 8);
   cudaFuncSetAttribute(k_rate, cudaFuncAttributeMaxDynamicSharedMemorySize, 98304 + 1024);
-  const char *names[3] = {"MMAs only", "+ tcgen05.st stream (4 warps)", "+ 8 tcgen05.cp per chunk"};
+  const char *names[5] = {"MMAs only", "+ tcgen05.st stream (4 warps)", "+ 8 tcgen05.cp per chunk",
+                          "+ st stream into the other A stage", "+ st stream over both A stages"};
   const int chunks = 2000;
-  for (int mode = 0; mode < 3; ++mode) {
+  for (int mode = 0; mode < 5; ++mode) {
     for (int rep = 0; rep < 2; ++rep) {
       k_rate<<<148, 384, 98304 + 1024>>>(mode, chunks, out);
       cudaDeviceSynchronize();
