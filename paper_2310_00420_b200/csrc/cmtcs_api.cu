@@ -275,6 +275,7 @@ size_t carve(const Dims &d, char *base, Bufs *b) {
   b->Upart = cv.take<float>(dn && d.S1 > 1 ? Tl * d.S1 * d.Pp * N : 1);
   b->Umpart = cv.take<double>(dn && d.S1 > 1 ? Tl * d.S1 * N * d.Cp : 1);
   b->resm = cv.take<double>(Tl * C);
+  b->ftw = cv.take<double>(d.op == CMTCS_OP_DENSE ? 1 : 2 * D);
   b->tmark = cv.take<int>(Tl);
   b->tilecnt = cv.take<int>(Tl * d.nCT * d.nRT1);
   b->gridbar = cv.take<unsigned>(1);
@@ -531,6 +532,7 @@ cmtcs_status cmtcs_init(cmtcs_ctx **out, const cmtcs_problem *p, const float *ph
   c->kp.b = b;
   c->kp.tc = make_tc(d);
   c->kp.tc.pf = getenv("CMTCS_PF") ? atoi(getenv("CMTCS_PF")) : 0;
+  c->kp.tc.l2hint = getenv("CMTCS_L2HINT") ? atoi(getenv("CMTCS_L2HINT")) : 0;
   c->kp.phi = phi;
   c->kp.y = y;
   c->kp.beta = p->beta;

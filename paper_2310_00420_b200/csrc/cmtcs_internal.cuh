@@ -87,6 +87,7 @@ struct Bufs {
   int *dep;          // [2][Tl] per-task completion counters of stage 1 / stage 2 units (monotonic)
   int *assign;       // [Tl]
   double *resm;      // [Tl][C]  ‖y_t − Φ_t μ_tc‖² (partial-Fourier path; the dense path uses Um)
+  double *ftw;       // [2·D]    partial Fourier: per-stage twiddles tw2[h + pos] = exp(−2πi pos/2h), fp64 pairs
 };
 
 // tensor-core operator configuration (chosen at init from P)
@@ -100,6 +101,7 @@ struct TcCfg {
   int stages;        // smem pipeline depth
   unsigned stage_bytes;
   int pf;            // L2 prefetch distance of the A tiles (chunks ahead of the one being loaded; 0 = off)
+  int l2hint;        // TMA L2 cache hints: A tiles evict-first, B tiles evict-last (CMTCS_L2HINT)
   int pair;          // CTA pairs: 2-CTA clusters issuing cta_group::2 MMAs (M = 256 rows: a row-tile
                      // pair), each CTA staging half of the tile's B columns
   int use_dtile;     // stage-2 epilogue reads its d tile (NT × 128 fp32) from smem, staged by TMA

@@ -846,7 +846,16 @@ __device__ __forceinline__ void produce(const KParams &p, const TcMaps &mp, unsi
       if (rank == 0) mbar_arrive_expect_tx_warp(&tl.bfull[st], 2 * b_bytes);
       tma_load_4d_warp_pair(base + A_BYTES, bmap, k, x.brow + (int)rank * (p.tc.NT / 2), x.t, 0, bl);
     }
-    if (x.stage == 1) {
+    if (p.tc.l2hint) {
+      // A streams (evict first); B and the mean chunk are re-read by the task's other row tiles
+      const uint64_t pa = l2_policy_evict_first(), pb = l2_policy_evict_last();
+      tma_load_3d_warp_hint(base, x.stage == 1 ? &mp.phi : &mp.phit, k, x.arow, at, fb, pa);
+      if (x.nmma && !PR) tma_load_4d_warp_hint(base + A_BYTES, bmap, k, x.brow, x.t, 0, fb, pb);
+      if (x.mean) {
+        if (x.stage == 1) tma_load_3d_warp_hint(base + A_BYTES + b_stage, &mp.dm, k, 0, x.t, fb, pb);
+        else tma_load_3d_warp_hint(base + A_BYTES + b_stage, &mp.um, 0, k, x.t, fb, pb);
+      }
+    } else if (x.stage == 1) {
       tma_load_3d_warp(base, &mp.phi, k, x.arow, at, fb);
       if (x.nmma && !PR) tma_load_4d_warp(base + A_BYTES, bmap, k, x.brow, x.t, 0, fb);   // hi | lo tiles
       if (x.mean) tma_load_3d_warp(base + A_BYTES + b_stage, &mp.dm, k, 0, x.t, fb);

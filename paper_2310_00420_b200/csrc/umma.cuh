@@ -228,6 +228,36 @@ __device__ __forceinline__ void tma_load_3d_warp(void *smem, const CUtensorMap *
       "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(mbar))
       : "memory");
 }
+// L2 cache policies for TMA loads: the A operand (Φ / Φᵀ tiles) streams through once per stage
+// (evict first), the B operand (directions / U, re-read by every row tile of a task) stays (evict last)
+__device__ __forceinline__ uint64_t l2_policy_evict_first() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ uint64_t l2_policy_evict_last() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ void tma_load_3d_warp_hint(void *smem, const CUtensorMap *map, int x, int y, int z,
+                                                      uint64_t *mbar, uint64_t pol) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%2, %3, %4}], [%5], %6;\n\t}\n" ::"r"(
+          smem_u32(smem)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(mbar)), "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_4d_warp_hint(void *smem, const CUtensorMap *map, int x, int y, int z, int w,
+                                                      uint64_t *mbar, uint64_t pol) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%2, %3, %4, %5}], [%6], %7;\n\t}\n" ::"r"(
+          smem_u32(smem)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(w), "r"(smem_u32(mbar)), "l"(pol)
+      : "memory");
+}
 // 4-D box (the hi | lo planes of a per-task operand: dims {cols, rows, task, plane})
 __device__ __forceinline__ void tma_load_4d_warp(void *smem, const CUtensorMap *map, int x, int y, int z, int w,
                                                  uint64_t *mbar) {

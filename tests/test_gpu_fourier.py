@@ -37,10 +37,13 @@ def small_fourier(T=3, C=2, D=512, N=128, K=6, sigma=0.05, seed=41, support=20):
     return synthetic.generate(cfg)
 
 
-def test_fourier_rhs_and_operator_through_one_step(torch_cuda):
+@pytest.mark.parametrize("C,K,D", [(2, 6, 512), (3, 5, 1024)])
+def test_fourier_rhs_and_operator_through_one_step(torch_cuda, C, K, D):
     """A single EM step on a small partial-Fourier problem from an asymmetric state: μ, s, ν̄, q, L
-    and α against the oracle (dense DFT Φ), every block converged on both sides."""
-    data = small_fourier()
+    and α against the oracle (dense DFT Φ), every block converged on both sides.  (3, 5): an odd
+    number of probe columns per task — the paired-column kernel's last pair has one column — and
+    an even log₂D (the FFT's radix-4 passes without the closing radix-2 stage)."""
+    data = small_fourier(C=C, K=K, T=3, D=D, N=D // 4)
     cfg = data["cfg"]
     alpha = np.random.default_rng(3).uniform(0.5, 5.0, (cfg.C, cfg.D))
     g = make_gpu(data, alpha=alpha, em_iter0=2, cap=cfg.cg_cap, tol=1e-7, mean_tol=MEAN_TOL)

@@ -17,7 +17,7 @@ KEYS = {
     "grid_size": "launch__grid_size",
     "registers": "launch__registers_per_thread",
 }
-SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1, "usecond": 1e3, "msecond": 1e6,
+SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12, "nsecond": 1, "usecond": 1e3, "msecond": 1e6, "second": 1e9,
          "ns": 1, "us": 1e3, "ms": 1e6}
 
 

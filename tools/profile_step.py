@@ -15,7 +15,7 @@ import synthetic  # noqa: E402
 from paper_2310_00420_b200 import CoFEM  # noqa: E402
 
 ap = argparse.ArgumentParser()
-ap.add_argument("--config", type=int, default=2)
+ap.add_argument("--config", type=int, default=2, help="1-6 (6: partial Fourier)")
 ap.add_argument("--warmup", type=int, default=3)
 ap.add_argument("--tasks", type=int, default=0, help="use only the first n tasks (0 = all)")
 ap.add_argument("--steps", type=int, default=1)
@@ -23,9 +23,14 @@ a = ap.parse_args()
 cfg = synthetic.CONFIGS[a.config]
 tasks = range(a.tasks) if a.tasks else None
 data = synthetic.generate(cfg, tasks)
-m = CoFEM(torch.from_numpy(data["phi"]).cuda(), torch.from_numpy(data["y"]).cuda(), T=cfg.T, C=cfg.C, K=cfg.K,
-          beta=cfg.beta, cg_max_iters=cfg.cg_cap, cg_rel_tol=cfg.cg_tol, probe_seed=cfg.probe_seed,
-          shared_phi=cfg.shared_phi)
+if cfg.operator == "fourier":   # config 6: Φ_t = Ω_t F given by its sampled rows
+    m = CoFEM(None, torch.from_numpy(data["y"]).cuda(), fourier_rows=torch.from_numpy(data["rows"]).cuda(), D=cfg.D,
+              T=cfg.T, C=cfg.C, K=cfg.K, beta=cfg.beta, cg_max_iters=cfg.cg_cap, cg_rel_tol=cfg.cg_tol,
+              probe_seed=cfg.probe_seed)
+else:
+    m = CoFEM(torch.from_numpy(data["phi"]).cuda(), torch.from_numpy(data["y"]).cuda(), T=cfg.T, C=cfg.C, K=cfg.K,
+              beta=cfg.beta, cg_max_iters=cfg.cg_cap, cg_rel_tol=cfg.cg_tol, probe_seed=cfg.probe_seed,
+              shared_phi=cfg.shared_phi)
 for _ in range(a.warmup):
     m.em_step(1)
 m.set_timing(True)
