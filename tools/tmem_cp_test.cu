@@ -100,7 +100,12 @@ __global__ void __launch_bounds__(384, 1) k_rate(int mode, int chunks, unsigned 
   __syncthreads();
   fence_after_sync();
   const uint32_t tm = slot;
-  if (t == 0) {
+  if (t == 0 && mode == 5) {   // store stream alone: thread 0 just waits ~chunks*768 cycles
+    const long long c0 = clock64();
+    while (clock64() - c0 < (long long)chunks * 768) {}
+    out[blockIdx.x] = (unsigned long long)(clock64() - c0);
+    stop = 1;
+  } else if (t == 0) {
     const uint32_t idesc = idesc_tf32(128, NB);
     // B hi | lo at sm + 32 KB (2 × 16 KB), A hi | lo tiles at sm (2 × 16 KB) for the copies
     const uint64_t bh = desc_sw128(smem_u32(sm + 32768)), bl = desc_sw128(smem_u32(sm + 49152));
@@ -130,12 +135,14 @@ __global__ void __launch_bounds__(384, 1) k_rate(int mode, int chunks, unsigned 
     out[blockIdx.x] = (unsigned long long)(c1 - c0);
     stop = 1;
   } else if (w >= 8 && (mode == 1 || mode >= 3)) {
+    // (mode 5: the stream of mode 3 with no MMAs running)
     // mode 1: stores to columns 256..319 (away from the A operand); mode 3: to the OTHER A stage
     // (384 + 64·((c+1)&1) — what the kernel's A warps do); mode 4: into the A stage being read
-    const uint32_t col = mode == 1 ? 256u : 384u;
+    const uint32_t col = mode == 1 ? 256u : 384u;   // modes 3, 4, 5: the A stages
     const uint32_t lane_base = tm + ((uint32_t)((w & 3) * 32) << 16) + col;
     float x = 0.f;
     int it = 0;
+    const long long s0 = clock64();
     while (!stop) {
       const uint32_t off = mode == 1 ? 0u : (mode == 3 ? 64u * (uint32_t)((it + 1) & 1) : 64u * (uint32_t)(it & 1));
       st16(lane_base + off, x);
@@ -146,6 +153,8 @@ __global__ void __launch_bounds__(384, 1) k_rate(int mode, int chunks, unsigned 
       x += 1.f;
       ++it;
     }
+    const long long s1 = clock64();
+    if ((threadIdx.x & 31) == 0 && w == 8) out[148 + blockIdx.x] = (unsigned long long)((s1 - s0) / (it > 0 ? it : 1));
   }
   fence_before_sync();
   __syncthreads();
@@ -181,22 +190,25 @@ int main() {
   printf("check (%s): max |D_st - ref| %.3g, |D_cp - ref| %.3g, |D_st - D_cp| %.3g\n", cudaGetErrorString(e), e_st,
          e_cp, e_ab);
   // part 2
-  unsigned long long *out, h[148];
-  cudaMalloc(&out, 148 * 8);
+  unsigned long long *out, h[296];
+  cudaMalloc(&out, 296 * 8);
   cudaFuncSetAttribute(k_rate, cudaFuncAttributeMaxDynamicSharedMemorySize, 98304 + 1024);
-  const char *names[5] = {"MMAs only", "+ tcgen05.st stream (4 warps)", "+ 8 tcgen05.cp per chunk",
-                          "+ st stream into the other A stage", "+ st stream over both A stages"};
+  const char *names[6] = {"MMAs only", "+ tcgen05.st stream (4 warps)", "+ 8 tcgen05.cp per chunk",
+                          "+ st stream into the other A stage", "+ st stream over both A stages", "st stream alone"};
   const int chunks = 2000;
-  for (int mode = 0; mode < 5; ++mode) {
+  for (int mode = 0; mode < 6; ++mode) {
     for (int rep = 0; rep < 2; ++rep) {
+      cudaMemset(out + 148, 0, 148 * 8);
       k_rate<<<148, 384, 98304 + 1024>>>(mode, chunks, out);
       cudaDeviceSynchronize();
     }
     cudaMemcpy(h, out, sizeof(h), cudaMemcpyDeviceToHost);
     unsigned long long mx = 0;
     for (int i = 0; i < 148; ++i) mx = h[i] > mx ? h[i] : mx;
-    printf("%-30s: %.0f clk per chunk (12 MMAs, N=%d; floor %d)  %s\n", names[mode], (double)mx / chunks, NB,
-           12 * NB / 2, cudaGetErrorString(cudaGetLastError()));
+    unsigned long long smx = 0;
+    for (int i = 148; i < 296; ++i) smx = h[i] > smx ? h[i] : smx;
+    printf("%-36s: %.0f clk per chunk (12 MMAs, N=%d; floor %d); store warp: %llu clk per 32 KB-per-CTA round  %s\n",
+           names[mode], (double)mx / chunks, NB, 12 * NB / 2, smx, cudaGetErrorString(cudaGetLastError()));
   }
   return 0;
 }
