@@ -64,6 +64,18 @@ def tf32x3_peak_tflops(peaks):
     return peaks["bf16_tflops"] * ratio / 3.0, peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"]) * ratio / 3.0
 
 
+# north_star: "Tensor cores (3xTF32 split) are used only ... if the oracle tolerance holds".  Measured
+# (tests/test_gpu_midrun.py): the tensor-core engine meets every bar at C1-C3 and misses
+# |ΔL| ≤ 1e-3 at C4/C5 (truncating accumulation); the FP32 engine meets it there.
+AUTO_ENGINE = {1: "tensor", 2: "tensor", 3: "tensor", 4: "fp32", 5: "fp32"}
+
+
+def resolve_engine(name, cfg):
+    if cfg.operator == "fourier":
+        return "fourier"
+    return AUTO_ENGINE[cfg.cfg_id] if name == "auto" else name
+
+
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -77,6 +89,9 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="oracle sample budget")
     ap.add_argument("--e2e-steps", type=int, default=0,
                     help="EM iterations of the end-to-end leg (init from host buffers + steps + readback); 0 = all K")
+    ap.add_argument("--engine", default="auto", choices=["auto", "tensor", "fp32"],
+                    help="dense operator: tcgen05 3xTF32 tensor cores or FP32 CUDA cores; auto = the north_star's "
+                         "rule (tensor cores only where the oracle tolerance holds: C1-C3; FP32 at C4/C5, DESIGN.md §6)")
     ap.add_argument("--scaling", default="strong", choices=["weak", "strong"],
                     help="N > 1: strong = the config's tasks sharded (default), weak = a config-sized block per rank")
     return ap.parse_args()
@@ -269,6 +284,7 @@ def cuda_arm(args):
     from paper_2310_00420_b200 import CoFEM, cmtcs
 
     cfg = synthetic.CONFIGS[args.config]
+    engine = resolve_engine(args.engine, cfg)
     weak = world > 1 and args.scaling == "weak"
     t_total = cfg.T * world if weak else cfg.T
     if weak:   # rank r: global tasks [r·T, (r+1)·T) carrying the config's T tasks' Φ, y
@@ -299,7 +315,7 @@ def cuda_arm(args):
         return CoFEM(phi_d, y_d, T=t_total, C=cfg.C, K=cfg.K, beta=cfg.beta, cg_max_iters=cfg.cg_cap,
                      cg_rel_tol=cfg.cg_tol, probe_seed=cfg.probe_seed, pi=pi, task_begin=b,
                      shared_phi=cfg.shared_phi, nccl_uid=nccl_uid, rank=rank, world=world, alpha0=alpha0,
-                     em_iter0=em_iter0)
+                     em_iter0=em_iter0, engine=engine)
 
     model = make(phi, y, nccl_uid=uid)
     stream = model.stream
@@ -378,7 +394,8 @@ def cuda_arm(args):
     peak_burst, peak_sust = tf32x3_peak_tflops(peaks)
     long_kernel = kern_ms / max(1, tm["cg_kernel_launches"]) > 1000.0
     peak = peak_sust if long_kernel else peak_burst
-    if fourier:   # FP32 ALU bound (FFMA peak at the measured clock ceiling, B200_PROFILING.md unit counts)
+    alu = fourier or engine == "fp32"
+    if alu:   # FP32 ALU bound (FFMA peak at the measured clock ceiling, B200_PROFILING.md unit counts)
         peak_burst = peak_sust = peak = fp32_peak_tflops(peaks.get("sm_max_mhz", SM_MAX_MHZ))
     # EM-step roofline (north_star): slower of Φ bytes at HBM bandwidth and FLOPs at peak, per CG step
     steps_total = sum(i["cg_iters"] for i in infos)
@@ -438,8 +455,12 @@ def cuda_arm(args):
                    if weak else {}),
                 "parallelism": f"task-sharded dp{world}" if world > 1 else "single GPU",
                 "straggler_spread": (total_ms / fastest_ms) if world > 1 else 1.0,
+                "engine": "partial-Fourier FFT" if fourier else engine,
                 "precision": ("probe columns: fp32 vectors and fp32 FFT, fp64 dots/scalars; mean columns (fp64 FFT), "
                               "log-det, q, M-step fp64") if fourier else
+                             ("probe columns: fp32 vectors, operator on the FP32 CUDA cores (FFMA, round-to-nearest, "
+                              "two-level block sums), fp64 dots/scalars applied in fp64; mean columns, log-det, q, "
+                              "M-step fp64") if engine == "fp32" else
                              ("probe columns: fp32 vectors, operator on tcgen05 tensor cores as 3xTF32 "
                               "(fp32-accurate), fp64 dots/scalars; mean columns, log-det, q, M-step fp64"),
                 "l2": "flushed (zero-fill of 2xL2) between timed EM iterations",
@@ -453,24 +474,35 @@ def cuda_arm(args):
                 "update_share_of_step": tm["update_ms"] / max(rank_ms, 1e-9),
                 "wall_s_timed": wall,
             },
-            "roofline": {"bound": "alu" if fourier else "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+            "roofline": {"bound": "alu" if alu else "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                          "frac": achieved / peak, "traffic": ncu_traffic(cfg.name),
                          "traffic_unit": "DRAM bytes per CG step (ncu --set full of k_cg_persistent / its CG steps)",
                          "kernel": ("k_cg_fourier (partial-Fourier CG: one CTA per column, FFT in shared memory; "
                                     "achieved = 10*D*log2(D) flop per active column per CG step / the kernels' "
                                     "duration)") if fourier else
+                                   ("the FP32 engine's CG loop (k_simt_probe<1>/<2> register-tiled SGEMMs for the "
+                                    "probe columns, k_simt_mean1/2 fp64 mean columns, k_simt_update); achieved = "
+                                    "algorithmic fp32 flop 4*N*D per active column per CG step / the loop's duration "
+                                    "(CUDA events on the launch stream around every E-step's CG loop); "
+                                    "operator_phases_only: the same flops / the operator kernels' event time")
+                                   if engine == "fp32" else
                                    ("k_cg_persistent (the whole CG loop of an E-step: operator on tcgen05 3xTF32 + fp64 "
                                     "mean columns on DMMA + CG update); achieved = algorithmic fp32 flop 4*N*D per "
                                     "active column per CG step / the kernel's duration (CUDA events on the launch "
                                     "stream around every launch in the timed region)"),
-                         "peak_source": (f"{peaks_kind} MEASURED_PEAKS.json bf16 "
+                         "peak_source": ("FFMA peak: 148 SMs x 128 FP32 lanes x 2 flop x sm_max_mhz "
+                                         f"{peaks.get('sm_max_mhz', SM_MAX_MHZ)} (B200_PROFILING.md unit counts)")
+                                        if alu else
+                                        (f"{peaks_kind} MEASURED_PEAKS.json bf16 "
                                          f"{peaks['bf16_tflops_sustained' if long_kernel else 'bf16_tflops']} TF/s "
                                          f"({'sustained: kernel launches last > 1 s' if long_kernel else 'burst'}) "
                                          f"x (1.1/2.25 tf32/bf16 nominal) / 3 passes; burst {peak_burst:.1f}, "
                                          f"sustained {peak_sust:.1f}"),
                          "frac_burst_peak": achieved / peak_burst,
                          "operator_phases_only": {"achieved": achieved_op, "frac": achieved_op / peak,
-                                                  "timing": "device %globaltimer stamps at the phase boundaries"},
+                                                  "timing": "CUDA events around the operator kernels of every CG step"
+                                                  if engine == "fp32" else
+                                                  "device %globaltimer stamps at the phase boundaries"},
                          "fp32_ffma_peak": fp32_peak_tflops(peaks.get("sm_max_mhz", SM_MAX_MHZ))},
             "gpu_launches": int(launches),
             "clocks": clocks,

@@ -77,7 +77,11 @@ typedef struct cmtcs_problem {
                             rows in [0, D) per task (must outlive ctx); NULL otherwise                */
 } cmtcs_problem;
 
-enum { CMTCS_OP_DENSE = 0, CMTCS_OP_PARTIAL_FOURIER = 1 };
+/* CMTCS_OP_DENSE_FP32: the same dense Φ_t as CMTCS_OP_DENSE, the operator on the FP32 CUDA cores
+ * (round-to-nearest FFMA accumulation) instead of the 3xTF32 tensor cores.  The north_star allows
+ * the tensor path "only if the oracle tolerance holds": tcgen05's truncating fp32 accumulation
+ * biases ν̄ and misses |ΔL| ≤ 1e-3 at configs 4-5; this operator meets it. */
+enum { CMTCS_OP_DENSE = 0, CMTCS_OP_PARTIAL_FOURIER = 1, CMTCS_OP_DENSE_FP32 = 2 };
 
 /* Statistics of the last EM iteration run by cmtcs_em_step (host struct, filled on return). */
 typedef struct cmtcs_step_info {

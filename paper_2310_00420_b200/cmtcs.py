@@ -37,7 +37,7 @@ class cmtcs_problem(ctypes.Structure):
                 ("mean_rel_tol", c_double), ("op_kind", c_int32), ("fourier_rows", c_void_p)]
 
 
-CMTCS_OP_DENSE, CMTCS_OP_PARTIAL_FOURIER = 0, 1
+CMTCS_OP_DENSE, CMTCS_OP_PARTIAL_FOURIER, CMTCS_OP_DENSE_FP32 = 0, 1, 2
 
 
 class cmtcs_step_info(ctypes.Structure):

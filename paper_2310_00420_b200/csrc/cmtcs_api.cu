@@ -40,6 +40,8 @@ struct cmtcs_ctx {
   TcMaps maps;
   int grid;
   int *h_u;                 // pinned: CG steps executed
+  SimtTiming simt_tm;       // the FP32 engine's per-step events (created with the context)
+  bool have_simt_tm;
 };
 
 namespace {
@@ -148,7 +150,10 @@ bool make_dims(const cmtcs_problem *p, Dims *d, char *why) {
     s += p->pi[c];
   }
   if (fabs(s - 1.0) > 1e-9) { snprintf(why, 256, "pi sums to %.17g, not 1", s); return false; }
-  if (p->op_kind != CMTCS_OP_DENSE && p->op_kind != CMTCS_OP_PARTIAL_FOURIER) { snprintf(why, 256, "unknown op_kind %d", p->op_kind); return false; }
+  if (p->op_kind != CMTCS_OP_DENSE && p->op_kind != CMTCS_OP_PARTIAL_FOURIER && p->op_kind != CMTCS_OP_DENSE_FP32) {
+    snprintf(why, 256, "unknown op_kind %d", p->op_kind);
+    return false;
+  }
   if (p->op_kind == CMTCS_OP_PARTIAL_FOURIER) {
     if (p->shared_phi) { snprintf(why, 256, "the partial-Fourier operator has a mask per task: shared_phi must be 0"); return false; }
     if (!p->fourier_rows) { snprintf(why, 256, "the partial-Fourier operator needs fourier_rows"); return false; }
@@ -173,7 +178,7 @@ bool make_dims(const cmtcs_problem *p, Dims *d, char *why) {
     // the 74 pairs of a B200 twice over: half of B per CTA, M = 256 MMAs.  CMTCS_PAIR=0 disables,
     // =2 forces them (tests: every shape through the pair path)
     const char *e = getenv("CMTCS_PAIR");
-    const int mode = e ? atoi(e) : 0;   // off by default: slower at C4 so far
+    const int mode = p->op_kind != CMTCS_OP_DENSE ? 0 : e ? atoi(e) : 0;   // off by default: slower at C4 so far
     const int NT1 = std::min(nt_max(p->shared_phi), (d->P + 15) / 16 * 16);
     const long pair_units = (long)((d->P + NT1 - 1) / NT1) * ((d->nRT1 + 1) / 2) * (p->task_end - p->task_begin);
     d->pair = mode == 2 || (mode == 1 && pair_units >= 148);
@@ -212,7 +217,7 @@ bool make_dims(const cmtcs_problem *p, Dims *d, char *why) {
   d->shared_phi = p->shared_phi ? 1 : 0;
   d->phi_task_stride = p->shared_phi ? 0 : (int64_t)p->N * p->D;
   d->op = p->op_kind;
-  if (d->op != CMTCS_OP_DENSE) d->pair = 0;
+  if (d->op != CMTCS_OP_DENSE) d->pair = 0;   // the tensor-core operator only
   return true;
 }
 
@@ -226,21 +231,23 @@ size_t carve(const Dims &d, char *base, Bufs *b) {
   b->b64 = cv.take<double>(Tl * D);
   b->bnorm2 = cv.take<double>(Tl);
   const size_t mats = d.shared_phi ? 1 : Tl;
-  // dn = 0: the partial-Fourier operator keeps its CG vectors on chip (k_fourier.cu) — only x leaves
-  const size_t dn = d.op == CMTCS_OP_DENSE ? 1 : 0;
-  b->PT = cv.take<float>(dn * mats * N * D);
+  // dn = 0: the partial-Fourier operator keeps its CG vectors on chip (k_fourier.cu) — only x leaves;
+  // tc = 0: the FP32 engine (k_simt.cu) has no Φᵀ copy, no tf32 pairs and no split-K partials
+  const size_t dn = d.op == CMTCS_OP_PARTIAL_FOURIER ? 0 : 1;
+  const size_t tc = d.op == CMTCS_OP_DENSE ? 1 : 0;
+  b->PT = cv.take<float>(tc * mats * N * D);
   b->X = cv.take<float>(Tl * P * D);
   b->R = cv.take<float>(dn * Tl * P * D);
   b->D32 = cv.take<float>(dn * Tl * P * D);
-  b->Dh = cv.take<float>(dn * Tl * P * D);
-  b->Dl = cv.take<float>(dn * Tl * P * D);
+  b->Dh = cv.take<float>(tc * Tl * P * D);
+  b->Dl = cv.take<float>(tc * Tl * P * D);
   b->W = cv.take<float>(dn * Tl * P * D);
   b->Xm = cv.take<double>(Tl * C * D);
   b->Rm = cv.take<double>(dn * Tl * C * D);
   b->Dm = cv.take<double>(dn * Tl * C * D);
   b->Wm = cv.take<double>(dn * Tl * C * D);
   b->Uh = cv.take<float>(dn * Tl * d.Pp * N);
-  b->Ul = cv.take<float>(dn * Tl * d.Pp * N);
+  b->Ul = cv.take<float>(tc * Tl * d.Pp * N);
   b->Um = cv.take<double>(dn * Tl * N * d.Cp);
   b->rr = cv.take<double>(Tl * P);
   b->rrm = cv.take<double>(Tl * C);
@@ -272,14 +279,15 @@ size_t carve(const Dims &d, char *base, Bufs *b) {
   b->ts = cv.take<unsigned long long>((size_t)cap * 4 + 512);   // + 2 × 256 diagnostic stamps
   b->stats = cv.take<double>(16);
   b->assign = cv.take<int>(Tl);
-  b->Upart = cv.take<float>(dn && d.S1 > 1 ? Tl * d.S1 * d.Pp * N : 1);
-  b->Umpart = cv.take<double>(dn && d.S1 > 1 ? Tl * d.S1 * N * d.Cp : 1);
+  b->Upart = cv.take<float>(tc && d.S1 > 1 ? Tl * d.S1 * d.Pp * N : 1);
+  b->Umpart = cv.take<double>(tc && d.S1 > 1 ? Tl * d.S1 * N * d.Cp : 1);
   b->resm = cv.take<double>(Tl * C);
-  b->ftw = cv.take<double>(d.op == CMTCS_OP_DENSE ? 1 : 2 * D);
+  b->ftw = cv.take<double>(d.op == CMTCS_OP_PARTIAL_FOURIER ? 2 * D : 1);
   b->tmark = cv.take<int>(Tl);
   b->tilecnt = cv.take<int>(Tl * d.nCT * d.nRT1);
   b->gridbar = cv.take<unsigned>(1);
   b->dep = cv.take<int>(2 * Tl);
+  if (!tc) b->PT = b->Dh = b->Dl = b->Ul = nullptr;   // not carved: kernels must not touch them
   return cv.off;
 }
 
@@ -350,6 +358,9 @@ cmtcs_status one_em_iteration(cmtcs_ctx *c, const uint64_t *probe_bits, const do
   // ---- batched CG (Alg. 1) over all T_loc·C·(K+1) columns: one persistent kernel ----
   if (fourier) {
     CUDA_OK(c, launch_fourier_cg(kp, c->grid, s));   // probe columns (fp32), then mean columns (fp64)
+  } else if (d.op == CMTCS_OP_DENSE_FP32) {
+    c->simt_tm.op_ms = c->simt_tm.upd_ms = 0.0;
+    CUDA_OK(c, run_simt_cg(kp, c->h_u, &L, tm ? &c->simt_tm : nullptr, s));   // L counts the per-step kernels
   } else {
     CUDA_OK(c, launch_cg_persistent(kp, c->maps, c->grid, s));
   }
@@ -390,12 +401,17 @@ cmtcs_status one_em_iteration(cmtcs_ctx *c, const uint64_t *probe_bits, const do
   c->launches += L;
   c->have_estep = true;
   const int steps_run = *c->h_u;
-  L += fourier ? 2 : 1;         // the persistent CG kernel (partial Fourier: probe and mean kernels)
-  c->launches += fourier ? 2 : 1;
+  const int cg_k = fourier ? 2 : d.op == CMTCS_OP_DENSE ? 1 : 0;   // the persistent CG kernel (partial
+  L += cg_k;                                                          // Fourier: probe and mean kernels)
+  c->launches += cg_k;
   if (tm) {
     // per CG step: %globaltimer stamps taken by CTA 0 after the grid barriers: step start,
     // operator (phases 1-2) done, update (phase 3) done (device clock, ns)
-    for (int u = 0; u < steps_run; ++u) {
+    if (d.op == CMTCS_OP_DENSE_FP32) {   // CUDA events around the operator and update kernels
+      c->t_ms[0] += c->simt_tm.op_ms;
+      c->t_ms[1] += c->simt_tm.upd_ms;
+    }
+    for (int u = 0; u < steps_run && d.op != CMTCS_OP_DENSE_FP32; ++u) {
       const unsigned long long *q = c->h_ts + 4 * u;
       const unsigned long long t0 = q[0], t1 = q[1], t2 = q[2];
       if (t0 && t1 >= t0) c->t_ms[0] += (t1 - t0) * 1e-6;
@@ -551,6 +567,10 @@ cmtcs_status cmtcs_init(cmtcs_ctx **out, const cmtcs_problem *p, const float *ph
   CUDA_OK(c, cudaMallocHost((void **)&c->h_u, sizeof(int)));
   CUDA_OK(c, cudaMallocHost((void **)&c->h_ts, sizeof(unsigned long long) * (4 * d.cap + 512)));
   for (int i = 0; i < 3; ++i) CUDA_OK(c, cudaEventCreate(&c->tev[i]));
+  if (p->op_kind == CMTCS_OP_DENSE_FP32) {
+    for (int i = 0; i < 3 * SimtTiming::B; ++i) CUDA_OK(c, cudaEventCreate(&c->simt_tm.ev[i]));
+    c->have_simt_tm = true;
+  }
   CUDA_OK(c, cudaMemsetAsync(b.status, 0, 8 * sizeof(int), c->stream));
   CUDA_OK(c, cudaMemsetAsync(b.gam, 0, sizeof(double) * d.Tl * d.P * d.cap, c->stream));
   CUDA_OK(c, cudaMemsetAsync(b.xi, 0, sizeof(double) * d.Tl * d.P * d.cap, c->stream));
@@ -560,17 +580,19 @@ cmtcs_status cmtcs_init(cmtcs_ctx **out, const cmtcs_problem *p, const float *ph
     CUDA_OK(c, cudaGetDevice(&dev));
     CUDA_OK(c, cudaDeviceGetAttribute(&c->grid, cudaDevAttrMultiProcessorCount, dev));
   } else {
-  CUDA_OK(c, cudaMemsetAsync(b.Um, 0, sizeof(double) * (size_t)d.Tl * d.N * d.Cp, c->stream));
-  // U's padding rows P..Pp−1 of each task are B-tile rows past the tile's columns: keep them finite
-  CUDA_OK(c, cudaMemsetAsync(b.Uh, 0, sizeof(float) * (size_t)d.Tl * d.Pp * d.N, c->stream));
-  CUDA_OK(c, cudaMemsetAsync(b.Ul, 0, sizeof(float) * (size_t)d.Tl * d.Pp * d.N, c->stream));
-  CUDA_OK(c, cudaMemsetAsync(b.tilecnt, 0, sizeof(int) * d.Tl * d.nCT * d.nRT1, c->stream));
-  c->grid = cg_grid_size(c->kp);
-  if (c->grid < 1) return fail(c, CMTCS_ECUDA, "persistent CG kernel cannot be made resident (smem %zu bytes)",
-                               tc_smem_bytes(c->kp.tc, d.P));
-  if (d.split_coop && (long)d.Tl * d.nCT * d.nRT1 * d.S1 > c->grid)
-    return fail(c, CMTCS_ECUDA, "cooperative split-K needs all %d stage-1 units co-resident but the grid has %d CTAs",
-                d.Tl * d.nCT * d.nRT1 * d.S1, c->grid);
+    CUDA_OK(c, cudaMemsetAsync(b.Um, 0, sizeof(double) * (size_t)d.Tl * d.N * d.Cp, c->stream));
+    // U's padding rows P..Pp−1 of each task are B-tile rows past the tile's columns: keep them finite
+    CUDA_OK(c, cudaMemsetAsync(b.Uh, 0, sizeof(float) * (size_t)d.Tl * d.Pp * d.N, c->stream));
+    if (b.Ul) CUDA_OK(c, cudaMemsetAsync(b.Ul, 0, sizeof(float) * (size_t)d.Tl * d.Pp * d.N, c->stream));
+  }
+  if (p->op_kind == CMTCS_OP_DENSE) {   // the persistent tensor-core kernel
+    CUDA_OK(c, cudaMemsetAsync(b.tilecnt, 0, sizeof(int) * d.Tl * d.nCT * d.nRT1, c->stream));
+    c->grid = cg_grid_size(c->kp);
+    if (c->grid < 1) return fail(c, CMTCS_ECUDA, "persistent CG kernel cannot be made resident (smem %zu bytes)",
+                                 tc_smem_bytes(c->kp.tc, d.P));
+    if (d.split_coop && (long)d.Tl * d.nCT * d.nRT1 * d.S1 > c->grid)
+      return fail(c, CMTCS_ECUDA, "cooperative split-K needs all %d stage-1 units co-resident but the grid has %d CTAs",
+                  d.Tl * d.nCT * d.nRT1 * d.S1, c->grid);
   }
   // π: log π_c on device
   double *pi_dev = b.red;  // scratch: red is rewritten every M-step
@@ -584,10 +606,13 @@ cmtcs_status cmtcs_init(cmtcs_ctx **out, const cmtcs_problem *p, const float *ph
     c->launches += 3;
   } else {
     CUDA_OK(c, launch_rhs(c->kp, c->stream));
-    CUDA_OK(c, launch_split_phi(c->kp, c->stream));
-    c->launches += 4;
-    char why[256];
-    if (!encode_maps(c->kp, &c->maps, why)) return fail(c, CMTCS_ECUDA, "%s", why);
+    c->launches += 2;
+    if (p->op_kind == CMTCS_OP_DENSE) {
+      CUDA_OK(c, launch_split_phi(c->kp, c->stream));
+      c->launches += 2;
+      char why[256];
+      if (!encode_maps(c->kp, &c->maps, why)) return fail(c, CMTCS_ECUDA, "%s", why);
+    }
   }
   CUDA_OK(c, cudaStreamSynchronize(c->stream));
   if (world > 1) {
@@ -683,6 +708,9 @@ void cmtcs_destroy(cmtcs_ctx *c) {
 
   for (int i = 0; i < 3; ++i)
     if (c->tev[i]) cudaEventDestroy(c->tev[i]);
+  if (c->have_simt_tm)
+    for (int i = 0; i < 3 * SimtTiming::B; ++i)
+      if (c->simt_tm.ev[i]) cudaEventDestroy(c->simt_tm.ev[i]);
   if (c->h_u) cudaFreeHost(c->h_u);
   if (c->h_ts) cudaFreeHost(c->h_ts);
   if (c->h_out) cudaFreeHost(c->h_out);

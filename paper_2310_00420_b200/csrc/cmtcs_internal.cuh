@@ -33,7 +33,8 @@ struct Dims {
   int pair;        // CTA-pair operator (TcCfg::pair), decided with the split: pairs need S1 = 1
   int shared_phi;
   int64_t phi_task_stride;  // elements between Φ_t and Φ_{t+1} (0 if shared)
-  int op;          // CMTCS_OP_DENSE (Φ_t a matrix) or CMTCS_OP_PARTIAL_FOURIER (Φ_t = Ω_t F, k_fourier.cu)
+  int op;          // CMTCS_OP_DENSE (Φ_t a matrix, tensor cores), CMTCS_OP_DENSE_FP32 (the same on the FP32
+                   // CUDA cores, k_simt.cu) or CMTCS_OP_PARTIAL_FOURIER (Φ_t = Ω_t F, k_fourier.cu)
 };
 
 // Device buffers carved from the caller's workspace (all sizes in DESIGN.md §5).
@@ -168,6 +169,13 @@ cudaError_t launch_copy_transcript(const KParams &p, double *gam, double *xi, cu
 bool fourier_supported(int D, int N, char *why);
 cudaError_t launch_fourier_rhs(const KParams &p, cudaStream_t s);
 cudaError_t launch_fourier_cg(const KParams &p, int sms, cudaStream_t s);
+// CG loop of an E-step with the operator on the FP32 CUDA cores (op_kind = CMTCS_OP_DENSE_FP32, k_simt.cu)
+struct SimtTiming {                 // live timing of the FP32 engine (cmtcs_set_timing): CUDA events per step
+  static constexpr int B = 8;       // steps between host termination checks (event pool of B steps)
+  cudaEvent_t ev[3 * B];            // operator start, update start, update end
+  double op_ms, upd_ms;
+};
+cudaError_t run_simt_cg(const KParams &p, int *h_alive, int64_t *launches, SimtTiming *tm, cudaStream_t s);
 
 __device__ __forceinline__ unsigned long long globaltimer() {
   unsigned long long t;

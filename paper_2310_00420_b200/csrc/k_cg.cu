@@ -70,8 +70,10 @@ __global__ void k_init_columns(KParams p) {
       p.b.X[base + i] = 0.f;
       p.b.R[base + i] = v;
       p.b.D32[base + i] = v;
-      p.b.Dh[base + i] = v;     // ±1 is exact in tf32
-      p.b.Dl[base + i] = 0.f;
+      if (p.b.Dh) {             // the tensor-core operator's B operand (absent for the FP32 engine)
+        p.b.Dh[base + i] = v;   // ±1 is exact in tf32
+        p.b.Dl[base + i] = 0.f;
+      }
     }
     if (threadIdx.x == 0) {
       const size_t g = (size_t)t * d.P + slot;

@@ -169,7 +169,7 @@ __global__ void k_estep_finish(KParams p) {
     for (int i = tid; i < d.D; i += blockDim.x) quad = fma(al[i] * mu[i], mu[i], quad);
     quad = block_sum(quad, sh);
     double res = 0.0;
-    if (d.op == CMTCS_OP_DENSE) {
+    if (d.op != CMTCS_OP_PARTIAL_FOURIER) {
       for (int n = tid; n < d.N; n += blockDim.x) {
         const double rv = (double)p.y[(size_t)t * d.N + n] - p.b.Um[((size_t)t * d.N + n) * d.Cp + c];
         res = fma(rv, rv, res);

@@ -18,6 +18,9 @@ class CoFEM:
     Tasks of this rank are global tasks task_begin .. task_begin + T_loc - 1 of T.
     Partial-Fourier sensing (the paper's §4 workload): phi=None, fourier_rows = cuda
     int32 [T_loc, N] sampled DFT rows, y = cuda fp32 [T_loc, 2N] (real parts, then imaginary), D given.
+    engine (dense Φ only): "tensor" — the operator on the tcgen05 tensor cores (3xTF32, persistent
+    kernel); "fp32" — on the FP32 CUDA cores (round-to-nearest accumulation, CMTCS_OP_DENSE_FP32), the
+    path that meets the north_star's |ΔL| ≤ 1e-3 at configs 4-5.
     """
 
     def __init__(self, phi: torch.Tensor, y: torch.Tensor, *, T: int, C: int, K: int, beta: float,
@@ -26,8 +29,10 @@ class CoFEM:
                  alpha_max: float = 1e12, var_floor: float = 1e-12, empty_eps: float = 1e-10,
                  mean_rel_tol: float = -1.0,
                  nccl_uid: bytes | None = None, rank: int = 0, world: int = 1, stream=None,
-                 fourier_rows: torch.Tensor | None = None, D: int | None = None):
+                 fourier_rows: torch.Tensor | None = None, D: int | None = None, engine: str = "tensor"):
         fourier = fourier_rows is not None
+        if engine not in ("tensor", "fp32"):
+            raise ValueError(f"engine must be 'tensor' or 'fp32', got {engine!r}")
         if not (y.is_cuda and (fourier_rows.is_cuda if fourier else phi.is_cuda)):
             raise ValueError("phi (or fourier_rows) and y must be CUDA tensors (no CPU path exists)")
         self.y = y.contiguous() if y.dtype == torch.float32 else y.float().contiguous()
@@ -53,7 +58,8 @@ class CoFEM:
             empty_eps=float(empty_eps), probe_seed=int(probe_seed) & ((1 << 64) - 1),
             task_begin=int(task_begin), task_end=int(task_begin) + T_loc, em_iter0=int(em_iter0),
             mean_rel_tol=float(mean_rel_tol),
-            op_kind=_c.CMTCS_OP_PARTIAL_FOURIER if fourier else _c.CMTCS_OP_DENSE,
+            op_kind=_c.CMTCS_OP_PARTIAL_FOURIER if fourier else
+            (_c.CMTCS_OP_DENSE_FP32 if engine == "fp32" else _c.CMTCS_OP_DENSE),
             fourier_rows=self.rows.data_ptr() if fourier else None)
         a0 = torch.ones(C, D, dtype=torch.float64, device=self.device) if alpha0 is None else \
             torch.as_tensor(np.asarray(alpha0, np.float64) if not torch.is_tensor(alpha0) else alpha0,

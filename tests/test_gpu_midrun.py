@@ -11,6 +11,9 @@ converges) and the mean systems are solved to 1e-10 (P-μ); C4 and C5 run the ta
 sampled in a context holding only those tasks (the probes and M-step are those of the sample).
 Bars as tests/test_gpu_parity.py: μ, s (converged blocks), α rel_∞ ≤ 1e-4; q ≤ 1e-3;
 |ΔL| ≤ 1e-3; ν̄ ≤ 5e-3 + 1e-6|ν̄|; end-to-end α when q is one-hot to 1e-5, q-conditioned α always.
+Both dense engines run every state: the FP32-CUDA-core engine (CMTCS_OP_DENSE_FP32) against every
+north_star bar, the tensor-core engine against the same bars except L at C4/C5 (its documented
+accumulation floor, DESIGN.md §6/§9).
 """
 import json
 import os
@@ -43,12 +46,12 @@ def torch_cuda():
     return torch
 
 
-def _run(data, g, alpha, it, cap, q_override=None):
+def _run(data, g, alpha, it, cap, q_override=None, engine="tensor"):
     """One GPU EM step from (alpha, it) through the C ABI: posterior, info, probe steps."""
     import torch
     cfg = data["cfg"]
     m = make_gpu(data, alpha=alpha, em_iter0=it, cap=cap, mean_tol=float(g["mean_tol"]), T=cfg.T,
-                 task_begin=int(data["tasks"][0]))
+                 task_begin=int(data["tasks"][0]), engine=engine)
     info = m.em_step(1, q_override=None if q_override is None else torch.tensor(q_override).cuda())
     post = to_np(m.posterior())
     steps = m.transcript()["steps"].cpu().numpy().reshape(len(data["tasks"]), cfg.C, cfg.K)
@@ -56,14 +59,15 @@ def _run(data, g, alpha, it, cap, q_override=None):
     return post, info, steps
 
 
+@pytest.mark.parametrize("engine", ["tensor", "fp32"])
 @pytest.mark.parametrize("name,cid", [("c3_step8", 3), ("c4_step5", 4), ("c5_step2", 5)])
-def test_midrun_single_step(torch_cuda, name, cid):
+def test_midrun_single_step(torch_cuda, name, cid, engine):
     g = np.load(os.path.join(GOLDEN, f"{name}.npz"))
     cfg = synthetic.CONFIGS[cid]
     tasks = [int(t) for t in g["tasks"]]
     data = synthetic.generate(cfg, tasks)
     alpha, it, cap = g["alpha_in"], int(g["it"]), int(g["cap"])
-    post, info, steps = _run(data, g, alpha, it, cap)
+    post, info, steps = _run(data, g, alpha, it, cap, engine=engine)
     mu_o, s_o = g["mu"].astype(np.float64), g["s"].astype(np.float64)
     mu_e = rel_inf(post["mu"], mu_o)
     s_e = rel_inf(post["s"], s_o)
@@ -74,9 +78,9 @@ def test_midrun_single_step(torch_cuda, name, cid):
     L_e = abs(L_gpu - float(g["L"]))
     a_e = np.max(rel_inf(post["alpha"], g["alpha_next"]))
     # q-conditioned α: the GPU's M-step fed the oracle's q, from the same state
-    post_q, _, _ = _run(data, g, alpha, it, cap, q_override=g["q"])
+    post_q, _, _ = _run(data, g, alpha, it, cap, q_override=g["q"], engine=engine)
     aq_e = np.max(rel_inf(post_q["alpha"], g["alpha_next"]))
-    print(f"{name}: mu {mu_e.max():.2e} s {s_e[conv].max() if conv.any() else float('nan'):.2e} "
+    print(f"{name} [{engine}]: mu {mu_e.max():.2e} s {s_e[conv].max() if conv.any() else float('nan'):.2e} "
           f"(converged {conv.sum()}/{conv.size}) nu {nu_e.max():.2e} (|nu| {np.abs(g['nu']).max():.3g}) "
           f"q {q_e:.2e} L {L_e:.2e} alpha {a_e:.2e} q-cond alpha {aq_e:.2e} "
           f"GPU probe steps max {steps.max()} oracle {int(g['probe_steps'].max())}")
@@ -85,7 +89,7 @@ def test_midrun_single_step(torch_cuda, name, cid):
     assert np.all(nu_e <= nu_tol(g["nu"]))
     assert q_e <= Q_TOL
     assert aq_e <= A_TOL
-    if cid in L_TENSOR_FLOOR:
+    if engine == "tensor" and cid in L_TENSOR_FLOOR:
         # documented departure: the tcgen05 fp32 accumulation truncates, which
         # shifts ν̄ by 2-5e-7 relative at D = 8192-16384 and L by more than the north_star's 1e-3 on
         # these 1-2-task samples (an fp32 emulation with round-to-nearest accumulation gives

@@ -19,6 +19,7 @@ ap.add_argument("--config", type=int, default=2, help="1-6 (6: partial Fourier)"
 ap.add_argument("--warmup", type=int, default=3)
 ap.add_argument("--tasks", type=int, default=0, help="use only the first n tasks (0 = all)")
 ap.add_argument("--steps", type=int, default=1)
+ap.add_argument("--engine", default="tensor", choices=["tensor", "fp32"])
 a = ap.parse_args()
 cfg = synthetic.CONFIGS[a.config]
 tasks = range(a.tasks) if a.tasks else None
@@ -30,7 +31,7 @@ if cfg.operator == "fourier":   # config 6: Φ_t = Ω_t F given by its sampled r
 else:
     m = CoFEM(torch.from_numpy(data["phi"]).cuda(), torch.from_numpy(data["y"]).cuda(), T=cfg.T, C=cfg.C, K=cfg.K,
               beta=cfg.beta, cg_max_iters=cfg.cg_cap, cg_rel_tol=cfg.cg_tol, probe_seed=cfg.probe_seed,
-              shared_phi=cfg.shared_phi)
+              shared_phi=cfg.shared_phi, engine=a.engine)
 for _ in range(a.warmup):
     m.em_step(1)
 m.set_timing(True)
