@@ -232,10 +232,10 @@ size_t carve(const Dims &d, char *base, Bufs *b) {
   b->bnorm2 = cv.take<double>(Tl);
   const size_t mats = d.shared_phi ? 1 : Tl;
   // dn = 0: the partial-Fourier operator keeps its CG vectors on chip (k_fourier.cu) — only x leaves;
-  // tc = 0: the FP32 engine (k_simt.cu) has no Φᵀ copy, no tf32 pairs and no split-K partials
+  // tc = 0: the FP32 engine (k_simt.cu) has no tf32 pairs and no split-K partials
   const size_t dn = d.op == CMTCS_OP_PARTIAL_FOURIER ? 0 : 1;
   const size_t tc = d.op == CMTCS_OP_DENSE ? 1 : 0;
-  b->PT = cv.take<float>(tc * mats * N * D);
+  b->PT = cv.take<float>(dn * mats * N * D);   // Φᵀ: both dense engines' M-major operand
   b->X = cv.take<float>(Tl * P * D);
   b->R = cv.take<float>(dn * Tl * P * D);
   b->D32 = cv.take<float>(dn * Tl * P * D);
@@ -287,7 +287,8 @@ size_t carve(const Dims &d, char *base, Bufs *b) {
   b->tilecnt = cv.take<int>(Tl * d.nCT * d.nRT1);
   b->gridbar = cv.take<unsigned>(1);
   b->dep = cv.take<int>(2 * Tl);
-  if (!tc) b->PT = b->Dh = b->Dl = b->Ul = nullptr;   // not carved: kernels must not touch them
+  if (!tc) b->Dh = b->Dl = b->Ul = nullptr;   // not carved: kernels must not touch them
+  if (!dn) b->PT = nullptr;
   return cv.off;
 }
 
@@ -606,10 +607,10 @@ cmtcs_status cmtcs_init(cmtcs_ctx **out, const cmtcs_problem *p, const float *ph
     c->launches += 3;
   } else {
     CUDA_OK(c, launch_rhs(c->kp, c->stream));
-    c->launches += 2;
+    CUDA_OK(c, launch_split_phi(c->kp, c->stream));   // Φᵀ
+    c->launches += 3;
     if (p->op_kind == CMTCS_OP_DENSE) {
-      CUDA_OK(c, launch_split_phi(c->kp, c->stream));
-      c->launches += 2;
+      c->launches += 1;
       char why[256];
       if (!encode_maps(c->kp, &c->maps, why)) return fail(c, CMTCS_ECUDA, "%s", why);
     }

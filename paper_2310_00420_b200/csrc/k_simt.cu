@@ -16,13 +16,14 @@
 //   k_simt_mean2      Wm likewise in fp64, dᵀWm partials
 //   k_simt_update     Alg. 1 lines 3-7 per column (γ_u, x, r, ξ_u, d; convergence; transcript)
 //
-// The probe operator is a 128 × 128 × 8 register-tiled SGEMM (256 threads, 8 × 8 outputs per
-// thread, double-buffered shared memory fed from registers): stage 1 multiplies Φ_t (K-major) by the
+// The probe operator is a 128 × 128 register-tiled SGEMM (256 threads, 8 × 8 outputs per thread,
+// a 4-stage cp.async ring of 16-k slabs): stage 1 multiplies Φ_t (K-major) by the
 // directions (K-major); stage 2 reads Φ_t itself as the M-major A operand (no Φᵀ copy) against U.
 // Both stages accumulate in fp32 FFMA (round to nearest); the stage-2 epilogue forms
 // W = β·acc + α ⊙ d in fp64 from the fp64 α and rounds once, and dᵀW (the same rounded W the residual
 // update subtracts) in fp64.  γ_u and ξ_u are fp64 and applied in fp64.
 #include <stdlib.h>
+
 
 #include "cmtcs_internal.cuh"
 
@@ -52,23 +53,49 @@ __device__ __forceinline__ double warp_sum_d(double v) {
 
 // ---- probe operator: U = Φ D (STAGE 1), W = βΦᵀU + α ⊙ D (STAGE 2) -----------------------------
 // grid (ceil(P / 128), ceil(M / 128), T_loc); a tile with no active column returns at once.
-// Accumulation (TWO): a serial fp32 sum over K = 16384 has a random rounding error ~ε·√K relative
-// to the partial sums; the two-level form sums each 64-long block of the contraction in fp32 and
-// adds the block sums (round to nearest) into a second accumulator, ~ε·(√64 + √(K/64)).
-template <int STAGE, bool TWO>
-struct SimtCfg {
-  static constexpr int BK = TWO ? 16 : 8;          // contraction slab
-  static constexpr int NV = BK / 8;                // float4 of A (and of B) staged per thread and slab
-  static constexpr int FLUSH = TWO ? 64 / BK : 0;  // slabs per block sum
-  static constexpr int MINB = TWO ? 1 : 2;         // CTAs per SM (register budget 255 / 128)
+// Both stages are one GEMM shape, C[j][m] = Σ_k A[k][m] · B[j][k]: A is M-major — stage 1 reads
+// Φᵀ (transposed once at init, [D][N]), stage 2 reads Φ itself — and B is K-major (the directions'
+// or U's rows).
+//
+// Operands stream through a KST-stage cp.async ring of 16-k slabs (no register staging: the copies
+// are in flight for KST − 1 slabs of FMAs).  The M-major A slab (16 k × 128 m) is stored as is; a
+// thread reads its rows' float4 at each k, and consecutive rows form the register pairs of packed
+// FFMA2 (two round-to-nearest fp32 FMAs per instruction, the B value a scalar broadcast operand).
+// The K-major B slab keeps its global layout: row r holds its 16 k as four 16-byte quads at quad
+// position q ^ ((r >> 3) & 3) of a 20-float row (16-byte group 5r + quad mod 8), so that the 16
+// threads of a half-warp reading rows 4·tx + j at one k quad hit all 8 bank groups twice (two
+// wavefronts per 256 bytes, the minimum; the unswizzled row hits 4 groups); a thread reads a float4
+// of 4 consecutive k per row.
+//
+// Accumulation: a serial fp32 sum over K = 16384 has a random rounding error ~ε·√K relative to the
+// partial sums; each 64-long block of the contraction is summed in fp32 and the block sums are added
+// (round to nearest) into a second accumulator, ~ε·(√64 + √(K/64)).
+constexpr int KBK = 16;                    // k per slab
+constexpr int KST = 4;                     // ring stages
+constexpr int KLD = 20;                    // K-major smem row (16 k + 4 pad), floats
+constexpr int FLUSH = 64 / KBK;            // slabs per block sum
+
+__device__ __forceinline__ void cp_async16(uint32_t saddr, const void *gmem, bool valid) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(saddr), "l"(gmem), "r"(valid ? 16 : 0)
+               : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
+__device__ __forceinline__ int kq_phys(int row, int q) { return q ^ ((row >> 3) & 3); }
+
+struct SimtSmem {
+  float a[KST][KBK * SLD];                 // M-major A slabs [k][m]
+  float b[KST][SBN * KLD];                 // K-major B slabs [j][k] (swizzled quads)
 };
 
-template <int STAGE, bool TWO>
-__global__ void __launch_bounds__(STH, SimtCfg<STAGE, TWO>::MINB) k_simt_probe(KParams p, int u) {
-  using CF = SimtCfg<STAGE, TWO>;
-  constexpr int BK = CF::BK, NV = CF::NV;
-  __shared__ __align__(16) float As[2][BK][SLD];
-  __shared__ __align__(16) float Bs[2][BK][SLD];
+// VAR (experiments): 0 = FFMA2 + two-level sums (1 CTA / SM); 1 = scalar FFMA + two-level;
+// 2 = FFMA2, single-level sums, 2 CTAs / SM (≤ 128 registers)
+template <int STAGE, int VAR>
+__global__ void __launch_bounds__(STH, VAR == 2 ? 2 : 1) k_simt_probe(KParams p, int u) {
+  constexpr bool TWO = VAR != 2;
+  extern __shared__ __align__(16) unsigned char simt_raw[];
+  SimtSmem &sm = *reinterpret_cast<SimtSmem *>(simt_raw);
   __shared__ double red[STH / 32][SBN];
   if (loop_done(p, u)) return;
   const Dims &d = p.d;
@@ -80,106 +107,103 @@ __global__ void __launch_bounds__(STH, SimtCfg<STAGE, TWO>::MINB) k_simt_probe(K
   const int *flag = p.b.flag + (size_t)t * d.P + j0;
   if (!__syncthreads_or(tid < ncol && flag[tid] == 1)) return;
   if (STAGE == 2 && rt == 0 && tid == 0) atomicAdd(p.b.histp + u, ncol);
-  const float *__restrict__ phi = p.phi + (size_t)t * d.phi_task_stride;
+  // A[k][m]: stage 1 Φᵀ_t [D][N], stage 2 Φ_t [N][D]; row length M
+  const float *__restrict__ amat = STAGE == 1 ? p.b.PT + (size_t)t * d.phi_task_stride
+                                              : p.phi + (size_t)t * d.phi_task_stride;
   const float *__restrict__ bsrc = STAGE == 1 ? p.b.D32 + (size_t)t * d.P * d.D : p.b.Uh + (size_t)t * d.Pp * d.N;
+  const uint32_t sa0 = (uint32_t)__cvta_generic_to_shared(&sm.a[0][0]);
+  const uint32_t sb0 = (uint32_t)__cvta_generic_to_shared(&sm.b[0][0]);
 
-  // NV float4 of A and of B per thread and slab, staged in registers across the slab's FMAs.
-  // K-major tiles (stage-1 A, both B): rows idx/(BK/4), k quads idx%(BK/4), stored transposed
-  // [k][row] (the k quads of a warp fall ≥ 8 banks apart: row stride SLD ≡ 4 mod 32);
-  // stage-2 A is Φ itself, M-major: k = idx/32, rows (idx%32)·4, stored as is.
-  float4 ra[NV], rb[NV];
-  auto gload = [&](int k0) {
-    const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+  // slab kt → ring slot kt % KST: 2 × 16-byte copies per thread and operand
+  auto issue = [&](int kt) {
+    const int slot = kt % KST, k0 = kt * KBK;
 #pragma unroll
-    for (int v = 0; v < NV; ++v) {
+    for (int v = 0; v < 2; ++v) {
       const int idx = tid + v * STH;
-      if (STAGE == 1) {
-        const int m = m0 + idx / (BK / 4), k = k0 + (idx % (BK / 4)) * 4;
-        ra[v] = (m < M && k < KD) ? ldcs4(phi + (size_t)m * d.D + k) : z;
-      } else {
-        const int k = k0 + (idx >> 5), m = m0 + (idx & 31) * 4;
-        ra[v] = (k < KD && m < M) ? ldcs4(phi + (size_t)k * d.D + m) : z;
+      {                                         // A: k row idx/32, 4 m at (idx%32)·4
+        const int kr = idx >> 5, c4 = (idx & 31) * 4, k = k0 + kr, m = m0 + c4;
+        const bool ok = k < KD && m < M;
+        cp_async16(sa0 + 4u * (uint32_t)(slot * KBK * SLD + kr * SLD + c4), ok ? amat + (size_t)k * M + m : amat, ok);
       }
-      const int row = idx / (BK / 4), k = k0 + (idx % (BK / 4)) * 4;
-      rb[v] = (row < ncol && k < KD) ? ldg4(bsrc + (size_t)(j0 + row) * KD + k) : z;
-    }
-  };
-  auto sstore = [&](int buf) {
-#pragma unroll
-    for (int v = 0; v < NV; ++v) {
-      const int idx = tid + v * STH;
-      const int row = idx / (BK / 4), kq = (idx % (BK / 4)) * 4;
-      if (STAGE == 1) {
-        As[buf][kq + 0][row] = ra[v].x;
-        As[buf][kq + 1][row] = ra[v].y;
-        As[buf][kq + 2][row] = ra[v].z;
-        As[buf][kq + 3][row] = ra[v].w;
-      } else {
-        *reinterpret_cast<float4 *>(&As[buf][idx >> 5][(idx & 31) * 4]) = ra[v];
-      }
-      Bs[buf][kq + 0][row] = rb[v].x;
-      Bs[buf][kq + 1][row] = rb[v].y;
-      Bs[buf][kq + 2][row] = rb[v].z;
-      Bs[buf][kq + 3][row] = rb[v].w;
+      const int r = idx >> 2, q = idx & 3, k = k0 + 4 * q;   // B: column r of the tile, k quad q
+      const bool ok = r < ncol && k < KD;
+      cp_async16(sb0 + 4u * (uint32_t)(slot * SBN * KLD + r * KLD + 4 * kq_phys(r, q)),
+                 ok ? bsrc + (size_t)(j0 + r) * KD + k : bsrc, ok);
     }
   };
 
-  // acc2[i][h] = outputs (row i, columns 2h, 2h+1): packed FFMA2 (two round-to-nearest fp32 FMAs per
-  // instruction, the A value a scalar broadcast operand) halves the issue slots of the math
-  float2 acc2[8][4], tot2[TWO ? 8 : 1][TWO ? 4 : 1];
+  // acc2[ip][j]: rows (2ip, 2ip+1) of this thread's 8 (ty·4 + i, i < 4; 64 + ty·4 + i − 4), column j
+  // of its 8 (tx·4 + j, j < 4; 64 + tx·4 + j − 4)
+  float2 acc2[4][8], tot2[TWO ? 4 : 1][TWO ? 8 : 1];
 #pragma unroll
-  for (int i = 0; i < 8; ++i)
+  for (int i = 0; i < 4; ++i)
 #pragma unroll
-    for (int h = 0; h < 4; ++h) acc2[i][h] = make_float2(0.f, 0.f);
-  if (TWO) {
+    for (int j = 0; j < 8; ++j) {
+      acc2[i][j] = make_float2(0.f, 0.f);
+      if (TWO) tot2[TWO ? i : 0][TWO ? j : 0] = make_float2(0.f, 0.f);
+    }
+  const int nk = (KD + KBK - 1) / KBK;
 #pragma unroll
-    for (int i = 0; i < 8; ++i)
-#pragma unroll
-      for (int h = 0; h < 4; ++h) tot2[TWO ? i : 0][TWO ? h : 0] = make_float2(0.f, 0.f);
+  for (int s = 0; s < KST - 1; ++s) {
+    if (s < nk) issue(s);
+    cp_commit();
   }
-  const int nk = (KD + BK - 1) / BK;
-  gload(0);
-  sstore(0);
-  __syncthreads();
   for (int kt = 0; kt < nk; ++kt) {
-    const int buf = kt & 1;
-    if (kt + 1 < nk) gload((kt + 1) * BK);
+    cp_wait<KST - 2>();
+    __syncthreads();                            // slab kt landed for all; slot (kt − 1) % KST is free
+    if (kt + KST - 1 < nk) issue(kt + KST - 1);
+    cp_commit();
+    const int slot = kt % KST;
+    const float *As = sm.a[slot], *Bs = sm.b[slot];
 #pragma unroll
-    for (int kk = 0; kk < BK; ++kk) {
-      const float4 a0 = *reinterpret_cast<const float4 *>(&As[buf][kk][ty * 4]);
-      const float4 a1 = *reinterpret_cast<const float4 *>(&As[buf][kk][64 + ty * 4]);
-      const float4 b0 = *reinterpret_cast<const float4 *>(&Bs[buf][kk][tx * 4]);
-      const float4 b1 = *reinterpret_cast<const float4 *>(&Bs[buf][kk][64 + tx * 4]);
-      const float a[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
-      const float2 b[4] = {make_float2(b0.x, b0.y), make_float2(b0.z, b0.w), make_float2(b1.x, b1.y),
-                           make_float2(b1.z, b1.w)};
+    for (int q = 0; q < 4; ++q) {               // 4 k per step
+      float4 bq[8];
 #pragma unroll
-      for (int i = 0; i < 8; ++i)
+      for (int j = 0; j < 8; ++j) {
+        const int r = (j < 4 ? tx * 4 + j : 64 + tx * 4 + j - 4);
+        bq[j] = *reinterpret_cast<const float4 *>(Bs + r * KLD + 4 * kq_phys(r, q));
+      }
 #pragma unroll
-        for (int h = 0; h < 4; ++h) acc2[i][h] = __ffma2_rn(make_float2(a[i], a[i]), b[h], acc2[i][h]);
+      for (int e = 0; e < 4; ++e) {
+        const float4 lo = *reinterpret_cast<const float4 *>(As + (4 * q + e) * SLD + ty * 4);
+        const float4 hi = *reinterpret_cast<const float4 *>(As + (4 * q + e) * SLD + 64 + ty * 4);
+        const float2 ap[4] = {make_float2(lo.x, lo.y), make_float2(lo.z, lo.w), make_float2(hi.x, hi.y),
+                              make_float2(hi.z, hi.w)};
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const float bv = reinterpret_cast<const float *>(&bq[j])[e];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            if (VAR == 1) {
+              acc2[i][j].x = fmaf(ap[i].x, bv, acc2[i][j].x);
+              acc2[i][j].y = fmaf(ap[i].y, bv, acc2[i][j].y);
+            } else {
+              acc2[i][j] = __ffma2_rn(ap[i], make_float2(bv, bv), acc2[i][j]);
+            }
+          }
+        }
+      }
     }
-    if (TWO && ((kt + 1) % CF::FLUSH == 0 || kt + 1 == nk)) {
+    if (TWO && ((kt + 1) % FLUSH == 0 || kt + 1 == nk)) {
 #pragma unroll
-      for (int i = 0; i < 8; ++i)
+      for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int h = 0; h < 4; ++h) {
-          float2 &tt = tot2[TWO ? i : 0][TWO ? h : 0];
-          tt.x += acc2[i][h].x;
-          tt.y += acc2[i][h].y;
-          acc2[i][h] = make_float2(0.f, 0.f);
+        for (int j = 0; j < 8; ++j) {
+          tot2[TWO ? i : 0][TWO ? j : 0].x += acc2[i][j].x;
+          tot2[TWO ? i : 0][TWO ? j : 0].y += acc2[i][j].y;
+          acc2[i][j] = make_float2(0.f, 0.f);
         }
     }
-    if (kt + 1 < nk) sstore(buf ^ 1);
-    __syncthreads();
   }
+  cp_wait<0>();
   float acc[8][8];
 #pragma unroll
-  for (int i = 0; i < 8; ++i)
+  for (int i = 0; i < 4; ++i)
 #pragma unroll
-    for (int h = 0; h < 4; ++h) {
-      const float2 v = TWO ? tot2[TWO ? i : 0][TWO ? h : 0] : acc2[i][h];
-      acc[i][2 * h] = v.x;
-      acc[i][2 * h + 1] = v.y;
+    for (int j = 0; j < 8; ++j) {
+      const float2 v = TWO ? tot2[TWO ? i : 0][TWO ? j : 0] : acc2[i][j];
+      acc[2 * i][j] = v.x;
+      acc[2 * i + 1][j] = v.y;
     }
 
   // acc[i][j]: row m0 + (i < 4 ? ty*4 + i : 64 + ty*4 + i-4), column j0 + (j < 4 ? tx*4 + j : 64 + tx*4 + j-4)
@@ -508,8 +532,21 @@ cudaError_t run_simt_cg(const KParams &p, int *h_alive, int64_t *launches, SimtT
   const dim3 gm1((d.N + SBM - 1) / SBM, d.Tl), gm2((d.D + SBM - 1) / SBM, d.Tl);
   const int gu = (d.Tl * (d.P + d.C) + 7) / 8;
   constexpr int B = SimtTiming::B;
-  const bool two = !getenv("CMTCS_SIMT_ONE");   // experiments: single fp32 accumulator
-  cudaError_t e = cudaMemsetAsync(p.b.u, 0, sizeof(int), s);
+  cudaError_t e = cudaSuccess;
+  static int var = -1;   // dynamic shared memory above 48 KB (one process per GPU); CMTCS_SIMT_VAR experiments
+  if (var < 0) {
+    var = getenv("CMTCS_SIMT_VAR") ? atoi(getenv("CMTCS_SIMT_VAR")) : 0;
+    if (var < 0 || var > 2) var = 0;
+    const int sb = (int)sizeof(SimtSmem);
+    e = cudaFuncSetAttribute(k_simt_probe<1, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, sb);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_simt_probe<2, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, sb);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_simt_probe<1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, sb);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_simt_probe<2, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, sb);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_simt_probe<1, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, sb);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_simt_probe<2, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, sb);
+    if (e != cudaSuccess) return e;
+  }
+  e = cudaMemsetAsync(p.b.u, 0, sizeof(int), s);
   if (e != cudaSuccess) return e;
   auto collect = [&](int n) -> cudaError_t {   // the last n steps' events (their work has completed)
     for (int i = 0; i < n; ++i) {
@@ -526,11 +563,13 @@ cudaError_t run_simt_cg(const KParams &p, int *h_alive, int64_t *launches, SimtT
   for (int u = 0; u < d.cap; ++u) {
     const int slot = u % B;
     if (tm) cudaEventRecord(tm->ev[3 * slot], s);
-    if (two) k_simt_probe<1, true><<<g1, STH, 0, s>>>(p, u);
-    else k_simt_probe<1, false><<<g1, STH, 0, s>>>(p, u);
+    if (var == 0) k_simt_probe<1, 0><<<g1, STH, sizeof(SimtSmem), s>>>(p, u);
+    else if (var == 1) k_simt_probe<1, 1><<<g1, STH, sizeof(SimtSmem), s>>>(p, u);
+    else k_simt_probe<1, 2><<<g1, STH, sizeof(SimtSmem), s>>>(p, u);
     k_simt_mean1<<<gm1, MTH, 0, s>>>(p, u);
-    if (two) k_simt_probe<2, true><<<g2, STH, 0, s>>>(p, u);
-    else k_simt_probe<2, false><<<g2, STH, 0, s>>>(p, u);
+    if (var == 0) k_simt_probe<2, 0><<<g2, STH, sizeof(SimtSmem), s>>>(p, u);
+    else if (var == 1) k_simt_probe<2, 1><<<g2, STH, sizeof(SimtSmem), s>>>(p, u);
+    else k_simt_probe<2, 2><<<g2, STH, sizeof(SimtSmem), s>>>(p, u);
     k_simt_mean2<<<gm2, MTH, 0, s>>>(p, u);
     if (tm) cudaEventRecord(tm->ev[3 * slot + 1], s);
     k_simt_update<<<gu, 256, 0, s>>>(p, u);
