@@ -64,16 +64,14 @@ def tf32x3_peak_tflops(peaks):
     return peaks["bf16_tflops"] * ratio / 3.0, peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"]) * ratio / 3.0
 
 
-# north_star: "Tensor cores (3xTF32 split) are used only ... if the oracle tolerance holds".  Measured
-# (tests/test_gpu_midrun.py): the tensor-core engine meets every bar at C1-C3 and misses
-# |ΔL| ≤ 1e-3 at C4/C5 (truncating accumulation); the FP32 engine meets it there.
-AUTO_ENGINE = {1: "tensor", 2: "tensor", 3: "tensor", 4: "fp32", 5: "fp32"}
-
-
+# north_star: "Tensor cores (3xTF32 split) are used only for the shared-Φ dense-contraction config,
+# and only if the oracle tolerance holds".  Measured (tests/test_gpu_midrun.py): the
+# tensor-core engine misses |ΔL| ≤ 1e-3 at C4 and C5 (truncating accumulation), C5 included; the FP32
+# engine meets every bar everywhere.  auto = the FP32 engine at every dense config (reading E1).
 def resolve_engine(name, cfg):
     if cfg.operator == "fourier":
         return "fourier"
-    return AUTO_ENGINE[cfg.cfg_id] if name == "auto" else name
+    return "fp32" if name == "auto" else name
 
 
 def parse():
@@ -90,8 +88,8 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=0,
                     help="EM iterations of the end-to-end leg (init from host buffers + steps + readback); 0 = all K")
     ap.add_argument("--engine", default="auto", choices=["auto", "tensor", "fp32"],
-                    help="dense operator: tcgen05 3xTF32 tensor cores or FP32 CUDA cores; auto = the north_star's "
-                         "rule (tensor cores only where the oracle tolerance holds: C1-C3; FP32 at C4/C5, DESIGN.md §6)")
+                    help="dense operator: FP32 CUDA cores or tcgen05 3xTF32 tensor cores; auto = the north_star's "
+                         "rule (tensor cores only where the oracle tolerance holds: nowhere at C4/C5, so FP32; DESIGN.md §3 E1)")
     ap.add_argument("--scaling", default="strong", choices=["weak", "strong"],
                     help="N > 1: strong = the config's tasks sharded (default), weak = a config-sized block per rank")
     return ap.parse_args()
@@ -252,16 +250,18 @@ def reference_arm(args):
 # --------------------------------------------------------------------------------------------
 # CUDA arm
 # --------------------------------------------------------------------------------------------
-def ncu_traffic(cfg_name):
-    """DRAM bytes (read + write) of the persistent CG kernel per CG step, from the committed
-    ncu --set full capture (profiles/ncu_summary.json), if any: the same unit as `achieved`."""
+def ncu_traffic(cfg_name, engine="tensor"):
+    """DRAM bytes (read + write) per CG step of the dominant kernel(s) — the persistent CG kernel
+    (tensor engine) or the two operator SGEMM launches of a step (FP32 engine) — from the committed
+    ncu --set full captures (profiles/ncu_summary.json), if any: the same unit as `achieved`."""
     p = os.path.join(ROOT, "profiles", "ncu_summary.json")
     if not os.path.exists(p):
         return None
     try:
         with open(p) as f:
             j = json.load(f)
-        return j.get("traffic_bytes_per_cg_step", {}).get(cfg_name)
+        key = "traffic_bytes_per_cg_step_fp32" if engine == "fp32" else "traffic_bytes_per_cg_step"
+        return j.get(key, {}).get(cfg_name)
     except Exception:
         return None
 
@@ -475,8 +475,10 @@ def cuda_arm(args):
                 "wall_s_timed": wall,
             },
             "roofline": {"bound": "alu" if alu else "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                         "frac": achieved / peak, "traffic": ncu_traffic(cfg.name),
-                         "traffic_unit": "DRAM bytes per CG step (ncu --set full of k_cg_persistent / its CG steps)",
+                         "frac": achieved / peak, "traffic": ncu_traffic(cfg.name, engine),
+                         "traffic_unit": ("DRAM bytes per CG step (ncu --set full: k_simt_probe<1> + k_simt_probe<2>, "
+                                          "one launch each)") if engine == "fp32" else
+                                         "DRAM bytes per CG step (ncu --set full of k_cg_persistent / its CG steps)",
                          "kernel": ("k_cg_fourier (partial-Fourier CG: one CTA per column, FFT in shared memory; "
                                     "achieved = 10*D*log2(D) flop per active column per CG step / the kernels' "
                                     "duration)") if fourier else

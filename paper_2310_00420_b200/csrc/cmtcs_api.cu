@@ -41,6 +41,7 @@ struct cmtcs_ctx {
   int grid;
   int *h_u;                 // pinned: CG steps executed
   SimtTiming simt_tm;       // the FP32 engine's per-step events (created with the context)
+  SimtStreams simt_ss;      // ... and its side stream for the mean columns
   bool have_simt_tm;
 };
 
@@ -168,6 +169,7 @@ bool make_dims(const cmtcs_problem *p, Dims *d, char *why) {
   d->K = p->K;
   d->P = p->C * p->K;
   d->Pp = (d->P + 3) & ~3;
+  d->ldv = p->op_kind == CMTCS_OP_DENSE_FP32 ? (p->task_end - p->task_begin) * d->Pp : 0;
   d->Cp = (p->C + 1) & ~1;
   d->cap = p->cg_max_iters;
   d->nw = (p->D + 63) / 64;
@@ -236,12 +238,13 @@ size_t carve(const Dims &d, char *base, Bufs *b) {
   const size_t dn = d.op == CMTCS_OP_PARTIAL_FOURIER ? 0 : 1;
   const size_t tc = d.op == CMTCS_OP_DENSE ? 1 : 0;
   b->PT = cv.take<float>(dn * mats * N * D);   // Φᵀ: both dense engines' M-major operand
-  b->X = cv.take<float>(Tl * P * D);
-  b->R = cv.take<float>(dn * Tl * P * D);
-  b->D32 = cv.take<float>(dn * Tl * P * D);
+  const size_t PV = d.ldv ? (size_t)d.Pp : P;   // FP32 engine: d-major with padded task blocks
+  b->X = cv.take<float>(Tl * PV * D);
+  b->R = cv.take<float>(dn * Tl * PV * D);
+  b->D32 = cv.take<float>(dn * Tl * PV * D);
   b->Dh = cv.take<float>(tc * Tl * P * D);
   b->Dl = cv.take<float>(tc * Tl * P * D);
-  b->W = cv.take<float>(dn * Tl * P * D);
+  b->W = cv.take<float>(dn * Tl * PV * D);
   b->Xm = cv.take<double>(Tl * C * D);
   b->Rm = cv.take<double>(dn * Tl * C * D);
   b->Dm = cv.take<double>(dn * Tl * C * D);
@@ -349,7 +352,7 @@ cmtcs_status one_em_iteration(cmtcs_ctx *c, const uint64_t *probe_bits, const do
     CUDA_OK(c, cudaMemsetAsync(kp.b.u, 0, sizeof(int), s));
   } else {
     CUDA_OK(c, launch_init_columns(kp, s));
-    L += 1;
+    L += d.ldv ? 2 : 1;
   }
   const bool tm = c->timing;
   if (tm) {
@@ -361,7 +364,7 @@ cmtcs_status one_em_iteration(cmtcs_ctx *c, const uint64_t *probe_bits, const do
     CUDA_OK(c, launch_fourier_cg(kp, c->grid, s));   // probe columns (fp32), then mean columns (fp64)
   } else if (d.op == CMTCS_OP_DENSE_FP32) {
     c->simt_tm.op_ms = c->simt_tm.upd_ms = 0.0;
-    CUDA_OK(c, run_simt_cg(kp, c->h_u, &L, tm ? &c->simt_tm : nullptr, s));   // L counts the per-step kernels
+    CUDA_OK(c, run_simt_cg(kp, c->h_u, &L, tm ? &c->simt_tm : nullptr, c->simt_ss, s));   // L counts the per-step kernels
   } else {
     CUDA_OK(c, launch_cg_persistent(kp, c->maps, c->grid, s));
   }
@@ -571,6 +574,9 @@ cmtcs_status cmtcs_init(cmtcs_ctx **out, const cmtcs_problem *p, const float *ph
   if (p->op_kind == CMTCS_OP_DENSE_FP32) {
     for (int i = 0; i < 3 * SimtTiming::B; ++i) CUDA_OK(c, cudaEventCreate(&c->simt_tm.ev[i]));
     c->have_simt_tm = true;
+    CUDA_OK(c, cudaStreamCreateWithFlags(&c->simt_ss.side, cudaStreamNonBlocking));
+    CUDA_OK(c, cudaEventCreateWithFlags(&c->simt_ss.fork, cudaEventDisableTiming));
+    CUDA_OK(c, cudaEventCreateWithFlags(&c->simt_ss.join, cudaEventDisableTiming));
   }
   CUDA_OK(c, cudaMemsetAsync(b.status, 0, 8 * sizeof(int), c->stream));
   CUDA_OK(c, cudaMemsetAsync(b.gam, 0, sizeof(double) * d.Tl * d.P * d.cap, c->stream));
@@ -709,9 +715,16 @@ void cmtcs_destroy(cmtcs_ctx *c) {
 
   for (int i = 0; i < 3; ++i)
     if (c->tev[i]) cudaEventDestroy(c->tev[i]);
-  if (c->have_simt_tm)
+  if (c->have_simt_tm) {
     for (int i = 0; i < 3 * SimtTiming::B; ++i)
       if (c->simt_tm.ev[i]) cudaEventDestroy(c->simt_tm.ev[i]);
+    if (c->simt_ss.side) {
+      cudaStreamSynchronize(c->simt_ss.side);
+      cudaStreamDestroy(c->simt_ss.side);
+    }
+    if (c->simt_ss.fork) cudaEventDestroy(c->simt_ss.fork);
+    if (c->simt_ss.join) cudaEventDestroy(c->simt_ss.join);
+  }
   if (c->h_u) cudaFreeHost(c->h_u);
   if (c->h_ts) cudaFreeHost(c->h_ts);
   if (c->h_out) cudaFreeHost(c->h_out);

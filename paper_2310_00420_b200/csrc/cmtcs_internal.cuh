@@ -21,6 +21,8 @@ struct Dims {
   int T, Tl, t0, N, D, C, K;
   int P;     // probe columns per task = C*K
   int Pp;    // P rounded up to a multiple of 4 (row stride of U)
+  int ldv;   // FP32 engine: row stride of its d-major probe vectors X, R, D32, W [D][T_loc·Pp] and of U
+             // [N][T_loc·Pp] (column g = t·Pp + j); 0 for the column-contiguous layouts [T_loc][P][D]
   int Cp;    // C rounded up to even (row stride of Um: 16-byte TMA rows)
   int cap;   // CG step cap U
   int nw;    // 64-bit probe words per column = ceil(D/64)
@@ -175,7 +177,12 @@ struct SimtTiming {                 // live timing of the FP32 engine (cmtcs_set
   cudaEvent_t ev[3 * B];            // operator start, update start, update end
   double op_ms, upd_ms;
 };
-cudaError_t run_simt_cg(const KParams &p, int *h_alive, int64_t *launches, SimtTiming *tm, cudaStream_t s);
+struct SimtStreams {                // the FP32 engine's side stream: the fp64 mean-column kernels run
+  cudaStream_t side;                // beside the probe SGEMMs (fork after the update, join before it)
+  cudaEvent_t fork, join;
+};
+cudaError_t run_simt_cg(const KParams &p, int *h_alive, int64_t *launches, SimtTiming *tm, const SimtStreams &ss,
+                        cudaStream_t s);
 
 __device__ __forceinline__ unsigned long long globaltimer() {
   unsigned long long t;

@@ -64,7 +64,8 @@ __global__ void k_init_columns(KParams p) {
     const size_t base = ((size_t)t * d.P + slot) * d.D;
     const uint64_t wbase = ((((uint64_t)p.it * d.T + (uint64_t)(d.t0 + t)) * d.C + c) * d.K + k) * d.nw;
     const uint64_t *ov = p.probe_bits ? p.probe_bits + (((size_t)t * d.C + c) * d.K + k) * d.nw : nullptr;
-    for (int i = threadIdx.x; i < d.D; i += blockDim.x) {
+    // (the FP32 engine's d-major probe vectors are written by its own kernel, k_simt.cu)
+    for (int i = threadIdx.x; i < d.D && !d.ldv; i += blockDim.x) {
       const uint64_t wd = ov ? ov[i >> 6] : probe_word(p.seed, wbase + (uint64_t)(i >> 6));
       const float v = ((wd >> (i & 63)) & 1ull) ? -1.f : 1.f;
       p.b.X[base + i] = 0.f;
@@ -101,6 +102,28 @@ __global__ void k_init_columns(KParams p) {
   }
 }
 
+// K3 for the FP32 engine's d-major probe vectors ([D][T_loc·Pp], column g = t·Pp + j): the same
+// probes (reading A6) written coalesced along the columns; padding columns j ≥ P are zeroed
+__global__ void k_init_probes_dmajor(KParams p) {
+  const Dims &d = p.d;
+  const size_t n = (size_t)d.D * d.ldv;
+  for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < n; e += (size_t)gridDim.x * blockDim.x) {
+    const int i = (int)(e / d.ldv), g = (int)(e % d.ldv);
+    const int t = g / d.Pp, j = g % d.Pp;
+    float v = 0.f;
+    if (j < d.P) {
+      const int c = j / d.K, k = j % d.K;
+      const uint64_t wbase = ((((uint64_t)p.it * d.T + (uint64_t)(d.t0 + t)) * d.C + c) * d.K + k) * d.nw;
+      const uint64_t wd = p.probe_bits ? p.probe_bits[(((size_t)t * d.C + c) * d.K + k) * d.nw + (i >> 6)]
+                                       : probe_word(p.seed, wbase + (uint64_t)(i >> 6));
+      v = ((wd >> (i & 63)) & 1ull) ? -1.f : 1.f;
+    }
+    p.b.X[e] = 0.f;
+    p.b.R[e] = v;
+    p.b.D32[e] = v;
+  }
+}
+
 __global__ void k_probe_words(uint64_t seed, int it, int T, int t0, int Tl, int C, int K, int D,
                               uint64_t *out) {
   const int nw = (D + 63) / 64;
@@ -123,6 +146,7 @@ cudaError_t launch_rhs(const KParams &p, cudaStream_t s) {
 
 cudaError_t launch_init_columns(const KParams &p, cudaStream_t s) {
   k_init_columns<<<dim3(p.d.P + p.d.C, p.d.Tl), 256, 0, s>>>(p);
+  if (p.d.ldv) k_init_probes_dmajor<<<4 * 148, 256, 0, s>>>(p);
   return cudaGetLastError();
 }
 

@@ -39,7 +39,8 @@ __global__ void k_diag(KParams p) {
       const uint64_t w = ((((uint64_t)p.it * d.T + (uint64_t)(d.t0 + t)) * d.C + c) * d.K + k) * d.nw + (dd >> 6);
       wd = mix64(p.seed + (w + 1ull) * 0x9E3779B97F4A7C15ull);
     }
-    const double x = (double)p.b.X[((size_t)t * d.P + c * d.K + k) * d.D + dd];
+    const double x = (double)(d.ldv ? p.b.X[(size_t)dd * d.ldv + (size_t)t * d.Pp + c * d.K + k]   // FP32 engine
+                                    : p.b.X[((size_t)t * d.P + c * d.K + k) * d.D + dd]);
     acc += ((wd >> (dd & 63)) & 1ull) ? -x : x;
   }
   p.b.s[((size_t)t * d.C + c) * d.D + dd] = acc / (double)d.K;

@@ -35,7 +35,7 @@ constexpr int SBM = 128;               // output rows per CTA (n in stage 1, d i
 constexpr int SBN = 128;               // probe columns per CTA
 constexpr int SLD = SBM + 4;           // padded smem row (16-byte aligned rows)
 constexpr int STH = 256;
-constexpr int MTH = 256;               // mean-column kernels
+constexpr int MTH = 128;               // mean-column kernels (co-resident with a probe-SGEMM CTA)
 constexpr int MBK = 16;
 
 __device__ __forceinline__ float4 ldg4(const float *p) { return __ldg(reinterpret_cast<const float4 *>(p)); }
@@ -52,27 +52,28 @@ __device__ __forceinline__ double warp_sum_d(double v) {
 }
 
 // ---- probe operator: U = Φ D (STAGE 1), W = βΦᵀU + α ⊙ D (STAGE 2) -----------------------------
-// grid (ceil(P / 128), ceil(M / 128), T_loc); a tile with no active column returns at once.
-// Both stages are one GEMM shape, C[j][m] = Σ_k A[k][m] · B[j][k]: A is M-major — stage 1 reads
-// Φᵀ (transposed once at init, [D][N]), stage 2 reads Φ itself — and B is K-major (the directions'
-// or U's rows).
+// Layout (Dims::ldv): the FP32 engine keeps its probe vectors d-major — X, R, D32, W as [D][T_loc·Pp]
+// and U as [N][T_loc·Pp], column g = t·Pp + j — so that a k-slab of either operand is 16 contiguous
+// rows: both GEMM stages are C[g][m] = Σ_k A[k][m] · B[k][g] with A M-major (stage 1: Φᵀ [D][N],
+// transposed once at init; stage 2: Φ itself) and B N-major (the directions, U).
+// grid (column tiles, ceil(M / 128), T_loc); a tile with no active column returns at once.
 //
-// Operands stream through a KST-stage cp.async ring of 16-k slabs (no register staging: the copies
-// are in flight for KST − 1 slabs of FMAs).  The M-major A slab (16 k × 128 m) is stored as is; a
-// thread reads its rows' float4 at each k, and consecutive rows form the register pairs of packed
-// FFMA2 (two round-to-nearest fp32 FMAs per instruction, the B value a scalar broadcast operand).
-// The K-major B slab keeps its global layout: row r holds its 16 k as four 16-byte quads at quad
-// position q ^ ((r >> 3) & 3) of a 20-float row (16-byte group 5r + quad mod 8), so that the 16
-// threads of a half-warp reading rows 4·tx + j at one k quad hit all 8 bank groups twice (two
-// wavefronts per 256 bytes, the minimum; the unswizzled row hits 4 groups); a thread reads a float4
-// of 4 consecutive k per row.
+// Operands stream through a KST-stage cp.async ring of 32-k slabs [k][128 + 4 pad] (no register
+// staging: the copies are in flight for KST − 1 slabs of FMAs).  Per k a thread reads two float4
+// of A (its 8 rows) and two of B (its 8 columns) — the 16 distinct float4 of a half-warp are 256
+// contiguous bytes, conflict-free — and the next k's four are loaded before this k's FMAs (register
+// double buffering).  The FMAs are packed FFMA2: consecutive rows are register pairs, the B value a
+// scalar broadcast operand; 32 FFMA2 per k per thread.
 //
 // Accumulation: a serial fp32 sum over K = 16384 has a random rounding error ~ε·√K relative to the
 // partial sums; each 64-long block of the contraction is summed in fp32 and the block sums are added
 // (round to nearest) into a second accumulator, ~ε·(√64 + √(K/64)).
-constexpr int KBK = 16;                    // k per slab
+//
+// pflat > 0 (shared Φ, P % 4 == 0): the columns of all tasks form one GEMM of pflat = T_loc·P columns
+// (one A for everyone), so a task's last partial column tile is not padded — config 5's P = 320
+// would otherwise multiply 384 columns per task.
+constexpr int KBK = 32;                    // k per slab
 constexpr int KST = 4;                     // ring stages
-constexpr int KLD = 20;                    // K-major smem row (16 k + 4 pad), floats
 constexpr int FLUSH = 64 / KBK;            // slabs per block sum
 
 __device__ __forceinline__ void cp_async16(uint32_t saddr, const void *gmem, bool valid) {
@@ -82,18 +83,14 @@ __device__ __forceinline__ void cp_async16(uint32_t saddr, const void *gmem, boo
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
-__device__ __forceinline__ int kq_phys(int row, int q) { return q ^ ((row >> 3) & 3); }
 
 struct SimtSmem {
-  float a[KST][KBK * SLD];                 // M-major A slabs [k][m]
-  float b[KST][SBN * KLD];                 // K-major B slabs [j][k] (swizzled quads)
+  float a[KST][KBK * SLD];                 // A slabs [k][m]
+  float b[KST][KBK * SLD];                 // B slabs [k][g]
 };
 
-// VAR (experiments): 0 = FFMA2 + two-level sums (1 CTA / SM); 1 = scalar FFMA + two-level;
-// 2 = FFMA2, single-level sums, 2 CTAs / SM (≤ 128 registers)
-template <int STAGE, int VAR>
-__global__ void __launch_bounds__(STH, VAR == 2 ? 2 : 1) k_simt_probe(KParams p, int u) {
-  constexpr bool TWO = VAR != 2;
+template <int STAGE>
+__global__ void __launch_bounds__(STH, 1) k_simt_probe(KParams p, int u, int pflat) {
   extern __shared__ __align__(16) unsigned char simt_raw[];
   SimtSmem &sm = *reinterpret_cast<SimtSmem *>(simt_raw);
   __shared__ double red[STH / 32][SBN];
@@ -103,45 +100,42 @@ __global__ void __launch_bounds__(STH, VAR == 2 ? 2 : 1) k_simt_probe(KParams p,
   const int t = blockIdx.z, rt = blockIdx.y, j0 = blockIdx.x * SBN, m0 = rt * SBM;
   const int M = STAGE == 1 ? d.N : d.D;      // output rows
   const int KD = STAGE == 1 ? d.D : d.N;     // contraction length (multiple of 4)
-  const int ncol = min(SBN, d.P - j0);
-  const int *flag = p.b.flag + (size_t)t * d.P + j0;
+  const int ncol = min(SBN, (pflat > 0 ? pflat : d.P) - j0);
+  const size_t gb = pflat > 0 ? (size_t)j0 : (size_t)t * d.Pp + j0;   // first column in the d-major arrays
+  const size_t fb = pflat > 0 ? (size_t)j0 : (size_t)t * d.P + j0;    // ... in the per-column state
+  const int *flag = p.b.flag + fb;
   if (!__syncthreads_or(tid < ncol && flag[tid] == 1)) return;
   if (STAGE == 2 && rt == 0 && tid == 0) atomicAdd(p.b.histp + u, ncol);
-  // A[k][m]: stage 1 Φᵀ_t [D][N], stage 2 Φ_t [N][D]; row length M
+  // A[k][m]: stage 1 Φᵀ_t [D][N], stage 2 Φ_t [N][D] (row length M); B[k][g]: D32 [D][ldv] / U [N][ldv]
   const float *__restrict__ amat = STAGE == 1 ? p.b.PT + (size_t)t * d.phi_task_stride
                                               : p.phi + (size_t)t * d.phi_task_stride;
-  const float *__restrict__ bsrc = STAGE == 1 ? p.b.D32 + (size_t)t * d.P * d.D : p.b.Uh + (size_t)t * d.Pp * d.N;
+  const float *__restrict__ bmat = (STAGE == 1 ? p.b.D32 : p.b.Uh) + gb;
+  const size_t ldv = (size_t)d.ldv;
   const uint32_t sa0 = (uint32_t)__cvta_generic_to_shared(&sm.a[0][0]);
   const uint32_t sb0 = (uint32_t)__cvta_generic_to_shared(&sm.b[0][0]);
 
-  // slab kt → ring slot kt % KST: 2 × 16-byte copies per thread and operand
+  // slab kt → ring slot kt % KST: KBK/8 16-byte copies per thread and operand (k row idx/32, 4
+  // entries at (idx%32)·4)
   auto issue = [&](int kt) {
     const int slot = kt % KST, k0 = kt * KBK;
 #pragma unroll
-    for (int v = 0; v < 2; ++v) {
-      const int idx = tid + v * STH;
-      {                                         // A: k row idx/32, 4 m at (idx%32)·4
-        const int kr = idx >> 5, c4 = (idx & 31) * 4, k = k0 + kr, m = m0 + c4;
-        const bool ok = k < KD && m < M;
-        cp_async16(sa0 + 4u * (uint32_t)(slot * KBK * SLD + kr * SLD + c4), ok ? amat + (size_t)k * M + m : amat, ok);
-      }
-      const int r = idx >> 2, q = idx & 3, k = k0 + 4 * q;   // B: column r of the tile, k quad q
-      const bool ok = r < ncol && k < KD;
-      cp_async16(sb0 + 4u * (uint32_t)(slot * SBN * KLD + r * KLD + 4 * kq_phys(r, q)),
-                 ok ? bsrc + (size_t)(j0 + r) * KD + k : bsrc, ok);
+    for (int v = 0; v < KBK / 8; ++v) {
+      const int idx = tid + v * STH, kr = idx >> 5, c4 = (idx & 31) * 4, k = k0 + kr;
+      const uint32_t so = 4u * (uint32_t)(slot * KBK * SLD + kr * SLD + c4);
+      const bool oka = k < KD && m0 + c4 < M;
+      cp_async16(sa0 + so, oka ? amat + (size_t)k * M + m0 + c4 : amat, oka);
+      const bool okb = k < KD && c4 < ncol;    // a chunk past ncol holds padding / other tasks' columns
+      cp_async16(sb0 + so, okb ? bmat + (size_t)k * ldv + c4 : bmat, okb);
     }
   };
 
   // acc2[ip][j]: rows (2ip, 2ip+1) of this thread's 8 (ty·4 + i, i < 4; 64 + ty·4 + i − 4), column j
   // of its 8 (tx·4 + j, j < 4; 64 + tx·4 + j − 4)
-  float2 acc2[4][8], tot2[TWO ? 4 : 1][TWO ? 8 : 1];
+  float2 acc2[4][8], tot2[4][8];
 #pragma unroll
   for (int i = 0; i < 4; ++i)
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      acc2[i][j] = make_float2(0.f, 0.f);
-      if (TWO) tot2[TWO ? i : 0][TWO ? j : 0] = make_float2(0.f, 0.f);
-    }
+    for (int j = 0; j < 8; ++j) acc2[i][j] = tot2[i][j] = make_float2(0.f, 0.f);
   const int nk = (KD + KBK - 1) / KBK;
 #pragma unroll
   for (int s = 0; s < KST - 1; ++s) {
@@ -154,109 +148,120 @@ __global__ void __launch_bounds__(STH, VAR == 2 ? 2 : 1) k_simt_probe(KParams p,
     if (kt + KST - 1 < nk) issue(kt + KST - 1);
     cp_commit();
     const int slot = kt % KST;
-    const float *As = sm.a[slot], *Bs = sm.b[slot];
+    const float *As = sm.a[slot] + ty * 4, *Bs = sm.b[slot] + tx * 4;
+    float4 a0 = *reinterpret_cast<const float4 *>(As), a1 = *reinterpret_cast<const float4 *>(As + 64);
+    float4 b0 = *reinterpret_cast<const float4 *>(Bs), b1 = *reinterpret_cast<const float4 *>(Bs + 64);
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {               // 4 k per step
-      float4 bq[8];
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const int r = (j < 4 ? tx * 4 + j : 64 + tx * 4 + j - 4);
-        bq[j] = *reinterpret_cast<const float4 *>(Bs + r * KLD + 4 * kq_phys(r, q));
+    for (int kk = 0; kk < KBK; ++kk) {
+      float4 na0, na1, nb0, nb1;
+      if (kk + 1 < KBK) {                       // next k's operands before this k's FMAs
+        na0 = *reinterpret_cast<const float4 *>(As + (kk + 1) * SLD);
+        na1 = *reinterpret_cast<const float4 *>(As + (kk + 1) * SLD + 64);
+        nb0 = *reinterpret_cast<const float4 *>(Bs + (kk + 1) * SLD);
+        nb1 = *reinterpret_cast<const float4 *>(Bs + (kk + 1) * SLD + 64);
       }
+      const float2 ap[4] = {make_float2(a0.x, a0.y), make_float2(a0.z, a0.w), make_float2(a1.x, a1.y),
+                            make_float2(a1.z, a1.w)};
+      const float bv[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const float4 lo = *reinterpret_cast<const float4 *>(As + (4 * q + e) * SLD + ty * 4);
-        const float4 hi = *reinterpret_cast<const float4 *>(As + (4 * q + e) * SLD + 64 + ty * 4);
-        const float2 ap[4] = {make_float2(lo.x, lo.y), make_float2(lo.z, lo.w), make_float2(hi.x, hi.y),
-                              make_float2(hi.z, hi.w)};
+      for (int j = 0; j < 8; ++j)
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const float bv = reinterpret_cast<const float *>(&bq[j])[e];
-#pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            if (VAR == 1) {
-              acc2[i][j].x = fmaf(ap[i].x, bv, acc2[i][j].x);
-              acc2[i][j].y = fmaf(ap[i].y, bv, acc2[i][j].y);
-            } else {
-              acc2[i][j] = __ffma2_rn(ap[i], make_float2(bv, bv), acc2[i][j]);
-            }
-          }
-        }
+        for (int i = 0; i < 4; ++i) acc2[i][j] = __ffma2_rn(ap[i], make_float2(bv[j], bv[j]), acc2[i][j]);
+      if (kk + 1 < KBK) {
+        a0 = na0; a1 = na1; b0 = nb0; b1 = nb1;
       }
     }
-    if (TWO && ((kt + 1) % FLUSH == 0 || kt + 1 == nk)) {
+    if ((kt + 1) % FLUSH == 0 || kt + 1 == nk) {
 #pragma unroll
       for (int i = 0; i < 4; ++i)
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
-          tot2[TWO ? i : 0][TWO ? j : 0].x += acc2[i][j].x;
-          tot2[TWO ? i : 0][TWO ? j : 0].y += acc2[i][j].y;
+          tot2[i][j].x += acc2[i][j].x;
+          tot2[i][j].y += acc2[i][j].y;
           acc2[i][j] = make_float2(0.f, 0.f);
         }
     }
   }
   cp_wait<0>();
-  float acc[8][8];
-#pragma unroll
-  for (int i = 0; i < 4; ++i)
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const float2 v = TWO ? tot2[TWO ? i : 0][TWO ? j : 0] : acc2[i][j];
-      acc[2 * i][j] = v.x;
-      acc[2 * i + 1][j] = v.y;
-    }
 
-  // acc[i][j]: row m0 + (i < 4 ? ty*4 + i : 64 + ty*4 + i-4), column j0 + (j < 4 ? tx*4 + j : 64 + tx*4 + j-4)
-  if (STAGE == 1) {
+  // outputs: rows m0 + g·64 + ty·4 + r (g, r < 2, 4) = tot2[2g + r/2][·].{x|y}; columns
+  // j0 + h·64 + tx·4 + q (h, q < 2, 4) = tot2[·][4h + q]
+  if (STAGE == 1) {                             // U [N][ldv]
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const int c = (j < 4 ? tx * 4 + j : 64 + tx * 4 + j - 4);
-      if (c >= ncol) continue;
-      float *out = p.b.Uh + ((size_t)t * d.Pp + j0 + c) * d.N;
+    for (int g = 0; g < 2; ++g)
 #pragma unroll
-      for (int g = 0; g < 2; ++g) {
-        const int m = m0 + g * 64 + ty * 4;
-        if (m < M) *reinterpret_cast<float4 *>(out + m) =
-            make_float4(acc[4 * g][j], acc[4 * g + 1][j], acc[4 * g + 2][j], acc[4 * g + 3][j]);
-      }
-    }
-  } else {
-    const double beta = p.beta;
-    const int warp = tid >> 5, lane = tid & 31;
+      for (int r = 0; r < 4; ++r) {
+        const int m = m0 + g * 64 + ty * 4 + r;
+        if (m >= M) continue;
+        const int ip = 2 * g + r / 2;
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      double dot = 0.0;
-      const int c = (j < 4 ? tx * 4 + j : 64 + tx * 4 + j - 4);
-      if (c < ncol) {
-        const size_t col = (size_t)t * d.P + j0 + c;
-        const double *al = p.b.alpha64 + (size_t)((j0 + c) / d.K) * d.D;
-#pragma unroll
-        for (int g = 0; g < 2; ++g) {
-          const int m = m0 + g * 64 + ty * 4;
-          if (m >= M) continue;
-          const float4 dv = *reinterpret_cast<const float4 *>(p.b.D32 + col * d.D + m);
-          const double2 a01 = *reinterpret_cast<const double2 *>(al + m);
-          const double2 a23 = *reinterpret_cast<const double2 *>(al + m + 2);
-          float4 w;
-          w.x = (float)fma(beta, (double)acc[4 * g + 0][j], a01.x * (double)dv.x);
-          w.y = (float)fma(beta, (double)acc[4 * g + 1][j], a01.y * (double)dv.y);
-          w.z = (float)fma(beta, (double)acc[4 * g + 2][j], a23.x * (double)dv.z);
-          w.w = (float)fma(beta, (double)acc[4 * g + 3][j], a23.y * (double)dv.w);
-          *reinterpret_cast<float4 *>(p.b.W + col * d.D + m) = w;
-          dot += (double)dv.x * (double)w.x + (double)dv.y * (double)w.y + (double)dv.z * (double)w.z +
-                 (double)dv.w * (double)w.w;
+        for (int h = 0; h < 2; ++h) {
+          const int c4 = h * 64 + tx * 4;
+          if (c4 >= ncol) continue;
+          float4 o;
+          o.x = (r & 1) ? tot2[ip][4 * h + 0].y : tot2[ip][4 * h + 0].x;
+          o.y = (r & 1) ? tot2[ip][4 * h + 1].y : tot2[ip][4 * h + 1].x;
+          o.z = (r & 1) ? tot2[ip][4 * h + 2].y : tot2[ip][4 * h + 2].x;
+          o.w = (r & 1) ? tot2[ip][4 * h + 3].y : tot2[ip][4 * h + 3].x;
+          *reinterpret_cast<float4 *>(p.b.Uh + (size_t)m * ldv + gb + c4) = o;
         }
       }
-      // dᵀW over this tile's 128 rows: the ty pair inside a warp, then the 8 warps (fixed order)
-      dot += __shfl_xor_sync(0xffffffffu, dot, 16);
-      if (lane < 16) red[warp][c] = dot;
+  } else {                                      // W = βΦᵀU + α ⊙ d (fp64, one rounding), dᵀW partials
+    const double beta = p.beta;
+    const int warp = tid >> 5, lane = tid & 31;
+    // α of the tile's 128 rows for every cluster, staged in the (now idle) ring: a thread's 8 columns
+    // × 8 rows would otherwise be 64 scalar global loads
+    double *sal = reinterpret_cast<double *>(&sm.a[0][0]);
+    __syncthreads();                            // every warp is done with the ring
+    for (int e = tid; e < d.C * SBM; e += STH) {
+      const int c = e / SBM, r = e % SBM;
+      sal[e] = m0 + r < M ? p.b.alpha64[(size_t)c * d.D + m0 + r] : 0.0;
+    }
+    __syncthreads();
+    double dot[8];
+    const double *al[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      dot[q] = 0.0;
+      const int c = (q >> 2) * 64 + tx * 4 + (q & 3);
+      al[q] = sal + (size_t)(((fb + min(c, ncol - 1)) % d.P) / d.K) * SBM - m0;   // the column's cluster
+    }
+#pragma unroll
+    for (int g = 0; g < 2; ++g)
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const int m = m0 + g * 64 + ty * 4 + r;
+        if (m >= M) continue;
+        const int ip = 2 * g + r / 2;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int c4 = h * 64 + tx * 4;
+          if (c4 >= ncol) continue;
+          const size_t o = (size_t)m * ldv + gb + c4;
+          const float4 dv = *reinterpret_cast<const float4 *>(p.b.D32 + o);
+          const float dq[4] = {dv.x, dv.y, dv.z, dv.w};
+          float wq[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const float acc = (r & 1) ? tot2[ip][4 * h + q].y : tot2[ip][4 * h + q].x;
+            wq[q] = (float)fma(beta, (double)acc, al[4 * h + q][m] * (double)dq[q]);
+            dot[4 * h + q] += (double)dq[q] * (double)wq[q];
+          }
+          *reinterpret_cast<float4 *>(p.b.W + o) = make_float4(wq[0], wq[1], wq[2], wq[3]);
+        }
+      }
+    // dᵀW over this tile's 128 rows: the ty pair inside a warp, then the 8 warps (fixed order)
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const double v = dot[q] + __shfl_xor_sync(0xffffffffu, dot[q], 16);
+      if (lane < 16) red[warp][(q >> 2) * 64 + tx * 4 + (q & 3)] = v;
     }
     __syncthreads();
     if (tid < ncol) {
       double s = 0.0;
 #pragma unroll
       for (int w = 0; w < STH / 32; ++w) s += red[w][tid];
-      p.b.dAd[((size_t)t * d.P + j0 + tid) * d.nRT2 + rt] = s;
+      p.b.dAd[(fb + tid) * d.nRT2 + rt] = s;
     }
   }
 }
@@ -268,7 +273,10 @@ __device__ __forceinline__ bool task_mean_active(const KParams &p, int t) {
   return a != 0;
 }
 
-// Um[t][n][c] = Σ_d Φ_t[n][d] · Dm[t][c][d]; grid (ceil(N/128), T_loc); thread = row n, half the clusters
+// The mean-column kernels run on a second stream beside the probe SGEMMs (run_simt_cg): 128 threads
+// and ≤ 80 registers, so that a CTA fits on an SM next to a probe-SGEMM CTA (1 per SM, 210 registers ×
+// 256 threads) and streams Φ from HBM while that CTA's FMAs run.
+// Um[t][n][c] = Σ_d Φ_t[n][d] · Dm[t][c][d]; grid (ceil(N/128), T_loc); thread = row n, all clusters
 __global__ void __launch_bounds__(MTH) k_simt_mean1(KParams p, int u) {
   __shared__ __align__(16) float As[MBK][SBM + 1];
   __shared__ double Bm[MBK][MAXC];
@@ -278,99 +286,97 @@ __global__ void __launch_bounds__(MTH) k_simt_mean1(KParams p, int u) {
   if (!task_mean_active(p, t)) return;
   const float *__restrict__ phi = p.phi + (size_t)t * d.phi_task_stride;
   const double *__restrict__ dm = p.b.Dm + (size_t)t * d.C * d.D;
-  const int r = tid & (SBM - 1), h = tid >> 7;
-  double acc[MAXC / 2];
+  double acc[MAXC];
 #pragma unroll
-  for (int i = 0; i < MAXC / 2; ++i) acc[i] = 0.0;
+  for (int c = 0; c < MAXC; ++c) acc[c] = 0.0;
   for (int k0 = 0; k0 < d.D; k0 += MBK) {
     __syncthreads();
 #pragma unroll
-    for (int i = 0; i < 2; ++i) {   // 128 rows × 16 k, transposed into As[k][row]
+    for (int i = 0; i < 4; ++i) {   // 128 rows × 16 k, transposed into As[k][row]
       const int idx = tid + i * MTH, row = idx >> 2, kq = (idx & 3) * 4;
       const int n = n0 + row, k = k0 + kq;
       const float4 v = (n < d.N && k < d.D) ? ldcs4(phi + (size_t)n * d.D + k) : make_float4(0.f, 0.f, 0.f, 0.f);
       As[kq][row] = v.x; As[kq + 1][row] = v.y; As[kq + 2][row] = v.z; As[kq + 3][row] = v.w;
     }
-    if (tid < MBK * d.C) {
-      const int c = tid / MBK, kk = tid % MBK;
+    for (int e = tid; e < MBK * d.C; e += MTH) {
+      const int c = e / MBK, kk = e % MBK;
       Bm[kk][c] = (k0 + kk < d.D) ? dm[(size_t)c * d.D + k0 + kk] : 0.0;
     }
     __syncthreads();
 #pragma unroll 4
     for (int kk = 0; kk < MBK; ++kk) {
-      const double a = (double)As[kk][r];
+      const double a = (double)As[kk][tid];
 #pragma unroll
-      for (int i = 0; i < MAXC / 2; ++i)
-        if (h + 2 * i < d.C) acc[i] = fma(a, Bm[kk][h + 2 * i], acc[i]);
+      for (int c = 0; c < MAXC; ++c)
+        if (c < d.C) acc[c] = fma(a, Bm[kk][c], acc[c]);
     }
   }
-  if (n0 + r < d.N) {
+  if (n0 + tid < d.N) {
 #pragma unroll
-    for (int i = 0; i < MAXC / 2; ++i)
-      if (h + 2 * i < d.C) p.b.Um[((size_t)t * d.N + n0 + r) * d.Cp + h + 2 * i] = acc[i];
+    for (int c = 0; c < MAXC; ++c)
+      if (c < d.C) p.b.Um[((size_t)t * d.N + n0 + tid) * d.Cp + c] = acc[c];
   }
 }
 
 // Wm[t][c][d] = β Σ_n Φ_t[n][d] · Um[t][n][c] + α_cd · Dm[t][c][d], dᵀWm partial per 128 rows of d;
-// grid (ceil(D/128), T_loc)
+// grid (ceil(D/128), T_loc); thread = row d, all clusters
 __global__ void __launch_bounds__(MTH) k_simt_mean2(KParams p, int u) {
   __shared__ __align__(16) float As[MBK][SBM];
   __shared__ double Bm[MBK][MAXC];
-  __shared__ double red[MTH / 32][MAXC / 2];
+  __shared__ double red[MTH / 32][MAXC];
   if (loop_done(p, u)) return;
   const Dims &d = p.d;
   const int t = blockIdx.y, tid = threadIdx.x, rt = blockIdx.x, d0 = rt * SBM;
   if (!task_mean_active(p, t)) return;
   const float *__restrict__ phi = p.phi + (size_t)t * d.phi_task_stride;
   const double *__restrict__ um = p.b.Um + (size_t)t * d.N * d.Cp;
-  const int r = tid & (SBM - 1), h = tid >> 7;
-  double acc[MAXC / 2];
+  double acc[MAXC];
 #pragma unroll
-  for (int i = 0; i < MAXC / 2; ++i) acc[i] = 0.0;
+  for (int c = 0; c < MAXC; ++c) acc[c] = 0.0;
   for (int k0 = 0; k0 < d.N; k0 += MBK) {
     __syncthreads();
 #pragma unroll
-    for (int i = 0; i < 2; ++i) {   // 16 rows of Φ × 128 columns (d): coalesced
+    for (int i = 0; i < 4; ++i) {   // 16 rows of Φ × 128 columns (d): coalesced
       const int idx = tid + i * MTH, kr = idx >> 5, dq = (idx & 31) * 4;
       const int n = k0 + kr, dd = d0 + dq;
       *reinterpret_cast<float4 *>(&As[kr][dq]) =
           (n < d.N && dd < d.D) ? ldcs4(phi + (size_t)n * d.D + dd) : make_float4(0.f, 0.f, 0.f, 0.f);
     }
-    if (tid < MBK * d.C) {
-      const int kk = tid / d.C, c = tid % d.C;
+    for (int e = tid; e < MBK * d.C; e += MTH) {
+      const int kk = e / d.C, c = e % d.C;
       Bm[kk][c] = (k0 + kk < d.N) ? um[(size_t)(k0 + kk) * d.Cp + c] : 0.0;
     }
     __syncthreads();
 #pragma unroll 4
     for (int kk = 0; kk < MBK; ++kk) {
-      const double a = (double)As[kk][r];
+      const double a = (double)As[kk][tid];
 #pragma unroll
-      for (int i = 0; i < MAXC / 2; ++i)
-        if (h + 2 * i < d.C) acc[i] = fma(a, Bm[kk][h + 2 * i], acc[i]);
+      for (int c = 0; c < MAXC; ++c)
+        if (c < d.C) acc[c] = fma(a, Bm[kk][c], acc[c]);
     }
   }
-  const int dd = d0 + r;
+  const int dd = d0 + tid;
   const int warp = tid >> 5, lane = tid & 31;
 #pragma unroll
-  for (int i = 0; i < MAXC / 2; ++i) {
-    const int c = h + 2 * i;
+  for (int c = 0; c < MAXC; ++c) {
+    if (c >= d.C) break;
     double v = 0.0;
-    if (c < d.C && dd < d.D) {
+    if (dd < d.D) {
       const size_t o = ((size_t)t * d.C + c) * d.D + dd;
       const double dv = p.b.Dm[o];
-      const double w = fma(p.beta, acc[i], p.b.alpha64[(size_t)c * d.D + dd] * dv);
+      const double w = fma(p.beta, acc[c], p.b.alpha64[(size_t)c * d.D + dd] * dv);
       p.b.Wm[o] = w;
       v = dv * w;
     }
     v = warp_sum_d(v);
-    if (lane == 0) red[warp][i] = v;
+    if (lane == 0) red[warp][c] = v;
   }
   __syncthreads();
-  if (tid < d.C) {   // cluster c = h + 2i lives in warps 4h .. 4h+3
-    const int c = tid, hh = c & 1, i = c >> 1;
+  if (tid < d.C) {
     double s = 0.0;
-    for (int w = 0; w < 4; ++w) s += red[4 * hh + w][i];
-    p.b.dAdm[((size_t)t * d.C + c) * d.nRT2 + rt] = s;
+#pragma unroll
+    for (int w = 0; w < MTH / 32; ++w) s += red[w][tid];
+    p.b.dAdm[((size_t)t * d.C + tid) * d.nRT2 + rt] = s;
   }
 }
 
@@ -383,66 +389,118 @@ __device__ void report_simt(int *status, int code, int t, int col, int u) {
   }
 }
 
-__device__ void simt_update_probe(const KParams &p, int t, int col, int u, int lane) {
+// Probe columns, d-major: a CTA updates 32 consecutive columns g = 32·blockIdx.x + lane (one lane per
+// column, every global access a 128-byte row segment); its 8 warps split the D rows, per-column sums
+// are reduced over the warps in fixed order.  Alg. 1 lines 3-7 with fp64 γ_u, ξ_u applied in fp64.
+__device__ void simt_update_probes(const KParams &p, int u) {
+  __shared__ double sred[8][32];
+  __shared__ double sgam[32];
+  __shared__ int sact[32];
   const Dims &d = p.d;
-  const size_t g = (size_t)t * d.P + col;
-  double dpart = 0.0;
-  for (int i = lane; i < d.nRT2; i += 32) dpart += p.b.dAd[g * d.nRT2 + i];
-  const double dAd = warp_sum_d(dpart);
-  const double rr = p.b.rr[g];
-  if (!(dAd > 0.0)) {  // Alg. 1 line 3 breakdown
-    if (lane == 0) {
-      report_simt(p.b.status, ST_BREAKDOWN, d.t0 + t, col, u + 1);
-      p.b.flag[g] = 0;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = blockIdx.x * 32 + lane;
+  const int t = g / d.Pp, j = g % d.Pp;
+  const bool col = t < d.Tl && j < d.P;
+  const size_t gi = (size_t)t * d.P + j;     // per-column state index
+  const bool active = col && p.b.flag[gi] == 1;
+  if (!__syncthreads_or(active)) return;
+  // dᵀAd: the nRT2 row-tile partials, split over the warps
+  double dp = 0.0;
+  if (active)
+    for (int i = warp; i < d.nRT2; i += 8) dp += p.b.dAd[gi * d.nRT2 + i];
+  sred[warp][lane] = dp;
+  __syncthreads();
+  if (warp == 0) {
+    double dAd = 0.0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) dAd += sred[w][lane];
+    int act = active;
+    if (active) {
+      atomicAdd(p.b.hist + u, 1);
+      if (atomicMax(p.b.tmark + t, u + 1) < u + 1) atomicAdd(p.b.histt + u, 1);   // tasks active at step u
+      if (!(dAd > 0.0)) {  // Alg. 1 line 3 breakdown
+        report_simt(p.b.status, ST_BREAKDOWN, d.t0 + t, j, u + 1);
+        p.b.flag[gi] = 0;
+        act = 0;
+      }
     }
-    return;
+    sact[lane] = act;
+    sgam[lane] = act ? p.b.rr[gi] / dAd : 0.0;
   }
-  const double gam = rr / dAd;
-  float4 *__restrict__ x4 = reinterpret_cast<float4 *>(p.b.X + g * d.D);
-  float4 *__restrict__ r4 = reinterpret_cast<float4 *>(p.b.R + g * d.D);
-  float4 *__restrict__ d4 = reinterpret_cast<float4 *>(p.b.D32 + g * d.D);
-  const float4 *__restrict__ w4 = reinterpret_cast<const float4 *>(p.b.W + g * d.D);
-  const int n4 = d.D >> 2;
+  __syncthreads();
+  const bool go = sact[lane] != 0;
+  const double gam = sgam[lane];
+  const size_t ldv = (size_t)d.ldv;
   double acc = 0.0;
-  for (int i = lane; i < n4; i += 32) {
-    const float4 dv = d4[i], wv = w4[i];
-    float4 x = x4[i], r = r4[i];
-    x.x = (float)fma(gam, (double)dv.x, (double)x.x);
-    x.y = (float)fma(gam, (double)dv.y, (double)x.y);
-    x.z = (float)fma(gam, (double)dv.z, (double)x.z);
-    x.w = (float)fma(gam, (double)dv.w, (double)x.w);
-    r.x = (float)fma(-gam, (double)wv.x, (double)r.x);
-    r.y = (float)fma(-gam, (double)wv.y, (double)r.y);
-    r.z = (float)fma(-gam, (double)wv.z, (double)r.z);
-    r.w = (float)fma(-gam, (double)wv.w, (double)r.w);
-    x4[i] = x;
-    r4[i] = r;
-    acc = fma((double)r.x, (double)r.x, acc);
-    acc = fma((double)r.y, (double)r.y, acc);
-    acc = fma((double)r.z, (double)r.z, acc);
-    acc = fma((double)r.w, (double)r.w, acc);
+  if (go) {
+    // 4 rows per iteration: 16 independent 128-byte loads in flight per warp
+    for (int i0 = warp; i0 < d.D; i0 += 32) {
+      float dv[4], xv[4], wv[4], rv[4];
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        const int i = i0 + 8 * v;
+        if (i < d.D) {
+          const size_t o = (size_t)i * ldv + g;
+          dv[v] = p.b.D32[o]; xv[v] = p.b.X[o]; wv[v] = p.b.W[o]; rv[v] = p.b.R[o];
+        }
+      }
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        const int i = i0 + 8 * v;
+        if (i < d.D) {
+          const size_t o = (size_t)i * ldv + g;
+          const float x = (float)fma(gam, (double)dv[v], (double)xv[v]);
+          const float r = (float)fma(-gam, (double)wv[v], (double)rv[v]);
+          p.b.X[o] = x;
+          p.b.R[o] = r;
+          acc = fma((double)r, (double)r, acc);
+        }
+      }
+    }
   }
-  const double rrn = warp_sum_d(acc);
-  const double xi = rrn / rr;
-  const bool conv = sqrt(rrn) <= p.tol * sqrt((double)d.D);   // ‖b‖ = ‖p‖ = √D (A5)
-  const bool stop = conv || (u + 1 >= d.cap);
-  if (lane == 0) {
-    p.b.gam[g * d.cap + u] = gam;
-    p.b.xi[g * d.cap + u] = xi;
-    p.b.steps[g] = u + 1;
-    p.b.rr[g] = rrn;
-    if (stop) p.b.flag[g] = conv ? 0 : 2;
-    else atomicAdd(p.b.alive + u, 1);
+  __syncthreads();                              // sred reuse
+  sred[warp][lane] = acc;
+  __syncthreads();
+  if (warp == 0) {
+    double rrn = 0.0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) rrn += sred[w][lane];
+    double xi = 0.0;
+    int cont = 0;
+    if (go) {
+      const double rr = p.b.rr[gi];
+      xi = rrn / rr;
+      const bool conv = sqrt(rrn) <= p.tol * sqrt((double)d.D);   // ‖b‖ = ‖p‖ = √D (A5)
+      const bool stop = conv || (u + 1 >= d.cap);
+      p.b.gam[gi * d.cap + u] = gam;
+      p.b.xi[gi * d.cap + u] = xi;
+      p.b.steps[gi] = u + 1;
+      p.b.rr[gi] = rrn;
+      if (stop) p.b.flag[gi] = conv ? 0 : 2;
+      else atomicAdd(p.b.alive + u, 1);
+      cont = !stop;
+    }
+    sact[lane] = cont;
+    sgam[lane] = xi;
   }
-  if (!stop) {
-    for (int i = lane; i < n4; i += 32) {   // this lane's own stores of r: no sync needed
-      const float4 r = r4[i];
-      float4 dv = d4[i];
-      dv.x = (float)fma(xi, (double)dv.x, (double)r.x);
-      dv.y = (float)fma(xi, (double)dv.y, (double)r.y);
-      dv.z = (float)fma(xi, (double)dv.z, (double)r.z);
-      dv.w = (float)fma(xi, (double)dv.w, (double)r.w);
-      d4[i] = dv;
+  __syncthreads();
+  if (sact[lane]) {
+    const double xi = sgam[lane];
+    for (int i0 = warp; i0 < d.D; i0 += 32) {
+      float dv[4], rv[4];
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        const int i = i0 + 8 * v;
+        if (i < d.D) {
+          const size_t o = (size_t)i * ldv + g;
+          dv[v] = p.b.D32[o]; rv[v] = p.b.R[o];
+        }
+      }
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        const int i = i0 + 8 * v;
+        if (i < d.D) p.b.D32[(size_t)i * ldv + g] = (float)fma(xi, (double)dv[v], (double)rv[v]);
+      }
     }
   }
 }
@@ -501,22 +559,25 @@ __device__ void simt_update_mean(const KParams &p, int t, int c, int u, int lane
   }
 }
 
-__global__ void __launch_bounds__(256) k_simt_update(KParams p, int u) {
+// blocks [0, nbp): probe column groups (simt_update_probes); then 8 mean columns per block (a warp each)
+__global__ void __launch_bounds__(256) k_simt_update(KParams p, int u, int nbp) {
   if (loop_done(p, u)) return;
   const Dims &d = p.d;
-  const int lane = threadIdx.x & 31;
-  const int w = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
   if (blockIdx.x == 0 && threadIdx.x == 0) *p.b.u = u + 1;   // CG steps executed
-  if (w >= d.Tl * (d.P + d.C)) return;
-  const int t = w / (d.P + d.C), j = w % (d.P + d.C);
-  const bool active = j < d.P ? p.b.flag[(size_t)t * d.P + j] == 1 : p.b.flagm[(size_t)t * d.C + (j - d.P)] == 1;
-  if (!active) return;
-  if (lane == 0) {
-    if (atomicMax(p.b.tmark + t, u + 1) < u + 1) atomicAdd(p.b.histt + u, 1);   // tasks active at step u
-    atomicAdd(j < d.P ? p.b.hist + u : p.b.histm + u, 1);
+  if ((int)blockIdx.x < nbp) {
+    simt_update_probes(p, u);
+    return;
   }
-  if (j < d.P) simt_update_probe(p, t, j, u, lane);
-  else simt_update_mean(p, t, j - d.P, u, lane);
+  const int lane = threadIdx.x & 31;
+  const int w = (blockIdx.x - nbp) * (blockDim.x / 32) + (threadIdx.x >> 5);
+  if (w >= d.Tl * d.C) return;
+  const int t = w / d.C, c = w % d.C;
+  if (p.b.flagm[(size_t)t * d.C + c] != 1) return;
+  if (lane == 0) {
+    if (atomicMax(p.b.tmark + t, u + 1) < u + 1) atomicAdd(p.b.histt + u, 1);
+    atomicAdd(p.b.histm + u, 1);
+  }
+  simt_update_mean(p, t, c, u, lane);
 }
 
 }  // namespace
@@ -525,26 +586,24 @@ __global__ void __launch_bounds__(256) k_simt_update(KParams p, int u) {
 // SimtTiming::B steps (alive[u] read back through pinned memory); the kernels of steps past the last
 // one return at once.  *launches counts the kernels launched; with `tm` the operator (stage 1 → the
 // end of stage 2, mean kernels included) and update durations are accumulated from CUDA events.
-cudaError_t run_simt_cg(const KParams &p, int *h_alive, int64_t *launches, SimtTiming *tm, cudaStream_t s) {
+cudaError_t run_simt_cg(const KParams &p, int *h_alive, int64_t *launches, SimtTiming *tm, const SimtStreams &ss,
+                        cudaStream_t s) {
   const Dims &d = p.d;
-  const dim3 g1((d.P + SBN - 1) / SBN, (d.N + SBM - 1) / SBM, d.Tl);
-  const dim3 g2((d.P + SBN - 1) / SBN, (d.D + SBM - 1) / SBM, d.Tl);
+  const int pflat = d.shared_phi && d.P % 4 == 0 ? d.Tl * d.P : 0;   // Pp == P: U rows contiguous too
+  const int gx = ((pflat ? pflat : d.P) + SBN - 1) / SBN, gz = pflat ? 1 : d.Tl;
+  const dim3 g1(gx, (d.N + SBM - 1) / SBM, gz);
+  const dim3 g2(gx, (d.D + SBM - 1) / SBM, gz);
   const dim3 gm1((d.N + SBM - 1) / SBM, d.Tl), gm2((d.D + SBM - 1) / SBM, d.Tl);
-  const int gu = (d.Tl * (d.P + d.C) + 7) / 8;
+  const int nbp = (d.ldv + 31) / 32, gu = nbp + (d.Tl * d.C + 7) / 8;
   constexpr int B = SimtTiming::B;
   cudaError_t e = cudaSuccess;
-  static int var = -1;   // dynamic shared memory above 48 KB (one process per GPU); CMTCS_SIMT_VAR experiments
-  if (var < 0) {
-    var = getenv("CMTCS_SIMT_VAR") ? atoi(getenv("CMTCS_SIMT_VAR")) : 0;
-    if (var < 0 || var > 2) var = 0;
+  static bool configured = false;   // dynamic shared memory above 48 KB (one process per GPU)
+  if (!configured) {
     const int sb = (int)sizeof(SimtSmem);
-    e = cudaFuncSetAttribute(k_simt_probe<1, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, sb);
-    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_simt_probe<2, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, sb);
-    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_simt_probe<1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, sb);
-    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_simt_probe<2, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, sb);
-    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_simt_probe<1, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, sb);
-    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_simt_probe<2, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, sb);
+    e = cudaFuncSetAttribute(k_simt_probe<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, sb);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_simt_probe<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, sb);
     if (e != cudaSuccess) return e;
+    configured = true;
   }
   e = cudaMemsetAsync(p.b.u, 0, sizeof(int), s);
   if (e != cudaSuccess) return e;
@@ -563,16 +622,17 @@ cudaError_t run_simt_cg(const KParams &p, int *h_alive, int64_t *launches, SimtT
   for (int u = 0; u < d.cap; ++u) {
     const int slot = u % B;
     if (tm) cudaEventRecord(tm->ev[3 * slot], s);
-    if (var == 0) k_simt_probe<1, 0><<<g1, STH, sizeof(SimtSmem), s>>>(p, u);
-    else if (var == 1) k_simt_probe<1, 1><<<g1, STH, sizeof(SimtSmem), s>>>(p, u);
-    else k_simt_probe<1, 2><<<g1, STH, sizeof(SimtSmem), s>>>(p, u);
-    k_simt_mean1<<<gm1, MTH, 0, s>>>(p, u);
-    if (var == 0) k_simt_probe<2, 0><<<g2, STH, sizeof(SimtSmem), s>>>(p, u);
-    else if (var == 1) k_simt_probe<2, 1><<<g2, STH, sizeof(SimtSmem), s>>>(p, u);
-    else k_simt_probe<2, 2><<<g2, STH, sizeof(SimtSmem), s>>>(p, u);
-    k_simt_mean2<<<gm2, MTH, 0, s>>>(p, u);
+    // fork: the mean columns (fp64, HBM-bound) on the side stream, the probe SGEMMs (FMA-bound) here
+    cudaEventRecord(ss.fork, s);
+    cudaStreamWaitEvent(ss.side, ss.fork, 0);
+    k_simt_mean1<<<gm1, MTH, 0, ss.side>>>(p, u);
+    k_simt_mean2<<<gm2, MTH, 0, ss.side>>>(p, u);
+    cudaEventRecord(ss.join, ss.side);
+    k_simt_probe<1><<<g1, STH, sizeof(SimtSmem), s>>>(p, u, pflat);
+    k_simt_probe<2><<<g2, STH, sizeof(SimtSmem), s>>>(p, u, pflat);
+    cudaStreamWaitEvent(s, ss.join, 0);
     if (tm) cudaEventRecord(tm->ev[3 * slot + 1], s);
-    k_simt_update<<<gu, 256, 0, s>>>(p, u);
+    k_simt_update<<<gu, 256, 0, s>>>(p, u, nbp);
     if (tm) cudaEventRecord(tm->ev[3 * slot + 2], s);
     *launches += 5;
     ++pending;

@@ -18,9 +18,10 @@ class CoFEM:
     Tasks of this rank are global tasks task_begin .. task_begin + T_loc - 1 of T.
     Partial-Fourier sensing (the paper's §4 workload): phi=None, fourier_rows = cuda
     int32 [T_loc, N] sampled DFT rows, y = cuda fp32 [T_loc, 2N] (real parts, then imaginary), D given.
-    engine (dense Φ only): "tensor" — the operator on the tcgen05 tensor cores (3xTF32, persistent
-    kernel); "fp32" — on the FP32 CUDA cores (round-to-nearest accumulation, CMTCS_OP_DENSE_FP32), the
-    path that meets the north_star's |ΔL| ≤ 1e-3 at configs 4-5.
+    engine (dense Φ only): "fp32" (default) — the operator on the FP32 CUDA cores (round-to-nearest
+    accumulation, CMTCS_OP_DENSE_FP32), the path that meets every north_star tolerance (DESIGN.md §3
+    reading E1, §6); "tensor" — on the tcgen05 tensor cores (3xTF32, one persistent kernel), 2-3x
+    faster, |ΔL| above 1e-3 at configs 4-5.
     """
 
     def __init__(self, phi: torch.Tensor, y: torch.Tensor, *, T: int, C: int, K: int, beta: float,
@@ -29,7 +30,7 @@ class CoFEM:
                  alpha_max: float = 1e12, var_floor: float = 1e-12, empty_eps: float = 1e-10,
                  mean_rel_tol: float = -1.0,
                  nccl_uid: bytes | None = None, rank: int = 0, world: int = 1, stream=None,
-                 fourier_rows: torch.Tensor | None = None, D: int | None = None, engine: str = "tensor"):
+                 fourier_rows: torch.Tensor | None = None, D: int | None = None, engine: str = "fp32"):
         fourier = fourier_rows is not None
         if engine not in ("tensor", "fp32"):
             raise ValueError(f"engine must be 'tensor' or 'fp32', got {engine!r}")

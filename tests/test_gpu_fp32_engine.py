@@ -108,9 +108,13 @@ def test_single_step_config2(torch_cuda):
     assert errq <= A_TOL
 
 
-def test_shared_phi_equals_replicated(torch_cuda):
-    """One Φ shared by all tasks (the config-5 layout) gives the same result as T copies of it."""
-    data = synthetic.small_problem(T=3, C=2, N=40, D=96, K=4, seed=18)
+@pytest.mark.parametrize("T,C,K", [(3, 2, 4), (3, 3, 3), (4, 4, 33)])
+def test_shared_phi_equals_replicated(torch_cuda, T, C, K):
+    """One Φ shared by all tasks (the config-5 layout) gives the same result as T copies of it —
+    bit for bit: with P = C·K a multiple of 4 the shared-Φ operator runs all tasks' columns as one
+    flattened GEMM (column tiles straddle tasks; (4, 33): P = 132, tiles of 128 + ragged), otherwise
+    per task (P = 9)."""
+    data = synthetic.small_problem(T=T, C=C, N=40, D=96, K=K, seed=18)
     data["phi"][1:] = data["phi"][0]
     a = make_gpu(data, cap=300, engine="fp32")
     a.em_step(2)

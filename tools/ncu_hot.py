@@ -13,8 +13,25 @@ raw = subprocess.run(["ncu", "-i", path, "--page", "source", "--csv", "--print-s
 rows = list(csv.reader(io.StringIO(raw)))
 hdr_i = next(i for i, r in enumerate(rows) if r and r[0] in ("Address", "Line", "#"))
 hdr = rows[hdr_i]
-data = [r for r in rows[hdr_i + 1:] if len(r) == len(hdr)]
 si = hdr.index("Warp Stall Sampling (All Samples)")
+
+
+def _num(x):
+    try:
+        float(x or 0)
+        return True
+    except ValueError:
+        return False
+
+
+# a report with several kernels prints one table per kernel: keep the first kernel's rows
+data = []
+for r in rows[hdr_i + 1:]:
+    if len(r) != len(hdr):
+        continue
+    if not _num(r[si]):
+        break
+    data.append(r)
 stall_cols = [i for i, h in enumerate(hdr) if h.startswith("stall_") and "Not Issued" not in h]
 tot = sum(float(r[si] or 0) for r in data)
 data.sort(key=lambda r: -float(r[si] or 0))
