@@ -46,11 +46,12 @@ def test_breakdown_reports_task_column_step(torch_cuda):
     g.close()
 
 
-def test_nonfinite_measurements_give_enumeric(torch_cuda):
+@pytest.mark.parametrize("engine", ["tensor", "fp32"])
+def test_nonfinite_measurements_give_enumeric(torch_cuda, engine):
     from paper_2310_00420_b200 import CmtcsError
     data = synthetic.small_problem(T=2, C=2, N=16, D=32, K=3, seed=22)
     data["y"][0, 3] = np.nan
-    g = make_gpu(data, cap=50)
+    g = make_gpu(data, cap=50, engine=engine)
     with pytest.raises(CmtcsError, match="ENUMERIC") as ei:
         g.em_step(1)
     assert ei.value.status == 7 and "task 0" in str(ei.value)

@@ -36,11 +36,13 @@ def torch_cuda():
 SAMPLES = [(3, [0, 41], None), (4, [0], [0, 5]), (5, [7], [3])]
 
 
+@pytest.mark.parametrize("engine", ["fp32", "tensor"])
 @pytest.mark.parametrize("cid,tasks,clusters", SAMPLES)
-def test_full_size_sampled_blocks(torch_cuda, cid, tasks, clusters):
+def test_full_size_sampled_blocks(torch_cuda, cid, tasks, clusters, engine):
+    """Both dense engines; the FP32 one is bench.py's default (reading E1)."""
     cfg = synthetic.CONFIGS[cid]
     data = synthetic.generate(cfg)
-    g = make_gpu(data, mean_tol=MEAN_TOL)
+    g = make_gpu(data, mean_tol=MEAN_TOL, engine=engine)
     info = g.em_step(1)
     post = to_np(g.posterior())
     steps = g.transcript()["steps"].cpu().numpy().reshape(cfg.T, cfg.C, cfg.K)
@@ -66,7 +68,7 @@ def test_full_size_sampled_blocks(torch_cuda, cid, tasks, clusters):
         conv = np.all(steps[t, cl] < cfg.cg_cap, axis=-1) & np.all(
             np.asarray(o["probe_steps"]).reshape(len(cl), cfg.K) < cfg.cg_cap, axis=-1)
         nu_err = np.abs(post["logdet"][t, cl] - o["nu"])
-        print(f"C{cid} task {t} clusters {cl}: mu {mu_err.max():.2e} s {s_err.max():.2e} "
+        print(f"C{cid} [{engine}] task {t} clusters {cl}: mu {mu_err.max():.2e} s {s_err.max():.2e} "
               f"nu {nu_err.max():.2e} (|nu| {np.abs(o['nu']).max():.3g}) converged {conv.sum()}/{conv.size}")
         assert mu_err.max() <= MU_TOL
         assert conv.any() and s_err[conv].max() <= S_TOL

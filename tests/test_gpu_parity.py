@@ -19,6 +19,7 @@ from gpu_common import compare_step, make_gpu, oracle_state, rel_inf, to_np
 pytestmark = pytest.mark.gpu
 
 MU_TOL, S_TOL, Q_TOL, A_TOL, L_TOL = 1e-4, 1e-4, 1e-3, 1e-4, 1e-3
+ENGINES = ["tensor", "fp32"]   # the two dense operator engines (op_kind, DESIGN.md §3 reading E1)
 
 
 def nu_tol(nu):
@@ -223,16 +224,17 @@ def test_q_conditioned_alpha(torch_cuda, it):
     assert err <= A_TOL
 
 
-def test_probe_override_matches_hash(torch_cuda):
+@pytest.mark.parametrize("engine", ENGINES)
+def test_probe_override_matches_hash(torch_cuda, engine):
     from paper_2310_00420_b200 import probe_words
     cfg = synthetic.CONFIGS[1]
     data = synthetic.generate(cfg)
-    a = make_gpu(data, em_iter0=2)
+    a = make_gpu(data, em_iter0=2, engine=engine)
     a.em_step(1)
     pa = to_np(a.posterior())
     a.close()
     words = probe_words(cfg.probe_seed, 2, cfg.T, 0, cfg.T, cfg.C, cfg.K, cfg.D)
-    b = make_gpu(data, em_iter0=2)
+    b = make_gpu(data, em_iter0=2, engine=engine)
     b.em_step(1, probe_bits=words)
     pb = to_np(b.posterior())
     b.close()
@@ -240,7 +242,8 @@ def test_probe_override_matches_hash(torch_cuda):
         np.testing.assert_array_equal(pa[k], pb[k])
 
 
-def test_oracle_probes_injected(torch_cuda):
+@pytest.mark.parametrize("engine", ENGINES)
+def test_oracle_probes_injected(torch_cuda, engine):
     """probe_bits carries the ORACLE's probes (another seed) into the GPU step."""
     import torch
     cfg = synthetic.CONFIGS[1]
@@ -250,7 +253,7 @@ def test_oracle_probes_injected(torch_cuda):
     words = np.stack([[[O.probe_word(seed2, ((((it * cfg.T + t) * cfg.C + c) * cfg.K + k) * nw)
                                      + np.arange(nw, dtype=np.uint64))
                         for k in range(cfg.K)] for c in range(cfg.C)] for t in range(cfg.T)])
-    g = make_gpu(data, cap=256)
+    g = make_gpu(data, cap=256, engine=engine)
     g.em_step(1, probe_bits=torch.tensor(words.view(np.int64)).cuda())
     post = to_np(g.posterior())
     g.close()
@@ -260,9 +263,10 @@ def test_oracle_probes_injected(torch_cuda):
 
 
 # ------------------------------------------------------------------------------ edge cases --
-def test_single_cluster_and_single_probe(torch_cuda):
+@pytest.mark.parametrize("engine", ENGINES)
+def test_single_cluster_and_single_probe(torch_cuda, engine):
     data = synthetic.small_problem(T=2, C=1, N=16, D=40, K=1, seed=13)
-    g = make_gpu(data, K=1, cap=200, tol=1e-8)
+    g = make_gpu(data, K=1, cap=200, tol=1e-8, engine=engine)
     g.em_step(1)
     post = to_np(g.posterior())
     g.close()
@@ -272,10 +276,11 @@ def test_single_cluster_and_single_probe(torch_cuda):
     assert np.max(rel_inf(post["s"], orc["s"])) <= S_TOL
 
 
-def test_zero_measurements_give_zero_mean(torch_cuda):
+@pytest.mark.parametrize("engine", ENGINES)
+def test_zero_measurements_give_zero_mean(torch_cuda, engine):
     data = synthetic.small_problem(T=2, C=2, N=16, D=32, K=3, seed=14)
     data["y"][0] = 0.0
-    g = make_gpu(data, cap=100)
+    g = make_gpu(data, cap=100, engine=engine)
     g.em_step(1)
     post = to_np(g.posterior())
     tr = g.transcript()
@@ -284,11 +289,12 @@ def test_zero_measurements_give_zero_mean(torch_cuda):
     assert np.all(tr["mu_steps"].cpu().numpy().reshape(2, 2)[0] == 0)
 
 
-def test_cap_one_and_tol_zero(torch_cuda):
+@pytest.mark.parametrize("engine", ENGINES)
+def test_cap_one_and_tol_zero(torch_cuda, engine):
     """cap = 1: every column takes exactly one step; tol = 0: no early stop before the cap."""
     data = synthetic.small_problem(T=2, C=2, N=16, D=32, K=3, seed=15)
     for cap, tol in [(1, 1e-6), (7, 0.0)]:
-        g = make_gpu(data, cap=cap, tol=tol)
+        g = make_gpu(data, cap=cap, tol=tol, engine=engine)
         info = g.em_step(1)
         post = to_np(g.posterior())
         g.close()
@@ -299,12 +305,13 @@ def test_cap_one_and_tol_zero(torch_cuda):
         assert np.all(np.abs(post["logdet"] - orc["nu"]) <= nu_tol(orc["nu"]))
 
 
-def test_prior_only_tasks_exact(torch_cuda):
+@pytest.mark.parametrize("engine", ENGINES)
+def test_prior_only_tasks_exact(torch_cuda, engine):
     """Φ = 0 ⇒ s = 1/α and ν̄ = −Σ log α exactly (A diagonal)."""
     data = synthetic.small_problem(T=2, C=2, N=8, D=32, K=4, seed=16)
     data["phi"][:] = 0.0
     alpha = np.stack([np.repeat([0.5, 2.0], 16), np.repeat([1.5, 4.0], 16)])
-    g = make_gpu(data, alpha=alpha, cap=50, tol=1e-12)
+    g = make_gpu(data, alpha=alpha, cap=50, tol=1e-12, engine=engine)
     g.em_step(1)
     post = to_np(g.posterior())
     g.close()
@@ -422,13 +429,14 @@ def test_single_step_config2(torch_cuda):
     assert errq <= A_TOL
 
 
-def test_task_shards_match_whole(torch_cuda):
+@pytest.mark.parametrize("engine", ENGINES)
+def test_task_shards_match_whole(torch_cuda, engine):
     """Two contexts holding tasks [0, 2) and [2, 4) of config 1 (the per-rank view of a 2-GPU run,
     here on one GPU without NCCL) produce the same E-step as one context holding all 4 tasks."""
     cfg = synthetic.CONFIGS[1]
     data = synthetic.generate(cfg)
     alpha = np.random.default_rng(4).uniform(0.5, 2.0, (cfg.C, cfg.D))
-    whole = make_gpu(data, alpha=alpha, em_iter0=5, cap=256)
+    whole = make_gpu(data, alpha=alpha, em_iter0=5, cap=256, engine=engine)
     whole.em_step(1)
     pw = to_np(whole.posterior())
     sums_w = whole.estep_sums().cpu().numpy()
@@ -437,7 +445,7 @@ def test_task_shards_match_whole(torch_cuda):
     sums = []
     for b, e in [(0, 2), (2, 4)]:
         part = synthetic.generate(cfg, range(b, e))
-        g = make_gpu(part, alpha=alpha, em_iter0=5, cap=256, T=cfg.T, task_begin=b)
+        g = make_gpu(part, alpha=alpha, em_iter0=5, cap=256, T=cfg.T, task_begin=b, engine=engine)
         g.em_step(1)
         pp = to_np(g.posterior())
         sums.append(g.estep_sums().cpu().numpy())
