@@ -35,8 +35,8 @@ constexpr int SBM = 128;               // output rows per CTA (n in stage 1, d i
 constexpr int SBN = 128;               // probe columns per CTA
 constexpr int SLD = SBM + 4;           // padded smem row (16-byte aligned rows)
 constexpr int STH = 256;
-constexpr int MTH = 128;               // mean-column kernels (co-resident with a probe-SGEMM CTA)
 constexpr int MBK = 16;
+constexpr int MTH = 128;               // mean-column kernels (co-resident with a probe-SGEMM CTA)
 
 __device__ __forceinline__ float4 ldg4(const float *p) { return __ldg(reinterpret_cast<const float4 *>(p)); }
 __device__ __forceinline__ float4 ldcs4(const float *p) { return __ldcs(reinterpret_cast<const float4 *>(p)); }
@@ -69,12 +69,25 @@ __device__ __forceinline__ double warp_sum_d(double v) {
 // partial sums; each 64-long block of the contraction is summed in fp32 and the block sums are added
 // (round to nearest) into a second accumulator, ~ε·(√64 + √(K/64)).
 //
+// (Measured alternatives, C4 32 tasks, ms per EM iteration: this form 1462; 512 threads with 4 × 8
+// outputs each, ≤ 128 registers, 4 warps per scheduler: 1614.)
+//
 // pflat > 0 (shared Φ, P % 4 == 0): the columns of all tasks form one GEMM of pflat = T_loc·P columns
 // (one A for everyone), so a task's last partial column tile is not padded — config 5's P = 320
 // would otherwise multiply 384 columns per task.
-constexpr int KBK = 32;                    // k per slab
-constexpr int KST = 4;                     // ring stages
-constexpr int FLUSH = 64 / KBK;            // slabs per block sum
+// SMT = true (default): 16-k slabs, 2 stages, the block-sum totals in shared memory (thread-private
+// float4 slots, conflict-free), ≤ 128 registers and 106 KB: 2 CTAs per SM, so one CTA's barrier,
+// prologue and epilogue overlap the other's FMAs; SMT = false (CMTCS_SIMT_SMT=0): 32-k slabs, 4
+// stages, the totals in registers (210 registers: 1 CTA per SM)
+template <bool SMT>
+struct PCfg {
+  static constexpr int KBK = SMT ? 16 : 32;  // k per slab
+  static constexpr int KST = SMT ? 2 : 4;    // ring stages
+  static constexpr int FLUSH = 64 / KBK;     // slabs per block sum
+  static constexpr int MINB = SMT ? 2 : 1;
+  static constexpr size_t RING = (size_t)KST * 2 * KBK * SLD * sizeof(float);
+  static constexpr size_t SMEM = RING + (SMT ? 64 * STH * sizeof(float) : 0);
+};
 
 __device__ __forceinline__ void cp_async16(uint32_t saddr, const void *gmem, bool valid) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(saddr), "l"(gmem), "r"(valid ? 16 : 0)
@@ -84,15 +97,14 @@ __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_grou
 template <int N>
 __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
 
-struct SimtSmem {
-  float a[KST][KBK * SLD];                 // A slabs [k][m]
-  float b[KST][KBK * SLD];                 // B slabs [k][g]
-};
 
-template <int STAGE>
-__global__ void __launch_bounds__(STH, 1) k_simt_probe(KParams p, int u, int pflat) {
+template <int STAGE, bool SMT>
+__global__ void __launch_bounds__(STH, PCfg<SMT>::MINB) k_simt_probe(KParams p, int u, int pflat) {
+  using CF = PCfg<SMT>;
+  constexpr int KBK = CF::KBK, KST = CF::KST, FLUSH = CF::FLUSH;
   extern __shared__ __align__(16) unsigned char simt_raw[];
-  SimtSmem &sm = *reinterpret_cast<SimtSmem *>(simt_raw);
+  float *ring = reinterpret_cast<float *>(simt_raw);   // [KST][A slab | B slab], slab [KBK][SLD]
+  float4 *tot4 = reinterpret_cast<float4 *>(simt_raw + CF::RING);   // SMT: [16][STH] block-sum totals
   __shared__ double red[STH / 32][SBN];
   if (loop_done(p, u)) return;
   const Dims &d = p.d;
@@ -111,8 +123,8 @@ __global__ void __launch_bounds__(STH, 1) k_simt_probe(KParams p, int u, int pfl
                                               : p.phi + (size_t)t * d.phi_task_stride;
   const float *__restrict__ bmat = (STAGE == 1 ? p.b.D32 : p.b.Uh) + gb;
   const size_t ldv = (size_t)d.ldv;
-  const uint32_t sa0 = (uint32_t)__cvta_generic_to_shared(&sm.a[0][0]);
-  const uint32_t sb0 = (uint32_t)__cvta_generic_to_shared(&sm.b[0][0]);
+  const uint32_t sa0 = (uint32_t)__cvta_generic_to_shared(ring);
+  const uint32_t sb0 = sa0 + 4u * (uint32_t)(KBK * SLD);
 
   // slab kt → ring slot kt % KST: KBK/8 16-byte copies per thread and operand (k row idx/32, 4
   // entries at (idx%32)·4)
@@ -121,7 +133,7 @@ __global__ void __launch_bounds__(STH, 1) k_simt_probe(KParams p, int u, int pfl
 #pragma unroll
     for (int v = 0; v < KBK / 8; ++v) {
       const int idx = tid + v * STH, kr = idx >> 5, c4 = (idx & 31) * 4, k = k0 + kr;
-      const uint32_t so = 4u * (uint32_t)(slot * KBK * SLD + kr * SLD + c4);
+      const uint32_t so = 4u * (uint32_t)(slot * 2 * KBK * SLD + kr * SLD + c4);
       const bool oka = k < KD && m0 + c4 < M;
       cp_async16(sa0 + so, oka ? amat + (size_t)k * M + m0 + c4 : amat, oka);
       const bool okb = k < KD && c4 < ncol;    // a chunk past ncol holds padding / other tasks' columns
@@ -131,11 +143,18 @@ __global__ void __launch_bounds__(STH, 1) k_simt_probe(KParams p, int u, int pfl
 
   // acc2[ip][j]: rows (2ip, 2ip+1) of this thread's 8 (ty·4 + i, i < 4; 64 + ty·4 + i − 4), column j
   // of its 8 (tx·4 + j, j < 4; 64 + tx·4 + j − 4)
-  float2 acc2[4][8], tot2[4][8];
+  float2 acc2[4][8], tot2[SMT ? 1 : 4][SMT ? 1 : 8];
 #pragma unroll
   for (int i = 0; i < 4; ++i)
 #pragma unroll
-    for (int j = 0; j < 8; ++j) acc2[i][j] = tot2[i][j] = make_float2(0.f, 0.f);
+    for (int j = 0; j < 8; ++j) {
+      acc2[i][j] = make_float2(0.f, 0.f);
+      if (!SMT) tot2[SMT ? 0 : i][SMT ? 0 : j] = make_float2(0.f, 0.f);
+    }
+  if (SMT) {
+#pragma unroll
+    for (int q = 0; q < 16; ++q) tot4[q * STH + tid] = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
   const int nk = (KD + KBK - 1) / KBK;
 #pragma unroll
   for (int s = 0; s < KST - 1; ++s) {
@@ -148,7 +167,7 @@ __global__ void __launch_bounds__(STH, 1) k_simt_probe(KParams p, int u, int pfl
     if (kt + KST - 1 < nk) issue(kt + KST - 1);
     cp_commit();
     const int slot = kt % KST;
-    const float *As = sm.a[slot] + ty * 4, *Bs = sm.b[slot] + tx * 4;
+    const float *As = ring + slot * 2 * KBK * SLD + ty * 4, *Bs = ring + (slot * 2 + 1) * KBK * SLD + tx * 4;
     float4 a0 = *reinterpret_cast<const float4 *>(As), a1 = *reinterpret_cast<const float4 *>(As + 64);
     float4 b0 = *reinterpret_cast<const float4 *>(Bs), b1 = *reinterpret_cast<const float4 *>(Bs + 64);
 #pragma unroll
@@ -172,20 +191,49 @@ __global__ void __launch_bounds__(STH, 1) k_simt_probe(KParams p, int u, int pfl
       }
     }
     if ((kt + 1) % FLUSH == 0 || kt + 1 == nk) {
+      if (SMT) {                                // totals in shared memory (thread-private float4 slots)
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
+        for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          tot2[i][j].x += acc2[i][j].x;
-          tot2[i][j].y += acc2[i][j].y;
-          acc2[i][j] = make_float2(0.f, 0.f);
-        }
+          for (int h = 0; h < 4; ++h) {
+            float4 tt = tot4[(i * 4 + h) * STH + tid];
+            tt.x += acc2[i][2 * h].x;
+            tt.y += acc2[i][2 * h].y;
+            tt.z += acc2[i][2 * h + 1].x;
+            tt.w += acc2[i][2 * h + 1].y;
+            tot4[(i * 4 + h) * STH + tid] = tt;
+            acc2[i][2 * h] = acc2[i][2 * h + 1] = make_float2(0.f, 0.f);
+          }
+      } else {
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            tot2[SMT ? 0 : i][SMT ? 0 : j].x += acc2[i][j].x;
+            tot2[SMT ? 0 : i][SMT ? 0 : j].y += acc2[i][j].y;
+            acc2[i][j] = make_float2(0.f, 0.f);
+          }
+      }
     }
   }
   cp_wait<0>();
+  float2 fin[4][8];                             // the totals
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int h = 0; h < 4; ++h) {
+      if (SMT) {
+        const float4 tt = tot4[(i * 4 + h) * STH + tid];
+        fin[i][2 * h] = make_float2(tt.x, tt.y);
+        fin[i][2 * h + 1] = make_float2(tt.z, tt.w);
+      } else {
+        fin[i][2 * h] = tot2[SMT ? 0 : i][SMT ? 0 : 2 * h];
+        fin[i][2 * h + 1] = tot2[SMT ? 0 : i][SMT ? 0 : 2 * h + 1];
+      }
+    }
 
-  // outputs: rows m0 + g·64 + ty·4 + r (g, r < 2, 4) = tot2[2g + r/2][·].{x|y}; columns
-  // j0 + h·64 + tx·4 + q (h, q < 2, 4) = tot2[·][4h + q]
+  // outputs: rows m0 + g·64 + ty·4 + r (g, r < 2, 4) = fin[2g + r/2][·].{x|y}; columns
+  // j0 + h·64 + tx·4 + q (h, q < 2, 4) = fin[·][4h + q]
   if (STAGE == 1) {                             // U [N][ldv]
 #pragma unroll
     for (int g = 0; g < 2; ++g)
@@ -199,10 +247,10 @@ __global__ void __launch_bounds__(STH, 1) k_simt_probe(KParams p, int u, int pfl
           const int c4 = h * 64 + tx * 4;
           if (c4 >= ncol) continue;
           float4 o;
-          o.x = (r & 1) ? tot2[ip][4 * h + 0].y : tot2[ip][4 * h + 0].x;
-          o.y = (r & 1) ? tot2[ip][4 * h + 1].y : tot2[ip][4 * h + 1].x;
-          o.z = (r & 1) ? tot2[ip][4 * h + 2].y : tot2[ip][4 * h + 2].x;
-          o.w = (r & 1) ? tot2[ip][4 * h + 3].y : tot2[ip][4 * h + 3].x;
+          o.x = (r & 1) ? fin[ip][4 * h + 0].y : fin[ip][4 * h + 0].x;
+          o.y = (r & 1) ? fin[ip][4 * h + 1].y : fin[ip][4 * h + 1].x;
+          o.z = (r & 1) ? fin[ip][4 * h + 2].y : fin[ip][4 * h + 2].x;
+          o.w = (r & 1) ? fin[ip][4 * h + 3].y : fin[ip][4 * h + 3].x;
           *reinterpret_cast<float4 *>(p.b.Uh + (size_t)m * ldv + gb + c4) = o;
         }
       }
@@ -211,7 +259,7 @@ __global__ void __launch_bounds__(STH, 1) k_simt_probe(KParams p, int u, int pfl
     const int warp = tid >> 5, lane = tid & 31;
     // α of the tile's 128 rows for every cluster, staged in the (now idle) ring: a thread's 8 columns
     // × 8 rows would otherwise be 64 scalar global loads
-    double *sal = reinterpret_cast<double *>(&sm.a[0][0]);
+    double *sal = reinterpret_cast<double *>(ring);
     __syncthreads();                            // every warp is done with the ring
     for (int e = tid; e < d.C * SBM; e += STH) {
       const int c = e / SBM, r = e % SBM;
@@ -243,7 +291,7 @@ __global__ void __launch_bounds__(STH, 1) k_simt_probe(KParams p, int u, int pfl
           float wq[4];
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
-            const float acc = (r & 1) ? tot2[ip][4 * h + q].y : tot2[ip][4 * h + q].x;
+            const float acc = (r & 1) ? fin[ip][4 * h + q].y : fin[ip][4 * h + q].x;
             wq[q] = (float)fma(beta, (double)acc, al[4 * h + q][m] * (double)dq[q]);
             dot[4 * h + q] += (double)dq[q] * (double)wq[q];
           }
@@ -274,8 +322,9 @@ __device__ __forceinline__ bool task_mean_active(const KParams &p, int t) {
 }
 
 // The mean-column kernels run on a second stream beside the probe SGEMMs (run_simt_cg): 128 threads
-// and ≤ 80 registers, so that a CTA fits on an SM next to a probe-SGEMM CTA (1 per SM, 210 registers ×
-// 256 threads) and streams Φ from HBM while that CTA's FMAs run.
+// and ≤ 80 registers, so that with the 1-CTA SGEMM form (210 registers × 256 threads) a mean CTA fits
+// on an SM next to it and streams Φ from HBM while its FMAs run; with the default 2-CTA form (all
+// registers taken) the mean CTAs interleave with the SGEMM CTAs at CTA boundaries.
 // Um[t][n][c] = Σ_d Φ_t[n][d] · Dm[t][c][d]; grid (ceil(N/128), T_loc); thread = row n, all clusters
 __global__ void __launch_bounds__(MTH) k_simt_mean1(KParams p, int u) {
   __shared__ __align__(16) float As[MBK][SBM + 1];
@@ -597,11 +646,15 @@ cudaError_t run_simt_cg(const KParams &p, int *h_alive, int64_t *launches, SimtT
   const int nbp = (d.ldv + 31) / 32, gu = nbp + (d.Tl * d.C + 7) / 8;
   constexpr int B = SimtTiming::B;
   cudaError_t e = cudaSuccess;
+  // the 2-CTA form by default (C4, 32 tasks: 1387 vs 1426 ms per EM iteration); CMTCS_SIMT_SMT=0 the other
+  static const bool smt = !getenv("CMTCS_SIMT_SMT") || atoi(getenv("CMTCS_SIMT_SMT")) != 0;
   static bool configured = false;   // dynamic shared memory above 48 KB (one process per GPU)
   if (!configured) {
-    const int sb = (int)sizeof(SimtSmem);
-    e = cudaFuncSetAttribute(k_simt_probe<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, sb);
-    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_simt_probe<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, sb);
+    const int s0 = (int)PCfg<false>::SMEM, s1 = (int)PCfg<true>::SMEM;
+    e = cudaFuncSetAttribute(k_simt_probe<1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, s0);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_simt_probe<2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, s0);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_simt_probe<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, s1);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_simt_probe<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, s1);
     if (e != cudaSuccess) return e;
     configured = true;
   }
@@ -628,8 +681,13 @@ cudaError_t run_simt_cg(const KParams &p, int *h_alive, int64_t *launches, SimtT
     k_simt_mean1<<<gm1, MTH, 0, ss.side>>>(p, u);
     k_simt_mean2<<<gm2, MTH, 0, ss.side>>>(p, u);
     cudaEventRecord(ss.join, ss.side);
-    k_simt_probe<1><<<g1, STH, sizeof(SimtSmem), s>>>(p, u, pflat);
-    k_simt_probe<2><<<g2, STH, sizeof(SimtSmem), s>>>(p, u, pflat);
+    if (smt) {
+      k_simt_probe<1, true><<<g1, STH, PCfg<true>::SMEM, s>>>(p, u, pflat);
+      k_simt_probe<2, true><<<g2, STH, PCfg<true>::SMEM, s>>>(p, u, pflat);
+    } else {
+      k_simt_probe<1, false><<<g1, STH, PCfg<false>::SMEM, s>>>(p, u, pflat);
+      k_simt_probe<2, false><<<g2, STH, PCfg<false>::SMEM, s>>>(p, u, pflat);
+    }
     cudaStreamWaitEvent(s, ss.join, 0);
     if (tm) cudaEventRecord(tm->ev[3 * slot + 1], s);
     k_simt_update<<<gu, 256, 0, s>>>(p, u, nbp);
