@@ -11,9 +11,9 @@
 // Per CG step u (one launch each, stream-ordered; every kernel returns at once when the previous
 // update left no column active, so the host checks termination only every few steps):
 //   k_simt_probe<1>   U[t][j][n] = Σ_d Φ_t[n][d] · D[t][j][d]                     (probe columns)
-//   k_simt_mean1      Um[t][n][c] = Σ_d Φ_t[n][d] · Dm[t][c][d]                  (fp64 mean columns)
+//   k_simt_mean<1>    Um[t][n][c] = Σ_d Φ_t[n][d] · Dm[t][c][d]                  (fp64 mean columns)
 //   k_simt_probe<2>   W[t][j][d] = β Σ_n Φ_t[n][d] · U[t][j][n] + α_c ⊙ D, dᵀW partials per 128 rows
-//   k_simt_mean2      Wm likewise in fp64, dᵀWm partials
+//   k_simt_mean<2>    Wm likewise in fp64, dᵀWm partials
 //   k_simt_update     Alg. 1 lines 3-7 per column (γ_u, x, r, ξ_u, d; convergence; transcript)
 //
 // The probe operator is a 128 × 128 register-tiled SGEMM (256 threads, 8 × 8 outputs per thread,
@@ -182,10 +182,18 @@ __global__ void __launch_bounds__(STH, PCfg<SMT>::MINB) k_simt_probe(KParams p, 
       const float2 ap[4] = {make_float2(a0.x, a0.y), make_float2(a0.z, a0.w), make_float2(a1.x, a1.y),
                             make_float2(a1.z, a1.w)};
       const float bv[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+#if CMTCS_SIMT_JI
 #pragma unroll
       for (int j = 0; j < 8; ++j)
 #pragma unroll
         for (int i = 0; i < 4; ++i) acc2[i][j] = __ffma2_rn(ap[i], make_float2(bv[j], bv[j]), acc2[i][j]);
+#else
+      // row pair outermost: consecutive FFMA2 share the 64-bit A pair (operand reuse of the wide source)
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc2[i][j] = __ffma2_rn(ap[i], make_float2(bv[j], bv[j]), acc2[i][j]);
+#endif
       if (kk + 1 < KBK) {
         a0 = na0; a1 = na1; b0 = nb0; b1 = nb1;
       }
@@ -325,95 +333,95 @@ __device__ __forceinline__ bool task_mean_active(const KParams &p, int t) {
 // and ≤ 80 registers, so that with the 1-CTA SGEMM form (210 registers × 256 threads) a mean CTA fits
 // on an SM next to it and streams Φ from HBM while its FMAs run; with the default 2-CTA form (all
 // registers taken) the mean CTAs interleave with the SGEMM CTAs at CTA boundaries.
-// Um[t][n][c] = Σ_d Φ_t[n][d] · Dm[t][c][d]; grid (ceil(N/128), T_loc); thread = row n, all clusters
-__global__ void __launch_bounds__(MTH) k_simt_mean1(KParams p, int u) {
-  __shared__ __align__(16) float As[MBK][SBM + 1];
-  __shared__ double Bm[MBK][MAXC];
-  if (loop_done(p, u)) return;
-  const Dims &d = p.d;
-  const int t = blockIdx.y, tid = threadIdx.x, n0 = blockIdx.x * SBM;
-  if (!task_mean_active(p, t)) return;
-  const float *__restrict__ phi = p.phi + (size_t)t * d.phi_task_stride;
-  const double *__restrict__ dm = p.b.Dm + (size_t)t * d.C * d.D;
-  double acc[MAXC];
-#pragma unroll
-  for (int c = 0; c < MAXC; ++c) acc[c] = 0.0;
-  for (int k0 = 0; k0 < d.D; k0 += MBK) {
-    __syncthreads();
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {   // 128 rows × 16 k, transposed into As[k][row]
-      const int idx = tid + i * MTH, row = idx >> 2, kq = (idx & 3) * 4;
-      const int n = n0 + row, k = k0 + kq;
-      const float4 v = (n < d.N && k < d.D) ? ldcs4(phi + (size_t)n * d.D + k) : make_float4(0.f, 0.f, 0.f, 0.f);
-      As[kq][row] = v.x; As[kq + 1][row] = v.y; As[kq + 2][row] = v.z; As[kq + 3][row] = v.w;
-    }
-    for (int e = tid; e < MBK * d.C; e += MTH) {
-      const int c = e / MBK, kk = e % MBK;
-      Bm[kk][c] = (k0 + kk < d.D) ? dm[(size_t)c * d.D + k0 + kk] : 0.0;
-    }
-    __syncthreads();
-#pragma unroll 4
-    for (int kk = 0; kk < MBK; ++kk) {
-      const double a = (double)As[kk][tid];
-#pragma unroll
-      for (int c = 0; c < MAXC; ++c)
-        if (c < d.C) acc[c] = fma(a, Bm[kk][c], acc[c]);
-    }
-  }
-  if (n0 + tid < d.N) {
-#pragma unroll
-    for (int c = 0; c < MAXC; ++c)
-      if (c < d.C) p.b.Um[((size_t)t * d.N + n0 + tid) * d.Cp + c] = acc[c];
-  }
-}
-
-// Wm[t][c][d] = β Σ_n Φ_t[n][d] · Um[t][n][c] + α_cd · Dm[t][c][d], dᵀWm partial per 128 rows of d;
-// grid (ceil(D/128), T_loc); thread = row d, all clusters
-__global__ void __launch_bounds__(MTH) k_simt_mean2(KParams p, int u) {
-  __shared__ __align__(16) float As[MBK][SBM];
-  __shared__ double Bm[MBK][MAXC];
+// Both mean kernels: C[m][c] = Σ_k A[k][m]·B[k][c] in fp64, A the M-major fp32 matrix (stage 1: Φᵀ
+// [D][N]; stage 2: Φ [N][D]) in 16-k slabs (a thread per row m: conflict-free reads, no transposes),
+// B the C mean columns (stage 1: Dm [C][D] read as [k][c]; stage 2: Um [N][Cp]).  Double-buffered
+// shared memory fed from registers: the next slab's loads are issued before this slab's FMAs.
+// grid (ceil(M/128), T_loc); stage 2 adds α ⊙ Dm and the dᵀWm partial of its 128 rows.
+template <int STAGE>
+__global__ void __launch_bounds__(MTH) k_simt_mean(KParams p, int u) {
+  __shared__ __align__(16) float As[2][MBK][SBM];
+  __shared__ double Bm[2][MBK][MAXC];
   __shared__ double red[MTH / 32][MAXC];
   if (loop_done(p, u)) return;
   const Dims &d = p.d;
-  const int t = blockIdx.y, tid = threadIdx.x, rt = blockIdx.x, d0 = rt * SBM;
+  const int t = blockIdx.y, tid = threadIdx.x, rt = blockIdx.x, m0 = rt * SBM;
   if (!task_mean_active(p, t)) return;
-  const float *__restrict__ phi = p.phi + (size_t)t * d.phi_task_stride;
+  const int M = STAGE == 1 ? d.N : d.D, KD = STAGE == 1 ? d.D : d.N, C = d.C;
+  const float *__restrict__ amat = (STAGE == 1 ? p.b.PT : p.phi) + (size_t)t * d.phi_task_stride;
+  const double *__restrict__ dm = p.b.Dm + (size_t)t * C * d.D;
   const double *__restrict__ um = p.b.Um + (size_t)t * d.N * d.Cp;
+  constexpr int NA = MBK * SBM / 4 / MTH;      // float4 of A per thread and slab
+  constexpr int NB = MBK * MAXC / MTH;         // B entries per thread and slab (C ≤ MAXC)
+  float4 ra[NA];
+  double rb[NB];
+  auto gload = [&](int k0) {
+#pragma unroll
+    for (int v = 0; v < NA; ++v) {
+      const int idx = tid + v * MTH, kr = idx >> 5, c4 = (idx & 31) * 4, k = k0 + kr;
+      ra[v] = (k < KD && m0 + c4 < M) ? ldcs4(amat + (size_t)k * M + m0 + c4) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+    for (int v = 0; v < NB; ++v) {
+      const int e = tid + v * MTH, kk = e / MAXC, c = e % MAXC, k = k0 + kk;
+      rb[v] = (c < C && k < KD) ? (STAGE == 1 ? dm[(size_t)c * d.D + k] : um[(size_t)k * d.Cp + c]) : 0.0;
+    }
+  };
+  auto sstore = [&](int buf) {
+#pragma unroll
+    for (int v = 0; v < NA; ++v) {
+      const int idx = tid + v * MTH;
+      *reinterpret_cast<float4 *>(&As[buf][idx >> 5][(idx & 31) * 4]) = ra[v];
+    }
+#pragma unroll
+    for (int v = 0; v < NB; ++v) {
+      const int e = tid + v * MTH;
+      Bm[buf][e / MAXC][e % MAXC] = rb[v];
+    }
+  };
   double acc[MAXC];
 #pragma unroll
   for (int c = 0; c < MAXC; ++c) acc[c] = 0.0;
-  for (int k0 = 0; k0 < d.N; k0 += MBK) {
-    __syncthreads();
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {   // 16 rows of Φ × 128 columns (d): coalesced
-      const int idx = tid + i * MTH, kr = idx >> 5, dq = (idx & 31) * 4;
-      const int n = k0 + kr, dd = d0 + dq;
-      *reinterpret_cast<float4 *>(&As[kr][dq]) =
-          (n < d.N && dd < d.D) ? ldcs4(phi + (size_t)n * d.D + dd) : make_float4(0.f, 0.f, 0.f, 0.f);
-    }
-    for (int e = tid; e < MBK * d.C; e += MTH) {
-      const int kk = e / d.C, c = e % d.C;
-      Bm[kk][c] = (k0 + kk < d.N) ? um[(size_t)(k0 + kk) * d.Cp + c] : 0.0;
-    }
-    __syncthreads();
+  const int nk = (KD + MBK - 1) / MBK;
+  gload(0);
+  sstore(0);
+  __syncthreads();
+  for (int kt = 0; kt < nk; ++kt) {
+    const int buf = kt & 1;
+    if (kt + 1 < nk) gload((kt + 1) * MBK);
 #pragma unroll 4
     for (int kk = 0; kk < MBK; ++kk) {
-      const double a = (double)As[kk][tid];
+      const double a = (double)As[buf][kk][tid];
+      const double2 *bb = reinterpret_cast<const double2 *>(Bm[buf][kk]);
+#pragma unroll
+      for (int c2 = 0; c2 < MAXC / 2; ++c2) {
+        if (2 * c2 >= C) break;
+        const double2 bv = bb[c2];              // two clusters per broadcast load
+        acc[2 * c2] = fma(a, bv.x, acc[2 * c2]);
+        acc[2 * c2 + 1] = fma(a, bv.y, acc[2 * c2 + 1]);
+      }
+    }
+    if (kt + 1 < nk) sstore(buf ^ 1);           // that buffer's readers passed the last barrier
+    __syncthreads();
+  }
+  const int m = m0 + tid;
+  if (STAGE == 1) {
+    if (m < M) {
 #pragma unroll
       for (int c = 0; c < MAXC; ++c)
-        if (c < d.C) acc[c] = fma(a, Bm[kk][c], acc[c]);
+        if (c < C) p.b.Um[((size_t)t * d.N + m) * d.Cp + c] = acc[c];
     }
+    return;
   }
-  const int dd = d0 + tid;
   const int warp = tid >> 5, lane = tid & 31;
 #pragma unroll
   for (int c = 0; c < MAXC; ++c) {
-    if (c >= d.C) break;
+    if (c >= C) break;
     double v = 0.0;
-    if (dd < d.D) {
-      const size_t o = ((size_t)t * d.C + c) * d.D + dd;
+    if (m < M) {
+      const size_t o = ((size_t)t * C + c) * d.D + m;
       const double dv = p.b.Dm[o];
-      const double w = fma(p.beta, acc[c], p.b.alpha64[(size_t)c * d.D + dd] * dv);
+      const double w = fma(p.beta, acc[c], p.b.alpha64[(size_t)c * d.D + m] * dv);
       p.b.Wm[o] = w;
       v = dv * w;
     }
@@ -421,11 +429,11 @@ __global__ void __launch_bounds__(MTH) k_simt_mean2(KParams p, int u) {
     if (lane == 0) red[warp][c] = v;
   }
   __syncthreads();
-  if (tid < d.C) {
-    double s = 0.0;
+  if (tid < C) {
+    double sum = 0.0;
 #pragma unroll
-    for (int w = 0; w < MTH / 32; ++w) s += red[w][tid];
-    p.b.dAdm[((size_t)t * d.C + tid) * d.nRT2 + rt] = s;
+    for (int w = 0; w < MTH / 32; ++w) sum += red[w][tid];
+    p.b.dAdm[((size_t)t * C + tid) * d.nRT2 + rt] = sum;
   }
 }
 
@@ -678,8 +686,8 @@ cudaError_t run_simt_cg(const KParams &p, int *h_alive, int64_t *launches, SimtT
     // fork: the mean columns (fp64, HBM-bound) on the side stream, the probe SGEMMs (FMA-bound) here
     cudaEventRecord(ss.fork, s);
     cudaStreamWaitEvent(ss.side, ss.fork, 0);
-    k_simt_mean1<<<gm1, MTH, 0, ss.side>>>(p, u);
-    k_simt_mean2<<<gm2, MTH, 0, ss.side>>>(p, u);
+    k_simt_mean<1><<<gm1, MTH, 0, ss.side>>>(p, u);
+    k_simt_mean<2><<<gm2, MTH, 0, ss.side>>>(p, u);
     cudaEventRecord(ss.join, ss.side);
     if (smt) {
       k_simt_probe<1, true><<<g1, STH, PCfg<true>::SMEM, s>>>(p, u, pflat);
