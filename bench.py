@@ -483,7 +483,7 @@ def cuda_arm(args):
                                     "achieved = 10*D*log2(D) flop per active column per CG step / the kernels' "
                                     "duration)") if fourier else
                                    ("the FP32 engine's CG loop (k_simt_probe<1>/<2> register-tiled SGEMMs for the "
-                                    "probe columns, k_simt_mean1/2 fp64 mean columns, k_simt_update); achieved = "
+                                    "probe columns, k_simt_mean<1/2> fp64 mean columns, k_simt_update); achieved = "
                                     "algorithmic fp32 flop 4*N*D per active column per CG step / the loop's duration "
                                     "(CUDA events on the launch stream around every E-step's CG loop); "
                                     "operator_phases_only: the same flops / the operator kernels' event time")
