@@ -112,16 +112,25 @@ __global__ void __launch_bounds__(STH, PCfg<SMT>::MINB) k_simt_probe(KParams p, 
   const int t = blockIdx.z, rt = blockIdx.y, j0 = blockIdx.x * SBN, m0 = rt * SBM;
   const int M = STAGE == 1 ? d.N : d.D;      // output rows
   const int KD = STAGE == 1 ? d.D : d.N;     // contraction length (multiple of 4)
-  const int ncol = min(SBN, (pflat > 0 ? pflat : d.P) - j0);
-  const size_t gb = pflat > 0 ? (size_t)j0 : (size_t)t * d.Pp + j0;   // first column in the d-major arrays
-  const size_t fb = pflat > 0 ? (size_t)j0 : (size_t)t * d.P + j0;    // ... in the per-column state
-  const int *flag = p.b.flag + fb;
-  if (!__syncthreads_or(tid < ncol && flag[tid] == 1)) return;
+  // active-column compaction: this tile multiplies the 4-column groups [32·x, 32·x + 32) of its column
+  // space's list of groups with an active column (k_simt_groups): a tile ends up with retired
+  // columns only inside a partly active group.  Column space: a task's P columns (d-major base
+  // t·Pp, state base t·P), or all tasks' (flat: one space, bases 0).
+  const int space = pflat > 0 ? 0 : t, ncs = pflat > 0 ? pflat : d.P;
+  const int nlist = p.b.m_act[space];
+  if (j0 >= 4 * nlist) return;                   // CTA-uniform
+  const int ngrp = min(SBN / 4, nlist - j0 / 4);
+  __shared__ int sgrp[SBN / 4];
+  if (tid < SBN / 4) sgrp[tid] = tid < ngrp ? p.b.act[(size_t)space * d.Pp / 4 * (pflat > 0 ? d.Tl : 1) + j0 / 4 + tid] : 0;
+  __syncthreads();
+  const int ncol = 4 * ngrp;                     // multiplied columns of this tile (chunks of 4)
+  const size_t gb = pflat > 0 ? 0 : (size_t)t * d.Pp;   // the space's base in the d-major arrays
+  const size_t fb = pflat > 0 ? 0 : (size_t)t * d.P;    // ... in the per-column state
   if (STAGE == 2 && rt == 0 && tid == 0) atomicAdd(p.b.histp + u, ncol);
   // A[k][m]: stage 1 Φᵀ_t [D][N], stage 2 Φ_t [N][D] (row length M); B[k][g]: D32 [D][ldv] / U [N][ldv]
   const float *__restrict__ amat = STAGE == 1 ? p.b.PT + (size_t)t * d.phi_task_stride
                                               : p.phi + (size_t)t * d.phi_task_stride;
-  const float *__restrict__ bmat = (STAGE == 1 ? p.b.D32 : p.b.Uh) + gb;
+  const float *__restrict__ bmat = (STAGE == 1 ? p.b.D32 : p.b.Uh) + gb;   // + 4·group per chunk
   const size_t ldv = (size_t)d.ldv;
   const uint32_t sa0 = (uint32_t)__cvta_generic_to_shared(ring);
   const uint32_t sb0 = sa0 + 4u * (uint32_t)(KBK * SLD);
@@ -136,8 +145,8 @@ __global__ void __launch_bounds__(STH, PCfg<SMT>::MINB) k_simt_probe(KParams p, 
       const uint32_t so = 4u * (uint32_t)(slot * 2 * KBK * SLD + kr * SLD + c4);
       const bool oka = k < KD && m0 + c4 < M;
       cp_async16(sa0 + so, oka ? amat + (size_t)k * M + m0 + c4 : amat, oka);
-      const bool okb = k < KD && c4 < ncol;    // a chunk past ncol holds padding / other tasks' columns
-      cp_async16(sb0 + so, okb ? bmat + (size_t)k * ldv + c4 : bmat, okb);
+      const bool okb = k < KD && c4 < ncol;    // chunk c4/4 = group sgrp[c4/4] (its padding columns too)
+      cp_async16(sb0 + so, okb ? bmat + (size_t)k * ldv + 4 * sgrp[c4 >> 2] : bmat, okb);
     }
   };
 
@@ -253,7 +262,7 @@ __global__ void __launch_bounds__(STH, PCfg<SMT>::MINB) k_simt_probe(KParams p, 
           o.y = (r & 1) ? fin[ip][4 * h + 1].y : fin[ip][4 * h + 1].x;
           o.z = (r & 1) ? fin[ip][4 * h + 2].y : fin[ip][4 * h + 2].x;
           o.w = (r & 1) ? fin[ip][4 * h + 3].y : fin[ip][4 * h + 3].x;
-          *reinterpret_cast<float4 *>(p.b.Uh + (size_t)m * ldv + gb + c4) = o;
+          *reinterpret_cast<float4 *>(p.b.Uh + (size_t)m * ldv + gb + 4 * sgrp[c4 >> 2]) = o;
         }
       }
   } else {                                      // W = βΦᵀU + α ⊙ d (fp64, one rounding), dᵀW partials
@@ -274,7 +283,8 @@ __global__ void __launch_bounds__(STH, PCfg<SMT>::MINB) k_simt_probe(KParams p, 
     for (int q = 0; q < 8; ++q) {
       dot[q] = 0.0;
       const int c = (q >> 2) * 64 + tx * 4 + (q & 3);
-      al[q] = sal + (size_t)(((fb + min(c, ncol - 1)) % d.P) / d.K) * SBM - m0;   // the column's cluster
+      const int jc = min(4 * sgrp[min(c, ncol - 1) >> 2] + (c & 3), ncs - 1);   // column in the space
+      al[q] = sal + (size_t)(((fb + jc) % d.P) / d.K) * SBM - m0;                 // the column's cluster
     }
 #pragma unroll
     for (int g = 0; g < 2; ++g)
@@ -287,7 +297,7 @@ __global__ void __launch_bounds__(STH, PCfg<SMT>::MINB) k_simt_probe(KParams p, 
         for (int h = 0; h < 2; ++h) {
           const int c4 = h * 64 + tx * 4;
           if (c4 >= ncol) continue;
-          const size_t o = (size_t)m * ldv + gb + c4;
+          const size_t o = (size_t)m * ldv + gb + 4 * sgrp[c4 >> 2];
           const float4 dv = *reinterpret_cast<const float4 *>(p.b.D32 + o);
           const float dq[4] = {dv.x, dv.y, dv.z, dv.w};
           float wq[4];
@@ -307,11 +317,12 @@ __global__ void __launch_bounds__(STH, PCfg<SMT>::MINB) k_simt_probe(KParams p, 
       if (lane < 16) red[warp][(q >> 2) * 64 + tx * 4 + (q & 3)] = v;
     }
     __syncthreads();
-    if (tid < ncol) {
+    const int jt = tid < ncol ? 4 * sgrp[tid >> 2] + (tid & 3) : ncs;   // this thread's column, if real
+    if (jt < ncs) {
       double s = 0.0;
 #pragma unroll
       for (int w = 0; w < STH / 32; ++w) s += red[w][tid];
-      p.b.dAd[(fb + tid) * d.nRT2 + rt] = s;
+      p.b.dAd[(fb + jt) * d.nRT2 + rt] = s;
     }
   }
 }
@@ -631,6 +642,30 @@ __global__ void __launch_bounds__(256) k_simt_update(KParams p, int u, int nbp) 
   simt_update_mean(p, t, c, u, lane);
 }
 
+// Active 4-column groups of every column space (a task's P columns, or all tasks' in the flat
+// shared-Φ GEMM), in order: act[space·G + i], count m_act[space] (G = Pp/4, or T_loc·P/4 flat).  One
+// warp per space, ballot compaction.
+__global__ void k_simt_groups(KParams p, int u, int pflat) {
+  if (loop_done(p, u)) return;
+  const Dims &d = p.d;
+  const int space = blockIdx.x, lane = threadIdx.x;
+  const int ncs = pflat > 0 ? pflat : d.P, ng = (ncs + 3) / 4;
+  const size_t fb = pflat > 0 ? 0 : (size_t)space * d.P;
+  const size_t lb = (size_t)space * d.Pp / 4 * (pflat > 0 ? d.Tl : 1);
+  int cnt = 0;
+  for (int q0 = 0; q0 < ng; q0 += 32) {
+    const int q = q0 + lane;
+    bool a = false;
+    if (q < ng)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) a |= (4 * q + e < ncs) && p.b.flag[fb + 4 * q + e] == 1;
+    const unsigned m = __ballot_sync(0xffffffffu, a);
+    if (a) p.b.act[lb + cnt + __popc(m & ((1u << lane) - 1u))] = q;
+    cnt += __popc(m);
+  }
+  if (lane == 0) p.b.m_act[space] = cnt;
+}
+
 }  // namespace
 
 // The CG loop of an E-step on the CUDA cores.  Termination is checked on the host every
@@ -677,6 +712,7 @@ cudaError_t run_simt_cg(const KParams &p, int *h_alive, int64_t *launches, SimtT
   for (int u = 0; u < d.cap; ++u) {
     const int slot = u % B;
     if (tm) cudaEventRecord(tm->ev[3 * slot], s);
+    k_simt_groups<<<pflat ? 1 : d.Tl, 32, 0, s>>>(p, u, pflat);
     // fork: the mean columns (fp64, HBM-bound) on the side stream, the probe SGEMMs (FMA-bound) here
     cudaEventRecord(ss.fork, s);
     cudaStreamWaitEvent(ss.side, ss.fork, 0);
@@ -694,7 +730,7 @@ cudaError_t run_simt_cg(const KParams &p, int *h_alive, int64_t *launches, SimtT
     if (tm) cudaEventRecord(tm->ev[3 * slot + 1], s);
     k_simt_update<<<gu, 256, 0, s>>>(p, u, nbp);
     if (tm) cudaEventRecord(tm->ev[3 * slot + 2], s);
-    *launches += 5;
+    *launches += 6;
     ++pending;
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
