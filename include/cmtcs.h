@@ -55,7 +55,8 @@ typedef struct cmtcs_problem {
   int32_t K;             /* Rademacher probes per (t, c), K ≥ 1                                 */
   int32_t shared_phi;    /* 1: one Φ [N][D] shared by all tasks; 0: Φ_t per task               */
   double beta;           /* noise precision β = 1/σ² > 0                                        */
-  const double *pi;      /* host, C entries > 0 summing to 1 ± 1e-9 (fixed prior)  */
+  const double *pi;      /* host, C entries > 0 summing to 1 ± 1e-9: the prior π,
+                            fixed, or the initial value when learn_pi = 1                         */
   int32_t cg_max_iters;  /* U: CG step cap per system, ≥ 1                                      */
   double cg_rel_tol;     /* ≥ 0: a column stops after step u when ‖r_{u+1}‖₂ ≤ tol·‖b‖₂         */
   double alpha_max;      /* α cap (1e12)                                                        */
@@ -75,6 +76,12 @@ typedef struct cmtcs_problem {
                             power of two in [512, 8192] and shared_phi = 0                           */
   const int32_t *fourier_rows; /* device, BORROWED, op_kind = PARTIAL_FOURIER: int32 [T_loc][N], distinct
                             rows in [0, D) per task (must outlive ctx); NULL otherwise                */
+  int32_t learn_pi;      /* 0: π fixed (the paper's setting).  1: π is learned — every
+                            M-step also sets π_c = (1/T) Σ_t q_tc over all T tasks (all ranks: the
+                            Σ_t q_tc of the Eq. 4 all-reduce), the mixture-weight M-step PAPER.md:30
+                            points to ("can also be learned", McLachlan); the next E-step's Eq. 3
+                            softmax uses it (reading P1).  An emptied cluster gets π_c = 0
+                            (log π_c = −∞, q_tc = 0 from then on).                                  */
 } cmtcs_problem;
 
 /* CMTCS_OP_DENSE_FP32: the same dense Φ_t as CMTCS_OP_DENSE, the operator on the FP32 CUDA cores
@@ -139,6 +146,10 @@ cmtcs_status cmtcs_em_step(cmtcs_ctx *ctx, int32_t n_iters, const uint64_t *prob
  *   (argmax, ties → lowest c), recon fp64 [T_loc][D] = μ_{t,a_t}.  ESTATE before any em_step. */
 cmtcs_status cmtcs_posterior(cmtcs_ctx *ctx, double *mu, double *s, double *logdet, double *q,
                              double *alpha, int32_t *assign, double *recon);
+
+/* The current mixture weights π (fp64 [C], host or device): the initial p->pi, or after each
+ * M-step with learn_pi the learned ones.  ESTATE on an unusable context. */
+cmtcs_status cmtcs_get_pi(cmtcs_ctx *ctx, double *pi);
 
 /* Replace α (host or device fp64 [C][D], all > 0) and the next EM-iteration index (resume /
  * single-step parity from an identical state). */

@@ -10,6 +10,7 @@ notation.  Citations are PAPER.md line numbers (the LaTeX source) with the equat
   L(θ)    log-likelihood ......................... PAPER.md:33
   Eq. 3   Σ, μ, q, ℓ (E-step) .................... PAPER.md:45-59
   Eq. 4   α update (M-step) ...................... PAPER.md:61-64
+  π update (learned mixture weights) ............. PAPER.md:30 (m_step_pi, reading P1)
   Eq. 5   diagonal estimator s ................... PAPER.md:72-76
   Eq. 6   linear systems A x_k = p_k, A μ = βΦᵀy .. PAPER.md:77-80
   Alg. 1  conjugate gradient ..................... PAPER.md:86-98
@@ -248,6 +249,14 @@ def m_step(q: np.ndarray, mu: np.ndarray, s: np.ndarray, alpha_old: np.ndarray,
     return m_step_finish(num, den, alpha_old, alpha_max, empty_eps)
 
 
+def m_step_pi(q: np.ndarray) -> np.ndarray:
+    """Mixture-weight M-step when π is learned (π "can also be learned by the model",
+    citing the mixture-model EM of McLachlan & Basford): the π-dependent part of the EM surrogate,
+    Σ_t Σ_c q_tc log π_c, is maximised on the simplex by π_c = (1/T) Σ_t q_tc (reading P1)."""
+    q = np.asarray(q, dtype=np.float64)
+    return q.sum(axis=0) / q.shape[0]
+
+
 def m_step_sums(q, mu, s, var_floor=1e-12):
     """The two sums of Eq. 4 over the tasks given (a rank's shard sums to a partial)."""
     q = np.asarray(q, dtype=np.float64)
@@ -427,20 +436,26 @@ def nmse(zhat: np.ndarray, z: np.ndarray) -> float:
 
 
 def run(data: dict, iters: int, mode: str = "cofem", alpha0: Optional[np.ndarray] = None,
-        em_iter0: int = 0, alpha_max=1e12, var_floor=1e-12, empty_eps=1e-10, callback=None, **kw) -> dict:
+        em_iter0: int = 0, alpha_max=1e12, var_floor=1e-12, empty_eps=1e-10, callback=None,
+        learn_pi: bool = False, **kw) -> dict:
     """Alg. 2: `iters` EM iterations from α₀, then the readout.
 
-    The readout uses q and μ of the last E-step (reading A3)."""
+    The readout uses q and μ of the last E-step (reading A3).  learn_pi: π is updated with α in
+    every M-step (m_step_pi, reading P1); the E-step of iteration i uses the π of iteration i − 1."""
     alpha = np.array(data["alpha0"] if alpha0 is None else alpha0, dtype=np.float64)
+    data = dict(data)
+    data["pi"] = np.array(data["pi"], dtype=np.float64)
     hist = []
     e = None
     for i in range(iters):
         e = e_step(data, alpha, em_iter0 + i, mode, **kw)
         alpha_new = m_step(e["q"], e["mu"], e["s"], alpha, alpha_max, var_floor, empty_eps)
-        hist.append(dict(L=e["L"], q=e["q"], alpha_in=alpha))
+        hist.append(dict(L=e["L"], q=e["q"], alpha_in=alpha, pi_in=data["pi"]))
         if callback is not None:
             callback(i, e, alpha_new)
         alpha = alpha_new
+        if learn_pi:
+            data["pi"] = m_step_pi(e["q"])
     a, zhat = readout(e["q"], e["mu"])
-    return dict(alpha=alpha, assign=a, zhat=zhat, last=e, history=hist,
+    return dict(alpha=alpha, pi=data["pi"], assign=a, zhat=zhat, last=e, history=hist,
                 nmse=nmse(zhat, data["z"]) if "z" in data else None)

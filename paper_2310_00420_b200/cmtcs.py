@@ -19,7 +19,7 @@ STATUS = {0: "CMTCS_OK", 1: "CMTCS_EINVAL", 2: "CMTCS_ENOMEM", 3: "CMTCS_ECUDA",
 EXPORTED = ["cmtcs_get_unique_id", "cmtcs_workspace_size", "cmtcs_init", "cmtcs_em_step",
             "cmtcs_posterior", "cmtcs_set_state", "cmtcs_transcript", "cmtcs_last_error",
             "cmtcs_destroy", "cmtcs_kernel_launches", "cmtcs_probe_words", "cmtcs_lanczos_quadrature",
-            "cmtcs_set_timing", "cmtcs_get_timing", "cmtcs_estep_sums"]
+            "cmtcs_set_timing", "cmtcs_get_timing", "cmtcs_estep_sums", "cmtcs_get_pi"]
 
 
 class CmtcsError(RuntimeError):
@@ -34,7 +34,8 @@ class cmtcs_problem(ctypes.Structure):
                 ("cg_max_iters", c_int32), ("cg_rel_tol", c_double), ("alpha_max", c_double),
                 ("var_floor", c_double), ("empty_eps", c_double), ("probe_seed", c_uint64),
                 ("task_begin", c_int32), ("task_end", c_int32), ("em_iter0", c_int32),
-                ("mean_rel_tol", c_double), ("op_kind", c_int32), ("fourier_rows", c_void_p)]
+                ("mean_rel_tol", c_double), ("op_kind", c_int32), ("fourier_rows", c_void_p),
+                ("learn_pi", c_int32)]
 
 
 CMTCS_OP_DENSE, CMTCS_OP_PARTIAL_FOURIER, CMTCS_OP_DENSE_FP32 = 0, 1, 2
@@ -90,6 +91,8 @@ def _load() -> ctypes.CDLL:
     lib.cmtcs_get_timing.restype = st
     lib.cmtcs_estep_sums.argtypes = [vp, vp]
     lib.cmtcs_estep_sums.restype = st
+    lib.cmtcs_get_pi.argtypes = [vp, vp]
+    lib.cmtcs_get_pi.restype = st
     return lib
 
 
@@ -187,3 +190,7 @@ def cmtcs_get_timing(ctx: int, reset: bool = False) -> dict:
 
 def cmtcs_estep_sums(ctx: int, out_ptr: int):
     _check(_lib.cmtcs_estep_sums(ctx, out_ptr), ctx)
+
+
+def cmtcs_get_pi(ctx: int, out_ptr: int):
+    _check(_lib.cmtcs_get_pi(ctx, out_ptr), ctx)

@@ -151,6 +151,7 @@ bool make_dims(const cmtcs_problem *p, Dims *d, char *why) {
     s += p->pi[c];
   }
   if (fabs(s - 1.0) > 1e-9) { snprintf(why, 256, "pi sums to %.17g, not 1", s); return false; }
+  if (p->learn_pi != 0 && p->learn_pi != 1) { snprintf(why, 256, "learn_pi must be 0 or 1"); return false; }
   if (p->op_kind != CMTCS_OP_DENSE && p->op_kind != CMTCS_OP_PARTIAL_FOURIER && p->op_kind != CMTCS_OP_DENSE_FP32) {
     snprintf(why, 256, "unknown op_kind %d", p->op_kind);
     return false;
@@ -556,6 +557,7 @@ cmtcs_status cmtcs_init(cmtcs_ctx **out, const cmtcs_problem *p, const float *ph
   c->kp.phi = phi;
   c->kp.y = y;
   c->kp.beta = p->beta;
+  c->kp.learn_pi = p->learn_pi;
   c->kp.tol = p->cg_rel_tol;
   c->kp.tol_mean = p->mean_rel_tol < 0 ? p->cg_rel_tol : p->mean_rel_tol;
   c->kp.alpha_max = p->alpha_max;
@@ -665,6 +667,19 @@ cmtcs_status cmtcs_posterior(cmtcs_ctx *c, double *mu, double *s, double *logdet
     c->launches += 1;
     if (assign) CUDA_OK(c, cudaMemcpyAsync(assign, b.assign, d.Tl * sizeof(int), cudaMemcpyDeviceToDevice, st));
   }
+  return CMTCS_OK;
+}
+
+cmtcs_status cmtcs_get_pi(cmtcs_ctx *c, double *pi) {
+  if (!c) return fail(nullptr, CMTCS_EINVAL, "ctx is NULL");
+  if (c->broken) return CMTCS_ESTATE;
+  if (!pi) return fail(c, CMTCS_EINVAL, "pi is NULL");
+  const int C = c->kp.d.C;
+  double lp[MAXC], v[MAXC];
+  CUDA_OK(c, cudaMemcpyAsync(lp, c->kp.b.logpi, C * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  CUDA_OK(c, cudaStreamSynchronize(c->stream));
+  for (int i = 0; i < C; ++i) v[i] = exp(lp[i]);
+  CUDA_OK(c, cudaMemcpy(pi, v, C * sizeof(double), cudaMemcpyDefault));
   return CMTCS_OK;
 }
 

@@ -140,6 +140,7 @@ struct KParams {
   int it;                      // global EM iteration index of this E-step
   const uint64_t *probe_bits;  // optional override
   const double *q_override;    // optional
+  int learn_pi;                // M-step also sets log π_c = log((1/T) Σ_t q_tc) (reading P1)
   int trace_step;              // CMTCS_TRACE_STEP (default 5): the CG step CMTCS_PHASE_LOG traces
   int dbg_flags;               // CMTCS_DBG (diagnostics only, wrong results): 1 no DMMA, 2 no tcgen05.mma,
                                // 4 no tf32 split, 8/16/32 accumulator layouts, 64 no epilogue, 128 no TMA;

@@ -247,12 +247,16 @@ __global__ void k_mstep_partial(KParams p) {
   }
 }
 
-// K10: α̃_cd = min(num_c / den_cd, α_max); clusters with num_c < empty_eps keep α (A10).
+// K10: α̃_cd = min(num_c / den_cd, α_max); clusters with num_c < empty_eps keep α (A10); with
+// learn_pi also log π_c.
 __global__ void k_mstep_finish(KParams p) {
   const Dims &d = p.d;
   const int dd = blockIdx.x * blockDim.x + threadIdx.x, c = blockIdx.y;
-  if (dd >= d.D) return;
   const double num = p.b.red[(size_t)d.C * d.D + c];
+  // learned mixture weights (reading P1): π_c = (1/T) Σ_t q_tc, num all-reduced over
+  // the ranks' tasks and T the global task count; the next E-step's softmax reads log π
+  if (p.learn_pi && dd == 0) p.b.logpi[c] = log(num / (double)d.T);
+  if (dd >= d.D) return;
   if (num < p.empty_eps) return;
   const double a = fmin(num / p.b.red[(size_t)c * d.D + dd], p.alpha_max);
   p.b.alpha64[(size_t)c * d.D + dd] = a;

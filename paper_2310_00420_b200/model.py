@@ -30,7 +30,8 @@ class CoFEM:
                  alpha_max: float = 1e12, var_floor: float = 1e-12, empty_eps: float = 1e-10,
                  mean_rel_tol: float = -1.0,
                  nccl_uid: bytes | None = None, rank: int = 0, world: int = 1, stream=None,
-                 fourier_rows: torch.Tensor | None = None, D: int | None = None, engine: str = "fp32"):
+                 fourier_rows: torch.Tensor | None = None, D: int | None = None, engine: str = "fp32",
+                 learn_pi: bool = False):
         fourier = fourier_rows is not None
         if engine not in ("tensor", "fp32"):
             raise ValueError(f"engine must be 'tensor' or 'fp32', got {engine!r}")
@@ -61,7 +62,7 @@ class CoFEM:
             mean_rel_tol=float(mean_rel_tol),
             op_kind=_c.CMTCS_OP_PARTIAL_FOURIER if fourier else
             (_c.CMTCS_OP_DENSE_FP32 if engine == "fp32" else _c.CMTCS_OP_DENSE),
-            fourier_rows=self.rows.data_ptr() if fourier else None)
+            fourier_rows=self.rows.data_ptr() if fourier else None, learn_pi=int(bool(learn_pi)))
         a0 = torch.ones(C, D, dtype=torch.float64, device=self.device) if alpha0 is None else \
             torch.as_tensor(np.asarray(alpha0, np.float64) if not torch.is_tensor(alpha0) else alpha0,
                             dtype=torch.float64).to(self.device).contiguous()
@@ -101,6 +102,12 @@ class CoFEM:
         _c.cmtcs_posterior(self.ctx, *(out[k].data_ptr() for k in ("mu", "s", "logdet", "q", "alpha",
                                                                     "assign", "recon")))
         self.stream.synchronize()
+        return out
+
+    def pi(self) -> np.ndarray:
+        """The current mixture weights π (learned ones after each M-step when learn_pi)."""
+        out = np.zeros(self.C, np.float64)
+        _c.cmtcs_get_pi(self.ctx, out.ctypes.data)
         return out
 
     def set_state(self, alpha, em_iter: int):

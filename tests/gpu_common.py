@@ -16,7 +16,7 @@ def rel_inf(a, b, axis=-1):
 
 
 def make_gpu(data, *, K=None, tol=None, cap=None, alpha=None, em_iter0=0, task_begin=None, T=None,
-             seed=None, mean_tol=-1.0, engine="tensor"):
+             seed=None, mean_tol=-1.0, engine="tensor", learn_pi=False):
     import torch
     from paper_2310_00420_b200 import CoFEM
     cfg = data["cfg"]
@@ -31,7 +31,8 @@ def make_gpu(data, *, K=None, tol=None, cap=None, alpha=None, em_iter0=0, task_b
                  probe_seed=cfg.probe_seed if seed is None else seed, pi=data["pi"],
                  alpha0=data["alpha0"] if alpha is None else alpha,
                  task_begin=int(data["tasks"][0]) if task_begin is None else task_begin,
-                 shared_phi=cfg.shared_phi, em_iter0=em_iter0, mean_rel_tol=mean_tol, engine=engine)
+                 shared_phi=cfg.shared_phi, em_iter0=em_iter0, mean_rel_tol=mean_tol, engine=engine,
+                 learn_pi=learn_pi)
 
 
 def to_np(post):

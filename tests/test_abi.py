@@ -50,8 +50,8 @@ int main(void){
          offsetof(cmtcs_problem, probe_seed), offsetof(cmtcs_problem, em_iter0), sizeof(cmtcs_step_info));
   printf("%zu %zu %zu %zu\n", offsetof(cmtcs_step_info, probe_steps_mean), offsetof(cmtcs_step_info, kernel_launches), offsetof(cmtcs_step_info, tile_col_iters),
          offsetof(cmtcs_problem, mean_rel_tol));
-  printf("%zu %zu %d %d\n", offsetof(cmtcs_problem, op_kind), offsetof(cmtcs_problem, fourier_rows), (int)CMTCS_OP_PARTIAL_FOURIER,
-         (int)CMTCS_OP_DENSE_FP32);
+  printf("%zu %zu %d %d %zu\n", offsetof(cmtcs_problem, op_kind), offsetof(cmtcs_problem, fourier_rows), (int)CMTCS_OP_PARTIAL_FOURIER,
+         (int)CMTCS_OP_DENSE_FP32, offsetof(cmtcs_problem, learn_pi));
   return 0; }
 '''
     with tempfile.TemporaryDirectory() as d:
@@ -63,7 +63,8 @@ int main(void){
     P, S = cmtcs.cmtcs_problem, cmtcs.cmtcs_step_info
     want = [ctypes.sizeof(P), P.beta.offset, P.probe_seed.offset, P.em_iter0.offset, ctypes.sizeof(S),
             S.probe_steps_mean.offset, S.kernel_launches.offset, S.tile_col_iters.offset, P.mean_rel_tol.offset,
-            P.op_kind.offset, P.fourier_rows.offset, cmtcs.CMTCS_OP_PARTIAL_FOURIER, cmtcs.CMTCS_OP_DENSE_FP32]
+            P.op_kind.offset, P.fourier_rows.offset, cmtcs.CMTCS_OP_PARTIAL_FOURIER, cmtcs.CMTCS_OP_DENSE_FP32,
+            P.learn_pi.offset]
     assert [int(x) for x in out] == want
 
 
@@ -93,3 +94,9 @@ def test_invalid_problem_rejected_without_gpu():
     pi[0] = 0.7
     with pytest.raises(cmtcs.CmtcsError, match="EINVAL"):
         cmtcs.cmtcs_workspace_size(p)
+    pi[0] = 0.5
+    p.learn_pi = 2                               # learn_pi is a 0/1 switch
+    with pytest.raises(cmtcs.CmtcsError, match="EINVAL"):
+        cmtcs.cmtcs_workspace_size(p)
+    p.learn_pi = 1
+    assert cmtcs.cmtcs_workspace_size(p) > 0

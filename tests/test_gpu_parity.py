@@ -380,6 +380,42 @@ def test_full_run_config1(torch_cuda):
     assert capfree.sum() >= 5
 
 
+@pytest.mark.parametrize("engine", ["fp32", "tensor"])
+def test_full_run_config1_learned_pi(torch_cuda, engine):
+    """π learned in every M-step (reading P1) from a lopsided π₀ = (0.8, 0.2), config 1:
+    π after each M-step within 1e-3 of the oracle's (π is a mean of q: the q bar), identical argmax,
+    |ΔNMSE| ≤ 1e-3, |ΔL| ≤ 1e-3 on the common-state prefix (as test_full_run_config1)."""
+    cfg = synthetic.CONFIGS[1]
+    data = dict(synthetic.generate(cfg))
+    data["pi"] = np.array([0.8, 0.2])
+    pis_orc, caps_orc = [], []
+
+    def cb(i, e, a):
+        pis_orc.append(O.m_step_pi(e["q"]))
+        caps_orc.append(int(np.sum(e["probe_steps"] >= cfg.cg_cap)))
+    orc = O.run(data, cfg.em_iters, learn_pi=True, callback=cb)
+    g = make_gpu(data, engine=engine, learn_pi=True)
+    assert np.allclose(g.pi(), [0.8, 0.2], rtol=1e-15, atol=0)
+    infos, pis = [], []
+    for _ in range(cfg.em_iters):
+        infos.append(g.em_step(1))
+        pis.append(g.pi())
+    post = to_np(g.posterior())
+    g.close()
+    dpi = np.max(np.abs(np.array(pis) - np.array(pis_orc)), axis=1)
+    gaps = np.abs(np.array([i["loglik"] for i in infos]) - np.array([h["L"] for h in orc["history"]]))
+    capfree = np.array([i["n_cap_hit"] == 0 and c == 0 for i, c in zip(infos, caps_orc)])
+    capped = ~capfree
+    prefix = (int(np.argmax(capped)) + 1) if capped.any() else len(capfree)
+    print("learned pi: GPU", pis[-1], "oracle", orc["pi"], "max |dpi| per iteration", dpi, "L gaps", gaps,
+          "prefix", prefix)
+    assert np.all(np.abs(np.array(pis).sum(axis=1) - 1.0) < 1e-12)
+    assert np.max(dpi[:prefix]) <= Q_TOL and np.max(dpi) <= Q_TOL
+    assert list(post["assign"]) == list(orc["assign"])
+    assert abs(O.nmse(post["recon"], data["z"]) - orc["nmse"]) <= 1e-3
+    assert np.max(gaps[:prefix]) <= L_TOL
+
+
 def test_full_run_config2(torch_cuda):
     """The bench configuration's whole run (config 2, 30 EM iterations from alpha0 = 1): identical
     argmax assignments and |ΔNMSE| ≤ 1e-3 (north_star) against the fp64 oracle's run, stored by

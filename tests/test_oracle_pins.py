@@ -315,6 +315,43 @@ def test_exact_em_likelihood_monotone():
     assert L[-1] > L[0]
 
 
+def test_mstep_pi_maximises_the_surrogate_on_the_simplex():
+    """Learned π (reading P1): m_step_pi must maximise Σ_t Σ_c q_tc log π_c over the
+    probability simplex — checked against scipy's constrained optimiser and 2000 Dirichlet points."""
+    import scipy.optimize
+    rng = np.random.default_rng(11)
+    q = rng.dirichlet(np.ones(4) * 0.7, size=9)          # 9 tasks × 4 clusters, rows sum to 1
+    f = lambda p: float(np.sum(q * np.log(p)))
+    pi = O.m_step_pi(q)
+    assert pi.shape == (4,) and abs(pi.sum() - 1.0) < 1e-15 and np.all(pi > 0)
+    res = scipy.optimize.minimize(lambda p: -f(p), np.full(4, 0.25), method="SLSQP",
+                                  bounds=[(1e-9, 1.0)] * 4, tol=1e-14,
+                                  constraints=[{"type": "eq", "fun": lambda p: p.sum() - 1.0}])
+    np.testing.assert_allclose(pi, res.x, atol=1e-6)
+    others = rng.dirichlet(np.ones(4), size=2000)
+    assert f(pi) >= max(f(p) for p in others)
+    # one-hot responsibilities: the weights are the cluster fractions (brute count)
+    onehot = np.eye(3)[[0, 0, 2, 0, 2, 1, 0, 0]]
+    np.testing.assert_array_equal(O.m_step_pi(onehot) * 8, [5, 1, 2])
+
+
+def test_exact_em_with_learned_pi_likelihood_monotone():
+    """EM theory with π learned as well: L(θ) does not decrease, and π
+    moves from a lopsided start towards the data's cluster sizes (2 tasks of each cluster)."""
+    data = synthetic.small_problem(T=4, C=2, N=12, D=24, sigma=0.1, seed=3, support=3)
+    data = dict(data)
+    data["pi"] = np.array([0.9, 0.1])
+    rng = np.random.default_rng(0)
+    alpha0 = rng.uniform(0.0, 1.0, (2, 24)) + 1e-3
+    r = O.run(data, 25, mode="exact", alpha0=alpha0, learn_pi=True)
+    L = [h["L"] for h in r["history"]]
+    assert all(L[i + 1] >= L[i] - 1e-9 * abs(L[i]) for i in range(len(L) - 1))
+    assert abs(r["pi"].sum() - 1.0) < 1e-12
+    fixed = O.run(data, 25, mode="exact", alpha0=alpha0)
+    assert L[-1] >= fixed["history"][-1]["L"] - 1e-9 * abs(L[-1])   # an extra free parameter
+    assert abs(r["pi"][0] - 0.5) < abs(0.9 - 0.5)
+
+
 def test_single_cluster_q_is_one():
     data = synthetic.small_problem(T=3, C=1, N=10, D=20, seed=4)
     e = O.e_step(data, np.ones((1, 20)), 0, mode="cofem", K=4, tol=1e-10, cap=80)
