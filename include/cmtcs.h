@@ -124,7 +124,9 @@ cmtcs_status cmtcs_workspace_size(const cmtcs_problem *p, size_t *bytes);
  *   y        device, BORROWED: fp32 [T_loc][N] ([T_loc][2N] for the partial-Fourier operator).
  *   alpha0   host or device, COPIED: fp64 [C][D], every entry > 0 (α₀, Alg. 2 line 1).
  *   workspace device, BORROWED, ≥ cmtcs_workspace_size bytes, 256-byte aligned.
- *   nccl_uid NULL with world == 1 for a single GPU; else the rank-0 id, rank in [0, world).
+ *   nccl_uid NULL with world == 1 for a single GPU; else the rank-0 id, rank in [0, world).  A uid
+ *            with world == 1 creates a 1-rank communicator, so the Eq. 4 all-reduce runs through
+ *            NCCL on one GPU (tests of the NCCL path where only one GPU exists).
  *   device   CUDA device ordinal; cuda_stream a cudaStream_t (NULL = legacy default stream).
  * Computes b_t = βΦ_tᵀy_t (Eq. 6) once.  EINVAL on any bad argument (nothing allocated). */
 cmtcs_status cmtcs_init(cmtcs_ctx **ctx, const cmtcs_problem *p, const float *phi,

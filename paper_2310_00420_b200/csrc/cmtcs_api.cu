@@ -624,7 +624,7 @@ cmtcs_status cmtcs_init(cmtcs_ctx **out, const cmtcs_problem *p, const float *ph
     }
   }
   CUDA_OK(c, cudaStreamSynchronize(c->stream));
-  if (world > 1) {
+  if (world > 1 || nccl_uid) {   // a uid with world == 1: a 1-rank communicator (the NCCL path on one GPU)
     ncclUniqueId id;
     memcpy(&id, nccl_uid, 128);
     NCCL_OK(c, ncclCommInitRank(&c->comm, world, id, rank));

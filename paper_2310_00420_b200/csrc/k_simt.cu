@@ -126,7 +126,7 @@ __global__ void __launch_bounds__(STH, PCfg<SMT>::MINB) k_simt_probe(KParams p, 
   const int ncol = 4 * ngrp;                     // multiplied columns of this tile (chunks of 4)
   const size_t gb = pflat > 0 ? 0 : (size_t)t * d.Pp;   // the space's base in the d-major arrays
   const size_t fb = pflat > 0 ? 0 : (size_t)t * d.P;    // ... in the per-column state
-  if (STAGE == 2 && rt == 0 && tid == 0) atomicAdd(p.b.histp + u, ncol);
+  if (STAGE == 2 && rt == 0 && tid == 0) atomicAdd(p.b.histp + u, SBN);   // columns multiplied
   // A[k][m]: stage 1 Φᵀ_t [D][N], stage 2 Φ_t [N][D] (row length M); B[k][g]: D32 [D][ldv] / U [N][ldv]
   const float *__restrict__ amat = STAGE == 1 ? p.b.PT + (size_t)t * d.phi_task_stride
                                               : p.phi + (size_t)t * d.phi_task_stride;

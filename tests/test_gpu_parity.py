@@ -382,19 +382,25 @@ def test_full_run_config1(torch_cuda):
 
 @pytest.mark.parametrize("engine", ["fp32", "tensor"])
 def test_full_run_config1_learned_pi(torch_cuda, engine):
-    """π learned in every M-step (reading P1) from a lopsided π₀ = (0.8, 0.2), config 1:
-    π after each M-step within 1e-3 of the oracle's (π is a mean of q: the q bar), identical argmax,
-    |ΔNMSE| ≤ 1e-3, |ΔL| ≤ 1e-3 on the common-state prefix (as test_full_run_config1)."""
+    """π learned in every M-step (reading P1) from a lopsided π₀ = (0.8, 0.2), config 1
+    with the CG cap raised to 4·64 on both sides (as smoke()), so that no column stops at the cap
+    (DESIGN.md §6).  Full run (north_star: identical argmax, |ΔNMSE| ≤ 1e-3): π after every M-step
+    within 1e-3 of the oracle's (π is a mean of q: the q bar); |ΔL| ≤ 1e-3 over the first 5
+    iterations (later the two runs' α drift apart by accumulated rounding — the full-run L gap
+    reaches ~1e-2 at C1 — so L is then checked the north_star way): one EM step from the oracle's
+    own entry state (α, π) of the iteration with the largest full-run L gap, |ΔL| ≤ 1e-3 and the
+    learned π within 1e-3."""
     cfg = synthetic.CONFIGS[1]
+    cap = 4 * cfg.cg_cap
     data = dict(synthetic.generate(cfg))
     data["pi"] = np.array([0.8, 0.2])
     pis_orc, caps_orc = [], []
 
     def cb(i, e, a):
         pis_orc.append(O.m_step_pi(e["q"]))
-        caps_orc.append(int(np.sum(e["probe_steps"] >= cfg.cg_cap)))
-    orc = O.run(data, cfg.em_iters, learn_pi=True, callback=cb)
-    g = make_gpu(data, engine=engine, learn_pi=True)
+        caps_orc.append(int(np.sum(e["probe_steps"] >= cap)))
+    orc = O.run(data, cfg.em_iters, learn_pi=True, callback=cb, cap=cap)
+    g = make_gpu(data, engine=engine, learn_pi=True, cap=cap)
     assert np.allclose(g.pi(), [0.8, 0.2], rtol=1e-15, atol=0)
     infos, pis = [], []
     for _ in range(cfg.em_iters):
@@ -404,16 +410,26 @@ def test_full_run_config1_learned_pi(torch_cuda, engine):
     g.close()
     dpi = np.max(np.abs(np.array(pis) - np.array(pis_orc)), axis=1)
     gaps = np.abs(np.array([i["loglik"] for i in infos]) - np.array([h["L"] for h in orc["history"]]))
-    capfree = np.array([i["n_cap_hit"] == 0 and c == 0 for i, c in zip(infos, caps_orc)])
-    capped = ~capfree
-    prefix = (int(np.argmax(capped)) + 1) if capped.any() else len(capfree)
     print("learned pi: GPU", pis[-1], "oracle", orc["pi"], "max |dpi| per iteration", dpi, "L gaps", gaps,
-          "prefix", prefix)
+          "cap hits GPU", [i["n_cap_hit"] for i in infos], "oracle", caps_orc)
+    assert sum(caps_orc) == 0 and all(i["n_cap_hit"] == 0 for i in infos)
     assert np.all(np.abs(np.array(pis).sum(axis=1) - 1.0) < 1e-12)
-    assert np.max(dpi[:prefix]) <= Q_TOL and np.max(dpi) <= Q_TOL
+    assert np.max(dpi) <= Q_TOL
+    assert np.max(gaps[:5]) <= L_TOL
     assert list(post["assign"]) == list(orc["assign"])
     assert abs(O.nmse(post["recon"], data["z"]) - orc["nmse"]) <= 1e-3
-    assert np.max(gaps[:prefix]) <= L_TOL
+    # single step from the oracle's entry state of the worst iteration
+    i = int(np.argmax(gaps))
+    h = orc["history"][i]
+    d1 = dict(data)
+    d1["pi"] = h["pi_in"]
+    g = make_gpu(d1, engine=engine, learn_pi=True, cap=cap, alpha=h["alpha_in"], em_iter0=i)
+    L1 = g.em_step(1)["loglik"]
+    pi1 = g.pi()
+    g.close()
+    print("single step at iteration", i, "|dL|", abs(L1 - h["L"]), "|dpi|", np.max(np.abs(pi1 - pis_orc[i])))
+    assert abs(L1 - h["L"]) <= L_TOL
+    assert np.max(np.abs(pi1 - pis_orc[i])) <= Q_TOL
 
 
 def test_full_run_config2(torch_cuda):
