@@ -327,6 +327,217 @@ __global__ void __launch_bounds__(STH, PCfg<SMT>::MINB) k_simt_probe(KParams p, 
   }
 }
 
+// 4-warp form (default): the same 128 × 128 tile with 128 threads, 16 rows × 8 columns per thread
+// (64 FFMA2 per 6 shared loads per k, against 32 per 4 in the 8-warp form above: the FMA pipe, not
+// the issue slots or the shared-memory pipe, paces it), ≤ 255 registers, 2 CTAs per SM.  Thread
+// (tx = tid % 16, ty = tid / 16, ty < 8): rows ty·4 + i + 32·g (g, i < 4), columns tx·4 + q + 64·h
+// (h < 2, q < 4).  The two-level block sums as above: totals in 32 thread-private float4 slots.
+constexpr int QTH = 128;
+constexpr int QKBK = 16, QKST = 2;
+constexpr size_t QRING = (size_t)QKST * 2 * QKBK * SLD * sizeof(float);
+constexpr size_t QSMEM = QRING + (size_t)32 * QTH * sizeof(float4);
+
+template <int STAGE>
+__global__ void __launch_bounds__(QTH, 2) k_simt_probe4(KParams p, int u, int pflat) {
+  constexpr int KBK = QKBK, KST = QKST, FLUSH = 64 / KBK;
+  extern __shared__ __align__(16) unsigned char simt_raw[];
+  float *ring = reinterpret_cast<float *>(simt_raw);   // [KST][A slab | B slab], slab [KBK][SLD]
+  float4 *tot4 = reinterpret_cast<float4 *>(simt_raw + QRING);   // [32][QTH] block-sum totals
+  __shared__ double red[QTH / 32][SBN];
+  if (loop_done(p, u)) return;
+  const Dims &d = p.d;
+  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+  const int t = blockIdx.z, rt = blockIdx.y, j0 = blockIdx.x * SBN, m0 = rt * SBM;
+  const int M = STAGE == 1 ? d.N : d.D;      // output rows
+  const int KD = STAGE == 1 ? d.D : d.N;     // contraction length (multiple of 4)
+  // active-column compaction as in k_simt_probe
+  const int space = pflat > 0 ? 0 : t, ncs = pflat > 0 ? pflat : d.P;
+  const int nlist = p.b.m_act[space];
+  if (j0 >= 4 * nlist) return;                   // CTA-uniform
+  const int ngrp = min(SBN / 4, nlist - j0 / 4);
+  __shared__ int sgrp[SBN / 4];
+  if (tid < SBN / 4) sgrp[tid] = tid < ngrp ? p.b.act[(size_t)space * d.Pp / 4 * (pflat > 0 ? d.Tl : 1) + j0 / 4 + tid] : 0;
+  __syncthreads();
+  const int ncol = 4 * ngrp;
+  const size_t gb = pflat > 0 ? 0 : (size_t)t * d.Pp;
+  const size_t fb = pflat > 0 ? 0 : (size_t)t * d.P;
+  if (STAGE == 2 && rt == 0 && tid == 0) atomicAdd(p.b.histp + u, SBN);   // columns multiplied
+  const float *__restrict__ amat = STAGE == 1 ? p.b.PT + (size_t)t * d.phi_task_stride
+                                              : p.phi + (size_t)t * d.phi_task_stride;
+  const float *__restrict__ bmat = (STAGE == 1 ? p.b.D32 : p.b.Uh) + gb;
+  const size_t ldv = (size_t)d.ldv;
+  const uint32_t sa0 = (uint32_t)__cvta_generic_to_shared(ring);
+  // a thread's copies: slab rows kr = tid/32 + 4v (v < 4), 4 entries at (tid%32)·4, A and B alike;
+  // its source columns and their validity are fixed for the whole K loop
+  const int kr0 = tid >> 5, c4 = (tid & 31) * 4;
+  const bool oka_m = m0 + c4 < M, okb_c = c4 < ncol;
+  const float *asrc = amat + (size_t)kr0 * M + m0 + c4;
+  const float *bsrc = bmat + (size_t)kr0 * ldv + (okb_c ? 4 * sgrp[c4 >> 2] : 0);
+  const uint32_t st0 = sa0 + 4u * (uint32_t)(kr0 * SLD + c4);
+  auto issue = [&](int kt) {
+    const int k0 = kt * KBK;
+    const uint32_t so = st0 + 4u * (uint32_t)((kt % KST) * 2 * KBK * SLD);
+#pragma unroll
+    for (int v = 0; v < KBK / 4; ++v) {
+      const bool kin = k0 + kr0 + 4 * v < KD;
+      const bool oa = oka_m && kin, ob = okb_c && kin;
+      cp_async16(so + 4u * (uint32_t)(4 * v * SLD), oa ? asrc + (size_t)(k0 + 4 * v) * M : amat, oa);
+      cp_async16(so + 4u * (uint32_t)((KBK + 4 * v) * SLD), ob ? bsrc + (size_t)(k0 + 4 * v) * ldv : bmat, ob);
+    }
+  };
+
+  // acc2[ip][j]: rows (2ip, 2ip+1) of this thread's 16 (ip = 2g + i/2: ty·4 + i + 32g), column j of
+  // its 8 (tx·4 + (j&3) + 64·(j>>2))
+  float2 acc2[8][8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc2[i][j] = make_float2(0.f, 0.f);
+#pragma unroll
+  for (int q = 0; q < 32; ++q) tot4[q * QTH + tid] = make_float4(0.f, 0.f, 0.f, 0.f);
+  const int nk = (KD + KBK - 1) / KBK;
+#pragma unroll
+  for (int s = 0; s < KST - 1; ++s) {
+    if (s < nk) issue(s);
+    cp_commit();
+  }
+  for (int kt = 0; kt < nk; ++kt) {
+    cp_wait<KST - 2>();
+    __syncthreads();                            // slab kt landed for all; slot (kt − 1) % KST is free
+    if (kt + KST - 1 < nk) issue(kt + KST - 1);
+    cp_commit();
+    const int slot = kt % KST;
+    const float *As = ring + slot * 2 * KBK * SLD + ty * 4, *Bs = ring + (slot * 2 + 1) * KBK * SLD + tx * 4;
+    float4 a[4], b[2];
+#pragma unroll
+    for (int g = 0; g < 4; ++g) a[g] = *reinterpret_cast<const float4 *>(As + 32 * g);
+#pragma unroll
+    for (int h = 0; h < 2; ++h) b[h] = *reinterpret_cast<const float4 *>(Bs + 64 * h);
+#pragma unroll
+    for (int kk = 0; kk < KBK; ++kk) {
+      float4 na[4], nb[2];
+      if (kk + 1 < KBK) {                       // next k's operands before this k's FMAs
+#pragma unroll
+        for (int g = 0; g < 4; ++g) na[g] = *reinterpret_cast<const float4 *>(As + (kk + 1) * SLD + 32 * g);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) nb[h] = *reinterpret_cast<const float4 *>(Bs + (kk + 1) * SLD + 64 * h);
+      }
+      float2 ap[8];
+#pragma unroll
+      for (int g = 0; g < 4; ++g) {
+        ap[2 * g] = make_float2(a[g].x, a[g].y);
+        ap[2 * g + 1] = make_float2(a[g].z, a[g].w);
+      }
+      const float bv[8] = {b[0].x, b[0].y, b[0].z, b[0].w, b[1].x, b[1].y, b[1].z, b[1].w};
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+#pragma unroll
+        for (int i = 0; i < 8; ++i) acc2[i][j] = __ffma2_rn(ap[i], make_float2(bv[j], bv[j]), acc2[i][j]);
+      if (kk + 1 < KBK) {
+#pragma unroll
+        for (int g = 0; g < 4; ++g) a[g] = na[g];
+        b[0] = nb[0];
+        b[1] = nb[1];
+      }
+    }
+    if ((kt + 1) % FLUSH == 0 || kt + 1 == nk) {   // totals in shared memory (thread-private slots)
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+          float4 tt = tot4[(i * 4 + h) * QTH + tid];
+          tt.x += acc2[i][2 * h].x;
+          tt.y += acc2[i][2 * h].y;
+          tt.z += acc2[i][2 * h + 1].x;
+          tt.w += acc2[i][2 * h + 1].y;
+          tot4[(i * 4 + h) * QTH + tid] = tt;
+          acc2[i][2 * h] = acc2[i][2 * h + 1] = make_float2(0.f, 0.f);
+        }
+    }
+  }
+  cp_wait<0>();
+  // outputs: row m0 + 32g + ty·4 + r (g, r < 4) = tot slot ip = 2g + r/2, .{x|z} (r even) / .{y|w};
+  // columns j0 + 64h + tx·4 + q: slot column pair (2h + q/2), element q&1
+  if (STAGE == 1) {                             // U [N][ldv]
+#pragma unroll
+    for (int g = 0; g < 4; ++g)
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const int m = m0 + 32 * g + ty * 4 + r;
+        if (m >= M) continue;
+        const int ip = 2 * g + r / 2;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int c = h * 64 + tx * 4;
+          if (c >= ncol) continue;
+          const float4 t0 = tot4[(ip * 4 + 2 * h) * QTH + tid], t1 = tot4[(ip * 4 + 2 * h + 1) * QTH + tid];
+          // slot (ip, hh) = {col 2hh: (row 2ip, row 2ip+1), col 2hh+1: (row 2ip, row 2ip+1)}
+          const float4 o = (r & 1) ? make_float4(t0.y, t0.w, t1.y, t1.w) : make_float4(t0.x, t0.z, t1.x, t1.z);
+          *reinterpret_cast<float4 *>(p.b.Uh + (size_t)m * ldv + gb + 4 * sgrp[c >> 2]) = o;
+        }
+      }
+  } else {                                      // W = βΦᵀU + α ⊙ d (fp64, one rounding), dᵀW partials
+    const double beta = p.beta;
+    const int warp = tid >> 5, lane = tid & 31;
+    double *sal = reinterpret_cast<double *>(ring);   // α of the tile's rows per cluster (idle ring)
+    __syncthreads();
+    for (int e = tid; e < d.C * SBM; e += QTH) {
+      const int c = e / SBM, r = e % SBM;
+      sal[e] = m0 + r < M ? p.b.alpha64[(size_t)c * d.D + m0 + r] : 0.0;
+    }
+    __syncthreads();
+    double dot[8];
+    const double *al[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      dot[q] = 0.0;
+      const int c = (q >> 2) * 64 + tx * 4 + (q & 3);
+      const int jc = min(4 * sgrp[min(c, ncol - 1) >> 2] + (c & 3), ncs - 1);
+      al[q] = sal + (size_t)(((fb + jc) % d.P) / d.K) * SBM - m0;
+    }
+#pragma unroll
+    for (int g = 0; g < 4; ++g)
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const int m = m0 + 32 * g + ty * 4 + r;
+        if (m >= M) continue;
+        const int ip = 2 * g + r / 2;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int c = h * 64 + tx * 4;
+          if (c >= ncol) continue;
+          const float4 t0 = tot4[(ip * 4 + 2 * h) * QTH + tid], t1 = tot4[(ip * 4 + 2 * h + 1) * QTH + tid];
+          const float accq[4] = {(r & 1) ? t0.y : t0.x, (r & 1) ? t0.w : t0.z, (r & 1) ? t1.y : t1.x,
+                                 (r & 1) ? t1.w : t1.z};
+          const size_t o = (size_t)m * ldv + gb + 4 * sgrp[c >> 2];
+          const float4 dv = *reinterpret_cast<const float4 *>(p.b.D32 + o);
+          const float dq[4] = {dv.x, dv.y, dv.z, dv.w};
+          float wq[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            wq[q] = (float)fma(beta, (double)accq[q], al[4 * h + q][m] * (double)dq[q]);
+            dot[4 * h + q] += (double)dq[q] * (double)wq[q];
+          }
+          *reinterpret_cast<float4 *>(p.b.W + o) = make_float4(wq[0], wq[1], wq[2], wq[3]);
+        }
+      }
+    // dᵀW over this tile's 128 rows: the ty pair inside a warp, then the 4 warps (fixed order)
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const double v = dot[q] + __shfl_xor_sync(0xffffffffu, dot[q], 16);
+      if (lane < 16) red[warp][(q >> 2) * 64 + tx * 4 + (q & 3)] = v;
+    }
+    __syncthreads();
+    const int jt = tid < ncol ? 4 * sgrp[tid >> 2] + (tid & 3) : ncs;
+    if (jt < ncs) {
+      double s = 0.0;
+#pragma unroll
+      for (int w = 0; w < QTH / 32; ++w) s += red[w][tid];
+      p.b.dAd[(fb + jt) * d.nRT2 + rt] = s;
+    }
+  }
+}
+
 // ---- fp64 mean columns ----------------------------------------------------------------------------
 __device__ __forceinline__ bool task_mean_active(const KParams &p, int t) {
   int a = 0;
@@ -683,8 +894,10 @@ cudaError_t run_simt_cg(const KParams &p, int *h_alive, int64_t *launches, SimtT
   const int nbp = (d.ldv + 31) / 32, gu = nbp + (d.Tl * d.C + 7) / 8;
   constexpr int B = SimtTiming::B;
   cudaError_t e = cudaSuccess;
-  // the 2-CTA form by default (C4, 32 tasks: 1387 vs 1426 ms per EM iteration); CMTCS_SIMT_SMT=0 the other
-  static const bool smt = !getenv("CMTCS_SIMT_SMT") || atoi(getenv("CMTCS_SIMT_SMT")) != 0;
+  // form: 0 the 4-warp 16 × 8-per-thread SGEMM (default); CMTCS_SIMT_FORM=1 the 8-warp 8 × 8 form with 2
+  // CTAs per SM, 2 the same with 1 CTA per SM (C4, 32 tasks: 1387 vs 1426 ms per EM iteration)
+  static const int form = getenv("CMTCS_SIMT_FORM") ? atoi(getenv("CMTCS_SIMT_FORM")) : 0;
+  const bool smt = form != 2;
   static bool configured = false;   // dynamic shared memory above 48 KB (one process per GPU)
   if (!configured) {
     const int s0 = (int)PCfg<false>::SMEM, s1 = (int)PCfg<true>::SMEM;
@@ -692,6 +905,8 @@ cudaError_t run_simt_cg(const KParams &p, int *h_alive, int64_t *launches, SimtT
     if (e == cudaSuccess) e = cudaFuncSetAttribute(k_simt_probe<2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, s0);
     if (e == cudaSuccess) e = cudaFuncSetAttribute(k_simt_probe<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, s1);
     if (e == cudaSuccess) e = cudaFuncSetAttribute(k_simt_probe<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, s1);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_simt_probe4<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)QSMEM);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_simt_probe4<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)QSMEM);
     if (e != cudaSuccess) return e;
     configured = true;
   }
@@ -719,7 +934,10 @@ cudaError_t run_simt_cg(const KParams &p, int *h_alive, int64_t *launches, SimtT
     k_simt_mean<1><<<gm1, MTH, 0, ss.side>>>(p, u);
     k_simt_mean<2><<<gm2, MTH, 0, ss.side>>>(p, u);
     cudaEventRecord(ss.join, ss.side);
-    if (smt) {
+    if (form == 0) {
+      k_simt_probe4<1><<<g1, QTH, QSMEM, s>>>(p, u, pflat);
+      k_simt_probe4<2><<<g2, QTH, QSMEM, s>>>(p, u, pflat);
+    } else if (smt) {
       k_simt_probe<1, true><<<g1, STH, PCfg<true>::SMEM, s>>>(p, u, pflat);
       k_simt_probe<2, true><<<g2, STH, PCfg<true>::SMEM, s>>>(p, u, pflat);
     } else {
