@@ -476,13 +476,13 @@ def cuda_arm(args):
             },
             "roofline": {"bound": "alu" if alu else "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                          "frac": achieved / peak, "traffic": ncu_traffic(cfg.name, engine),
-                         "traffic_unit": ("DRAM bytes per CG step (ncu --set full: k_simt_probe<1> + k_simt_probe<2>, "
+                         "traffic_unit": ("DRAM bytes per CG step (ncu --set full: k_simt_probe4<1> + k_simt_probe4<2>, "
                                           "one launch each)") if engine == "fp32" else
                                          "DRAM bytes per CG step (ncu --set full of k_cg_persistent / its CG steps)",
                          "kernel": ("k_cg_fourier (partial-Fourier CG: one CTA per column, FFT in shared memory; "
                                     "achieved = 10*D*log2(D) flop per active column per CG step / the kernels' "
                                     "duration)") if fourier else
-                                   ("the FP32 engine's CG loop (k_simt_probe<1>/<2> register-tiled SGEMMs for the "
+                                   ("the FP32 engine's CG loop (k_simt_probe4<1>/<2> register-tiled SGEMMs for the "
                                     "probe columns, k_simt_mean<1/2> fp64 mean columns, k_simt_update); achieved = "
                                     "algorithmic fp32 flop 4*N*D per active column per CG step / the loop's duration "
                                     "(CUDA events on the launch stream around every E-step's CG loop); "
