@@ -337,9 +337,13 @@ constexpr int QKBK = 16, QKST = 2;
 constexpr size_t QRING = (size_t)QKST * 2 * QKBK * SLD * sizeof(float);
 constexpr size_t QSMEM = QRING + (size_t)32 * QTH * sizeof(float4);
 
-template <int STAGE>
+// VAR (measured variants, CMTCS_SIMT_VAR): bit 0 — block sums of 128 k instead of 64 (half the
+// flushes; ε·(√128 + √(K/128))); bit 1 — copy addresses as running pointers with the
+// k-bound test only on the last slab.
+template <int STAGE, int VAR = 0>
 __global__ void __launch_bounds__(QTH, 2) k_simt_probe4(KParams p, int u, int pflat) {
-  constexpr int KBK = QKBK, KST = QKST, FLUSH = 64 / KBK;
+  constexpr int KBK = QKBK, KST = QKST, FLUSH = ((VAR & 1) ? 128 : 64) / KBK;
+  constexpr bool LEAN = (VAR & 2) != 0;
   extern __shared__ __align__(16) unsigned char simt_raw[];
   float *ring = reinterpret_cast<float *>(simt_raw);   // [KST][A slab | B slab], slab [KBK][SLD]
   float4 *tot4 = reinterpret_cast<float4 *>(simt_raw + QRING);   // [32][QTH] block-sum totals
@@ -374,9 +378,25 @@ __global__ void __launch_bounds__(QTH, 2) k_simt_probe4(KParams p, int u, int pf
   const float *asrc = amat + (size_t)kr0 * M + m0 + c4;
   const float *bsrc = bmat + (size_t)kr0 * ldv + (okb_c ? 4 * sgrp[c4 >> 2] : 0);
   const uint32_t st0 = sa0 + 4u * (uint32_t)(kr0 * SLD + c4);
+  const char *apn = reinterpret_cast<const char *>(oka_m ? asrc : amat);   // LEAN: the next slab's sources
+  const char *bpn = reinterpret_cast<const char *>(okb_c ? bsrc : bmat);
+  const size_t a4 = oka_m ? (size_t)16 * M : 0, b4 = okb_c ? (size_t)16 * ldv : 0;   // bytes per 4 k rows
   auto issue = [&](int kt) {
     const int k0 = kt * KBK;
     const uint32_t so = st0 + 4u * (uint32_t)((kt % KST) * 2 * KBK * SLD);
+    if (LEAN && k0 + KBK <= KD) {               // a whole slab inside the contraction (CTA-uniform)
+      const uint32_t na = oka_m ? 16u : 0u, nb = okb_c ? 16u : 0u;
+#pragma unroll
+      for (int v = 0; v < KBK / 4; ++v) {
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(so + 4u * (uint32_t)(4 * v * SLD)),
+                     "l"(apn + v * a4), "r"(na) : "memory");
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(so + 4u * (uint32_t)((KBK + 4 * v) * SLD)),
+                     "l"(bpn + v * b4), "r"(nb) : "memory");
+      }
+      apn += (KBK / 4) * a4;
+      bpn += (KBK / 4) * b4;
+      return;
+    }
 #pragma unroll
     for (int v = 0; v < KBK / 4; ++v) {
       const bool kin = k0 + kr0 + 4 * v < KD;
@@ -898,6 +918,7 @@ cudaError_t run_simt_cg(const KParams &p, int *h_alive, int64_t *launches, SimtT
   // CTAs per SM, 2 the same with 1 CTA per SM (C4, 32 tasks: 1387 vs 1426 ms per EM iteration)
   static const int form = getenv("CMTCS_SIMT_FORM") ? atoi(getenv("CMTCS_SIMT_FORM")) : 0;
   const bool smt = form != 2;
+  static const int var = getenv("CMTCS_SIMT_VAR") ? atoi(getenv("CMTCS_SIMT_VAR")) & 3 : 0;
   static bool configured = false;   // dynamic shared memory above 48 KB (one process per GPU)
   if (!configured) {
     const int s0 = (int)PCfg<false>::SMEM, s1 = (int)PCfg<true>::SMEM;
@@ -905,8 +926,11 @@ cudaError_t run_simt_cg(const KParams &p, int *h_alive, int64_t *launches, SimtT
     if (e == cudaSuccess) e = cudaFuncSetAttribute(k_simt_probe<2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, s0);
     if (e == cudaSuccess) e = cudaFuncSetAttribute(k_simt_probe<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, s1);
     if (e == cudaSuccess) e = cudaFuncSetAttribute(k_simt_probe<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, s1);
-    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_simt_probe4<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)QSMEM);
-    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_simt_probe4<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)QSMEM);
+#define CMTCS_P4_ATTR(V)                                                                                       \
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_simt_probe4<1, V>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)QSMEM); \
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_simt_probe4<2, V>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)QSMEM);
+    CMTCS_P4_ATTR(0) CMTCS_P4_ATTR(1) CMTCS_P4_ATTR(2) CMTCS_P4_ATTR(3)
+#undef CMTCS_P4_ATTR
     if (e != cudaSuccess) return e;
     configured = true;
   }
@@ -935,8 +959,16 @@ cudaError_t run_simt_cg(const KParams &p, int *h_alive, int64_t *launches, SimtT
     k_simt_mean<2><<<gm2, MTH, 0, ss.side>>>(p, u);
     cudaEventRecord(ss.join, ss.side);
     if (form == 0) {
-      k_simt_probe4<1><<<g1, QTH, QSMEM, s>>>(p, u, pflat);
-      k_simt_probe4<2><<<g2, QTH, QSMEM, s>>>(p, u, pflat);
+      switch (var) {
+#define CMTCS_P4_RUN(V)                                        \
+  case V:                                                      \
+    k_simt_probe4<1, V><<<g1, QTH, QSMEM, s>>>(p, u, pflat);   \
+    k_simt_probe4<2, V><<<g2, QTH, QSMEM, s>>>(p, u, pflat);   \
+    break;
+        CMTCS_P4_RUN(1) CMTCS_P4_RUN(2) CMTCS_P4_RUN(3)
+        default: CMTCS_P4_RUN(0)
+#undef CMTCS_P4_RUN
+      }
     } else if (smt) {
       k_simt_probe<1, true><<<g1, STH, PCfg<true>::SMEM, s>>>(p, u, pflat);
       k_simt_probe<2, true><<<g2, STH, PCfg<true>::SMEM, s>>>(p, u, pflat);
