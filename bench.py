@@ -470,8 +470,9 @@ def cuda_arm(args):
                 "algorithmic_tflop_per_s_em": flops_all / (total_ms * 1e-3) / 1e12,
                 "em_step_roofline_frac": em_roof_frac,
                 "cg_kernel_share_of_step": kern_ms / max(rank_ms, 1e-9),
-                "op_share_of_step": op_ms / max(rank_ms, 1e-9),
-                "update_share_of_step": tm["update_ms"] / max(rank_ms, 1e-9),
+                # None: the FP32 engine runs two task halves as overlapping loops, phases are not separable
+                "op_share_of_step": op_ms / max(rank_ms, 1e-9) if op_ms > 0 else None,
+                "update_share_of_step": tm["update_ms"] / max(rank_ms, 1e-9) if op_ms > 0 else None,
                 "wall_s_timed": wall,
             },
             "roofline": {"bound": "alu" if alu else "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
@@ -501,7 +502,8 @@ def cuda_arm(args):
                                          f"x (1.1/2.25 tf32/bf16 nominal) / 3 passes; burst {peak_burst:.1f}, "
                                          f"sustained {peak_sust:.1f}"),
                          "frac_burst_peak": achieved / peak_burst,
-                         "operator_phases_only": {"achieved": achieved_op, "frac": achieved_op / peak,
+                         "operator_phases_only": None if op_ms <= 0 else
+                                                 {"achieved": achieved_op, "frac": achieved_op / peak,
                                                   "timing": "CUDA events around the operator kernels of every CG step"
                                                   if engine == "fp32" else
                                                   "device %globaltimer stamps at the phase boundaries"},

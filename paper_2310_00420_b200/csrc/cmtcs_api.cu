@@ -273,7 +273,7 @@ size_t carve(const Dims &d, char *base, Bufs *b) {
   b->ll = cv.take<double>(Tl);
   b->red = cv.take<double>(C * D + C + 1);
   b->red_local = cv.take<double>(C * D + C + 1);
-  b->alive = cv.take<int>(cap);
+  b->alive = cv.take<int>(2 * cap);
   b->hist = cv.take<int>(cap);
   b->histm = cv.take<int>(cap);
   b->histt = cv.take<int>(cap);
@@ -342,7 +342,7 @@ cmtcs_status one_em_iteration(cmtcs_ctx *c, const uint64_t *probe_bits, const do
   kp.probe_bits = probe_bits;
   kp.q_override = q_override;
   int64_t L = 0;
-  CUDA_OK(c, cudaMemsetAsync(kp.b.alive, 0, sizeof(int) * d.cap, s));
+  CUDA_OK(c, cudaMemsetAsync(kp.b.alive, 0, sizeof(int) * 2 * d.cap, s));
   CUDA_OK(c, cudaMemsetAsync(kp.b.hist, 0, sizeof(int) * d.cap, s));
   CUDA_OK(c, cudaMemsetAsync(kp.b.histm, 0, sizeof(int) * d.cap, s));
   CUDA_OK(c, cudaMemsetAsync(kp.b.histt, 0, sizeof(int) * d.cap, s));
@@ -558,6 +558,7 @@ cmtcs_status cmtcs_init(cmtcs_ctx **out, const cmtcs_problem *p, const float *ph
   c->kp.y = y;
   c->kp.beta = p->beta;
   c->kp.learn_pi = p->learn_pi;
+  c->kp.toff = c->kp.tcnt = 0;
   c->kp.tol = p->cg_rel_tol;
   c->kp.tol_mean = p->mean_rel_tol < 0 ? p->cg_rel_tol : p->mean_rel_tol;
   c->kp.alpha_max = p->alpha_max;
@@ -570,7 +571,7 @@ cmtcs_status cmtcs_init(cmtcs_ctx **out, const cmtcs_problem *p, const float *ph
   CUDA_OK(c, cudaMallocHost((void **)&c->h_out, 32 * sizeof(double)));
   CUDA_OK(c, cudaMallocHost((void **)&c->h_status, 8 * sizeof(int)));
 
-  CUDA_OK(c, cudaMallocHost((void **)&c->h_u, sizeof(int)));
+  CUDA_OK(c, cudaMallocHost((void **)&c->h_u, 2 * sizeof(int)));
   CUDA_OK(c, cudaMallocHost((void **)&c->h_ts, sizeof(unsigned long long) * (4 * d.cap + 512)));
   for (int i = 0; i < 3; ++i) CUDA_OK(c, cudaEventCreate(&c->tev[i]));
   if (p->op_kind == CMTCS_OP_DENSE_FP32) {

@@ -71,7 +71,7 @@ struct Bufs {
   double *ll;        // [Tl]
   double *red;       // [C*D + C + 1]  Eq. 4 sums (den, num) and Σ_t log p(y_t)
   double *red_local; // [C*D + C + 1]  the same before the all-reduce (this rank's tasks)
-  int *alive;        // [cap]  columns still active after step u
+  int *alive;        // [2·cap]  columns still active after step u (FP32 engine: one [cap] array per task half)
   int *hist;         // [cap]  probe columns active at step u
   int *histm;        // [cap]  mean columns active at step u
   int *histt;        // [cap]  tasks with an active column at step u
@@ -140,6 +140,7 @@ struct KParams {
   int it;                      // global EM iteration index of this E-step
   const uint64_t *probe_bits;  // optional override
   const double *q_override;    // optional
+  int toff, tcnt;              // FP32 engine: the task window [toff, toff + tcnt) of this launch (tcnt = 0: all tasks)
   int learn_pi;                // M-step also sets log π_c = log((1/T) Σ_t q_tc) (reading P1)
   int trace_step;              // CMTCS_TRACE_STEP (default 5): the CG step CMTCS_PHASE_LOG traces
   int dbg_flags;               // CMTCS_DBG (diagnostics only, wrong results): 1 no DMMA, 2 no tcgen05.mma,
@@ -179,8 +180,8 @@ struct SimtTiming {                 // live timing of the FP32 engine (cmtcs_set
   double op_ms, upd_ms;
 };
 struct SimtStreams {                // the FP32 engine's side stream: the fp64 mean-column kernels run
-  cudaStream_t side;                // beside the probe SGEMMs (fork after the update, join before it)
-  cudaEvent_t fork, join;
+  cudaStream_t side;                // beside the probe SGEMMs (fork after the update, join before it);
+  cudaEvent_t fork, join;           // with two task halves (run_simt_cg) it carries the second half's CG loop
 };
 cudaError_t run_simt_cg(const KParams &p, int *h_alive, int64_t *launches, SimtTiming *tm, const SimtStreams &ss,
                         cudaStream_t s);

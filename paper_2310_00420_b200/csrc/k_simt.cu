@@ -109,7 +109,7 @@ __global__ void __launch_bounds__(STH, PCfg<SMT>::MINB) k_simt_probe(KParams p, 
   if (loop_done(p, u)) return;
   const Dims &d = p.d;
   const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
-  const int t = blockIdx.z, rt = blockIdx.y, j0 = blockIdx.x * SBN, m0 = rt * SBM;
+  const int t = blockIdx.z + p.toff, rt = blockIdx.y, j0 = blockIdx.x * SBN, m0 = rt * SBM;
   const int M = STAGE == 1 ? d.N : d.D;      // output rows
   const int KD = STAGE == 1 ? d.D : d.N;     // contraction length (multiple of 4)
   // active-column compaction: this tile multiplies the 4-column groups [32·x, 32·x + 32) of its column
@@ -329,7 +329,8 @@ __global__ void __launch_bounds__(STH, PCfg<SMT>::MINB) k_simt_probe(KParams p, 
 
 // 4-warp form (default): the same 128 × 128 tile with 128 threads, 16 rows × 8 columns per thread
 // (64 FFMA2 per 6 shared loads per k, against 32 per 4 in the 8-warp form above: the FMA pipe, not
-// the issue slots or the shared-memory pipe, paces it), ≤ 255 registers, 2 CTAs per SM.  Thread
+// the issue slots or the shared-memory pipe, paces it), ≤ 255 registers, 2 CTAs per SM; block sums of
+// 128 k and running copy pointers by default (VAR = 3 below, DESIGN.md §4/§5).  Thread
 // (tx = tid % 16, ty = tid / 16, ty < 8): rows ty·4 + i + 32·g (g, i < 4), columns tx·4 + q + 64·h
 // (h < 2, q < 4).  The two-level block sums as above: totals in 32 thread-private float4 slots.
 constexpr int QTH = 128;
@@ -339,10 +340,10 @@ constexpr size_t QSMEM = QRING + (size_t)32 * QTH * sizeof(float4);
 
 // VAR (measured variants, CMTCS_SIMT_VAR): bit 0 — block sums of 128 k instead of 64 (half the
 // flushes; ε·(√128 + √(K/128))); bit 1 — copy addresses as running pointers with the
-// k-bound test only on the last slab.
+// k-bound test only on the last slab; bit 2 — the block-sum adds as packed FADD2; bit 3 — block sums of 256 k (only as VAR = 14).
 template <int STAGE, int VAR = 0>
 __global__ void __launch_bounds__(QTH, 2) k_simt_probe4(KParams p, int u, int pflat) {
-  constexpr int KBK = QKBK, KST = QKST, FLUSH = ((VAR & 1) ? 128 : 64) / KBK;
+  constexpr int KBK = QKBK, KST = QKST, FLUSH = ((VAR & 8) ? 256 : (VAR & 1) ? 128 : 64) / KBK;
   constexpr bool LEAN = (VAR & 2) != 0;
   extern __shared__ __align__(16) unsigned char simt_raw[];
   float *ring = reinterpret_cast<float *>(simt_raw);   // [KST][A slab | B slab], slab [KBK][SLD]
@@ -351,7 +352,7 @@ __global__ void __launch_bounds__(QTH, 2) k_simt_probe4(KParams p, int u, int pf
   if (loop_done(p, u)) return;
   const Dims &d = p.d;
   const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
-  const int t = blockIdx.z, rt = blockIdx.y, j0 = blockIdx.x * SBN, m0 = rt * SBM;
+  const int t = blockIdx.z + p.toff, rt = blockIdx.y, j0 = blockIdx.x * SBN, m0 = rt * SBM;
   const int M = STAGE == 1 ? d.N : d.D;      // output rows
   const int KD = STAGE == 1 ? d.D : d.N;     // contraction length (multiple of 4)
   // active-column compaction as in k_simt_probe
@@ -466,10 +467,16 @@ __global__ void __launch_bounds__(QTH, 2) k_simt_probe4(KParams p, int u, int pf
 #pragma unroll
         for (int h = 0; h < 4; ++h) {
           float4 tt = tot4[(i * 4 + h) * QTH + tid];
-          tt.x += acc2[i][2 * h].x;
-          tt.y += acc2[i][2 * h].y;
-          tt.z += acc2[i][2 * h + 1].x;
-          tt.w += acc2[i][2 * h + 1].y;
+          if (VAR & 4) {                           // packed adds (FADD2): the same round-to-nearest sums
+            const float2 lo = __fadd2_rn(make_float2(tt.x, tt.y), acc2[i][2 * h]);
+            const float2 hi = __fadd2_rn(make_float2(tt.z, tt.w), acc2[i][2 * h + 1]);
+            tt = make_float4(lo.x, lo.y, hi.x, hi.y);
+          } else {
+            tt.x += acc2[i][2 * h].x;
+            tt.y += acc2[i][2 * h].y;
+            tt.z += acc2[i][2 * h + 1].x;
+            tt.w += acc2[i][2 * h + 1].y;
+          }
           tot4[(i * 4 + h) * QTH + tid] = tt;
           acc2[i][2 * h] = acc2[i][2 * h + 1] = make_float2(0.f, 0.f);
         }
@@ -581,7 +588,7 @@ __global__ void __launch_bounds__(MTH) k_simt_mean(KParams p, int u) {
   __shared__ double red[MTH / 32][MAXC];
   if (loop_done(p, u)) return;
   const Dims &d = p.d;
-  const int t = blockIdx.y, tid = threadIdx.x, rt = blockIdx.x, m0 = rt * SBM;
+  const int t = blockIdx.y + p.toff, tid = threadIdx.x, rt = blockIdx.x, m0 = rt * SBM;
   if (!task_mean_active(p, t)) return;
   const int M = STAGE == 1 ? d.N : d.D, KD = STAGE == 1 ? d.D : d.N, C = d.C;
   const float *__restrict__ amat = (STAGE == 1 ? p.b.PT : p.phi) + (size_t)t * d.phi_task_stride;
@@ -691,7 +698,7 @@ __device__ void simt_update_probes(const KParams &p, int u) {
   __shared__ int sact[32];
   const Dims &d = p.d;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int g = blockIdx.x * 32 + lane;
+  const int g = (blockIdx.x + p.toff * d.Pp / 32) * 32 + lane;   // a task window starts on a 32-column block
   const int t = g / d.Pp, j = g % d.Pp;
   const bool col = t < d.Tl && j < d.P;
   const size_t gi = (size_t)t * d.P + j;     // per-column state index
@@ -856,14 +863,14 @@ __device__ void simt_update_mean(const KParams &p, int t, int c, int u, int lane
 __global__ void __launch_bounds__(256) k_simt_update(KParams p, int u, int nbp) {
   if (loop_done(p, u)) return;
   const Dims &d = p.d;
-  if (blockIdx.x == 0 && threadIdx.x == 0) *p.b.u = u + 1;   // CG steps executed
+  if (blockIdx.x == 0 && threadIdx.x == 0) atomicMax(p.b.u, u + 1);   // CG steps executed (either task half)
   if ((int)blockIdx.x < nbp) {
     simt_update_probes(p, u);
     return;
   }
   const int lane = threadIdx.x & 31;
-  const int w = (blockIdx.x - nbp) * (blockDim.x / 32) + (threadIdx.x >> 5);
-  if (w >= d.Tl * d.C) return;
+  const int w = p.toff * d.C + (blockIdx.x - nbp) * (blockDim.x / 32) + (threadIdx.x >> 5);
+  if (w >= (p.tcnt ? p.toff + p.tcnt : d.Tl) * d.C) return;
   const int t = w / d.C, c = w % d.C;
   if (p.b.flagm[(size_t)t * d.C + c] != 1) return;
   if (lane == 0) {
@@ -879,7 +886,7 @@ __global__ void __launch_bounds__(256) k_simt_update(KParams p, int u, int nbp) 
 __global__ void k_simt_groups(KParams p, int u, int pflat) {
   if (loop_done(p, u)) return;
   const Dims &d = p.d;
-  const int space = blockIdx.x, lane = threadIdx.x;
+  const int space = blockIdx.x + p.toff, lane = threadIdx.x;   // (flat: one space, toff = 0)
   const int ncs = pflat > 0 ? pflat : d.P, ng = (ncs + 3) / 4;
   const size_t fb = pflat > 0 ? 0 : (size_t)space * d.P;
   const size_t lb = (size_t)space * d.Pp / 4 * (pflat > 0 ? d.Tl : 1);
@@ -918,7 +925,7 @@ cudaError_t run_simt_cg(const KParams &p, int *h_alive, int64_t *launches, SimtT
   // CTAs per SM, 2 the same with 1 CTA per SM (C4, 32 tasks: 1387 vs 1426 ms per EM iteration)
   static const int form = getenv("CMTCS_SIMT_FORM") ? atoi(getenv("CMTCS_SIMT_FORM")) : 0;
   const bool smt = form != 2;
-  static const int var = getenv("CMTCS_SIMT_VAR") ? atoi(getenv("CMTCS_SIMT_VAR")) & 3 : 0;
+  static const int var = getenv("CMTCS_SIMT_VAR") ? atoi(getenv("CMTCS_SIMT_VAR")) & 15 : 3;
   static bool configured = false;   // dynamic shared memory above 48 KB (one process per GPU)
   if (!configured) {
     const int s0 = (int)PCfg<false>::SMEM, s1 = (int)PCfg<true>::SMEM;
@@ -929,13 +936,72 @@ cudaError_t run_simt_cg(const KParams &p, int *h_alive, int64_t *launches, SimtT
 #define CMTCS_P4_ATTR(V)                                                                                       \
   if (e == cudaSuccess) e = cudaFuncSetAttribute(k_simt_probe4<1, V>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)QSMEM); \
   if (e == cudaSuccess) e = cudaFuncSetAttribute(k_simt_probe4<2, V>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)QSMEM);
-    CMTCS_P4_ATTR(0) CMTCS_P4_ATTR(1) CMTCS_P4_ATTR(2) CMTCS_P4_ATTR(3)
+    CMTCS_P4_ATTR(0) CMTCS_P4_ATTR(1) CMTCS_P4_ATTR(2) CMTCS_P4_ATTR(3) CMTCS_P4_ATTR(4) CMTCS_P4_ATTR(5) CMTCS_P4_ATTR(6) CMTCS_P4_ATTR(7) CMTCS_P4_ATTR(14)
 #undef CMTCS_P4_ATTR
     if (e != cudaSuccess) return e;
     configured = true;
   }
   e = cudaMemsetAsync(p.b.u, 0, sizeof(int), s);
   if (e != cudaSuccess) return e;
+  // Two task halves as two independent CG loops (default where every task has its own Φ and the second
+  // half starts on a 32-column block; CMTCS_SIMT_SPLIT=0: one loop): half 0 on `s`, half 1 on the side
+  // stream, each with its own alive[] array.  A column's arithmetic is unchanged (same kernels, same
+  // tiles); what changes is what shares the GPU: one half's HBM-bound update and mean kernels and the
+  // partial last wave of its SGEMMs run beside the other half's FMA-bound SGEMMs.  Per-step event
+  // timing (op_ms / upd_ms) does not apply to overlapped phases and stays 0.
+  static const int split = getenv("CMTCS_SIMT_SPLIT") ? atoi(getenv("CMTCS_SIMT_SPLIT")) : 1;
+  int th = 0;
+  if (split && form == 0 && !pflat && d.Tl >= 2) {
+    int align = 32, a = d.Pp % 32;
+    while (a) { const int r = align % a; align = a; a = r; }   // gcd(32, Pp) (Pp % 32 == 0: 32)
+    align = 32 / align;                                        // tasks per whole 32-column block
+    th = d.Tl / 2 / align * align;
+  }
+  if (th > 0) {
+    KParams ph[2] = {p, p};
+    ph[0].toff = 0, ph[0].tcnt = th;
+    ph[1].toff = th, ph[1].tcnt = d.Tl - th;
+    ph[1].b.alive = p.b.alive + d.cap;
+    const cudaStream_t st[2] = {s, ss.side};
+    e = cudaEventRecord(ss.fork, s);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(ss.side, ss.fork, 0);
+    if (e != cudaSuccess) return e;
+    for (int u = 0; u < d.cap; ++u) {
+      for (int h = 0; h < 2; ++h) {
+        const KParams &q = ph[h];
+        const dim3 h1(gx, g1.y, q.tcnt), h2(gx, g2.y, q.tcnt), hm1(gm1.x, q.tcnt), hm2(gm2.x, q.tcnt);
+        const int hbp = (q.tcnt * d.Pp + 31) / 32, hu = hbp + (q.tcnt * d.C + 7) / 8;
+        k_simt_groups<<<q.tcnt, 32, 0, st[h]>>>(q, u, 0);
+        k_simt_mean<1><<<hm1, MTH, 0, st[h]>>>(q, u);
+        k_simt_mean<2><<<hm2, MTH, 0, st[h]>>>(q, u);
+        switch (var) {
+#define CMTCS_P4_RUN(V)                                             \
+  case V:                                                           \
+    k_simt_probe4<1, V><<<h1, QTH, QSMEM, st[h]>>>(q, u, 0);        \
+    k_simt_probe4<2, V><<<h2, QTH, QSMEM, st[h]>>>(q, u, 0);        \
+    break;
+          CMTCS_P4_RUN(1) CMTCS_P4_RUN(2) CMTCS_P4_RUN(3) CMTCS_P4_RUN(4) CMTCS_P4_RUN(5) CMTCS_P4_RUN(6) CMTCS_P4_RUN(7) CMTCS_P4_RUN(14)
+          default: CMTCS_P4_RUN(0)
+#undef CMTCS_P4_RUN
+        }
+        k_simt_update<<<hu, 256, 0, st[h]>>>(q, u, hbp);
+      }
+      *launches += 12;
+      e = cudaGetLastError();
+      if (e != cudaSuccess) return e;
+      if (u % B == B - 1 || u + 1 == d.cap) {
+        for (int h = 0; h < 2 && e == cudaSuccess; ++h)
+          e = cudaMemcpyAsync(h_alive + h, ph[h].b.alive + u, sizeof(int), cudaMemcpyDeviceToHost, st[h]);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(ss.side);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+        if (e != cudaSuccess) return e;
+        if (h_alive[0] == 0 && h_alive[1] == 0) break;
+      }
+    }
+    e = cudaEventRecord(ss.join, ss.side);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(s, ss.join, 0);
+    return e;
+  }
   auto collect = [&](int n) -> cudaError_t {   // the last n steps' events (their work has completed)
     for (int i = 0; i < n; ++i) {
       float a = 0.f, b2 = 0.f;
@@ -965,7 +1031,7 @@ cudaError_t run_simt_cg(const KParams &p, int *h_alive, int64_t *launches, SimtT
     k_simt_probe4<1, V><<<g1, QTH, QSMEM, s>>>(p, u, pflat);   \
     k_simt_probe4<2, V><<<g2, QTH, QSMEM, s>>>(p, u, pflat);   \
     break;
-        CMTCS_P4_RUN(1) CMTCS_P4_RUN(2) CMTCS_P4_RUN(3)
+        CMTCS_P4_RUN(1) CMTCS_P4_RUN(2) CMTCS_P4_RUN(3) CMTCS_P4_RUN(4) CMTCS_P4_RUN(5) CMTCS_P4_RUN(6) CMTCS_P4_RUN(7) CMTCS_P4_RUN(14)
         default: CMTCS_P4_RUN(0)
 #undef CMTCS_P4_RUN
       }
