@@ -690,10 +690,11 @@ __device__ void report_simt(int *status, int code, int t, int col, int u) {
 }
 
 // Probe columns, d-major: a CTA updates 32 consecutive columns g = 32·blockIdx.x + lane (one lane per
-// column, every global access a 128-byte row segment); its 8 warps split the D rows, per-column sums
+// column, every global access a 128-byte row segment); its NW warps split the D rows, per-column sums
 // are reduced over the warps in fixed order.  Alg. 1 lines 3-7 with fp64 γ_u, ξ_u applied in fp64.
+template <int NW>
 __device__ void simt_update_probes(const KParams &p, int u) {
-  __shared__ double sred[8][32];
+  __shared__ double sred[NW][32];
   __shared__ double sgam[32];
   __shared__ int sact[32];
   const Dims &d = p.d;
@@ -707,13 +708,13 @@ __device__ void simt_update_probes(const KParams &p, int u) {
   // dᵀAd: the nRT2 row-tile partials, split over the warps
   double dp = 0.0;
   if (active)
-    for (int i = warp; i < d.nRT2; i += 8) dp += p.b.dAd[gi * d.nRT2 + i];
+    for (int i = warp; i < d.nRT2; i += NW) dp += p.b.dAd[gi * d.nRT2 + i];
   sred[warp][lane] = dp;
   __syncthreads();
   if (warp == 0) {
     double dAd = 0.0;
 #pragma unroll
-    for (int w = 0; w < 8; ++w) dAd += sred[w][lane];
+    for (int w = 0; w < NW; ++w) dAd += sred[w][lane];
     int act = active;
     if (active) {
       atomicAdd(p.b.hist + u, 1);
@@ -734,11 +735,11 @@ __device__ void simt_update_probes(const KParams &p, int u) {
   double acc = 0.0;
   if (go) {
     // 4 rows per iteration: 16 independent 128-byte loads in flight per warp
-    for (int i0 = warp; i0 < d.D; i0 += 32) {
+    for (int i0 = warp; i0 < d.D; i0 += 4 * NW) {
       float dv[4], xv[4], wv[4], rv[4];
 #pragma unroll
       for (int v = 0; v < 4; ++v) {
-        const int i = i0 + 8 * v;
+        const int i = i0 + NW * v;
         if (i < d.D) {
           const size_t o = (size_t)i * ldv + g;
           dv[v] = p.b.D32[o]; xv[v] = p.b.X[o]; wv[v] = p.b.W[o]; rv[v] = p.b.R[o];
@@ -746,7 +747,7 @@ __device__ void simt_update_probes(const KParams &p, int u) {
       }
 #pragma unroll
       for (int v = 0; v < 4; ++v) {
-        const int i = i0 + 8 * v;
+        const int i = i0 + NW * v;
         if (i < d.D) {
           const size_t o = (size_t)i * ldv + g;
           const float x = (float)fma(gam, (double)dv[v], (double)xv[v]);
@@ -764,7 +765,7 @@ __device__ void simt_update_probes(const KParams &p, int u) {
   if (warp == 0) {
     double rrn = 0.0;
 #pragma unroll
-    for (int w = 0; w < 8; ++w) rrn += sred[w][lane];
+    for (int w = 0; w < NW; ++w) rrn += sred[w][lane];
     double xi = 0.0;
     int cont = 0;
     if (go) {
@@ -786,11 +787,11 @@ __device__ void simt_update_probes(const KParams &p, int u) {
   __syncthreads();
   if (sact[lane]) {
     const double xi = sgam[lane];
-    for (int i0 = warp; i0 < d.D; i0 += 32) {
+    for (int i0 = warp; i0 < d.D; i0 += 4 * NW) {
       float dv[4], rv[4];
 #pragma unroll
       for (int v = 0; v < 4; ++v) {
-        const int i = i0 + 8 * v;
+        const int i = i0 + NW * v;
         if (i < d.D) {
           const size_t o = (size_t)i * ldv + g;
           dv[v] = p.b.D32[o]; rv[v] = p.b.R[o];
@@ -798,7 +799,7 @@ __device__ void simt_update_probes(const KParams &p, int u) {
       }
 #pragma unroll
       for (int v = 0; v < 4; ++v) {
-        const int i = i0 + 8 * v;
+        const int i = i0 + NW * v;
         if (i < d.D) p.b.D32[(size_t)i * ldv + g] = (float)fma(xi, (double)dv[v], (double)rv[v]);
       }
     }
@@ -859,13 +860,19 @@ __device__ void simt_update_mean(const KParams &p, int t, int c, int u, int lane
   }
 }
 
-// blocks [0, nbp): probe column groups (simt_update_probes); then 8 mean columns per block (a warp each)
-__global__ void __launch_bounds__(256) k_simt_update(KParams p, int u, int nbp) {
+// blocks [0, nbp): probe column groups (simt_update_probes); then NW mean columns per block (a warp each)
+// NW warps per CTA: 8 (default, 256 threads × 80 registers); 4 (CMTCS_SIMT_UPDW=4): 128 threads of
+// ≤ 64 registers — exactly what two resident SGEMM CTAs (2 × 128 × 224 registers) leave of an SM, so
+// that one task half's update could run beside the other half's SGEMMs (run_simt_cg) — measured
+// slower (C4 32 tasks 1227 → 1299 ms per EM iteration: the narrower update itself loses more than
+// the overlap gains).
+template <int NW>
+__global__ void __launch_bounds__(32 * NW, NW == 4 ? 8 : 1) k_simt_update(KParams p, int u, int nbp) {
   if (loop_done(p, u)) return;
   const Dims &d = p.d;
   if (blockIdx.x == 0 && threadIdx.x == 0) atomicMax(p.b.u, u + 1);   // CG steps executed (either task half)
   if ((int)blockIdx.x < nbp) {
-    simt_update_probes(p, u);
+    simt_update_probes<NW>(p, u);
     return;
   }
   const int lane = threadIdx.x & 31;
@@ -918,7 +925,8 @@ cudaError_t run_simt_cg(const KParams &p, int *h_alive, int64_t *launches, SimtT
   const dim3 g1(gx, (d.N + SBM - 1) / SBM, gz);
   const dim3 g2(gx, (d.D + SBM - 1) / SBM, gz);
   const dim3 gm1((d.N + SBM - 1) / SBM, d.Tl), gm2((d.D + SBM - 1) / SBM, d.Tl);
-  const int nbp = (d.ldv + 31) / 32, gu = nbp + (d.Tl * d.C + 7) / 8;
+  static const int updw = getenv("CMTCS_SIMT_UPDW") && atoi(getenv("CMTCS_SIMT_UPDW")) == 4 ? 4 : 8;   // warps per update CTA
+  const int nbp = (d.ldv + 31) / 32, gu = nbp + (d.Tl * d.C + updw - 1) / updw;
   constexpr int B = SimtTiming::B;
   cudaError_t e = cudaSuccess;
   // form: 0 the 4-warp 16 × 8-per-thread SGEMM (default); CMTCS_SIMT_FORM=1 the 8-warp 8 × 8 form with 2
@@ -970,7 +978,7 @@ cudaError_t run_simt_cg(const KParams &p, int *h_alive, int64_t *launches, SimtT
       for (int h = 0; h < 2; ++h) {
         const KParams &q = ph[h];
         const dim3 h1(gx, g1.y, q.tcnt), h2(gx, g2.y, q.tcnt), hm1(gm1.x, q.tcnt), hm2(gm2.x, q.tcnt);
-        const int hbp = (q.tcnt * d.Pp + 31) / 32, hu = hbp + (q.tcnt * d.C + 7) / 8;
+        const int hbp = (q.tcnt * d.Pp + 31) / 32, hu = hbp + (q.tcnt * d.C + updw - 1) / updw;
         k_simt_groups<<<q.tcnt, 32, 0, st[h]>>>(q, u, 0);
         k_simt_mean<1><<<hm1, MTH, 0, st[h]>>>(q, u);
         k_simt_mean<2><<<hm2, MTH, 0, st[h]>>>(q, u);
@@ -984,7 +992,8 @@ cudaError_t run_simt_cg(const KParams &p, int *h_alive, int64_t *launches, SimtT
           default: CMTCS_P4_RUN(0)
 #undef CMTCS_P4_RUN
         }
-        k_simt_update<<<hu, 256, 0, st[h]>>>(q, u, hbp);
+        if (updw == 8) k_simt_update<8><<<hu, 256, 0, st[h]>>>(q, u, hbp);
+        else k_simt_update<4><<<hu, 128, 0, st[h]>>>(q, u, hbp);
       }
       *launches += 12;
       e = cudaGetLastError();
@@ -1044,7 +1053,8 @@ cudaError_t run_simt_cg(const KParams &p, int *h_alive, int64_t *launches, SimtT
     }
     cudaStreamWaitEvent(s, ss.join, 0);
     if (tm) cudaEventRecord(tm->ev[3 * slot + 1], s);
-    k_simt_update<<<gu, 256, 0, s>>>(p, u, nbp);
+    if (updw == 8) k_simt_update<8><<<gu, 256, 0, s>>>(p, u, nbp);
+    else k_simt_update<4><<<gu, 128, 0, s>>>(p, u, nbp);
     if (tm) cudaEventRecord(tm->ev[3 * slot + 2], s);
     *launches += 6;
     ++pending;
