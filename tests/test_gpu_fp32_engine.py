@@ -179,3 +179,26 @@ def test_engines_agree(torch_cuda):
     assert np.max(rel_inf(out["fp32"]["mu"], out["tensor"]["mu"])) <= 1e-8
     assert np.max(rel_inf(out["fp32"]["s"], out["tensor"]["s"])) <= 1e-4
     assert np.max(np.abs(out["fp32"]["logdet"] - out["tensor"]["logdet"])) <= 5e-3
+
+@pytest.mark.parametrize("T,C,K,N,D", [(5, 2, 16, 96, 160), (6, 4, 20, 130, 300)])
+def test_task_halves_bit_identical(torch_cuda, T, C, K, N, D):
+    """The two-half CG loops (run_simt_cg) leave every column's arithmetic untouched:
+    the posterior of an EM step is bit-identical to the single-loop run (CMTCS_SIMT_SPLIT=0), with
+    uneven halves (T = 5: 2 + 3 tasks, P = 32 columns per task; T = 6, P = 80: 2 + 4 — the split must
+    land on a 32-column block) and ragged N, D.  The library reads the setting once per process, so
+    each mode runs in its own interpreter (tests/split_worker.py)."""
+    import json
+    import os
+    import subprocess
+    import sys
+    worker = os.path.join(os.path.dirname(os.path.abspath(__file__)), "split_worker.py")
+    out = {}
+    for mode in ("0", "1"):
+        env = dict(os.environ, CMTCS_SIMT_SPLIT=mode)
+        r = subprocess.run([sys.executable, worker, *map(str, (T, C, K, N, D))], env=env, capture_output=True,
+                           text=True, timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        out[mode] = json.loads(r.stdout.strip().splitlines()[-1])
+    assert out["1"]["launches"] > out["0"]["launches"], out       # the split path really ran (12 vs 6 per step)
+    assert out["0"]["sha"] == out["1"]["sha"], out
+    assert out["0"]["loglik"] == out["1"]["loglik"] and out["0"]["probe_col_iters"] == out["1"]["probe_col_iters"]

@@ -20,3 +20,5 @@ rm -f $O/prof_c4_fp32.ncu-rep.tmp; ls -la $O
 timeout 900 python bench.py --config 3 --steps 10 --warmup 5 > $O/bench_c3_fp32.json 2> $O/bench_c3_fp32.err; echo "c3 rc=$?"
 timeout 1500 python bench.py --config 5 --steps 2 --warmup 3 --no-e2e > $O/bench_c5_fp32.json 2> $O/bench_c5_fp32.err; echo "c5 rc=$?"
 cut -c1-300 $O/bench_c3_fp32.json $O/bench_c5_fp32.json
+(time timeout 1500 python -m pytest tests -m gpu -x -q) > $O/gpu_tests.log 2>&1; echo "tests rc=$?"; tail -4 $O/gpu_tests.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo "smoke rc=$?"; tail -1 $O/smoke.log
