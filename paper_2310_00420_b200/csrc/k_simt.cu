@@ -952,7 +952,8 @@ cudaError_t run_simt_cg(const KParams &p, int *h_alive, int64_t *launches, SimtT
   e = cudaMemsetAsync(p.b.u, 0, sizeof(int), s);
   if (e != cudaSuccess) return e;
   // Two task halves as two independent CG loops (default where every task has its own Φ and the second
-  // half starts on a 32-column block; CMTCS_SIMT_SPLIT=0: one loop): half 0 on `s`, half 1 on the side
+  // half starts on a 32-column block and a half fills the GPU; CMTCS_SIMT_SPLIT=0: one loop, 2: split
+  // whatever the size): half 0 on `s`, half 1 on the side
   // stream, each with its own alive[] array.  A column's arithmetic is unchanged (same kernels, same
   // tiles); what changes is what shares the GPU: one half's HBM-bound update and mean kernels and the
   // partial last wave of its SGEMMs run beside the other half's FMA-bound SGEMMs.  Per-step event
@@ -964,6 +965,9 @@ cudaError_t run_simt_cg(const KParams &p, int *h_alive, int64_t *launches, SimtT
     while (a) { const int r = align % a; align = a; a = r; }   // gcd(32, Pp) (Pp % 32 == 0: 32)
     align = 32 / align;                                        // tasks per whole 32-column block
     th = d.Tl / 2 / align * align;
+    // auto (1): only where a half's stage-1 SGEMM has a CTA for every SM — below that the loop is
+    // launch-latency bound and the longer in-stream chain loses (C2: 25.4 → 20.9 EM it/s); 2: always
+    if (split == 1 && (long long)gx * g1.y * th < 148) th = 0;
   }
   if (th > 0) {
     KParams ph[2] = {p, p};

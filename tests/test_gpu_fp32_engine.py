@@ -180,7 +180,7 @@ def test_engines_agree(torch_cuda):
     assert np.max(rel_inf(out["fp32"]["s"], out["tensor"]["s"])) <= 1e-4
     assert np.max(np.abs(out["fp32"]["logdet"] - out["tensor"]["logdet"])) <= 5e-3
 
-@pytest.mark.parametrize("T,C,K,N,D", [(5, 2, 16, 96, 160), (6, 4, 20, 130, 300)])
+@pytest.mark.parametrize("T,C,K,N,D", [(5, 2, 16, 96, 160), (6, 4, 20, 132, 300)])
 def test_task_halves_bit_identical(torch_cuda, T, C, K, N, D):
     """The two-half CG loops (run_simt_cg) leave every column's arithmetic untouched:
     the posterior of an EM step is bit-identical to the single-loop run (CMTCS_SIMT_SPLIT=0), with
@@ -193,12 +193,12 @@ def test_task_halves_bit_identical(torch_cuda, T, C, K, N, D):
     import sys
     worker = os.path.join(os.path.dirname(os.path.abspath(__file__)), "split_worker.py")
     out = {}
-    for mode in ("0", "1"):
+    for mode in ("0", "2"):      # 2: split whatever the size (the default, 1, splits only GPU-filling halves)
         env = dict(os.environ, CMTCS_SIMT_SPLIT=mode)
         r = subprocess.run([sys.executable, worker, *map(str, (T, C, K, N, D))], env=env, capture_output=True,
                            text=True, timeout=600)
         assert r.returncode == 0, r.stderr[-2000:]
         out[mode] = json.loads(r.stdout.strip().splitlines()[-1])
-    assert out["1"]["launches"] > out["0"]["launches"], out       # the split path really ran (12 vs 6 per step)
-    assert out["0"]["sha"] == out["1"]["sha"], out
-    assert out["0"]["loglik"] == out["1"]["loglik"] and out["0"]["probe_col_iters"] == out["1"]["probe_col_iters"]
+    assert out["2"]["launches"] > out["0"]["launches"], out       # the split path really ran (12 vs 6 per step)
+    assert out["0"]["sha"] == out["2"]["sha"], out
+    assert out["0"]["loglik"] == out["2"]["loglik"] and out["0"]["probe_col_iters"] == out["2"]["probe_col_iters"]
