@@ -340,7 +340,7 @@ constexpr size_t QSMEM = QRING + (size_t)32 * QTH * sizeof(float4);
 
 // VAR (measured variants, CMTCS_SIMT_VAR): bit 0 — block sums of 128 k instead of 64 (half the
 // flushes; ε·(√128 + √(K/128))); bit 1 — copy addresses as running pointers with the
-// k-bound test only on the last slab; bit 2 — the block-sum adds as packed FADD2; bit 3 — block sums of 256 k (only as VAR = 14).
+// k-bound test only on the last slab; bit 2 — the block-sum adds as packed FADD2; bit 3 — block sums of 256 k (only as VAR = 11 or 14).
 template <int STAGE, int VAR = 0>
 __global__ void __launch_bounds__(QTH, 2) k_simt_probe4(KParams p, int u, int pflat) {
   constexpr int KBK = QKBK, KST = QKST, FLUSH = ((VAR & 8) ? 256 : (VAR & 1) ? 128 : 64) / KBK;
@@ -944,7 +944,7 @@ cudaError_t run_simt_cg(const KParams &p, int *h_alive, int64_t *launches, SimtT
 #define CMTCS_P4_ATTR(V)                                                                                       \
   if (e == cudaSuccess) e = cudaFuncSetAttribute(k_simt_probe4<1, V>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)QSMEM); \
   if (e == cudaSuccess) e = cudaFuncSetAttribute(k_simt_probe4<2, V>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)QSMEM);
-    CMTCS_P4_ATTR(0) CMTCS_P4_ATTR(1) CMTCS_P4_ATTR(2) CMTCS_P4_ATTR(3) CMTCS_P4_ATTR(4) CMTCS_P4_ATTR(5) CMTCS_P4_ATTR(6) CMTCS_P4_ATTR(7) CMTCS_P4_ATTR(14)
+    CMTCS_P4_ATTR(0) CMTCS_P4_ATTR(1) CMTCS_P4_ATTR(2) CMTCS_P4_ATTR(3) CMTCS_P4_ATTR(4) CMTCS_P4_ATTR(5) CMTCS_P4_ATTR(6) CMTCS_P4_ATTR(7) CMTCS_P4_ATTR(11) CMTCS_P4_ATTR(14)
 #undef CMTCS_P4_ATTR
     if (e != cudaSuccess) return e;
     configured = true;
@@ -992,7 +992,7 @@ cudaError_t run_simt_cg(const KParams &p, int *h_alive, int64_t *launches, SimtT
     k_simt_probe4<1, V><<<h1, QTH, QSMEM, st[h]>>>(q, u, 0);        \
     k_simt_probe4<2, V><<<h2, QTH, QSMEM, st[h]>>>(q, u, 0);        \
     break;
-          CMTCS_P4_RUN(1) CMTCS_P4_RUN(2) CMTCS_P4_RUN(3) CMTCS_P4_RUN(4) CMTCS_P4_RUN(5) CMTCS_P4_RUN(6) CMTCS_P4_RUN(7) CMTCS_P4_RUN(14)
+          CMTCS_P4_RUN(1) CMTCS_P4_RUN(2) CMTCS_P4_RUN(3) CMTCS_P4_RUN(4) CMTCS_P4_RUN(5) CMTCS_P4_RUN(6) CMTCS_P4_RUN(7) CMTCS_P4_RUN(11) CMTCS_P4_RUN(14)
           default: CMTCS_P4_RUN(0)
 #undef CMTCS_P4_RUN
         }
@@ -1044,7 +1044,7 @@ cudaError_t run_simt_cg(const KParams &p, int *h_alive, int64_t *launches, SimtT
     k_simt_probe4<1, V><<<g1, QTH, QSMEM, s>>>(p, u, pflat);   \
     k_simt_probe4<2, V><<<g2, QTH, QSMEM, s>>>(p, u, pflat);   \
     break;
-        CMTCS_P4_RUN(1) CMTCS_P4_RUN(2) CMTCS_P4_RUN(3) CMTCS_P4_RUN(4) CMTCS_P4_RUN(5) CMTCS_P4_RUN(6) CMTCS_P4_RUN(7) CMTCS_P4_RUN(14)
+        CMTCS_P4_RUN(1) CMTCS_P4_RUN(2) CMTCS_P4_RUN(3) CMTCS_P4_RUN(4) CMTCS_P4_RUN(5) CMTCS_P4_RUN(6) CMTCS_P4_RUN(7) CMTCS_P4_RUN(11) CMTCS_P4_RUN(14)
         default: CMTCS_P4_RUN(0)
 #undef CMTCS_P4_RUN
       }
